@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the GN Hessian-matvec hot path (BASELINE config 4: 1024^2 fp64, nt=16, H2,
+beta=1e-3, GN, SL) — one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl vrg|reference]
+
+A step is one reduced-space GN Hessian matvec HessianOperator::apply(vtilde)
+(src/inverse.cpp:229-233) at a fixed iterate, i.e. one pass of the hot path.  With N > 1
+(torchrun, one process per GPU) every rank holds its own independent image pair and
+iterate (batched pairs): no data-path collective, weak scaling.
+
+`value`   : matvecs/s over all ranks, inputs resident in HBM, device-timed (CUDA events on
+            the launching stream, barrier + synchronize on both sides, max over ranks).
+`e2e`     : the same metric through the drop-in host-buffer call vrg_hess_apply_host
+            (H2D of vtilde from pinned memory + matvec + D2H of the result, every step).
+`roofline`: dominant kernel of the matvec, algorithmic bytes / average launch time from
+            per-launch CUDA events of a second (profiled) pass over the same K steps.
+`cpu_baseline`: the unmodified reference (oracle/_ref) on the host cores, rank 0, N=1 only.
+`--impl reference`: the reference CPU implementation on the host cores (all threads), same
+            metric/config; ranks > 0 exit without work.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GRID, NT, BETA, NORM = 1024, 16, 1e-3, 2
+F_BYTES = 8 * N_GRID * N_GRID
+METRIC = "GN Hessian matvecs/s at 1024^2 fp64 (nt=16, H2, SL)"
+UNIT = "matvec/s"
+CONFIG = {
+    "workload": "config4: single GN Hessian matvec, 1024x1024 fp64, nt=16, H2 beta=1e-3, SL, compressible",
+    "grid": [N_GRID, N_GRID], "nt": NT, "beta": BETA, "norm": "H2",
+    "inputs": "seeded synthetic: smoothed-noise template (sigma=4 px), (1+|k|^2)^-2 random velocity max|v|=0.3",
+    "l2": "per-matvec working set ~0.7 GB of cached state fields >> 126 MB L2 (inputs larger than L2)",
+}
+
+
+# ------------------------------------------------------------------------------ inputs
+def make_problem(rank: int):
+    from paper_1604_02153_b200 import synth
+
+    mT = synth.smoothed_noise(N_GRID, N_GRID, 1000 + rank)
+    v1, v2 = synth.smooth_velocity(N_GRID, N_GRID, 2000 + rank)
+    vtA = synth.smooth_velocity(N_GRID, N_GRID, 3000 + rank)
+    vtB = synth.smooth_velocity(N_GRID, N_GRID, 4000 + rank)
+    return mT, (v1, v2), vtA, vtB
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ algorithmic bytes
+# Per-launch algorithmic bytes (multiples of F = one fp64 field) of the library's kernels in
+# one matvec.  Reads of the gathered coefficient field count once.
+KERNEL_BYTES_F = {
+    "evaluate/adjoint_bodyforce": 12,  # coef, X_D(2), dvDep, dv, G(2), b(2) in; lam, b(2) out
+    "evaluate/incstate": 12,           # coef, X_D(2), vtD(2), GD(2), vt(2), G(2) in; m~ out
+    "evaluate/store2": 7,              # coef(2), X_D(2) in; 2 out  (+ shared weights)
+    "k_prefilter_rows": 2,
+    "k_prefilter_cols": 2,
+    "pointwise/adjoint_seed": 6,       # m~, G(2), b... : m~ + G(2) in, lam + b(2) out
+    "evaluate/state_step": 4,
+}
+
+
+def matvec_algorithmic_bytes(nt: int = NT) -> int:
+    """B_mv = (24 nt + 12) F."""
+    return (24 * nt + 12) * F_BYTES
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_vrg(args, rank, world, local_rank):
+    import torch
+
+    from paper_1604_02153_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = api.Context(local_rank)
+    mT, v, vtA, vtB = make_problem(rank)
+    T = lambda a: ctx.field(a)  # noqa: E731
+    mT_d, v_d = T(mT), (T(v[0]), T(v[1]))
+    # reference image: the template transported by the true velocity (GN does not depend on it)
+    mR_d = api.Solver(ctx, v_d, NT).solve_state_final(mT_d)
+    H = api.HessianOperator(ctx, v_d, mR_d, mT_d, NORM, BETA, api.COMPRESSIBLE, NT)
+    vts = [ctx.empty(2, N_GRID, N_GRID) for _ in range(2)]
+    vts[0][0].copy_(T(vtA[0])); vts[0][1].copy_(T(vtA[1]))
+    vts[1][0].copy_(T(vtB[0])); vts[1][1].copy_(T(vtB[1]))
+    out = ctx.empty(2, N_GRID, N_GRID)
+    stream = ctx.stream
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, k):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(k):
+            fn(i)
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    step = lambda i: H.apply((vts[i & 1][0], vts[i & 1][1]), out=out)  # noqa: E731
+    for i in range(args.warmup):
+        step(i)
+    launches0 = ctypes_launches(ctx)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    ms = timed(step, args.steps)
+    clk = clocks.stop()
+    launches = ctypes_launches(ctx) - launches0
+    value = world * args.steps / (ms / 1e3)
+
+    # e2e: drop-in host-buffer call, pinned host memory, copies inside the timed region
+    hin = [torch.empty(2, N_GRID, N_GRID, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    hin[0].copy_(vts[0].cpu()); hin[1].copy_(vts[1].cpu())
+    hout = torch.empty(2, N_GRID, N_GRID, dtype=torch.float64, pin_memory=True)
+    e2e_step = lambda i: H.apply_host(hin[i & 1][0], hin[i & 1][1], hout[0], hout[1])  # noqa: E731
+    for i in range(max(1, args.warmup)):
+        e2e_step(i)
+    barrier()
+    t0 = time.perf_counter()
+    ms_e2e = timed(e2e_step, args.steps)
+    wall_e2e = time.perf_counter() - t0
+    e2e_value = world * args.steps / (ms_e2e / 1e3)
+
+    # profiled pass: per-launch CUDA events of every kernel of the same K steps
+    ctx.lib.vrg_profile(ctx.h, 1)
+    for i in range(args.steps):
+        step(i)
+    prof = profile_dump(ctx)
+    ctx.lib.vrg_profile(ctx.h, 0)
+
+    # SL transport unit: one SL state step m_j = I[m_{j-1}](X_D) at 1024^2 (config 4 unit ii)
+    sl = sl_step_rate(api, ctx, v_d, mT_d, timed)
+    return dict(value=value, ms=ms, launches=launches, clocks=clk, e2e=e2e_value, ms_e2e=ms_e2e,
+                wall_e2e=wall_e2e, prof=prof, sl=sl)
+
+
+def ctypes_launches(ctx):
+    import ctypes as C
+
+    n = C.c_longlong()
+    ctx.lib.vrg_launch_count(ctx.h, C.byref(n))
+    return n.value
+
+
+def profile_dump(ctx):
+    import ctypes as C
+
+    buf = C.create_string_buffer(1 << 16)
+    ctx.check(ctx.lib.vrg_profile_dump(ctx.h, buf, len(buf)))
+    prof = {}
+    for line in buf.value.decode().splitlines():
+        tag, cnt, tot = line.split("\t")
+        prof[tag] = (int(cnt), float(tot))
+    return prof
+
+
+def sl_step_rate(api, ctx, v_d, mT_d, timed):
+    nt = NT
+    s = api.Solver(ctx, v_d, nt)
+    s.solve_state_final(mT_d)  # builds the characteristics
+    ctx.lib.vrg_profile(ctx.h, 1)
+    s.solve_state_final(mT_d)
+    prof = profile_dump(ctx)
+    ctx.lib.vrg_profile(ctx.h, 0)
+    keys = ["k_prefilter_rows", "k_prefilter_cols", "evaluate/state_step"]
+    per_step_ms = sum(prof[k][1] for k in keys if k in prof) / nt
+    return {"unit": "one SL state step (prefilter rows+cols, 16-tap gather), 1024^2",
+            "algorithmic_bytes": 4 * F_BYTES, "us_per_step": per_step_ms * 1e3,
+            "gbps": 4 * F_BYTES / (per_step_ms / 1e3) / 1e9}
+
+
+# ------------------------------------------------------------------------------ CPU reference
+def reference_sample(threads: int, matvecs_per_thread: int = 1):
+    """One steady-state reference matvec (HessianOperator::apply, 1024^2, nt=16) per thread,
+    threads in parallel (ctypes releases the GIL).  Returns (seconds, matvecs)."""
+    from oracle import ref
+
+    mT, v, vtA, _ = make_problem(0)
+    ops = [None] * threads
+
+    def build(i):
+        ops[i] = ref.Hessian(v[0], v[1], mT, mT, NORM, BETA, 0, NT)
+        ops[i].apply(vtA[0], vtA[1])  # first apply builds the lazy caches
+
+    ths = [threading.Thread(target=build, args=(i,)) for i in range(threads)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+
+    def work(i):
+        for _ in range(matvecs_per_thread):
+            ops[i].apply(vtA[0], vtA[1])
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+    return time.perf_counter() - t0, threads * matvecs_per_thread, ops
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    from oracle import ref
+
+    if not ref.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libveloreg_ref.so not built (make -C oracle)"}
+    threads = min(cpu_threads(), 64)
+    from oracle import ref as R
+    mT, v, vtA, _ = make_problem(0)
+    ops = []
+    lock = threading.Lock()
+
+    def build():
+        h = R.Hessian(v[0], v[1], mT, mT, NORM, BETA, 0, NT)
+        h.apply(vtA[0], vtA[1])
+        with lock:
+            ops.append(h)
+
+    ths = [threading.Thread(target=build) for _ in range(threads)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+
+    def one_step():
+        ws = [threading.Thread(target=lambda h=h: h.apply(vtA[0], vtA[1])) for h in ops]
+        [w.start() for w in ws]
+        [w.join() for w in ws]
+
+    for _ in range(args.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    dt = time.perf_counter() - t0
+    value = threads * args.steps / dt
+    sample = (f"each step = {threads} concurrent steady-state HessianOperator::apply calls (one per host thread) "
+              f"of the unmodified reference, 1024^2 nt=16 H2, FFT backend = repo FFTW3-API shim")
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": CONFIG,
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline_leg():
+    from oracle import ref
+
+    if not ref.available():
+        return None
+    threads = min(cpu_threads(), 32)
+    dt, nmv, _ = reference_sample(threads)
+    return {"value": nmv / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{nmv} steady-state reference HessianOperator::apply calls at 1024^2 nt=16, one per host "
+                      f"thread in parallel ({dt:.1f} s); FFT via the repo's FFTW3-API shim"}
+
+
+# ------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="vrg", choices=["vrg", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        res = run_reference(args, rank)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    import torch
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = run_vrg(args, rank, world, local_rank)
+    if rank == 0:
+        prof = r["prof"]
+        dom = max(prof.items(), key=lambda kv: kv[1][1])
+        tag, (cnt, tot_ms) = dom
+        avg_s = tot_ms / cnt / 1e3
+        bytes_launch = KERNEL_BYTES_F.get(tag, 0) * F_BYTES
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except OSError:
+            pass
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        achieved = bytes_launch / avg_s / 1e9 if bytes_launch else None
+        prof_total = sum(t for _, t in prof.values())
+        mv_bytes = matvec_algorithmic_bytes()
+        line = {
+            "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": dict(CONFIG, parallelism=f"pairs{world}"),
+            "e2e": {"value": r["e2e"], "unit": UNIT, "h2d_bytes_per_step": 2 * F_BYTES, "d2h_bytes_per_step": 2 * F_BYTES,
+                    "call": "vrg_hess_apply_host (pinned host buffers)"},
+            "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
+            "roofline": {"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "bytes_per_launch": bytes_launch, "avg_launch_us": avg_s * 1e6,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"},
+            "matvec_roofline": {"algorithmic_bytes": mv_bytes, "model": "(24 nt + 12) F, SURVEY 8(d)",
+                                "achieved_gbps": mv_bytes * r["value"] / world / 1e9,
+                                "frac": mv_bytes * r["value"] / world / 1e9 / peak},
+            "sl_interp": r["sl"],
+            "kernel_share": {k: round(t / prof_total, 4) for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_leg()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/* vrg.h — C ABI of libvrg, the B200-native (sm_100a) drop-in for the reduced-space
+ * Gauss–Newton Hessian-matvec path of the reference solver `veloreg`
+ * (arXiv 1604.02153; reference C++ API in /root/reference/proj/core/include/veloreg).
+ *
+ * Every entry point replaces one reference interface, cited as path:line relative to
+ * /root/reference/proj/core.  Conventions:
+ *   - plain C: int status, opaque handles, plain pointers and sizes, no exceptions;
+ *   - fields are fp64 arrays of n1*n2 values, row-major, axis 1 fastest, node (i1,i2) at
+ *     (-pi + i1*2pi/n1, -pi + i2*2pi/n2) (include/veloreg/field.hpp:13-54); a trajectory is
+ *     (nt+1) consecutive fields; a vector field is two pointers (components 0 and 1);
+ *   - unless a name ends in _host, array arguments are DEVICE pointers on the context's
+ *     device; calls are ordered on the context's stream; calls that return host-visible
+ *     results (scalars, errors) synchronise that stream;
+ *   - status codes mirror the reference's exception types: VRG_INVALID_ARGUMENT for
+ *     std::invalid_argument, VRG_BLOWUP for transport::BlowupError (transport.hpp:35-38);
+ *     the message (identical to the reference's what()) is returned by vrg_last_error(ctx);
+ *   - operation counters follow counters.hpp:1-23 semantics; read them per context with
+ *     vrg_counters and add them to the process counters the host keeps.
+ */
+#ifndef VRG_H
+#define VRG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRG_OK 0
+#define VRG_INVALID_ARGUMENT 1
+#define VRG_BLOWUP 2
+#define VRG_RUNTIME_ERROR 3
+#define VRG_NOT_SUPPORTED 4
+
+/* enum values shared with the reference */
+#define VRG_H1SEMI 1 /* spectral::RegNorm (spectral.hpp:12) */
+#define VRG_H2SEMI 2
+#define VRG_H3SEMI 3
+#define VRG_COMPRESSIBLE 0 /* inverse::Deformation (inverse.hpp:15) */
+#define VRG_INCOMPRESSIBLE 1
+#define VRG_NEAR_INCOMPRESSIBLE 2
+#define VRG_FORWARD 0 /* transport::TraceDirection (transport.hpp:15) */
+#define VRG_BACKWARD 1
+#define VRG_GAUSS_NEWTON 0 /* transport::HessianMode (transport.hpp:16) */
+#define VRG_FULL_NEWTON 1
+#define VRG_BAND_LOW 0 /* spectral::Band (spectral.hpp:44) */
+#define VRG_BAND_HIGH 1
+
+typedef struct vrg_ctx_s* vrg_ctx_t;
+typedef struct vrg_solver_s* vrg_solver_t;
+typedef struct vrg_hess_s* vrg_hess_t;
+typedef struct vrg_coarse_s* vrg_coarse_t;
+
+/* ---- context / memory (no reference counterpart: the device runtime under the pImpls) ---- */
+const char* vrg_version(void);
+int vrg_ctx_create(int device, void* cuda_stream /* nullable: own stream */, vrg_ctx_t* out);
+void vrg_ctx_destroy(vrg_ctx_t ctx);
+const char* vrg_last_error(vrg_ctx_t ctx); /* ctx may be NULL: last error of this thread */
+int vrg_sync(vrg_ctx_t ctx);
+int vrg_malloc(vrg_ctx_t ctx, unsigned long long bytes, void** out);
+int vrg_free(vrg_ctx_t ctx, void* p);
+int vrg_host_alloc(vrg_ctx_t ctx, unsigned long long bytes, void** out); /* pinned */
+int vrg_host_free(vrg_ctx_t ctx, void* p);
+int vrg_copy_h2d(vrg_ctx_t ctx, void* dst, const void* src, unsigned long long bytes);
+int vrg_copy_d2h(vrg_ctx_t ctx, void* dst, const void* src, unsigned long long bytes);
+/* counters::snapshot / counters::reset (counters.hpp:16-20, counters.cpp:10-22), per context */
+int vrg_counters(vrg_ctx_t ctx, long long* ffts, long long* interps);
+int vrg_counters_reset(vrg_ctx_t ctx);
+/* instrumentation (no reference counterpart): kernels this library launched on the context,
+ * and an optional CUDA-event profile per launch site.  vrg_profile_dump writes lines
+ * "tag<TAB>launches<TAB>total_ms" and resets the profile. */
+int vrg_launch_count(vrg_ctx_t ctx, long long* launches);
+int vrg_profile(vrg_ctx_t ctx, int enable);
+int vrg_profile_dump(vrg_ctx_t ctx, char* buf, int cap);
+
+/* ---- field BLAS-1 (field.hpp:62-80, field.cpp:19-119) ---- */
+int vrg_dot(vrg_ctx_t ctx, int n1, int n2, const double* a1, const double* a2, const double* b1, const double* b2,
+            double* out); /* a2/b2 may be NULL for scalar fields */
+int vrg_norm_linf(vrg_ctx_t ctx, int n1, int n2, const double* a1, const double* a2, double* out);
+int vrg_axpy(vrg_ctx_t ctx, unsigned long long n, double a, const double* x, double* y);
+
+/* ---- interp (interp.hpp:27-34) ---- */
+int vrg_prefilter(vrg_ctx_t ctx, int n1, int n2, const double* u, double* c);
+int vrg_evaluate(vrg_ctx_t ctx, int n1, int n2, const double* c, const double* x1, const double* x2, double* out);
+
+/* ---- transport (transport.hpp:18-113) ---- */
+int vrg_derive_steps(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, double cfl, int* nt);
+int vrg_trace(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, double ht, int direction,
+              double* x1, double* x2); /* traceCharacteristics, transport.hpp:49 */
+/* transport::Solver (transport.hpp:71-100), scheme SL. */
+int vrg_solver_create(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, int nt, vrg_solver_t* out);
+void vrg_solver_destroy(vrg_solver_t s);
+int vrg_solver_state(vrg_solver_t s, const double* m0, double* traj);        /* solveState */
+int vrg_solver_adjoint(vrg_solver_t s, const double* lam1, double* traj);    /* solveAdjoint */
+int vrg_solver_state_final(vrg_solver_t s, const double* m0, double* out);   /* solveStateFinal */
+int vrg_solver_adjoint_final(vrg_solver_t s, const double* lam1, double* out); /* solveAdjointFinal */
+int vrg_solver_incstate(vrg_solver_t s, const double* vt1, const double* vt2, const double* state_traj,
+                        double* traj); /* solveIncState */
+int vrg_solver_incadjoint(vrg_solver_t s, const double* vt1, const double* vt2, const double* lt1,
+                          const double* adjoint_traj /* nullable */, int mode, double* traj); /* solveIncAdjoint */
+int vrg_solver_jacobian(vrg_solver_t s, double* out);                        /* jacobianDeterminant */
+int vrg_solver_departure(vrg_solver_t s, int direction, double* x1, double* x2); /* cached Characteristics */
+
+/* ---- spectral (spectral.hpp:27-56) ---- */
+int vrg_gradient(vrg_ctx_t ctx, int n1, int n2, const double* u, double* g1, double* g2);
+int vrg_divergence(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, double* out);
+int vrg_apply_reg(vrg_ctx_t ctx, int n1, int n2, int norm, double beta, const double* v1, const double* v2,
+                  double* o1, double* o2);
+int vrg_apply_inv_reg(vrg_ctx_t ctx, int n1, int n2, int norm, double beta, double power, const double* v1,
+                      const double* v2, double* o1, double* o2);
+int vrg_project_div_free(vrg_ctx_t ctx, int n1, int n2, const double* b1, const double* b2, double* o1, double* o2);
+int vrg_resample(vrg_ctx_t ctx, int n1, int n2, const double* u, int t1, int t2, double* out);
+int vrg_cutoff(vrg_ctx_t ctx, int n1, int n2, const double* u, int band, double* out);
+int vrg_gaussian_smooth(vrg_ctx_t ctx, int n1, int n2, const double* u, double sigma, double* out);
+
+/* ---- inverse (inverse.hpp:60-105) ---- */
+/* inverse::HessianOperator(v, problem, model, tg, cfg{SL}, mode, state) (inverse.hpp:74-80).
+ * state_traj: nullable device trajectory to reuse (inverse.cpp:162-172). */
+int vrg_hess_create(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                    const double* mT, int norm, double beta, int deformation, int nt, int mode,
+                    const double* state_traj, vrg_hess_t* out);
+void vrg_hess_destroy(vrg_hess_t h);
+int vrg_hess_apply(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);      /* apply */
+int vrg_hess_apply_data(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2); /* applyDataTerm */
+/* applySplitHessianOf (precond.cpp:20-26): M^{-1/2} Q M^{-1/2} s + s */
+int vrg_hess_apply_split(vrg_hess_t h, const double* s1, const double* s2, double* o1, double* o2);
+/* apply() from HOST buffers: H2D of vtilde, matvec, D2H of the result (the drop-in call a
+ * host-side caller of HessianOperator::apply makes; value semantics of inverse.hpp:83). */
+int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);
+int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajectory */
+
+/* evaluateGradient / evaluateObjective (inverse.hpp:60-71); scalars = [objective, mismatch, regTerm] */
+int vrg_evaluate_gradient(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                          const double* mT, int norm, double beta, int deformation, int nt, double* g1, double* g2,
+                          double* scalars);
+int vrg_evaluate_objective(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                           const double* mT, int norm, double beta, int deformation, int nt, double* scalars);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VRG_H */

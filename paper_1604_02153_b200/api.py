@@ -1,0 +1,340 @@
+"""Python host mirror of the reference's operator/solver API over the C ABI (include/vrg.h).
+
+Names, argument meaning and error behaviour follow veloreg:: (include/veloreg/*.hpp):
+``interp.prefilter/evaluate``, ``transport.Solver``, ``spectral.*``,
+``inverse.HessianOperator``, ``evaluateGradient/evaluateObjective``.  Fields are float64
+CUDA tensors of shape (n1, n2) on the context's device; vector fields are pairs of tensors.
+Exceptions: InvalidArgument (std::invalid_argument), BlowupError (transport::BlowupError),
+NotSupported.  Every call runs the sm_100a kernels in libvrg.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi
+
+H1SEMI, H2SEMI, H3SEMI = 1, 2, 3
+COMPRESSIBLE, INCOMPRESSIBLE, NEAR_INCOMPRESSIBLE = 0, 1, 2
+FORWARD, BACKWARD = 0, 1
+GAUSS_NEWTON, FULL_NEWTON = 0, 1
+BAND_LOW, BAND_HIGH = 0, 1
+
+
+class VrgError(RuntimeError):
+    code = _capi.VRG_RUNTIME_ERROR
+
+
+class InvalidArgument(VrgError, ValueError):
+    code = _capi.VRG_INVALID_ARGUMENT
+
+
+class BlowupError(VrgError):
+    code = _capi.VRG_BLOWUP
+
+
+class NotSupported(VrgError, NotImplementedError):
+    code = _capi.VRG_NOT_SUPPORTED
+
+
+_ERRORS = {1: InvalidArgument, 2: BlowupError, 3: VrgError, 4: NotSupported}
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+class Context:
+    """One device + stream (the library's vrg_ctx_t).  Kernels run on torch's current stream of
+    `device`, so torch ops and library calls are stream-ordered."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise VrgError("libvrg needs a CUDA device (no CPU fallback)")
+        self.lib = _capi.load()
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        code = self.lib.vrg_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        if code:
+            raise _ERRORS.get(code, VrgError)(self.lib.vrg_last_error(None).decode())
+        self.h = h
+
+    def check(self, code: int):
+        if code:
+            raise _ERRORS.get(code, VrgError)(self.lib.vrg_last_error(self.h).decode())
+
+    def counters(self):
+        f, i = C.c_longlong(), C.c_longlong()
+        self.lib.vrg_counters(self.h, C.byref(f), C.byref(i))
+        return f.value, i.value
+
+    def reset_counters(self):
+        self.lib.vrg_counters_reset(self.h)
+
+    def sync(self):
+        self.check(self.lib.vrg_sync(self.h))
+
+    def field(self, a) -> torch.Tensor:
+        """A float64 contiguous device tensor holding `a` (numpy array or tensor)."""
+        t = torch.as_tensor(a, dtype=torch.float64)
+        return t.to(self.device).contiguous()
+
+    def empty(self, *shape) -> torch.Tensor:
+        return torch.empty(*shape, dtype=torch.float64, device=self.device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vrg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _shape(u):
+    n1, n2 = u.shape[-2], u.shape[-1]
+    return int(n1), int(n2)
+
+
+# ---------------------------------------------------------------- field BLAS-1 (field.hpp:62-80)
+def dot(ctx, a, b):
+    """h1*h2*sum(a*b) for scalar fields, sum over components for pairs (field.cpp:47-54)."""
+    out = C.c_double()
+    if isinstance(a, tuple):
+        n1, n2 = _shape(a[0])
+        ctx.check(ctx.lib.vrg_dot(ctx.h, n1, n2, _p(a[0]), _p(a[1]), _p(b[0]), _p(b[1]), C.byref(out)))
+    else:
+        n1, n2 = _shape(a)
+        ctx.check(ctx.lib.vrg_dot(ctx.h, n1, n2, _p(a), None, _p(b), None, C.byref(out)))
+    return out.value
+
+
+def norm_linf(ctx, a):
+    out = C.c_double()
+    if isinstance(a, tuple):
+        n1, n2 = _shape(a[0])
+        ctx.check(ctx.lib.vrg_norm_linf(ctx.h, n1, n2, _p(a[0]), _p(a[1]), C.byref(out)))
+    else:
+        n1, n2 = _shape(a)
+        ctx.check(ctx.lib.vrg_norm_linf(ctx.h, n1, n2, _p(a), None, C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------- interp (interp.hpp:27-34)
+def prefilter(ctx, u):
+    n1, n2 = _shape(u)
+    c = ctx.empty(n1, n2)
+    ctx.check(ctx.lib.vrg_prefilter(ctx.h, n1, n2, _p(u), _p(c)))
+    return c
+
+
+def evaluate(ctx, c, x1, x2):
+    n1, n2 = _shape(c)
+    if tuple(x1.shape) != (n1, n2) or tuple(x2.shape) != (n1, n2):
+        raise InvalidArgument("evaluate: point set does not match coefficient grid")
+    out = ctx.empty(n1, n2)
+    ctx.check(ctx.lib.vrg_evaluate(ctx.h, n1, n2, _p(c), _p(x1), _p(x2), _p(out)))
+    return out
+
+
+# ---------------------------------------------------------------- spectral (spectral.hpp:27-56)
+def gradient(ctx, u):
+    n1, n2 = _shape(u)
+    g = ctx.empty(2, n1, n2)
+    ctx.check(ctx.lib.vrg_gradient(ctx.h, n1, n2, _p(u), _p(g[0]), _p(g[1])))
+    return g[0], g[1]
+
+
+def divergence(ctx, v):
+    n1, n2 = _shape(v[0])
+    out = ctx.empty(n1, n2)
+    ctx.check(ctx.lib.vrg_divergence(ctx.h, n1, n2, _p(v[0]), _p(v[1]), _p(out)))
+    return out
+
+
+def apply_reg(ctx, v, norm, beta):
+    n1, n2 = _shape(v[0])
+    o = ctx.empty(2, n1, n2)
+    ctx.check(ctx.lib.vrg_apply_reg(ctx.h, n1, n2, norm, beta, _p(v[0]), _p(v[1]), _p(o[0]), _p(o[1])))
+    return o[0], o[1]
+
+
+def apply_inv_reg(ctx, v, norm, beta, power):
+    n1, n2 = _shape(v[0])
+    o = ctx.empty(2, n1, n2)
+    ctx.check(ctx.lib.vrg_apply_inv_reg(ctx.h, n1, n2, norm, beta, power, _p(v[0]), _p(v[1]), _p(o[0]), _p(o[1])))
+    return o[0], o[1]
+
+
+def project_div_free(ctx, b):
+    n1, n2 = _shape(b[0])
+    o = ctx.empty(2, n1, n2)
+    ctx.check(ctx.lib.vrg_project_div_free(ctx.h, n1, n2, _p(b[0]), _p(b[1]), _p(o[0]), _p(o[1])))
+    return o[0], o[1]
+
+
+def resample(ctx, u, target):
+    n1, n2 = _shape(u)
+    out = ctx.empty(*target)
+    ctx.check(ctx.lib.vrg_resample(ctx.h, n1, n2, _p(u), int(target[0]), int(target[1]), _p(out)))
+    return out
+
+
+def cutoff_filter(ctx, u, band):
+    n1, n2 = _shape(u)
+    out = ctx.empty(n1, n2)
+    ctx.check(ctx.lib.vrg_cutoff(ctx.h, n1, n2, _p(u), band, _p(out)))
+    return out
+
+
+def gaussian_smooth(ctx, u, sigma):
+    n1, n2 = _shape(u)
+    out = ctx.empty(n1, n2)
+    ctx.check(ctx.lib.vrg_gaussian_smooth(ctx.h, n1, n2, _p(u), sigma, _p(out)))
+    return out
+
+
+# ---------------------------------------------------------------- transport (transport.hpp)
+def derive_steps(ctx, v, cfl):
+    n1, n2 = _shape(v[0])
+    nt = C.c_int()
+    ctx.check(ctx.lib.vrg_derive_steps(ctx.h, n1, n2, _p(v[0]), _p(v[1]), cfl, C.byref(nt)))
+    return nt.value
+
+
+def trace_characteristics(ctx, v, ht, direction=FORWARD):
+    n1, n2 = _shape(v[0])
+    x = ctx.empty(2, n1, n2)
+    ctx.check(ctx.lib.vrg_trace(ctx.h, n1, n2, _p(v[0]), _p(v[1]), ht, direction, _p(x[0]), _p(x[1])))
+    return x[0], x[1]
+
+
+class Solver:
+    """transport::Solver with scheme SL (transport.hpp:71-100)."""
+
+    def __init__(self, ctx, v, nt):
+        self.ctx = ctx
+        self.shape = _shape(v[0])
+        self.nt = int(nt)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.vrg_solver_create(ctx.h, *self.shape, _p(v[0]), _p(v[1]), self.nt, C.byref(h)))
+        self.h = h
+
+    def _traj(self):
+        return self.ctx.empty(self.nt + 1, *self.shape)
+
+    def solve_state(self, m0):
+        t = self._traj()
+        self.ctx.check(self.ctx.lib.vrg_solver_state(self.h, _p(m0), _p(t)))
+        return t
+
+    def solve_adjoint(self, lam1):
+        t = self._traj()
+        self.ctx.check(self.ctx.lib.vrg_solver_adjoint(self.h, _p(lam1), _p(t)))
+        return t
+
+    def solve_state_final(self, m0):
+        o = self.ctx.empty(*self.shape)
+        self.ctx.check(self.ctx.lib.vrg_solver_state_final(self.h, _p(m0), _p(o)))
+        return o
+
+    def solve_adjoint_final(self, lam1):
+        o = self.ctx.empty(*self.shape)
+        self.ctx.check(self.ctx.lib.vrg_solver_adjoint_final(self.h, _p(lam1), _p(o)))
+        return o
+
+    def solve_inc_state(self, vt, state):
+        t = self._traj()
+        self.ctx.check(self.ctx.lib.vrg_solver_incstate(self.h, _p(vt[0]), _p(vt[1]), _p(state), _p(t)))
+        return t
+
+    def solve_inc_adjoint(self, vt, lt1, adjoint=None, mode=GAUSS_NEWTON):
+        t = self._traj()
+        self.ctx.check(self.ctx.lib.vrg_solver_incadjoint(self.h, _p(vt[0]), _p(vt[1]), _p(lt1), _p(adjoint), mode,
+                                                          _p(t)))
+        return t
+
+    def jacobian_determinant(self):
+        o = self.ctx.empty(*self.shape)
+        self.ctx.check(self.ctx.lib.vrg_solver_jacobian(self.h, _p(o)))
+        return o
+
+    def departure(self, direction=FORWARD):
+        x = self.ctx.empty(2, *self.shape)
+        self.ctx.check(self.ctx.lib.vrg_solver_departure(self.h, direction, _p(x[0]), _p(x[1])))
+        return x[0], x[1]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.vrg_solver_destroy(self.h)
+            self.h = None
+
+
+# ---------------------------------------------------------------- inverse (inverse.hpp)
+class HessianOperator:
+    """inverse::HessianOperator, GN mode, SL scheme with fixed nt (inverse.hpp:74-97)."""
+
+    def __init__(self, ctx, v, mR, mT, norm, beta, deformation, nt, mode=GAUSS_NEWTON, state=None):
+        self.ctx = ctx
+        self.shape = _shape(v[0])
+        self.nt = int(nt)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.vrg_hess_create(ctx.h, *self.shape, _p(v[0]), _p(v[1]), _p(mR), _p(mT), norm, beta,
+                                          deformation, self.nt, mode, _p(state), C.byref(h)))
+        self.h = h
+
+    def _out(self, out):
+        return out if out is not None else self.ctx.empty(2, *self.shape)
+
+    def apply(self, vt, out=None):
+        o = self._out(out)
+        self.ctx.check(self.ctx.lib.vrg_hess_apply(self.h, _p(vt[0]), _p(vt[1]), _p(o[0]), _p(o[1])))
+        return o[0], o[1]
+
+    def apply_data_term(self, vt, out=None):
+        o = self._out(out)
+        self.ctx.check(self.ctx.lib.vrg_hess_apply_data(self.h, _p(vt[0]), _p(vt[1]), _p(o[0]), _p(o[1])))
+        return o[0], o[1]
+
+    def apply_split(self, s, out=None):
+        o = self._out(out)
+        self.ctx.check(self.ctx.lib.vrg_hess_apply_split(self.h, _p(s[0]), _p(s[1]), _p(o[0]), _p(o[1])))
+        return o[0], o[1]
+
+    def apply_host(self, vt1, vt2, o1, o2):
+        """apply() on host (numpy or pinned torch) buffers: H2D + matvec + D2H."""
+        def hp(a):
+            return C.c_void_p(a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr())
+        self.ctx.check(self.ctx.lib.vrg_hess_apply_host(self.h, hp(vt1), hp(vt2), hp(o1), hp(o2)))
+
+    def state(self):
+        t = self.ctx.empty(self.nt + 1, *self.shape)
+        self.ctx.check(self.ctx.lib.vrg_hess_state(self.h, _p(t)))
+        return t
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.vrg_hess_destroy(self.h)
+            self.h = None
+
+
+def evaluate_gradient(ctx, v, mR, mT, norm, beta, deformation, nt):
+    n1, n2 = _shape(v[0])
+    g = ctx.empty(2, n1, n2)
+    sc = (C.c_double * 3)()
+    ctx.check(ctx.lib.vrg_evaluate_gradient(ctx.h, n1, n2, _p(v[0]), _p(v[1]), _p(mR), _p(mT), norm, beta,
+                                            deformation, nt, _p(g[0]), _p(g[1]), C.cast(sc, C.c_void_p)))
+    return (g[0], g[1]), tuple(sc)
+
+
+def evaluate_objective(ctx, v, mR, mT, norm, beta, deformation, nt):
+    n1, n2 = _shape(v[0])
+    sc = (C.c_double * 3)()
+    ctx.check(ctx.lib.vrg_evaluate_objective(ctx.h, n1, n2, _p(v[0]), _p(v[1]), _p(mR), _p(mT), norm, beta,
+                                             deformation, nt, C.cast(sc, C.c_void_p)))
+    return tuple(sc)

@@ -1,0 +1,424 @@
+// extern "C" boundary of libvrg (include/vrg.h).  Exceptions never cross it: each entry point
+// maps them to the status codes the reference's exception types correspond to.
+#include <cstdio>
+#include <cstring>
+#include <map>
+
+#include "../../include/vrg.h"
+#include "inverse.cuh"
+
+struct vrg_ctx_s {
+    vrg::Ctx ctx;
+    vrg_ctx_s(int dev, cudaStream_t s) : ctx(dev, s) {}
+};
+struct vrg_solver_s {
+    vrg_ctx_s* owner;
+    vrg::Solver solver;
+};
+struct vrg_hess_s {
+    vrg_ctx_s* owner;
+    vrg::Hessian hess;
+    vrg::DBuf io;  // device staging for the host-buffer entry point
+};
+
+namespace {
+
+thread_local std::string g_threadErr;
+
+template <class F>
+int guarded(vrg_ctx_s* c, F&& f) {
+    std::string msg;
+    int code = VRG_OK;
+    try {
+        if (c) VRG_CUDA(cudaSetDevice(c->ctx.device));
+        f();
+        return VRG_OK;
+    } catch (const vrg::BlowupError& e) {
+        code = VRG_BLOWUP;
+        msg = e.what();
+    } catch (const std::invalid_argument& e) {
+        code = VRG_INVALID_ARGUMENT;
+        msg = e.what();
+    } catch (const vrg::NotSupported& e) {
+        code = VRG_NOT_SUPPORTED;
+        msg = e.what();
+    } catch (const std::exception& e) {
+        code = VRG_RUNTIME_ERROR;
+        msg = e.what();
+    }
+    g_threadErr = msg;
+    if (c) c->ctx.err = msg;
+    return code;
+}
+
+vrg::GridDims dims(int n1, int n2) {
+    vrg::checkGrid(n1, n2);
+    return vrg::GridDims(n1, n2);
+}
+
+vrg::Model modelOf(int norm, double beta, int deformation) {
+    if (norm < 1 || norm > 3) throw vrg::InvalidArgument("unknown regularization norm");
+    if (deformation < 0 || deformation > 2) throw vrg::InvalidArgument("unknown deformation model");
+    vrg::Model m;
+    m.norm = norm;
+    m.betaV = beta;
+    m.deformation = deformation;
+    return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vrg_version(void) { return "vrg 0.1 (sm_100a)"; }
+
+int vrg_ctx_create(int device, void* stream, vrg_ctx_t* out) {
+    *out = nullptr;
+    return guarded(nullptr, [&] { *out = new vrg_ctx_s(device, static_cast<cudaStream_t>(stream)); });
+}
+
+void vrg_ctx_destroy(vrg_ctx_t c) { delete c; }
+
+const char* vrg_last_error(vrg_ctx_t c) { return c ? c->ctx.err.c_str() : g_threadErr.c_str(); }
+
+int vrg_sync(vrg_ctx_t c) {
+    return guarded(c, [&] { c->ctx.sync(); });
+}
+
+int vrg_malloc(vrg_ctx_t c, unsigned long long bytes, void** out) {
+    return guarded(c, [&] { VRG_CUDA(cudaMalloc(out, bytes)); });
+}
+
+int vrg_free(vrg_ctx_t c, void* p) {
+    return guarded(c, [&] { VRG_CUDA(cudaFree(p)); });
+}
+
+int vrg_host_alloc(vrg_ctx_t c, unsigned long long bytes, void** out) {
+    return guarded(c, [&] { VRG_CUDA(cudaMallocHost(out, bytes)); });
+}
+
+int vrg_host_free(vrg_ctx_t c, void* p) {
+    return guarded(c, [&] { VRG_CUDA(cudaFreeHost(p)); });
+}
+
+int vrg_copy_h2d(vrg_ctx_t c, void* dst, const void* src, unsigned long long bytes) {
+    return guarded(c, [&] {
+        VRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->ctx.stream));
+        c->ctx.sync();
+    });
+}
+
+int vrg_copy_d2h(vrg_ctx_t c, void* dst, const void* src, unsigned long long bytes) {
+    return guarded(c, [&] {
+        VRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->ctx.stream));
+        c->ctx.sync();
+    });
+}
+
+int vrg_counters(vrg_ctx_t c, long long* ffts, long long* interps) {
+    *ffts = c->ctx.ffts;
+    *interps = c->ctx.interps;
+    return VRG_OK;
+}
+
+int vrg_counters_reset(vrg_ctx_t c) {
+    c->ctx.ffts = 0;
+    c->ctx.interps = 0;
+    return VRG_OK;
+}
+
+int vrg_launch_count(vrg_ctx_t c, long long* launches) {
+    *launches = c->ctx.launches;
+    return VRG_OK;
+}
+
+int vrg_profile(vrg_ctx_t c, int enable) {
+    return guarded(c, [&] {
+        c->ctx.sync();
+        c->ctx.profOn = enable != 0;
+        c->ctx.profRecs.clear();
+        c->ctx.evNext = 0;
+    });
+}
+
+int vrg_profile_dump(vrg_ctx_t c, char* buf, int cap) {
+    return guarded(c, [&] {
+        vrg::Ctx& ctx = c->ctx;
+        ctx.sync();
+        std::map<std::string, std::pair<long long, double>> acc;
+        for (const auto& r : ctx.profRecs) {
+            float ms = 0.f;
+            VRG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            auto& e = acc[r.tag];
+            e.first += 1;
+            e.second += ms;
+        }
+        std::string out;
+        for (const auto& kv : acc) {
+            char line[256];
+            std::snprintf(line, sizeof line, "%s\t%lld\t%.6f\n", kv.first.c_str(), kv.second.first, kv.second.second);
+            out += line;
+        }
+        ctx.profRecs.clear();
+        ctx.evNext = 0;
+        if (cap > 0) {
+            std::strncpy(buf, out.c_str(), static_cast<std::size_t>(cap) - 1);
+            buf[cap - 1] = '\0';
+        }
+    });
+}
+
+// ---- BLAS-1
+int vrg_dot(vrg_ctx_t c, int n1, int n2, const double* a1, const double* a2, const double* b1, const double* b2,
+            double* out) {
+    return guarded(c, [&] { *out = vrg::dot(c->ctx, dims(n1, n2), a1, a2, b1, b2); });
+}
+
+int vrg_norm_linf(vrg_ctx_t c, int n1, int n2, const double* a1, const double* a2, double* out) {
+    return guarded(c, [&] { *out = vrg::normLinf(c->ctx, dims(n1, n2).points(), a1, a2); });
+}
+
+int vrg_axpy(vrg_ctx_t c, unsigned long long n, double a, const double* x, double* y) {
+    return guarded(c, [&] { vrg::axpby(c->ctx, n, a, x, 1.0, y); });
+}
+
+// ---- interp
+int vrg_prefilter(vrg_ctx_t c, int n1, int n2, const double* u, double* coef) {
+    return guarded(c, [&] {
+        const auto g = dims(n1, n2);
+        double* tmp = c->ctx.scratchBuf(30, sizeof(double) * g.points());
+        unsigned* flag = reinterpret_cast<unsigned*>(c->ctx.scratchBuf(31, 64));
+        VRG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), c->ctx.stream));
+        vrg::launchPrefilter(c->ctx, g, u, coef, tmp, flag);
+        unsigned h = 0;
+        VRG_CUDA(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, c->ctx.stream));
+        c->ctx.sync();
+        if (h) throw vrg::InvalidArgument("prefilter: non-finite value");
+    });
+}
+
+int vrg_evaluate(vrg_ctx_t c, int n1, int n2, const double* coef, const double* x1, const double* x2, double* out) {
+    return guarded(c, [&] {
+        const auto g = dims(n1, n2);
+        if (vrg::anyNonFinite(c->ctx, g.points(), x1, x2))
+            throw vrg::InvalidArgument("evaluate: non-finite point coordinate");
+        vrg::launchEvaluate<1>(c->ctx, g, vrg::CoeffSet<1>{{coef}}, x1, x2, vrg::EpiStore1{nullptr, out});
+        c->ctx.interps += 1;
+        c->ctx.sync();
+    });
+}
+
+// ---- transport
+int vrg_derive_steps(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, double cfl, int* nt) {
+    return guarded(c, [&] { *nt = vrg::deriveSteps(c->ctx, dims(n1, n2), v1, v2, cfl); });
+}
+
+int vrg_trace(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, double ht, int direction, double* x1,
+              double* x2) {
+    return guarded(c, [&] {
+        const auto g = dims(n1, n2);
+        if (!(ht > 0.0)) throw vrg::InvalidArgument("traceCharacteristics: ht must be positive");
+        if (vrg::anyNonFinite(c->ctx, g.points(), v1, v2))
+            throw vrg::InvalidArgument("traceCharacteristics velocity: non-finite value");
+        double* cv = c->ctx.scratchBuf(32, sizeof(double) * 2 * g.points());
+        double* tmp = c->ctx.scratchBuf(30, sizeof(double) * g.points());
+        vrg::launchPrefilter(c->ctx, g, v1, cv, tmp, nullptr);
+        vrg::launchPrefilter(c->ctx, g, v2, cv + g.points(), tmp, nullptr);
+        vrg::launchTrace(c->ctx, g, v1, v2, cv, cv + g.points(), ht, direction, x1, x2);
+        c->ctx.interps += 2;
+        c->ctx.sync();
+    });
+}
+
+int vrg_solver_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, int nt, vrg_solver_t* out) {
+    *out = nullptr;
+    return guarded(c, [&] { *out = new vrg_solver_s{c, vrg::Solver(c->ctx, dims(n1, n2), v1, v2, nt)}; });
+}
+
+void vrg_solver_destroy(vrg_solver_t s) { delete s; }
+
+int vrg_solver_state(vrg_solver_t s, const double* m0, double* traj) {
+    return guarded(s->owner, [&] { s->solver.state(m0, traj, true); });
+}
+
+int vrg_solver_adjoint(vrg_solver_t s, const double* lam1, double* traj) {
+    return guarded(s->owner, [&] { s->solver.adjoint(lam1, traj, true); });
+}
+
+int vrg_solver_state_final(vrg_solver_t s, const double* m0, double* out) {
+    return guarded(s->owner, [&] { s->solver.stateFinal(m0, out); });
+}
+
+int vrg_solver_adjoint_final(vrg_solver_t s, const double* lam1, double* out) {
+    return guarded(s->owner, [&] { s->solver.adjointFinal(lam1, out); });
+}
+
+int vrg_solver_incstate(vrg_solver_t s, const double* vt1, const double* vt2, const double* state, double* traj) {
+    return guarded(s->owner, [&] { s->solver.incState(vt1, vt2, state, traj); });
+}
+
+int vrg_solver_incadjoint(vrg_solver_t s, const double* vt1, const double* vt2, const double* lt1,
+                          const double* adjoint, int mode, double* traj) {
+    return guarded(s->owner, [&] {
+        (void)vt1;
+        (void)vt2;
+        if (mode == VRG_FULL_NEWTON) {
+            if (!adjoint)
+                throw vrg::InvalidArgument("solveIncAdjoint: full Newton mode requires the adjoint trajectory");
+            throw vrg::NotSupported("solveIncAdjoint: full-Newton SL incremental adjoint is not implemented yet");
+        }
+        // Gauss-Newton drops every term in lambda: same operator as the adjoint
+        // (transport.cpp:392-397), unguarded.
+        s->solver.adjoint(lt1, traj, false);
+    });
+}
+
+int vrg_solver_jacobian(vrg_solver_t s, double* out) {
+    return guarded(s->owner, [&] { s->solver.jacobian(out); });
+}
+
+int vrg_solver_departure(vrg_solver_t s, int direction, double* x1, double* x2) {
+    return guarded(s->owner, [&] {
+        const double* X = s->solver.departure(direction);
+        const std::size_t N = s->solver.g.points();
+        vrg::copy(s->solver.ctx, N, X, x1);
+        vrg::copy(s->solver.ctx, N, X + N, x2);
+        s->solver.ctx.sync();
+    });
+}
+
+// ---- spectral
+int vrg_gradient(vrg_ctx_t c, int n1, int n2, const double* u, double* g1, double* g2) {
+    return guarded(c, [&] {
+        vrg::gradient(c->ctx, dims(n1, n2), u, g1, g2);
+        c->ctx.sync();
+    });
+}
+
+int vrg_divergence(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, double* out) {
+    return guarded(c, [&] {
+        vrg::divergence(c->ctx, dims(n1, n2), v1, v2, out);
+        c->ctx.sync();
+    });
+}
+
+int vrg_apply_reg(vrg_ctx_t c, int n1, int n2, int norm, double beta, const double* v1, const double* v2, double* o1,
+                  double* o2) {
+    return guarded(c, [&] {
+        if (beta <= 0.0) throw vrg::InvalidArgument("applyReg: beta must be positive");
+        vrg::Weights w(dims(n1, n2), modelOf(norm, beta, 0).norm);
+        vrg::applyRealSymbol(c->ctx, w.g, v1, v2, o1, o2, w.regSymbol(beta));
+        c->ctx.sync();
+    });
+}
+
+int vrg_apply_inv_reg(vrg_ctx_t c, int n1, int n2, int norm, double beta, double power, const double* v1,
+                      const double* v2, double* o1, double* o2) {
+    return guarded(c, [&] {
+        if (beta <= 0.0) throw vrg::InvalidArgument("applyInvReg: beta must be positive");
+        vrg::Weights w(dims(n1, n2), modelOf(norm, beta, 0).norm);
+        vrg::applyRealSymbol(c->ctx, w.g, v1, v2, o1, o2, w.invRegSymbol(beta, power));
+        c->ctx.sync();
+    });
+}
+
+int vrg_project_div_free(vrg_ctx_t c, int n1, int n2, const double* b1, const double* b2, double* o1, double* o2) {
+    return guarded(c, [&] {
+        vrg::projectDivFree(c->ctx, dims(n1, n2), b1, b2, o1, o2);
+        c->ctx.sync();
+    });
+}
+
+int vrg_resample(vrg_ctx_t c, int n1, int n2, const double* u, int t1, int t2, double* out) {
+    return guarded(c, [&] {
+        vrg::resample(c->ctx, dims(n1, n2), u, dims(t1, t2), out);
+        c->ctx.sync();
+    });
+}
+
+int vrg_cutoff(vrg_ctx_t c, int n1, int n2, const double* u, int band, double* out) {
+    return guarded(c, [&] {
+        const auto g = dims(n1, n2);
+        vrg::cutoff(c->ctx, g, u, band == VRG_BAND_LOW ? out : nullptr, band == VRG_BAND_LOW ? nullptr : out);
+        c->ctx.sync();
+    });
+}
+
+int vrg_gaussian_smooth(vrg_ctx_t c, int n1, int n2, const double* u, double sigma, double* out) {
+    return guarded(c, [&] {
+        vrg::gaussianSmooth(c->ctx, dims(n1, n2), u, sigma, out);
+        c->ctx.sync();
+    });
+}
+
+// ---- inverse
+int vrg_hess_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                    const double* mT, int norm, double beta, int deformation, int nt, int mode, const double* state,
+                    vrg_hess_t* out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        if (mode != VRG_GAUSS_NEWTON)
+            throw vrg::NotSupported("HessianOperator: full-Newton mode is not implemented on the device yet");
+        *out = new vrg_hess_s{c, vrg::Hessian(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation),
+                                              nt, state),
+                              vrg::DBuf()};
+    });
+}
+
+void vrg_hess_destroy(vrg_hess_t h) { delete h; }
+
+int vrg_hess_apply(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2) {
+    return guarded(h->owner, [&] { h->hess.apply(vt1, vt2, o1, o2); });
+}
+
+int vrg_hess_apply_data(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2) {
+    return guarded(h->owner, [&] { h->hess.applyDataTerm(vt1, vt2, o1, o2); });
+}
+
+int vrg_hess_apply_split(vrg_hess_t h, const double* s1, const double* s2, double* o1, double* o2) {
+    return guarded(h->owner, [&] { h->hess.applySplit(s1, s2, o1, o2); });
+}
+
+int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2) {
+    return guarded(h->owner, [&] {
+        vrg::Ctx& ctx = h->hess.ctx;
+        const std::size_t N = h->hess.g.points();
+        if (!h->io) h->io.alloc(sizeof(double) * 4 * N);
+        double* d = h->io.d();
+        VRG_CUDA(cudaMemcpyAsync(d, vt1, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+        VRG_CUDA(cudaMemcpyAsync(d + N, vt2, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+        h->hess.apply(d, d + N, d + 2 * N, d + 3 * N);
+        VRG_CUDA(cudaMemcpyAsync(o1, d + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        VRG_CUDA(cudaMemcpyAsync(o2, d + 3 * N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+    });
+}
+
+int vrg_hess_state(vrg_hess_t h, double* traj) {
+    return guarded(h->owner, [&] {
+        const std::size_t N = h->hess.g.points();
+        vrg::copy(h->hess.ctx, (h->hess.nt + 1) * N, h->hess.state(), traj);
+        h->hess.ctx.sync();
+    });
+}
+
+int vrg_evaluate_gradient(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                          const double* mT, int norm, double beta, int deformation, int nt, double* g1, double* g2,
+                          double* scalars) {
+    return guarded(c, [&] {
+        vrg::evaluateGradient(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation), nt, g1, g2,
+                              scalars, nullptr, nullptr, nullptr);
+        c->ctx.sync();
+    });
+}
+
+int vrg_evaluate_objective(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                           const double* mT, int norm, double beta, int deformation, int nt, double* scalars) {
+    return guarded(c, [&] {
+        vrg::evaluateObjective(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation), nt, scalars,
+                               nullptr);
+        c->ctx.sync();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// Shared runtime pieces of libvrg: context, device buffers, errors, cuFFT plan cache.
+//
+// Layout in HBM: every scalar field is one contiguous fp64 array of
+// n1*n2 values, row-major with axis 1 fastest, node (i1,i2) at (-pi+i1*h1, -pi+i2*h2) — the
+// reference's Grid/ScalarField layout (include/veloreg/field.hpp:15-54).  Vector fields are two
+// such arrays (SoA).  Trajectories are (nt+1) consecutive fields.  Half spectra are n1 x
+// (n2/2+1) cufftDoubleComplex, the FFTW r2c layout of src/fft.cpp:57-78.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace vrg {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 2.0 * kPi;
+constexpr double kBlowupFactor = 1e3;  // src/transport.cpp:14
+
+// Status codes of the C ABI (include/vrg.h).
+enum Status : int { kOk = 0, kInvalidArgument = 1, kBlowup = 2, kRuntime = 3, kNotSupported = 4 };
+
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct BlowupError : std::runtime_error {  // transport::BlowupError (transport.hpp:35-38)
+    using std::runtime_error::runtime_error;
+};
+struct NotSupported : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void throwCuda(cudaError_t e, const char* what, const char* file, int line);
+void throwCufft(cufftResult r, const char* what, const char* file, int line);
+
+#define VRG_CUDA(x)                                                              \
+    do {                                                                         \
+        cudaError_t e_ = (x);                                                    \
+        if (e_ != cudaSuccess) ::vrg::throwCuda(e_, #x, __FILE__, __LINE__);     \
+    } while (0)
+#define VRG_CUFFT(x)                                                             \
+    do {                                                                         \
+        cufftResult r_ = (x);                                                    \
+        if (r_ != CUFFT_SUCCESS) ::vrg::throwCufft(r_, #x, __FILE__, __LINE__);  \
+    } while (0)
+#define VRG_LAUNCH_CHECK() VRG_CUDA(cudaGetLastError())
+
+// Owning device allocation (RAII).
+class DBuf {
+public:
+    DBuf() = default;
+    explicit DBuf(std::size_t bytes) { alloc(bytes); }
+    ~DBuf() { release(); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr; o.bytes_ = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p_ = o.p_; bytes_ = o.bytes_; o.p_ = nullptr; o.bytes_ = 0; }
+        return *this;
+    }
+    void alloc(std::size_t bytes) {
+        release();
+        if (bytes) VRG_CUDA(cudaMalloc(&p_, bytes));
+        bytes_ = bytes;
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        bytes_ = 0;
+    }
+    template <typename T = double>
+    T* as() const { return static_cast<T*>(p_); }
+    double* d() const { return static_cast<double*>(p_); }
+    std::size_t bytes() const { return bytes_; }
+    explicit operator bool() const { return p_ != nullptr; }
+
+private:
+    void* p_ = nullptr;
+    std::size_t bytes_ = 0;
+};
+
+struct GridDims {
+    int n1 = 0, n2 = 0;
+    GridDims() = default;
+    GridDims(int a, int b) : n1(a), n2(b) {}
+    std::size_t points() const { return static_cast<std::size_t>(n1) * n2; }
+    int specCols() const { return n2 / 2 + 1; }
+    std::size_t specPoints() const { return static_cast<std::size_t>(n1) * specCols(); }
+    double h1() const { return kTwoPi / n1; }
+    double h2() const { return kTwoPi / n2; }
+    bool operator==(const GridDims& o) const { return n1 == o.n1 && n2 == o.n2; }
+    bool operator!=(const GridDims& o) const { return !(*this == o); }
+    bool operator<(const GridDims& o) const { return std::tie(n1, n2) < std::tie(o.n1, o.n2); }
+};
+
+// Grid::Grid validation (src/field.cpp:9-15).
+void checkGrid(int n1, int n2);
+
+// One context per (device, stream).  Not thread-safe across concurrent calls on the same
+// context: one host thread drives one context (one per GPU for batched pairs).
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool ownStream = false;
+    std::string err;
+    // Logical operation counters with the reference's semantics (src/counters.cpp): one FFT
+    // per forward/inverse 2-D transform of one scalar field, one interp per scattered
+    // evaluation of one scalar field.
+    long long ffts = 0, interps = 0;
+    int numSMs = 148;
+    std::size_t l2Bytes = 0;
+
+    struct PlanKey {
+        int n1, n2, type, batch;
+        bool operator<(const PlanKey& o) const {
+            return std::tie(n1, n2, type, batch) < std::tie(o.n1, o.n2, o.type, o.batch);
+        }
+    };
+    std::map<PlanKey, cufftHandle> plans;
+    // Scratch spectra / fields reused across calls (grown on demand, freed with the context).
+    std::map<std::pair<int, std::size_t>, DBuf> scratch;
+    DBuf reduce;  // reduction scratch (partials + results)
+    double* hostScalars = nullptr;  // pinned staging for scalar reads
+
+    // Kernel launches issued by this library (cuFFT's own kernels are not counted), and an
+    // optional per-tag CUDA-event profile of every launch site (bench.py roofline).
+    long long launches = 0;
+    bool profOn = false;
+    struct ProfRec {
+        const char* tag;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfRec> profRecs;
+    std::vector<cudaEvent_t> evPool;
+    std::size_t evNext = 0;
+    cudaEvent_t profEvent();
+
+    Ctx(int dev, cudaStream_t s);
+    ~Ctx();
+    cufftHandle plan(const GridDims& g, cufftType type, int batch);
+    double* scratchBuf(int slot, std::size_t bytes);
+    void sync();
+};
+
+// Marks one kernel launch of this library; records a CUDA event pair around it when the
+// context profile is on.  Construct immediately before the launch, destroy right after.
+struct LaunchScope {
+    Ctx& c;
+    const char* tag;
+    cudaEvent_t a = nullptr;
+    LaunchScope(Ctx& ctx, const char* t, bool mine = true) : c(ctx), tag(t) {
+        if (mine) ++c.launches;
+        if (c.profOn) {
+            a = c.profEvent();
+            cudaEventRecord(a, c.stream);
+        }
+    }
+    ~LaunchScope() {
+        if (a) {
+            cudaEvent_t b = c.profEvent();
+            cudaEventRecord(b, c.stream);
+            c.profRecs.push_back({tag, a, b});
+        }
+    }
+};
+
+inline dim3 grid1d(std::size_t n, int block) { return dim3(static_cast<unsigned>((n + block - 1) / block)); }
+
+}  // namespace vrg

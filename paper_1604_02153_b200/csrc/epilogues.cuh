@@ -1,0 +1,84 @@
+// Epilogues of the SL transport steps (shared by transport.cu and inverse.cu).
+#pragma once
+
+#include "eval.cuh"
+
+namespace vrg {
+
+// K3 epilogue: X_D = x - sgn*0.5*ht*(v + v(x*)), evaluated with the reference's operation
+// order and no FMA contraction (src/transport.cpp:84-85), so X_D is bit-identical.
+struct EpiTrace {
+    static constexpr const char* kName = "evaluate/trace";
+    static constexpr bool kGuard = false;
+    double* guardPartials = nullptr;
+    const double* v1;
+    const double* v2;
+    double* x1;
+    double* x2;
+    int n2;
+    double h1, h2, sgnHalfHt;
+    __device__ double operator()(std::size_t p, const double* vs) const {
+        const int i1 = static_cast<int>(p / n2), i2 = static_cast<int>(p - static_cast<std::size_t>(i1) * n2);
+        const double c1 = __dadd_rn(-kPi, __dmul_rn(h1, static_cast<double>(i1)));
+        const double c2 = __dadd_rn(-kPi, __dmul_rn(h2, static_cast<double>(i2)));
+        x1[p] = __dsub_rn(c1, __dmul_rn(sgnHalfHt, __dadd_rn(v1[p], vs[0])));
+        x2[p] = __dsub_rn(c2, __dmul_rn(sgnHalfHt, __dadd_rn(v2[p], vs[1])));
+        return 0.0;
+    }
+};
+
+// K4 epilogue: m_j = I[m_{j-1}](X_D) with the guard watching |m_j|.
+struct EpiStateStep {
+    static constexpr const char* kName = "evaluate/state_step";
+    static constexpr bool kGuard = true;
+    double* guardPartials;
+    double* out;
+    __device__ double operator()(std::size_t p, const double* v) const {
+        out[p] = v[0];
+        return v[0];
+    }
+};
+
+// K5 epilogue (slContinuityStep, src/transport.cpp:206-210).
+struct EpiContinuity {
+    static constexpr const char* kName = "evaluate/continuity";
+    static constexpr bool kGuard = true;
+    double* guardPartials;
+    const double* dvDep;
+    const double* dv;
+    double ht;
+    double* out;
+    __device__ double operator()(std::size_t p, const double* v) const {
+        const double uD = v[0];
+        const double f0 = uD * dvDep[p];
+        const double pred = uD + ht * f0;
+        const double o = uD + 0.5 * ht * (f0 + pred * dv[p]);
+        out[p] = o;
+        return o;
+    }
+};
+
+// K6 epilogue (solveIncState SL, src/transport.cpp:333-338).
+struct EpiIncState {
+    static constexpr const char* kName = "evaluate/incstate";
+    static constexpr bool kGuard = false;
+    double* guardPartials = nullptr;
+    const double* vt1D;
+    const double* vt2D;
+    const double* gd1;
+    const double* gd2;
+    const double* vt1;
+    const double* vt2;
+    const double* g1;
+    const double* g2;
+    double halfHt;
+    double* out;
+    __device__ double operator()(std::size_t p, const double* v) const {
+        const double sPrevD = -(vt1D[p] * gd1[p] + vt2D[p] * gd2[p]);
+        const double sCur = -(vt1[p] * g1[p] + vt2[p] * g2[p]);
+        out[p] = v[0] + halfHt * (sPrevD + sCur);
+        return 0.0;
+    }
+};
+
+}  // namespace vrg

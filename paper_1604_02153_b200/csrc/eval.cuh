@@ -1,0 +1,136 @@
+// K2: tensor-product cubic B-spline evaluation at one departure point per grid node, with a
+// fused per-node epilogue.  Restates interp::evaluate (src/interp.cpp:87-127): wrap, cell,
+// 4+4 weights, 16-tap periodic gather.  NF coefficient fields sharing one point set are
+// evaluated together so the weights and indices are computed once (e.g. both components of
+// a vector field, or the pair (grad m)_D).
+//
+// The epilogue functor receives (p, value[0..NF)) and returns the value the blow-up guard
+// watches (|.|, NaN ignored like std::max in normLinf, src/field.cpp:59-65); block maxima
+// go to guardPartials[blockIdx.x] when Epi::kGuard.
+#pragma once
+
+#include "interp.cuh"
+
+namespace vrg {
+
+constexpr int kEvalBlock = 256;
+
+template <int NF>
+struct CoeffSet {
+    const double* c[NF];
+};
+
+template <int NF, class Epi>
+__global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const double* __restrict__ x1,
+                                                         const double* __restrict__ x2, int n1, int n2, double h1,
+                                                         double h2, Epi epi) {
+    const std::size_t N = static_cast<std::size_t>(n1) * n2;
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double guard = 0.0;
+    if (p < N) {
+        int i1[4], i2[4];
+        double w1[4], w2[4];
+        cellOf(__ldg(x1 + p), h1, n1, i1, w1);
+        cellOf(__ldg(x2 + p), h2, n2, i2, w2);
+        double val[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const double* row = cs.c[f] + static_cast<std::size_t>(i1[a]) * n2;
+                double rowAcc = 0.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * __ldg(row + i2[b]);
+                acc += w1[a] * rowAcc;
+            }
+            val[f] = acc;
+        }
+        const double gv = fabs(epi(p, val));
+        if (gv == gv) guard = gv;  // NaN ignored, inf kept
+    }
+    if constexpr (Epi::kGuard) {
+        __shared__ double red[kEvalBlock / 32];
+        for (int o = 16; o > 0; o >>= 1) guard = fmax(guard, __shfl_xor_sync(0xffffffffu, guard, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = guard;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double m = red[0];
+            for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
+            epi.guardPartials[blockIdx.x] = m;
+        }
+    }
+}
+
+// Same block layout and guard reduction as k_evaluate, without the gather (values = 0):
+// used where the interpolated field is identically zero (m~_0 = 0) or for pure pointwise work.
+template <class Epi>
+__global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double guard = 0.0;
+    if (p < N) {
+        const double z[2] = {0.0, 0.0};
+        const double gv = fabs(epi(p, z));
+        if (gv == gv) guard = gv;
+    }
+    if constexpr (Epi::kGuard) {
+        __shared__ double red[kEvalBlock / 32];
+        for (int o = 16; o > 0; o >>= 1) guard = fmax(guard, __shfl_xor_sync(0xffffffffu, guard, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = guard;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double m = red[0];
+            for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
+            epi.guardPartials[blockIdx.x] = m;
+        }
+    }
+}
+
+template <class Epi>
+void launchPointwise(Ctx& ctx, const GridDims& g, const Epi& epi) {
+    {
+        LaunchScope ls_(ctx, Epi::kName);
+        k_pointwise<Epi><<<grid1d(g.points(), kEvalBlock), kEvalBlock, 0, ctx.stream>>>(g.points(), epi);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+template <int NF, class Epi>
+void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const double* x1, const double* x2, const Epi& epi) {
+    const std::size_t N = g.points();
+    {
+        LaunchScope ls_(ctx, Epi::kName);
+        k_evaluate<NF, Epi><<<grid1d(N, kEvalBlock), kEvalBlock, 0, ctx.stream>>>(cs, x1, x2, g.n1, g.n2, g.h1(),
+                                                                                   g.h2(), epi);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+inline unsigned evalBlocks(const GridDims& g) { return grid1d(g.points(), kEvalBlock).x; }
+
+// Plain stores.
+struct EpiStore1 {
+    static constexpr const char* kName = "evaluate/store1";
+    static constexpr bool kGuard = false;
+    double* guardPartials = nullptr;
+    double* out;
+    __device__ double operator()(std::size_t p, const double* v) const {
+        out[p] = v[0];
+        return 0.0;
+    }
+};
+
+struct EpiStore2 {
+    static constexpr const char* kName = "evaluate/store2";
+    static constexpr bool kGuard = false;
+    double* guardPartials = nullptr;
+    double* out0;
+    double* out1;
+    __device__ double operator()(std::size_t p, const double* v) const {
+        out0[p] = v[0];
+        out1[p] = v[1];
+        return 0.0;
+    }
+};
+
+}  // namespace vrg

@@ -1,0 +1,54 @@
+// Periodic cubic B-spline interpolation on sm_100a: prefilter (K1) and evaluation at departure
+// points with fused epilogues (K2).  Restates interp::prefilter / interp::evaluate
+// (src/interp.cpp:16-127) with a GPU-shaped algorithm; see DESIGN.md "K1/K2".
+#pragma once
+
+#include "common.cuh"
+
+namespace vrg {
+
+// Recursive-filter form of the periodic prefilter.  The exact inverse of circulant
+// [1/6, 2/3, 1/6] is c_k = sqrt(3) * sum_m z^|m| f_{k+m}, z = sqrt(3)-2; it splits into a
+// causal recurrence y+_k = f_k + z y+_{k-1} and an anticausal one y-_k = z (f_{k+1} + y-_{k+1}),
+// c = sqrt(3) (y+ + y-).  Each thread filters a chunk of kChunk outputs, starting both
+// recurrences kWarm samples outside the chunk (periodic wrap); the neglected tail is
+// 2.4 |z|^(kWarm+1) max|f| < 1e-16 max|f|.  The reference solves the same system exactly with
+// Thomas + Sherman-Morrison (src/interp.cpp:16-57); both agree to rounding.
+constexpr double kZ = -0.26794919243112270647;   // sqrt(3) - 2
+constexpr double kSqrt3 = 1.7320508075688772935;
+constexpr int kWarm = 28;
+constexpr int kChunk = 32;
+
+// Launches the two prefilter passes (rows of length n2, then columns of length n1) on
+// ctx.stream: c = P u.  `tmp` holds n1*n2 doubles.  If `nonfinite` is non-null, a non-finite
+// input value sets *nonfinite = 1 (checkFinite(u, "prefilter"), src/interp.cpp:76).
+void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite);
+
+// B-spline weights, src/interp.cpp:59-65.
+__device__ __forceinline__ void bsplineWeights(double f, double w[4]) {
+    const double f2 = f * f, f3 = f2 * f;
+    w[0] = (1.0 - 3.0 * f + 3.0 * f2 - f3) / 6.0;
+    w[1] = (3.0 * f3 - 6.0 * f2 + 4.0) / 6.0;
+    w[2] = (-3.0 * f3 + 3.0 * f2 + 3.0 * f + 1.0) / 6.0;
+    w[3] = f3 / 6.0;
+}
+
+// Cell index and fractional offset of a coordinate along one axis, src/interp.cpp:100-109.
+// The wrap x - 2 pi floor((x+pi)/2pi) uses round-to-nearest multiply/subtract (no FMA) so the
+// wrapped coordinate is bit-identical to the reference's.
+__device__ __forceinline__ void cellOf(double x, double h, int n, int idx[4], double w[4]) {
+    const double xw = __dsub_rn(x, __dmul_rn(kTwoPi, floor(__dadd_rn(x, kPi) / kTwoPi)));
+    const double s = __dadd_rn(xw, kPi) / h;
+    const double bf = floor(s);
+    bsplineWeights(s - bf, w);
+    int b = static_cast<int>(bf) - 1;
+    // b in [-1, n] for finite wrapped points; wrapIndex of src/interp.cpp:67-71
+    b = b < 0 ? b + n : (b >= n ? b - n : b);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        idx[t] = b;
+        b = (b + 1 == n) ? 0 : b + 1;
+    }
+}
+
+}  // namespace vrg

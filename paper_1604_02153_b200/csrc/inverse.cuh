@@ -1,0 +1,76 @@
+// Reduced-space operators on the device: inverse::HessianOperator (GN, SL) and the
+// gradient/objective evaluations (include/veloreg/inverse.hpp:60-97, src/inverse.cpp:96-233).
+#pragma once
+
+#include <memory>
+
+#include "transport.cuh"
+
+namespace vrg {
+
+enum Deformation : int { kCompressible = 0, kIncompressible = 1, kNearIncompressible = 2 };
+
+struct Model {
+    int norm = kH2;
+    double betaV = 1e-2;
+    int deformation = kCompressible;
+    double betaW = 1e-1;
+};
+
+// GN Hessian at one velocity iterate, everything device-resident.
+//
+// Per-iterate invariants are built once in the constructor and reused by every matvec
+// (they are pure functions of (v, m_T), so results are bit-identical to recomputing them as
+// the reference does per call, src/inverse.cpp:177-187):
+//   state m_j (j=0..nt), G_j = grad m_j, GD_j = (grad m_{j-1})_D at the forward departure
+//   points (j=1..nt), X_D in both directions, div v and (div v)_D backward.
+class Hessian {
+public:
+    // `stateTraj` (nullable): reuse a state trajectory (HessianOperator ctor, inverse.cpp:162-172).
+    Hessian(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR, const double* mT,
+            const Model& model, int nt, const double* stateTraj);
+
+    Ctx& ctx;
+    GridDims g;
+    Model model;
+    int nt;
+    Solver solver;
+    Weights weights;
+
+    // out = beta A vt + K[b(vt)]  (HessianOperator::apply, inverse.cpp:229-233)
+    void apply(const double* vt1, const double* vt2, double* o1, double* o2);
+    // out = K[b(vt)]  (applyDataTerm, inverse.cpp:235-237)
+    void applyDataTerm(const double* vt1, const double* vt2, double* o1, double* o2);
+    // out = M^{-1/2} Q M^{-1/2} s + s  (applySplitHessianOf, precond.cpp:20-26)
+    void applySplit(const double* s1, const double* s2, double* o1, double* o2);
+
+    const double* state() const { return state_.d(); }
+    // device-visible guard check result of the last data term (throws like solveAdjoint).
+    void checkLastGuard();
+    // counter increments of one data term in the reference (steady state)
+    void countDataTerm();
+
+private:
+    // b = sum_j w_j lt_j grad m_j of the GN incremental adjoint seeded with -m~(1).
+    // If regOut1/2 non-null, the last step also writes out = reg + b (compressible fusion).
+    void dataTerm(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
+                  const double* reg2, double* out1, double* out2);
+
+    DBuf state_;  // (nt+1) N
+    DBuf G_;      // (nt+1) x [g1 | g2]
+    DBuf GD_;     // nt x [gd1 | gd2], GD_[j-1] = (grad m_{j-1})_D
+    DBuf work_;   // vtD (2N), mt ping-pong (2N), lam ping-pong (2N), b (2N), coef2 (N), reg (2N)
+    DBuf spec_;   // 4 half spectra
+    GuardLog adjLog_;
+    long long lazyInterps_ = 0, lazyFfts_ = 0;
+};
+
+void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
+               double* b2);
+void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
+                       const double* mT, const Model& model, int nt, double* scalars, double* stateOut);
+void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
+                      const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
+                      double* stateOut, double* adjOut, const double* reuseState);
+
+}  // namespace vrg

@@ -1,0 +1,345 @@
+// Context, errors, cuFFT plan cache and BLAS-1 / reduction kernels (K9).
+// BLAS-1 restates src/field.cpp:19-119: dot = h1*h2*sum(u*w) per component, normLinf = max|x|
+// with NaN ignored (std::max semantics), axpy/scale.  Reductions are two-stage with a fixed
+// block count and a fixed-order final pass, so results are run-to-run deterministic.
+#include <cstdio>
+#include <cstring>
+
+#include "blas.cuh"
+
+namespace vrg {
+
+void throwCuda(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+                  file, line, what);
+    throw std::runtime_error(buf);
+}
+
+void throwCufft(cufftResult r, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "cuFFT error %d at %s:%d: %s", static_cast<int>(r), file, line, what);
+    throw std::runtime_error(buf);
+}
+
+void checkGrid(int n1, int n2) {
+    if (n1 < 4 || n1 % 2 != 0 || n2 < 4 || n2 % 2 != 0)
+        throw InvalidArgument("Grid: axis sizes must be even and >= 4");
+}
+
+Ctx::Ctx(int dev, cudaStream_t s) : device(dev) {
+    VRG_CUDA(cudaSetDevice(dev));
+    VRG_CUDA(cudaFree(nullptr));
+    if (s) {
+        stream = s;
+    } else {
+        VRG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        ownStream = true;
+    }
+    VRG_CUDA(cudaDeviceGetAttribute(&numSMs, cudaDevAttrMultiProcessorCount, dev));
+    int l2 = 0;
+    VRG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    l2Bytes = static_cast<std::size_t>(l2);
+    reduce.alloc(sizeof(double) * (kReduceBlocks * 4 + 64));
+    VRG_CUDA(cudaMallocHost(&hostScalars, sizeof(double) * 64));
+}
+
+Ctx::~Ctx() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& kv : plans) cufftDestroy(kv.second);
+    for (cudaEvent_t e : evPool) cudaEventDestroy(e);
+    plans.clear();
+    scratch.clear();
+    reduce.release();
+    if (hostScalars) cudaFreeHost(hostScalars);
+    if (ownStream && stream) cudaStreamDestroy(stream);
+}
+
+cufftHandle Ctx::plan(const GridDims& g, cufftType type, int batch) {
+    PlanKey key{g.n1, g.n2, static_cast<int>(type), batch};
+    auto it = plans.find(key);
+    if (it != plans.end()) return it->second;
+    cufftHandle h;
+    int n[2] = {g.n1, g.n2};
+    VRG_CUFFT(cufftCreate(&h));
+    std::size_t work = 0;
+    if (type == CUFFT_D2Z) {
+        VRG_CUFFT(cufftMakePlanMany(h, 2, n, nullptr, 1, static_cast<int>(g.points()), nullptr, 1,
+                                    static_cast<int>(g.specPoints()), CUFFT_D2Z, batch, &work));
+    } else {
+        VRG_CUFFT(cufftMakePlanMany(h, 2, n, nullptr, 1, static_cast<int>(g.specPoints()), nullptr, 1,
+                                    static_cast<int>(g.points()), CUFFT_Z2D, batch, &work));
+    }
+    VRG_CUFFT(cufftSetStream(h, stream));
+    plans[key] = h;
+    return h;
+}
+
+double* Ctx::scratchBuf(int slot, std::size_t bytes) {
+    auto key = std::make_pair(slot, bytes);
+    auto it = scratch.find(key);
+    if (it != scratch.end()) return it->second.d();
+    DBuf b(bytes);
+    double* p = b.d();
+    scratch.emplace(key, std::move(b));
+    return p;
+}
+
+void Ctx::sync() { VRG_CUDA(cudaStreamSynchronize(stream)); }
+
+cudaEvent_t Ctx::profEvent() {
+    if (evNext == evPool.size()) {
+        cudaEvent_t e;
+        VRG_CUDA(cudaEventCreate(&e));
+        evPool.push_back(e);
+    }
+    return evPool[evNext++];
+}
+
+// ------------------------------------------------------------------------------ kernels
+namespace {
+
+__device__ __forceinline__ double warpSum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warpMax(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Stage 1: per-block partial sums of sum_i a_i*b_i for up to two (a,b) pairs (kept separate).
+__global__ void __launch_bounds__(kReduceThreads) k_dot_partial(const double* __restrict__ a0,
+                                                                const double* __restrict__ b0,
+                                                                const double* __restrict__ a1,
+                                                                const double* __restrict__ b1, std::size_t n,
+                                                                double* partial) {
+    double s0 = 0.0, s1 = 0.0;
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        s0 += a0[i] * b0[i];
+        if (a1) s1 += a1[i] * b1[i];
+    }
+    __shared__ double r0[kReduceThreads / 32], r1[kReduceThreads / 32];
+    s0 = warpSum(s0);
+    s1 = warpSum(s1);
+    if ((threadIdx.x & 31) == 0) {
+        r0[threadIdx.x >> 5] = s0;
+        r1[threadIdx.x >> 5] = s1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < kReduceThreads / 32; ++w) {
+            t0 += r0[w];
+            t1 += r1[w];
+        }
+        partial[blockIdx.x] = t0;
+        partial[kReduceBlocks + blockIdx.x] = t1;
+    }
+}
+
+// Stage 2: out = scale*(sum partial0) + scale*(sum partial1)  (dot per component, then added,
+// field.cpp:47-54).
+__global__ void k_dot_final(const double* partial, int nb, double scale, double* out) {
+    __shared__ double r0[32], r1[32];
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        s0 += partial[i];
+        s1 += partial[kReduceBlocks + i];
+    }
+    s0 = warpSum(s0);
+    s1 = warpSum(s1);
+    if ((threadIdx.x & 31) == 0) {
+        r0[threadIdx.x >> 5] = s0;
+        r1[threadIdx.x >> 5] = s1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
+            t0 += r0[w];
+            t1 += r1[w];
+        }
+        *out = scale * t0 + scale * t1;
+    }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial(const double* __restrict__ a0,
+                                                                   const double* __restrict__ a1, std::size_t n,
+                                                                   double* partial) {
+    double m = 0.0;
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        m = fmax(m, fabs(a0[i]));  // fmax drops NaN like std::max(m, NaN) == m
+        if (a1) m = fmax(m, fabs(a1[i]));
+    }
+    __shared__ double r[kReduceThreads / 32];
+    m = warpMax(m);
+    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kReduceThreads / 32; ++w) t = fmax(t, r[w]);
+        partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_max_final(const double* partial, int nb, double scale, double* out) {
+    __shared__ double r[32];
+    double m = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) m = fmax(m, partial[i]);
+    m = warpMax(m);
+    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t = fmax(t, r[w]);
+        *out = scale * t;
+    }
+}
+
+__global__ void k_nonfinite(const double* __restrict__ a, std::size_t n, unsigned* flag) {
+    bool bad = false;
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        bad |= !isfinite(a[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+__global__ void k_axpby(std::size_t n, double a, const double* __restrict__ x, double b, double* y) {
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = b == 1.0 ? y[i] + a * x[i] : (b == 0.0 ? a * x[i] : b * y[i] + a * x[i]);
+}
+
+__global__ void k_lincomb(std::size_t n, double a, const double* __restrict__ x, double b,
+                          const double* __restrict__ y, double* out) {
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = a * x[i] + b * y[i];
+}
+
+__global__ void k_fill(std::size_t n, double v, double* y) {
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = v;
+}
+
+unsigned elemBlocks(const Ctx& ctx, std::size_t n) {
+    const std::size_t want = (n + 255) / 256;
+    const std::size_t cap = static_cast<std::size_t>(ctx.numSMs) * 8;
+    return static_cast<unsigned>(std::max<std::size_t>(1, std::min(want, cap)));
+}
+
+}  // namespace
+
+double* launchDot(Ctx& ctx, std::size_t n, const double* a0, const double* b0, const double* a1, const double* b1,
+                  double scale, int slot) {
+    double* partial = ctx.reduce.d();
+    double* out = partial + 2 * kReduceBlocks + slot;
+    const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
+    {
+        LaunchScope ls_(ctx, "k_dot_partial");
+        k_dot_partial<<<nb, kReduceThreads, 0, ctx.stream>>>(a0, b0, a1, b1, n, partial);
+    }
+    VRG_LAUNCH_CHECK();
+    {
+        LaunchScope ls_(ctx, "k_dot_final");
+        k_dot_final<<<1, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
+    }
+    VRG_LAUNCH_CHECK();
+    return out;
+}
+
+double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1, double scale, int slot) {
+    double* partial = ctx.reduce.d();
+    double* out = partial + 2 * kReduceBlocks + slot;
+    const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
+    {
+        LaunchScope ls_(ctx, "k_maxabs_partial");
+        k_maxabs_partial<<<nb, kReduceThreads, 0, ctx.stream>>>(a0, a1, n, partial);
+    }
+    VRG_LAUNCH_CHECK();
+    {
+        LaunchScope ls_(ctx, "k_max_final");
+        k_max_final<<<1, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
+    }
+    VRG_LAUNCH_CHECK();
+    return out;
+}
+
+void launchMaxFinal(Ctx& ctx, const double* partials, int nb, double scale, double* out) {
+    {
+        LaunchScope ls_(ctx, "k_max_final");
+        k_max_final<<<1, 1024, 0, ctx.stream>>>(partials, nb, scale, out);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+double readScalar(Ctx& ctx, const double* dev) {
+    VRG_CUDA(cudaMemcpyAsync(ctx.hostScalars, dev, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    return ctx.hostScalars[0];
+}
+
+double dot(Ctx& ctx, const GridDims& g, const double* a0, const double* a1, const double* b0, const double* b1) {
+    return readScalar(ctx, launchDot(ctx, g.points(), a0, b0, a1, b1, g.h1() * g.h2(), 0));
+}
+
+double normLinf(Ctx& ctx, std::size_t n, const double* a0, const double* a1) {
+    return readScalar(ctx, launchMaxAbs(ctx, n, a0, a1, 1.0, 0));
+}
+
+bool anyNonFinite(Ctx& ctx, std::size_t n, const double* a0, const double* a1) {
+    unsigned* flag = reinterpret_cast<unsigned*>(ctx.reduce.d() + 2 * kReduceBlocks + 60);
+    VRG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), ctx.stream));
+    {
+        LaunchScope ls_(ctx, "k_nonfinite");
+        k_nonfinite<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(a0, n, flag);
+    }
+    VRG_LAUNCH_CHECK();
+    if (a1) {
+        {
+            LaunchScope ls_(ctx, "k_nonfinite");
+            k_nonfinite<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(a1, n, flag);
+        }
+        VRG_LAUNCH_CHECK();
+    }
+    unsigned h = 0;
+    VRG_CUDA(cudaMemcpyAsync(ctx.hostScalars, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    std::memcpy(&h, ctx.hostScalars, sizeof(unsigned));
+    return h != 0;
+}
+
+void axpby(Ctx& ctx, std::size_t n, double a, const double* x, double b, double* y) {
+    {
+        LaunchScope ls_(ctx, "k_axpby");
+        k_axpby<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, a, x, b, y);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void lincomb(Ctx& ctx, std::size_t n, double a, const double* x, double b, const double* y, double* out) {
+    {
+        LaunchScope ls_(ctx, "k_lincomb");
+        k_lincomb<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, a, x, b, y, out);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void fill(Ctx& ctx, std::size_t n, double v, double* y) {
+    {
+        LaunchScope ls_(ctx, "k_fill");
+        k_fill<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, v, y);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void copy(Ctx& ctx, std::size_t n, const double* src, double* dst) {
+    if (src != dst) VRG_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
+}  // namespace vrg

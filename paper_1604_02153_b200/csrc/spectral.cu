@@ -1,0 +1,344 @@
+// K7 implementation: cuFFT plans from the context cache + symbol kernels.
+#include <cmath>
+
+#include "spectral.cuh"
+
+namespace vrg {
+
+namespace {
+
+constexpr int kSpecBlock = 256;
+
+__device__ __forceinline__ int waveOf(int idx, int n) { return idx <= n / 2 ? idx : idx - n; }  // fft.cpp:80
+__device__ __forceinline__ double waveNyq0(int idx, int n) {                                     // spectral.cpp:31-33
+    return idx == n / 2 ? 0.0 : static_cast<double>(waveOf(idx, n));
+}
+
+__device__ __forceinline__ cplx cmulI(double k, cplx v) { return make_double2(-k * v.y, k * v.x); }  // (i k) * v
+__device__ __forceinline__ cplx cscale(cplx v, double a) { return make_double2(v.x * a, v.y * a); }
+
+__global__ void k_grad(const cplx* __restrict__ s, cplx* __restrict__ o1, cplx* __restrict__ o2, int n1, int n2,
+                       double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const cplx v = s[i];
+    o1[i] = cscale(cmulI(waveNyq0(r, n1), v), scale);
+    o2[i] = cscale(cmulI(waveNyq0(c, n2), v), scale);
+}
+
+__global__ void k_div(const cplx* __restrict__ s1, const cplx* __restrict__ s2, cplx* __restrict__ o, int n1, int n2,
+                      double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const cplx a = cmulI(waveNyq0(r, n1), s1[i]);
+    const cplx b = cmulI(waveNyq0(c, n2), s2[i]);
+    o[i] = cscale(make_double2(a.x + b.x, a.y + b.y), scale);
+}
+
+__global__ void k_scale(cplx* s, std::size_t n, int nf, const double* __restrict__ sym, double scale) {
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double m = sym ? sym[i] * scale : scale;
+    for (int f = 0; f < nf; ++f) s[f * n + i] = cscale(s[f * n + i], m);
+}
+
+__device__ __forceinline__ void leray(int r, int c, int n1, int n2, cplx& s1, cplx& s2) {
+    const double k1 = waveNyq0(r, n1), k2 = waveNyq0(c, n2);
+    const double ksq = k1 * k1 + k2 * k2;
+    if (ksq == 0.0) return;  // mean and pure-Nyquist modes pass through
+    const cplx kdotb = make_double2(k1 * s1.x + k2 * s2.x, k1 * s1.y + k2 * s2.y);
+    s1 = make_double2(s1.x - k1 * kdotb.x / ksq, s1.y - k1 * kdotb.y / ksq);
+    s2 = make_double2(s2.x - k2 * kdotb.x / ksq, s2.y - k2 * kdotb.y / ksq);
+}
+
+__global__ void k_leray(cplx* s1, cplx* s2, int n1, int n2) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    cplx a = s1[i], b = s2[i];
+    leray(r, c, n1, n2, a, b);
+    s1[i] = a;
+    s2[i] = b;
+}
+
+__global__ void k_combine(const cplx* __restrict__ b1, const cplx* __restrict__ b2, const cplx* __restrict__ a1,
+                          const cplx* __restrict__ a2, const double* __restrict__ sym, bool doLeray, double scale,
+                          cplx* o1, cplx* o2, int n1, int n2) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    cplx x = b1[i], y = b2[i];
+    if (doLeray) {
+        const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+        leray(r, c, n1, n2, x, y);
+    }
+    if (sym) {
+        const double m = sym[i];
+        x = cscale(x, m);
+        y = cscale(y, m);
+    }
+    if (a1) {
+        x = make_double2(x.x + a1[i].x, x.y + a1[i].y);
+        y = make_double2(y.x + a2[i].x, y.y + a2[i].y);
+    }
+    o1[i] = cscale(x, scale);
+    o2[i] = cscale(y, scale);
+}
+
+// spectral::resample (src/spectral.cpp:157-179) from source spectrum to target spectrum.
+__global__ void k_resample(const cplx* __restrict__ s, int sn1, int sn2, cplx* __restrict__ t, int tn1, int tn2,
+                           double amp, double scale) {
+    const int tc = tn2 / 2 + 1, sc = sn2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(tn1) * tc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int rt = static_cast<int>(i / tc), c = static_cast<int>(i - static_cast<std::size_t>(rt) * tc);
+    const int band1 = min(sn1, tn1) / 2, band2 = min(sn2, tn2) / 2;
+    const int k1 = waveOf(rt, tn1), k2 = waveOf(c, tn2);
+    cplx v = make_double2(0.0, 0.0);
+    if (abs(k1) < band1 && abs(k2) < band2) {
+        const int rs = k1 >= 0 ? k1 : k1 + sn1;
+        v = cscale(s[static_cast<std::size_t>(rs) * sc + c], amp);
+    }
+    t[i] = cscale(v, scale);
+}
+
+// spectral::cutoffFilter (src/spectral.cpp:188-203): both bands from one spectrum.
+__global__ void k_cutoff(const cplx* __restrict__ s, cplx* lo, cplx* hi, int n1, int n2, double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const bool low = abs(waveOf(r, n1)) < n1 / 4 && abs(waveOf(c, n2)) < n2 / 4;
+    const cplx v = cscale(s[i], scale);
+    const cplx z = make_double2(0.0, 0.0);
+    if (lo) lo[i] = low ? v : z;
+    if (hi) hi[i] = low ? z : v;
+}
+
+__global__ void k_gauss(cplx* s, int n1, int n2, double s1, double s2, double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const double k1 = waveOf(r, n1), k2 = waveOf(c, n2);
+    s[i] = cscale(s[i], exp(-0.5 * (k1 * k1 * s1 * s1 + k2 * k2 * s2 * s2)) * scale);
+}
+
+inline dim3 specGrid(const GridDims& g) { return grid1d(g.specPoints(), kSpecBlock); }
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ weights
+Weights::Weights(const GridDims& gd, int nrm) : g(gd), norm(nrm) {
+    const int nc = g.specCols();
+    gammaHost.resize(g.specPoints());
+    gammaRegHost.resize(g.specPoints());
+    const int order = nrm == kH1 ? 1 : nrm == kH3 ? 3 : 2;
+    for (int r = 0; r < g.n1; ++r) {
+        const double k1 = r <= g.n1 / 2 ? r : r - g.n1;
+        for (int c = 0; c < nc; ++c) {
+            const double k2 = c <= g.n2 / 2 ? c : c - g.n2;
+            const double ksq = k1 * k1 + k2 * k2;
+            double val = 1.0;
+            for (int p = 0; p < order; ++p) val *= ksq;
+            gammaHost[static_cast<std::size_t>(r) * nc + c] = val;
+            gammaRegHost[static_cast<std::size_t>(r) * nc + c] = val == 0.0 ? 1.0 : val;
+        }
+    }
+}
+
+const double* Weights::regSymbol(double beta) {
+    auto it = regSymbols.find(beta);
+    if (it != regSymbols.end()) return it->second.d();
+    std::vector<double> h(gammaHost.size());
+    for (std::size_t i = 0; i < h.size(); ++i) h[i] = beta * gammaHost[i];
+    DBuf b(sizeof(double) * h.size());
+    VRG_CUDA(cudaMemcpy(b.d(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    const double* p = b.d();
+    regSymbols.emplace(beta, std::move(b));
+    return p;
+}
+
+const double* Weights::invRegSymbol(double beta, double power) {
+    auto key = std::make_pair(beta, power);
+    auto it = symbols.find(key);
+    if (it != symbols.end()) return it->second.d();
+    std::vector<double> h(gammaRegHost.size());
+    for (std::size_t i = 0; i < h.size(); ++i) h[i] = std::pow(beta * gammaRegHost[i], power);
+    DBuf b(sizeof(double) * h.size());
+    VRG_CUDA(cudaMemcpy(b.d(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    const double* p = b.d();
+    symbols.emplace(key, std::move(b));
+    return p;
+}
+
+// ------------------------------------------------------------------------------ FFT
+cplx* specScratch(Ctx& ctx, const GridDims& g, int slot, int count) {
+    return reinterpret_cast<cplx*>(ctx.scratchBuf(1000 + slot, sizeof(cplx) * g.specPoints() * count));
+}
+
+void fftForward(Ctx& ctx, const GridDims& g, const double* u, cplx* s, int batch) {
+    cufftHandle p = ctx.plan(g, CUFFT_D2Z, batch);
+    LaunchScope ls_(ctx, "cufft_d2z", false);
+    VRG_CUFFT(cufftExecD2Z(p, const_cast<double*>(u), reinterpret_cast<cufftDoubleComplex*>(s)));
+}
+
+void fftInverse(Ctx& ctx, const GridDims& g, cplx* s, double* u, int batch) {
+    cufftHandle p = ctx.plan(g, CUFFT_Z2D, batch);
+    LaunchScope ls_(ctx, "cufft_z2d", false);
+    VRG_CUFFT(cufftExecZ2D(p, reinterpret_cast<cufftDoubleComplex*>(s), u));
+}
+
+// Forward transform of a vector field (batched when the components are contiguous).
+static void fftForward2(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, cplx* s) {
+    if (v2 == v1 + g.points()) {
+        fftForward(ctx, g, v1, s, 2);
+    } else {
+        fftForward(ctx, g, v1, s, 1);
+        fftForward(ctx, g, v2, s + g.specPoints(), 1);
+    }
+}
+
+static void fftInverse2(Ctx& ctx, const GridDims& g, cplx* s, double* o1, double* o2) {
+    if (o2 == o1 + g.points()) {
+        fftInverse(ctx, g, s, o1, 2);
+    } else {
+        fftInverse(ctx, g, s, o1, 1);
+        fftInverse(ctx, g, s + g.specPoints(), o2, 1);
+    }
+}
+
+// ------------------------------------------------------------------------------ operators
+void gradient(Ctx& ctx, const GridDims& g, const double* u, double* g1, double* g2) {
+    cplx* s = specScratch(ctx, g, 0, 1);
+    cplx* o = specScratch(ctx, g, 1, 2);
+    fftForward(ctx, g, u, s, 1);
+    {
+        LaunchScope ls_(ctx, "k_grad");
+        k_grad<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, o, o + g.specPoints(), g.n1, g.n2, 1.0 / g.points());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse2(ctx, g, o, g1, g2);
+    ctx.ffts += 3;
+}
+
+void divergence(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double* out) {
+    cplx* s = specScratch(ctx, g, 1, 2);
+    cplx* o = specScratch(ctx, g, 0, 1);
+    fftForward2(ctx, g, v1, v2, s);
+    {
+        LaunchScope ls_(ctx, "k_div");
+        k_div<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, s + g.specPoints(), o, g.n1, g.n2, 1.0 / g.points());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, g, o, out, 1);
+    ctx.ffts += 3;
+}
+
+void applyRealSymbol(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double* o1, double* o2,
+                     const double* sym) {
+    cplx* s = specScratch(ctx, g, 1, 2);
+    fftForward2(ctx, g, v1, v2, s);
+    specScale(ctx, g, s, 2, sym, 1.0 / g.points());
+    fftInverse2(ctx, g, s, o1, o2);
+    ctx.ffts += 4;
+}
+
+void projectDivFree(Ctx& ctx, const GridDims& g, const double* b1, const double* b2, double* o1, double* o2) {
+    cplx* s = specScratch(ctx, g, 1, 2);
+    fftForward2(ctx, g, b1, b2, s);
+    {
+        LaunchScope ls_(ctx, "k_leray");
+        k_leray<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, s + g.specPoints(), g.n1, g.n2);
+    }
+    VRG_LAUNCH_CHECK();
+    specScale(ctx, g, s, 2, nullptr, 1.0 / g.points());
+    fftInverse2(ctx, g, s, o1, o2);
+    ctx.ffts += 4;
+}
+
+void resample(Ctx& ctx, const GridDims& src, const double* u, const GridDims& dst, double* out) {
+    if (src == dst) {
+        if (out != u) VRG_CUDA(cudaMemcpyAsync(out, u, sizeof(double) * src.points(), cudaMemcpyDeviceToDevice, ctx.stream));
+        return;
+    }
+    cplx* s = specScratch(ctx, src, 2, 1);
+    cplx* t = specScratch(ctx, dst, 3, 1);
+    fftForward(ctx, src, u, s, 1);
+    const double amp = static_cast<double>(dst.points()) / static_cast<double>(src.points());
+    {
+        LaunchScope ls_(ctx, "k_resample");
+        k_resample<<<specGrid(dst), kSpecBlock, 0, ctx.stream>>>(s, src.n1, src.n2, t, dst.n1, dst.n2, amp,
+                                                                 1.0 / dst.points());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, dst, t, out, 1);
+    ctx.ffts += 2;
+}
+
+void cutoff(Ctx& ctx, const GridDims& g, const double* u, double* low, double* high) {
+    cplx* s = specScratch(ctx, g, 0, 1);
+    cplx* o = specScratch(ctx, g, 1, 2);
+    fftForward(ctx, g, u, s, 1);
+    {
+        LaunchScope ls_(ctx, "k_cutoff");
+        k_cutoff<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, low ? o : nullptr, high ? o + g.specPoints() : nullptr,
+                                                             g.n1, g.n2, 1.0 / g.points());
+    }
+    VRG_LAUNCH_CHECK();
+    if (low) fftInverse(ctx, g, o, low, 1);
+    if (high) fftInverse(ctx, g, o + g.specPoints(), high, 1);
+    ctx.ffts += (low ? 2 : 0) + (high ? 2 : 0);
+}
+
+void gaussianSmooth(Ctx& ctx, const GridDims& g, const double* u, double sigma, double* out) {
+    cplx* s = specScratch(ctx, g, 0, 1);
+    fftForward(ctx, g, u, s, 1);
+    {
+        LaunchScope ls_(ctx, "k_gauss");
+        k_gauss<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.n1, g.n2, sigma * g.h1(), sigma * g.h2(),
+                                                            1.0 / g.points());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, g, s, out, 1);
+    ctx.ffts += 2;
+}
+
+void specScale(Ctx& ctx, const GridDims& g, cplx* s, int nf, const double* sym, double scale) {
+    {
+        LaunchScope ls_(ctx, "k_scale");
+        k_scale<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.specPoints(), nf, sym, scale);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void specLeray(Ctx& ctx, const GridDims& g, cplx* s1, cplx* s2) {
+    {
+        LaunchScope ls_(ctx, "k_leray");
+        k_leray<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s1, s2, g.n1, g.n2);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void specCombine(Ctx& ctx, const GridDims& g, const cplx* b1, const cplx* b2, const cplx* a1, const cplx* a2,
+                 const double* sym, bool doLeray, double scale, cplx* o1, cplx* o2) {
+    {
+        LaunchScope ls_(ctx, "k_combine");
+        k_combine<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(b1, b2, a1, a2, sym, doLeray, scale, o1, o2, g.n1, g.n2);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+}  // namespace vrg

@@ -1,0 +1,314 @@
+// Semi-Lagrangian transport kernels (K3 trace, K4 state step, K5 continuity step, K6
+// incremental-state step) and the device transport::Solver.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "epilogues.cuh"
+#include "transport.cuh"
+
+namespace vrg {
+
+// ------------------------------------------------------------------------------ epilogues
+namespace {
+
+// Star points x* = x - sgn*ht*v (src/transport.cpp:73-74), no FMA.
+__global__ void k_star(const double* __restrict__ v1, const double* __restrict__ v2, int n1, int n2, double h1,
+                       double h2, double sgnHt, double* x1, double* x2) {
+    const std::size_t N = static_cast<std::size_t>(n1) * n2;
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const int i1 = static_cast<int>(p / n2), i2 = static_cast<int>(p - static_cast<std::size_t>(i1) * n2);
+    const double c1 = __dadd_rn(-kPi, __dmul_rn(h1, static_cast<double>(i1)));
+    const double c2 = __dadd_rn(-kPi, __dmul_rn(h2, static_cast<double>(i2)));
+    x1[p] = __dsub_rn(c1, __dmul_rn(sgnHt, v1[p]));
+    x2[p] = __dsub_rn(c2, __dmul_rn(sgnHt, v2[p]));
+}
+
+// Block maxima of |field| into guard partials (same block layout as k_evaluate).
+__global__ void __launch_bounds__(kEvalBlock) k_fieldmax(const double* __restrict__ f, std::size_t N, double* partial) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double g = 0.0;
+    if (p < N) g = fmax(0.0, fabs(f[p]));
+    __shared__ double red[kEvalBlock / 32];
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = g;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = red[0];
+        for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
+        partial[blockIdx.x] = m;
+    }
+}
+
+__global__ void k_stepmax(const double* partials, unsigned blocks, double* out) {
+    const double* p = partials + static_cast<std::size_t>(blockIdx.x) * blocks;
+    double m = 0.0;
+    for (unsigned i = threadIdx.x; i < blocks; i += blockDim.x) m = fmax(m, p[i]);
+    __shared__ double red[32];
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t = fmax(t, red[w]);
+        out[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_ones(std::size_t N, double* y) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < N) y[p] = 1.0;
+}
+
+}  // namespace
+
+void launchFieldMax(Ctx& ctx, const GridDims& g, const double* f, double* partial) {
+    {
+        LaunchScope ls_(ctx, "k_fieldmax");
+        k_fieldmax<<<evalBlocks(g), kEvalBlock, 0, ctx.stream>>>(f, g.points(), partial);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------------------ guard log
+void GuardLog::ensure(int nsteps, unsigned nblocks) {
+    if (nsteps <= steps && nblocks == blocks) return;
+    steps = nsteps;
+    blocks = nblocks;
+    partials.alloc(sizeof(double) * static_cast<std::size_t>(steps) * blocks);
+    stepMax.alloc(sizeof(double) * steps);
+    flags.alloc(sizeof(unsigned) * steps);
+}
+
+void GuardLog::reset(Ctx& ctx) { VRG_CUDA(cudaMemsetAsync(flags.d(), 0, sizeof(unsigned) * steps, ctx.stream)); }
+
+void GuardLog::finalize(Ctx& ctx) {
+    {
+        LaunchScope ls_(ctx, "k_stepmax");
+        k_stepmax<<<steps, 256, 0, ctx.stream>>>(partials.d(), blocks, stepMax.d());
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep) {
+    std::vector<double> mx(nt + 1);
+    std::vector<unsigned> fl(nt + 1);
+    VRG_CUDA(cudaMemcpyAsync(mx.data(), stepMax.d(), sizeof(double) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
+    VRG_CUDA(cudaMemcpyAsync(fl.data(), flags.d(), sizeof(unsigned) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const double threshold = kBlowupFactor * mx[thresholdStep];
+    for (int s = 1; s <= nt; ++s) {
+        const int j = forward ? s : nt + 1 - s;    // step label (transport.cpp:221, 235)
+        const int in = forward ? j - 1 : j;         // frame fed to the prefilter
+        const int out = forward ? j : j - 1;        // frame produced
+        if (fl[in]) throw InvalidArgument("prefilter: non-finite value");
+        if (guard && mx[out] > threshold)
+            throw BlowupError(std::string(eq) + " solve exceeded the blow-up guard at step " + std::to_string(j));
+    }
+}
+
+// ------------------------------------------------------------------------------ helpers
+int deriveSteps(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double cfl) {
+    if (!(cfl > 0.0) || cfl > 20.0) throw InvalidArgument("cfl must lie in (0, 20]");
+    const double m1 = normLinf(ctx, g.points(), v1);
+    const double m2 = normLinf(ctx, g.points(), v2);
+    double ratio = 0.0;
+    ratio = std::max(ratio, m1 / (cfl * g.h1()));
+    ratio = std::max(ratio, m2 / (cfl * g.h2()));
+    const int nt = static_cast<int>(std::ceil(ratio));
+    return std::max(2, nt);
+}
+
+void launchTrace(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* cv1,
+                 const double* cv2, double ht, int dir, double* x1, double* x2) {
+    const double sgn = dir == kForward ? 1.0 : -1.0;
+    // star points staged in the output buffers, then overwritten by the departure points
+    // (each thread reads its own star point before writing its departure point)
+    double* s1 = ctx.scratchBuf(10, sizeof(double) * g.points());
+    double* s2 = ctx.scratchBuf(11, sizeof(double) * g.points());
+    {
+        LaunchScope ls_(ctx, "k_star");
+        k_star<<<grid1d(g.points(), 256), 256, 0, ctx.stream>>>(v1, v2, g.n1, g.n2, g.h1(), g.h2(), sgn * ht, s1, s2);
+    }
+    VRG_LAUNCH_CHECK();
+    EpiTrace epi{nullptr, v1, v2, x1, x2, g.n2, g.h1(), g.h2(), sgn * 0.5 * ht};
+    launchEvaluate<2>(ctx, g, CoeffSet<2>{{cv1, cv2}}, s1, s2, epi);
+}
+
+// ------------------------------------------------------------------------------ Solver
+Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2, int steps)
+    : ctx(c), g(gd), nt(steps), ht(1.0 / steps) {
+    checkGrid(g.n1, g.n2);
+    if (steps < 1) throw InvalidArgument("TimeGrid: nt must be >= 1");
+    v.alloc(sizeof(double) * 2 * g.points());
+    copy(ctx, g.points(), vv1, v.d());
+    copy(ctx, g.points(), vv2, v.d() + g.points());
+    if (anyNonFinite(ctx, 2 * g.points(), v.d())) throw InvalidArgument("transport velocity: non-finite value");
+    coef_.alloc(sizeof(double) * g.points());
+    tmp_.alloc(sizeof(double) * g.points());
+    log.ensure(nt + 1, evalBlocks(g));
+}
+
+double* Solver::coef() { return coef_.d(); }
+double* Solver::tmp() { return tmp_.d(); }
+
+const double* Solver::departure(int dir) {
+    if (!haveX_[dir]) {
+        if (!haveCv_) {
+            cv_.alloc(sizeof(double) * 2 * g.points());
+            launchPrefilter(ctx, g, v1(), cv_.d(), tmp_.d(), nullptr);
+            launchPrefilter(ctx, g, v2(), cv_.d() + g.points(), tmp_.d(), nullptr);
+            haveCv_ = true;
+        }
+        X_[dir].alloc(sizeof(double) * 2 * g.points());
+        launchTrace(ctx, g, v1(), v2(), cv_.d(), cv_.d() + g.points(), ht, dir, X_[dir].d(), X_[dir].d() + g.points());
+        ctx.interps += 2;  // traceCharacteristics evaluates both components (transport.cpp:77-78)
+        haveX_[dir] = true;
+    }
+    return X_[dir].d();
+}
+
+const double* Solver::divVelocity() {
+    if (!haveDivv_) {
+        divv_.alloc(sizeof(double) * g.points());
+        divergence(ctx, g, v1(), v2(), divv_.d());  // counts 3 FFTs
+        haveDivv_ = true;
+    }
+    return divv_.d();
+}
+
+const double* Solver::divVelocityAtDeparture(int dir) {
+    if (!haveDvDep_[dir]) {
+        const double* dv = divVelocity();
+        const double* X = departure(dir);
+        dvDep_[dir].alloc(sizeof(double) * g.points());
+        launchPrefilter(ctx, g, dv, coef_.d(), tmp_.d(), nullptr);
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + g.points(), EpiStore1{nullptr, dvDep_[dir].d()});
+        ctx.interps += 1;
+        haveDvDep_[dir] = true;
+    }
+    return dvDep_[dir].d();
+}
+
+void Solver::continuityStep(const double* u, double* out, int dir, double* guardPartial, unsigned* flag) {
+    const double* X = departure(dir);
+    const double* dv = divVelocity();
+    const double* dvd = divVelocityAtDeparture(dir);
+    launchPrefilter(ctx, g, u, coef_.d(), tmp_.d(), flag);
+    EpiContinuity epi{guardPartial ? guardPartial : log.partial(0), dvd, dv, ht, out};
+    launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + g.points(), epi);
+    ctx.interps += 1;
+}
+
+void Solver::state(const double* m0, double* traj, bool guard) {
+    const double* X = departure(kForward);
+    const std::size_t N = g.points();
+    log.reset(ctx);
+    copy(ctx, N, m0, traj);
+    launchFieldMax(ctx, g, traj, log.partial(0));
+    for (int j = 1; j <= nt; ++j) {
+        launchPrefilter(ctx, g, traj + (j - 1) * N, coef_.d(), tmp_.d(), log.flag(j - 1));
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), traj + j * N});
+    }
+    ctx.interps += nt;
+    log.finalize(ctx);
+    log.check(ctx, "state", nt, true, guard, 0);
+}
+
+void Solver::stateFinal(const double* m0, double* out) {
+    const double* X = departure(kForward);
+    const std::size_t N = g.points();
+    double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
+    log.reset(ctx);
+    launchFieldMax(ctx, g, m0, log.partial(0));
+    const double* cur = m0;
+    for (int j = 1; j <= nt; ++j) {
+        double* dst = (j == nt) ? out : buf + (j % 2) * N;
+        launchPrefilter(ctx, g, cur, coef_.d(), tmp_.d(), log.flag(j - 1));
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), dst});
+        cur = dst;
+    }
+    ctx.interps += nt;
+    log.finalize(ctx);
+    log.check(ctx, "state", nt, true, true, 0);
+}
+
+void Solver::adjoint(const double* lam1, double* traj, bool guard) {
+    const std::size_t N = g.points();
+    log.reset(ctx);
+    copy(ctx, N, lam1, traj + nt * N);
+    launchFieldMax(ctx, g, traj + nt * N, log.partial(nt));
+    for (int j = nt; j >= 1; --j)
+        continuityStep(traj + j * N, traj + (j - 1) * N, kBackward, log.partial(j - 1), log.flag(j));
+    log.finalize(ctx);
+    log.check(ctx, "adjoint", nt, false, guard, nt);
+}
+
+void Solver::adjointFinal(const double* lam1, double* out) {
+    const std::size_t N = g.points();
+    double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
+    log.reset(ctx);
+    launchFieldMax(ctx, g, lam1, log.partial(nt));
+    const double* cur = lam1;
+    for (int j = nt; j >= 1; --j) {
+        double* dst = (j == 1) ? out : buf + (j % 2) * N;
+        continuityStep(cur, dst, kBackward, log.partial(j - 1), log.flag(j));
+        cur = dst;
+    }
+    log.finalize(ctx);
+    log.check(ctx, "adjoint", nt, false, true, nt);
+}
+
+void Solver::incState(const double* vt1, const double* vt2, const double* stateTraj, double* out) {
+    const std::size_t N = g.points();
+    const double* X = departure(kForward);
+    // vt at departure (2 interps), then per step (grad m_{j-1})_D (2 interps), grad m_j, m~_D
+    DBuf work(sizeof(double) * 8 * N);
+    double* vtD = work.d();          // [vt1D | vt2D]
+    double* gPrev = vtD + 2 * N;     // grad m_{j-1}
+    double* gCur = gPrev + 2 * N;    // grad m_j
+    double* gD = gCur + 2 * N;       // (grad m_{j-1})_D
+    double* c2 = ctx.scratchBuf(13, sizeof(double) * N);
+    launchPrefilter(ctx, g, vt1, coef_.d(), tmp_.d(), nullptr);
+    launchPrefilter(ctx, g, vt2, c2, tmp_.d(), nullptr);
+    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, vtD, vtD + N});
+    ctx.interps += 2;
+    gradient(ctx, g, stateTraj, gPrev, gPrev + N);
+    fill(ctx, N, 0.0, out);
+    for (int j = 1; j <= nt; ++j) {
+        launchPrefilter(ctx, g, gPrev, coef_.d(), tmp_.d(), nullptr);
+        launchPrefilter(ctx, g, gPrev + N, c2, tmp_.d(), nullptr);
+        launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, gD, gD + N});
+        gradient(ctx, g, stateTraj + j * N, gCur, gCur + N);
+        EpiIncState epi{nullptr, vtD, vtD + N, gD, gD + N, vt1, vt2, gCur, gCur + N, 0.5 * ht, out + j * N};
+        if (j == 1) {
+            launchPointwise(ctx, g, epi);  // m~_0 = 0
+        } else {
+            launchPrefilter(ctx, g, out + (j - 1) * N, coef_.d(), tmp_.d(), nullptr);
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi);
+        }
+        ctx.interps += 3;
+        std::swap(gPrev, gCur);
+    }
+    ctx.sync();
+}
+
+void Solver::jacobian(double* out) {
+    const std::size_t N = g.points();
+    double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
+    {
+        LaunchScope ls_(ctx, "k_ones");
+        k_ones<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, buf);
+    }
+    VRG_LAUNCH_CHECK();
+    const double* cur = buf;
+    for (int j = 1; j <= nt; ++j) {
+        double* dst = (j == nt) ? out : buf + (j % 2) * N;
+        continuityStep(cur, dst, kForward, log.partial(0), nullptr);
+        cur = dst;
+    }
+    ctx.sync();
+}
+
+}  // namespace vrg

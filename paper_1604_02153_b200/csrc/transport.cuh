@@ -1,0 +1,90 @@
+// Semi-Lagrangian transport on the device: transport::Solver (include/veloreg/transport.hpp:
+// 71-100, src/transport.cpp:91-454), SL branches only.  The RK2/RK2A spectral schemes are out
+// of scope and raise NotSupported at the C ABI.
+#pragma once
+
+#include "blas.cuh"
+#include "eval.cuh"
+#include "spectral.cuh"
+
+namespace vrg {
+
+enum Direction : int { kForward = 0, kBackward = 1 };
+
+// transport::deriveSteps (src/transport.cpp:44-50) on device fields.
+int deriveSteps(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double cfl);
+
+// traceCharacteristics (src/transport.cpp:60-89), from the prefiltered velocity
+// coefficients (cv1, cv2) so both directions share one prefilter.
+void launchTrace(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* cv1,
+                 const double* cv2, double ht, int dir, double* x1, double* x2);
+
+// Block maxima of |f| into guard partials (evaluate block layout).
+void launchFieldMax(Ctx& ctx, const GridDims& g, const double* f, double* partial);
+
+// Per-step guard bookkeeping for one solve: block maxima per step, reduced per step, plus the
+// prefilter non-finite flags, read back once when the solve ends.
+struct GuardLog {
+    int steps = 0;        // number of step slots (nt+1)
+    unsigned blocks = 0;  // evaluate blocks per step
+    DBuf partials;        // steps*blocks
+    DBuf stepMax;         // steps doubles
+    DBuf flags;           // steps unsigned
+    void ensure(int nsteps, unsigned nblocks);
+    double* partial(int step) const { return partials.d() + static_cast<std::size_t>(step) * blocks; }
+    unsigned* flag(int step) const { return flags.as<unsigned>() + step; }
+    void reset(Ctx& ctx);
+    void finalize(Ctx& ctx);  // per-step maxima from the partials (stream-ordered)
+    // Host readback; throws the reference's first error in solve order.
+    //   order: steps visited, each (prefilter-input step index, output step index).
+    void check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep);
+};
+
+class Solver {
+public:
+    Solver(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, int nt);
+    Ctx& ctx;
+    GridDims g;
+    int nt;
+    double ht;
+    DBuf v;  // [v1 | v2]
+
+    const double* v1() const { return v.d(); }
+    const double* v2() const { return v.d() + g.points(); }
+
+    // Lazy per-velocity caches (src/transport.cpp:107-127), with the reference's counter
+    // increments when first built.
+    const double* departure(int dir);  // [x1 | x2]
+    const double* divVelocity();
+    const double* divVelocityAtDeparture(int dir);
+
+    // Scratch owned by the solver.
+    double* coef();
+    double* tmp();
+
+    // slState (src/transport.cpp:214-227): traj = (nt+1) fields, traj[0] = m0.
+    void state(const double* m0, double* traj, bool guard);
+    // solveStateFinal (src/transport.cpp:267-278): out = m(1), two ping-pong buffers.
+    void stateFinal(const double* m0, double* out);
+    // slAdjoint (src/transport.cpp:229-241): traj[nt] = lam1, marching back.
+    void adjoint(const double* lam1, double* traj, bool guard);
+    void adjointFinal(const double* lam1, double* out);
+    // solveIncState SL (src/transport.cpp:322-342): out trajectory (nt+1) fields.
+    void incState(const double* vt1, const double* vt2, const double* stateTraj, double* out);
+    // jacobianDeterminant SL (src/transport.cpp:456-464).
+    void jacobian(double* out);
+
+    // One SL continuity step (slContinuityStep, src/transport.cpp:200-212) of u along dir.
+    void continuityStep(const double* u, double* out, int dir, double* guardPartial, unsigned* flag);
+
+    GuardLog log;
+
+private:
+    DBuf cv_;  // prefiltered velocity [c1 | c2]
+    DBuf X_[2];
+    DBuf divv_, dvDep_[2];
+    DBuf coef_, tmp_;
+    bool haveCv_ = false, haveX_[2] = {false, false}, haveDivv_ = false, haveDvDep_[2] = {false, false};
+};
+
+}  // namespace vrg

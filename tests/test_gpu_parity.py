@@ -1,0 +1,273 @@
+"""GPU parity: libvrg (sm_100a, through the C ABI) against the oracle.
+
+Oracles: the committed golden vectors produced by the unmodified reference
+(tests/golden/*.npz), the numpy restatement (oracle/veloreg_np.py) and, when it travelled
+with the snapshot, the compiled reference itself (oracle/_ref).  Tolerances: the north_star
+bar is fp64 relative 1e-10 per transport solve and per Hessian matvec; the tests use it (or
+tighter where the computation is a single stage).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import veloreg_np as O
+from paper_1604_02153_b200 import synth
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-10  # north_star: fp64 relative per transport solve / per matvec
+
+
+def gold(name):
+    return dict(np.load(os.path.join(GOLD, name + ".npz")))
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1604_02153_b200 import api as A
+
+    return A
+
+
+# ------------------------------------------------------------------ interp (K1, K2)
+def test_prefilter_golden(ctx, api):
+    d = gold("interp_48x32")
+    c = api.prefilter(ctx, ctx.field(d["u"]))
+    assert rel(c, d["coef"]) < 1e-13
+
+
+@pytest.mark.parametrize("shape", [(4, 4), (8, 6), (32, 32), (64, 64), (96, 40), (256, 256), (1024, 1024)])
+def test_prefilter_oracle(ctx, api, shape):
+    u = synth.uniform(7, shape[0] * shape[1]).reshape(shape) - 0.5
+    c = api.prefilter(ctx, ctx.field(u))
+    assert rel(c, O.prefilter(u)) < 1e-13
+
+
+def test_prefilter_constant_pin(ctx, api):
+    # test_interp.cpp:40-44: constant 2.75 stays 2.75 to 1e-13
+    c = api.prefilter(ctx, ctx.field(np.full((32, 32), 2.75))).cpu().numpy()
+    assert np.abs(c - 2.75).max() <= 2.75e-13
+
+
+def test_evaluate_golden(ctx, api):
+    d = gold("interp_48x32")
+    out = api.evaluate(ctx, ctx.field(d["coef"]), ctx.field(d["x1"]), ctx.field(d["x2"]))
+    assert rel(out, d["eval"]) < 1e-13
+
+
+def test_evaluate_node_reproduction(ctx, api):
+    # test_interp.cpp:46-51
+    u = gold("interp_48x32")["rbl_seed3"]
+    X1, X2 = O.coords(u.shape)
+    back = api.evaluate(ctx, api.prefilter(ctx, ctx.field(u)), ctx.field(X1), ctx.field(X2))
+    assert np.abs(back.cpu().numpy() - u).max() <= 1e-10 * (1.0 + np.abs(u).max())
+
+
+def test_evaluate_period_shift(ctx, api):
+    # test_interp.cpp:64-75
+    u = gold("interp_48x32")["rbl_seed3"]
+    rng = np.random.default_rng(18)
+    x1 = rng.uniform(-np.pi, np.pi, u.shape)
+    x2 = rng.uniform(-np.pi, np.pi, u.shape)
+    c = api.prefilter(ctx, ctx.field(u))
+    a = api.evaluate(ctx, c, ctx.field(x1), ctx.field(x2))
+    b = api.evaluate(ctx, c, ctx.field(x1 + 2 * np.pi), ctx.field(x2 - 4 * np.pi))
+    assert float((a - b).abs().max()) <= 1e-12
+
+
+def test_evaluate_rejects_nonfinite(ctx, api):
+    c = ctx.field(np.zeros((16, 16)))
+    x = np.zeros((16, 16))
+    x[3, 4] = np.nan
+    with pytest.raises(api.InvalidArgument, match="non-finite point coordinate"):
+        api.evaluate(ctx, c, ctx.field(x), ctx.field(np.zeros((16, 16))))
+    u = np.zeros((16, 16))
+    u[0, 0] = np.inf
+    with pytest.raises(api.InvalidArgument, match="prefilter: non-finite value"):
+        api.prefilter(ctx, ctx.field(u))
+
+
+# ------------------------------------------------------------------ spectral (K7)
+def test_spectral_golden(ctx, api):
+    d = gold("interp_48x32")
+    u = ctx.field(d["u"])
+    a = (ctx.field(d["a1"]), ctx.field(d["a2"]))
+    g1, g2 = api.gradient(ctx, u)
+    assert rel(g1, d["grad1"]) < 1e-12 and rel(g2, d["grad2"]) < 1e-12
+    assert rel(api.divergence(ctx, a), d["div"]) < 1e-12
+    r1, r2 = api.apply_reg(ctx, a, 2, 1e-2)
+    assert rel(r1, d["reg1"]) < 1e-12 and rel(r2, d["reg2"]) < 1e-12
+    i1, i2 = api.apply_inv_reg(ctx, a, 2, 1e-2, -0.5)
+    assert rel(i1, d["ireg1"]) < 1e-12 and rel(i2, d["ireg2"]) < 1e-12
+    l1, l2 = api.project_div_free(ctx, a)
+    assert rel(l1, d["leray1"]) < 1e-12 and rel(l2, d["leray2"]) < 1e-12
+    rc = api.resample(ctx, u, (24, 16))
+    assert rel(rc, d["restrict"]) < 1e-12
+    assert rel(api.resample(ctx, rc, (48, 32)), d["prolong"]) < 1e-12
+    assert rel(api.cutoff_filter(ctx, u, api.BAND_LOW), d["low"]) < 1e-12
+    assert rel(api.cutoff_filter(ctx, u, api.BAND_HIGH), d["high"]) < 1e-12
+
+
+def test_gradient_closed_form(ctx, api):
+    # test_spectral.cpp:25-61 style: exact derivatives of trigonometric fields to 1e-12
+    X1, X2 = O.coords((64, 64))
+    u = np.sin(X1) * np.cos(2 * X2) + np.cos(3 * X1)
+    g1, g2 = api.gradient(ctx, ctx.field(u))
+    assert np.abs(g1.cpu().numpy() - (np.cos(X1) * np.cos(2 * X2) - 3 * np.sin(3 * X1))).max() < 1e-12
+    assert np.abs(g2.cpu().numpy() + 2 * np.sin(X1) * np.sin(2 * X2)).max() < 1e-12
+
+
+# ------------------------------------------------------------------ transport (K3-K6)
+def _cfg1(ctx):
+    d = gold("cfg1_64")
+    n, nt, beta = d["meta"]
+    return d, int(nt), float(beta), (ctx.field(d["w1"]), ctx.field(d["w2"]))
+
+
+def test_trace_golden(ctx, api):
+    d, nt, _, w = _cfg1(ctx)
+    xf = api.trace_characteristics(ctx, w, 1.0 / nt, api.FORWARD)
+    xb = api.trace_characteristics(ctx, w, 1.0 / nt, api.BACKWARD)
+    assert rel(xf[0], d["xf1"]) < 1e-15 and rel(xf[1], d["xf2"]) < 1e-15
+    assert rel(xb[0], d["xb1"]) < 1e-15 and rel(xb[1], d["xb2"]) < 1e-15
+
+
+def test_state_adjoint_incstate_golden(ctx, api):
+    d, nt, _, w = _cfg1(ctx)
+    s = api.Solver(ctx, w, nt)
+    st = s.solve_state(ctx.field(d["mT"]))
+    assert rel(st, d["state"]) < TOL
+    assert rel(s.solve_adjoint(ctx.field(d["lam1"])), d["adjoint"]) < TOL
+    assert rel(s.solve_inc_state((ctx.field(d["vt1"]), ctx.field(d["vt2"])), st), d["incstate"]) < TOL
+    assert rel(s.solve_state_final(ctx.field(d["mT"])), d["state"][-1]) < TOL
+    assert rel(s.solve_adjoint_final(ctx.field(d["lam1"])), d["adjoint"][0]) < TOL
+
+
+def test_counters_match_reference(ctx, api):
+    # test_diag_io.cpp:62-75 / acceptance C11: SL state = 2 + nt interps and no FFT;
+    # adjoint = 3 + nt interps (+ 3 FFTs for div v) on a fresh Solver
+    d, nt, _, w = _cfg1(ctx)
+    ctx.reset_counters()
+    api.Solver(ctx, w, nt).solve_state(ctx.field(d["mT"]))
+    assert ctx.counters() == tuple(d["count_state"])
+    ctx.reset_counters()
+    api.Solver(ctx, w, nt).solve_adjoint(ctx.field(d["lam1"]))
+    assert ctx.counters() == tuple(d["count_adjoint"])
+
+
+def test_incadjoint_gn_equals_adjoint_bitexact(ctx, api):
+    # test_transport.cpp:211-238: GN incremental adjoint == adjoint, == 0.0
+    d, nt, _, w = _cfg1(ctx)
+    s = api.Solver(ctx, w, nt)
+    lam = ctx.field(d["lam1"])
+    a = s.solve_adjoint(lam)
+    vt = (ctx.field(d["vt1"]), ctx.field(d["vt2"]))
+    gn = s.solve_inc_adjoint(vt, lam, None, api.GAUSS_NEWTON)
+    assert float((a - gn).abs().max()) == 0.0
+
+
+def test_zero_velocity_identity(ctx, api):
+    # test_transport.cpp:102-112 (SL): v = 0 transports nothing to 1e-14
+    mT = synth.config12_fields(64)[0]
+    z = (ctx.field(np.zeros((64, 64))), ctx.field(np.zeros((64, 64))))
+    s = api.Solver(ctx, z, 4)
+    st = s.solve_state(ctx.field(mT)).cpu().numpy()
+    assert np.abs(st - mT[None]).max() <= 1e-14
+    ad = s.solve_adjoint(ctx.field(mT)).cpu().numpy()
+    assert np.abs(ad - mT[None]).max() <= 1e-14
+
+
+@pytest.mark.parametrize("amp,nt", [(16.0, 8), (16.0, 4), (30.0, 8)])
+def test_blowup_guard_message(ctx, api, ref, amp, nt):
+    # strongly compressible velocity: the adjoint grows like exp(int div v) past 1e3
+    X1, _ = O.coords((32, 32))
+    v1 = amp * np.sin(X1)
+    v2 = np.zeros_like(v1)
+    lam = np.ones((32, 32)) + 0.1 * np.cos(X1)
+    with pytest.raises(Exception) as e_ref:
+        ref.solve_adjoint(v1, v2, nt, lam)
+    with pytest.raises(api.BlowupError) as e_gpu:
+        api.Solver(ctx, (ctx.field(v1), ctx.field(v2)), nt).solve_adjoint(ctx.field(lam))
+    assert str(e_gpu.value) == str(e_ref.value)
+
+
+# ------------------------------------------------------------------ Hessian matvec (the hot path)
+def test_hessian_apply_golden(ctx, api):
+    d, nt, beta, w = _cfg1(ctx)
+    H = api.HessianOperator(ctx, w, ctx.field(d["mR"]), ctx.field(d["mT"]), api.H2SEMI, beta, api.COMPRESSIBLE, nt)
+    vt = (ctx.field(d["vt1"]), ctx.field(d["vt2"]))
+    h1, h2 = H.apply(vt)
+    assert rel(h1, d["hv1"]) < TOL and rel(h2, d["hv2"]) < TOL
+    d1, d2 = H.apply_data_term(vt)
+    assert rel(d1, d["dt1"]) < TOL and rel(d2, d["dt2"]) < TOL
+    # steady state: a second apply is bit-identical (cached per-iterate invariants)
+    k1, k2 = H.apply(vt)
+    assert float((k1 - h1).abs().max()) == 0.0 and float((k2 - h2).abs().max()) == 0.0
+
+
+def test_hessian_incompressible_golden(ctx, api):
+    d = gold("incomp_64")
+    n, nt, beta = d["meta"]
+    w = (ctx.field(d["w1"]), ctx.field(d["w2"]))
+    H = api.HessianOperator(ctx, w, ctx.field(d["mR"]), ctx.field(d["mT"]), api.H1SEMI, float(beta),
+                            api.INCOMPRESSIBLE, int(nt))
+    h1, h2 = H.apply((ctx.field(d["vt1"]), ctx.field(d["vt2"])))
+    assert rel(h1, d["hv1"]) < TOL and rel(h2, d["hv2"]) < TOL
+
+
+def test_hessian_split_vs_oracle(ctx, api):
+    d, nt, beta, w = _cfg1(ctx)
+    Ho = O.Hessian(d["w1"], d["w2"], d["mR"], d["mT"], 2, beta, 0, nt)
+    e1, e2 = Ho.split_apply(d["vt1"], d["vt2"])
+    H = api.HessianOperator(ctx, w, ctx.field(d["mR"]), ctx.field(d["mT"]), api.H2SEMI, beta, api.COMPRESSIBLE, nt)
+    s1, s2 = H.apply_split((ctx.field(d["vt1"]), ctx.field(d["vt2"])))
+    assert rel(s1, e1) < TOL and rel(s2, e2) < TOL
+
+
+def test_hessian_counters(ctx, api):
+    # HessianOperator::apply steady state: 4nt+2 interps and 6nt+10 FFTs
+    d, nt, beta, w = _cfg1(ctx)
+    H = api.HessianOperator(ctx, w, ctx.field(d["mR"]), ctx.field(d["mT"]), api.H2SEMI, beta, api.COMPRESSIBLE, nt)
+    vt = (ctx.field(d["vt1"]), ctx.field(d["vt2"]))
+    H.apply(vt)
+    ctx.reset_counters()
+    H.apply(vt)
+    assert ctx.counters() == (6 * nt + 10, 4 * nt + 2)
+
+
+def test_gradient_objective_golden(ctx, api):
+    d, nt, beta, w = _cfg1(ctx)
+    (g1, g2), sc = api.evaluate_gradient(ctx, w, ctx.field(d["mR"]), ctx.field(d["mT"]), 2, beta, 0, nt)
+    assert rel(g1, d["g1"]) < TOL and rel(g2, d["g2"]) < TOL
+    assert np.allclose(sc, d["gscalars"], rtol=1e-12, atol=0)
+    so = api.evaluate_objective(ctx, w, ctx.field(d["mR"]), ctx.field(d["mT"]), 2, beta, 0, nt)
+    assert np.allclose(so, d["oscalars"], rtol=1e-12, atol=0)
+    di = gold("incomp_64")
+    n, nt2, beta2 = di["meta"]
+    (h1, h2), sc2 = api.evaluate_gradient(ctx, (ctx.field(di["w1"]), ctx.field(di["w2"])), ctx.field(di["mR"]),
+                                          ctx.field(di["mT"]), 1, float(beta2), 1, int(nt2))
+    assert rel(h1, di["g1"]) < TOL and rel(h2, di["g2"]) < TOL
+
+
+@pytest.mark.parametrize("n,nt", [(128, 8), (256, 8)])
+def test_hessian_oracle_random(ctx, api, n, nt):
+    """Seeded config-3/4 style inputs (smoothed noise template, smooth random v) vs numpy."""
+    mT = synth.smoothed_noise(n, n, 1000)
+    v1, v2 = synth.smooth_velocity(n, n, 2000)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    mR = O.Solver(v1, v2, nt).solve_state(mT)[-1]
+    w1, w2 = 0.5 * v1, 0.5 * v2
+    Ho = O.Hessian(w1, w2, mR, mT, 2, 1e-3, 0, nt)
+    e1, e2 = Ho.apply(vt1, vt2)
+    H = api.HessianOperator(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT), 2, 1e-3, 0, nt)
+    h1, h2 = H.apply((ctx.field(vt1), ctx.field(vt2)))
+    assert rel(h1, e1) < TOL and rel(h2, e2) < TOL

@@ -1,0 +1,191 @@
+"""CPU: pin the numpy restatement (oracle/veloreg_np.py) before trusting it.
+
+1. against the golden vectors the UNMODIFIED reference produced (tests/golden/*.npz);
+2. against the reference's own analytic/property pins (test_interp.cpp, test_spectral.cpp,
+   test_transport.cpp), re-run on the restatement;
+3. against the compiled reference itself (oracle/_ref) on fresh seeded inputs, when built.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import veloreg_np as O
+from paper_1604_02153_b200 import synth
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def gold(name):
+    return dict(np.load(os.path.join(GOLD, name + ".npz")))
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+# ------------------------------------------------------------------ 1. golden vectors
+def test_golden_interp_spectral():
+    d = gold("interp_48x32")
+    assert rel(O.prefilter(d["u"]), d["coef"]) < 1e-14
+    assert rel(O.evaluate(d["coef"], d["x1"], d["x2"]), d["eval"]) < 1e-14
+    g1, g2 = O.gradient(d["u"])
+    assert rel(g1, d["grad1"]) < 1e-13 and rel(g2, d["grad2"]) < 1e-13
+    assert rel(O.divergence(d["a1"], d["a2"]), d["div"]) < 1e-13
+    # beta |k|^4 amplifies FFT rounding at the top modes (pocketfft vs the shimmed FFTW path)
+    assert rel(O.apply_reg(d["a1"], d["a2"], 2, 1e-2)[0], d["reg1"]) < 1e-11
+    assert rel(O.apply_inv_reg(d["a1"], d["a2"], 2, 1e-2, -0.5)[1], d["ireg2"]) < 1e-13
+    l1, l2 = O.project_div_free(d["a1"], d["a2"])
+    assert rel(l1, d["leray1"]) < 1e-13 and rel(l2, d["leray2"]) < 1e-13
+    assert rel(O.resample(d["u"], (24, 16)), d["restrict"]) < 1e-13
+    assert rel(O.resample(d["restrict"], (48, 32)), d["prolong"]) < 1e-13
+    assert rel(O.cutoff(d["u"], False), d["low"]) < 1e-13
+    assert rel(O.cutoff(d["u"], True), d["high"]) < 1e-13
+
+
+def test_golden_cfg1_transport_and_matvec():
+    d = gold("cfg1_64")
+    n, nt, beta = d["meta"]
+    nt = int(nt)
+    s = O.Solver(d["w1"], d["w2"], nt)
+    xf = s.characteristics(False)
+    assert rel(xf[0], d["xf1"]) == 0.0 and rel(xf[1], d["xf2"]) == 0.0
+    st = s.solve_state(d["mT"])
+    assert rel(st, d["state"]) < 1e-13
+    assert rel(s.solve_adjoint(d["lam1"]), d["adjoint"]) < 1e-13
+    assert rel(s.solve_incstate(d["vt1"], d["vt2"], st), d["incstate"]) < 1e-13
+    H = O.Hessian(d["w1"], d["w2"], d["mR"], d["mT"], 2, float(beta), 0, nt)
+    h1, h2 = H.apply(d["vt1"], d["vt2"])
+    assert rel(h1, d["hv1"]) < 1e-11 and rel(h2, d["hv2"]) < 1e-11
+    (g1, g2), obj, mis, reg, _, _ = O.evaluate_gradient(d["w1"], d["w2"], d["mR"], d["mT"], 2, float(beta), 0, nt)
+    # g = beta A v + b nearly cancels at this iterate (max|g| ~ 3e-3 vs terms ~ 1): rounding
+    # of the terms shows up at ~1e-10 relative to max|g|
+    assert rel(g1, d["g1"]) < 1e-9 and rel(g2, d["g2"]) < 1e-9
+    assert np.allclose([obj, mis, reg], d["gscalars"], rtol=1e-13, atol=0)
+
+
+def test_golden_incompressible():
+    d = gold("incomp_64")
+    n, nt, beta = d["meta"]
+    H = O.Hessian(d["w1"], d["w2"], d["mR"], d["mT"], 1, float(beta), 1, int(nt))
+    h1, h2 = H.apply(d["vt1"], d["vt2"])
+    assert rel(h1, d["hv1"]) < 1e-13 and rel(h2, d["hv2"]) < 1e-13
+
+
+# ------------------------------------------------------------------ 2. reference analytic pins
+def _random_points(shape, seed, lo=-10.0, hi=10.0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, shape), rng.uniform(lo, hi, shape)
+
+
+def test_pin_prefilter_constant():  # test_interp.cpp:40-44
+    c = O.prefilter(np.full((32, 32), 2.75))
+    assert np.abs(c - 2.75).max() <= 2.75e-13
+
+
+def test_pin_half_cell_sine():  # test_interp.cpp:53-62
+    X1, X2 = O.coords((64, 64))
+    u = np.sin(X1)
+    h = 2 * math.pi / 64
+    out = O.evaluate(O.prefilter(u), X1 + 0.5 * h, X2)
+    assert np.abs(out - np.sin(X1 + 0.5 * h)).max() <= 1e-5
+
+
+def test_pin_constants_anywhere():  # test_interp.cpp:77-82
+    x1, x2 = _random_points((32, 32), 23)
+    vals = O.evaluate(O.prefilter(np.full((32, 32), -0.4)), x1, x2)
+    assert np.abs(vals + 0.4).max() <= 1e-12
+
+
+def test_pin_fourth_order():  # test_interp.cpp:84-104
+    f = lambda a, b: np.sin(3 * a) * np.cos(2 * b) + np.cos(a)  # noqa: E731
+    errs = []
+    for n in (32, 64, 128):
+        X1, X2 = O.coords((n, n))
+        x1, x2 = _random_points((n, n), 29, -math.pi, math.pi)
+        vals = O.evaluate(O.prefilter(f(X1, X2)), x1, x2)
+        errs.append(np.abs(vals - f(x1, x2)).max())
+    assert math.log2(errs[0] / errs[1]) >= 3.5 and math.log2(errs[1] / errs[2]) >= 3.5
+
+
+def test_pin_derive_steps():  # test_transport.cpp:30-41 (SMOOTH A/B velocities, 64^2)
+    X1, X2 = O.coords((64, 64))
+    a1, a2 = 0.5 * np.sin(X2) * np.cos(X1), 0.5 * np.sin(X1) * np.cos(X2)
+    assert [O.derive_steps(a1, a2, c) for c in (0.2, 1.0, 5.0, 10.0)] == [26, 6, 2, 2]
+    b1, b2 = np.sin(2 * X2) * np.cos(2 * X1), np.sin(2 * X1) * np.cos(2 * X2)
+    assert O.derive_steps(b1, b2, 0.2) == 51
+    with pytest.raises(ValueError):
+        O.derive_steps(a1, a2, 0.0)
+    with pytest.raises(ValueError):
+        O.derive_steps(a1, a2, 21.0)
+
+
+def test_pin_characteristics_constant_flow():  # test_transport.cpp:43-62
+    n = 64
+    c1, c2 = np.full((n, n), 0.3), np.full((n, n), -0.1)
+    X1, X2 = O.coords((n, n))
+    x1, x2 = O.trace(c1, c2, 0.05)
+    assert abs(x1[5, 9] - (X1[5, 9] - 0.05 * 0.3)) <= 1e-14 * abs(X1[5, 9])
+    assert abs(x2[5, 9] - (X2[5, 9] + 0.05 * 0.1)) <= 1e-14 * abs(X2[5, 9])
+    b1, _ = O.trace(c1, c2, 0.05, backward=True)
+    assert abs(b1[5, 9] - (X1[5, 9] + 0.05 * 0.3)) <= 1e-14 * abs(X1[5, 9])
+
+
+def test_pin_sl_full_period():  # test_transport.cpp:123-130
+    n = 64
+    X1, X2 = O.coords((n, n))
+    m0 = 0.25 * (1 + np.cos(X1)) * (1 + np.cos(X2))
+    v1, v2 = np.full((n, n), 2 * math.pi), np.zeros((n, n))
+    m1 = O.Solver(v1, v2, 8).solve_state(m0)[-1]
+    assert np.abs(m1 - m0).max() <= 1e-3
+
+
+def test_pin_spectral_resample_roundtrip():  # test_spectral.cpp:190-214
+    u = O.resample(synth.smooth_scalar(32, 32, 9), (32, 32))
+    up = O.resample(u, (64, 64))
+    back = O.resample(up, (32, 32))
+    # band-limited below 16: prolongation then restriction is exact
+    lo = O.cutoff(u, False)
+    assert np.abs(O.resample(O.resample(lo, (64, 64)), (32, 32)) - lo).max() <= 1e-14
+    assert back.shape == (32, 32)
+
+
+def test_pin_cutoff_partition():  # test_spectral.cpp:216-232
+    u = synth.smooth_scalar(64, 64, 4)
+    assert np.abs(O.cutoff(u, False) + O.cutoff(u, True) - u).max() <= 1e-14
+
+
+def test_pin_leray_divergence_free():  # test_spectral.cpp:164-188
+    a1, a2 = synth.smooth_velocity(64, 64, 8)
+    p1, p2 = O.project_div_free(a1, a2)
+    assert np.abs(O.divergence(p1, p2)).max() <= 1e-12 * max(np.abs(a1).max(), 1.0)
+
+
+def test_synth_generator_deterministic():
+    a = synth.normal(123, 1001)
+    b = synth.normal(123, 1001)
+    assert np.array_equal(a, b) and abs(a.mean()) < 0.1 and abs(a.std() - 1) < 0.1
+    v1, v2 = synth.smooth_velocity(64, 64, 2000)
+    assert abs(max(np.abs(v1).max(), np.abs(v2).max()) - 0.3) < 1e-15
+
+
+# ------------------------------------------------------------------ 3. compiled reference (fresh inputs)
+def test_oracle_vs_compiled_reference_random(ref):
+    n, nt = 64, 6
+    mT = synth.smoothed_noise(n, n, 1001)
+    v1, v2 = synth.smooth_velocity(n, n, 2001)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3001)
+    mR = ref.solve_state_final(v1, v2, nt, mT)
+    w1, w2 = 0.5 * v1, 0.5 * v2
+    a = ref.Hessian(w1, w2, mR, mT, 2, 1e-3, 0, nt).apply(vt1, vt2)
+    b = O.Hessian(w1, w2, mR, mT, 2, 1e-3, 0, nt).apply(vt1, vt2)
+    assert rel(b[0], a[0]) < 1e-11 and rel(b[1], a[1]) < 1e-11
+    c = ref.Coarse(w1, w2, mR, mT, 2, 1e-3, 0)
+    co = O.Coarse(w1, w2, mR, mT, 2, 1e-3, 0)
+    x = ref.random_bandlimited_velocity(n, n, 5)
+    r1 = c.two_level(x[0], x[1], 1, 10, 0.1, 0.5, 1.0, 4.0)
+    r2 = O.two_level(x[0], x[1], co, 1, 10, 0.1, 0.5, 1.0, 4.0)
+    assert rel(r2[0], r1[0]) < 1e-12
