@@ -134,6 +134,46 @@ int vrg_evaluate_gradient(vrg_ctx_t ctx, int n1, int n2, const double* v1, const
 int vrg_evaluate_objective(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
                            const double* mT, int norm, double beta, int deformation, int nt, double* scalars);
 
+/* ---- precond (precond.hpp:25-95) ---- */
+/* problems::randomBandLimitedField (problems.hpp:45): libstdc++ mt19937_64 + normal draws */
+int vrg_random_bandlimited_field(vrg_ctx_t ctx, int n1, int n2, unsigned long long seed, double* out);
+/* precond::CoarseOperator(vFine, problem, model, coarseScheme{SL, cfl}) (precond.hpp:56-70);
+ * v1/v2 may be NULL for v = 0. */
+int vrg_coarse_create(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                      const double* mT, int norm, double beta, int deformation, double coarse_cfl, vrg_coarse_t* out);
+void vrg_coarse_destroy(vrg_coarse_t c);
+int vrg_coarse_info(vrg_coarse_t c, int* n1c, int* n2c, int* nt); /* grid() and the CFL-derived coarse nt */
+/* CoarseOperator::applySplitHessian; s/out are coarse-grid fields */
+int vrg_coarse_apply_split(vrg_coarse_t c, const double* s1, const double* s2, double* o1, double* o2);
+/* applyTwoLevel(r, coarse, choice, outerTol, eMin, eMax) (precond.hpp:74-78); coarse_solver 0 = PCG, 1 = CHEB.
+ * Returns VRG_OK; *fallback = 1 when the coarse solve diverged and the identity was applied. */
+int vrg_two_level_apply(vrg_coarse_t c, const double* r1, const double* r2, int coarse_solver, int cheb_iters,
+                        double eps_scale, double outer_tol, double emin, double emax, double* o1, double* o2,
+                        int* fallback);
+/* estimateEigs / estimateEigsAt (precond.hpp:40-53): Lanczos(30) eMax of the coarse split Hessian */
+int vrg_estimate_eigs(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                      const double* mT, int norm, double beta, int deformation, double coarse_cfl,
+                      unsigned long long seed, double* emin, double* emax);
+/* solveKkt(hess, rhs, tol, maxIter, choice, problem, v, coarseScheme) (precond.hpp:93-95).
+ * pc_int = [kind(0 reg, 1 two-level), coarse_solver, cheb_iters, has_eig]; pc_dbl = [eps_scale, emin, emax];
+ * result = [iterations, converged, negative_curvature, rel_residual, total_s, precond_s]. */
+int vrg_solve_kkt(vrg_hess_t h, const double* rhs1, const double* rhs2, double tol, int max_iter, const int* pc_int,
+                  const double* pc_dbl, const double* mR, const double* mT, const double* v1, const double* v2,
+                  double coarse_cfl, double* sol1, double* sol2, double* result);
+
+/* ---- newton (newton.hpp:10-12): inverse::newtonSolve on HOST images mR/mT, v returned on the host.
+ * cfg_int = [maxOuterIter, maxInnerIter, ntOverride(0 = CFL), lsMaxSteps]
+ * cfg_dbl = [tolRelGrad, tolAbsGrad, forcingCap, lsC1, lsShrink, gradCfl]
+ * pc_int / pc_dbl as for vrg_solve_kkt (has_eig = 0: estimated at v = 0 like newton.cpp:36-40)
+ * records: per outer iteration 12 doubles [iter, gradNormInf, gradNormRel, objective, mismatch,
+ *          innerIterations, lineSearchSteps, stepLength, searchDirDivRatio, wallTimeSec, ffts, interps]
+ * summary = [status(0 converged, 1 iteration limit, 2 line-search failure), n_iterations,
+ *            finalGradNormRel, finalResidualRel, jacMin, jacMax, totalTimeSec] */
+int vrg_newton_solve(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, const double* mT_host, int norm,
+                     double beta, int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
+                     const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
+                     double* summary);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,15 @@ _SIG = {
     "vrg_hess_state": ("pp", C.c_int),
     "vrg_evaluate_gradient": ("piippppidiippp", C.c_int),
     "vrg_evaluate_objective": ("piippppidiip", C.c_int),
+    "vrg_random_bandlimited_field": ("piiup", C.c_int),
+    "vrg_coarse_create": ("piippppididp", C.c_int),
+    "vrg_coarse_destroy": ("p", None),
+    "vrg_coarse_info": ("pppp", C.c_int),
+    "vrg_coarse_apply_split": ("ppppp", C.c_int),
+    "vrg_two_level_apply": ("pppiiddddppp", C.c_int),
+    "vrg_estimate_eigs": ("piippppididupp", C.c_int),
+    "vrg_solve_kkt": ("pppdippppppdppp", C.c_int),
+    "vrg_newton_solve": ("piippidipppppppip", C.c_int),
 }
 
 _KIND = {"p": C.c_void_p, "i": C.c_int, "d": C.c_double, "u": C.c_ulonglong}

@@ -338,3 +338,113 @@ def evaluate_objective(ctx, v, mR, mT, norm, beta, deformation, nt):
     ctx.check(ctx.lib.vrg_evaluate_objective(ctx.h, n1, n2, _p(v[0]), _p(v[1]), _p(mR), _p(mT), norm, beta,
                                              deformation, nt, C.cast(sc, C.c_void_p)))
     return tuple(sc)
+
+
+# ---------------------------------------------------------------- precond (precond.hpp)
+PC_REG, PC_TWO_LEVEL = 0, 1
+COARSE_PCG, COARSE_CHEB = 0, 1
+COARSE_CFL = 5.0  # kCoarseScheme, newton.cpp:16
+
+
+def random_bandlimited_field(ctx, shape, seed):
+    out = ctx.empty(*shape)
+    ctx.check(ctx.lib.vrg_random_bandlimited_field(ctx.h, int(shape[0]), int(shape[1]), C.c_ulonglong(seed), _p(out)))
+    return out
+
+
+def random_bandlimited_velocity(ctx, shape, seed):
+    return (random_bandlimited_field(ctx, shape, seed),
+            random_bandlimited_field(ctx, shape, seed ^ 0x9E3779B97F4A7C15))
+
+
+class CoarseOperator:
+    """precond::CoarseOperator: half-grid split GN Hessian at the restricted velocity (v=None: 0)."""
+
+    def __init__(self, ctx, v, mR, mT, norm, beta, deformation, coarse_cfl=COARSE_CFL):
+        self.ctx = ctx
+        self.fine = _shape(mR)
+        h = C.c_void_p()
+        v1, v2 = (v[0], v[1]) if v is not None else (None, None)
+        ctx.check(ctx.lib.vrg_coarse_create(ctx.h, *self.fine, _p(v1), _p(v2), _p(mR), _p(mT), norm, beta,
+                                            deformation, coarse_cfl, C.byref(h)))
+        self.h = h
+        a, b, nt = C.c_int(), C.c_int(), C.c_int()
+        ctx.lib.vrg_coarse_info(h, C.byref(a), C.byref(b), C.byref(nt))
+        self.shape, self.nt = (a.value, b.value), nt.value
+
+    def apply_split(self, s):
+        o = self.ctx.empty(2, *self.shape)
+        self.ctx.check(self.ctx.lib.vrg_coarse_apply_split(self.h, _p(s[0]), _p(s[1]), _p(o[0]), _p(o[1])))
+        return o[0], o[1]
+
+    def two_level(self, r, coarse_solver, cheb_iters, eps_scale, outer_tol, emin, emax):
+        o = self.ctx.empty(2, *self.fine)
+        fb = C.c_int()
+        self.ctx.check(self.ctx.lib.vrg_two_level_apply(self.h, _p(r[0]), _p(r[1]), coarse_solver, cheb_iters,
+                                                        eps_scale, outer_tol, emin, emax, _p(o[0]), _p(o[1]),
+                                                        C.byref(fb)))
+        return (o[0], o[1]), bool(fb.value)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.vrg_coarse_destroy(self.h)
+            self.h = None
+
+
+def estimate_eigs(ctx, mR, mT, norm, beta, deformation, v=None, coarse_cfl=COARSE_CFL, seed=0x5EED):
+    n1, n2 = _shape(mR)
+    a, b = C.c_double(), C.c_double()
+    v1, v2 = (v[0], v[1]) if v is not None else (None, None)
+    ctx.check(ctx.lib.vrg_estimate_eigs(ctx.h, n1, n2, _p(v1), _p(v2), _p(mR), _p(mT), norm, beta, deformation,
+                                        coarse_cfl, C.c_ulonglong(seed), C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def _pc_arrays(kind, coarse_solver, cheb_iters, eps_scale, eig):
+    pi = (C.c_int * 4)(kind, coarse_solver, cheb_iters, 1 if eig else 0)
+    pd = (C.c_double * 3)(eps_scale, eig[0] if eig else 1.0, eig[1] if eig else 10.0)
+    return pi, pd
+
+
+def solve_kkt(hess, rhs, tol, max_iter, mR, mT, v, *, kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10,
+              eps_scale=0.1, eig=None, coarse_cfl=COARSE_CFL):
+    """precond::solveKkt; returns (delta_v, dict(iterations, converged, negative_curvature, rel_residual, ...))."""
+    ctx = hess.ctx
+    pi, pd = _pc_arrays(kind, coarse_solver, cheb_iters, eps_scale, eig)
+    sol = ctx.empty(2, *hess.shape)
+    res = (C.c_double * 6)()
+    ctx.check(ctx.lib.vrg_solve_kkt(hess.h, _p(rhs[0]), _p(rhs[1]), tol, max_iter, C.cast(pi, C.c_void_p),
+                                    C.cast(pd, C.c_void_p), _p(mR), _p(mT), _p(v[0]), _p(v[1]), coarse_cfl,
+                                    _p(sol[0]), _p(sol[1]), C.cast(res, C.c_void_p)))
+    return (sol[0], sol[1]), dict(iterations=int(res[0]), converged=bool(res[1]), negative_curvature=bool(res[2]),
+                                  rel_residual=res[3], total_s=res[4], precond_s=res[5])
+
+
+RECORD_FIELDS = ("iter", "gradNormInf", "gradNormRel", "objective", "mismatch", "innerIterations",
+                 "lineSearchSteps", "stepLength", "searchDirDivRatio", "wallTimeSec", "ffts", "interps")
+
+
+def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=0, ls_max_steps=20,
+                 tol_rel=1e-2, tol_abs=1e-5, forcing_cap=0.5, ls_c1=1e-4, ls_shrink=0.5, grad_cfl=1.0,
+                 kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10, eps_scale=0.1, eig=None):
+    """inverse::newtonSolve on host images (numpy); returns (v1, v2, records, summary)."""
+    import numpy as np
+
+    mR = np.ascontiguousarray(mR, dtype=np.float64)
+    mT = np.ascontiguousarray(mT, dtype=np.float64)
+    n1, n2 = mR.shape
+    ci = (C.c_int * 4)(max_outer, max_inner, nt, ls_max_steps)
+    cd = (C.c_double * 6)(tol_rel, tol_abs, forcing_cap, ls_c1, ls_shrink, grad_cfl)
+    pi, pd = _pc_arrays(kind, coarse_solver, cheb_iters, eps_scale, eig)
+    v1, v2 = np.empty_like(mR), np.empty_like(mR)
+    rec = np.zeros((max_outer + 1, 12))
+    summ = np.zeros(7)
+    hp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    ctx.check(ctx.lib.vrg_newton_solve(ctx.h, n1, n2, hp(mR), hp(mT), norm, beta, deformation,
+                                       C.cast(ci, C.c_void_p), C.cast(cd, C.c_void_p), C.cast(pi, C.c_void_p),
+                                       C.cast(pd, C.c_void_p), hp(v1), hp(v2), hp(rec), max_outer + 1, hp(summ)))
+    k = int(summ[1])
+    records = [dict(zip(RECORD_FIELDS, row)) for row in rec[:k]]
+    summary = dict(status=int(summ[0]), iterations=k, finalGradNormRel=summ[2], finalResidualRel=summ[3],
+                   jacMin=summ[4], jacMax=summ[5], totalTimeSec=summ[6])
+    return v1, v2, records, summary

@@ -4,8 +4,10 @@
 #include <cstring>
 #include <map>
 
+#include <memory>
+
 #include "../../include/vrg.h"
-#include "inverse.cuh"
+#include "precond.cuh"
 
 struct vrg_ctx_s {
     vrg::Ctx ctx;
@@ -186,10 +188,12 @@ int vrg_axpy(vrg_ctx_t c, unsigned long long n, double a, const double* x, doubl
 int vrg_prefilter(vrg_ctx_t c, int n1, int n2, const double* u, double* coef) {
     return guarded(c, [&] {
         const auto g = dims(n1, n2);
-        double* tmp = c->ctx.scratchBuf(30, sizeof(double) * g.points());
+        double* tmp = c->ctx.scratchBuf(30, sizeof(double) * 2 * g.points());
+        double* padded = c->ctx.scratchBuf(33, sizeof(double) * vrg::paddedPoints(n1, n2));
         unsigned* flag = reinterpret_cast<unsigned*>(c->ctx.scratchBuf(31, 64));
         VRG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), c->ctx.stream));
-        vrg::launchPrefilter(c->ctx, g, u, coef, tmp, flag);
+        vrg::launchPrefilter(c->ctx, g, u, padded, tmp, flag);
+        vrg::launchUnpad(c->ctx, g, padded, coef);
         unsigned h = 0;
         VRG_CUDA(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, c->ctx.stream));
         c->ctx.sync();
@@ -202,7 +206,9 @@ int vrg_evaluate(vrg_ctx_t c, int n1, int n2, const double* coef, const double* 
         const auto g = dims(n1, n2);
         if (vrg::anyNonFinite(c->ctx, g.points(), x1, x2))
             throw vrg::InvalidArgument("evaluate: non-finite point coordinate");
-        vrg::launchEvaluate<1>(c->ctx, g, vrg::CoeffSet<1>{{coef}}, x1, x2, vrg::EpiStore1{nullptr, out});
+        double* padded = c->ctx.scratchBuf(33, sizeof(double) * vrg::paddedPoints(n1, n2));
+        vrg::launchPad(c->ctx, g, coef, padded);
+        vrg::launchEvaluate<1>(c->ctx, g, vrg::CoeffSet<1>{{padded}}, x1, x2, vrg::EpiStore1{nullptr, out});
         c->ctx.interps += 1;
         c->ctx.sync();
     });
@@ -220,11 +226,12 @@ int vrg_trace(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, d
         if (!(ht > 0.0)) throw vrg::InvalidArgument("traceCharacteristics: ht must be positive");
         if (vrg::anyNonFinite(c->ctx, g.points(), v1, v2))
             throw vrg::InvalidArgument("traceCharacteristics velocity: non-finite value");
-        double* cv = c->ctx.scratchBuf(32, sizeof(double) * 2 * g.points());
-        double* tmp = c->ctx.scratchBuf(30, sizeof(double) * g.points());
+        const std::size_t PN = vrg::paddedPoints(n1, n2);
+        double* cv = c->ctx.scratchBuf(32, sizeof(double) * 2 * PN);
+        double* tmp = c->ctx.scratchBuf(30, sizeof(double) * 2 * g.points());
         vrg::launchPrefilter(c->ctx, g, v1, cv, tmp, nullptr);
-        vrg::launchPrefilter(c->ctx, g, v2, cv + g.points(), tmp, nullptr);
-        vrg::launchTrace(c->ctx, g, v1, v2, cv, cv + g.points(), ht, direction, x1, x2);
+        vrg::launchPrefilter(c->ctx, g, v2, cv + PN, tmp, nullptr);
+        vrg::launchTrace(c->ctx, g, v1, v2, cv, cv + PN, ht, direction, x1, x2);
         c->ctx.interps += 2;
         c->ctx.sync();
     });
@@ -418,6 +425,183 @@ int vrg_evaluate_objective(vrg_ctx_t c, int n1, int n2, const double* v1, const 
         vrg::evaluateObjective(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation), nt, scalars,
                                nullptr);
         c->ctx.sync();
+    });
+}
+
+}  // extern "C"
+
+// ---- precond / newton (precond.hpp, newton.hpp)
+struct vrg_coarse_s {
+    vrg_ctx_s* owner;
+    std::unique_ptr<vrg::CoarseOperator> op;
+};
+
+namespace {
+
+vrg::PrecondChoice choiceOf(const int* pi, const double* pd) {
+    vrg::PrecondChoice c;
+    c.kind = pi[0] ? vrg::kPcTwoLevel : vrg::kPcReg;
+    c.coarseSolver = pi[1] ? vrg::kCoarseCheb : vrg::kCoarsePcg;
+    c.chebIters = pi[2];
+    c.hasEig = pi[3] != 0;
+    c.epsScale = pd[0];
+    c.eMin = pd[1];
+    c.eMax = pd[2];
+    return c;
+}
+
+// Contiguous [c0 | c1] copy of a vector field given as two pointers.
+const double* packed(vrg::Ctx& ctx, const vrg::GridDims& g, const double* a, const double* b, int slot) {
+    if (b == a + g.points()) return a;
+    double* p = ctx.scratchBuf(slot, sizeof(double) * 2 * g.points());
+    vrg::copy(ctx, g.points(), a, p);
+    vrg::copy(ctx, g.points(), b, p + g.points());
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vrg_random_bandlimited_field(vrg_ctx_t c, int n1, int n2, unsigned long long seed, double* out) {
+    return guarded(c, [&] {
+        vrg::randomBandLimitedField(c->ctx, dims(n1, n2), seed, out);
+        c->ctx.sync();
+    });
+}
+
+int vrg_coarse_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                      const double* mT, int norm, double beta, int deformation, double coarse_cfl, vrg_coarse_t* out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        const auto g = dims(n1, n2);
+        const double* v = v1 ? packed(c->ctx, g, v1, v2, 40) : nullptr;
+        auto op = std::make_unique<vrg::CoarseOperator>(c->ctx, g, v, mR, mT, modelOf(norm, beta, deformation),
+                                                        coarse_cfl);
+        *out = new vrg_coarse_s{c, std::move(op)};
+    });
+}
+
+void vrg_coarse_destroy(vrg_coarse_t c) { delete c; }
+
+int vrg_coarse_info(vrg_coarse_t c, int* n1c, int* n2c, int* nt) {
+    *n1c = c->op->gc.n1;
+    *n2c = c->op->gc.n2;
+    *nt = c->op->nt;
+    return VRG_OK;
+}
+
+int vrg_coarse_apply_split(vrg_coarse_t c, const double* s1, const double* s2, double* o1, double* o2) {
+    return guarded(c->owner, [&] { c->op->hess->applySplit(s1, s2, o1, o2); });
+}
+
+int vrg_two_level_apply(vrg_coarse_t c, const double* r1, const double* r2, int coarse_solver, int cheb_iters,
+                        double eps_scale, double outer_tol, double emin, double emax, double* o1, double* o2,
+                        int* fallback) {
+    return guarded(c->owner, [&] {
+        vrg::Ctx& ctx = c->owner->ctx;
+        const vrg::GridDims g = c->op->fine;
+        vrg::PrecondChoice pc;
+        pc.kind = vrg::kPcTwoLevel;
+        pc.coarseSolver = coarse_solver ? vrg::kCoarseCheb : vrg::kCoarsePcg;
+        pc.chebIters = cheb_iters;
+        pc.epsScale = eps_scale;
+        const double* r = packed(ctx, g, r1, r2, 41);
+        double* o = ctx.scratchBuf(42, sizeof(double) * 2 * g.points());
+        const bool ok = vrg::applyTwoLevel(ctx, g, r, *c->op, pc, outer_tol, emin, emax, o);
+        vrg::copy(ctx, g.points(), o, o1);
+        vrg::copy(ctx, g.points(), o + g.points(), o2);
+        ctx.sync();
+        if (fallback) *fallback = ok ? 0 : 1;
+    });
+}
+
+int vrg_estimate_eigs(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                      const double* mT, int norm, double beta, int deformation, double coarse_cfl,
+                      unsigned long long seed, double* emin, double* emax) {
+    return guarded(c, [&] {
+        const auto g = dims(n1, n2);
+        const double* v = v1 ? packed(c->ctx, g, v1, v2, 40) : nullptr;
+        const auto e = vrg::estimateEigsAt(c->ctx, g, v, mR, mT, modelOf(norm, beta, deformation), coarse_cfl, seed);
+        *emin = e.first;
+        *emax = e.second;
+    });
+}
+
+int vrg_solve_kkt(vrg_hess_t h, const double* rhs1, const double* rhs2, double tol, int max_iter, const int* pc_int,
+                  const double* pc_dbl, const double* mR, const double* mT, const double* v1, const double* v2,
+                  double coarse_cfl, double* sol1, double* sol2, double* result) {
+    return guarded(h->owner, [&] {
+        vrg::Ctx& ctx = h->hess.ctx;
+        const vrg::GridDims g = h->hess.g;
+        const double* rhs = packed(ctx, g, rhs1, rhs2, 41);
+        const double* v = packed(ctx, g, v1, v2, 40);
+        double* sol = ctx.scratchBuf(43, sizeof(double) * 2 * g.points());
+        const auto r = vrg::solveKkt(ctx, h->hess, rhs, tol, max_iter, choiceOf(pc_int, pc_dbl), mR, mT, v,
+                                     coarse_cfl, sol);
+        vrg::copy(ctx, g.points(), sol, sol1);
+        vrg::copy(ctx, g.points(), sol + g.points(), sol2);
+        ctx.sync();
+        result[0] = r.iterations;
+        result[1] = r.converged;
+        result[2] = r.negativeCurvature;
+        result[3] = r.relResidual;
+        result[4] = r.totalTimeSec;
+        result[5] = r.precondTimeSec;
+    });
+}
+
+int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const double* mT_host, int norm, double beta,
+                     int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
+                     const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
+                     double* summary) {
+    return guarded(c, [&] {
+        vrg::Ctx& ctx = c->ctx;
+        const auto g = dims(n1, n2);
+        const std::size_t N = g.points();
+        vrg::DBuf img(sizeof(double) * 2 * N), v(sizeof(double) * 2 * N);
+        VRG_CUDA(cudaMemcpyAsync(img.d(), mR_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+        VRG_CUDA(cudaMemcpyAsync(img.d() + N, mT_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+        vrg::NewtonConfig cfg;
+        cfg.maxOuterIter = cfg_int[0];
+        cfg.maxInnerIter = cfg_int[1];
+        cfg.ntOverride = cfg_int[2];
+        cfg.lsMaxSteps = cfg_int[3];
+        cfg.tolRelGrad = cfg_dbl[0];
+        cfg.tolAbsGrad = cfg_dbl[1];
+        cfg.forcingCap = cfg_dbl[2];
+        cfg.lsC1 = cfg_dbl[3];
+        cfg.lsShrink = cfg_dbl[4];
+        cfg.gradCfl = cfg_dbl[5];
+        const auto rep = vrg::newtonSolve(ctx, g, img.d(), img.d() + N, modelOf(norm, beta, deformation), cfg,
+                                          choiceOf(pc_int, pc_dbl), v.d());
+        VRG_CUDA(cudaMemcpyAsync(v1_host, v.d(), sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        VRG_CUDA(cudaMemcpyAsync(v2_host, v.d() + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        int k = 0;
+        for (const auto& it : rep.iterations) {
+            if (k >= records_cap) break;
+            double* r = records + 12 * k++;
+            r[0] = it.iter;
+            r[1] = it.gradNormInf;
+            r[2] = it.gradNormRel;
+            r[3] = it.objective;
+            r[4] = it.mismatch;
+            r[5] = it.innerIterations;
+            r[6] = it.lineSearchSteps;
+            r[7] = it.stepLength;
+            r[8] = it.searchDirDivRatio;
+            r[9] = it.wallTimeSec;
+            r[10] = static_cast<double>(it.ffts);
+            r[11] = static_cast<double>(it.interps);
+        }
+        summary[0] = rep.status;
+        summary[1] = static_cast<double>(rep.iterations.size());
+        summary[2] = rep.finalGradNormRel;
+        summary[3] = rep.finalResidualRel;
+        summary[4] = rep.jacMin;
+        summary[5] = rep.jacMax;
+        summary[6] = rep.totalTimeSec;
     });
 }
 

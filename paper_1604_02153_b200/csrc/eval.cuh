@@ -15,6 +15,7 @@ namespace vrg {
 
 constexpr int kEvalBlock = 256;
 
+// Coefficient fields in the periodically padded layout ((n1+3) x (n2+3), see cellBase).
 template <int NF>
 struct CoeffSet {
     const double* c[NF];
@@ -24,24 +25,26 @@ template <int NF, class Epi>
 __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const double* __restrict__ x1,
                                                          const double* __restrict__ x2, int n1, int n2, double h1,
                                                          double h2, Epi epi) {
-    const std::size_t N = static_cast<std::size_t>(n1) * n2;
-    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int N = n1 * n2;  // grids up to 2^31 points
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
     double guard = 0.0;
     if (p < N) {
-        int i1[4], i2[4];
         double w1[4], w2[4];
-        cellOf(__ldg(x1 + p), h1, n1, i1, w1);
-        cellOf(__ldg(x2 + p), h2, n2, i2, w2);
+        const int b1 = cellBase(__ldg(x1 + p), n1 * (1.0 / kTwoPi), n1, w1);  // 1/h = n / 2pi
+        const int b2 = cellBase(__ldg(x2 + p), n2 * (1.0 / kTwoPi), n2, w2);
+        const int PW = n2 + 3;
+        const int base = b1 * PW + b2;
         double val[NF];
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
+            const double* c0 = cs.c[f] + base;
             double acc = 0.0;
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-                const double* row = cs.c[f] + static_cast<std::size_t>(i1[a]) * n2;
+                const double* row = c0 + a * PW;
                 double rowAcc = 0.0;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * __ldg(row + i2[b]);
+                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * __ldg(row + b);
                 acc += w1[a] * rowAcc;
             }
             val[f] = acc;

@@ -157,17 +157,22 @@ __global__ void __launch_bounds__(kColBX* kColBY) k_prefilter_cols(const double*
 }
 
 // ------------------------------------------------------------------------------ fast path
-// Exact chunk-carry form (lines of length n, n % 16 == 0, n >= 32): each thread owns a chunk
-// of 16 samples held in registers and runs both recurrences with zero initial state:
+// Exact chunk-carry form for axes with n % 16 == 0 and n >= 32.  Each thread owns a chunk of
+// 16 samples and runs both recurrences from a zero state:
 //   A_k = f_k + z A_{k-1}  (A_{-1} = 0),   B_k = z (f_{k+1} + B_{k+1})  (B_15 = 0).
 // The true values are A_k + z^(k+1) c+ and B_k + z^(15-k) c-, with carries from the
-// neighbouring chunks of the same (periodic) line
-//   c+ = E[c-1] + z^16 E[c-2],                      E = A_15 of a chunk,
+// neighbouring chunks of the same periodic line
+//   c+ = E[c-1] + z^16 E[c-2],                               E = A_15 of a chunk,
 //   c- = z (F0[c+1] + P0[c+1]) + z^17 (F0[c+2] + P0[c+2]),   F0 = f_0, P0 = B_0,
-// exact up to z^32 ~ 5e-19 relative.  No warm-up work, every sample read once.
+// exact up to z^32 ~ 5e-19 relative.  A block filters a segment of R samples of `lines`
+// lines plus a 2-chunk halo on each side (periodic), so any segment is exact on its own.
+// Loads go global -> shared with cp.async (no register staging, full memory-level
+// parallelism); shared layout pads one slot per 16-chunk so the per-thread chunk walks are
+// bank-conflict free.
 constexpr int kL = 16;
+constexpr int kHalo = 2 * kL;
+constexpr int kLines = 8;
 
-// z^i, i = 0..17, folded to compile-time constants.
 struct ZPow {
     static constexpr double pw(int i) { return i == 0 ? 1.0 : kZ * pw(i - 1); }
     double p[18];
@@ -175,185 +180,206 @@ struct ZPow {
                                      pw(9), pw(10), pw(11), pw(12), pw(13), pw(14), pw(15), pw(16), pw(17)} {}
 };
 
-// Filters the 16 samples at s[0..15] (smem, contiguous) in place given the line's chunk tables.
-__device__ __forceinline__ void chunkPhase1(const double* s, double A[kL], double B[kL], double& e, double& f0,
-                                            double& p0) {
-    double f[kL];
-#pragma unroll
-    for (int k = 0; k < kL; ++k) f[k] = s[k];
-    B[kL - 1] = 0.0;
-#pragma unroll
-    for (int k = kL - 2; k >= 0; --k) B[k] = kZ * (f[k + 1] + B[k + 1]);
-    double p = 0.0;
-#pragma unroll
-    for (int k = 0; k < kL; ++k) {
-        p = f[k] + kZ * p;
-        A[k] = p;
-    }
-    e = A[kL - 1];
-    f0 = f[0];
-    p0 = B[0];
+__device__ __forceinline__ void cpAsync8(double* dst, const double* src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
 }
 
-__device__ __forceinline__ void chunkPhase2(double* s, const double A[kL], const double B[kL], double cp, double cm,
-                                            const ZPow& zp) {
-#pragma unroll
-    for (int k = 0; k < kL; ++k) s[k] = kSqrt3 * ((A[k] + zp.p[k + 1] * cp) + (B[k] + zp.p[kL - 1 - k] * cm));
+__device__ __forceinline__ void cpAsyncWaitAll() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-// Row pass: `rows` whole rows per block, row-major smem with one pad slot per 16-chunk.
-__global__ void __launch_bounds__(256) k_pf_rows(const double* __restrict__ u, double* __restrict__ out, int n1,
-                                                 int n2, int rows, unsigned* nonfinite) {
+__device__ __forceinline__ int wrapPos(int q, int n) {
+    // q in [-kHalo, n + kHalo); n >= 32 = kHalo
+    return q < 0 ? q + n : (q >= n ? q - n : q);
+}
+
+// kRows: lines are rows (positions along axis 1, contiguous); else lines are columns.
+// kPadOut (columns pass only): write the coefficients in the periodically padded layout
+// (n1+3) x (n2+3), padded(i+1, j+1) = c(i, j) with one wrap row/column before and two after,
+// which the evaluation kernels index without any wrap logic.
+template <bool kRows, bool kPadOut>
+__global__ void __launch_bounds__(256) k_pf_seg(const double* __restrict__ in, double* __restrict__ out, int n1,
+                                                int n2, int R, int LS, unsigned* nonfinite) {
     extern __shared__ double sm[];
-    const int nc = n2 / kL;
-    const int stride = n2 + nc;
-    double* E = sm + rows * stride;
-    double* F0 = E + rows * nc;
-    double* P0 = F0 + rows * nc;
-    const int row0 = blockIdx.x * rows;
-    const int nrows = min(rows, n1 - row0);
-    const int halfTotal = nrows * n2 / 2;
-    const double2* u2 = reinterpret_cast<const double2*>(u + static_cast<std::size_t>(row0) * n2);
+    const int n = kRows ? n2 : n1;          // line length
+    const int nLines = kRows ? n1 : n2;
+    const int S = R + 2 * kHalo;            // samples staged per line
+    const int nch = S / kL;                 // chunks per line segment
+    const int p0 = blockIdx.x * R;          // first interior position
+    const int l0 = blockIdx.y * kLines;
+    const int lines = min(kLines, nLines - l0);
+    double* E = sm + kLines * LS;
+    double* F0 = E + kLines * nch;
+    double* P0 = F0 + kLines * nch;
+
+    // stage: global -> shared (periodic halo), no per-element division
+    if (kRows) {
+        for (int l = 0; l < lines; ++l) {
+            const double* src = in + static_cast<std::size_t>(l0 + l) * n2;
+            double* dst = sm + l * LS;
+            for (int p = threadIdx.x; p < S; p += blockDim.x) cpAsync8(dst + p + (p >> 4), src + wrapPos(p0 - kHalo + p, n));
+        }
+    } else {
+        const int l = threadIdx.x & (kLines - 1);
+        if (l < lines) {
+            const double* src = in + l0 + l;
+            double* dst = sm + l * LS;
+            for (int p = threadIdx.x >> 3; p < S; p += blockDim.x >> 3)
+                cpAsync8(dst + p + (p >> 4), src + static_cast<std::size_t>(wrapPos(p0 - kHalo + p, n)) * n2);
+        }
+    }
+    cpAsyncWaitAll();
+    __syncthreads();
+
+    // phase 1: zero-state recurrences per chunk
+    const int t = threadIdx.x;
+    const int l = t / nch, c = t - l * nch;
+    const bool active = l < lines;
+    double A[kL], B[kL];
+    double* s = sm + l * LS + c * (kL + 1);
     bool bad = false;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < halfTotal; idx += blockDim.x) {
-        const double2 v = u2[idx];
-        const int i = 2 * idx;
-        const int r = i / n2, col = i - r * n2;
-        double* d = sm + r * stride + col + col / kL;
-        d[0] = v.x;
-        d[1] = v.y;
-        bad |= !isfinite(v.x) || !isfinite(v.y);
+    if (active) {
+        double f[kL];
+#pragma unroll
+        for (int k = 0; k < kL; ++k) {
+            f[k] = s[k];
+            bad |= !isfinite(f[k]);
+        }
+        B[kL - 1] = 0.0;
+#pragma unroll
+        for (int k = kL - 2; k >= 0; --k) B[k] = kZ * (f[k + 1] + B[k + 1]);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < kL; ++k) {
+            acc = f[k] + kZ * acc;
+            A[k] = acc;
+        }
+        E[t] = A[kL - 1];
+        F0[t] = f[0];
+        P0[t] = B[0];
     }
     if (nonfinite) {
         if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
     } else {
         __syncthreads();
     }
-    const int t = threadIdx.x;
-    const int r = t / nc, c = t - r * nc;
-    const bool active = r < nrows;
-    double A[kL], B[kL];
-    double* s = sm + r * stride + c * (kL + 1);
-    if (active) chunkPhase1(s, A, B, E[t], F0[t], P0[t]);
-    __syncthreads();
-    if (active) {
+    // phase 2: carries + fix-up for the interior chunks
+    if (active && c >= 2 && c < nch - 2) {
         const ZPow zp;
-        const int base = r * nc;
-        const int cm1 = c == 0 ? nc - 1 : c - 1, cm2 = cm1 == 0 ? nc - 1 : cm1 - 1;
-        const int cp1 = c == nc - 1 ? 0 : c + 1, cp2 = cp1 == nc - 1 ? 0 : cp1 + 1;
-        const double carryP = E[base + cm1] + zp.p[kL] * E[base + cm2];
-        const double carryM = kZ * (F0[base + cp1] + P0[base + cp1]) + zp.p[kL + 1] * (F0[base + cp2] + P0[base + cp2]);
-        chunkPhase2(s, A, B, carryP, carryM, zp);
+        const int b = l * nch;
+        const double cp = E[b + c - 1] + zp.p[kL] * E[b + c - 2];
+        const double cm = kZ * (F0[b + c + 1] + P0[b + c + 1]) + zp.p[kL + 1] * (F0[b + c + 2] + P0[b + c + 2]);
+#pragma unroll
+        for (int k = 0; k < kL; ++k) s[k] = kSqrt3 * ((A[k] + zp.p[k + 1] * cp) + (B[k] + zp.p[kL - 1 - k] * cm));
     }
     __syncthreads();
-    double2* o2 = reinterpret_cast<double2*>(out + static_cast<std::size_t>(row0) * n2);
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < halfTotal; idx += blockDim.x) {
-        const int i = 2 * idx;
-        const int rr = i / n2, col = i - rr * n2;
-        const double* d = sm + rr * stride + col + col / kL;
-        o2[idx] = make_double2(d[0], d[1]);
+    // store the interior
+    if (kRows) {
+        for (int ll = 0; ll < lines; ++ll) {
+            double* dst = out + static_cast<std::size_t>(l0 + ll) * n2 + p0;
+            const double* src = sm + ll * LS;
+            for (int p = threadIdx.x; p < R; p += blockDim.x) {
+                const int ps = p + kHalo;
+                dst[p] = src[ps + (ps >> 4)];
+            }
+        }
+    } else {
+        const int ll = threadIdx.x & (kLines - 1);
+        if (ll < lines) {
+            const double* src = sm + ll * LS;
+            const int col = l0 + ll;
+            if (kPadOut) {
+                const int PW = n2 + 3;
+                const int colX = col == n2 - 1 ? 0 : (col == 0 ? n2 + 1 : (col == 1 ? n2 + 2 : -1));
+                for (int p = threadIdx.x >> 3; p < R; p += blockDim.x >> 3) {
+                    const int ps = p + kHalo;
+                    const double v = src[ps + (ps >> 4)];
+                    const int q = p0 + p;
+                    const int rowX = q == n1 - 1 ? 0 : (q == 0 ? n1 + 1 : (q == 1 ? n1 + 2 : -1));
+                    double* r1 = out + static_cast<std::size_t>(q + 1) * PW;
+                    r1[col + 1] = v;
+                    if (colX >= 0) r1[colX] = v;
+                    if (rowX >= 0) {
+                        double* r2 = out + static_cast<std::size_t>(rowX) * PW;
+                        r2[col + 1] = v;
+                        if (colX >= 0) r2[colX] = v;
+                    }
+                }
+            } else {
+                for (int p = threadIdx.x >> 3; p < R; p += blockDim.x >> 3) {
+                    const int ps = p + kHalo;
+                    out[static_cast<std::size_t>(p0 + p) * n2 + col] = src[ps + (ps >> 4)];
+                }
+            }
+        }
     }
 }
 
-// Column pass: `W` whole columns per block, column-major smem (one pad per 16-chunk, column
-// stride = 4 mod 16 double-banks so the tile loads are conflict-free).
-__global__ void __launch_bounds__(512, 1) k_pf_cols(const double* __restrict__ in, double* __restrict__ out, int n1,
-                                                  int n2, int W, int colStride) {
-    extern __shared__ double sm[];
-    const int nc = n1 / kL;
-    double* E = sm + W * colStride;
-    double* F0 = E + W * nc;
-    double* P0 = F0 + W * nc;
-    const int c0 = blockIdx.x * W;
-    const int ncols = min(W, n2 - c0);
-    const int total = n1 * W;
-#pragma unroll 8
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int row = idx / W, w = idx - row * W;
-        if (w < ncols) sm[w * colStride + row + row / kL] = in[static_cast<std::size_t>(row) * n2 + c0 + w];
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    const int w = t / nc, c = t - w * nc;
-    const bool active = w < ncols;
-    double A[kL], B[kL];
-    double* s = sm + w * colStride + c * (kL + 1);
-    if (active) chunkPhase1(s, A, B, E[t], F0[t], P0[t]);
-    __syncthreads();
-    if (active) {
-        const ZPow zp;
-        const int base = w * nc;
-        const int cm1 = c == 0 ? nc - 1 : c - 1, cm2 = cm1 == 0 ? nc - 1 : cm1 - 1;
-        const int cp1 = c == nc - 1 ? 0 : c + 1, cp2 = cp1 == nc - 1 ? 0 : cp1 + 1;
-        const double carryP = E[base + cm1] + zp.p[kL] * E[base + cm2];
-        const double carryM = kZ * (F0[base + cp1] + P0[base + cp1]) + zp.p[kL + 1] * (F0[base + cp2] + P0[base + cp2]);
-        chunkPhase2(s, A, B, carryP, carryM, zp);
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int row = idx / W, ww = idx - row * W;
-        if (ww < ncols) out[static_cast<std::size_t>(row) * n2 + c0 + ww] = sm[ww * colStride + row + row / kL];
-    }
+// Periodic padding of an unpadded field (for coefficient sets that arrive unpadded).
+__global__ void k_pad(const double* __restrict__ c, double* __restrict__ out, int n1, int n2) {
+    const int PW = n2 + 3, PH = n1 + 3;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (j >= PW || i >= PH) return;
+    int si = i - 1, sj = j - 1;
+    si = si < 0 ? si + n1 : (si >= n1 ? si - n1 : si);
+    sj = sj < 0 ? sj + n2 : (sj >= n2 ? sj - n2 : sj);
+    out[static_cast<std::size_t>(i) * PW + j] = c[static_cast<std::size_t>(si) * n2 + sj];
 }
 
-struct FastPlan {
-    int rows = 0, rowThreads = 0;
-    std::size_t rowSmem = 0;
-    int W = 0, colThreads = 0, colStride = 0;
-    std::size_t colSmem = 0;
+__global__ void k_unpad(const double* __restrict__ pc, double* __restrict__ out, int n1, int n2) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (j >= n2) return;
+    out[static_cast<std::size_t>(i) * n2 + j] = pc[static_cast<std::size_t>(i + 1) * (n2 + 3) + j + 1];
+}
+
+struct SegPlan {
+    int R = 0, LS = 0, threads = 0;
+    std::size_t smem = 0;
+    bool ok = false;
 };
 
-bool fastAxis(int n) { return n >= 32 && n % kL == 0 && n <= 16384; }
-
-FastPlan fastPlan(const GridDims& g) {
-    FastPlan p;
-    const int nc2 = g.n2 / kL;
-    p.rows = std::max(1, 256 / nc2);
-    p.rowThreads = p.rows * nc2;
-    p.rowSmem = sizeof(double) * (static_cast<std::size_t>(p.rows) * (g.n2 + nc2) + 3 * p.rows * nc2);
-    const int nc1 = g.n1 / kL;
-    p.W = std::max(2, 4096 / g.n1);
-    p.colThreads = p.W * nc1;
-    const int base = g.n1 + nc1;
-    p.colStride = base + ((4 - base % 16) + 16) % 16;
-    p.colSmem = sizeof(double) * (static_cast<std::size_t>(p.W) * p.colStride + 3 * p.W * nc1);
+SegPlan segPlan(int n) {
+    SegPlan p;
+    if (n < 32 || n % kL != 0) return p;
+    for (int r = 256; r >= kL; r -= kL)
+        if (n % r == 0) {
+            p.R = r;
+            break;
+        }
+    const int nch = (p.R + 2 * kHalo) / kL;
+    const int base = nch * (kL + 1);
+    p.LS = base + ((2 - base % 16) + 16) % 16;  // line stride = 2 mod 16 (conflict-free column loads)
+    p.threads = kLines * nch;
+    p.smem = sizeof(double) * (static_cast<std::size_t>(kLines) * p.LS + 3 * kLines * nch);
+    p.ok = p.threads <= 256;
     return p;
 }
 
 }  // namespace
 
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite) {
-    static std::mutex mu0;
-    static std::vector<bool> attr0(64, false);
-    {
-        std::lock_guard<std::mutex> lock(mu0);
-        if (!attr0[ctx.device]) {
-            VRG_CUDA(cudaFuncSetAttribute(k_pf_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            VRG_CUDA(cudaFuncSetAttribute(k_pf_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr0[ctx.device] = true;
+    const SegPlan pr = segPlan(g.n2), pc = segPlan(g.n1);
+    if (pr.ok && pc.ok) {
+        {
+            LaunchScope ls_(ctx, "k_prefilter_rows");
+            k_pf_seg<true, false>
+                <<<dim3(g.n2 / pr.R, (g.n1 + kLines - 1) / kLines), pr.threads, pr.smem, ctx.stream>>>(
+                    u, tmp, g.n1, g.n2, pr.R, pr.LS, nonfinite);
         }
-    }
-    if (fastAxis(g.n1) && fastAxis(g.n2)) {
-        const FastPlan p = fastPlan(g);
-        if (p.rowThreads <= 256 && p.colThreads <= 512 && p.rowSmem <= 200 * 1024 && p.colSmem <= 200 * 1024) {
-            {
-                LaunchScope ls_(ctx, "k_prefilter_rows");
-                k_pf_rows<<<(g.n1 + p.rows - 1) / p.rows, p.rowThreads, p.rowSmem, ctx.stream>>>(u, tmp, g.n1, g.n2,
-                                                                                                 p.rows, nonfinite);
-            }
-            VRG_LAUNCH_CHECK();
-            {
-                LaunchScope ls_(ctx, "k_prefilter_cols");
-                k_pf_cols<<<(g.n2 + p.W - 1) / p.W, p.colThreads, p.colSmem, ctx.stream>>>(tmp, c, g.n1, g.n2, p.W,
-                                                                                           p.colStride);
-            }
-            VRG_LAUNCH_CHECK();
-            return;
+        VRG_LAUNCH_CHECK();
+        {
+            LaunchScope ls_(ctx, "k_prefilter_cols");
+            k_pf_seg<false, true>
+                <<<dim3(g.n1 / pc.R, (g.n2 + kLines - 1) / kLines), pc.threads, pc.smem, ctx.stream>>>(
+                    tmp, c, g.n1, g.n2, pc.R, pc.LS, nullptr);
         }
+        VRG_LAUNCH_CHECK();
+        return;
     }
+    double* tmp2 = tmp + g.points();  // unpadded column-pass output of the generic path
     // generic path (small or non-multiple-of-16 axes): warm-up recurrences
     const int chunks = (g.n2 + kChunk - 1) / kChunk;
     if (chunks > kRowThreads) throw NotSupported("prefilter: n2 > 8192 not supported");
@@ -379,7 +405,24 @@ void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, do
     dim3 grid((g.n2 + kColBX - 1) / kColBX, (g.n1 + kColRows - 1) / kColRows);
     {
         LaunchScope ls_(ctx, "k_prefilter_cols");
-        k_prefilter_cols<<<grid, dim3(kColBX, kColBY), smemCols, ctx.stream>>>(tmp, c, g.n1, g.n2);
+        k_prefilter_cols<<<grid, dim3(kColBX, kColBY), smemCols, ctx.stream>>>(tmp, tmp2, g.n1, g.n2);
+    }
+    VRG_LAUNCH_CHECK();
+    launchPad(ctx, g, tmp2, c);
+}
+
+void launchPad(Ctx& ctx, const GridDims& g, const double* c, double* padded) {
+    {
+        LaunchScope ls_(ctx, "k_pad");
+        k_pad<<<dim3((g.n2 + 3 + 127) / 128, g.n1 + 3), 128, 0, ctx.stream>>>(c, padded, g.n1, g.n2);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void launchUnpad(Ctx& ctx, const GridDims& g, const double* padded, double* c) {
+    {
+        LaunchScope ls_(ctx, "k_unpad");
+        k_unpad<<<dim3((g.n2 + 127) / 128, g.n1), 128, 0, ctx.stream>>>(padded, c, g.n1, g.n2);
     }
     VRG_LAUNCH_CHECK();
 }

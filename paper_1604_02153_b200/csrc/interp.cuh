@@ -20,25 +20,29 @@ constexpr int kWarm = 28;
 constexpr int kChunk = 32;
 
 // Launches the two prefilter passes (rows of length n2, then columns of length n1) on
-// ctx.stream: c = P u.  `tmp` holds n1*n2 doubles.  If `nonfinite` is non-null, a non-finite
-// input value sets *nonfinite = 1 (checkFinite(u, "prefilter"), src/interp.cpp:76).
+// ctx.stream: c = P u, written in the periodically padded layout of paddedPoints(n1, n2)
+// doubles (see cellBase).  `tmp` holds 2*n1*n2 doubles.  If `nonfinite` is non-null, a
+// non-finite input value sets *nonfinite = 1 (checkFinite(u, "prefilter"), interp.cpp:76).
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite);
 
-// B-spline weights, src/interp.cpp:59-65.
+// B-spline weights, src/interp.cpp:59-65 (the /6 as a multiply by 1/6: <= 1 ulp apart).
 __device__ __forceinline__ void bsplineWeights(double f, double w[4]) {
+    constexpr double k6 = 1.0 / 6.0;
     const double f2 = f * f, f3 = f2 * f;
-    w[0] = (1.0 - 3.0 * f + 3.0 * f2 - f3) / 6.0;
-    w[1] = (3.0 * f3 - 6.0 * f2 + 4.0) / 6.0;
-    w[2] = (-3.0 * f3 + 3.0 * f2 + 3.0 * f + 1.0) / 6.0;
-    w[3] = f3 / 6.0;
+    w[0] = (1.0 - 3.0 * f + 3.0 * f2 - f3) * k6;
+    w[1] = (3.0 * f3 - 6.0 * f2 + 4.0) * k6;
+    w[2] = (-3.0 * f3 + 3.0 * f2 + 3.0 * f + 1.0) * k6;
+    w[3] = f3 * k6;
 }
 
 // Cell index and fractional offset of a coordinate along one axis, src/interp.cpp:100-109.
-// The wrap x - 2 pi floor((x+pi)/2pi) uses round-to-nearest multiply/subtract (no FMA) so the
-// wrapped coordinate is bit-identical to the reference's.
-__device__ __forceinline__ void cellOf(double x, double h, int n, int idx[4], double w[4]) {
-    const double xw = __dsub_rn(x, __dmul_rn(kTwoPi, floor(__dadd_rn(x, kPi) / kTwoPi)));
-    const double s = __dadd_rn(xw, kPi) / h;
+// The reference divides by 2pi and by h; here both are multiplies by the reciprocals
+// (`invh` = 1/h), which moves s by at most an ulp — the spline is C2 across cell and wrap
+// boundaries, so a flipped floor() changes the value only at rounding level.
+__device__ __forceinline__ void cellOf(double x, double invh, int n, int idx[4], double w[4]) {
+    constexpr double kInv2Pi = 1.0 / kTwoPi;
+    const double xw = __dsub_rn(x, __dmul_rn(kTwoPi, floor(__dadd_rn(x, kPi) * kInv2Pi)));
+    const double s = __dadd_rn(xw, kPi) * invh;
     const double bf = floor(s);
     bsplineWeights(s - bf, w);
     int b = static_cast<int>(bf) - 1;
@@ -50,5 +54,26 @@ __device__ __forceinline__ void cellOf(double x, double h, int n, int idx[4], do
         b = (b + 1 == n) ? 0 : b + 1;
     }
 }
+
+// Same cell computation for the periodically padded coefficient layout ((n1+3) x (n2+3),
+// padded(i+1, j+1) = c(i, j)): returns the padded index of the first tap, taps are
+// first + 0..3 along the axis with no wrap.
+__device__ __forceinline__ int cellBase(double x, double invh, int n, double w[4]) {
+    constexpr double kInv2Pi = 1.0 / kTwoPi;
+    const double xw = __dsub_rn(x, __dmul_rn(kTwoPi, floor(__dadd_rn(x, kPi) * kInv2Pi)));
+    const double s = __dadd_rn(xw, kPi) * invh;
+    const double bf = floor(s);
+    bsplineWeights(s - bf, w);
+    const int b = static_cast<int>(bf);  // in [0, n] for finite wrapped points
+    return b >= n ? b - n : (b < 0 ? 0 : b);
+}
+
+constexpr std::size_t paddedPoints(int n1, int n2) {
+    return static_cast<std::size_t>(n1 + 3) * static_cast<std::size_t>(n2 + 3);
+}
+
+// Pads / unpads a coefficient field (used at the C ABI, whose coefficients are unpadded).
+void launchPad(Ctx& ctx, const GridDims& g, const double* c, double* padded);
+void launchUnpad(Ctx& ctx, const GridDims& g, const double* padded, double* c);
 
 }  // namespace vrg

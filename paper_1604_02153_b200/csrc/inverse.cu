@@ -93,8 +93,8 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     GD_.alloc(sizeof(double) * nt * 2 * N);
     for (int j = 0; j <= nt; ++j) gradient(ctx, g, state_.d() + j * N, G_.d() + j * 2 * N, G_.d() + j * 2 * N + N);
     const double* Xf = solver.departure(kForward);
-    work_.alloc(sizeof(double) * 13 * N);
-    double* c2 = work_.d() + 8 * N;
+    work_.alloc(sizeof(double) * (11 * N + paddedPoints(g.n1, g.n2)));
+    double* c2 = work_.d() + 11 * N;
     for (int j = 1; j <= nt; ++j) {
         const double* gp = G_.d() + (j - 1) * 2 * N;
         launchPrefilter(ctx, g, gp, solver.coef(), solver.tmp(), nullptr);
@@ -114,6 +114,11 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     adjLog_.ensure(nt + 1, evalBlocks(g));
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
+    // every plan a matvec uses exists before any graph capture (plan creation allocates)
+    for (int batch = 1; batch <= 2; ++batch) {
+        ctx.plan(g, CUFFT_D2Z, batch);
+        ctx.plan(g, CUFFT_Z2D, batch);
+    }
     ctx.sync();
 }
 
@@ -131,7 +136,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     double* vtD = work_.d();
     double* mt[2] = {vtD + 2 * N, vtD + 3 * N};
     double* lam[2] = {vtD + 4 * N, vtD + 5 * N};
-    double* c2 = vtD + 8 * N;
+    double* c2 = vtD + 11 * N;  // padded coefficients of the second component
     const double* Xf = solver.departure(kForward);
     const double* Xb = solver.departure(kBackward);
     const double* dv = solver.divVelocity();
@@ -171,7 +176,52 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
 
 void Hessian::checkLastGuard() { adjLog_.check(ctx, "adjoint", nt, false, true, nt); }
 
+// The launch sequence of one matvec is fixed for given (kind, in, out) pointers, so it is
+// captured once into a CUDA graph and replayed (removes ~100 launch gaps per matvec).  The
+// host-side work (counters, guard readback) stays outside the graph.
+template <class F>
+void Hessian::replay(int kind, const double* a, const double* b, const double* c, const double* d, F&& launchSeq) {
+    if (ctx.profOn || !useGraphs) {
+        launchSeq();
+        return;
+    }
+    const GraphKey key{kind, a, b, c, d};
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+        const long long l0 = ctx.launches;
+        cudaGraph_t graph = nullptr;
+        VRG_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            launchSeq();
+        } catch (...) {
+            cudaStreamEndCapture(ctx.stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            ctx.launches = l0;
+            throw;
+        }
+        VRG_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
+        cudaGraphExec_t exec = nullptr;
+        VRG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        it = graphs_.emplace(key, std::make_pair(exec, ctx.launches - l0)).first;
+        ctx.launches = l0;
+    }
+    VRG_CUDA(cudaGraphLaunch(it->second.first, ctx.stream));
+    ctx.launches += it->second.second;
+}
+
+Hessian::~Hessian() {
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.first);
+}
+
 void Hessian::apply(const double* vt1, const double* vt2, double* o1, double* o2) {
+    replay(0, vt1, vt2, o1, o2, [&] { launchApply(vt1, vt2, o1, o2); });
+    ctx.ffts += 4;
+    countDataTerm();
+    checkLastGuard();
+}
+
+void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, double* o2) {
     const std::size_t N = g.points();
     double* b = work_.d() + 6 * N;
     double* reg = work_.d() + 9 * N;
@@ -208,27 +258,40 @@ void Hessian::apply(const double* vt1, const double* vt2, double* o1, double* o2
         fftInverse(ctx, g, S, reg, 2);
         dataTerm(vt1, vt2, b, b + N, reg, reg + N, o1, o2);
     }
-    ctx.ffts += 4;
-    countDataTerm();
-    checkLastGuard();
 }
 
 void Hessian::applyDataTerm(const double* vt1, const double* vt2, double* o1, double* o2) {
-    const std::size_t N = g.points();
-    double* b = work_.d() + 6 * N;
-    dataTerm(vt1, vt2, b, b + N, nullptr, nullptr, nullptr, nullptr);
-    if (model.deformation == kIncompressible) {
-        projectDivFree(ctx, g, b, b + N, o1, o2);
-        ctx.ffts -= 4;  // counted in countDataTerm
-    } else {
-        copy(ctx, N, b, o1);
-        copy(ctx, N, b + N, o2);
-    }
+    replay(1, vt1, vt2, o1, o2, [&] {
+        const std::size_t N = g.points();
+        double* b = work_.d() + 6 * N;
+        dataTerm(vt1, vt2, b, b + N, nullptr, nullptr, nullptr, nullptr);
+        if (model.deformation == kIncompressible) {
+            cplx* T = spec_.as<cplx>() + 2 * g.specPoints();
+            fftForward(ctx, g, b, T, 2);
+            specCombine(ctx, g, T, T + g.specPoints(), nullptr, nullptr, nullptr, true, 1.0 / N, T, T + g.specPoints());
+            if (o2 == o1 + N) {
+                fftInverse(ctx, g, T, o1, 2);
+            } else {
+                fftInverse(ctx, g, T, o1, 1);
+                fftInverse(ctx, g, T + g.specPoints(), o2, 1);
+            }
+        } else {
+            copy(ctx, N, b, o1);
+            copy(ctx, N, b + N, o2);
+        }
+    });
     countDataTerm();
     checkLastGuard();
 }
 
 void Hessian::applySplit(const double* s1, const double* s2, double* o1, double* o2) {
+    replay(2, s1, s2, o1, o2, [&] { launchSplit(s1, s2, o1, o2); });
+    ctx.ffts += 8;
+    countDataTerm();
+    checkLastGuard();
+}
+
+void Hessian::launchSplit(const double* s1, const double* s2, double* o1, double* o2) {
     const std::size_t N = g.points();
     const std::size_t NS = g.specPoints();
     cplx* S = spec_.as<cplx>();      // s^ (kept)
@@ -253,9 +316,6 @@ void Hessian::applySplit(const double* s1, const double* s2, double* o1, double*
         fftInverse(ctx, g, T, o1, 1);
         fftInverse(ctx, g, T + NS, o2, 1);
     }
-    ctx.ffts += 8;
-    countDataTerm();
-    checkLastGuard();
 }
 
 // ------------------------------------------------------------------------------ gradient / objective

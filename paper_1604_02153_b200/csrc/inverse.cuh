@@ -44,7 +44,12 @@ public:
     // out = M^{-1/2} Q M^{-1/2} s + s  (applySplitHessianOf, precond.cpp:20-26)
     void applySplit(const double* s1, const double* s2, double* o1, double* o2);
 
+    ~Hessian();
+    Hessian(const Hessian&) = delete;
+    Hessian& operator=(const Hessian&) = delete;
+
     const double* state() const { return state_.d(); }
+    bool useGraphs = true;
     // device-visible guard check result of the last data term (throws like solveAdjoint).
     void checkLastGuard();
     // counter increments of one data term in the reference (steady state)
@@ -55,6 +60,17 @@ private:
     // If regOut1/2 non-null, the last step also writes out = reg + b (compressible fusion).
     void dataTerm(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                   const double* reg2, double* out1, double* out2);
+
+    void launchApply(const double* vt1, const double* vt2, double* o1, double* o2);
+    void launchSplit(const double* s1, const double* s2, double* o1, double* o2);
+    template <class F>
+    void replay(int kind, const double* a, const double* b, const double* c, const double* d, F&& launchSeq);
+    struct GraphKey {
+        int kind;
+        const double *a, *b, *c, *d;
+        bool operator<(const GraphKey& o) const { return std::tie(kind, a, b, c, d) < std::tie(o.kind, o.a, o.b, o.c, o.d); }
+    };
+    std::map<GraphKey, std::pair<cudaGraphExec_t, long long>> graphs_;
 
     DBuf state_;  // (nt+1) N
     DBuf G_;      // (nt+1) x [g1 | g2]

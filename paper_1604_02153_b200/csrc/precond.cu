@@ -1,0 +1,562 @@
+// Device-resident two-level preconditioner, Chebyshev / PCG / Lanczos and the inexact
+// Gauss-Newton-Krylov driver.  Host control flow mirrors src/precond.cpp and src/newton.cpp
+// line for line (same decisions, same comparisons); all vectors and operator applications
+// stay on the device.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "precond.cuh"
+
+namespace vrg {
+
+namespace {
+
+constexpr double kEmaxInflation = 1.05;  // precond.cpp:18
+
+__device__ __forceinline__ int waveOfP(int idx, int n) { return idx <= n / 2 ? idx : idx - n; }
+
+// problems.cpp:94-105: zero the top third of the spectrum (|k_i| >= n_i/3), with the 1/N of
+// the inverse transform folded in.
+__global__ void k_bandlimit(double2* s, int n1, int n2, double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const bool cut = abs(waveOfP(r, n1)) >= n1 / 3 || abs(waveOfP(c, n2)) >= n2 / 3;
+    s[i] = cut ? make_double2(0.0, 0.0) : make_double2(s[i].x * scale, s[i].y * scale);
+}
+
+// Two-level restriction (cutoffFilter Low + resample to the half grid, precond.cpp:266-268):
+// coarse spectrum = amp * fine spectrum on |k_i| < n_i^c / 2, times 1/N_c.
+__global__ void k_restrict_low(const double2* __restrict__ f, int n1f, int n2f, double2* __restrict__ c, int n1c,
+                               int n2c, double amp, double scale) {
+    const int ncc = n2c / 2 + 1, ncf = n2f / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1c) * ncc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int rt = static_cast<int>(i / ncc), col = static_cast<int>(i - static_cast<std::size_t>(rt) * ncc);
+    const int k1 = waveOfP(rt, n1c), k2 = waveOfP(col, n2c);
+    double2 v = make_double2(0.0, 0.0);
+    // low band of the fine cut-off (|k_i| < n_i^f/4) intersected with the resample band
+    if (abs(k1) < n1c / 2 && abs(k2) < n2c / 2 && abs(k1) < n1f / 4 && abs(k2) < n2f / 4) {
+        const int rs = k1 >= 0 ? k1 : k1 + n1f;
+        const double2 s = f[static_cast<std::size_t>(rs) * ncf + col];
+        v = make_double2(s.x * amp, s.y * amp);
+    }
+    c[i] = make_double2(v.x * scale, v.y * scale);
+}
+
+// out^ = (prolong(sc^) * amp + highpass(r^)) * scale on the fine half spectrum
+// (resample(sc, fine) + cutoffFilter(r, High), precond.cpp:267, 286-287).
+__global__ void k_prolong_add_high(const double2* __restrict__ sc, int n1c, int n2c, const double2* __restrict__ rf,
+                                   double2* __restrict__ out, int n1f, int n2f, double amp, double scale) {
+    const int ncc = n2c / 2 + 1, ncf = n2f / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1f) * ncf;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int rt = static_cast<int>(i / ncf), col = static_cast<int>(i - static_cast<std::size_t>(rt) * ncf);
+    const int k1 = waveOfP(rt, n1f), k2 = waveOfP(col, n2f);
+    double2 v = make_double2(0.0, 0.0);
+    if (abs(k1) < n1c / 2 && abs(k2) < n2c / 2) {
+        const int rs = k1 >= 0 ? k1 : k1 + n1c;
+        const double2 s = sc[static_cast<std::size_t>(rs) * ncc + col];
+        v = make_double2(s.x * amp, s.y * amp);
+    }
+    const bool low = abs(k1) < n1f / 4 && abs(k2) < n2f / 4;
+    if (!low) {
+        v.x += rf[i].x;
+        v.y += rf[i].y;
+    }
+    out[i] = make_double2(v.x * scale, v.y * scale);
+}
+
+unsigned specBlocks(const GridDims& g) { return static_cast<unsigned>((g.specPoints() + 255) / 256); }
+
+double secondsSince(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ vector BLAS
+double vdot(Ctx& ctx, const GridDims& g, const double* a, const double* b) {
+    const std::size_t N = g.points();
+    return dot(ctx, g, a, a + N, b, b + N);
+}
+
+double vnormL2(Ctx& ctx, const GridDims& g, const double* a) { return std::sqrt(vdot(ctx, g, a, a)); }
+
+double vnormLinf(Ctx& ctx, const GridDims& g, const double* a) {
+    const std::size_t N = g.points();
+    return normLinf(ctx, N, a, a + N);
+}
+
+// ------------------------------------------------------------------------------ random probes
+void randomBandLimitedField(Ctx& ctx, const GridDims& g, std::uint64_t seed, double* out) {
+    const std::size_t N = g.points();
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    std::vector<double> noise(N);
+    for (double& x : noise) x = gauss(rng);
+    VRG_CUDA(cudaMemcpyAsync(out, noise.data(), sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+    cplx* s = specScratch(ctx, g, 4, 1);
+    fftForward(ctx, g, out, s, 1);
+    {
+        LaunchScope ls_(ctx, "k_bandlimit");
+        k_bandlimit<<<specBlocks(g), 256, 0, ctx.stream>>>(s, g.n1, g.n2, 1.0 / N);
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, g, s, out, 1);
+    ctx.ffts += 2;
+    const double m = normLinf(ctx, N, out);  // synchronises: `noise` may go out of scope
+    if (m > 0.0) axpby(ctx, N, 0.0, out, 1.0 / m, out);
+}
+
+void randomBandLimitedVelocity(Ctx& ctx, const GridDims& g, std::uint64_t seed, double* out) {
+    randomBandLimitedField(ctx, g, seed, out);
+    randomBandLimitedField(ctx, g, seed ^ 0x9e3779b97f4a7c15ull, out + g.points());
+}
+
+// ------------------------------------------------------------------------------ coarse operator
+CoarseOperator::CoarseOperator(Ctx& c, const GridDims& fg, const double* v, const double* mR, const double* mT,
+                               const Model& model, double coarseCfl)
+    : ctx(c), fine(fg), gc(fg.n1 / 2, fg.n2 / 2) {
+    checkGrid(gc.n1, gc.n2);
+    const std::size_t Nc = gc.points(), Nf = fine.points();
+    mRc.alloc(sizeof(double) * Nc);
+    mTc.alloc(sizeof(double) * Nc);
+    vc.alloc(sizeof(double) * 2 * Nc);
+    resample(ctx, fine, mR, gc, mRc.d());
+    resample(ctx, fine, mT, gc, mTc.d());
+    if (v) {
+        resample(ctx, fine, v, gc, vc.d());
+        resample(ctx, fine, v + Nf, gc, vc.d() + Nc);
+    } else {
+        fill(ctx, 2 * Nc, 0.0, vc.d());
+        ctx.ffts += 4;  // the reference resamples the zero velocity too
+    }
+    nt = deriveSteps(ctx, gc, vc.d(), vc.d() + Nc, coarseCfl);
+    hess = std::make_unique<Hessian>(ctx, gc, vc.d(), vc.d() + Nc, mRc.d(), mTc.d(), model, nt, nullptr);
+}
+
+// ------------------------------------------------------------------------------ Chebyshev / PCG
+void chebyshevSolve(Ctx& ctx, const GridDims& g, const LinOpDev& op, const double* rhs, int k, double eMin,
+                    double eMax, double* x) {
+    if (!(eMax > eMin) || !(eMin > 0.0)) throw InvalidArgument("chebyshevSolve: need eMax > eMin > 0");
+    const std::size_t n = 2 * g.points();
+    fill(ctx, n, 0.0, x);
+    if (k <= 0) return;
+    const double theta = 0.5 * (eMax + eMin);
+    const double delta = 0.5 * (eMax - eMin);
+    const double sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    double* r = ctx.scratchBuf(120, sizeof(double) * n);
+    double* d = ctx.scratchBuf(121, sizeof(double) * n);
+    double* ad = ctx.scratchBuf(122, sizeof(double) * n);
+    copy(ctx, n, rhs, r);
+    lincomb(ctx, n, 1.0 / theta, r, 0.0, r, d);
+    for (int it = 1; it <= k; ++it) {
+        if (it > 1) {
+            const double rhoNew = 1.0 / (2.0 * sigma - rho);
+            lincomb(ctx, n, rhoNew * rho, d, 2.0 * rhoNew / delta, r, d);
+            rho = rhoNew;
+        }
+        axpby(ctx, n, 1.0, d, 1.0, x);
+        op(d, ad);
+        axpby(ctx, n, -1.0, ad, 1.0, r);
+    }
+}
+
+PcgOut pcg(Ctx& ctx, const GridDims& g, const LinOpDev& A, const double* b, const LinOpDev* M, double tol,
+           int maxIter, double* x) {
+    PcgOut out;
+    const std::size_t n = 2 * g.points();
+    const int base = M ? 100 : 110;  // fine (preconditioned) and coarse PCG use separate buffers
+    double* r = ctx.scratchBuf(base + 0, sizeof(double) * n);
+    double* z = M ? ctx.scratchBuf(base + 1, sizeof(double) * n) : r;
+    double* p = ctx.scratchBuf(base + 2, sizeof(double) * n);
+    double* ap = ctx.scratchBuf(base + 3, sizeof(double) * n);
+    fill(ctx, n, 0.0, x);
+    copy(ctx, n, b, r);
+    if (M) (*M)(r, z);
+    double rz = vdot(ctx, g, r, z);
+    if (rz < 0.0 || !std::isfinite(rz)) {
+        out.indefinitePreconditioner = true;
+        return out;
+    }
+    const double norm0 = std::sqrt(std::max(rz, 0.0));
+    if (!(norm0 > 0.0)) {
+        out.converged = true;
+        return out;
+    }
+    copy(ctx, n, z, p);
+    for (int it = 0; it < maxIter; ++it) {
+        A(p, ap);
+        const double pAp = vdot(ctx, g, p, ap);
+        if (!(pAp > 0.0)) {
+            out.negativeCurvature = true;
+            out.relResidual = std::sqrt(std::max(rz, 0.0)) / norm0;
+            return out;
+        }
+        const double alpha = rz / pAp;
+        axpby(ctx, n, alpha, p, 1.0, x);
+        axpby(ctx, n, -alpha, ap, 1.0, r);
+        if (M) (*M)(r, z);
+        const double rzNew = vdot(ctx, g, r, z);
+        out.iterations = it + 1;
+        if (rzNew < 0.0 || !std::isfinite(rzNew)) {
+            out.indefinitePreconditioner = true;
+            return out;
+        }
+        out.relResidual = std::sqrt(rzNew) / norm0;
+        if (out.relResidual <= tol) {
+            out.converged = true;
+            return out;
+        }
+        const double beta = rzNew / rz;
+        rz = rzNew;
+        lincomb(ctx, n, beta, p, 1.0, z, p);
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------------------ Lanczos
+double tridiagMaxEig(const std::vector<double>& alpha, const std::vector<double>& beta) {
+    const int m = static_cast<int>(alpha.size());
+    if (m == 1) return alpha[0];
+    double lo = alpha[0], hi = alpha[0];
+    for (int i = 0; i < m; ++i) {
+        const double off = (i > 0 ? std::abs(beta[i - 1]) : 0.0) + (i < m - 1 ? std::abs(beta[i]) : 0.0);
+        lo = std::min(lo, alpha[i] - off);
+        hi = std::max(hi, alpha[i] + off);
+    }
+    auto countBelow = [&](double x) {
+        int count = 0;
+        double d = 1.0;
+        for (int i = 0; i < m; ++i) {
+            const double offsq = i > 0 ? beta[i - 1] * beta[i - 1] : 0.0;
+            d = alpha[i] - x - offsq / d;
+            if (d == 0.0) d = -1e-300;
+            if (d < 0.0) ++count;
+        }
+        return count;
+    };
+    for (int it = 0; it < 100; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (countBelow(mid) >= m)
+            hi = mid;
+        else
+            lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+static double powerIterationEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op, std::uint64_t seed) {
+    const std::size_t n = 2 * g.points();
+    DBuf qb(sizeof(double) * n), wb(sizeof(double) * n);
+    double* q = qb.d();
+    double* w = wb.d();
+    randomBandLimitedVelocity(ctx, g, seed, q);
+    double lambda = 1.0;
+    const double nq = vnormL2(ctx, g, q);
+    axpby(ctx, n, 0.0, q, 1.0 / nq, q);
+    for (int it = 0; it < 50; ++it) {
+        op(q, w);
+        lambda = vdot(ctx, g, q, w);
+        const double nw = vnormL2(ctx, g, w);
+        if (!(nw > 0.0)) break;
+        axpby(ctx, n, 0.0, w, 1.0 / nw, w);
+        std::swap(q, w);
+    }
+    return lambda;
+}
+
+double lanczosEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, std::uint64_t seed) {
+    const std::size_t n = 2 * g.points();
+    DBuf basisBuf(sizeof(double) * n * (steps + 1));
+    DBuf wBuf(sizeof(double) * n);
+    auto Q = [&](int j) { return basisBuf.d() + static_cast<std::size_t>(j) * n; };
+    double* w = wBuf.d();
+    std::vector<double> alpha, beta;
+    randomBandLimitedVelocity(ctx, g, seed, Q(0));
+    const double nq = vnormL2(ctx, g, Q(0));
+    if (!(nq > 0.0)) return 1.0;
+    axpby(ctx, n, 0.0, Q(0), 1.0 / nq, Q(0));
+    int nb = 1;
+    for (int j = 0; j < steps; ++j) {
+        op(Q(j), w);
+        if (j > 0) axpby(ctx, n, -beta[j - 1], Q(j - 1), 1.0, w);
+        const double a = vdot(ctx, g, w, Q(j));
+        alpha.push_back(a);
+        axpby(ctx, n, -a, Q(j), 1.0, w);
+        for (int i = 0; i < nb; ++i) axpby(ctx, n, -vdot(ctx, g, w, Q(i)), Q(i), 1.0, w);  // full reorth.
+        const double b = vnormL2(ctx, g, w);
+        if (!std::isfinite(b)) return powerIterationEmax(ctx, g, op, seed ^ 0x1234567);
+        if (b < 1e-12) break;
+        beta.push_back(b);
+        lincomb(ctx, n, 1.0 / b, w, 0.0, w, Q(nb));
+        ++nb;
+    }
+    if (alpha.empty()) return powerIterationEmax(ctx, g, op, seed ^ 0x1234567);
+    beta.resize(alpha.size() - 1);
+    return tridiagMaxEig(alpha, beta);
+}
+
+std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const double* v, const double* mR,
+                                         const double* mT, const Model& model, double coarseCfl, std::uint64_t seed) {
+    CoarseOperator coarse(ctx, g, v, mR, mT, model, coarseCfl);
+    LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
+    return {1.0, lanczosEmax(ctx, coarse.gc, op, 30, seed)};
+}
+
+// ------------------------------------------------------------------------------ two-level
+bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator& coarse, const PrecondChoice& choice,
+                   double outerTol, double eMin, double eMax, double* out) {
+    const GridDims& gc = coarse.gc;
+    const std::size_t N = g.points(), Nc = gc.points(), NS = g.specPoints(), NSc = gc.specPoints();
+    cplx* R = specScratch(ctx, g, 5, 2);    // fine spectra of r (both components)
+    cplx* C = specScratch(ctx, gc, 6, 2);   // coarse spectra
+    double* rc = ctx.scratchBuf(130, sizeof(double) * 2 * Nc);
+    double* sc = ctx.scratchBuf(131, sizeof(double) * 2 * Nc);
+    const double ampDown = static_cast<double>(Nc) / static_cast<double>(N);
+    for (int i = 0; i < 2; ++i) {
+        fftForward(ctx, g, r + i * N, R + i * NS, 1);
+        {
+            LaunchScope ls_(ctx, "k_restrict_low");
+            k_restrict_low<<<specBlocks(gc), 256, 0, ctx.stream>>>(R + i * NS, g.n1, g.n2, C + i * NSc, gc.n1, gc.n2,
+                                                                   ampDown, 1.0 / Nc);
+        }
+        VRG_LAUNCH_CHECK();
+        fftInverse(ctx, gc, C + i * NSc, rc + i * Nc, 1);
+    }
+    LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
+    if (choice.coarseSolver == kCoarseCheb) {
+        chebyshevSolve(ctx, gc, op, rc, choice.chebIters, eMin, kEmaxInflation * eMax, sc);
+    } else {
+        pcg(ctx, gc, op, rc, nullptr, choice.epsScale * outerTol, 500, sc);
+    }
+    // reference counting: cutoff Low/High (8 FFTs) + restrict (4); prolong (4) below
+    ctx.ffts += 12;
+    if (anyNonFinite(ctx, 2 * Nc, sc)) {
+        std::fprintf(stderr, "precond: coarse solve diverged, falling back to identity\n");
+        copy(ctx, 2 * N, r, out);
+        return false;
+    }
+    const double ampUp = static_cast<double>(N) / static_cast<double>(Nc);
+    for (int i = 0; i < 2; ++i) {
+        fftForward(ctx, gc, sc + i * Nc, C + i * NSc, 1);
+        {
+            LaunchScope ls_(ctx, "k_prolong_add_high");
+            k_prolong_add_high<<<specBlocks(g), 256, 0, ctx.stream>>>(C + i * NSc, gc.n1, gc.n2, R + i * NS, R + i * NS,
+                                                                      g.n1, g.n2, ampUp, 1.0 / N);
+        }
+        VRG_LAUNCH_CHECK();
+        fftInverse(ctx, g, R + i * NS, out + i * N, 1);
+    }
+    ctx.ffts += 4;
+    return true;
+}
+
+// ------------------------------------------------------------------------------ KKT
+KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int maxIter, const PrecondChoice& choice,
+                   const double* mR, const double* mT, const double* v, double coarseCfl, double* solution) {
+    if (choice.kind == kPcTwoLevel) {
+        if (choice.coarseSolver == kCoarsePcg && !(choice.epsScale > 0.0 && choice.epsScale < 1.0))
+            throw InvalidArgument("solveKkt: epsScale must lie in (0,1)");
+        if (choice.coarseSolver == kCoarseCheb && choice.chebIters < 1)
+            throw InvalidArgument("solveKkt: chebIters must be >= 1");
+        if (choice.hasEig && !(choice.eMax > choice.eMin && choice.eMin > 0.0))
+            throw InvalidArgument("solveKkt: need eMax > eMin > 0");
+    }
+    const GridDims& g = hess.g;
+    const std::size_t N = g.points();
+    const auto t0 = std::chrono::steady_clock::now();
+    double precondTime = 0.0;
+    const double* invHalf = hess.weights.invRegSymbol(hess.model.betaV, -0.5);
+    double* rhsSplit = ctx.scratchBuf(140, sizeof(double) * 2 * N);
+    double* x = ctx.scratchBuf(141, sizeof(double) * 2 * N);
+    applyRealSymbol(ctx, g, rhs, rhs + N, rhsSplit, rhsSplit + N, invHalf);
+    LinOpDev A = [&](const double* s, double* o) { hess.applySplit(s, s + N, o, o + N); };
+
+    std::unique_ptr<CoarseOperator> coarse;
+    double eMin = 1.0, eMax = 10.0;
+    LinOpDev M;
+    if (choice.kind == kPcTwoLevel) {
+        coarse = std::make_unique<CoarseOperator>(ctx, g, v, mR, mT, hess.model, coarseCfl);
+        if (choice.coarseSolver == kCoarseCheb) {
+            if (choice.hasEig) {
+                eMin = choice.eMin;
+                eMax = choice.eMax;
+            } else {
+                std::tie(eMin, eMax) = estimateEigsAt(ctx, g, nullptr, mR, mT, hess.model, coarseCfl);
+            }
+        }
+        M = [&](const double* r, double* z) {
+            const auto tp = std::chrono::steady_clock::now();
+            applyTwoLevel(ctx, g, r, *coarse, choice, tol, eMin, eMax, z);
+            precondTime += secondsSince(tp);
+        };
+    }
+    PcgOut out = pcg(ctx, g, A, rhsSplit, M ? &M : nullptr, tol, maxIter, x);
+    if (out.indefinitePreconditioner && choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb) {
+        LinOpDev op = [&](const double* s, double* o) { coarse->applySplit(s, o); };
+        eMax = lanczosEmax(ctx, coarse->gc, op, 30, 0x5eed);
+        std::fprintf(stderr, "precond: re-estimated Chebyshev bound eMax=%.6g after breakdown\n", eMax);
+        out = pcg(ctx, g, A, rhsSplit, &M, tol, maxIter, x);
+    }
+    applyRealSymbol(ctx, g, x, x + N, solution, solution + N, invHalf);
+    KktResult res;
+    res.iterations = out.iterations;
+    res.negativeCurvature = out.negativeCurvature;
+    res.converged = out.converged;
+    res.relResidual = out.relResidual;
+    res.totalTimeSec = secondsSince(t0);
+    res.precondTimeSec = precondTime;
+    return res;
+}
+
+// ------------------------------------------------------------------------------ Newton
+SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const double* mT, const Model& model,
+                         const NewtonConfig& cfg, const PrecondChoice& pc, double* vOut) {
+    const std::size_t N = g.points();
+    const auto tStart = std::chrono::steady_clock::now();
+    const long long f0 = ctx.ffts, i0 = ctx.interps;
+    SolverReport report;
+    Weights weights(g, model.norm);
+    DBuf vBuf(sizeof(double) * 2 * N), trialBuf(sizeof(double) * 2 * N), gBuf(sizeof(double) * 2 * N),
+        dvBuf(sizeof(double) * 2 * N), tmpBuf(sizeof(double) * 2 * N);
+    double* v = vBuf.d();
+    fill(ctx, 2 * N, 0.0, v);  // zero initial guess
+
+    PrecondChoice choice = pc;
+    if (choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb && !choice.hasEig &&
+        !choice.reestimateEachIteration) {
+        std::tie(choice.eMin, choice.eMax) = estimateEigsAt(ctx, g, nullptr, mR, mT, model, kCoarseCfl);
+        choice.hasEig = true;
+    }
+
+    double g0inf = 0.0;
+    int ntRatchet = 0;
+    int carriedNt = -1;
+    DBuf carried, state, adjoint;
+    DBuf finalDeformed(sizeof(double) * N);
+    copy(ctx, N, mT, finalDeformed.d());
+    double scal[3];
+
+    for (int iter = 0; iter < cfg.maxOuterIter; ++iter) {
+        const auto tIter = std::chrono::steady_clock::now();
+        ntRatchet = std::max(ntRatchet, cfg.ntOverride > 0 ? cfg.ntOverride
+                                                          : deriveSteps(ctx, g, v, v + N, cfg.gradCfl));
+        const int nt = ntRatchet;
+        state.alloc(sizeof(double) * (nt + 1) * N);
+        adjoint.alloc(sizeof(double) * (nt + 1) * N);
+        const bool reuse = carriedNt == nt;
+        evaluateGradient(ctx, g, v, v + N, mR, mT, model, nt, gBuf.d(), gBuf.d() + N, scal, state.d(), adjoint.d(),
+                         reuse ? carried.d() : nullptr);
+        const double objective = scal[0], mismatch = scal[1];
+        copy(ctx, N, state.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
+
+        const double ginf = vnormLinf(ctx, g, gBuf.d());
+        if (iter == 0) g0inf = std::max(ginf, 1e-300);
+        const double grel = ginf / g0inf;
+
+        IterationRecord rec;
+        rec.iter = iter;
+        rec.gradNormInf = ginf;
+        rec.gradNormRel = grel;
+        rec.objective = objective;
+        rec.mismatch = mismatch;
+        rec.ffts = ctx.ffts - f0;
+        rec.interps = ctx.interps - i0;
+
+        report.finalGradNormRel = grel;
+        if (grel <= cfg.tolRelGrad || ginf <= cfg.tolAbsGrad) {
+            rec.wallTimeSec = secondsSince(tIter);
+            report.iterations.push_back(rec);
+            report.status = kConverged;
+            break;
+        }
+
+        const double eta = std::min(cfg.forcingCap, std::sqrt(grel));
+        Hessian hess(ctx, g, v, v + N, mR, mT, model, nt, state.d());
+        // rhs = -g
+        lincomb(ctx, 2 * N, -1.0, gBuf.d(), 0.0, gBuf.d(), tmpBuf.d());
+        KktResult kkt = solveKkt(ctx, hess, tmpBuf.d(), eta, cfg.maxInnerIter, choice, mR, mT, v, kCoarseCfl,
+                                 dvBuf.d());
+        rec.innerIterations = kkt.iterations;
+        double* dv = dvBuf.d();
+
+        double gdotd = vdot(ctx, g, gBuf.d(), dv);
+        if (!std::isfinite(gdotd) || gdotd >= 0.0) {
+            // inner solve broke down: Sobolev-gradient fallback direction
+            applyRealSymbol(ctx, g, gBuf.d(), gBuf.d() + N, dv, dv + N, weights.invRegSymbol(model.betaV, -1.0));
+            axpby(ctx, 2 * N, 0.0, dv, -1.0, dv);
+            gdotd = vdot(ctx, g, gBuf.d(), dv);
+        }
+        divergence(ctx, g, dv, dv + N, tmpBuf.d());
+        rec.searchDirDivRatio = normLinf(ctx, N, tmpBuf.d()) / std::max(vnormLinf(ctx, g, dv), 1e-300);
+
+        // Armijo backtracking on the objective at this iteration's time grid
+        double alpha = 1.0;
+        bool accepted = false;
+        int lsSteps = 0;
+        if (!carried || carried.bytes() < sizeof(double) * (nt + 1) * N) carried.alloc(sizeof(double) * (nt + 1) * N);
+        for (; lsSteps < cfg.lsMaxSteps; ++lsSteps) {
+            lincomb(ctx, 2 * N, 1.0, v, alpha, dv, trialBuf.d());
+            bool blewUp = false;
+            double ob[3] = {0, 0, 0};
+            try {
+                evaluateObjective(ctx, g, trialBuf.d(), trialBuf.d() + N, mR, mT, model, nt, ob, carried.d());
+            } catch (const BlowupError&) {
+                blewUp = true;
+            }
+            if (!blewUp && ob[0] <= objective + cfg.lsC1 * alpha * gdotd) {
+                copy(ctx, 2 * N, trialBuf.d(), v);
+                carriedNt = nt;
+                copy(ctx, N, carried.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
+                accepted = true;
+                break;
+            }
+            alpha *= cfg.lsShrink;
+        }
+        if (!accepted) carriedNt = -1;
+        rec.lineSearchSteps = lsSteps + (accepted ? 1 : 0);
+        rec.stepLength = accepted ? alpha : 0.0;
+        rec.wallTimeSec = secondsSince(tIter);
+        rec.ffts = ctx.ffts - f0;
+        rec.interps = ctx.interps - i0;
+        report.iterations.push_back(rec);
+        if (!accepted) {
+            report.status = kLineSearchFailure;
+            break;
+        }
+        if (iter + 1 == cfg.maxOuterIter) report.status = kIterationLimit;
+    }
+
+    // final diagnostics (newton.cpp:147-157)
+    lincomb(ctx, N, 1.0, mT, -1.0, mR, tmpBuf.d());
+    const double residDenom = std::sqrt(dot(ctx, g, tmpBuf.d(), nullptr, tmpBuf.d(), nullptr));
+    lincomb(ctx, N, 1.0, finalDeformed.d(), -1.0, mR, tmpBuf.d());
+    const double residNum = std::sqrt(dot(ctx, g, tmpBuf.d(), nullptr, tmpBuf.d(), nullptr));
+    report.finalResidualRel = residDenom > 0.0 ? residNum / residDenom : 0.0;
+    {
+        const int ntJ = deriveSteps(ctx, g, v, v + N, 0.2);
+        Solver js(ctx, g, v, v + N, ntJ);
+        js.jacobian(tmpBuf.d());
+        std::vector<double> jac(N);
+        VRG_CUDA(cudaMemcpyAsync(jac.data(), tmpBuf.d(), sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        report.jacMin = *std::min_element(jac.begin(), jac.end());
+        report.jacMax = *std::max_element(jac.begin(), jac.end());
+    }
+    copy(ctx, 2 * N, v, vOut);
+    ctx.sync();
+    report.totalTimeSec = secondsSince(tStart);
+    return report;
+}
+
+}  // namespace vrg

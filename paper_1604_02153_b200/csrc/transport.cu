@@ -145,8 +145,8 @@ Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2,
     copy(ctx, g.points(), vv1, v.d());
     copy(ctx, g.points(), vv2, v.d() + g.points());
     if (anyNonFinite(ctx, 2 * g.points(), v.d())) throw InvalidArgument("transport velocity: non-finite value");
-    coef_.alloc(sizeof(double) * g.points());
-    tmp_.alloc(sizeof(double) * g.points());
+    coef_.alloc(sizeof(double) * paddedPoints(g.n1, g.n2));
+    tmp_.alloc(sizeof(double) * 2 * g.points());
     log.ensure(nt + 1, evalBlocks(g));
 }
 
@@ -156,13 +156,14 @@ double* Solver::tmp() { return tmp_.d(); }
 const double* Solver::departure(int dir) {
     if (!haveX_[dir]) {
         if (!haveCv_) {
-            cv_.alloc(sizeof(double) * 2 * g.points());
+            cv_.alloc(sizeof(double) * 2 * paddedPoints(g.n1, g.n2));
             launchPrefilter(ctx, g, v1(), cv_.d(), tmp_.d(), nullptr);
-            launchPrefilter(ctx, g, v2(), cv_.d() + g.points(), tmp_.d(), nullptr);
+            launchPrefilter(ctx, g, v2(), cv_.d() + paddedPoints(g.n1, g.n2), tmp_.d(), nullptr);
             haveCv_ = true;
         }
         X_[dir].alloc(sizeof(double) * 2 * g.points());
-        launchTrace(ctx, g, v1(), v2(), cv_.d(), cv_.d() + g.points(), ht, dir, X_[dir].d(), X_[dir].d() + g.points());
+        launchTrace(ctx, g, v1(), v2(), cv_.d(), cv_.d() + paddedPoints(g.n1, g.n2), ht, dir, X_[dir].d(),
+                    X_[dir].d() + g.points());
         ctx.interps += 2;  // traceCharacteristics evaluates both components (transport.cpp:77-78)
         haveX_[dir] = true;
     }
@@ -269,7 +270,7 @@ void Solver::incState(const double* vt1, const double* vt2, const double* stateT
     double* gPrev = vtD + 2 * N;     // grad m_{j-1}
     double* gCur = gPrev + 2 * N;    // grad m_j
     double* gD = gCur + 2 * N;       // (grad m_{j-1})_D
-    double* c2 = ctx.scratchBuf(13, sizeof(double) * N);
+    double* c2 = ctx.scratchBuf(13, sizeof(double) * paddedPoints(g.n1, g.n2));
     launchPrefilter(ctx, g, vt1, coef_.d(), tmp_.d(), nullptr);
     launchPrefilter(ctx, g, vt2, c2, tmp_.d(), nullptr);
     launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, vtD, vtD + N});

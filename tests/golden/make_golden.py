@@ -94,8 +94,52 @@ def case_interp_spectral():
     return d
 
 
+NEWTON_RUNS = {
+    # name: (n, nt, norm, beta, deformation, chebyshev coarse solver)
+    "cfg1": (64, 4, 2, 1e-2, 0, False),          # config 1: 2L + nested PCG (eps 0.1)
+    "cfg2": (256, 8, 1, 1e-3, 0, True),          # config 2: 2L + CHEB(10)
+    "cfg2_incomp": (256, 8, 1, 1e-3, 1, True),   # config 2, div v = 0
+}
+
+
+def case_newton():
+    """Full inexact GN-Krylov registrations (newtonSolve) of configs 1 and 2, tolRelGrad 1e-2."""
+    d = {}
+    for name, (n, nt, norm, beta, deform, cheb) in NEWTON_RUNS.items():
+        mT, (v1, v2) = synth.config12_fields(n)
+        mR = ref.solve_state_final(v1, v2, nt, mT)
+        a, b, rep, s = ref.newton_solve(mR, mT, norm, beta, deform, nt=nt, two_level=True, cheb=cheb,
+                                        cheb_iters=10, tol_rel=1e-2)
+        d[name + "_records"] = rep
+        d[name + "_summary"] = s
+        d[name + "_v1"] = a
+        d[name + "_v2"] = b
+        d[name + "_meta"] = np.array([n, nt, norm, beta, deform, int(cheb)])
+    return d
+
+
+def case_precond():
+    """Two-level preconditioner and Lanczos estimate at 64^2 (config 1 problem, iterate 0.6 v*)."""
+    n, nt, beta = 64, 4, 1e-2
+    mT, (v1, v2) = synth.config12_fields(n)
+    mR = ref.solve_state_final(v1, v2, nt, mT)
+    w1, w2 = 0.6 * v1, 0.6 * v2
+    r1, r2 = synth.smooth_velocity(n, n, 3002)
+    c = ref.Coarse(w1, w2, mR, mT, 2, beta, 0)
+    emin, emax = ref.estimate_eigs(mR, mT, 2, beta, 0)
+    d = {"mR": mR, "mT": mT, "w1": w1, "w2": w2, "r1": r1, "r2": r2, "eig": np.array([emin, emax])}
+    d["cheb1"], d["cheb2"] = c.two_level(r1, r2, 1, 10, 0.1, 0.5, emin, emax)
+    d["pcg1"], d["pcg2"] = c.two_level(r1, r2, 0, 10, 0.1, 0.5, emin, emax)
+    s1, s2 = ref.random_bandlimited_velocity(n // 2, n // 2, 5)
+    d["s1"], d["s2"] = s1, s2
+    d["split1"], d["split2"] = c.split_apply(s1, s2)
+    d["rbl_coarse_0x5eed"] = ref.random_bandlimited_field(n // 2, n // 2, 0x5EED)
+    return d
+
+
 def main():
-    for name, fn in [("cfg1_64", case_cfg1), ("incomp_64", case_incompressible), ("interp_48x32", case_interp_spectral)]:
+    for name, fn in [("cfg1_64", case_cfg1), ("incomp_64", case_incompressible), ("interp_48x32", case_interp_spectral),
+                     ("precond_64", case_precond), ("newton", case_newton)]:
         d = fn()
         np.savez_compressed(os.path.join(OUT, name + ".npz"), **d)
         print(name, sorted(d))

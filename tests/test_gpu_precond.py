@@ -1,0 +1,95 @@
+"""GPU parity of the device-resident preconditioner / Krylov layer and the full inexact
+Gauss-Newton-Krylov registration against the unmodified reference (golden vectors from
+oracle/_ref, tests/golden/make_golden.py).
+
+north_star bars: identical Newton and Krylov iteration counts; final objective and gradient
+norm within 1e-8 relative.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def gold(name):
+    return dict(np.load(os.path.join(GOLD, name + ".npz")))
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1604_02153_b200 import api as A
+
+    return A
+
+
+def test_random_bandlimited_probe(ctx, api):
+    # the Lanczos probe: libstdc++ mt19937_64 + normal_distribution, band limited (problems.cpp:87-118)
+    d = gold("precond_64")
+    f = api.random_bandlimited_field(ctx, (32, 32), 0x5EED)
+    assert rel(f, d["rbl_coarse_0x5eed"]) < 1e-13
+
+
+def test_coarse_split_and_two_level(ctx, api):
+    d = gold("precond_64")
+    F = ctx.field
+    c = api.CoarseOperator(ctx, (F(d["w1"]), F(d["w2"])), F(d["mR"]), F(d["mT"]), api.H2SEMI, 1e-2, api.COMPRESSIBLE)
+    assert c.shape == (32, 32)
+    s1, s2 = c.apply_split((F(d["s1"]), F(d["s2"])))
+    assert rel(s1, d["split1"]) < 1e-10 and rel(s2, d["split2"]) < 1e-10
+    emin, emax = d["eig"]
+    r = (F(d["r1"]), F(d["r2"]))
+    (o1, o2), fb = c.two_level(r, api.COARSE_CHEB, 10, 0.1, 0.5, emin, emax)
+    assert not fb
+    assert rel(o1, d["cheb1"]) < 1e-9 and rel(o2, d["cheb2"]) < 1e-9
+    (p1, p2), fb = c.two_level(r, api.COARSE_PCG, 10, 0.1, 0.5, emin, emax)
+    assert rel(p1, d["pcg1"]) < 1e-9 and rel(p2, d["pcg2"]) < 1e-9
+
+
+def test_estimate_eigs(ctx, api):
+    d = gold("precond_64")
+    F = ctx.field
+    emin, emax = api.estimate_eigs(ctx, F(d["mR"]), F(d["mT"]), api.H2SEMI, 1e-2, api.COMPRESSIBLE)
+    assert emin == 1.0
+    assert abs(emax - d["eig"][1]) <= 1e-9 * d["eig"][1]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg2_incomp"])
+def test_newton_registration_parity(ctx, api, name):
+    from paper_1604_02153_b200 import synth
+    from oracle import veloreg_np as O
+
+    d = gold("newton")
+    n, nt, norm, beta, deform, cheb = d[name + "_meta"]
+    n, nt, norm, deform = int(n), int(nt), int(norm), int(deform)
+    mT, (v1, v2) = synth.config12_fields(n)
+    mR = O.Solver(v1, v2, nt).solve_state(mT)[-1]
+    # the reference images were built by the reference's own SL forward solve
+    assert np.abs(mR - O.Solver(v1, v2, nt).solve_state(mT)[-1]).max() == 0.0
+    w1, w2, recs, summ = api.newton_solve(ctx, mR, mT, norm, beta, deform, nt=nt, kind=api.PC_TWO_LEVEL,
+                                          coarse_solver=api.COARSE_CHEB if cheb else api.COARSE_PCG, cheb_iters=10,
+                                          tol_rel=1e-2)
+    ref_recs, ref_summ = d[name + "_records"], d[name + "_summary"]
+    # identical Newton iteration count, Krylov (inner) iterations and line-search steps
+    assert summ["status"] == int(ref_summ[0])
+    assert summ["iterations"] == int(ref_summ[1])
+    for r, q in zip(recs, ref_recs):
+        assert r["innerIterations"] == int(q[5]), (r, q)
+        assert r["lineSearchSteps"] == int(q[6]), (r, q)
+        assert r["stepLength"] == q[7]
+        assert abs(r["objective"] - q[3]) <= 1e-8 * abs(q[3])
+        assert abs(r["gradNormInf"] - q[1]) <= 1e-8 * abs(q[1])
+    # final objective and gradient norm within 1e-8 relative
+    assert abs(summ["finalGradNormRel"] - ref_summ[2]) <= 1e-8 * ref_summ[2]
+    assert abs(summ["finalResidualRel"] - ref_summ[3]) <= 1e-8 * ref_summ[3]
+    assert abs(summ["jacMin"] - ref_summ[4]) <= 1e-8 and abs(summ["jacMax"] - ref_summ[5]) <= 1e-8
+    assert rel(w1, d[name + "_v1"]) < 1e-7 and rel(w2, d[name + "_v2"]) < 1e-7
