@@ -22,6 +22,7 @@ iterate (batched pairs): no data-path collective, weak scaling.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -126,6 +127,16 @@ KERNEL_BYTES_F = {
 }
 
 
+# Kernel classes of one matvec (vrg_hess_bench_kernel ids): name, launches per matvec at nt,
+# algorithmic bytes per launch in F.
+KERNEL_CLASSES = {
+    0: ("evaluate/incstate (K6)", NT - 1, 12),
+    1: ("evaluate/adjoint_bodyforce (K5+K8)", NT, 12),
+    2: ("prefilter rows+cols (K1)", 2 * NT + 1, 4),
+    3: ("evaluate/store2 (K2, vt_D)", 1, 6),
+}
+
+
 def matvec_algorithmic_bytes(nt: int = NT) -> int:
     """B_mv = (24 nt + 12) F."""
     return (24 * nt + 12) * F_BYTES
@@ -203,10 +214,19 @@ def run_vrg(args, rank, world, local_rank):
     prof = profile_dump(ctx)
     ctx.lib.vrg_profile(ctx.h, 0)
 
+    # back-to-back timing of each matvec kernel class (roofline denominator)
+    kernels = {}
+    for kid, (name, per_mv, bytes_f) in KERNEL_CLASSES.items():
+        out_ms = ctypes.c_double()
+        ctx.check(ctx.lib.vrg_hess_bench_kernel(H.h, kid, 50, ctypes.byref(out_ms)))
+        kernels[name] = {"avg_us": out_ms.value * 1e3, "launches_per_matvec": per_mv,
+                         "bytes_per_launch": bytes_f * F_BYTES,
+                         "gbps": bytes_f * F_BYTES / (out_ms.value / 1e3) / 1e9}
+
     # SL transport unit: one SL state step m_j = I[m_{j-1}](X_D) at 1024^2 (config 4 unit ii)
     sl = sl_step_rate(api, ctx, v_d, mT_d, timed)
     return dict(value=value, ms=ms, launches=launches, clocks=clk, e2e=e2e_value, ms_e2e=ms_e2e,
-                wall_e2e=wall_e2e, prof=prof, sl=sl)
+                wall_e2e=wall_e2e, prof=prof, sl=sl, kernels=kernels)
 
 
 def ctypes_launches(ctx):
@@ -365,10 +385,11 @@ def main():
     r = run_vrg(args, rank, world, local_rank)
     if rank == 0:
         prof = r["prof"]
-        dom = max(prof.items(), key=lambda kv: kv[1][1])
-        tag, (cnt, tot_ms) = dom
-        avg_s = tot_ms / cnt / 1e3
-        bytes_launch = KERNEL_BYTES_F.get(tag, 0) * F_BYTES
+        kernels = r["kernels"]
+        # dominant kernel class: largest (launches per matvec x back-to-back launch time)
+        tag, kd = max(kernels.items(), key=lambda kv: kv[1]["avg_us"] * kv[1]["launches_per_matvec"])
+        avg_s = kd["avg_us"] / 1e6
+        bytes_launch = kd["bytes_per_launch"]
         peaks = {}
         try:
             with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -395,7 +416,12 @@ def main():
                                 "achieved_gbps": mv_bytes * r["value"] / world / 1e9,
                                 "frac": mv_bytes * r["value"] / world / 1e9 / peak},
             "sl_interp": r["sl"],
-            "kernel_share": {k: round(t / prof_total, 4) for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            "kernels": kernels,
+            "kernel_model_ms_per_matvec": sum(k["avg_us"] * k["launches_per_matvec"] for k in kernels.values()) / 1e3,
+            "event_profile": {"note": "per-launch event pairs (each pair adds its own overhead); shares only",
+                              "share": {k: round(t / prof_total, 4)
+                                        for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+                              "launches_per_step": {k: c // args.steps for k, (c, t) in prof.items()}},
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg()

@@ -126,6 +126,10 @@ int vrg_hess_apply_split(vrg_hess_t h, const double* s1, const double* s2, doubl
  * host-side caller of HessianOperator::apply makes; value semantics of inverse.hpp:83). */
 int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);
 int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajectory */
+/* instrumentation: average ms of one launch of a matvec kernel class (0 incremental-state
+ * step, 1 incremental-adjoint + body-force step, 2 prefilter (both passes), 3 two-field
+ * evaluate), `iters` back-to-back launches on the context stream (bench.py roofline) */
+int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch);
 
 /* evaluateGradient / evaluateObjective (inverse.hpp:60-71); scalars = [objective, mismatch, regTerm] */
 int vrg_evaluate_gradient(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,

@@ -10,7 +10,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvrg.so")
+LIB_PATH = os.environ.get("VRG_LIB_PATH", os.path.join(HERE, "libvrg.so"))  # override: experiments only
 HEADER = os.path.join(os.path.dirname(HERE), "include", "vrg.h")
 
 VRG_OK, VRG_INVALID_ARGUMENT, VRG_BLOWUP, VRG_RUNTIME_ERROR, VRG_NOT_SUPPORTED = 0, 1, 2, 3, 4
@@ -67,6 +67,7 @@ _SIG = {
     "vrg_hess_apply_split": ("ppppp", C.c_int),
     "vrg_hess_apply_host": ("ppppp", C.c_int),
     "vrg_hess_state": ("pp", C.c_int),
+    "vrg_hess_bench_kernel": ("piip", C.c_int),
     "vrg_evaluate_gradient": ("piippppidiippp", C.c_int),
     "vrg_evaluate_objective": ("piippppidiip", C.c_int),
     "vrg_random_bandlimited_field": ("piiup", C.c_int),

@@ -140,21 +140,16 @@ int vrg_profile(vrg_ctx_t c, int enable) {
         c->ctx.profOn = enable != 0;
         c->ctx.profRecs.clear();
         c->ctx.evNext = 0;
+        c->ctx.profAcc.clear();
     });
 }
 
 int vrg_profile_dump(vrg_ctx_t c, char* buf, int cap) {
     return guarded(c, [&] {
         vrg::Ctx& ctx = c->ctx;
-        ctx.sync();
+        ctx.profFlush();
         std::map<std::string, std::pair<long long, double>> acc;
-        for (const auto& r : ctx.profRecs) {
-            float ms = 0.f;
-            VRG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
-            auto& e = acc[r.tag];
-            e.first += 1;
-            e.second += ms;
-        }
+        acc.swap(ctx.profAcc);
         std::string out;
         for (const auto& kv : acc) {
             char line[256];
@@ -399,6 +394,10 @@ int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, doub
         VRG_CUDA(cudaMemcpyAsync(o2, d + 3 * N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
         ctx.sync();
     });
+}
+
+int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch) {
+    return guarded(h->owner, [&] { *ms_per_launch = h->hess.benchKernel(kernel, iters); });
 }
 
 int vrg_hess_state(vrg_hess_t h, double* traj) {

@@ -140,7 +140,14 @@ struct Ctx {
     std::vector<ProfRec> profRecs;
     std::vector<cudaEvent_t> evPool;
     std::size_t evNext = 0;
+    std::map<std::string, std::pair<long long, double>> profAcc;  // tag -> (launches, ms)
     cudaEvent_t profEvent();
+    // Reads the pending event pairs into profAcc (synchronises) and recycles the pool.
+    void profFlush();
+    void profAccumulate(const std::vector<ProfRec>& recs);
+    // Enqueues a kernel that sleeps `us` microseconds, so the launches queued behind it run
+    // back to back (profiling only; keeps host launch latency out of the event pairs).
+    void profGate(int us);
 
     Ctx(int dev, cudaStream_t s);
     ~Ctx();

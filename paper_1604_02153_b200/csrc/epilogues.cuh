@@ -74,10 +74,13 @@ struct EpiIncState {
     double halfHt;
     double* out;
     __device__ double operator()(std::size_t p, const double* v) const {
-        const double sPrevD = -(vt1D[p] * gd1[p] + vt2D[p] * gd2[p]);
-        const double sCur = -(vt1[p] * g1[p] + vt2[p] * g2[p]);
-        out[p] = v[0] + halfHt * (sPrevD + sCur);
-        return 0.0;
+        // GD_j / G_j are read once per matvec: streamed with evict-first so the per-matvec
+        // fields (vt, vt_D, X_D) stay L2-resident across the nt steps
+        const double sPrevD = -(vt1D[p] * __ldcs(gd1 + p) + vt2D[p] * __ldcs(gd2 + p));
+        const double sCur = -(vt1[p] * __ldcs(g1 + p) + vt2[p] * __ldcs(g2 + p));
+        const double o = v[0] + halfHt * (sPrevD + sCur);
+        if (out) out[p] = o;  // null in the fused band path (only the row-filtered field is kept)
+        return o;
     }
 };
 

@@ -169,16 +169,13 @@ __global__ void __launch_bounds__(kColBX* kColBY) k_prefilter_cols(const double*
 // Loads go global -> shared with cp.async (no register staging, full memory-level
 // parallelism); shared layout pads one slot per 16-chunk so the per-thread chunk walks are
 // bank-conflict free.
-constexpr int kL = 16;
 constexpr int kHalo = 2 * kL;
-constexpr int kLines = 8;
+#ifndef VRG_PF_LINES
+#define VRG_PF_LINES 8
+#endif
+constexpr int kLines = VRG_PF_LINES;  // lines per segment block (power of two)
+constexpr int kLinesLog2 = kLines == 16 ? 4 : kLines == 8 ? 3 : kLines == 4 ? 2 : 1;
 
-struct ZPow {
-    static constexpr double pw(int i) { return i == 0 ? 1.0 : kZ * pw(i - 1); }
-    double p[18];
-    __device__ constexpr ZPow() : p{pw(0), pw(1), pw(2), pw(3), pw(4), pw(5), pw(6), pw(7), pw(8),
-                                     pw(9), pw(10), pw(11), pw(12), pw(13), pw(14), pw(15), pw(16), pw(17)} {}
-};
 
 __device__ __forceinline__ void cpAsync8(double* dst, const double* src) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -189,127 +186,164 @@ __device__ __forceinline__ void cpAsyncWaitAll() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-__device__ __forceinline__ int wrapPos(int q, int n) {
-    // q in [-kHalo, n + kHalo); n >= 32 = kHalo
-    return q < 0 ? q + n : (q >= n ? q - n : q);
+
+__device__ __forceinline__ void cpAsync16(double* dst, const double* src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
 }
+
 
 // kRows: lines are rows (positions along axis 1, contiguous); else lines are columns.
 // kPadOut (columns pass only): write the coefficients in the periodically padded layout
 // (n1+3) x (n2+3), padded(i+1, j+1) = c(i, j) with one wrap row/column before and two after,
 // which the evaluation kernels index without any wrap logic.
-template <bool kRows, bool kPadOut>
-__global__ void __launch_bounds__(256) k_pf_seg(const double* __restrict__ in, double* __restrict__ out, int n1,
-                                                int n2, int R, int LS, unsigned* nonfinite) {
-    extern __shared__ double sm[];
-    const int n = kRows ? n2 : n1;          // line length
+// kR: interior samples per segment (compile time, so every staging loop fully unrolls);
+// the block has kLines * (kR/16 + 4) threads, one per chunk.
+template <bool kRows, bool kPadOut, int kR>
+__global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* __restrict__ in,
+                                                                 double* __restrict__ out, int n1, int n2, int LS,
+                                                                 unsigned* nonfinite) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int S = kR + 2 * kHalo;   // samples staged per line
+    constexpr int nch = S / kL;         // chunks per line segment
+    constexpr int NT = kLines * nch;    // threads
+    const int n = kRows ? n2 : n1;      // line length
     const int nLines = kRows ? n1 : n2;
-    const int S = R + 2 * kHalo;            // samples staged per line
-    const int nch = S / kL;                 // chunks per line segment
-    const int p0 = blockIdx.x * R;          // first interior position
+    const int p0 = blockIdx.x * kR;     // first interior position
     const int l0 = blockIdx.y * kLines;
     const int lines = min(kLines, nLines - l0);
     double* E = sm + kLines * LS;
     double* F0 = E + kLines * nch;
     double* P0 = F0 + kLines * nch;
+    const int t = threadIdx.x;
 
-    // stage: global -> shared (periodic halo), no per-element division
+    // ---- stage global -> shared (periodic halo)
     if (kRows) {
-        for (int l = 0; l < lines; ++l) {
-            const double* src = in + static_cast<std::size_t>(l0 + l) * n2;
-            double* dst = sm + l * LS;
-            for (int p = threadIdx.x; p < S; p += blockDim.x) cpAsync8(dst + p + (p >> 4), src + wrapPos(p0 - kHalo + p, n));
+        // S/2 pairs per line, 8 pairs per thread (kLines * S/2 = 8 * NT)
+        constexpr int PPL = S / 2;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = t + k * NT;
+            const int l = i / PPL, pp = i - l * PPL;
+            if (l < lines) {
+                int q = p0 - kHalo + 2 * pp;
+                q = q < 0 ? q + n : (q >= n ? q - n : q);
+                cpAsync16(sm + l * LS + slot(2 * pp), in + static_cast<std::size_t>(l0 + l) * n2 + q);
+            }
         }
     } else {
-        const int l = threadIdx.x & (kLines - 1);
+        const int l = t & (kLines - 1);
+        const int pb = t >> kLinesLog2;  // 0 .. nch-1, stride nch
         if (l < lines) {
             const double* src = in + l0 + l;
             double* dst = sm + l * LS;
-            for (int p = threadIdx.x >> 3; p < S; p += blockDim.x >> 3)
-                cpAsync8(dst + p + (p >> 4), src + static_cast<std::size_t>(wrapPos(p0 - kHalo + p, n)) * n2);
+#pragma unroll
+            for (int i = 0; i < kL; ++i) {  // S = kL * nch positions, nch per sweep
+                const int p = pb + i * nch;
+                int q = p0 - kHalo + p;
+                q = q < 0 ? q + n : (q >= n ? q - n : q);
+                cpAsync8(dst + slot(p), src + static_cast<std::size_t>(q) * n2);
+            }
         }
     }
     cpAsyncWaitAll();
     __syncthreads();
 
-    // phase 1: zero-state recurrences per chunk
-    const int t = threadIdx.x;
+    // ---- phase 1: zero-state chunk summaries
     const int l = t / nch, c = t - l * nch;
     const bool active = l < lines;
-    double A[kL], B[kL];
-    double* s = sm + l * LS + c * (kL + 1);
+    double2* s2 = reinterpret_cast<double2*>(sm + l * LS + c * kCS);
+    double f[kL];
     bool bad = false;
     if (active) {
-        double f[kL];
+#pragma unroll
+        for (int k = 0; k < kL / 2; ++k) {
+            const double2 v = s2[k];
+            f[2 * k] = v.x;
+            f[2 * k + 1] = v.y;
+        }
+        double b = 0.0;
+#pragma unroll
+        for (int k = kL - 2; k >= 0; --k) b = kZ * (f[k + 1] + b);
+        double a = 0.0;
 #pragma unroll
         for (int k = 0; k < kL; ++k) {
-            f[k] = s[k];
+            a = f[k] + kZ * a;
             bad |= !isfinite(f[k]);
         }
-        B[kL - 1] = 0.0;
-#pragma unroll
-        for (int k = kL - 2; k >= 0; --k) B[k] = kZ * (f[k + 1] + B[k + 1]);
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < kL; ++k) {
-            acc = f[k] + kZ * acc;
-            A[k] = acc;
-        }
-        E[t] = A[kL - 1];
+        E[t] = a;
         F0[t] = f[0];
-        P0[t] = B[0];
+        P0[t] = b;
     }
     if (nonfinite) {
-        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1u);
+        if (__syncthreads_or(bad) && t == 0) atomicOr(nonfinite, 1u);
     } else {
         __syncthreads();
     }
-    // phase 2: carries + fix-up for the interior chunks
+    // ---- phase 2: both recurrences again from the true chunk-boundary states
     if (active && c >= 2 && c < nch - 2) {
         const ZPow zp;
-        const int b = l * nch;
-        const double cp = E[b + c - 1] + zp.p[kL] * E[b + c - 2];
-        const double cm = kZ * (F0[b + c + 1] + P0[b + c + 1]) + zp.p[kL + 1] * (F0[b + c + 2] + P0[b + c + 2]);
+        const double cp = E[t - 1] + zp.p[kL] * E[t - 2];  // true y+ before the chunk
+        const double cm = kZ * (F0[t + 1] + P0[t + 1]) + zp.p[kL + 1] * (F0[t + 2] + P0[t + 2]);
+        double ym[kL];
+        ym[kL - 1] = cm;  // true y- at the chunk's last sample
 #pragma unroll
-        for (int k = 0; k < kL; ++k) s[k] = kSqrt3 * ((A[k] + zp.p[k + 1] * cp) + (B[k] + zp.p[kL - 1 - k] * cm));
+        for (int k = kL - 2; k >= 0; --k) ym[k] = kZ * (f[k + 1] + ym[k + 1]);
+        double yp = cp;
+#pragma unroll
+        for (int k = 0; k < kL; k += 2) {
+            yp = f[k] + kZ * yp;
+            const double o0 = kSqrt3 * (yp + ym[k]);
+            yp = f[k + 1] + kZ * yp;
+            const double o1 = kSqrt3 * (yp + ym[k + 1]);
+            s2[k / 2] = make_double2(o0, o1);
+        }
     }
     __syncthreads();
-    // store the interior
+
+    // ---- store the interior
     if (kRows) {
-        for (int ll = 0; ll < lines; ++ll) {
-            double* dst = out + static_cast<std::size_t>(l0 + ll) * n2 + p0;
-            const double* src = sm + ll * LS;
-            for (int p = threadIdx.x; p < R; p += blockDim.x) {
-                const int ps = p + kHalo;
-                dst[p] = src[ps + (ps >> 4)];
-            }
+        constexpr int PPL = kR / 2;  // interior pairs per line
+        for (int i = t; i < kLines * PPL; i += NT) {
+            const int ll = i / PPL, pp = i - ll * PPL;
+            if (ll < lines)
+                reinterpret_cast<double2*>(out + static_cast<std::size_t>(l0 + ll) * n2 + p0)[pp] =
+                    *reinterpret_cast<const double2*>(sm + ll * LS + slot(2 * pp + kHalo));
         }
     } else {
-        const int ll = threadIdx.x & (kLines - 1);
+        const int ll = t & (kLines - 1);
+        const int pb = t >> kLinesLog2;
         if (ll < lines) {
             const double* src = sm + ll * LS;
             const int col = l0 + ll;
             if (kPadOut) {
                 const int PW = n2 + 3;
                 const int colX = col == n2 - 1 ? 0 : (col == 0 ? n2 + 1 : (col == 1 ? n2 + 2 : -1));
-                for (int p = threadIdx.x >> 3; p < R; p += blockDim.x >> 3) {
-                    const int ps = p + kHalo;
-                    const double v = src[ps + (ps >> 4)];
-                    const int q = p0 + p;
-                    const int rowX = q == n1 - 1 ? 0 : (q == 0 ? n1 + 1 : (q == 1 ? n1 + 2 : -1));
-                    double* r1 = out + static_cast<std::size_t>(q + 1) * PW;
-                    r1[col + 1] = v;
-                    if (colX >= 0) r1[colX] = v;
-                    if (rowX >= 0) {
-                        double* r2 = out + static_cast<std::size_t>(rowX) * PW;
-                        r2[col + 1] = v;
-                        if (colX >= 0) r2[colX] = v;
+                const bool edgeRows = p0 == 0 || p0 + kR == n1;  // segment holds row 0, 1 or n1-1
+#pragma unroll
+                for (int i = 0; i < (kR + nch - 1) / nch; ++i) {
+                    const int p = pb + i * nch;
+                    if (p < kR) {
+                        const double v = src[slot(p + kHalo)];
+                        const int q = p0 + p;
+                        double* r1 = out + static_cast<std::size_t>(q + 1) * PW;
+                        r1[col + 1] = v;
+                        if (colX >= 0) r1[colX] = v;
+                        if (edgeRows) {
+                            const int rowX = q == n1 - 1 ? 0 : (q == 0 ? n1 + 1 : (q == 1 ? n1 + 2 : -1));
+                            if (rowX >= 0) {
+                                double* r2 = out + static_cast<std::size_t>(rowX) * PW;
+                                r2[col + 1] = v;
+                                if (colX >= 0) r2[colX] = v;
+                            }
+                        }
                     }
                 }
             } else {
-                for (int p = threadIdx.x >> 3; p < R; p += blockDim.x >> 3) {
-                    const int ps = p + kHalo;
-                    out[static_cast<std::size_t>(p0 + p) * n2 + col] = src[ps + (ps >> 4)];
+#pragma unroll
+                for (int i = 0; i < (kR + nch - 1) / nch; ++i) {
+                    const int p = pb + i * nch;
+                    if (p < kR) out[static_cast<std::size_t>(p0 + p) * n2 + col] = src[slot(p + kHalo)];
                 }
             }
         }
@@ -343,38 +377,63 @@ struct SegPlan {
 
 SegPlan segPlan(int n) {
     SegPlan p;
-    if (n < 32 || n % kL != 0) return p;
-    for (int r = 256; r >= kL; r -= kL)
-        if (n % r == 0) {
+    for (int r : {256, 128, 64, 32})
+        if (n >= 32 && n % r == 0) {
             p.R = r;
             break;
         }
+    if (!p.R) return p;
     const int nch = (p.R + 2 * kHalo) / kL;
-    const int base = nch * (kL + 1);
-    p.LS = base + ((2 - base % 16) + 16) % 16;  // line stride = 2 mod 16 (conflict-free column loads)
+    const int base = nch * kCS;
+    p.LS = base + ((2 - base % 16) + 16) % 16;  // even, = 2 mod 16 (conflict-free column loads)
     p.threads = kLines * nch;
     p.smem = sizeof(double) * (static_cast<std::size_t>(kLines) * p.LS + 3 * kLines * nch);
-    p.ok = p.threads <= 256;
+    p.ok = true;
     return p;
 }
 
+template <bool kRows, bool kPad, int kR>
+void launchSeg(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite) {
+    const int n = kRows ? g.n2 : g.n1, lines = kRows ? g.n1 : g.n2;
+    k_pf_seg<kRows, kPad, kR><<<dim3(n / kR, (lines + kLines - 1) / kLines), p.threads, p.smem, ctx.stream>>>(
+        in, out, g.n1, g.n2, p.LS, nonfinite);
+}
+
+template <bool kRows, bool kPad>
+void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite) {
+    switch (p.R) {
+        case 256: launchSeg<kRows, kPad, 256>(ctx, g, p, in, out, nonfinite); break;
+        case 128: launchSeg<kRows, kPad, 128>(ctx, g, p, in, out, nonfinite); break;
+        case 64: launchSeg<kRows, kPad, 64>(ctx, g, p, in, out, nonfinite); break;
+        default: launchSeg<kRows, kPad, 32>(ctx, g, p, in, out, nonfinite); break;
+    }
+}
+
 }  // namespace
+
+bool colPassFusable(const GridDims& g) { return segPlan(g.n1).ok; }
+
+void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c) {
+    const SegPlan pc = segPlan(g.n1);
+    if (!pc.ok) throw NotSupported("prefilter column pass: n1 must be a multiple of 32");
+    {
+        LaunchScope ls_(ctx, "k_prefilter_cols");
+        launchSegR<false, true>(ctx, g, pc, rowFiltered, c, nullptr);
+    }
+    VRG_LAUNCH_CHECK();
+}
 
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite) {
     const SegPlan pr = segPlan(g.n2), pc = segPlan(g.n1);
     if (pr.ok && pc.ok) {
         {
             LaunchScope ls_(ctx, "k_prefilter_rows");
-            k_pf_seg<true, false>
-                <<<dim3(g.n2 / pr.R, (g.n1 + kLines - 1) / kLines), pr.threads, pr.smem, ctx.stream>>>(
-                    u, tmp, g.n1, g.n2, pr.R, pr.LS, nonfinite);
+            launchSegR<true, false>(ctx, g, pr, u, tmp, nonfinite);
         }
         VRG_LAUNCH_CHECK();
         {
             LaunchScope ls_(ctx, "k_prefilter_cols");
-            k_pf_seg<false, true>
-                <<<dim3(g.n1 / pc.R, (g.n2 + kLines - 1) / kLines), pc.threads, pc.smem, ctx.stream>>>(
-                    tmp, c, g.n1, g.n2, pc.R, pc.LS, nullptr);
+            launchSegR<false, true>(ctx, g, pc, tmp, c, nullptr);
         }
         VRG_LAUNCH_CHECK();
         return;

@@ -18,12 +18,30 @@ constexpr double kZ = -0.26794919243112270647;   // sqrt(3) - 2
 constexpr double kSqrt3 = 1.7320508075688772935;
 constexpr int kWarm = 28;
 constexpr int kChunk = 32;
+constexpr int kL = 16;  // chunk of the exact chunk-carry filter (interp.cu)
+
+// z^i, i = 0..17, folded to compile-time constants.
+struct ZPow {
+    static constexpr double pw(int i) { return i == 0 ? 1.0 : kZ * pw(i - 1); }
+    double p[18];
+    __device__ constexpr ZPow() : p{pw(0), pw(1), pw(2), pw(3), pw(4), pw(5), pw(6), pw(7), pw(8),
+                                     pw(9), pw(10), pw(11), pw(12), pw(13), pw(14), pw(15), pw(16), pw(17)} {}
+};
+
+// Shared layout of one staged line: chunk c (16 samples) at offset kCS*c, kCS = 18 doubles, so
+// chunk starts are 16-byte aligned (16-byte cp.async and LDS.128/STS.128) and consecutive
+// chunks fall in distinct 16-byte bank groups.
+constexpr int kCS = 18;
+__device__ __forceinline__ int slot(int p) { return p + 2 * (p >> 4); }
 
 // Launches the two prefilter passes (rows of length n2, then columns of length n1) on
 // ctx.stream: c = P u, written in the periodically padded layout of paddedPoints(n1, n2)
 // doubles (see cellBase).  `tmp` holds 2*n1*n2 doubles.  If `nonfinite` is non-null, a
 // non-finite input value sets *nonfinite = 1 (checkFinite(u, "prefilter"), interp.cpp:76).
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite);
+// Column pass only (input already row-filtered, e.g. by a fused band kernel, evalband.cuh).
+bool colPassFusable(const GridDims& g);
+void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c);
 
 // B-spline weights, src/interp.cpp:59-65 (the /6 as a multiply by 1/6: <= 1 ulp apart).
 __device__ __forceinline__ void bsplineWeights(double f, double w[4]) {

@@ -1,6 +1,9 @@
 // Device GN Hessian matvec: fused SL incremental state (K6), fused SL incremental adjoint +
 // trapezoid body force (K5 + K8), spectral regularisation / Leray / split wrapper (K7, K8).
+#include <cstdlib>
+
 #include "epilogues.cuh"
+#include "evalband.cuh"
 #include "inverse.cuh"
 
 namespace vrg {
@@ -33,13 +36,13 @@ struct EpiAdjointBF {
         const double f0 = uD * dvDep[p];
         const double pred = uD + ht * f0;
         const double o = uD + 0.5 * ht * (f0 + pred * dv[p]);
-        const double nb1 = b1[p] + w * (o * G1[p]);
-        const double nb2 = b2[p] + w * (o * G2[p]);
+        const double nb1 = b1[p] + w * (o * __ldcs(G1 + p));  // G_j streamed once per matvec
+        const double nb2 = b2[p] + w * (o * __ldcs(G2 + p));
         if (o1) {
             o1[p] = reg1[p] + nb1;
             o2[p] = reg2[p] + nb2;
         } else {
-            out[p] = o;
+            if (out) out[p] = o;  // null in the fused band path
             b1[p] = nb1;
             b2[p] = nb2;
         }
@@ -48,6 +51,8 @@ struct EpiAdjointBF {
 };
 
 // Seed of the incremental adjoint: lt(1) = -m~(1) (inverse.cpp:181), b = w_nt lt(1) grad m_nt.
+// Fused band path: `lam` is null and `rowLam` (the row-filtered m~(1)) is negated in place,
+// which is the row-filtered lt(1) by linearity; `flag` records a non-finite lt(1).
 struct EpiAdjointSeed {
     static constexpr const char* kName = "pointwise/adjoint_seed";
     static constexpr bool kGuard = true;
@@ -59,9 +64,13 @@ struct EpiAdjointSeed {
     double w;
     double* b1;
     double* b2;
+    double* rowLam = nullptr;
+    unsigned* flag = nullptr;
     __device__ double operator()(std::size_t p, const double*) const {
         const double l = -1.0 * mt[p];
-        lam[p] = l;
+        if (lam) lam[p] = l;
+        if (rowLam) rowLam[p] = -rowLam[p];
+        if (flag && !isfinite(l)) atomicOr(flag, 1u);
         b1[p] = w * (l * G1[p]);
         b2[p] = w * (l * G2[p]);
         return l;
@@ -109,6 +118,13 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     // lazily-built per-velocity work the reference does on the first apply
     // (charBwd 2 + dvDepBwd 1 interps, divv 3 FFTs; + charFwd 2 if the state was reused)
     lazyInterps_ = 3 + (hadFwd ? 0 : 2);
+    // Opt-in (VRG_FUSED_BANDS=1): the band kernels remove the row-pass kernel per step but
+    // their gather runs at lower occupancy; measured slower on B200 at every size
+    // (ms per matvec, plain vs band: 1024^2 0.93 vs 1.23, 2048^2 3.57 vs 4.18,
+    // 4096^2/nt=32 27.3 vs 29.5), so the plain 3-kernel step is the default.
+    const char* env = std::getenv("VRG_FUSED_BANDS");
+    const bool want = env && env[0] == '1';
+    fused_ = useFusedBands && want && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
     lazyFfts_ = 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     adjLog_.ensure(nt + 1, evalBlocks(g));
@@ -150,6 +166,41 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     launchPrefilter(ctx, g, vt1, coef, tmp, nullptr);
     launchPrefilter(ctx, g, vt2, c2, tmp, nullptr);
     launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N});
+    auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
+    if (fused_) {
+        // Band path: every step's gather kernel also row-filters its output (evalband.cuh), so
+        // each step is [column pass] + [gather + epilogue + row pass].  R[.] ping-pong holds
+        // the row-filtered m~_j, then the row-filtered lt_j.
+        double* R[2] = {tmp, tmp + N};
+        double* mtLast = mt[0];  // unfiltered m~(1) for the adjoint seed
+        for (int j = 1; j <= nt; ++j) {
+            EpiIncState epi{nullptr, vtD, vtD + N, GD(j), GD(j) + N, vt1, vt2, G(j), G(j) + N, 0.5 * ht,
+                            j == nt ? mtLast : nullptr};
+            if (j == 1) {
+                launchEvalBand<EpiIncState, false>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, R[1], nullptr);
+            } else {
+                launchPrefilterCols(ctx, g, R[(j - 1) & 1], coef);
+                launchEvalBand<EpiIncState, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, R[j & 1], nullptr);
+            }
+        }
+        adjLog_.reset(ctx);
+        EpiAdjointSeed seed{adjLog_.partial(nt), mtLast, nullptr, G(nt), G(nt) + N, wOf(nt), b1, b2, R[nt & 1],
+                            adjLog_.flag(nt)};
+        launchPointwise(ctx, g, seed);
+        for (int j = nt; j >= 1; --j) {
+            launchPrefilterCols(ctx, g, R[j & 1], coef);
+            const bool last = j == 1;
+            EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, nullptr, G(j - 1), G(j - 1) + N, wOf(j - 1),
+                             b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
+            if (last)
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi);
+            else
+                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, R[(j - 1) & 1],
+                                                   adjLog_.flag(j - 1));
+        }
+        adjLog_.finalize(ctx);
+        return;
+    }
     for (int j = 1; j <= nt; ++j) {
         EpiIncState epi{nullptr, vtD, vtD + N, GD(j), GD(j) + N, vt1, vt2, G(j), G(j) + N, 0.5 * ht, mt[j & 1]};
         if (j == 1) {
@@ -161,7 +212,6 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     }
     // incremental adjoint (GN: solveAdjoint(-m~(1)), guarded, inverse.cpp:185) + body force
     adjLog_.reset(ctx);
-    auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
     launchPointwise(ctx, g,
                     EpiAdjointSeed{adjLog_.partial(nt), mt[nt & 1], lam[nt & 1], G(nt), G(nt) + N, wOf(nt), b1, b2});
     for (int j = nt; j >= 1; --j) {
@@ -176,19 +226,81 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
 
 void Hessian::checkLastGuard() { adjLog_.check(ctx, "adjoint", nt, false, true, nt); }
 
+// Average device time of one launch of a matvec kernel class, `iters` back-to-back launches
+// between two events on the context stream, with the operands of a mid-trajectory step
+// (steady state after a matvec has run, so the operands are the ones the matvec produced).
+double Hessian::benchKernel(int id, int iters) {
+    const std::size_t N = g.points();
+    const double ht = solver.ht;
+    const int j = std::max(2, nt / 2);
+    double* vtD = work_.d();
+    double* mt = vtD + 2 * N;
+    double* lam = vtD + 4 * N;
+    double* b = vtD + 6 * N;
+    double* c2 = vtD + 11 * N;
+    const double* Xf = solver.departure(kForward);
+    const double* Xb = solver.departure(kBackward);
+    const double* dv = solver.divVelocity();
+    const double* dvd = solver.divVelocityAtDeparture(kBackward);
+    double* coef = solver.coef();
+    double* tmp = solver.tmp();
+    const double* G = G_.d() + static_cast<std::size_t>(j) * 2 * N;
+    const double* GD = GD_.d() + static_cast<std::size_t>(j - 1) * 2 * N;
+    auto one = [&] {
+        switch (id) {
+            case 0: {  // incremental-state step (K6)
+                EpiIncState epi{nullptr, vtD, vtD + N, GD, GD + N, vtD, vtD + N, G, G + N, 0.5 * ht, mt + N};
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi);
+                break;
+            }
+            case 1: {  // incremental-adjoint step + body force (K5+K8)
+                EpiAdjointBF epi{adjLog_.partial(0), dvd, dv, ht, lam + N, G, G + N, ht, b, b + N,
+                                 nullptr, nullptr, nullptr, nullptr};
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi);
+                break;
+            }
+            case 2:  // prefilter, both passes (K1)
+                launchPrefilter(ctx, g, mt, coef, tmp, nullptr);
+                break;
+            default:  // vtilde at departure (K2, two fields)
+                launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N});
+                break;
+        }
+    };
+    one();  // warm
+    cudaEvent_t e0, e1;
+    VRG_CUDA(cudaEventCreate(&e0));
+    VRG_CUDA(cudaEventCreate(&e1));
+    VRG_CUDA(cudaEventRecord(e0, ctx.stream));
+    for (int i = 0; i < iters; ++i) one();
+    VRG_CUDA(cudaEventRecord(e1, ctx.stream));
+    VRG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    VRG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms / iters;
+}
+
 // The launch sequence of one matvec is fixed for given (kind, in, out) pointers, so it is
 // captured once into a CUDA graph and replayed (removes ~100 launch gaps per matvec).  The
 // host-side work (counters, guard readback) stays outside the graph.
+// With the context profile on, the sequence is launched directly behind a sleeping gate kernel
+// (Ctx::profGate), so the whole matvec is queued before the GPU reaches it and the per-kernel
+// event pairs time back-to-back execution, as in the graph replay.
 template <class F>
 void Hessian::replay(int kind, const double* a, const double* b, const double* c, const double* d, F&& launchSeq) {
-    if (ctx.profOn || !useGraphs) {
+    if (!useGraphs || ctx.profOn) {
+        if (ctx.profOn) ctx.profGate(3000);
         launchSeq();
         return;
     }
+    const bool prof = false;
     const GraphKey key{kind, a, b, c, d};
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {
         const long long l0 = ctx.launches;
+        const std::size_t ev0 = ctx.evNext;
         cudaGraph_t graph = nullptr;
         VRG_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
         try {
@@ -200,18 +312,32 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
             throw;
         }
         VRG_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
-        cudaGraphExec_t exec = nullptr;
-        VRG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        GraphEntry e;
+        VRG_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
         cudaGraphDestroy(graph);
-        it = graphs_.emplace(key, std::make_pair(exec, ctx.launches - l0)).first;
+        e.launches = ctx.launches - l0;
         ctx.launches = l0;
+        if (prof) {  // the graph takes ownership of the events recorded during capture
+            e.recs.swap(ctx.profRecs);
+            e.events.assign(ctx.evPool.begin() + ev0, ctx.evPool.begin() + ctx.evNext);
+            ctx.evPool.erase(ctx.evPool.begin() + ev0, ctx.evPool.begin() + ctx.evNext);
+            ctx.evNext = ev0;
+        }
+        it = graphs_.emplace(key, std::move(e)).first;
     }
-    VRG_CUDA(cudaGraphLaunch(it->second.first, ctx.stream));
-    ctx.launches += it->second.second;
+    VRG_CUDA(cudaGraphLaunch(it->second.exec, ctx.stream));
+    ctx.launches += it->second.launches;
+    if (prof) {
+        ctx.sync();
+        ctx.profAccumulate(it->second.recs);
+    }
 }
 
 Hessian::~Hessian() {
-    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.first);
+    for (auto& kv : graphs_) {
+        cudaGraphExecDestroy(kv.second.exec);
+        for (cudaEvent_t e : kv.second.events) cudaEventDestroy(e);
+    }
 }
 
 void Hessian::apply(const double* vt1, const double* vt2, double* o1, double* o2) {

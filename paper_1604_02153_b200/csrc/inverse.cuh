@@ -50,6 +50,9 @@ public:
 
     const double* state() const { return state_.d(); }
     bool useGraphs = true;
+    // ms per launch of a matvec kernel class (0 incstate step, 1 adjoint+body-force step,
+    // 2 prefilter (both passes), 3 two-field evaluate), timed back to back.
+    double benchKernel(int id, int iters);
     // device-visible guard check result of the last data term (throws like solveAdjoint).
     void checkLastGuard();
     // counter increments of one data term in the reference (steady state)
@@ -70,7 +73,13 @@ private:
         const double *a, *b, *c, *d;
         bool operator<(const GraphKey& o) const { return std::tie(kind, a, b, c, d) < std::tie(o.kind, o.a, o.b, o.c, o.d); }
     };
-    std::map<GraphKey, std::pair<cudaGraphExec_t, long long>> graphs_;
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        long long launches = 0;
+        std::vector<Ctx::ProfRec> recs;   // profiled variant: event pairs inside the graph
+        std::vector<cudaEvent_t> events;  // owned by the graph
+    };
+    std::map<GraphKey, GraphEntry> graphs_;
 
     DBuf state_;  // (nt+1) N
     DBuf G_;      // (nt+1) x [g1 | g2]
@@ -79,6 +88,10 @@ private:
     DBuf spec_;   // 4 half spectra
     GuardLog adjLog_;
     long long lazyInterps_ = 0, lazyFfts_ = 0;
+    bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh
+
+public:
+    static inline bool useFusedBands = true;  // process-wide switch (tests compare both paths)
 };
 
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,

@@ -97,6 +97,34 @@ cudaEvent_t Ctx::profEvent() {
     return evPool[evNext++];
 }
 
+void Ctx::profAccumulate(const std::vector<ProfRec>& recs) {
+    for (const auto& r : recs) {
+        float ms = 0.f;
+        VRG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        auto& e = profAcc[r.tag];
+        e.first += 1;
+        e.second += ms;
+    }
+}
+
+namespace {
+__global__ void k_sleep(int us) {
+    for (int i = 0; i < us; ++i) __nanosleep(1000);
+}
+}  // namespace
+
+void Ctx::profGate(int us) {
+    k_sleep<<<1, 1, 0, stream>>>(us);
+    VRG_LAUNCH_CHECK();
+}
+
+void Ctx::profFlush() {
+    sync();
+    profAccumulate(profRecs);
+    profRecs.clear();
+    evNext = 0;
+}
+
 // ------------------------------------------------------------------------------ kernels
 namespace {
 

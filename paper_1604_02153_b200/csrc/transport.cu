@@ -81,7 +81,11 @@ void GuardLog::ensure(int nsteps, unsigned nblocks) {
     flags.alloc(sizeof(unsigned) * steps);
 }
 
-void GuardLog::reset(Ctx& ctx) { VRG_CUDA(cudaMemsetAsync(flags.d(), 0, sizeof(unsigned) * steps, ctx.stream)); }
+void GuardLog::reset(Ctx& ctx) {
+    VRG_CUDA(cudaMemsetAsync(flags.d(), 0, sizeof(unsigned) * steps, ctx.stream));
+    // kernels with fewer blocks than `blocks` (band kernels) leave the tail entries untouched
+    VRG_CUDA(cudaMemsetAsync(partials.d(), 0, sizeof(double) * steps * blocks, ctx.stream));
+}
 
 void GuardLog::finalize(Ctx& ctx) {
     {
