@@ -134,6 +134,7 @@ KERNEL_CLASSES = {
     1: ("evaluate/adjoint_bodyforce (K5+K8)", NT, 12),
     2: ("prefilter rows+cols (K1)", 2 * NT + 1, 4),
     3: ("evaluate/store2 (K2, vt_D)", 1, 6),
+    4: ("prefilter cols only (K1 column pass)", 0, 2),  # included in id 2; breakdown only
 }
 
 

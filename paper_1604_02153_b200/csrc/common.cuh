@@ -180,4 +180,33 @@ struct LaunchScope {
 
 inline dim3 grid1d(std::size_t n, int block) { return dim3(static_cast<unsigned>((n + block - 1) / block)); }
 
+// Programmatic dependent launch (sm_90+).  Kernels of the time loops are launched with
+// programmatic stream serialisation: each one runs its independent prologue (departure
+// points, per-iterate fields), then pdlWait() until the predecessor grid has completed, then
+// pdlTrigger() so the successor may launch and run its own prologue under this body.  Because
+// every kernel waits before it triggers, at most two grids overlap and completion stays
+// transitive along the stream.
+__device__ __forceinline__ void pdlWait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdlTrigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Which kernel families get the PDL attribute (bit 0: evaluate/pointwise, bit 1: prefilter);
+// the kernels' wait/trigger instructions are no-ops under a plain launch.
+int pdlMask();
+
+template <class... KArgs, class... Args>
+void launchPdl(int family, void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,
+               Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdlMask() & family) ? 1 : 0;
+    VRG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 }  // namespace vrg

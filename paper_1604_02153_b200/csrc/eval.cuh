@@ -21,19 +21,27 @@ struct CoeffSet {
     const double* c[NF];
 };
 
+// xStable: the departure points are not written by any kernel still in flight (the matvec
+// time loops), so the cell computation runs before the programmatic-dependency wait.
 template <int NF, class Epi>
 __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const double* __restrict__ x1,
-                                                         const double* __restrict__ x2, int n1, int n2, double h1,
-                                                         double h2, Epi epi) {
+                                                         const double* __restrict__ x2, int n1, int n2, int xStable,
+                                                         Epi epi) {
     const int N = n1 * n2;  // grids up to 2^31 points
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     double guard = 0.0;
+    if (!xStable) pdlWait();
+    double w1[4], w2[4];
+    int base = 0;
     if (p < N) {
-        double w1[4], w2[4];
         const int b1 = cellBase(__ldg(x1 + p), n1 * (1.0 / kTwoPi), n1, w1);  // 1/h = n / 2pi
         const int b2 = cellBase(__ldg(x2 + p), n2 * (1.0 / kTwoPi), n2, w2);
+        base = b1 * (n2 + 3) + b2;
+    }
+    if (xStable) pdlWait();
+    pdlTrigger();
+    if (p < N) {
         const int PW = n2 + 3;
-        const int base = b1 * PW + b2;
         double val[NF];
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
@@ -71,6 +79,8 @@ template <class Epi>
 __global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi) {
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     double guard = 0.0;
+    pdlWait();
+    pdlTrigger();
     if (p < N) {
         const double z[2] = {0.0, 0.0};
         const double gv = fabs(epi(p, z));
@@ -93,20 +103,19 @@ template <class Epi>
 void launchPointwise(Ctx& ctx, const GridDims& g, const Epi& epi) {
     {
         LaunchScope ls_(ctx, Epi::kName);
-        k_pointwise<Epi><<<grid1d(g.points(), kEvalBlock), kEvalBlock, 0, ctx.stream>>>(g.points(), epi);
+        launchPdl(1, k_pointwise<Epi>, grid1d(g.points(), kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, g.points(), epi);
     }
-    VRG_LAUNCH_CHECK();
 }
 
 template <int NF, class Epi>
-void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const double* x1, const double* x2, const Epi& epi) {
+void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const double* x1, const double* x2, const Epi& epi,
+                    bool xStable = false) {
     const std::size_t N = g.points();
     {
         LaunchScope ls_(ctx, Epi::kName);
-        k_evaluate<NF, Epi><<<grid1d(N, kEvalBlock), kEvalBlock, 0, ctx.stream>>>(cs, x1, x2, g.n1, g.n2, g.h1(),
-                                                                                   g.h2(), epi);
+        launchPdl(1, k_evaluate<NF, Epi>, grid1d(N, kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, cs, x1, x2, g.n1, g.n2,
+                  xStable ? 1 : 0, epi);
     }
-    VRG_LAUNCH_CHECK();
 }
 
 inline unsigned evalBlocks(const GridDims& g) { return grid1d(g.points(), kEvalBlock).x; }

@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* _
                                                                  double* __restrict__ out, int n1, int n2, int LS,
                                                                  unsigned* nonfinite) {
     extern __shared__ __align__(16) double sm[];
+    pdlWait();  // the input is the predecessor's output
+    pdlTrigger();
     constexpr int S = kR + 2 * kHalo;   // samples staged per line
     constexpr int nch = S / kL;         // chunks per line segment
     constexpr int NT = kLines * nch;    // threads
@@ -395,8 +397,8 @@ SegPlan segPlan(int n) {
 template <bool kRows, bool kPad, int kR>
 void launchSeg(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite) {
     const int n = kRows ? g.n2 : g.n1, lines = kRows ? g.n1 : g.n2;
-    k_pf_seg<kRows, kPad, kR><<<dim3(n / kR, (lines + kLines - 1) / kLines), p.threads, p.smem, ctx.stream>>>(
-        in, out, g.n1, g.n2, p.LS, nonfinite);
+    launchPdl(2, k_pf_seg<kRows, kPad, kR>, dim3(n / kR, (lines + kLines - 1) / kLines), dim3(p.threads), p.smem,
+              ctx.stream, in, out, g.n1, g.n2, p.LS, nonfinite);
 }
 
 template <bool kRows, bool kPad>
@@ -409,18 +411,108 @@ void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in,
     }
 }
 
+// Column pass with the samples in registers: thread (column c0+col, chunk row cr) loads the
+// 16 rows of its chunk straight from global memory (each load coalesced over the 16 columns of
+// the block), so no shared staging of samples is needed; only the chunk summaries go through
+// shared memory.  kCR = kR/16 + 4 chunk rows (2-chunk periodic halo above and below); output
+// in the padded coefficient layout.
+constexpr int kColW = 16;
+
+template <int kR>
+__global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const double* __restrict__ in,
+                                                                     double* __restrict__ out, int n1, int n2) {
+    constexpr int kCR = kR / kL + 4;
+    __shared__ double E[kCR][kColW], F0[kCR][kColW], P0[kCR][kColW];
+    pdlWait();  // the input is the predecessor's output
+    pdlTrigger();
+    const int col = threadIdx.x & (kColW - 1);
+    const int cr = threadIdx.x / kColW;
+    const int gc = blockIdx.y * kColW + col;
+    const int p0 = blockIdx.x * kR;
+    const bool active = gc < n2;
+    double f[kL];
+    if (active) {
+        int q = p0 - kHalo + cr * kL;  // first row of this chunk (may wrap)
+        q = q < 0 ? q + n1 : (q >= n1 ? q - n1 : q);
+        const double* src = in + gc;
+#pragma unroll
+        for (int k = 0; k < kL; ++k) {
+            f[k] = __ldg(src + static_cast<std::size_t>(q) * n2);
+            q = q + 1 == n1 ? 0 : q + 1;
+        }
+        double b = 0.0;
+#pragma unroll
+        for (int k = kL - 2; k >= 0; --k) b = kZ * (f[k + 1] + b);
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < kL; ++k) a = f[k] + kZ * a;
+        E[cr][col] = a;
+        F0[cr][col] = f[0];
+        P0[cr][col] = b;
+    }
+    __syncthreads();
+    if (!active || cr < 2 || cr >= kCR - 2) return;
+    const ZPow zp;
+    const double cp = E[cr - 1][col] + zp.p[kL] * E[cr - 2][col];
+    const double cm = kZ * (F0[cr + 1][col] + P0[cr + 1][col]) + zp.p[kL + 1] * (F0[cr + 2][col] + P0[cr + 2][col]);
+    double ym[kL];
+    ym[kL - 1] = cm;
+#pragma unroll
+    for (int k = kL - 2; k >= 0; --k) ym[k] = kZ * (f[k + 1] + ym[k + 1]);
+    const int PW = n2 + 3;
+    const int colX = gc == n2 - 1 ? 0 : (gc == 0 ? n2 + 1 : (gc == 1 ? n2 + 2 : -1));
+    const int r0 = p0 + (cr - 2) * kL;  // first output row
+    const bool edgeRows = r0 == 0 || r0 + kL == n1;
+    double yp = cp;
+#pragma unroll
+    for (int k = 0; k < kL; ++k) {
+        yp = f[k] + kZ * yp;
+        const double v = kSqrt3 * (yp + ym[k]);
+        const int q = r0 + k;
+        double* r1 = out + static_cast<std::size_t>(q + 1) * PW;
+        r1[gc + 1] = v;
+        if (colX >= 0) r1[colX] = v;
+        if (edgeRows) {
+            const int rowX = q == n1 - 1 ? 0 : (q == 0 ? n1 + 1 : (q == 1 ? n1 + 2 : -1));
+            if (rowX >= 0) {
+                double* r2 = out + static_cast<std::size_t>(rowX) * PW;
+                r2[gc + 1] = v;
+                if (colX >= 0) r2[colX] = v;
+            }
+        }
+    }
+}
+
+template <int kR>
+void launchColsReg(Ctx& ctx, const GridDims& g, const double* in, double* out) {
+    launchPdl(2, k_pf_cols_reg<kR>, dim3(g.n1 / kR, (g.n2 + kColW - 1) / kColW), dim3(kColW * (kR / kL + 4)), 0,
+              ctx.stream, in, out, g.n1, g.n2);
+}
+
+// Column pass into the padded layout; false if n1 is not a multiple of 32.
+bool launchColumnPass(Ctx& ctx, const GridDims& g, const double* in, double* out) {
+    const SegPlan pc = segPlan(g.n1);
+    if (!pc.ok) return false;
+    {
+        LaunchScope ls_(ctx, "k_prefilter_cols");
+        switch (pc.R) {
+            case 256: launchColsReg<256>(ctx, g, in, out); break;
+            case 128: launchColsReg<128>(ctx, g, in, out); break;
+            case 64: launchColsReg<64>(ctx, g, in, out); break;
+            default: launchColsReg<32>(ctx, g, in, out); break;
+        }
+    }
+    VRG_LAUNCH_CHECK();
+    return true;
+}
+
 }  // namespace
 
 bool colPassFusable(const GridDims& g) { return segPlan(g.n1).ok; }
 
 void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c) {
-    const SegPlan pc = segPlan(g.n1);
-    if (!pc.ok) throw NotSupported("prefilter column pass: n1 must be a multiple of 32");
-    {
-        LaunchScope ls_(ctx, "k_prefilter_cols");
-        launchSegR<false, true>(ctx, g, pc, rowFiltered, c, nullptr);
-    }
-    VRG_LAUNCH_CHECK();
+    if (!launchColumnPass(ctx, g, rowFiltered, c))
+        throw NotSupported("prefilter column pass: n1 must be a multiple of 32");
 }
 
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite) {
@@ -431,11 +523,7 @@ void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, do
             launchSegR<true, false>(ctx, g, pr, u, tmp, nonfinite);
         }
         VRG_LAUNCH_CHECK();
-        {
-            LaunchScope ls_(ctx, "k_prefilter_cols");
-            launchSegR<false, true>(ctx, g, pc, tmp, c, nullptr);
-        }
-        VRG_LAUNCH_CHECK();
+        launchColumnPass(ctx, g, tmp, c);
         return;
     }
     double* tmp2 = tmp + g.points();  // unpadded column-pass output of the generic path

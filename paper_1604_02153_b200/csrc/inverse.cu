@@ -165,7 +165,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     // incremental state (solveIncState SL, transport.cpp:322-342)
     launchPrefilter(ctx, g, vt1, coef, tmp, nullptr);
     launchPrefilter(ctx, g, vt2, c2, tmp, nullptr);
-    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N});
+    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
     auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
     if (fused_) {
         // Band path: every step's gather kernel also row-filters its output (evalband.cuh), so
@@ -193,7 +193,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
             EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, nullptr, G(j - 1), G(j - 1) + N, wOf(j - 1),
                              b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
             if (last)
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
             else
                 launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, R[(j - 1) & 1],
                                                    adjLog_.flag(j - 1));
@@ -207,7 +207,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
             launchPointwise(ctx, g, epi);
         } else {
             launchPrefilter(ctx, g, mt[(j - 1) & 1], coef, tmp, nullptr);
-            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi);
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, true);
         }
     }
     // incremental adjoint (GN: solveAdjoint(-m~(1)), guarded, inverse.cpp:185) + body force
@@ -219,7 +219,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         const bool last = (j == 1) && out1;
         EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, lam[(j - 1) & 1], G(j - 1), G(j - 1) + N, wOf(j - 1),
                          b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
-        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi);
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
     }
     adjLog_.finalize(ctx);
 }
@@ -250,20 +250,23 @@ double Hessian::benchKernel(int id, int iters) {
         switch (id) {
             case 0: {  // incremental-state step (K6)
                 EpiIncState epi{nullptr, vtD, vtD + N, GD, GD + N, vtD, vtD + N, G, G + N, 0.5 * ht, mt + N};
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, true);
                 break;
             }
             case 1: {  // incremental-adjoint step + body force (K5+K8)
                 EpiAdjointBF epi{adjLog_.partial(0), dvd, dv, ht, lam + N, G, G + N, ht, b, b + N,
                                  nullptr, nullptr, nullptr, nullptr};
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
                 break;
             }
             case 2:  // prefilter, both passes (K1)
                 launchPrefilter(ctx, g, mt, coef, tmp, nullptr);
                 break;
+            case 4:  // prefilter column pass only (K1 cols)
+                launchPrefilterCols(ctx, g, tmp, coef);
+                break;
             default:  // vtilde at departure (K2, two fields)
-                launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N});
+                launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
                 break;
         }
     };

@@ -202,7 +202,7 @@ void Solver::continuityStep(const double* u, double* out, int dir, double* guard
     const double* dvd = divVelocityAtDeparture(dir);
     launchPrefilter(ctx, g, u, coef_.d(), tmp_.d(), flag);
     EpiContinuity epi{guardPartial ? guardPartial : log.partial(0), dvd, dv, ht, out};
-    launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + g.points(), epi);
+    launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + g.points(), epi, true);
     ctx.interps += 1;
 }
 
@@ -214,7 +214,7 @@ void Solver::state(const double* m0, double* traj, bool guard) {
     launchFieldMax(ctx, g, traj, log.partial(0));
     for (int j = 1; j <= nt; ++j) {
         launchPrefilter(ctx, g, traj + (j - 1) * N, coef_.d(), tmp_.d(), log.flag(j - 1));
-        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), traj + j * N});
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), traj + j * N}, true);
     }
     ctx.interps += nt;
     log.finalize(ctx);
@@ -231,7 +231,7 @@ void Solver::stateFinal(const double* m0, double* out) {
     for (int j = 1; j <= nt; ++j) {
         double* dst = (j == nt) ? out : buf + (j % 2) * N;
         launchPrefilter(ctx, g, cur, coef_.d(), tmp_.d(), log.flag(j - 1));
-        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), dst});
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), dst}, true);
         cur = dst;
     }
     ctx.interps += nt;
@@ -277,21 +277,21 @@ void Solver::incState(const double* vt1, const double* vt2, const double* stateT
     double* c2 = ctx.scratchBuf(13, sizeof(double) * paddedPoints(g.n1, g.n2));
     launchPrefilter(ctx, g, vt1, coef_.d(), tmp_.d(), nullptr);
     launchPrefilter(ctx, g, vt2, c2, tmp_.d(), nullptr);
-    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, vtD, vtD + N});
+    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, vtD, vtD + N}, true);
     ctx.interps += 2;
     gradient(ctx, g, stateTraj, gPrev, gPrev + N);
     fill(ctx, N, 0.0, out);
     for (int j = 1; j <= nt; ++j) {
         launchPrefilter(ctx, g, gPrev, coef_.d(), tmp_.d(), nullptr);
         launchPrefilter(ctx, g, gPrev + N, c2, tmp_.d(), nullptr);
-        launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, gD, gD + N});
+        launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, gD, gD + N}, true);
         gradient(ctx, g, stateTraj + j * N, gCur, gCur + N);
         EpiIncState epi{nullptr, vtD, vtD + N, gD, gD + N, vt1, vt2, gCur, gCur + N, 0.5 * ht, out + j * N};
         if (j == 1) {
             launchPointwise(ctx, g, epi);  // m~_0 = 0
         } else {
             launchPrefilter(ctx, g, out + (j - 1) * N, coef_.d(), tmp_.d(), nullptr);
-            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi);
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
         }
         ctx.interps += 3;
         std::swap(gPrev, gCur);
