@@ -135,6 +135,8 @@ KERNEL_CLASSES = {
     2: ("prefilter rows+cols (K1)", 2 * NT + 1, 4),
     3: ("evaluate/store2 (K2, vt_D)", 1, 6),
     4: ("prefilter cols only (K1 column pass)", 0, 2),  # included in id 2; breakdown only
+    5: ("reference: field copy D2D (not in matvec)", 0, 2),
+    6: ("reference: field axpy kernel (not in matvec)", 0, 3),
 }
 
 

@@ -17,7 +17,8 @@ struct EpiTrace {
     double* x2;
     int n2;
     double h1, h2, sgnHalfHt;
-    __device__ double operator()(std::size_t p, const double* vs) const {
+    VRG_NO_PREFETCH
+    __device__ double operator()(std::size_t p, const double* vs, const Pre&) const {
         const int i1 = static_cast<int>(p / n2), i2 = static_cast<int>(p - static_cast<std::size_t>(i1) * n2);
         const double c1 = __dadd_rn(-kPi, __dmul_rn(h1, static_cast<double>(i1)));
         const double c2 = __dadd_rn(-kPi, __dmul_rn(h2, static_cast<double>(i2)));
@@ -33,7 +34,8 @@ struct EpiStateStep {
     static constexpr bool kGuard = true;
     double* guardPartials;
     double* out;
-    __device__ double operator()(std::size_t p, const double* v) const {
+    VRG_NO_PREFETCH
+    __device__ double operator()(std::size_t p, const double* v, const Pre&) const {
         out[p] = v[0];
         return v[0];
     }
@@ -48,11 +50,15 @@ struct EpiContinuity {
     const double* dv;
     double ht;
     double* out;
-    __device__ double operator()(std::size_t p, const double* v) const {
+    struct Pre {
+        double dvDep, dv;
+    };
+    __device__ Pre prefetch(std::size_t p) const { return {dvDep[p], dv[p]}; }
+    __device__ double operator()(std::size_t p, const double* v, const Pre& q) const {
         const double uD = v[0];
-        const double f0 = uD * dvDep[p];
+        const double f0 = uD * q.dvDep;
         const double pred = uD + ht * f0;
-        const double o = uD + 0.5 * ht * (f0 + pred * dv[p]);
+        const double o = uD + 0.5 * ht * (f0 + pred * q.dv);
         out[p] = o;
         return o;
     }
@@ -73,12 +79,19 @@ struct EpiIncState {
     const double* g2;
     double halfHt;
     double* out;
-    __device__ double operator()(std::size_t p, const double* v) const {
+    // the whole source term is independent of the gathered value
+    struct Pre {
+        double s;
+    };
+    __device__ Pre prefetch(std::size_t p) const {
         // GD_j / G_j are read once per matvec: streamed with evict-first so the per-matvec
         // fields (vt, vt_D, X_D) stay L2-resident across the nt steps
         const double sPrevD = -(vt1D[p] * __ldcs(gd1 + p) + vt2D[p] * __ldcs(gd2 + p));
         const double sCur = -(vt1[p] * __ldcs(g1 + p) + vt2[p] * __ldcs(g2 + p));
-        const double o = v[0] + halfHt * (sPrevD + sCur);
+        return {halfHt * (sPrevD + sCur)};
+    }
+    __device__ double operator()(std::size_t p, const double* v, const Pre& q) const {
+        const double o = v[0] + q.s;
         if (out) out[p] = o;  // null in the fused band path (only the row-filtered field is kept)
         return o;
     }

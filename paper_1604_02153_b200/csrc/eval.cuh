@@ -15,6 +15,13 @@ namespace vrg {
 
 constexpr int kEvalBlock = 256;
 
+// Epilogues declare `Pre` (operands loaded before the gather, see k_evaluate) and
+// `prefetch(p)`; those without early operands use NoPre.
+struct NoPre {};
+#define VRG_NO_PREFETCH                 \
+    using Pre = NoPre;                  \
+    __device__ Pre prefetch(std::size_t) const { return {}; }
+
 // Coefficient fields in the periodically padded layout ((n1+3) x (n2+3), see cellBase).
 template <int NF>
 struct CoeffSet {
@@ -38,26 +45,44 @@ __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const 
         const int b2 = cellBase(__ldg(x2 + p), n2 * (1.0 / kTwoPi), n2, w2);
         base = b1 * (n2 + 3) + b2;
     }
+    // epilogue operands that no in-flight kernel writes (per-iterate fields) are loaded now,
+    // so their latency overlaps the departure-point loads and the gather
+    typename Epi::Pre pre{};
+    if (p < N) pre = epi.prefetch(p);
     if (xStable) pdlWait();
     pdlTrigger();
     if (p < N) {
         const int PW = n2 + 3;
-        double val[NF];
+        // all 16 (x NF) taps are issued before any is consumed (one memory latency, not four)
+        double tap[NF][16];
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             const double* c0 = cs.c[f] + base;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) tap[f][4 * a + b] = __ldg(c0 + a * PW + b);
+        }
+        // pin the taps in registers here: ptxas otherwise interleaves loads and FMAs in small
+        // groups to save registers, serialising several memory latencies per thread
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) asm volatile("" : "+d"(tap[f][i]));
+        double val[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
             double acc = 0.0;
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-                const double* row = c0 + a * PW;
                 double rowAcc = 0.0;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * __ldg(row + b);
+                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * tap[f][4 * a + b];
                 acc += w1[a] * rowAcc;
             }
             val[f] = acc;
         }
-        const double gv = fabs(epi(p, val));
+        const double gv = fabs(epi(p, val, pre));
         if (gv == gv) guard = gv;  // NaN ignored, inf kept
     }
     if constexpr (Epi::kGuard) {
@@ -83,7 +108,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi
     pdlTrigger();
     if (p < N) {
         const double z[2] = {0.0, 0.0};
-        const double gv = fabs(epi(p, z));
+        const double gv = fabs(epi(p, z, epi.prefetch(p)));
         if (gv == gv) guard = gv;
     }
     if constexpr (Epi::kGuard) {
@@ -126,7 +151,8 @@ struct EpiStore1 {
     static constexpr bool kGuard = false;
     double* guardPartials = nullptr;
     double* out;
-    __device__ double operator()(std::size_t p, const double* v) const {
+    VRG_NO_PREFETCH
+    __device__ double operator()(std::size_t p, const double* v, const Pre&) const {
         out[p] = v[0];
         return 0.0;
     }
@@ -138,7 +164,8 @@ struct EpiStore2 {
     double* guardPartials = nullptr;
     double* out0;
     double* out1;
-    __device__ double operator()(std::size_t p, const double* v) const {
+    VRG_NO_PREFETCH
+    __device__ double operator()(std::size_t p, const double* v, const Pre&) const {
         out0[p] = v[0];
         out1[p] = v[1];
         return 0.0;

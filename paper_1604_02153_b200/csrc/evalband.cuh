@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
                 val += w1[a] * rowAcc;
             }
         }
-        const double o = epi(p, &val);
+        const double o = epi(p, &val, epi.prefetch(p));
         const double ao = fabs(o);
         if (ao == ao) guard = fmax(guard, ao);
         bad |= !isfinite(o);

@@ -31,13 +31,19 @@ struct EpiAdjointBF {
     const double* reg2;
     double* o1;
     double* o2;
-    __device__ double operator()(std::size_t p, const double* v) const {
+    struct Pre {
+        double dvDep, dv, g1, g2;
+    };
+    __device__ Pre prefetch(std::size_t p) const {
+        return {dvDep[p], dv[p], __ldcs(G1 + p), __ldcs(G2 + p)};  // G_j streamed once per matvec
+    }
+    __device__ double operator()(std::size_t p, const double* v, const Pre& q) const {
         const double uD = v[0];
-        const double f0 = uD * dvDep[p];
+        const double f0 = uD * q.dvDep;
         const double pred = uD + ht * f0;
-        const double o = uD + 0.5 * ht * (f0 + pred * dv[p]);
-        const double nb1 = b1[p] + w * (o * __ldcs(G1 + p));  // G_j streamed once per matvec
-        const double nb2 = b2[p] + w * (o * __ldcs(G2 + p));
+        const double o = uD + 0.5 * ht * (f0 + pred * q.dv);
+        const double nb1 = b1[p] + w * (o * q.g1);
+        const double nb2 = b2[p] + w * (o * q.g2);
         if (o1) {
             o1[p] = reg1[p] + nb1;
             o2[p] = reg2[p] + nb2;
@@ -66,7 +72,8 @@ struct EpiAdjointSeed {
     double* b2;
     double* rowLam = nullptr;
     unsigned* flag = nullptr;
-    __device__ double operator()(std::size_t p, const double*) const {
+    VRG_NO_PREFETCH
+    __device__ double operator()(std::size_t p, const double*, const Pre&) const {
         const double l = -1.0 * mt[p];
         if (lam) lam[p] = l;
         if (rowLam) rowLam[p] = -rowLam[p];
@@ -264,6 +271,12 @@ double Hessian::benchKernel(int id, int iters) {
                 break;
             case 4:  // prefilter column pass only (K1 cols)
                 launchPrefilterCols(ctx, g, tmp, coef);
+                break;
+            case 5:  // reference point: one field copy (F read + F write), cudaMemcpyAsync D2D
+                copy(ctx, N, mt, tmp);
+                break;
+            case 6:  // reference point: one field axpy kernel (2F read + F write)
+                axpby(ctx, N, 0.5, mt, 1.0, tmp);
                 break;
             default:  // vtilde at departure (K2, two fields)
                 launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
