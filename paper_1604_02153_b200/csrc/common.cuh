@@ -127,6 +127,8 @@ struct Ctx {
     // Scratch spectra / fields reused across calls (grown on demand, freed with the context).
     std::map<std::pair<int, std::size_t>, DBuf> scratch;
     DBuf reduce;  // reduction scratch (partials + results)
+    DBuf gridSync;  // grid-barrier state (count, generation) of cooperative kernels, zeroed at creation
+    int coopPrefilterBlocks = -1;  // co-resident blocks of the cooperative prefilter (lazy)
     double* hostScalars = nullptr;  // pinned staging for scalar reads
 
     // Kernel launches issued by this library (cuFFT's own kernels are not counted), and an

@@ -1,11 +1,12 @@
-// K2 + K1(rows) fused: B-spline evaluation with the step epilogue over full-width row bands,
+// K2 + K1(rows) fused: B-spline evaluation with the step epilogue, one grid row per block,
 // followed in the same kernel by the row pass of the next step's prefilter.
 //
 // In the matvec time loops every interpolated field (m~_j, lt_j) is produced by the previous
-// step's gather, so the producer can row-filter it while the band is still in shared memory:
-// a block owns B = 4096/n2 whole rows (256 chunks of 16 samples), so the periodic row filter
-// is exact inside the block (chunk-carry form of interp.cu) and only the column pass remains
-// as a separate kernel.  This removes one kernel and one field write+read per step.
+// step's gather, so the producer can row-filter it while the row is still in shared memory:
+// a block owns one whole periodic row, so the row filter is exact inside the block
+// (chunk-carry form of interp.cu) and only the column pass remains a separate kernel.  This
+// removes one kernel and one field write+read per step.  The gather keeps the plain kernel's
+// structure (256 threads, epilogue operands prefetched, programmatic dependent launch).
 #pragma once
 
 #include "eval.cuh"
@@ -14,68 +15,88 @@ namespace vrg {
 
 constexpr int kBandThreads = 256;
 
-// Band kernels need n2 a power of two in [32, 4096] and n1 divisible by 4096/n2.
-inline bool bandFusable(const GridDims& g) {
-    const int n2 = g.n2;
-    if (n2 < 32 || n2 > 4096 || (n2 & (n2 - 1)) != 0) return false;
-    const int B = 4096 / n2;
-    return g.n1 % B == 0;
-}
-
-inline int bandLineStride(int n2) { return (n2 / kL) * kCS; }  // even
+// one block per row; n2 a multiple of 256 up to 4096 (chunks per row <= threads)
+inline bool bandFusable(const GridDims& g) { return g.n2 >= 256 && g.n2 <= 4096 && g.n2 % 256 == 0; }
 
 inline std::size_t bandSmem(const GridDims& g) {
-    const int B = 4096 / g.n2;
-    return sizeof(double) * (static_cast<std::size_t>(B) * bandLineStride(g.n2) + 3 * kBandThreads);
+    const int nc = g.n2 / kL;
+    return sizeof(double) * (static_cast<std::size_t>(nc) * kCS + 3 * nc);
 }
 
-inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n1 / (4096 / g.n2)); }
+inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n1); }
+
+// Without a gather (kGather = false: m~_0 = 0, the first incremental-state step) the epilogue
+// operands come from the immediate predecessor (vt_D), so the kernel waits before any load;
+// with a gather only the coefficient field is produced by the predecessor and the departure
+// points and epilogue operands are loaded before the programmatic-dependency wait.
+// Coefficient load that stays behind griddepcontrol.wait.  The wait sits inside the node loop
+// (first iteration) and ptxas hoists non-coherent (ld.global.nc / __ldg) gathers of the loop
+// body above it, which reads the coefficients before the predecessor column pass has written
+// them (seen in the SASS and as nondeterministic results under graph replay).  A coherent
+// load is ordered by the wait.
+__device__ __forceinline__ double ldAfterWait(const double* p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
 
 template <class Epi, bool kGather>
 __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
-                                                            const double* __restrict__ x2, int n1, int n2,
-                                                            int log2n2, Epi epi, double* __restrict__ rowOut,
-                                                            unsigned* nonfinite) {
+                                                            const double* __restrict__ x2, int n1, int n2, Epi epi,
+                                                            double* __restrict__ rowOut, unsigned* nonfinite) {
+    if (!kGather) {
+        pdlWait();
+        pdlTrigger();
+    }
     extern __shared__ __align__(16) double sm[];
-    const int nc = n2 / kL;         // chunks per row
-    const int B = kBandThreads / nc;  // rows per band
-    const int LS = nc * kCS;
-    const int r0 = blockIdx.x * B;
-    double* E = sm + B * LS;
-    double* F0 = E + kBandThreads;
-    double* P0 = F0 + kBandThreads;
+    const int nc = n2 / kL;
+    double* E = sm + nc * kCS;
+    double* F0 = E + nc;
+    double* P0 = F0 + nc;
     const int t = threadIdx.x;
+    const int r = blockIdx.x;
+    const int per = n2 / kBandThreads;  // nodes per thread (<= 16)
     const int PW = n2 + 3;
     const double inv1 = n1 * (1.0 / kTwoPi), inv2 = n2 * (1.0 / kTwoPi);
 
-    // ---- gather + epilogue, 16 nodes per thread, coalesced along the rows
     double guard = 0.0;
     bool bad = false;
-#pragma unroll 4
-    for (int k = 0; k < 16; ++k) {
-        const int idx = t + kBandThreads * k;
-        const int lr = idx >> log2n2, col = idx - (lr << log2n2);
-        const int p = (r0 + lr) * n2 + col;
-        double val = 0.0;
+    for (int k = 0; k < per; ++k) {
+        const int col = t + kBandThreads * k;
+        const int p = r * n2 + col;
+        double w1[4], w2[4];
+        int base = 0;
         if (kGather) {
-            double w1[4], w2[4];
             const int b1 = cellBase(__ldg(x1 + p), inv1, n1, w1);
             const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
-            const double* c0 = cs.c[0] + b1 * PW + b2;
+            base = b1 * PW + b2;
+        }
+        const typename Epi::Pre pre = epi.prefetch(p);
+        if (kGather && k == 0) {
+            pdlWait();
+            pdlTrigger();
+        }
+        double val = 0.0;
+        if (kGather) {
+            double tap[16];
+            const double* c0 = cs.c[0] + base;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) tap[4 * a + b] = ldAfterWait(c0 + a * PW + b);
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
-                const double* row = c0 + a * PW;
                 double rowAcc = 0.0;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * __ldg(row + b);
+                for (int b = 0; b < 4; ++b) rowAcc += w2[b] * tap[4 * a + b];
                 val += w1[a] * rowAcc;
             }
         }
-        const double o = epi(p, &val, epi.prefetch(p));
+        const double o = epi(p, &val, pre);
         const double ao = fabs(o);
         if (ao == ao) guard = fmax(guard, ao);
         bad |= !isfinite(o);
-        sm[lr * LS + slot(col)] = o;
+        sm[slot(col)] = o;
     }
     if constexpr (Epi::kGuard) {
         __shared__ double red[kBandThreads / 32];
@@ -91,17 +112,16 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
     // the next prefilter's input check (checkFinite(u, "prefilter"), interp.cpp:76)
     if (__syncthreads_or(bad) && t == 0 && nonfinite) atomicOr(nonfinite, 1u);
 
-    // ---- row pass of the prefilter on the band (exact: whole periodic rows in the block)
-    const int l = t / nc, c = t - l * nc;
-    double2* s2 = reinterpret_cast<double2*>(sm + l * LS + c * kCS);
+    // ---- row pass of the prefilter (exact: the whole periodic row is in the block)
     double f[kL];
+    double2* s2 = reinterpret_cast<double2*>(sm + t * kCS);
+    if (t < nc) {
 #pragma unroll
-    for (int k = 0; k < kL / 2; ++k) {
-        const double2 v = s2[k];
-        f[2 * k] = v.x;
-        f[2 * k + 1] = v.y;
-    }
-    {
+        for (int k = 0; k < kL / 2; ++k) {
+            const double2 v = s2[k];
+            f[2 * k] = v.x;
+            f[2 * k + 1] = v.y;
+        }
         double b = 0.0;
 #pragma unroll
         for (int k = kL - 2; k >= 0; --k) b = kZ * (f[k + 1] + b);
@@ -113,13 +133,13 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
         P0[t] = b;
     }
     __syncthreads();
-    {
+    if (t < nc) {
         const ZPow zp;
-        const int base = l * nc;
+        const int c = t;
         const int cm1 = c == 0 ? nc - 1 : c - 1, cm2 = cm1 == 0 ? nc - 1 : cm1 - 1;
         const int cp1 = c == nc - 1 ? 0 : c + 1, cp2 = cp1 == nc - 1 ? 0 : cp1 + 1;
-        const double cp = E[base + cm1] + zp.p[kL] * E[base + cm2];
-        const double cm = kZ * (F0[base + cp1] + P0[base + cp1]) + zp.p[kL + 1] * (F0[base + cp2] + P0[base + cp2]);
+        const double cp = E[cm1] + zp.p[kL] * E[cm2];
+        const double cm = kZ * (F0[cp1] + P0[cp1]) + zp.p[kL + 1] * (F0[cp2] + P0[cp2]);
         double ym[kL];
         ym[kL - 1] = cm;
 #pragma unroll
@@ -135,27 +155,19 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
         }
     }
     __syncthreads();
-    double* dst = rowOut + static_cast<std::size_t>(r0) * n2;
-#pragma unroll 4
-    for (int k = 0; k < 16; ++k) {
-        const int idx = t + kBandThreads * k;
-        const int lr = idx >> log2n2, col = idx - (lr << log2n2);
-        dst[idx] = sm[lr * LS + slot(col)];
+    double* dst = rowOut + static_cast<std::size_t>(r) * n2;
+    for (int k = 0; k < per; ++k) {
+        const int col = t + kBandThreads * k;
+        dst[col] = sm[slot(col)];
     }
 }
 
 template <class Epi, bool kGather>
 void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x1, const double* x2, const Epi& epi,
                     double* rowOut, unsigned* nonfinite) {
-    int log2n2 = 0;
-    while ((1 << log2n2) < g.n2) ++log2n2;
-    {
-        LaunchScope ls_(ctx, Epi::kName);
-        k_eval_band<Epi, kGather><<<bandBlocks(g), kBandThreads, bandSmem(g), ctx.stream>>>(cs, x1, x2, g.n1, g.n2,
-                                                                                            log2n2, epi, rowOut,
-                                                                                            nonfinite);
-    }
-    VRG_LAUNCH_CHECK();
+    LaunchScope ls_(ctx, Epi::kName);
+    launchPdl(1, k_eval_band<Epi, kGather>, dim3(bandBlocks(g)), dim3(kBandThreads), bandSmem(g), ctx.stream, cs, x1,
+              x2, g.n1, g.n2, epi, rowOut, nonfinite);
 }
 
 }  // namespace vrg

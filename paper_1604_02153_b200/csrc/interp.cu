@@ -200,25 +200,19 @@ __device__ __forceinline__ void cpAsync16(double* dst, const double* src) {
 // kR: interior samples per segment (compile time, so every staging loop fully unrolls);
 // the block has kLines * (kR/16 + 4) threads, one per chunk.
 template <bool kRows, bool kPadOut, int kR>
-__global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* __restrict__ in,
-                                                                 double* __restrict__ out, int n1, int n2, int LS,
-                                                                 unsigned* nonfinite) {
-    extern __shared__ __align__(16) double sm[];
-    pdlWait();  // the input is the predecessor's output
-    pdlTrigger();
+__device__ __forceinline__ void pfSeg(const double* __restrict__ in, double* __restrict__ out, int n1, int n2, int LS,
+                                      unsigned* nonfinite, int bx, int by, int t, double* sm, bool active) {
     constexpr int S = kR + 2 * kHalo;   // samples staged per line
     constexpr int nch = S / kL;         // chunks per line segment
     constexpr int NT = kLines * nch;    // threads
     const int n = kRows ? n2 : n1;      // line length
     const int nLines = kRows ? n1 : n2;
-    const int p0 = blockIdx.x * kR;     // first interior position
-    const int l0 = blockIdx.y * kLines;
-    const int lines = min(kLines, nLines - l0);
+    const int p0 = bx * kR;             // first interior position
+    const int l0 = by * kLines;
+    const int lines = active ? min(kLines, nLines - l0) : 0;  // inactive: barriers only
     double* E = sm + kLines * LS;
     double* F0 = E + kLines * nch;
     double* P0 = F0 + kLines * nch;
-    const int t = threadIdx.x;
-
     // ---- stage global -> shared (periodic halo)
     if (kRows) {
         // S/2 pairs per line, 8 pairs per thread (kLines * S/2 = 8 * NT)
@@ -253,11 +247,11 @@ __global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* _
 
     // ---- phase 1: zero-state chunk summaries
     const int l = t / nch, c = t - l * nch;
-    const bool active = l < lines;
+    const bool mine = l < lines;
     double2* s2 = reinterpret_cast<double2*>(sm + l * LS + c * kCS);
     double f[kL];
     bool bad = false;
-    if (active) {
+    if (mine) {
 #pragma unroll
         for (int k = 0; k < kL / 2; ++k) {
             const double2 v = s2[k];
@@ -283,7 +277,7 @@ __global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* _
         __syncthreads();
     }
     // ---- phase 2: both recurrences again from the true chunk-boundary states
-    if (active && c >= 2 && c < nch - 2) {
+    if (mine && c >= 2 && c < nch - 2) {
         const ZPow zp;
         const double cp = E[t - 1] + zp.p[kL] * E[t - 2];  // true y+ before the chunk
         const double cm = kZ * (F0[t + 1] + P0[t + 1]) + zp.p[kL + 1] * (F0[t + 2] + P0[t + 2]);
@@ -352,6 +346,16 @@ __global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* _
     }
 }
 
+template <bool kRows, bool kPadOut, int kR>
+__global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* __restrict__ in,
+                                                                 double* __restrict__ out, int n1, int n2, int LS,
+                                                                 unsigned* nonfinite) {
+    extern __shared__ __align__(16) double sm[];
+    pdlWait();  // the input is the predecessor's output
+    pdlTrigger();
+    pfSeg<kRows, kPadOut, kR>(in, out, n1, n2, LS, nonfinite, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
+}
+
 // Periodic padding of an unpadded field (for coefficient sets that arrive unpadded).
 __global__ void k_pad(const double* __restrict__ c, double* __restrict__ out, int n1, int n2) {
     const int PW = n2 + 3, PH = n1 + 3;
@@ -369,6 +373,16 @@ __global__ void k_unpad(const double* __restrict__ pc, double* __restrict__ out,
     const int i = blockIdx.y;
     if (j >= n2) return;
     out[static_cast<std::size_t>(i) * n2 + j] = pc[static_cast<std::size_t>(i + 1) * (n2 + 3) + j + 1];
+}
+
+bool coopPrefilter() {
+    static const bool on = [] {
+        // opt-in: one cooperative launch (rows, grid barrier, columns) measured no faster than
+        // the two launches on B200 at 1024^2 (12.35 us either way; matvec 0.93 vs 0.87 ms)
+        const char* e = std::getenv("VRG_COOP_PREFILTER");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 
 struct SegPlan {
@@ -419,16 +433,21 @@ void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in,
 constexpr int kColW = 16;
 
 template <int kR>
-__global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const double* __restrict__ in,
-                                                                     double* __restrict__ out, int n1, int n2) {
+struct ColsShared {
+    static constexpr int kCR = kR / kL + 4;
+    double E[kCR][kColW], F0[kCR][kColW], P0[kCR][kColW];
+};
+
+// One column segment (block coordinates bx = row segment, by = column group); all threads of
+// the block take part in the barrier whether or not their column exists (loop-safe).
+template <int kR>
+__device__ __forceinline__ void pfColsReg(const double* __restrict__ in, double* __restrict__ out, int n1, int n2,
+                                          int bx, int by, int t, ColsShared<kR>& sh) {
     constexpr int kCR = kR / kL + 4;
-    __shared__ double E[kCR][kColW], F0[kCR][kColW], P0[kCR][kColW];
-    pdlWait();  // the input is the predecessor's output
-    pdlTrigger();
-    const int col = threadIdx.x & (kColW - 1);
-    const int cr = threadIdx.x / kColW;
-    const int gc = blockIdx.y * kColW + col;
-    const int p0 = blockIdx.x * kR;
+    const int col = t & (kColW - 1);
+    const int cr = t / kColW;
+    const int gc = by * kColW + col;
+    const int p0 = bx * kR;
     const bool active = gc < n2;
     double f[kL];
     if (active) {
@@ -446,40 +465,102 @@ __global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const doubl
         double a = 0.0;
 #pragma unroll
         for (int k = 0; k < kL; ++k) a = f[k] + kZ * a;
-        E[cr][col] = a;
-        F0[cr][col] = f[0];
-        P0[cr][col] = b;
+        sh.E[cr][col] = a;
+        sh.F0[cr][col] = f[0];
+        sh.P0[cr][col] = b;
     }
     __syncthreads();
-    if (!active || cr < 2 || cr >= kCR - 2) return;
-    const ZPow zp;
-    const double cp = E[cr - 1][col] + zp.p[kL] * E[cr - 2][col];
-    const double cm = kZ * (F0[cr + 1][col] + P0[cr + 1][col]) + zp.p[kL + 1] * (F0[cr + 2][col] + P0[cr + 2][col]);
-    double ym[kL];
-    ym[kL - 1] = cm;
+    if (active && cr >= 2 && cr < kCR - 2) {
+        const ZPow zp;
+        const double cp = sh.E[cr - 1][col] + zp.p[kL] * sh.E[cr - 2][col];
+        const double cm = kZ * (sh.F0[cr + 1][col] + sh.P0[cr + 1][col]) +
+                          zp.p[kL + 1] * (sh.F0[cr + 2][col] + sh.P0[cr + 2][col]);
+        double ym[kL];
+        ym[kL - 1] = cm;
 #pragma unroll
-    for (int k = kL - 2; k >= 0; --k) ym[k] = kZ * (f[k + 1] + ym[k + 1]);
-    const int PW = n2 + 3;
-    const int colX = gc == n2 - 1 ? 0 : (gc == 0 ? n2 + 1 : (gc == 1 ? n2 + 2 : -1));
-    const int r0 = p0 + (cr - 2) * kL;  // first output row
-    const bool edgeRows = r0 == 0 || r0 + kL == n1;
-    double yp = cp;
+        for (int k = kL - 2; k >= 0; --k) ym[k] = kZ * (f[k + 1] + ym[k + 1]);
+        const int PW = n2 + 3;
+        const int colX = gc == n2 - 1 ? 0 : (gc == 0 ? n2 + 1 : (gc == 1 ? n2 + 2 : -1));
+        const int r0 = p0 + (cr - 2) * kL;  // first output row
+        const bool edgeRows = r0 == 0 || r0 + kL == n1;
+        double yp = cp;
 #pragma unroll
-    for (int k = 0; k < kL; ++k) {
-        yp = f[k] + kZ * yp;
-        const double v = kSqrt3 * (yp + ym[k]);
-        const int q = r0 + k;
-        double* r1 = out + static_cast<std::size_t>(q + 1) * PW;
-        r1[gc + 1] = v;
-        if (colX >= 0) r1[colX] = v;
-        if (edgeRows) {
-            const int rowX = q == n1 - 1 ? 0 : (q == 0 ? n1 + 1 : (q == 1 ? n1 + 2 : -1));
-            if (rowX >= 0) {
-                double* r2 = out + static_cast<std::size_t>(rowX) * PW;
-                r2[gc + 1] = v;
-                if (colX >= 0) r2[colX] = v;
+        for (int k = 0; k < kL; ++k) {
+            yp = f[k] + kZ * yp;
+            const double v = kSqrt3 * (yp + ym[k]);
+            const int q = r0 + k;
+            double* r1 = out + static_cast<std::size_t>(q + 1) * PW;
+            r1[gc + 1] = v;
+            if (colX >= 0) r1[colX] = v;
+            if (edgeRows) {
+                const int rowX = q == n1 - 1 ? 0 : (q == 0 ? n1 + 1 : (q == 1 ? n1 + 2 : -1));
+                if (rowX >= 0) {
+                    double* r2 = out + static_cast<std::size_t>(rowX) * PW;
+                    r2[gc + 1] = v;
+                    if (colX >= 0) r2[colX] = v;
+                }
             }
         }
+    }
+}
+
+template <int kR>
+__global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const double* __restrict__ in,
+                                                                     double* __restrict__ out, int n1, int n2) {
+    __shared__ ColsShared<kR> sh;
+    pdlWait();  // the input is the predecessor's output
+    pdlTrigger();
+    pfColsReg<kR>(in, out, n1, n2, blockIdx.x, blockIdx.y, threadIdx.x, sh);
+}
+
+// Grid-wide barrier for a cooperatively launched grid (all blocks co-resident): arrive on a
+// counter, the last block bumps the generation that the others spin on.
+__device__ __forceinline__ void gridBarrier(unsigned* count, unsigned* generation, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = generation;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *count = 0;
+            __threadfence();
+            atomicAdd(generation, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Both prefilter passes in one cooperative launch: row segments (two 160-thread halves per
+// block, kLines lines each) -> grid barrier -> column segments (320 threads).  Saves a kernel
+// boundary per prefilter.  kR = 256 only (R/16 + 4 = 20 chunks: 8*20 = 160, 16*20 = 320).
+constexpr int kCoopThreads = 320;
+
+__global__ void __launch_bounds__(kCoopThreads) k_pf_coop(const double* __restrict__ u, double* __restrict__ tmp,
+                                                          double* __restrict__ c, int n1, int n2, int LS,
+                                                          unsigned* nonfinite, unsigned* barrier) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ ColsShared<256> sh;
+    pdlWait();
+    const int half = threadIdx.x >= 160 ? 1 : 0;
+    const int th = threadIdx.x - 160 * half;
+    const int halfSmem = kLines * LS + 3 * kLines * 20;
+    const int segX = n2 / 256, rowItems = segX * ((n1 + kLines - 1) / kLines);
+    for (int base = 2 * blockIdx.x; base < rowItems; base += 2 * gridDim.x) {
+        const int item = base + half;
+        const bool active = item < rowItems;
+        pfSeg<true, false, 256>(u, tmp, n1, n2, LS, nonfinite, active ? item % segX : 0, active ? item / segX : 0, th,
+                                sm + half * halfSmem, active);
+        __syncthreads();
+    }
+    gridBarrier(barrier, barrier + 1, gridDim.x);
+    pdlTrigger();
+    const int segY = n1 / 256, colItems = segY * ((n2 + kColW - 1) / kColW);
+    for (int item = blockIdx.x; item < colItems; item += gridDim.x) {
+        pfColsReg<256>(tmp, c, n1, n2, item % segY, item / segY, threadIdx.x, sh);
+        __syncthreads();
     }
 }
 
@@ -517,6 +598,38 @@ void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered,
 
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite) {
     const SegPlan pr = segPlan(g.n2), pc = segPlan(g.n1);
+    if (pr.ok && pc.ok && pr.R == 256 && pc.R == 256 && coopPrefilter()) {
+        const int halfSmem = kLines * pr.LS + 3 * kLines * 20;
+        const std::size_t smem = sizeof(double) * 2 * halfSmem;
+        if (ctx.coopPrefilterBlocks < 0) {
+            VRG_CUDA(cudaFuncSetAttribute(k_pf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            int perSM = 0;
+            VRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_pf_coop, kCoopThreads, smem));
+            ctx.coopPrefilterBlocks = perSM * ctx.numSMs;
+        }
+        const int rowItems = (g.n2 / 256) * ((g.n1 + kLines - 1) / kLines);
+        const int colItems = (g.n1 / 256) * ((g.n2 + kColW - 1) / kColW);
+        const int blocks = std::min(ctx.coopPrefilterBlocks, std::max((rowItems + 1) / 2, colItems));
+        if (blocks > 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(blocks);
+            cfg.blockDim = dim3(kCoopThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = ctx.stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeCooperative;
+            attr[0].val.cooperative = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            unsigned* bar = ctx.gridSync.as<unsigned>();
+            {
+                LaunchScope ls_(ctx, "k_prefilter_coop");
+                VRG_CUDA(cudaLaunchKernelEx(&cfg, k_pf_coop, u, tmp, c, g.n1, g.n2, pr.LS, nonfinite, bar));
+            }
+            return;
+        }
+    }
     if (pr.ok && pc.ok) {
         {
             LaunchScope ls_(ctx, "k_prefilter_rows");

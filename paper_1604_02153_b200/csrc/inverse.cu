@@ -125,13 +125,13 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     // lazily-built per-velocity work the reference does on the first apply
     // (charBwd 2 + dvDepBwd 1 interps, divv 3 FFTs; + charFwd 2 if the state was reused)
     lazyInterps_ = 3 + (hadFwd ? 0 : 2);
-    // Opt-in (VRG_FUSED_BANDS=1): the band kernels remove the row-pass kernel per step but
-    // their gather runs at lower occupancy; measured slower on B200 at every size
-    // (ms per matvec, plain vs band: 1024^2 0.93 vs 1.23, 2048^2 3.57 vs 4.18,
-    // 4096^2/nt=32 27.3 vs 29.5), so the plain 3-kernel step is the default.
+    // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
+    // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
+    // 1024^2 on B200 (0.815 vs 0.867 ms).  VRG_FUSED_BANDS=0 selects the plain step.
     const char* env = std::getenv("VRG_FUSED_BANDS");
-    const bool want = env && env[0] == '1';
+    const bool want = !(env && env[0] == '0');
     fused_ = useFusedBands && want && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
+    if (const char* ge = std::getenv("VRG_GRAPHS")) useGraphs = ge[0] != '0';  // debugging switch
     lazyFfts_ = 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     adjLog_.ensure(nt + 1, evalBlocks(g));

@@ -51,6 +51,8 @@ Ctx::Ctx(int dev, cudaStream_t s) : device(dev) {
     VRG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
     l2Bytes = static_cast<std::size_t>(l2);
     reduce.alloc(sizeof(double) * (kReduceBlocks * 4 + 64));
+    gridSync.alloc(64);
+    VRG_CUDA(cudaMemset(gridSync.d(), 0, 64));
     VRG_CUDA(cudaMallocHost(&hostScalars, sizeof(double) * 64));
 }
 
