@@ -128,8 +128,20 @@ KERNEL_BYTES_F = {
 
 
 # Kernel classes of one matvec (vrg_hess_bench_kernel ids): name, launches per matvec at nt,
-# algorithmic bytes per launch in F.
-KERNEL_CLASSES = {
+# algorithmic bytes per launch in F.  Two launch structures: the band
+# path (default where the grid allows it: gather + epilogue + next row pass in one kernel,
+# then the column pass) and the plain 3-kernel step.
+KERNEL_CLASSES_BAND = {
+    7: ("band/incstate (K6 + K1 rows)", NT - 1, 12),      # X(2) coef vtD(2) GD(2) vt(2) G(2) in; rows out
+    8: ("band/adjoint_bodyforce (K5+K8 + K1 rows)", NT - 1, 12),  # X(2) coef dvD dv G(2) b(2) in; b(2) rows out
+    4: ("prefilter column pass (K1 cols)", 2 * NT - 1, 2),
+    1: ("evaluate/adjoint_bodyforce (K5+K8, last step)", 1, 12),
+    2: ("prefilter rows+cols (K1, vt)", 2, 4),
+    3: ("evaluate/store2 (K2, vt_D)", 1, 6),
+    5: ("reference: field copy D2D (not in matvec)", 0, 2),
+    6: ("reference: field axpy kernel (not in matvec)", 0, 3),
+}
+KERNEL_CLASSES_PLAIN = {
     0: ("evaluate/incstate (K6)", NT - 1, 12),
     1: ("evaluate/adjoint_bodyforce (K5+K8)", NT, 12),
     2: ("prefilter rows+cols (K1)", 2 * NT + 1, 4),
@@ -219,7 +231,10 @@ def run_vrg(args, rank, world, local_rank):
 
     # back-to-back timing of each matvec kernel class (roofline denominator)
     kernels = {}
-    for kid, (name, per_mv, bytes_f) in KERNEL_CLASSES.items():
+    band = ctypes.c_int()
+    ctx.check(ctx.lib.vrg_hess_band_path(H.h, ctypes.byref(band)))
+    classes = KERNEL_CLASSES_BAND if band.value else KERNEL_CLASSES_PLAIN
+    for kid, (name, per_mv, bytes_f) in classes.items():
         out_ms = ctypes.c_double()
         ctx.check(ctx.lib.vrg_hess_bench_kernel(H.h, kid, 50, ctypes.byref(out_ms)))
         kernels[name] = {"avg_us": out_ms.value * 1e3, "launches_per_matvec": per_mv,

@@ -128,8 +128,12 @@ int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, doub
 int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajectory */
 /* instrumentation: average ms of one launch of a matvec kernel class (0 incremental-state
  * step, 1 incremental-adjoint + body-force step, 2 prefilter (both passes), 3 two-field
- * evaluate), `iters` back-to-back launches on the context stream (bench.py roofline) */
+ * evaluate, 4 column pass, 5 D2D copy, 6 axpy, 7 band incremental-state step, 8 band
+ * incremental-adjoint step), `iters` back-to-back launches on the context stream (bench.py roofline) */
 int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch);
+/* 1 when the time loops run the band kernels (gather + epilogue + next row pass fused; ids 7
+ * and 8 of vrg_hess_bench_kernel), 0 for the plain 3-kernel step */
+int vrg_hess_band_path(vrg_hess_t h, int* band);
 
 /* evaluateGradient / evaluateObjective (inverse.hpp:60-71); scalars = [objective, mismatch, regTerm] */
 int vrg_evaluate_gradient(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,

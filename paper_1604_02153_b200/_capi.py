@@ -68,6 +68,7 @@ _SIG = {
     "vrg_hess_apply_host": ("ppppp", C.c_int),
     "vrg_hess_state": ("pp", C.c_int),
     "vrg_hess_bench_kernel": ("piip", C.c_int),
+    "vrg_hess_band_path": ("pp", C.c_int),
     "vrg_evaluate_gradient": ("piippppidiippp", C.c_int),
     "vrg_evaluate_objective": ("piippppidiip", C.c_int),
     "vrg_random_bandlimited_field": ("piiup", C.c_int),

@@ -400,6 +400,10 @@ int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_la
     return guarded(h->owner, [&] { *ms_per_launch = h->hess.benchKernel(kernel, iters); });
 }
 
+int vrg_hess_band_path(vrg_hess_t h, int* band) {
+    return guarded(h->owner, [&] { *band = h->hess.bandPath() ? 1 : 0; });
+}
+
 int vrg_hess_state(vrg_hess_t h, double* traj) {
     return guarded(h->owner, [&] {
         const std::size_t N = h->hess.g.points();

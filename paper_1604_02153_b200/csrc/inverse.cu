@@ -278,6 +278,20 @@ double Hessian::benchKernel(int id, int iters) {
             case 6:  // reference point: one field axpy kernel (2F read + F write)
                 axpby(ctx, N, 0.5, mt, 1.0, tmp);
                 break;
+            case 7: {  // band incremental-state step: gather + epilogue + next row pass
+                if (!fused_) throw NotSupported("bench kernel 7: band path not active on this grid");
+                EpiIncState epi{nullptr, vtD, vtD + N, GD, GD + N, vtD, vtD + N, G, G + N, 0.5 * ht, nullptr};
+                launchEvalBand<EpiIncState, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, tmp, nullptr);
+                break;
+            }
+            case 8: {  // band incremental-adjoint + body-force step
+                if (!fused_) throw NotSupported("bench kernel 8: band path not active on this grid");
+                EpiAdjointBF epi{adjLog_.partial(0), dvd, dv, ht, nullptr, G, G + N, ht, b, b + N,
+                                 nullptr, nullptr, nullptr, nullptr};
+                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, tmp + N,
+                                                   adjLog_.flag(0));
+                break;
+            }
             default:  // vtilde at departure (K2, two fields)
                 launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
                 break;

@@ -92,6 +92,7 @@ private:
 
 public:
     static inline bool useFusedBands = true;  // process-wide switch (tests compare both paths)
+    bool bandPath() const { return fused_; }
 };
 
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
