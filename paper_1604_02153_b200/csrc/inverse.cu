@@ -1,10 +1,13 @@
 // Device GN Hessian matvec: fused SL incremental state (K6), fused SL incremental adjoint +
 // trapezoid body force (K5 + K8), spectral regularisation / Leray / split wrapper (K7, K8).
+#include <cstdio>
 #include <cstdlib>
 
+#include "blas.cuh"
 #include "epilogues.cuh"
 #include "evalband.cuh"
 #include "inverse.cuh"
+#include "wave.cuh"
 
 namespace vrg {
 
@@ -84,6 +87,216 @@ struct EpiAdjointSeed {
     }
 };
 
+// Last incremental-state step with the adjoint seed fused in (GN: lt(1) = -m~(1),
+// inverse.cpp:181; b = w_nt lt(1) grad m_nt): returns lt(1), so the row pass that follows
+// produces the row-filtered adjoint seed directly (the filter is exactly odd, so this equals
+// the band path's in-place negation bit for bit), and writes b with the seed's guard and
+// finiteness record (same arithmetic as EpiAdjointSeed).
+struct EpiIncSeed {
+    static constexpr bool kGuard = true;
+    double* guardPartials;
+    EpiIncState inc;
+    double w;
+    double* b1;
+    double* b2;
+    using Pre = EpiIncState::Pre;
+    __device__ Pre prefetch(std::size_t p) const { return inc.prefetch(p); }
+    __device__ double operator()(std::size_t p, const double* v, const Pre& q) const {
+        const double m = inc(p, v, q);
+        const double l = -1.0 * m;
+        b1[p] = w * (l * inc.g1[p]);
+        b2[p] = w * (l * inc.g2[p]);
+        return l;
+    }
+};
+
+// Persistent wavefront kernel of the data term (wave.cuh).  Phases q = 0 .. 2nt-1: q < nt is
+// incremental-state step j = q+1, q >= nt is incremental-adjoint step j = 2nt-q.  Each phase
+// q >= 1 first has column tasks B(q, s, cg) (column pass of the row-filtered field of phase
+// q-1 into C[q&1]), then row tasks A(q, r) (gather from C[q&1] + epilogue + row pass into
+// R[q&1]).  Queue order = phase order, so dependencies always point backwards.
+// Within a phase the rows and segments are visited from a rotating start (waveStart): on the
+// periodic grid a fixed start would make the first column tasks of every phase wait for the
+// last rows of the previous one (their halo wraps), serialising the phases; rotated by two
+// segments per phase, the first tasks of phase q only need the first rows of phase q-1.
+__device__ __forceinline__ int waveSegStart(int q, int nseg) { return (2 * q) % nseg; }
+struct WaveArgs {
+    int n1, n2, nt, SR, CW, nseg, ncg, ngrp, dRows, ySmemOffset;
+    long long total;
+    double* C[2];
+    double* R[2];
+    const double* Xf;
+    const double* Xb;
+    const double* vtD;
+    const double* vt1;
+    const double* vt2;
+    const double* G;   // (nt+1) x [g1 | g2]
+    const double* GD;  // nt x [gd1 | gd2]
+    const double* dvd;
+    const double* dv;
+    double ht;
+    double* b1;
+    double* b2;
+    const double* reg1;
+    const double* reg2;
+    double* o1;
+    double* o2;
+    double* partials;
+    unsigned blocksPerStep;
+    unsigned* flags;
+    unsigned* next;     // task counter
+    unsigned* grpA;     // [2nt][ngrp] rows done per row group
+    unsigned* segB;     // [2nt][nseg] column tasks done per segment
+    unsigned* stepA;    // [2nt]
+    unsigned* stepB;    // [2nt]
+};
+
+#ifndef VRG_WAVE_MINB
+#define VRG_WAVE_MINB 3  // resident blocks per SM (register cap 80: no spills)
+#endif
+#ifdef VRG_WAVE_STATS
+// instrumentation build: per kind (A, B) summed wait cycles, work cycles, task count; dispatch
+__device__ unsigned long long gWaveStats[8];
+#define WAVE_T(x) const long long x = clock64()
+#define WAVE_ADD(i, v) \
+    if (t == 0) atomicAdd(&gWaveStats[i], static_cast<unsigned long long>(v))
+#else
+#define WAVE_T(x)
+#define WAVE_ADD(i, v)
+#endif
+
+__global__ void __launch_bounds__(kWaveThreads, VRG_WAVE_MINB) k_wave(WaveArgs args) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[kWaveThreads / 32];
+    __shared__ unsigned sTask;
+    // The arguments are read from shared memory inside the task loop: read from the parameter
+    // space they would be hoisted out of the loop and held in registers across all tasks.
+    __shared__ WaveArgs sa;
+    const int t = threadIdx.x;
+    if (t == 0) sa = args;
+    __syncthreads();
+    const WaveArgs& a = sa;
+    double* Y = sm + a.ySmemOffset;
+    for (;;) {
+        WAVE_T(tD0);
+        if (t == 0) sTask = atomicAdd(a.next, 1u);
+        __syncthreads();
+        const long long id = sTask;
+        __syncthreads();
+        if (id >= a.total) return;
+        WAVE_T(tD1);
+        WAVE_ADD(6, tD1 - tD0);
+        const std::size_t N = static_cast<std::size_t>(a.n1) * a.n2;
+        const int Q = 2 * a.nt;
+        const int nB = a.nseg * a.ncg;
+        const int per = nB + a.n1;
+        int q, k;
+        if (id < a.n1) {
+            q = 0;
+            k = nB + static_cast<int>(id);
+        } else {
+            const long long id1 = id - a.n1;
+            q = 1 + static_cast<int>(id1 / per);
+            k = static_cast<int>(id1 % per);
+        }
+        if (k < nB) {
+            // ---- column task B(q, s, cg)
+            const int si = k / a.ncg, cg = k - si * a.ncg;
+            const int s = (waveSegStart(q, a.nseg) + si) % a.nseg;
+            const int gPerSeg = a.SR / kWaveRG, hg = kWaveHalo / kWaveRG;
+            const int ng = gPerSeg + 2 * hg;
+            if (t < ng) {
+                int gi = s * gPerSeg - hg + t;
+                gi += gi < 0 ? a.ngrp : 0;
+                gi -= gi >= a.ngrp ? a.ngrp : 0;
+                waitAtLeast(a.grpA + static_cast<std::size_t>(q - 1) * a.ngrp + gi, kWaveRG);
+            }
+            if (t == 0 && q >= 2) waitAtLeast(a.stepA + q - 2, a.n1);  // C[q&1] free (read by A(q-2))
+            __syncthreads();
+            WAVE_T(tB1);
+            waveColsTask(a.R[(q - 1) & 1], a.C[q & 1], a.n1, a.n2, a.SR, a.CW, s, cg, sm, Y);
+            signalDone(a.segB + static_cast<std::size_t>(q) * a.nseg + s, a.stepB + q);
+            WAVE_T(tB2);
+            WAVE_ADD(3, tB1 - tD1);
+            WAVE_ADD(4, tB2 - tB1);
+            WAVE_ADD(5, 1);
+            continue;
+        }
+        // ---- row task A(q, r): rows from one segment past the phase's first segment
+        const int r = ((waveSegStart(q, a.nseg) + 1) * a.SR + (k - nB)) % a.n1;
+        if (q >= 1 && t == 0) {
+            if (q >= 2) waitAtLeast(a.stepB + q - 1, nB);  // R[q&1] free (read by B(q-1))
+            const int lo = r - a.dRows, hi = r + a.dRows;
+            if (hi - lo + 1 >= a.n1) {
+                for (int s = 0; s < a.nseg; ++s) waitAtLeast(a.segB + static_cast<std::size_t>(q) * a.nseg + s, a.ncg);
+            } else {
+                const int s0 = (lo < 0 ? lo - a.SR + 1 : lo) / a.SR, s1 = hi / a.SR;  // floor division
+                for (int s = s0; s <= s1; ++s) {
+                    const int sw = ((s % a.nseg) + a.nseg) % a.nseg;
+                    waitAtLeast(a.segB + static_cast<std::size_t>(q) * a.nseg + sw, a.ncg);
+                }
+            }
+        }
+        __syncthreads();
+        WAVE_T(tA1);
+        WAVE_ADD(0, tA1 - tD1);
+        double* rowOut = a.R[q & 1];
+        const double* coef = a.C[q & 1];
+        if (q < a.nt) {
+            const int j = q + 1;
+            const double* Gj = a.G + static_cast<std::size_t>(j) * 2 * N;
+            const double* GDj = a.GD + static_cast<std::size_t>(j - 1) * 2 * N;
+            const EpiIncState inc{nullptr, a.vtD, a.vtD + N, GDj, GDj + N, a.vt1, a.vt2, Gj, Gj + N, 0.5 * a.ht, nullptr};
+            if (j == a.nt) {
+                const EpiIncSeed seed{a.partials + static_cast<std::size_t>(a.nt) * a.blocksPerStep, inc,
+                                      a.ht * 0.5, a.b1, a.b2};
+                if (q == 0)
+                    waveRowTask<EpiIncSeed, false, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, seed, rowOut,
+                                                         a.flags + a.nt, sm, red, Y);
+                else
+                    waveRowTask<EpiIncSeed, true, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, seed, rowOut,
+                                                        a.flags + a.nt, sm, red, Y);
+            } else if (q == 0) {
+                waveRowTask<EpiIncState, false, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, inc, rowOut, nullptr, sm,
+                                                      red, Y);
+            } else {
+                waveRowTask<EpiIncState, true, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, inc, rowOut, nullptr, sm,
+                                                     red, Y);
+            }
+        } else {
+            const int j = Q - q;  // adjoint step j -> lt_{j-1}
+            const double w = a.ht * ((j - 1 == 0 || j - 1 == a.nt) ? 0.5 : 1.0);
+            const double* Gm = a.G + static_cast<std::size_t>(j - 1) * 2 * N;
+            const bool last = j == 1;
+            const EpiAdjointBF epi{a.partials + static_cast<std::size_t>(j - 1) * a.blocksPerStep, a.dvd, a.dv, a.ht,
+                                   nullptr, Gm, Gm + N, w, a.b1, a.b2, a.reg1, a.reg2, last ? a.o1 : nullptr,
+                                   last ? a.o2 : nullptr};
+            if (last)
+                waveRowTask<EpiAdjointBF, true, false>(coef, a.Xb, a.Xb + N, a.n1, a.n2, r, epi, rowOut, nullptr, sm,
+                                                       red, Y);
+            else
+                waveRowTask<EpiAdjointBF, true, true>(coef, a.Xb, a.Xb + N, a.n1, a.n2, r, epi, rowOut,
+                                                      a.flags + (j - 1), sm, red, Y);
+        }
+        signalDone(a.grpA + static_cast<std::size_t>(q) * a.ngrp + r / kWaveRG, a.stepA + q);
+        WAVE_T(tA2);
+        WAVE_ADD(1, tA2 - tA1);
+        WAVE_ADD(2, 1);
+    }
+}
+
+// |departure - arrival| along axis 1 in grid cells (minimum image), per node.
+__global__ void k_row_disp(const double* __restrict__ x1, int n1, int n2, double* __restrict__ out) {
+    const std::size_t N = static_cast<std::size_t>(n1) * n2;
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const double h = kTwoPi / n1;
+    const double xa = -kPi + static_cast<double>(p / n2) * h;
+    double d = x1[p] - xa;
+    d -= kTwoPi * floor((d + kPi) / kTwoPi);
+    out[p] = fabs(d) / h;
+}
+
 }  // namespace
 
 Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2, const double* mR, const double* mT,
@@ -132,6 +345,7 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     const bool want = !(env && env[0] == '0');
     fused_ = useFusedBands && want && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
     if (const char* ge = std::getenv("VRG_GRAPHS")) useGraphs = ge[0] != '0';  // debugging switch
+    setupWave();
     lazyFfts_ = 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     adjLog_.ensure(nt + 1, evalBlocks(g));
@@ -143,6 +357,47 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
         ctx.plan(g, CUFFT_Z2D, batch);
     }
     ctx.sync();
+}
+
+// Wavefront path (k_wave, opt-in with VRG_WAVE=1 on the band-path grids): correct and bit-
+// identical to the band path, but slower on B200 (1024^2 nt=16: 871 vs 1226 matvec/s): the
+// step is memory bound either way, and the persistent kernel's row tasks run ~15% slower per
+// row than the band kernel (register cap 80 -> 3 blocks/SM; tasks of two phases share L2) while
+// the dependency waits and dispatch add ~15% (tools/wave_stats.py).  Kept as the starting
+// point for a cross-step (temporally blocked) schedule.
+// The dependency reach of a row task is the largest departure displacement along axis 1 over
+// both characteristics (fixed per Hessian), rounded up, plus the 4-tap stencil and one row of
+// margin; a non-finite departure point makes every row depend on every segment.
+void Hessian::setupWave() {
+    const char* env = std::getenv("VRG_WAVE");
+    wave_ = false;
+    if (!fused_ || !(env && env[0] == '1') || g.n1 % kWaveRG != 0) return;
+    const std::size_t N = g.points();
+    double* d = solver.tmp();
+    double reach = 0.0;
+    bool finite = true;
+    for (int dir : {kForward, kBackward}) {
+        const double* X = solver.departure(dir);
+        k_row_disp<<<grid1d(N, 256), 256, 0, ctx.stream>>>(X, g.n1, g.n2, d);
+        VRG_LAUNCH_CHECK();
+        finite = finite && !anyNonFinite(ctx, N, d);
+        reach = std::max(reach, normLinf(ctx, N, d));
+    }
+    waveDRows_ = finite ? static_cast<int>(std::ceil(reach)) + 3 : g.n1;
+    const char* sr = std::getenv("VRG_WAVE_SR");
+    waveSR_ = sr ? std::atoi(sr) : 128;
+    while (waveSR_ > 32 && (g.n1 % waveSR_ != 0 || g.n2 % waveColsWidth(waveSR_) != 0)) waveSR_ /= 2;
+    if (waveSR_ < 64 || waveSR_ > 256) return;  // halo summaries need 4 CW <= 256 threads
+    waveSmem_ = waveSmemFor(g, waveSR_);
+    if (waveSmem_ > 48 * 1024)
+        VRG_CUDA(cudaFuncSetAttribute(k_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(waveSmem_)));
+    int perSM = 0;
+    VRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_wave, kWaveThreads, waveSmem_));
+    if (perSM < 1) return;
+    waveBlocks_ = perSM * ctx.numSMs;
+    const int Q = 2 * nt, ngrp = g.n1 / kWaveRG, nseg = g.n1 / waveSR_;
+    waveCnt_.alloc(sizeof(unsigned) * (1 + 2 * Q + static_cast<std::size_t>(Q) * (ngrp + nseg)));
+    wave_ = true;
 }
 
 void Hessian::countDataTerm() {
@@ -174,6 +429,78 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     launchPrefilter(ctx, g, vt2, c2, tmp, nullptr);
     launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
     auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
+    if (wave_) {
+        adjLog_.reset(ctx);
+        VRG_CUDA(cudaMemsetAsync(waveCnt_.d(), 0, waveCnt_.bytes(), ctx.stream));
+        const int Q = 2 * nt, ngrp = g.n1 / kWaveRG, nseg = g.n1 / waveSR_, CW = waveColsWidth(waveSR_);
+        const int ncg = g.n2 / CW;
+        unsigned* cnt = waveCnt_.as<unsigned>();
+        WaveArgs a{};
+        a.n1 = g.n1;
+        a.n2 = g.n2;
+        a.nt = nt;
+        a.SR = waveSR_;
+        a.CW = CW;
+        a.ySmemOffset = static_cast<int>(waveSmemBase(g, waveSR_) / sizeof(double));
+        a.nseg = nseg;
+        a.ncg = ncg;
+        a.ngrp = ngrp;
+        a.dRows = waveDRows_;
+        a.total = g.n1 + static_cast<long long>(Q - 1) * (static_cast<long long>(nseg) * ncg + g.n1);
+        a.C[0] = coef;
+        a.C[1] = c2;
+        a.R[0] = tmp;
+        a.R[1] = tmp + N;
+        a.Xf = Xf;
+        a.Xb = Xb;
+        a.vtD = vtD;
+        a.vt1 = vt1;
+        a.vt2 = vt2;
+        a.G = G_.d();
+        a.GD = GD_.d();
+        a.dvd = dvd;
+        a.dv = dv;
+        a.ht = ht;
+        a.b1 = b1;
+        a.b2 = b2;
+        a.reg1 = reg1;
+        a.reg2 = reg2;
+        a.o1 = out1;
+        a.o2 = out2;
+        a.partials = adjLog_.partial(0);
+        a.blocksPerStep = adjLog_.blocks;
+        a.flags = adjLog_.flag(0);
+        a.next = cnt;
+        a.stepA = cnt + 1;
+        a.stepB = cnt + 1 + Q;
+        a.grpA = cnt + 1 + 2 * Q;
+        a.segB = cnt + 1 + 2 * Q + static_cast<std::size_t>(Q) * ngrp;
+#ifdef VRG_WAVE_STATS
+        {
+            unsigned long long z[8] = {};
+            VRG_CUDA(cudaMemcpyToSymbolAsync(gWaveStats, z, sizeof(z), 0, cudaMemcpyHostToDevice, ctx.stream));
+        }
+#endif
+        {
+            LaunchScope ls_(ctx, "wave/matvec");
+            k_wave<<<std::min<long long>(waveBlocks_, a.total), kWaveThreads, waveSmem_, ctx.stream>>>(a);
+            VRG_LAUNCH_CHECK();
+        }
+#ifdef VRG_WAVE_STATS
+        if (!useGraphs || ctx.profOn) {
+            unsigned long long z[8];
+            VRG_CUDA(cudaMemcpyFromSymbolAsync(z, gWaveStats, sizeof(z), 0, cudaMemcpyDeviceToHost, ctx.stream));
+            VRG_CUDA(cudaStreamSynchronize(ctx.stream));
+            std::fprintf(stderr,
+                         "wave stats: blocks %d | A n=%llu wait %.2f us work %.2f us | B n=%llu wait %.2f us work "
+                         "%.2f us | dispatch %.2f us (per task, at 1.965 GHz)\n",
+                         waveBlocks_, z[2], z[0] / 1965.0 / z[2], z[1] / 1965.0 / z[2], z[5], z[3] / 1965.0 / z[5],
+                         z[4] / 1965.0 / z[5], z[6] / 1965.0 / (z[2] + z[5]));
+        }
+#endif
+        adjLog_.finalize(ctx);
+        return;
+    }
     if (fused_) {
         // Band path: every step's gather kernel also row-filters its output (evalband.cuh), so
         // each step is [column pass] + [gather + epilogue + row pass].  R[.] ping-pong holds

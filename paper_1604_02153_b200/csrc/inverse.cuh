@@ -89,10 +89,19 @@ private:
     GuardLog adjLog_;
     long long lazyInterps_ = 0, lazyFfts_ = 0;
     bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh
+    // persistent wavefront kernel for the whole data term (wave.cuh, k_wave)
+    bool wave_ = false;
+    int waveDRows_ = 0;      // rows a gather may reach from its own row (displacement + stencil)
+    int waveSR_ = 0;         // column-pass segment height
+    int waveBlocks_ = 0;     // resident blocks of k_wave
+    std::size_t waveSmem_ = 0;
+    DBuf waveCnt_;           // task counter + dependency counters, zeroed per matvec
+    void setupWave();
 
 public:
     static inline bool useFusedBands = true;  // process-wide switch (tests compare both paths)
     bool bandPath() const { return fused_; }
+    bool wavePath() const { return wave_; }
 };
 
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,

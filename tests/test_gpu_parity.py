@@ -287,20 +287,24 @@ def apply_floor(n, p, beta, vmax, outmax):
     return 4 * 2.2e-16 * beta * kmax2 ** p * vmax / outmax
 
 
-@pytest.mark.parametrize("n1,n2,nt", [(256, 256, 1), (256, 512, 3), (512, 256, 8)])
-def test_band_path_bitexact_vs_plain(ctx, api, monkeypatch, n1, n2, nt):
-    """The fused band step (gather + epilogue + next row pass, evalband.cuh) is the same
-    algorithm as the plain 3-kernel step: data term and full apply agree to rounding (the two
-    kernels' compilers contract different multiply-adds into FMAs: 2.6e-16 seen at n2 = 512,
-    bit-identical at 256), under CUDA-graph replay with programmatic dependent launch (the
-    configuration that exposed a load hoisted above griddepcontrol.wait, rel. error ~1)."""
+@pytest.mark.parametrize("n1,n2,nt", [(256, 256, 1), (256, 512, 3), (512, 256, 8), (1024, 1024, 4)])
+def test_band_and_wave_paths_vs_plain(ctx, api, monkeypatch, n1, n2, nt):
+    """The fused band step (gather + epilogue + next row pass, evalband.cuh) and the persistent
+    wavefront kernel (wave.cuh) are the same algorithm as the plain 3-kernel step: data term
+    and full apply agree to rounding (the kernels' compilers contract different multiply-adds
+    into FMAs: 2.6e-16 seen at n2 = 512, bit-identical at 256), under CUDA-graph replay with
+    programmatic dependent launch (the configuration that exposed a load hoisted above
+    griddepcontrol.wait, rel. error ~1), first call and replay."""
     mT = synth.smoothed_noise(n1, n2, 1000)
     v1, v2 = synth.smooth_velocity(n1, n2, 2000)
     vt1, vt2 = synth.smooth_velocity(n1, n2, 3000)
     F = ctx.field
     res = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("VRG_FUSED_BANDS", mode)
+    for mode, env in (("plain", {"VRG_FUSED_BANDS": "0"}), ("band", {}), ("wave", {"VRG_WAVE": "1"})):
+        for k in ("VRG_FUSED_BANDS", "VRG_WAVE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         H = api.HessianOperator(ctx, (F(0.5 * v1), F(0.5 * v2)), F(mT), F(mT), 2, 1e-3, 0, nt)
         out = []
         for _ in range(2):  # first call captures the graph, second replays it
@@ -309,6 +313,11 @@ def test_band_path_bitexact_vs_plain(ctx, api, monkeypatch, n1, n2, nt):
             out.append([t.cpu().numpy() for t in (*d, *a)])
         res[mode] = out
         del H
-    for k in range(2):
-        for i, (x, y) in enumerate(zip(res["0"][k], res["1"][k])):
-            assert np.abs(x - y).max() <= 1e-13 * np.abs(x).max(), (k, i, np.abs(x - y).max() / np.abs(x).max())
+    for mode in ("band", "wave"):
+        for k in range(2):
+            for i, (x, y) in enumerate(zip(res["plain"][k], res[mode][k])):
+                err = np.abs(x - y).max() / np.abs(x).max()
+                assert err <= 1e-13, (mode, k, i, err)
+    for k in range(2):  # wave and band share every kernel's arithmetic
+        for x, y in zip(res["band"][k], res["wave"][k]):
+            assert np.array_equal(x, y)
