@@ -141,6 +141,8 @@ KERNEL_CLASSES_BAND = {
     5: ("reference: field copy D2D (not in matvec)", 0, 2),
     6: ("reference: field axpy kernel (not in matvec)", 0, 3),
 }
+# ncu kernel-name fragments of the band-path classes (for the traffic lookup)
+NCU_NAMES = {7: "k_eval_band<EpiIncState, 1>", 8: "EpiAdjointBF, 1>", 4: "k_pf_cols_reg"}
 KERNEL_CLASSES_PLAIN = {
     0: ("evaluate/incstate (K6)", NT - 1, 12),
     1: ("evaluate/adjoint_bodyforce (K5+K8)", NT, 12),
@@ -239,7 +241,8 @@ def run_vrg(args, rank, world, local_rank):
         ctx.check(ctx.lib.vrg_hess_bench_kernel(H.h, kid, 50, ctypes.byref(out_ms)))
         kernels[name] = {"avg_us": out_ms.value * 1e3, "launches_per_matvec": per_mv,
                          "bytes_per_launch": bytes_f * F_BYTES,
-                         "gbps": bytes_f * F_BYTES / (out_ms.value / 1e3) / 1e9}
+                         "gbps": bytes_f * F_BYTES / (out_ms.value / 1e3) / 1e9,
+                         "ncu_kernel": NCU_NAMES.get(kid) if band.value else None}
 
     # SL transport unit: one SL state step m_j = I[m_{j-1}](X_D) at 1024^2 (config 4 unit ii)
     sl = sl_step_rate(api, ctx, v_d, mT_d, timed)
@@ -415,6 +418,17 @@ def main():
         except OSError:
             pass
         peak = float(peaks.get("hbm_gbs", 6650.0))
+        # DRAM traffic of the dominant kernel per launch, from the committed ncu --set full
+        # capture (profiles/, cold-cache replay: an upper bound of the warm per-launch traffic)
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+                tmap = json.load(f)
+            pat = kd.get("ncu_kernel")
+            hits = [v for k, v in tmap.items() if pat and pat in k]
+            traffic = hits[0] if hits else None
+        except (OSError, ValueError):
+            pass
         achieved = bytes_launch / avg_s / 1e9 if bytes_launch else None
         prof_total = sum(t for _, t in prof.values())
         mv_bytes = matvec_algorithmic_bytes()
@@ -427,7 +441,8 @@ def main():
             "gpu_launches": r["launches"],
             "clocks": r["clocks"],
             "roofline": {"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_source": "profiles/r1_ncu_traffic.json (ncu --set full, dram__bytes_read+write)",
                          "bytes_per_launch": bytes_launch, "avg_launch_us": avg_s * 1e6,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"},
             "matvec_roofline": {"algorithmic_bytes": mv_bytes, "model": "(24 nt + 12) F, SURVEY 8(d)",

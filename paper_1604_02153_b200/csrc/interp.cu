@@ -430,7 +430,10 @@ void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in,
 // the block), so no shared staging of samples is needed; only the chunk summaries go through
 // shared memory.  kCR = kR/16 + 4 chunk rows (2-chunk periodic halo above and below); output
 // in the padded coefficient layout.
-constexpr int kColW = 16;
+#ifndef VRG_COLW
+#define VRG_COLW 16
+#endif
+constexpr int kColW = VRG_COLW;
 
 template <int kR>
 struct ColsShared {
@@ -572,8 +575,11 @@ void launchColsReg(Ctx& ctx, const GridDims& g, const double* in, double* out) {
 
 // Column pass into the padded layout; false if n1 is not a multiple of 32.
 bool launchColumnPass(Ctx& ctx, const GridDims& g, const double* in, double* out) {
-    const SegPlan pc = segPlan(g.n1);
+    SegPlan pc = segPlan(g.n1);
     if (!pc.ok) return false;
+#ifdef VRG_COLS_RMAX
+    while (pc.R > VRG_COLS_RMAX) pc.R /= 2;
+#endif
     {
         LaunchScope ls_(ctx, "k_prefilter_cols");
         switch (pc.R) {

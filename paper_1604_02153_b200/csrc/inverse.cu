@@ -2,6 +2,9 @@
 // trapezoid body force (K5 + K8), spectral regularisation / Leray / split wrapper (K7, K8).
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "blas.cuh"
 #include "epilogues.cuh"
@@ -111,20 +114,23 @@ struct EpiIncSeed {
 };
 
 // Persistent wavefront kernel of the data term (wave.cuh).  Phases q = 0 .. 2nt-1: q < nt is
-// incremental-state step j = q+1, q >= nt is incremental-adjoint step j = 2nt-q.  Each phase
-// q >= 1 first has column tasks B(q, s, cg) (column pass of the row-filtered field of phase
-// q-1 into C[q&1]), then row tasks A(q, r) (gather from C[q&1] + epilogue + row pass into
-// R[q&1]).  Queue order = phase order, so dependencies always point backwards.
-// Within a phase the rows and segments are visited from a rotating start (waveStart): on the
-// periodic grid a fixed start would make the first column tasks of every phase wait for the
-// last rows of the previous one (their halo wraps), serialising the phases; rotated by two
-// segments per phase, the first tasks of phase q only need the first rows of phase q-1.
-__device__ __forceinline__ int waveSegStart(int q, int nseg) { return (2 * q) % nseg; }
+// incremental-state step j = q+1, q >= nt is incremental-adjoint step j = 2nt-q.  Phase q >= 1
+// has column tasks B(q, s, cg) (column pass of the row-filtered field of phase q-1, ring slot
+// (q-1)%NB of R, into slot q%NB of C) and every phase has row tasks A(q, r) (gather from C slot
+// q%NB + epilogue + row pass into R slot q%NB).
+// Schedule (Hessian::setupWave): the tasks are dispatched in the order of a host-built list
+// sorted by a key that interleaves consecutive phases along the rows -- phase q starts its
+// rows Delta rows after phase q-1 did and K key units later -- so a row's per-velocity data
+// (departure points, vt, vt_D, div v, ...) is re-read by the next step while it is still in
+// L2 (temporal blocking), and each task's dependencies have smaller keys (deadlock free).
+// R and C are rings of NB fields so that several phases can be in flight.
 struct WaveArgs {
-    int n1, n2, nt, SR, CW, nseg, ncg, ngrp, dRows, ySmemOffset;
-    long long total;
-    double* C[2];
-    double* R[2];
+    int n1, n2, nt, SR, CW, nseg, ncg, ngrp, dRows, ySmemOffset, NB;
+    unsigned total;
+    const unsigned* tasks;  // key-sorted task list: q << 20 | kind << 19 | index
+    double* Cring;          // NB padded coefficient fields
+    double* Rring;          // NB row-filtered fields
+    std::size_t cStride;    // padded points
     const double* Xf;
     const double* Xb;
     const double* vtD;
@@ -150,6 +156,7 @@ struct WaveArgs {
     unsigned* stepA;    // [2nt]
     unsigned* stepB;    // [2nt]
 };
+constexpr unsigned kWaveKindB = 1u << 19;
 
 #ifndef VRG_WAVE_MINB
 #define VRG_WAVE_MINB 3  // resident blocks per SM (register cap 80: no spills)
@@ -189,20 +196,13 @@ __global__ void __launch_bounds__(kWaveThreads, VRG_WAVE_MINB) k_wave(WaveArgs a
         const std::size_t N = static_cast<std::size_t>(a.n1) * a.n2;
         const int Q = 2 * a.nt;
         const int nB = a.nseg * a.ncg;
-        const int per = nB + a.n1;
-        int q, k;
-        if (id < a.n1) {
-            q = 0;
-            k = nB + static_cast<int>(id);
-        } else {
-            const long long id1 = id - a.n1;
-            q = 1 + static_cast<int>(id1 / per);
-            k = static_cast<int>(id1 % per);
-        }
-        if (k < nB) {
+        const unsigned code = a.tasks[id];
+        const int q = static_cast<int>(code >> 20);
+        const int idx = static_cast<int>(code & (kWaveKindB - 1));
+        const bool isB = (code & kWaveKindB) != 0;
+        if (isB) {
             // ---- column task B(q, s, cg)
-            const int si = k / a.ncg, cg = k - si * a.ncg;
-            const int s = (waveSegStart(q, a.nseg) + si) % a.nseg;
+            const int s = idx / a.ncg, cg = idx - s * a.ncg;
             const int gPerSeg = a.SR / kWaveRG, hg = kWaveHalo / kWaveRG;
             const int ng = gPerSeg + 2 * hg;
             if (t < ng) {
@@ -211,10 +211,12 @@ __global__ void __launch_bounds__(kWaveThreads, VRG_WAVE_MINB) k_wave(WaveArgs a
                 gi -= gi >= a.ngrp ? a.ngrp : 0;
                 waitAtLeast(a.grpA + static_cast<std::size_t>(q - 1) * a.ngrp + gi, kWaveRG);
             }
-            if (t == 0 && q >= 2) waitAtLeast(a.stepA + q - 2, a.n1);  // C[q&1] free (read by A(q-2))
+            if (t == 0 && q >= a.NB) waitAtLeast(a.stepA + q - a.NB, a.n1);  // C slot free (read by A(q-NB))
             __syncthreads();
             WAVE_T(tB1);
-            waveColsTask(a.R[(q - 1) & 1], a.C[q & 1], a.n1, a.n2, a.SR, a.CW, s, cg, sm, Y);
+            waveColsTask(a.Rring + static_cast<std::size_t>((q - 1) % a.NB) * N,
+                         a.Cring + static_cast<std::size_t>(q % a.NB) * a.cStride, a.n1, a.n2, a.SR, a.CW, s, cg, sm,
+                         Y);
             signalDone(a.segB + static_cast<std::size_t>(q) * a.nseg + s, a.stepB + q);
             WAVE_T(tB2);
             WAVE_ADD(3, tB1 - tD1);
@@ -222,10 +224,10 @@ __global__ void __launch_bounds__(kWaveThreads, VRG_WAVE_MINB) k_wave(WaveArgs a
             WAVE_ADD(5, 1);
             continue;
         }
-        // ---- row task A(q, r): rows from one segment past the phase's first segment
-        const int r = ((waveSegStart(q, a.nseg) + 1) * a.SR + (k - nB)) % a.n1;
+        // ---- row task A(q, r)
+        const int r = idx;
+        if (t == 0 && q >= a.NB) waitAtLeast(a.stepB + q + 1 - a.NB, nB);  // R slot free (read by B(q+1-NB))
         if (q >= 1 && t == 0) {
-            if (q >= 2) waitAtLeast(a.stepB + q - 1, nB);  // R[q&1] free (read by B(q-1))
             const int lo = r - a.dRows, hi = r + a.dRows;
             if (hi - lo + 1 >= a.n1) {
                 for (int s = 0; s < a.nseg; ++s) waitAtLeast(a.segB + static_cast<std::size_t>(q) * a.nseg + s, a.ncg);
@@ -240,8 +242,8 @@ __global__ void __launch_bounds__(kWaveThreads, VRG_WAVE_MINB) k_wave(WaveArgs a
         __syncthreads();
         WAVE_T(tA1);
         WAVE_ADD(0, tA1 - tD1);
-        double* rowOut = a.R[q & 1];
-        const double* coef = a.C[q & 1];
+        double* rowOut = a.Rring + static_cast<std::size_t>(q % a.NB) * N;
+        const double* coef = a.Cring + static_cast<std::size_t>(q % a.NB) * a.cStride;
         if (q < a.nt) {
             const int j = q + 1;
             const double* Gj = a.G + static_cast<std::size_t>(j) * 2 * N;
@@ -359,12 +361,13 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     ctx.sync();
 }
 
-// Wavefront path (k_wave, opt-in with VRG_WAVE=1 on the band-path grids): correct and bit-
-// identical to the band path, but slower on B200 (1024^2 nt=16: 871 vs 1226 matvec/s): the
-// step is memory bound either way, and the persistent kernel's row tasks run ~15% slower per
-// row than the band kernel (register cap 80 -> 3 blocks/SM; tasks of two phases share L2) while
-// the dependency waits and dispatch add ~15% (tools/wave_stats.py).  Kept as the starting
-// point for a cross-step (temporally blocked) schedule.
+// Wavefront path (k_wave, opt-in with VRG_WAVE=1 on the band-path grids): correct and equal to
+// the band path to rounding, but slower on B200 at 1024^2 nt=16 (band 1226 matvec/s; wave with
+// phase-ordered queue 871, with the temporally blocked key order 380-640 depending on K).  The
+// machine keeps ~580 rows in flight (9 us row-task latency x 65 rows/us), more than half the
+// grid, so consecutive steps cannot be overlapped along the rows without stalling on their
+// dependencies (tools/wave_stats.py: 6-16 us of dependency wait per row task), and a single
+// step is already memory bound.  Kept for larger grids and as the base of a cross-step schedule.
 // The dependency reach of a row task is the largest departure displacement along axis 1 over
 // both characteristics (fixed per Hessian), rounded up, plus the 4-tap stencil and one row of
 // margin; a non-finite departure point makes every row depend on every segment.
@@ -385,9 +388,81 @@ void Hessian::setupWave() {
     }
     waveDRows_ = finite ? static_cast<int>(std::ceil(reach)) + 3 : g.n1;
     const char* sr = std::getenv("VRG_WAVE_SR");
-    waveSR_ = sr ? std::atoi(sr) : 128;
+    waveSR_ = sr ? std::atoi(sr) : 64;
     while (waveSR_ > 32 && (g.n1 % waveSR_ != 0 || g.n2 % waveColsWidth(waveSR_) != 0)) waveSR_ /= 2;
     if (waveSR_ < 64 || waveSR_ > 256) return;  // halo summaries need 4 CW <= 256 threads
+    const int SR = waveSR_, D = waveDRows_, n1 = g.n1;
+    if (2 * D + SR >= n1) return;  // no locality to exploit
+    // Schedule keys (see WaveArgs): rows of phase q start at row start_q + M, its column
+    // segments at start_q, start_q = q * Delta; key(A) = q K + M + pos, key(B) = q K + spos - D - 1.
+    // Conditions for every dependency to have a smaller key: M >= D + SR, Delta >= M + 32,
+    // K > Delta + SR + D + 32.
+    const int M = D + SR;
+    const int Delta = (M + 32 + SR - 1) / SR * SR;
+    const char* kenv = std::getenv("VRG_WAVE_K");
+    const int K = std::max(kenv ? std::atoi(kenv) : 0, Delta + SR + D + 33);
+    const int Q = 2 * nt, nseg = n1 / SR, ncg = g.n2 / waveColsWidth(SR), nB = nseg * ncg;
+    waveNB_ = std::max(2, (n1 + D + K - 1) / K + 2);
+    struct T {
+        long long key;
+        unsigned code;
+    };
+    std::vector<T> list;
+    list.reserve(static_cast<std::size_t>(Q) * (n1 + nB));
+    for (int q = 0; q < Q; ++q) {
+        const long long start = (static_cast<long long>(q) * Delta) % n1;
+        for (int r = 0; r < n1; ++r) {
+            const long long pos = ((r - start - M) % n1 + n1) % n1;
+            list.push_back({static_cast<long long>(q) * K + M + pos, (static_cast<unsigned>(q) << 20) | r});
+        }
+        if (q == 0) continue;
+        for (int sgi = 0; sgi < nseg; ++sgi) {
+            const long long spos = ((static_cast<long long>(sgi) * SR - start) % n1 + n1) % n1;
+            for (int cg = 0; cg < ncg; ++cg)
+                list.push_back({static_cast<long long>(q) * K + spos - D - 1,
+                                (static_cast<unsigned>(q) << 20) | kWaveKindB | (sgi * ncg + cg)});
+        }
+    }
+    std::stable_sort(list.begin(), list.end(), [](const T& x, const T& y) { return x.key < y.key; });
+    // Host check of the schedule: every dependency (and every ring-slot reuse wait) of a task
+    // sits earlier in the list; otherwise the band path is kept.
+    std::vector<int> posA(static_cast<std::size_t>(Q) * n1), lastA(Q, -1), lastB(Q, -1), posSeg(static_cast<std::size_t>(Q) * nseg, -1);
+    for (int i = 0; i < static_cast<int>(list.size()); ++i) {
+        const unsigned c = list[i].code;
+        const int q = static_cast<int>(c >> 20), idx = static_cast<int>(c & (kWaveKindB - 1));
+        if (c & kWaveKindB) {
+            lastB[q] = i;
+            int& ps = posSeg[static_cast<std::size_t>(q) * nseg + idx / ncg];
+            ps = std::max(ps, i);
+        } else {
+            posA[static_cast<std::size_t>(q) * n1 + idx] = i;
+            lastA[q] = i;
+        }
+    }
+    bool ok = true;
+    for (int i = 0; i < static_cast<int>(list.size()) && ok; ++i) {
+        const unsigned c = list[i].code;
+        const int q = static_cast<int>(c >> 20), idx = static_cast<int>(c & (kWaveKindB - 1));
+        if (c & kWaveKindB) {
+            const int sgi = idx / ncg;
+            for (int rr = sgi * SR - kWaveHalo; rr < sgi * SR + SR + kWaveHalo && ok; ++rr)
+                ok = posA[static_cast<std::size_t>(q - 1) * n1 + ((rr % n1) + n1) % n1] < i;
+            if (q >= waveNB_) ok = ok && lastA[q - waveNB_] < i;
+        } else {
+            if (q >= waveNB_) ok = ok && lastB[q + 1 - waveNB_] < i;
+            if (q >= 1)
+                for (int rr = idx - D; rr <= idx + D && ok; ++rr)
+                    ok = posSeg[static_cast<std::size_t>(q) * nseg + (((rr % n1) + n1) % n1) / SR] < i;
+        }
+    }
+    if (!ok) return;
+    std::vector<unsigned> codes(list.size());
+    for (std::size_t i = 0; i < list.size(); ++i) codes[i] = list[i].code;
+    waveTasks_.alloc(sizeof(unsigned) * codes.size());
+    VRG_CUDA(cudaMemcpyAsync(waveTasks_.d(), codes.data(), sizeof(unsigned) * codes.size(), cudaMemcpyHostToDevice,
+                             ctx.stream));
+    waveTaskCount_ = static_cast<unsigned>(codes.size());
+    waveRing_.alloc(sizeof(double) * waveNB_ * (N + paddedPoints(g.n1, g.n2)));
     waveSmem_ = waveSmemFor(g, waveSR_);
     if (waveSmem_ > 48 * 1024)
         VRG_CUDA(cudaFuncSetAttribute(k_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(waveSmem_)));
@@ -395,8 +470,9 @@ void Hessian::setupWave() {
     VRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_wave, kWaveThreads, waveSmem_));
     if (perSM < 1) return;
     waveBlocks_ = perSM * ctx.numSMs;
-    const int Q = 2 * nt, ngrp = g.n1 / kWaveRG, nseg = g.n1 / waveSR_;
+    const int ngrp = g.n1 / kWaveRG;
     waveCnt_.alloc(sizeof(unsigned) * (1 + 2 * Q + static_cast<std::size_t>(Q) * (ngrp + nseg)));
+    ctx.sync();
     wave_ = true;
 }
 
@@ -446,11 +522,12 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         a.ncg = ncg;
         a.ngrp = ngrp;
         a.dRows = waveDRows_;
-        a.total = g.n1 + static_cast<long long>(Q - 1) * (static_cast<long long>(nseg) * ncg + g.n1);
-        a.C[0] = coef;
-        a.C[1] = c2;
-        a.R[0] = tmp;
-        a.R[1] = tmp + N;
+        a.total = waveTaskCount_;
+        a.tasks = waveTasks_.as<unsigned>();
+        a.NB = waveNB_;
+        a.Rring = waveRing_.d();
+        a.Cring = waveRing_.d() + static_cast<std::size_t>(waveNB_) * N;
+        a.cStride = paddedPoints(g.n1, g.n2);
         a.Xf = Xf;
         a.Xb = Xb;
         a.vtD = vtD;
@@ -483,7 +560,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
 #endif
         {
             LaunchScope ls_(ctx, "wave/matvec");
-            k_wave<<<std::min<long long>(waveBlocks_, a.total), kWaveThreads, waveSmem_, ctx.stream>>>(a);
+            k_wave<<<std::min<unsigned>(waveBlocks_, a.total), kWaveThreads, waveSmem_, ctx.stream>>>(a);
             VRG_LAUNCH_CHECK();
         }
 #ifdef VRG_WAVE_STATS

@@ -96,6 +96,10 @@ private:
     int waveBlocks_ = 0;     // resident blocks of k_wave
     std::size_t waveSmem_ = 0;
     DBuf waveCnt_;           // task counter + dependency counters, zeroed per matvec
+    DBuf waveTasks_;         // key-sorted task list
+    DBuf waveRing_;          // NB row-filtered fields, then NB padded coefficient fields
+    unsigned waveTaskCount_ = 0;
+    int waveNB_ = 2;
     void setupWave();
 
 public:
