@@ -14,6 +14,9 @@
 namespace vrg {
 
 constexpr int kBandThreads = 256;
+#ifndef VRG_BAND_PIPE
+#define VRG_BAND_PIPE 1
+#endif
 
 // one block per row; n2 a multiple of 256 up to 4096 (chunks per row <= threads)
 inline bool bandFusable(const GridDims& g) { return g.n2 >= 256 && g.n2 <= 4096 && g.n2 % 256 == 0; }
@@ -61,20 +64,56 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
 
     double guard = 0.0;
     bool bad = false;
+    // Software pipeline over the thread's nodes (incremental-state step, one-double epilogue
+    // operand): the departure point and epilogue operand of node k+1 are loaded while node k's
+    // taps are in flight, one memory round trip per node instead of two (the gather is latency
+    // bound).  The adjoint step's four prefetched operands would cost a resident block per SM
+    // (78 registers), which measured slower, so it keeps the plain order.
+    constexpr bool kPipe = VRG_BAND_PIPE && sizeof(typename Epi::Pre) <= sizeof(double);
+    double xa = 0.0, xb = 0.0;
+    typename Epi::Pre pre{};
+    if constexpr (kPipe) {
+        if (kGather) {
+            xa = __ldg(x1 + r * n2 + t);
+            xb = __ldg(x2 + r * n2 + t);
+        }
+        pre = epi.prefetch(r * n2 + t);
+        if (kGather) {
+            pdlWait();
+            pdlTrigger();
+        }
+    }
     for (int k = 0; k < per; ++k) {
         const int col = t + kBandThreads * k;
         const int p = r * n2 + col;
         double w1[4], w2[4];
         int base = 0;
-        if (kGather) {
-            const int b1 = cellBase(__ldg(x1 + p), inv1, n1, w1);
-            const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
-            base = b1 * PW + b2;
-        }
-        const typename Epi::Pre pre = epi.prefetch(p);
-        if (kGather && k == 0) {
-            pdlWait();
-            pdlTrigger();
+        typename Epi::Pre cur;
+        if constexpr (kPipe) {
+            if (kGather) {
+                const int b1 = cellBase(xa, inv1, n1, w1);
+                const int b2 = cellBase(xb, inv2, n2, w2);
+                base = b1 * PW + b2;
+            }
+            cur = pre;
+            if (k + 1 < per) {
+                if (kGather) {
+                    xa = __ldg(x1 + p + kBandThreads);
+                    xb = __ldg(x2 + p + kBandThreads);
+                }
+                pre = epi.prefetch(p + kBandThreads);
+            }
+        } else {
+            if (kGather) {
+                const int b1 = cellBase(__ldg(x1 + p), inv1, n1, w1);
+                const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
+                base = b1 * PW + b2;
+            }
+            cur = epi.prefetch(p);
+            if (kGather && k == 0) {
+                pdlWait();
+                pdlTrigger();
+            }
         }
         double val = 0.0;
         if (kGather) {
@@ -92,7 +131,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
                 val += w1[a] * rowAcc;
             }
         }
-        const double o = epi(p, &val, pre);
+        const double o = epi(p, &val, cur);
         const double ao = fabs(o);
         if (ao == ao) guard = fmax(guard, ao);
         bad |= !isfinite(o);
