@@ -245,9 +245,9 @@ def run_vrg(args, rank, world, local_rank):
                          "ncu_kernel": NCU_NAMES.get(kid) if band.value else None}
 
     # SL transport unit: one SL state step m_j = I[m_{j-1}](X_D) at 1024^2 (config 4 unit ii)
-    sl = sl_step_rate(api, ctx, v_d, mT_d, timed)
+    sl = sl_step_rate(ctx, H)
     return dict(value=value, ms=ms, launches=launches, clocks=clk, e2e=e2e_value, ms_e2e=ms_e2e,
-                wall_e2e=wall_e2e, prof=prof, sl=sl, kernels=kernels)
+                wall_e2e=wall_e2e, prof=prof, sl=sl, kernels=kernels, ctx=ctx, api=api)
 
 
 def ctypes_launches(ctx):
@@ -270,19 +270,24 @@ def profile_dump(ctx):
     return prof
 
 
-def sl_step_rate(api, ctx, v_d, mT_d, timed):
-    nt = NT
-    s = api.Solver(ctx, v_d, nt)
-    s.solve_state_final(mT_d)  # builds the characteristics
-    ctx.lib.vrg_profile(ctx.h, 1)
-    s.solve_state_final(mT_d)
-    prof = profile_dump(ctx)
-    ctx.lib.vrg_profile(ctx.h, 0)
-    keys = ["k_prefilter_rows", "k_prefilter_cols", "evaluate/state_step"]
-    per_step_ms = sum(prof[k][1] for k in keys if k in prof) / nt
-    return {"unit": "one SL state step (prefilter rows+cols, 16-tap gather), 1024^2",
-            "algorithmic_bytes": 4 * F_BYTES, "us_per_step": per_step_ms * 1e3,
-            "gbps": 4 * F_BYTES / (per_step_ms / 1e3) / 1e9}
+def sl_step_rate(ctx, H):
+    """Config 4 unit (ii): one SL state step m_j = I[m_{j-1}](X_D) at 1024^2, back-to-back steps
+    on the device (band form: gather + write m_j + the next prefilter's row pass, then the
+    column pass; plain form: prefilter rows + cols + gather)."""
+    band = ctypes.c_int()
+    ctx.check(ctx.lib.vrg_hess_band_path(H.h, ctypes.byref(band)))
+    res = {"unit": "one SL state step (prefilter rows+cols + 16-tap gather + write m_j), 1024^2",
+           "algorithmic_bytes": 4 * F_BYTES}
+    for kid, name in ((9, "band"), (10, "plain")):
+        if kid == 9 and not band.value:
+            continue
+        out_ms = ctypes.c_double()
+        ctx.check(ctx.lib.vrg_hess_bench_kernel(H.h, kid, 50, ctypes.byref(out_ms)))
+        res[name] = {"us_per_step": out_ms.value * 1e3, "gbps": 4 * F_BYTES / (out_ms.value / 1e3) / 1e9}
+    best = res.get("band", res["plain"])
+    res["us_per_step"] = best["us_per_step"]
+    res["gbps"] = best["gbps"]
+    return res
 
 
 # ------------------------------------------------------------------------------ CPU reference
@@ -377,6 +382,71 @@ def cpu_baseline_leg():
                       f"thread in parallel ({dt:.1f} s); FFT via the repo's FFTW3-API shim"}
 
 
+# ------------------------------------------------------------------------------ time to solution
+# Full inexact Gauss-Newton-Krylov registrations (newtonSolve) of the BASELINE configs that a
+# bench run can afford: configs 1 and 2 (against the reference on one host core) and one
+# config-3 pair (GPU only; the reference needs minutes per matvec-heavy solve at 512^2).
+TTS_RUNS = {
+    "config1_64_nt4_H2_1e-2_2L-pcg": dict(n=64, nt=4, norm=2, beta=1e-2, cheb=False, cpu=True),
+    "config2_256_nt8_H1_1e-3_2L-cheb10": dict(n=256, nt=8, norm=1, beta=1e-3, cheb=True, cpu=True),
+    "config3_512_nt16_H2_1e-3_2L-cheb10_pair0": dict(n=512, nt=16, norm=2, beta=1e-3, cheb=True, cpu=False),
+}
+
+
+def tts_problem(cfg):
+    from paper_1604_02153_b200 import synth
+
+    n, nt = cfg["n"], cfg["nt"]
+    if n <= 256:
+        mT, (v1, v2) = synth.config12_fields(n)
+    else:
+        mT = synth.smoothed_noise(n, n, 1000)
+        v1, v2 = synth.smooth_velocity(n, n, 2000)
+    return mT, v1, v2
+
+
+def time_to_solution(ctx, api, with_cpu):
+    """Wall time of newtonSolve (tolRelGrad 1e-2) through the C ABI with host images, and the
+    reference's on one host core for configs 1-2.  The reference image m_R is the template
+    transported by the known velocity with the device SL solver (bit-compatible with the
+    reference's, see tests/test_gpu_parity.py)."""
+    import torch
+
+    out = {}
+    for name, cfg in TTS_RUNS.items():
+        mT, v1, v2 = tts_problem(cfg)
+        mR = api.Solver(ctx, (ctx.field(v1), ctx.field(v2)), cfg["nt"]).solve_state_final(ctx.field(mT)).cpu().numpy()
+        kw = dict(nt=cfg["nt"], kind=api.PC_TWO_LEVEL, coarse_solver=api.COARSE_CHEB if cfg["cheb"] else api.COARSE_PCG,
+                  cheb_iters=10, tol_rel=1e-2)
+        api.newton_solve(ctx, mR, mT, cfg["norm"], cfg["beta"], api.COMPRESSIBLE, **kw)  # warm (plans, modules)
+        runs = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, _, recs, summ = api.newton_solve(ctx, mR, mT, cfg["norm"], cfg["beta"], api.COMPRESSIBLE, **kw)
+            torch.cuda.synchronize()
+            runs.append(time.perf_counter() - t0)
+        dt = min(runs)
+        entry = {"gpu_s": dt, "gpu_s_runs": runs, "newton_iterations": summ["iterations"],
+                 "krylov_iterations": int(sum(r["innerIterations"] for r in recs)),
+                 "final_grad_norm_rel": summ["finalGradNormRel"], "status": summ["status"]}
+        if with_cpu and cfg["cpu"]:
+            from oracle import ref
+
+            if ref.available():
+                t0 = time.perf_counter()
+                _, _, rrep, rs = ref.newton_solve(mR, mT, cfg["norm"], cfg["beta"], 0, nt=cfg["nt"], two_level=True,
+                                                  cheb=cfg["cheb"], cheb_iters=10, tol_rel=1e-2)
+                entry["cpu_reference_s"] = time.perf_counter() - t0
+                entry["cpu_cores"] = 1
+                entry["same_newton_and_krylov_iterations"] = bool(
+                    int(rs[1]) == summ["iterations"]
+                    and all(int(q[5]) == r["innerIterations"] for q, r in zip(rrep, recs)))
+                entry["speedup_vs_cpu"] = entry["cpu_reference_s"] / dt
+        out[name] = entry
+    return out
+
+
 # ------------------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -385,6 +455,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vrg", choices=["vrg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution registrations")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -458,6 +529,8 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg()
+        if not args.no_tts:
+            line["time_to_solution"] = time_to_solution(r["ctx"], r["api"], world == 1 and not args.no_cpu_baseline)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

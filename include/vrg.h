@@ -129,7 +129,8 @@ int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajec
 /* instrumentation: average ms of one launch of a matvec kernel class (0 incremental-state
  * step, 1 incremental-adjoint + body-force step, 2 prefilter (both passes), 3 two-field
  * evaluate, 4 column pass, 5 D2D copy, 6 axpy, 7 band incremental-state step, 8 band
- * incremental-adjoint step), `iters` back-to-back launches on the context stream (bench.py roofline) */
+ * incremental-adjoint step, 9 SL state step band form (gather + next row pass, then column
+ * pass), 10 SL state step plain form (prefilter + gather)), `iters` back-to-back launches on the context stream (bench.py roofline) */
 int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch);
 /* 1 when the time loops run the band kernels (gather + epilogue + next row pass fused; ids 7
  * and 8 of vrg_hess_bench_kernel), 0 for the plain 3-kernel step */

@@ -696,6 +696,16 @@ double Hessian::benchKernel(int id, int iters) {
                                                    adjLog_.flag(0));
                 break;
             }
+            case 9:  // SL state step (config 4 unit ii), band form: gather + m_j + next row pass, column pass
+                if (!solver.bandPath()) throw NotSupported("bench kernel 9: band path not active on this grid");
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N,
+                                                   EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
+                launchPrefilterCols(ctx, g, tmp, coef);
+                break;
+            case 10:  // SL state step, plain form: prefilter (rows + cols) + gather
+                launchPrefilter(ctx, g, mt, coef, tmp, nullptr);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, EpiStateStep{adjLog_.partial(0), mt + N}, true);
+                break;
             default:  // vtilde at departure (K2, two fields)
                 launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
                 break;

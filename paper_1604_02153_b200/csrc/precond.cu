@@ -6,6 +6,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <memory>
 #include <random>
 
 #include "precond.cuh"
@@ -420,6 +422,27 @@ KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int m
 }
 
 // ------------------------------------------------------------------------------ Newton
+// VRG_TRACE=1: per-phase host wall times of newtonSolve on stderr (diagnostics only).
+static bool traceOn() {
+    static const bool on = [] {
+        const char* e = std::getenv("VRG_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+struct PhaseTimer {
+    Ctx& ctx;
+    const char* what;
+    std::chrono::steady_clock::time_point t0;
+    PhaseTimer(Ctx& c, const char* w) : ctx(c), what(w), t0(std::chrono::steady_clock::now()) {}
+    ~PhaseTimer() {
+        if (!traceOn()) return;
+        ctx.sync();
+        std::fprintf(stderr, "trace %-22s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const double* mT, const Model& model,
                          const NewtonConfig& cfg, const PrecondChoice& pc, double* vOut) {
     const std::size_t N = g.points();
@@ -435,6 +458,7 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
     PrecondChoice choice = pc;
     if (choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb && !choice.hasEig &&
         !choice.reestimateEachIteration) {
+        PhaseTimer pt(ctx, "estimateEigs");
         std::tie(choice.eMin, choice.eMax) = estimateEigsAt(ctx, g, nullptr, mR, mT, model, kCoarseCfl);
         choice.hasEig = true;
     }
@@ -455,8 +479,11 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
         state.alloc(sizeof(double) * (nt + 1) * N);
         adjoint.alloc(sizeof(double) * (nt + 1) * N);
         const bool reuse = carriedNt == nt;
-        evaluateGradient(ctx, g, v, v + N, mR, mT, model, nt, gBuf.d(), gBuf.d() + N, scal, state.d(), adjoint.d(),
-                         reuse ? carried.d() : nullptr);
+        {
+            PhaseTimer pt(ctx, "evaluateGradient");
+            evaluateGradient(ctx, g, v, v + N, mR, mT, model, nt, gBuf.d(), gBuf.d() + N, scal, state.d(),
+                             adjoint.d(), reuse ? carried.d() : nullptr);
+        }
         const double objective = scal[0], mismatch = scal[1];
         copy(ctx, N, state.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
 
@@ -482,11 +509,15 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
         }
 
         const double eta = std::min(cfg.forcingCap, std::sqrt(grel));
+        std::unique_ptr<PhaseTimer> ptH(new PhaseTimer(ctx, "Hessian ctor"));
         Hessian hess(ctx, g, v, v + N, mR, mT, model, nt, state.d());
+        ptH.reset();
         // rhs = -g
         lincomb(ctx, 2 * N, -1.0, gBuf.d(), 0.0, gBuf.d(), tmpBuf.d());
+        std::unique_ptr<PhaseTimer> ptK(new PhaseTimer(ctx, "solveKkt"));
         KktResult kkt = solveKkt(ctx, hess, tmpBuf.d(), eta, cfg.maxInnerIter, choice, mR, mT, v, kCoarseCfl,
                                  dvBuf.d());
+        ptK.reset();
         rec.innerIterations = kkt.iterations;
         double* dv = dvBuf.d();
 
@@ -505,6 +536,7 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
         bool accepted = false;
         int lsSteps = 0;
         if (!carried || carried.bytes() < sizeof(double) * (nt + 1) * N) carried.alloc(sizeof(double) * (nt + 1) * N);
+        PhaseTimer ptLs(ctx, "line search");
         for (; lsSteps < cfg.lsMaxSteps; ++lsSteps) {
             lincomb(ctx, 2 * N, 1.0, v, alpha, dv, trialBuf.d());
             bool blewUp = false;

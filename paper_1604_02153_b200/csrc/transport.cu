@@ -4,7 +4,10 @@
 #include <cstring>
 #include <string>
 
+#include <cstdlib>
+
 #include "epilogues.cuh"
+#include "evalband.cuh"
 #include "transport.cuh"
 
 namespace vrg {
@@ -154,6 +157,17 @@ Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2,
     log.ensure(nt + 1, evalBlocks(g));
 }
 
+// Band path for the SL time loops (evalband.cuh): each step is the gather + epilogue + the next
+// prefilter's row pass in one kernel, then the column pass; same arithmetic as
+// prefilter + evaluate (VRG_FUSED_BANDS=0 selects the plain 3-kernel step).
+bool Solver::bandPath() const {
+    static const bool on = [] {
+        const char* e = std::getenv("VRG_FUSED_BANDS");
+        return !(e && e[0] == '0');
+    }();
+    return on && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
+}
+
 double* Solver::coef() { return coef_.d(); }
 double* Solver::tmp() { return tmp_.d(); }
 
@@ -206,15 +220,53 @@ void Solver::continuityStep(const double* u, double* out, int dir, double* guard
     ctx.interps += 1;
 }
 
+// Band form of the backward continuity loop (slAdjoint, transport.cpp:229-241): step j writes
+// lambda_{j-1} to dst(j) and row-filters it for step j-1; the prefilter input check of step j-1
+// (flag j-1) is done by step j's kernel, as in the plain path's prefilter.
+template <class DstFn>
+void Solver::continuityBand(const double* lam1, DstFn dst) {
+    const double* X = departure(kBackward);
+    const double* dv = divVelocity();
+    const double* dvd = divVelocityAtDeparture(kBackward);
+    const std::size_t N = g.points();
+    launchPrefilter(ctx, g, lam1, coef_.d(), tmp_.d(), log.flag(nt));
+    for (int j = nt; j >= 1; --j) {
+        const EpiContinuity epi{log.partial(j - 1), dvd, dv, ht, dst(j)};
+        if (j == 1) {
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
+        } else {
+            launchEvalBand<EpiContinuity, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, tmp_.d(),
+                                                log.flag(j - 1));
+            launchPrefilterCols(ctx, g, tmp_.d(), coef_.d());
+        }
+    }
+    ctx.interps += nt;
+}
+
 void Solver::state(const double* m0, double* traj, bool guard) {
     const double* X = departure(kForward);
     const std::size_t N = g.points();
     log.reset(ctx);
     copy(ctx, N, m0, traj);
     launchFieldMax(ctx, g, traj, log.partial(0));
-    for (int j = 1; j <= nt; ++j) {
-        launchPrefilter(ctx, g, traj + (j - 1) * N, coef_.d(), tmp_.d(), log.flag(j - 1));
-        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), traj + j * N}, true);
+    if (bandPath()) {
+        launchPrefilter(ctx, g, traj, coef_.d(), tmp_.d(), log.flag(0));
+        for (int j = 1; j <= nt; ++j) {
+            const EpiStateStep epi{log.partial(j), traj + j * N};
+            if (j == nt) {
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
+            } else {
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, tmp_.d(),
+                                                   log.flag(j));
+                launchPrefilterCols(ctx, g, tmp_.d(), coef_.d());
+            }
+        }
+    } else {
+        for (int j = 1; j <= nt; ++j) {
+            launchPrefilter(ctx, g, traj + (j - 1) * N, coef_.d(), tmp_.d(), log.flag(j - 1));
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), traj + j * N},
+                              true);
+        }
     }
     ctx.interps += nt;
     log.finalize(ctx);
@@ -227,12 +279,27 @@ void Solver::stateFinal(const double* m0, double* out) {
     double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
     log.reset(ctx);
     launchFieldMax(ctx, g, m0, log.partial(0));
-    const double* cur = m0;
-    for (int j = 1; j <= nt; ++j) {
-        double* dst = (j == nt) ? out : buf + (j % 2) * N;
-        launchPrefilter(ctx, g, cur, coef_.d(), tmp_.d(), log.flag(j - 1));
-        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), dst}, true);
-        cur = dst;
+    if (bandPath()) {
+        launchPrefilter(ctx, g, m0, coef_.d(), tmp_.d(), log.flag(0));
+        for (int j = 1; j <= nt; ++j) {
+            double* dst = (j == nt) ? out : buf + (j % 2) * N;
+            const EpiStateStep epi{log.partial(j), dst};
+            if (j == nt) {
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
+            } else {
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, tmp_.d(),
+                                                   log.flag(j));
+                launchPrefilterCols(ctx, g, tmp_.d(), coef_.d());
+            }
+        }
+    } else {
+        const double* cur = m0;
+        for (int j = 1; j <= nt; ++j) {
+            double* dst = (j == nt) ? out : buf + (j % 2) * N;
+            launchPrefilter(ctx, g, cur, coef_.d(), tmp_.d(), log.flag(j - 1));
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStateStep{log.partial(j), dst}, true);
+            cur = dst;
+        }
     }
     ctx.interps += nt;
     log.finalize(ctx);
@@ -244,8 +311,12 @@ void Solver::adjoint(const double* lam1, double* traj, bool guard) {
     log.reset(ctx);
     copy(ctx, N, lam1, traj + nt * N);
     launchFieldMax(ctx, g, traj + nt * N, log.partial(nt));
-    for (int j = nt; j >= 1; --j)
-        continuityStep(traj + j * N, traj + (j - 1) * N, kBackward, log.partial(j - 1), log.flag(j));
+    if (bandPath()) {
+        continuityBand(traj + nt * N, [&](int j) { return traj + (j - 1) * N; });
+    } else {
+        for (int j = nt; j >= 1; --j)
+            continuityStep(traj + j * N, traj + (j - 1) * N, kBackward, log.partial(j - 1), log.flag(j));
+    }
     log.finalize(ctx);
     log.check(ctx, "adjoint", nt, false, guard, nt);
 }
@@ -255,11 +326,15 @@ void Solver::adjointFinal(const double* lam1, double* out) {
     double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
     log.reset(ctx);
     launchFieldMax(ctx, g, lam1, log.partial(nt));
-    const double* cur = lam1;
-    for (int j = nt; j >= 1; --j) {
-        double* dst = (j == 1) ? out : buf + (j % 2) * N;
-        continuityStep(cur, dst, kBackward, log.partial(j - 1), log.flag(j));
-        cur = dst;
+    if (bandPath()) {
+        continuityBand(lam1, [&](int j) { return (j == 1) ? out : buf + (j % 2) * N; });
+    } else {
+        const double* cur = lam1;
+        for (int j = nt; j >= 1; --j) {
+            double* dst = (j == 1) ? out : buf + (j % 2) * N;
+            continuityStep(cur, dst, kBackward, log.partial(j - 1), log.flag(j));
+            cur = dst;
+        }
     }
     log.finalize(ctx);
     log.check(ctx, "adjoint", nt, false, true, nt);

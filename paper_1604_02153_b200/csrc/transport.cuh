@@ -60,6 +60,7 @@ public:
 
     // Scratch owned by the solver.
     double* coef();
+    bool bandPath() const;
     double* tmp();
 
     // slState (src/transport.cpp:214-227): traj = (nt+1) fields, traj[0] = m0.
@@ -80,6 +81,8 @@ public:
     GuardLog log;
 
 private:
+    template <class DstFn>
+    void continuityBand(const double* lam1, DstFn dst);
     DBuf cv_;  // prefiltered velocity [c1 | c2]
     DBuf X_[2];
     DBuf divv_, dvDep_[2];
