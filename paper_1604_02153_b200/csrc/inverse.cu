@@ -96,6 +96,7 @@ struct EpiAdjointSeed {
 // the band path's in-place negation bit for bit), and writes b with the seed's guard and
 // finiteness record (same arithmetic as EpiAdjointSeed).
 struct EpiIncSeed {
+    static constexpr const char* kName = "evaluate/incstate_seed";
     static constexpr bool kGuard = true;
     double* guardPartials;
     EpiIncState inc;
@@ -583,21 +584,25 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         // each step is [column pass] + [gather + epilogue + row pass].  R[.] ping-pong holds
         // the row-filtered m~_j, then the row-filtered lt_j.
         double* R[2] = {tmp, tmp + N};
-        double* mtLast = mt[0];  // unfiltered m~(1) for the adjoint seed
+        adjLog_.reset(ctx);
         for (int j = 1; j <= nt; ++j) {
-            EpiIncState epi{nullptr, vtD, vtD + N, GD(j), GD(j) + N, vt1, vt2, G(j), G(j) + N, 0.5 * ht,
-                            j == nt ? mtLast : nullptr};
-            if (j == 1) {
-                launchEvalBand<EpiIncState, false>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, R[1], nullptr);
+            const EpiIncState epi{nullptr, vtD, vtD + N, GD(j), GD(j) + N, vt1, vt2, G(j), G(j) + N, 0.5 * ht, nullptr};
+            if (j > 1) launchPrefilterCols(ctx, g, R[(j - 1) & 1], coef);
+            const CoeffSet<1> cs{{coef}};
+            if (j == nt) {
+                // the adjoint seed lt(1) = -m~(1) and b = w lt(1) grad m_nt fused into the last
+                // step; its row pass then yields the row-filtered seed directly
+                const EpiIncSeed seed{adjLog_.partial(nt), epi, wOf(nt), b1, b2};
+                if (j == 1)
+                    launchEvalBand<EpiIncSeed, false>(ctx, g, cs, Xf, Xf + N, seed, R[j & 1], adjLog_.flag(nt));
+                else
+                    launchEvalBand<EpiIncSeed, true>(ctx, g, cs, Xf, Xf + N, seed, R[j & 1], adjLog_.flag(nt));
+            } else if (j == 1) {
+                launchEvalBand<EpiIncState, false>(ctx, g, cs, Xf, Xf + N, epi, R[j & 1], nullptr);
             } else {
-                launchPrefilterCols(ctx, g, R[(j - 1) & 1], coef);
-                launchEvalBand<EpiIncState, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, R[j & 1], nullptr);
+                launchEvalBand<EpiIncState, true>(ctx, g, cs, Xf, Xf + N, epi, R[j & 1], nullptr);
             }
         }
-        adjLog_.reset(ctx);
-        EpiAdjointSeed seed{adjLog_.partial(nt), mtLast, nullptr, G(nt), G(nt) + N, wOf(nt), b1, b2, R[nt & 1],
-                            adjLog_.flag(nt)};
-        launchPointwise(ctx, g, seed);
         for (int j = nt; j >= 1; --j) {
             launchPrefilterCols(ctx, g, R[j & 1], coef);
             const bool last = j == 1;
