@@ -135,6 +135,36 @@ int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_la
 /* 1 when the time loops run the band kernels (gather + epilogue + next row pass fused; ids 7
  * and 8 of vrg_hess_bench_kernel), 0 for the plain 3-kernel step */
 int vrg_hess_band_path(vrg_hess_t h, int* band);
+/* device pointers of the operator's per-iterate invariants (read only, owned by h):
+ * [0] state m_j, (nt+1) fields; [1] grad m_j, (nt+1) x [d1 | d2]; [2] (grad m_{j-1})_D, nt x
+ * [d1 | d2]; [3] forward departure points [x1 | x2]; [4] backward departure points; [5] div v;
+ * [6] (div v) at the backward departure points.  Used to set up slab-decomposed operators. */
+int vrg_hess_buffers(vrg_hess_t h, const double** ptrs);
+
+/* ---- slab decomposition (host orchestration in slab.py) ----------
+ * A slab owns rows r0 .. r0+L-1 of an n1 x n2 grid.  Its coefficient window holds winRows
+ * padded rows (n2+3 columns, periodic column padding), window row w = grid row winBase + w
+ * (mod n1).  The prefilter of a slab field is: vrg_prefilter_rows on the L local rows, halo
+ * exchange of the row-filtered rows (winRows + 64 rows: window - 32 .. window + winRows + 31),
+ * then vrg_slab_cols.  Row pass only: rowFiltered = n1 x n2 (unpadded). */
+int vrg_prefilter_rows(vrg_ctx_t ctx, int n1, int n2, const double* u, double* rowFiltered, unsigned* nonfinite);
+int vrg_slab_cols(vrg_ctx_t ctx, int winRows, int n2, const double* inHalo, double* window);
+/* One SL step over the slab's L rows (band kernel: gather from the window at the departure
+ * points x1/x2 of the local rows (global coordinates), epilogue, and the row pass of the result
+ * into rowOut).  kind / operand fields `ops` (each L x n2):
+ *   0 store            out = I[c](X)                                   ops: out
+ *   1 incstate         m~ = I[c](X) + ht/2 (-vtD.GD - vt.G)            ops: vtD1 vtD2 gd1 gd2 vt1 vt2 g1 g2
+ *   2 incstate, m~_0=0 (no gather)                                     ops: as 1
+ *   3/4 last incstate + adjoint seed (gather / no gather): returns lt(1) = -m~(1), b = w lt(1) G
+ *                                                                      ops: as 1, b1 b2
+ *   5 adjoint + body force  b += w lt G                                ops: dvD dv g1 g2 b1 b2
+ *   6 last adjoint step     out = reg + b + w lt G                     ops: as 5, reg1 reg2 out1 out2
+ *   7 state step        out = I[c](X)  (guarded)                       ops: out
+ * guardPartials: L per-row maxima |result| (kinds 3-7); nonfinite: set if a result is not
+ * finite; winErr: set if a departure cell's taps fall outside the window. */
+int vrg_slab_step(vrg_ctx_t ctx, int kind, int n1, int n2, int L, int winBase, int winRows, const double* coef,
+                  const double* x1, const double* x2, const double* const* ops, int nops, double ht, double w,
+                  double* rowOut, double* guardPartials, unsigned* nonfinite, unsigned* winErr);
 
 /* evaluateGradient / evaluateObjective (inverse.hpp:60-71); scalars = [objective, mismatch, regTerm] */
 int vrg_evaluate_gradient(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,

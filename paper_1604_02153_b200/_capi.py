@@ -69,6 +69,10 @@ _SIG = {
     "vrg_hess_state": ("pp", C.c_int),
     "vrg_hess_bench_kernel": ("piip", C.c_int),
     "vrg_hess_band_path": ("pp", C.c_int),
+    "vrg_hess_buffers": ("pp", C.c_int),
+    "vrg_prefilter_rows": ("piippp", C.c_int),
+    "vrg_slab_cols": ("piipp", C.c_int),
+    "vrg_slab_step": ("piiiiiippppiddpppp", C.c_int),
     "vrg_evaluate_gradient": ("piippppidiippp", C.c_int),
     "vrg_evaluate_objective": ("piippppidiip", C.c_int),
     "vrg_random_bandlimited_field": ("piiup", C.c_int),

@@ -404,6 +404,36 @@ int vrg_hess_band_path(vrg_hess_t h, int* band) {
     return guarded(h->owner, [&] { *band = h->hess.bandPath() ? 1 : 0; });
 }
 
+int vrg_hess_buffers(vrg_hess_t h, const double** ptrs) {
+    return guarded(h->owner, [&] {
+        vrg::Hessian& H = h->hess;
+        ptrs[0] = H.state();
+        ptrs[1] = H.gradTraj();
+        ptrs[2] = H.gradDepTraj();
+        ptrs[3] = H.solver.departure(vrg::kForward);
+        ptrs[4] = H.solver.departure(vrg::kBackward);
+        ptrs[5] = H.solver.divVelocity();
+        ptrs[6] = H.solver.divVelocityAtDeparture(vrg::kBackward);
+    });
+}
+
+int vrg_prefilter_rows(vrg_ctx_t c, int n1, int n2, const double* u, double* rowFiltered, unsigned* nonfinite) {
+    return guarded(c, [&] { vrg::launchPrefilterRows(c->ctx, dims(n1, n2), u, rowFiltered, nonfinite); });
+}
+
+int vrg_slab_cols(vrg_ctx_t c, int winRows, int n2, const double* inHalo, double* window) {
+    return guarded(c, [&] { vrg::launchSlabCols(c->ctx, winRows, n2, inHalo, window); });
+}
+
+int vrg_slab_step(vrg_ctx_t c, int kind, int n1, int n2, int L, int winBase, int winRows, const double* coef,
+                  const double* x1, const double* x2, const double* const* ops, int nops, double ht, double w,
+                  double* rowOut, double* guardPartials, unsigned* nonfinite, unsigned* winErr) {
+    return guarded(c, [&] {
+        vrg::slabStep(c->ctx, kind, n1, n2, L, winBase, winRows, coef, x1, x2, ops, nops, ht, w, rowOut,
+                      guardPartials, nonfinite, winErr);
+    });
+}
+
 int vrg_hess_state(vrg_hess_t h, double* traj) {
     return guarded(h->owner, [&] {
         const std::size_t N = h->hess.g.points();

@@ -43,10 +43,20 @@ __device__ __forceinline__ double ldAfterWait(const double* p) {
     return v;
 }
 
-template <class Epi, bool kGather>
+// Coefficient window of a slab-decomposed grid (slab.py): the coefficients hold `rows` padded
+// rows, window row w = global grid row base + w (mod n1), instead of the whole periodically
+// padded field.  A departure cell whose 4 tap rows fall outside the window sets *err.
+struct BandWindow {
+    int base = -1;
+    int rows = 0;
+    unsigned* err = nullptr;
+};
+
+template <class Epi, bool kGather, bool kWindow = false>
 __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
                                                             const double* __restrict__ x2, int n1, int n2, Epi epi,
-                                                            double* __restrict__ rowOut, unsigned* nonfinite) {
+                                                            double* __restrict__ rowOut, unsigned* nonfinite,
+                                                            BandWindow win = BandWindow{}) {
     if (!kGather) {
         pdlWait();
         pdlTrigger();
@@ -61,6 +71,21 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
     const int per = n2 / kBandThreads;  // nodes per thread (<= 16)
     const int PW = n2 + 3;
     const double inv1 = n1 * (1.0 / kTwoPi), inv2 = n2 * (1.0 / kTwoPi);
+    // padded-layout row of the first tap (cellBase) -> row of the coefficient array
+    auto tapRow = [&](int b1) {
+        if constexpr (kWindow) {
+            int w = b1 - 1 - win.base;
+            w += w < 0 ? n1 : 0;
+            w -= w >= n1 ? n1 : 0;
+            if (w < 0 || w + 3 >= win.rows) {
+                atomicOr(win.err, 1u);
+                w = 0;
+            }
+            return w;
+        } else {
+            return b1;
+        }
+    };
 
     double guard = 0.0;
     bool bad = false;
@@ -91,7 +116,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
         typename Epi::Pre cur;
         if constexpr (kPipe) {
             if (kGather) {
-                const int b1 = cellBase(xa, inv1, n1, w1);
+                const int b1 = tapRow(cellBase(xa, inv1, n1, w1));
                 const int b2 = cellBase(xb, inv2, n2, w2);
                 base = b1 * PW + b2;
 #ifdef VRG_BAND_EXPERIMENT_NOGATHER
@@ -108,7 +133,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
             }
         } else {
             if (kGather) {
-                const int b1 = cellBase(__ldg(x1 + p), inv1, n1, w1);
+                const int b1 = tapRow(cellBase(__ldg(x1 + p), inv1, n1, w1));
                 const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
                 base = b1 * PW + b2;
 #ifdef VRG_BAND_EXPERIMENT_NOGATHER
@@ -212,7 +237,17 @@ void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x
                     double* rowOut, unsigned* nonfinite) {
     LaunchScope ls_(ctx, Epi::kName);
     launchPdl(1, k_eval_band<Epi, kGather>, dim3(bandBlocks(g)), dim3(kBandThreads), bandSmem(g), ctx.stream, cs, x1,
-              x2, g.n1, g.n2, epi, rowOut, nonfinite);
+              x2, g.n1, g.n2, epi, rowOut, nonfinite, BandWindow{});
+}
+
+// Slab launch: L local rows (blocks) of a grid with n1 global rows, coefficients in a window.
+template <class Epi, bool kGather>
+void launchEvalBandWindow(Ctx& ctx, int n1, int L, int n2, CoeffSet<1> cs, const double* x1, const double* x2,
+                          const Epi& epi, double* rowOut, unsigned* nonfinite, BandWindow win) {
+    LaunchScope ls_(ctx, Epi::kName);
+    const GridDims gl(L, n2);
+    launchPdl(1, k_eval_band<Epi, kGather, true>, dim3(L), dim3(kBandThreads), bandSmem(gl), ctx.stream, cs, x1, x2,
+              n1, n2, epi, rowOut, nonfinite, win);
 }
 
 }  // namespace vrg

@@ -593,9 +593,79 @@ bool launchColumnPass(Ctx& ctx, const GridDims& g, const double* in, double* out
     return true;
 }
 
+// Column pass of a slab's coefficient window (slab.py): `in` holds winRows + 64 row-filtered
+// rows (window rows -32 .. winRows+31, i.e. the halo the chunk carry needs is already there,
+// exchanged from the neighbouring slabs), `out` the winRows x (n2+3) window with the columns
+// periodically padded like the full layout.  Same per-chunk arithmetic as pfColsReg, no wrap
+// along axis 1.  Block: 16 columns x (16 output chunks + 4 halo chunks).
+__global__ void __launch_bounds__(kColW * 20) k_slab_cols(const double* __restrict__ in, double* __restrict__ out,
+                                                          int winRows, int n2) {
+    __shared__ double E[20][kColW], F0[20][kColW], P0[20][kColW];
+    pdlWait();
+    pdlTrigger();
+    const int t = threadIdx.x;
+    const int col = t % kColW;
+    const int cr = t / kColW;
+    const int gc = blockIdx.y * kColW + col;
+    const int inChunks = winRows / kL + 4;
+    const int ic = blockIdx.x * 16 + cr;  // input chunk (output chunk + 2)
+    const bool active = gc < n2 && ic < inChunks;
+    double f[kL];
+    if (active) {
+        const double* src = in + static_cast<std::size_t>(ic) * kL * n2 + gc;
+#pragma unroll
+        for (int k = 0; k < kL; ++k) f[k] = __ldg(src + static_cast<std::size_t>(k) * n2);
+        double b = 0.0;
+#pragma unroll
+        for (int k = kL - 2; k >= 0; --k) b = kZ * (f[k + 1] + b);
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < kL; ++k) a = f[k] + kZ * a;
+        E[cr][col] = a;
+        F0[cr][col] = f[0];
+        P0[cr][col] = b;
+    }
+    __syncthreads();
+    if (active && cr >= 2 && cr < 18 && ic < inChunks - 2) {
+        const ZPow zp;
+        const double cp = E[cr - 1][col] + zp.p[kL] * E[cr - 2][col];
+        const double cm = kZ * (F0[cr + 1][col] + P0[cr + 1][col]) + zp.p[kL + 1] * (F0[cr + 2][col] + P0[cr + 2][col]);
+        double ym[kL];
+        ym[kL - 1] = cm;
+#pragma unroll
+        for (int k = kL - 2; k >= 0; --k) ym[k] = kZ * (f[k + 1] + ym[k + 1]);
+        const int PW = n2 + 3;
+        const int colX = gc == n2 - 1 ? 0 : (gc == 0 ? n2 + 1 : (gc == 1 ? n2 + 2 : -1));
+        const int r0 = (ic - 2) * kL;  // first window row
+        double yp = cp;
+#pragma unroll
+        for (int k = 0; k < kL; ++k) {
+            yp = f[k] + kZ * yp;
+            const double v = kSqrt3 * (yp + ym[k]);
+            double* r1 = out + static_cast<std::size_t>(r0 + k) * PW;
+            r1[gc + 1] = v;
+            if (colX >= 0) r1[colX] = v;
+        }
+    }
+}
+
 }  // namespace
 
 bool colPassFusable(const GridDims& g) { return segPlan(g.n1).ok; }
+
+void launchSlabCols(Ctx& ctx, int winRows, int n2, const double* inHalo, double* window) {
+    if (winRows % kL != 0 || winRows <= 0) throw InvalidArgument("slab column pass: window rows must be a multiple of 16");
+    LaunchScope ls_(ctx, "k_slab_cols");
+    launchPdl(2, k_slab_cols, dim3((winRows / kL + 15) / 16, (n2 + kColW - 1) / kColW), dim3(kColW * 20), 0,
+              ctx.stream, inHalo, window, winRows, n2);
+}
+
+void launchPrefilterRows(Ctx& ctx, const GridDims& g, const double* u, double* rowFiltered, unsigned* nonfinite) {
+    const SegPlan pr = segPlan(g.n2);
+    if (!pr.ok) throw NotSupported("prefilter row pass: n2 must be a multiple of 32");
+    launchSegR<true, false>(ctx, g, pr, u, rowFiltered, nonfinite);
+    VRG_LAUNCH_CHECK();
+}
 
 void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c) {
     if (!launchColumnPass(ctx, g, rowFiltered, c))

@@ -42,6 +42,10 @@ void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, do
 // Column pass only (input already row-filtered, e.g. by a fused band kernel, evalband.cuh).
 bool colPassFusable(const GridDims& g);
 void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c);
+// Row pass only (rowFiltered unpadded n1 x n2); used per slab, whose rows are complete.
+void launchPrefilterRows(Ctx& ctx, const GridDims& g, const double* u, double* rowFiltered, unsigned* nonfinite);
+// Column pass of a slab's coefficient window from winRows + 64 row-filtered rows (slab.py).
+void launchSlabCols(Ctx& ctx, int winRows, int n2, const double* inHalo, double* window);
 
 // B-spline weights, src/interp.cpp:59-65 (the /6 as a multiply by 1/6: <= 1 ulp apart).
 __device__ __forceinline__ void bsplineWeights(double f, double w[4]) {

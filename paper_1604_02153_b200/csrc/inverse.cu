@@ -640,6 +640,55 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     adjLog_.finalize(ctx);
 }
 
+// ------------------------------------------------------------------------------ slabs
+// One SL step of a slab-decomposed grid (slab.py): the band kernel over the slab's L rows with
+// the coefficients in a window (BandWindow), epilogue by kind (see include/vrg.h).
+void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRows, const double* coef,
+              const double* x1, const double* x2, const double* const* ops, int nops, double ht, double w,
+              double* rowOut, double* guardPartials, unsigned* flag, unsigned* winErr) {
+    static const int kNeed[] = {1, 8, 8, 10, 10, 6, 10, 1};
+    if (kind < 0 || kind > 7) throw InvalidArgument("slab step: unknown kind");
+    if (nops < kNeed[kind]) throw InvalidArgument("slab step: too few operand fields");
+    if (!bandFusable(GridDims(L, n2)) || L < 1 || n1 < L) throw NotSupported("slab step: unsupported row length");
+    const BandWindow win{winBase, winRows, winErr};
+    const CoeffSet<1> cs{{coef}};
+    auto inc = [&] {
+        return EpiIncState{nullptr, ops[0], ops[1], ops[2], ops[3], ops[4], ops[5], ops[6], ops[7], 0.5 * ht, nullptr};
+    };
+    switch (kind) {
+        case 0:
+            launchEvalBandWindow<EpiStore1, true>(ctx, n1, L, n2, cs, x1, x2, EpiStore1{nullptr, const_cast<double*>(ops[0])},
+                                                  rowOut, flag, win);
+            break;
+        case 1: launchEvalBandWindow<EpiIncState, true>(ctx, n1, L, n2, cs, x1, x2, inc(), rowOut, flag, win); break;
+        case 2: launchEvalBandWindow<EpiIncState, false>(ctx, n1, L, n2, cs, x1, x2, inc(), rowOut, flag, win); break;
+        case 3:
+        case 4: {
+            const EpiIncSeed seed{guardPartials, inc(), w, const_cast<double*>(ops[8]), const_cast<double*>(ops[9])};
+            if (kind == 3)
+                launchEvalBandWindow<EpiIncSeed, true>(ctx, n1, L, n2, cs, x1, x2, seed, rowOut, flag, win);
+            else
+                launchEvalBandWindow<EpiIncSeed, false>(ctx, n1, L, n2, cs, x1, x2, seed, rowOut, flag, win);
+            break;
+        }
+        case 5:
+        case 6: {
+            const bool last = kind == 6;
+            const EpiAdjointBF epi{guardPartials, ops[0], ops[1], ht, nullptr, ops[2], ops[3], w,
+                                   const_cast<double*>(ops[4]), const_cast<double*>(ops[5]), last ? ops[6] : nullptr,
+                                   last ? ops[7] : nullptr, last ? const_cast<double*>(ops[8]) : nullptr,
+                                   last ? const_cast<double*>(ops[9]) : nullptr};
+            launchEvalBandWindow<EpiAdjointBF, true>(ctx, n1, L, n2, cs, x1, x2, epi, rowOut, flag, win);
+            break;
+        }
+        default:
+            launchEvalBandWindow<EpiStateStep, true>(ctx, n1, L, n2, cs, x1, x2,
+                                                     EpiStateStep{guardPartials, const_cast<double*>(ops[0])}, rowOut,
+                                                     flag, win);
+            break;
+    }
+}
+
 void Hessian::checkLastGuard() { adjLog_.check(ctx, "adjoint", nt, false, true, nt); }
 
 // Average device time of one launch of a matvec kernel class, `iters` back-to-back launches

@@ -105,8 +105,16 @@ private:
 public:
     static inline bool useFusedBands = true;  // process-wide switch (tests compare both paths)
     bool bandPath() const { return fused_; }
+    // device buffers of the per-iterate invariants: state (nt+1)N, G (nt+1)2N, GD nt 2N
+    const double* gradTraj() const { return G_.d(); }
+    const double* gradDepTraj() const { return GD_.d(); }
     bool wavePath() const { return wave_; }
 };
+
+// One SL step of a slab-decomposed grid (C ABI vrg_slab_step).
+void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRows, const double* coef,
+              const double* x1, const double* x2, const double* const* ops, int nops, double ht, double w,
+              double* rowOut, double* guardPartials, unsigned* flag, unsigned* winErr);
 
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
                double* b2);

@@ -1,0 +1,374 @@
+"""Slab-decomposed GN Hessian matvec for one large grid.
+
+The n1 x n2 grid is split along axis 1 into G slabs of L = n1/G rows, one per rank (one GPU
+per process under torchrun, NCCL over NVLink).  The reference is single-process; this is the
+B200 extension of `inverse::HessianOperator::apply` (src/inverse.cpp:176-233) for a grid whose
+matvec should use several GPUs.  Per SL step of the incremental state / adjoint:
+
+* the step's gather kernel (C ABI `vrg_slab_step`, the band kernel) interpolates at the
+  departure points of the slab's rows from a *coefficient window* (the slab's rows plus D+1
+  rows above and the rest of a 16-row multiple below, D = largest departure displacement in
+  rows), applies the step epilogue and row-filters the result (rows are complete in a slab);
+* the column pass needs the row-filtered field on the window plus the 32-row reach of the
+  chunk-carry filter: one halo exchange of `top`/`bot` rows with the two neighbouring slabs
+  (periodic ring), then `vrg_slab_cols` computes the window's coefficients, including the
+  halo rows redundantly, so the gather needs no second exchange;
+* the regularisation beta A vt uses a distributed 2-D FFT: row FFTs (local rows) -> all-to-all
+  transpose -> column FFTs -> symbol -> inverse -> all-to-all -> inverse row FFTs;
+* the blow-up guard reduces the per-row maxima of every step with a max over ranks and is
+  checked in the reference's order with its messages (transport.cpp:16-20).
+
+The per-iterate invariants (state trajectory, gradients, departure points, div v) are built
+once per Newton iterate by the single-device operator and sliced per slab (`from_operator`);
+the matvec, applied many times per iterate, is the decomposed hot path.
+
+Communicators: `DistComm` (torch.distributed; NCCL on GPUs, gloo on CPU for the host-logic
+tests) and `LocalComm` (G virtual slabs in one process, run phase by phase: single-device
+validation of the decomposition, no concurrency between the virtual ranks).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import api
+
+KIND_STORE, KIND_INC, KIND_INC0, KIND_SEED, KIND_SEED0, KIND_ADJ, KIND_ADJ_LAST, KIND_STATE = range(8)
+CARRY = 32  # rows of chunk-carry reach of the column pass (2 chunks of 16)
+
+
+# ------------------------------------------------------------------------------ communicators
+class LocalComm:
+    """G virtual slabs in one process: exchanges are tensor copies."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self.ranks = list(range(size))
+
+    def exchange_rows(self, locs, top, bot):
+        """locs[i] = (..., L, n2) slab of rank i -> (..., top + L + bot, n2) with the periodic
+        neighbours' rows (may span several slabs when L < top or L < bot)."""
+        full = torch.cat(locs, dim=-2)
+        n1 = full.shape[-2]
+        L = locs[0].shape[-2]
+        out = []
+        for i in self.ranks:
+            idx = torch.arange(i * L - top, i * L + L + bot, device=full.device) % n1
+            out.append(full.index_select(-2, idx))
+        return out
+
+    def alltoall(self, send):
+        """send[i][q] from rank i to rank q -> recv[q][i]."""
+        return [[send[i][q] for i in self.ranks] for q in self.ranks]
+
+    def allreduce_max(self, vals):
+        m = torch.stack([torch.as_tensor(v) for v in vals]).amax(0)
+        return [m for _ in self.ranks]
+
+
+class DistComm:
+    """One slab per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.ranks = [self.rank]
+
+    def exchange_rows(self, locs, top, bot):
+        (loc,) = locs
+        L = loc.shape[-2]
+        if top > L or bot > L:
+            raise api.InvalidArgument("slab halo is wider than a slab: use fewer ranks")
+        d, G, r = self.dist, self.size, self.rank
+        nxt, prv = (r + 1) % G, (r - 1) % G
+        up = torch.empty_like(loc[..., :top, :]) if top else None
+        dn = torch.empty_like(loc[..., :bot, :]) if bot else None
+        reqs = []
+        if G == 1:
+            if top:
+                up.copy_(loc[..., L - top:, :])
+            if bot:
+                dn.copy_(loc[..., :bot, :])
+        else:
+            ops = []
+            if top:
+                ops += [d.P2POp(d.isend, loc[..., L - top:, :].contiguous(), nxt, self.group),
+                        d.P2POp(d.irecv, up, prv, self.group)]
+            if bot:
+                ops += [d.P2POp(d.isend, loc[..., :bot, :].contiguous(), prv, self.group),
+                        d.P2POp(d.irecv, dn, nxt, self.group)]
+            reqs = d.batch_isend_irecv(ops)
+            for q in reqs:
+                q.wait()
+        parts = [p for p in (up, loc, dn) if p is not None]
+        return [torch.cat(parts, dim=-2)]
+
+    def alltoall(self, send):
+        (chunks,) = send
+        recv = [torch.empty_like(c) for c in chunks]
+        d = self.dist
+        if self.size == 1:
+            recv[0].copy_(chunks[0])
+        elif d.get_backend(self.group) == "nccl":
+            d.all_to_all(recv, [c.contiguous() for c in chunks], group=self.group)
+        else:  # gloo has no all_to_all: pairwise exchanges
+            recv[self.rank].copy_(chunks[self.rank])
+            ops = []
+            for q in range(self.size):
+                if q != self.rank:
+                    ops += [d.P2POp(d.isend, chunks[q].contiguous(), q, self.group),
+                            d.P2POp(d.irecv, recv[q], q, self.group)]
+            for r in d.batch_isend_irecv(ops):
+                r.wait()
+        return [recv]
+
+    def allreduce_max(self, vals):
+        (v,) = vals
+        t = torch.as_tensor(v).clone()
+        if self.size > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return [t]
+
+
+# ------------------------------------------------------------------------------ geometry
+class SlabGeometry:
+    """Rows, window and halo sizes of the slabs (host logic, tested on CPU)."""
+
+    def __init__(self, n1, n2, size, reach_rows):
+        if n1 % size:
+            raise api.InvalidArgument("slab decomposition: n1 must be a multiple of the number of ranks")
+        self.n1, self.n2, self.size = n1, n2, size
+        self.L = n1 // size
+        self.D = int(reach_rows)
+        need = self.L + 2 * self.D + 3               # rows r0-D-1 .. r0+L+D+1
+        self.win_rows = (need + 15) // 16 * 16
+        self.top = self.D + 1 + CARRY                # rows above the slab in the exchange
+        self.bot = self.win_rows - self.L - self.D - 1 + CARRY
+
+    def r0(self, rank):
+        return rank * self.L
+
+    def win_base(self, rank):
+        """Grid row of window row 0 (may be negative: periodic)."""
+        return self.r0(rank) - self.D - 1
+
+
+def row_reach(x1, n1, r0=0):
+    """Largest |departure - arrival| along axis 1 in cells over the rows of x1 (global row r0 +
+    local row), minimum image; non-finite -> inf."""
+    h = 2 * math.pi / n1
+    L = x1.shape[-2]
+    xa = (-math.pi + (r0 + torch.arange(L, device=x1.device, dtype=x1.dtype)) * h)[:, None]
+    d = x1 - xa
+    d = d - 2 * math.pi * torch.floor((d + math.pi) / (2 * math.pi))
+    if not bool(torch.isfinite(d).all()):
+        return float("inf")
+    return float(d.abs().max()) / h
+
+
+def reg_symbol_cols(n1, n2, norm, beta, c0, c1, device):
+    """beta * gamma on half-spectrum columns c0..c1-1 for all rows (spectral.cpp:46-66)."""
+    k1 = torch.arange(n1, device=device, dtype=torch.float64)
+    k1 = torch.where(k1 <= n1 // 2, k1, k1 - n1)
+    k2 = torch.arange(c0, c1, device=device, dtype=torch.float64)
+    ksq = k1[:, None] ** 2 + k2[None, :] ** 2
+    return beta * ksq ** int(norm)
+
+
+def distributed_reg(comm, vts, n1, n2, norm, beta):
+    """beta A vt (applyReg, spectral.cpp:109-120) of slab fields vts[i] = (..., L, n2): row FFTs
+    of the local rows, all-to-all transpose to column blocks, column FFTs, symbol, inverse
+    column FFTs, all-to-all back, inverse row FFTs (torch.fft = cuFFT on the device)."""
+    G = comm.size
+    nc = n2 // 2 + 1
+    wc = -(-nc // G)  # half-spectrum columns per rank in the transposed layout
+    L = n1 // G
+    send = []
+    for vt in vts:
+        s = torch.fft.rfft(vt, dim=-1)
+        s = torch.nn.functional.pad(s, (0, G * wc - nc))
+        send.append([s[..., q * wc:(q + 1) * wc].contiguous() for q in range(G)])
+    recv = comm.alltoall(send)
+    back = []
+    for k, q in enumerate(comm.ranks):
+        col = torch.cat(recv[k], dim=-2)  # (..., n1, wc)
+        f = torch.fft.fft(col, dim=-2)
+        c0, c1 = min(q * wc, nc), min((q + 1) * wc, nc)
+        sym = reg_symbol_cols(n1, n2, norm, beta, c0, c1, col.device)
+        f[..., :c1 - c0] *= sym
+        f[..., c1 - c0:] = 0
+        col = torch.fft.ifft(f, dim=-2)
+        back.append([col[..., r * L:(r + 1) * L, :].contiguous() for r in range(G)])
+    got = comm.alltoall(back)
+    return [torch.fft.irfft(torch.cat(got[k], dim=-1)[..., :nc], n=n2, dim=-1) for k in range(len(comm.ranks))]
+
+
+# ------------------------------------------------------------------------------ operator
+class SlabHessian:
+    """GN Hessian matvec of one grid decomposed over comm's ranks (see the module docstring)."""
+
+    def __init__(self, ctx, comm, n1, n2, nt, norm, beta, parts, reach_rows):
+        """parts[i]: dict of rank i's slab tensors: Xf, Xb (2, L, n2), G (nt+1, 2, L, n2),
+        GD (nt, 2, L, n2), dv, dvd (L, n2)."""
+        self.ctx, self.comm = ctx, comm
+        self.n1, self.n2, self.nt, self.norm, self.beta = n1, n2, nt, norm, beta
+        self.geo = SlabGeometry(n1, n2, comm.size, reach_rows)
+        self.parts = parts
+        g = self.geo
+        dev = ctx.device
+        self.win = [ctx.empty(g.win_rows, n2 + 3) for _ in comm.ranks]
+        self.winv = [ctx.empty(2, g.win_rows, n2 + 3) for _ in comm.ranks]
+        self.rows = [ctx.empty(g.L, n2) for _ in comm.ranks]
+        self.scr = [ctx.empty(g.L, n2) for _ in comm.ranks]
+        self.vtD = [ctx.empty(2, g.L, n2) for _ in comm.ranks]
+        self.b = [ctx.empty(2, g.L, n2) for _ in comm.ranks]
+        self.partials = [ctx.empty(nt + 1, g.L) for _ in comm.ranks]
+        self.flags = [torch.zeros(nt + 2, dtype=torch.int32, device=dev) for _ in comm.ranks]
+
+    # -- construction from the single-device operator (per-iterate invariants, sliced)
+    @classmethod
+    def from_operator(cls, ctx, comm, H: api.HessianOperator, norm, beta):
+        n1, n2 = H.shape
+        nt = H.nt
+        ptrs = (C.c_void_p * 7)()
+        ctx.check(ctx.lib.vrg_hess_buffers(H.h, ptrs))
+        N = n1 * n2
+
+        def view(ptr, count):
+            return _DeviceView(ptr, count, ctx.device).tensor()
+
+        G = view(ptrs[1], (nt + 1) * 2 * N).view(nt + 1, 2, n1, n2)
+        GD = view(ptrs[2], nt * 2 * N).view(nt, 2, n1, n2)
+        Xf = view(ptrs[3], 2 * N).view(2, n1, n2)
+        Xb = view(ptrs[4], 2 * N).view(2, n1, n2)
+        dv = view(ptrs[5], N).view(n1, n2)
+        dvd = view(ptrs[6], N).view(n1, n2)
+        L = n1 // comm.size
+        parts = []
+        reach = 0.0
+        for i in comm.ranks:
+            s = slice(i * L, (i + 1) * L)
+            p = dict(Xf=Xf[:, s].clone(), Xb=Xb[:, s].clone(), G=G[:, :, s].clone(), GD=GD[:, :, s].clone(),
+                     dv=dv[s].clone(), dvd=dvd[s].clone())
+            reach = max(reach, row_reach(p["Xf"][0], n1, i * L), row_reach(p["Xb"][0], n1, i * L))
+            parts.append(p)
+        reach = float(comm.allreduce_max([torch.tensor(reach)] * len(comm.ranks))[0])
+        if not math.isfinite(reach):
+            raise api.InvalidArgument("evaluate: non-finite point coordinate")
+        return cls(ctx, comm, n1, n2, nt, norm, beta, parts, math.ceil(reach) + 3)
+
+    # -- building blocks
+    def _prefilter(self, fields, windows):
+        """Coefficient windows of slab fields (per rank (L, n2)): row pass, halo exchange,
+        column pass."""
+        g, ctx = self.geo, self.ctx
+        for i, f in enumerate(fields):
+            ctx.check(ctx.lib.vrg_prefilter_rows(ctx.h, g.L, self.n2, api._p(f), api._p(self.scr[i]), None))
+        halo = self.comm.exchange_rows(self.scr, g.top, g.bot)
+        for i, hb in enumerate(halo):
+            ctx.check(ctx.lib.vrg_slab_cols(ctx.h, g.win_rows, self.n2, api._p(hb), api._p(windows[i])))
+
+    def _windows_from_rows(self, rowfiltered):
+        g, ctx = self.geo, self.ctx
+        halo = self.comm.exchange_rows(rowfiltered, g.top, g.bot)
+        for i, hb in enumerate(halo):
+            ctx.check(ctx.lib.vrg_slab_cols(ctx.h, g.win_rows, self.n2, api._p(hb), api._p(self.win[i])))
+
+    def _step(self, i, kind, coef, X, ops, ht, w, row_out, partial, flag):
+        g, ctx = self.geo, self.ctx
+        arr = (C.c_void_p * len(ops))(*[o.data_ptr() for o in ops])
+        ctx.check(ctx.lib.vrg_slab_step(ctx.h, kind, self.n1, self.n2, g.L, g.win_base(self.comm.ranks[i]),
+                                        g.win_rows, api._p(coef), api._p(X[0]), api._p(X[1]), arr, len(ops),
+                                        ht, w, api._p(row_out), api._p(partial),
+                                        C.c_void_p(flag.data_ptr()) if flag is not None else None,
+                                        C.c_void_p(self.flags[i][self.nt + 1:].data_ptr())))
+
+    def reg(self, vts):
+        return distributed_reg(self.comm, vts, self.n1, self.n2, self.norm, self.beta)
+
+    def apply(self, vts, outs=None, data_term_only=False):
+        """vts[i] = (2, L, n2) slab of vt on rank i -> H vt slabs (or the data term b)."""
+        nt, ht = self.nt, 1.0 / self.nt
+        ranks = range(len(self.comm.ranks))
+        outs = outs if outs is not None else [self.ctx.empty(2, self.geo.L, self.n2) for _ in ranks]
+        regs = self.reg(vts) if not data_term_only else None
+        for i in ranks:
+            self.flags[i].zero_()
+            self.partials[i].zero_()
+        wof = lambda j: ht * (0.5 if j in (0, nt) else 1.0)  # noqa: E731
+        # vt_D (2 interps)
+        for c in range(2):
+            self._prefilter([vt[c] for vt in vts], [wv[c] for wv in self.winv])
+        for i in ranks:
+            for c in range(2):
+                self._step(i, KIND_STORE, self.winv[i][c], self.parts[i]["Xf"], [self.vtD[i][c]], ht, 0.0,
+                           self.scr[i], self.partials[i][0], None)
+        # incremental state, the last step seeding the adjoint
+        for j in range(1, nt + 1):
+            if j > 1:
+                self._windows_from_rows(self.rows)
+            for i in ranks:
+                p = self.parts[i]
+                ops = [self.vtD[i][0], self.vtD[i][1], p["GD"][j - 1][0], p["GD"][j - 1][1], vts[i][0], vts[i][1],
+                       p["G"][j][0], p["G"][j][1]]
+                if j == nt:
+                    kind = KIND_SEED0 if j == 1 else KIND_SEED
+                    ops += [self.b[i][0], self.b[i][1]]
+                    self._step(i, kind, self.win[i], p["Xf"], ops, ht, wof(nt), self.rows[i], self.partials[i][nt],
+                               self.flags[i][nt:nt + 1])
+                else:
+                    kind = KIND_INC0 if j == 1 else KIND_INC
+                    self._step(i, kind, self.win[i], p["Xf"], ops, ht, 0.0, self.rows[i], self.partials[i][0], None)
+        # incremental adjoint + body force (+ beta A vt on the last step)
+        for j in range(nt, 0, -1):
+            self._windows_from_rows(self.rows)
+            for i in ranks:
+                p = self.parts[i]
+                ops = [p["dvd"], p["dv"], p["G"][j - 1][0], p["G"][j - 1][1], self.b[i][0], self.b[i][1]]
+                if j == 1:
+                    if data_term_only:
+                        zero = torch.zeros_like(self.b[i])
+                        ops += [zero[0], zero[1], outs[i][0], outs[i][1]]
+                    else:
+                        ops += [regs[i][0], regs[i][1], outs[i][0], outs[i][1]]
+                    self._step(i, KIND_ADJ_LAST, self.win[i], p["Xb"], ops, ht, wof(0), self.scr[i],
+                               self.partials[i][0], None)
+                else:
+                    self._step(i, KIND_ADJ, self.win[i], p["Xb"], ops, ht, wof(j - 1), self.rows[i],
+                               self.partials[i][j - 1], self.flags[i][j - 1:j])
+        self._check_guard()
+        return outs
+
+    def _check_guard(self):
+        """transport.cpp:16-20 guard of the GN adjoint (inverse.cpp:185) over all slabs, in the
+        reference's step order, and the window/finiteness flags."""
+        nt = self.nt
+        mx = self.comm.allreduce_max([p.amax(dim=1) for p in self.partials])[0].cpu()
+        fl = self.comm.allreduce_max([f.to(torch.float64) for f in self.flags])[0].cpu()
+        if fl[nt + 1] != 0:
+            raise api.VrgError("slab window too small for the departure displacement")
+        threshold = 1e3 * float(mx[nt])
+        for s in range(1, nt + 1):
+            j = nt + 1 - s
+            if fl[j] != 0:
+                raise api.InvalidArgument("prefilter: non-finite value")
+            if float(mx[j - 1]) > threshold:
+                raise api.BlowupError(f"adjoint solve exceeded the blow-up guard at step {j}")
+
+
+class _DeviceView:
+    """Zero-copy torch view of library-owned device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, count, device):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+        self.device = device
+
+    def tensor(self):
+        return torch.as_tensor(self, device=self.device)

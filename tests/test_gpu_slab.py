@@ -1,0 +1,73 @@
+"""GPU: slab-decomposed GN Hessian matvec against the single-device
+operator on the same inputs, with G virtual slabs on one device (LocalComm: every slab's work
+runs in turn, exchanges are copies; no kernels of different slabs wait on one another).  The
+multi-process NCCL path uses the same code with DistComm (tests/test_slab_cpu.py covers its
+host logic over gloo)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1604_02153_b200 import slab, synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1604_02153_b200 import api as A
+
+    return A
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def apply_floor(n, p, beta, vmax, outmax):
+    kmax2 = 2.0 * (n // 2) ** 2
+    return 4 * 2.2e-16 * beta * kmax2 ** p * vmax / outmax
+
+
+@pytest.mark.parametrize("n,nt,G", [(256, 4, 1), (256, 4, 2), (256, 8, 4), (512, 8, 4), (256, 4, 8)])
+def test_slab_matvec_vs_single_device(ctx, api, n, nt, G):
+    mT = synth.smoothed_noise(n, n, 1000)
+    v1, v2 = synth.smooth_velocity(n, n, 2000)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    F = ctx.field
+    w = (F(0.5 * v1), F(0.5 * v2))
+    H = api.HessianOperator(ctx, w, F(mT), F(mT), 2, 1e-3, api.COMPRESSIBLE, nt)
+    vt = (F(vt1), F(vt2))
+    d1, d2 = H.apply_data_term(vt)
+    h1, h2 = H.apply(vt)
+    comm = slab.LocalComm(G)
+    S = slab.SlabHessian.from_operator(ctx, comm, H, 2, 1e-3)
+    L = n // G
+    vts = [ctx.field(np.stack([vt1[i * L:(i + 1) * L], vt2[i * L:(i + 1) * L]])) for i in range(G)]
+    dt = S.apply(vts, data_term_only=True)
+    got = np.concatenate([o.cpu().numpy() for o in dt], axis=1)
+    assert rel(got[0], d1.cpu().numpy()) < TOL and rel(got[1], d2.cpu().numpy()) < TOL
+    full = S.apply(vts)
+    got = np.concatenate([o.cpu().numpy() for o in full], axis=1)
+    e1 = h1.cpu().numpy()
+    tol = max(TOL, apply_floor(n, 2, 1e-3, max(np.abs(vt1).max(), np.abs(vt2).max()), np.abs(e1).max()))
+    assert rel(got[0], e1) < tol and rel(got[1], h2.cpu().numpy()) < tol
+
+
+def test_slab_window_too_small_is_detected(ctx, api):
+    n, nt, G = 256, 4, 2
+    mT = synth.smoothed_noise(n, n, 1000)
+    v1, v2 = synth.smooth_velocity(n, n, 2000)
+    F = ctx.field
+    H = api.HessianOperator(ctx, (F(v1), F(v2)), F(mT), F(mT), 2, 1e-3, api.COMPRESSIBLE, nt)
+    S = slab.SlabHessian.from_operator(ctx, slab.LocalComm(G), H, 2, 1e-3)
+    S.geo = slab.SlabGeometry(n, n, G, 0)  # pretend the departure points stay in their rows
+    S.win = [ctx.empty(S.geo.win_rows, n + 3) for _ in range(G)]
+    S.winv = [ctx.empty(2, S.geo.win_rows, n + 3) for _ in range(G)]
+    L = n // G
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    vts = [ctx.field(np.stack([vt1[i * L:(i + 1) * L], vt2[i * L:(i + 1) * L]])) for i in range(G)]
+    with pytest.raises(api.VrgError, match="window too small"):
+        S.apply(vts)
