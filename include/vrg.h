@@ -52,6 +52,9 @@ typedef struct vrg_coarse_s* vrg_coarse_t;
 /* ---- context / memory (no reference counterpart: the device runtime under the pImpls) ---- */
 const char* vrg_version(void);
 int vrg_ctx_create(int device, void* cuda_stream /* nullable: own stream */, vrg_ctx_t* out);
+/* the CUDA stream the context launches on (its own non-blocking stream when created with a
+ * NULL stream), for callers that order their own work with the library's */
+void* vrg_ctx_stream(vrg_ctx_t ctx);
 void vrg_ctx_destroy(vrg_ctx_t ctx);
 const char* vrg_last_error(vrg_ctx_t ctx); /* ctx may be NULL: last error of this thread */
 int vrg_sync(vrg_ctx_t ctx);

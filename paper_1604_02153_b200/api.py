@@ -45,21 +45,37 @@ def _p(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
 
 
+_STREAMS = {}
+
+
 class Context:
-    """One device + stream (the library's vrg_ctx_t).  Kernels run on torch's current stream of
-    `device`, so torch ops and library calls are stream-ordered."""
+    """One device + stream (the library's vrg_ctx_t).  By default the first context of a device
+    creates the library's non-blocking stream and makes it torch's current stream of that
+    device (torch.cuda.ExternalStream), and later contexts share it: torch ops and library calls
+    are then stream-ordered.  (torch's own default stream is the legacy NULL stream, on which
+    CUDA graphs cannot be captured.)"""
 
     def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
         if not torch.cuda.is_available():
             raise VrgError("libvrg needs a CUDA device (no CPU fallback)")
         self.lib = _capi.load()
         self.device = torch.device("cuda", device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if stream is None or stream.cuda_stream == 0:
+            stream = _STREAMS.get(device)
+        handle = stream.cuda_stream if stream is not None else 0
         h = C.c_void_p()
-        code = self.lib.vrg_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        code = self.lib.vrg_ctx_create(device, C.c_void_p(handle), C.byref(h))
         if code:
             raise _ERRORS.get(code, VrgError)(self.lib.vrg_last_error(None).decode())
         self.h = h
+        self._owner = stream is None
+        if stream is None:  # the library created its stream: adopt it for torch
+            stream = torch.cuda.ExternalStream(self.lib.vrg_ctx_stream(h), device=self.device)
+            _STREAMS[device] = stream
+        self.stream = stream
+        with torch.cuda.device(self.device):
+            if torch.cuda.current_stream(self.device) != stream:
+                torch.cuda.set_stream(stream)
 
     def check(self, code: int):
         if code:
@@ -85,6 +101,8 @@ class Context:
         return torch.empty(*shape, dtype=torch.float64, device=self.device)
 
     def close(self):
+        if getattr(self, "_owner", False):
+            return  # owns the device's shared stream (torch's current stream): kept for the process
         if getattr(self, "h", None):
             self.lib.vrg_ctx_destroy(self.h)
             self.h = None

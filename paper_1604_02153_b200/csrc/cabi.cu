@@ -81,6 +81,8 @@ int vrg_ctx_create(int device, void* stream, vrg_ctx_t* out) {
 
 void vrg_ctx_destroy(vrg_ctx_t c) { delete c; }
 
+void* vrg_ctx_stream(vrg_ctx_t c) { return c ? static_cast<void*>(c->ctx.stream) : nullptr; }
+
 const char* vrg_last_error(vrg_ctx_t c) { return c ? c->ctx.err.c_str() : g_threadErr.c_str(); }
 
 int vrg_sync(vrg_ctx_t c) {
