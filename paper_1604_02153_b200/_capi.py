@@ -94,7 +94,7 @@ def header_symbols():
     """Names of all functions declared in include/vrg.h."""
     with open(HEADER) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(vrg_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void\*|void|const char\*)\s+(vrg_\w+)\s*\(", text, re.M)))
 
 
 def load():

