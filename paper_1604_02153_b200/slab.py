@@ -59,6 +59,18 @@ class LocalComm:
             out.append(full.index_select(-2, idx))
         return out
 
+    def fill_halos(self, bufs, L, top, bot):
+        """bufs[i] = (top + L + bot, n2) with the slab's rows at [top, top+L): fills the halo
+        rows from the periodic neighbours' slab rows."""
+        full = torch.cat([b[top:top + L] for b in bufs], dim=0)
+        n1 = full.shape[0]
+        for i in self.ranks:
+            if top:
+                bufs[i][:top] = full.index_select(0, torch.arange(i * L - top, i * L, device=full.device) % n1)
+            if bot:
+                bufs[i][top + L:] = full.index_select(
+                    0, torch.arange(i * L + L, i * L + L + bot, device=full.device) % n1)
+
     def alltoall(self, send):
         """send[i][q] from rank i to rank q -> recv[q][i]."""
         return [[send[i][q] for i in self.ranks] for q in self.ranks]
@@ -108,6 +120,27 @@ class DistComm:
                 q.wait()
         parts = [p for p in (up, loc, dn) if p is not None]
         return [torch.cat(parts, dim=-2)]
+
+    def fill_halos(self, bufs, L, top, bot):
+        (b,) = bufs
+        if top > L or bot > L:
+            raise api.InvalidArgument("slab halo is wider than a slab: use fewer ranks")
+        d, G, r = self.dist, self.size, self.rank
+        mid = b[top:top + L]
+        if G == 1:
+            if top:
+                b[:top] = mid[L - top:]
+            if bot:
+                b[top + L:] = mid[:bot]
+            return
+        nxt, prv = (r + 1) % G, (r - 1) % G
+        ops = []
+        if top:  # my last `top` rows are the next slab's top halo
+            ops += [d.P2POp(d.isend, mid[L - top:], nxt, self.group), d.P2POp(d.irecv, b[:top], prv, self.group)]
+        if bot:  # my first `bot` rows are the previous slab's bottom halo
+            ops += [d.P2POp(d.isend, mid[:bot], prv, self.group), d.P2POp(d.irecv, b[top + L:], nxt, self.group)]
+        for q in d.batch_isend_irecv(ops):
+            q.wait()
 
     def alltoall(self, send):
         (chunks,) = send
@@ -222,14 +255,21 @@ class SlabHessian:
         self.parts = parts
         g = self.geo
         dev = ctx.device
-        self.win = [ctx.empty(g.win_rows, n2 + 3) for _ in comm.ranks]
-        self.winv = [ctx.empty(2, g.win_rows, n2 + 3) for _ in comm.ranks]
-        self.rows = [ctx.empty(g.L, n2) for _ in comm.ranks]
+        self._alloc_windows()
         self.scr = [ctx.empty(g.L, n2) for _ in comm.ranks]
         self.vtD = [ctx.empty(2, g.L, n2) for _ in comm.ranks]
         self.b = [ctx.empty(2, g.L, n2) for _ in comm.ranks]
         self.partials = [ctx.empty(nt + 1, g.L) for _ in comm.ranks]
         self.flags = [torch.zeros(nt + 2, dtype=torch.int32, device=dev) for _ in comm.ranks]
+
+    def _alloc_windows(self):
+        g, ctx, n2 = self.geo, self.ctx, self.n2
+        self.win = [ctx.empty(g.win_rows, n2 + 3) for _ in self.comm.ranks]
+        self.winv = [ctx.empty(2, g.win_rows, n2 + 3) for _ in self.comm.ranks]
+        # row-filtered fields live inside their halo buffers (rows [top, top+L)), so a step's
+        # output needs no copy before the exchange
+        self.halo = [ctx.empty(g.top + g.L + g.bot, n2) for _ in self.comm.ranks]
+        self.rows = [h[g.top:g.top + g.L] for h in self.halo]
 
     # -- construction from the single-device operator (per-iterate invariants, sliced)
     @classmethod
@@ -269,15 +309,16 @@ class SlabHessian:
         column pass."""
         g, ctx = self.geo, self.ctx
         for i, f in enumerate(fields):
-            ctx.check(ctx.lib.vrg_prefilter_rows(ctx.h, g.L, self.n2, api._p(f), api._p(self.scr[i]), None))
-        halo = self.comm.exchange_rows(self.scr, g.top, g.bot)
-        for i, hb in enumerate(halo):
+            ctx.check(ctx.lib.vrg_prefilter_rows(ctx.h, g.L, self.n2, api._p(f), api._p(self.rows[i]), None))
+        self.comm.fill_halos(self.halo, g.L, g.top, g.bot)
+        for i, hb in enumerate(self.halo):
             ctx.check(ctx.lib.vrg_slab_cols(ctx.h, g.win_rows, self.n2, api._p(hb), api._p(windows[i])))
 
-    def _windows_from_rows(self, rowfiltered):
+    def _windows_from_rows(self):
+        """Coefficient windows from the row-filtered step outputs in self.rows."""
         g, ctx = self.geo, self.ctx
-        halo = self.comm.exchange_rows(rowfiltered, g.top, g.bot)
-        for i, hb in enumerate(halo):
+        self.comm.fill_halos(self.halo, g.L, g.top, g.bot)
+        for i, hb in enumerate(self.halo):
             ctx.check(ctx.lib.vrg_slab_cols(ctx.h, g.win_rows, self.n2, api._p(hb), api._p(self.win[i])))
 
     def _step(self, i, kind, coef, X, ops, ht, w, row_out, partial, flag):
@@ -312,7 +353,7 @@ class SlabHessian:
         # incremental state, the last step seeding the adjoint
         for j in range(1, nt + 1):
             if j > 1:
-                self._windows_from_rows(self.rows)
+                self._windows_from_rows()
             for i in ranks:
                 p = self.parts[i]
                 ops = [self.vtD[i][0], self.vtD[i][1], p["GD"][j - 1][0], p["GD"][j - 1][1], vts[i][0], vts[i][1],
@@ -327,7 +368,7 @@ class SlabHessian:
                     self._step(i, kind, self.win[i], p["Xf"], ops, ht, 0.0, self.rows[i], self.partials[i][0], None)
         # incremental adjoint + body force (+ beta A vt on the last step)
         for j in range(nt, 0, -1):
-            self._windows_from_rows(self.rows)
+            self._windows_from_rows()
             for i in ranks:
                 p = self.parts[i]
                 ops = [p["dvd"], p["dv"], p["G"][j - 1][0], p["G"][j - 1][1], self.b[i][0], self.b[i][1]]

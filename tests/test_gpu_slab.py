@@ -64,8 +64,7 @@ def test_slab_window_too_small_is_detected(ctx, api):
     H = api.HessianOperator(ctx, (F(v1), F(v2)), F(mT), F(mT), 2, 1e-3, api.COMPRESSIBLE, nt)
     S = slab.SlabHessian.from_operator(ctx, slab.LocalComm(G), H, 2, 1e-3)
     S.geo = slab.SlabGeometry(n, n, G, 0)  # pretend the departure points stay in their rows
-    S.win = [ctx.empty(S.geo.win_rows, n + 3) for _ in range(G)]
-    S.winv = [ctx.empty(2, S.geo.win_rows, n + 3) for _ in range(G)]
+    S._alloc_windows()
     L = n // G
     vt1, vt2 = synth.smooth_velocity(n, n, 3000)
     vts = [ctx.field(np.stack([vt1[i * L:(i + 1) * L], vt2[i * L:(i + 1) * L]])) for i in range(G)]

@@ -58,6 +58,20 @@ def test_local_exchange_periodic():
         assert torch.equal(o, full[rows])
 
 
+def test_local_fill_halos_matches_exchange():
+    n1, n2, G, top, bot = 64, 6, 4, 9, 13
+    full = torch.randn(n1, n2, dtype=torch.float64)
+    L = n1 // G
+    comm = slab.LocalComm(G)
+    bufs = [torch.zeros(top + L + bot, n2, dtype=torch.float64) for _ in range(G)]
+    for i in range(G):
+        bufs[i][top:top + L] = full[i * L:(i + 1) * L]
+    comm.fill_halos(bufs, L, top, bot)
+    ref = comm.exchange_rows(list(full.split(L, dim=0)), top, bot)
+    for b, r in zip(bufs, ref):
+        assert torch.equal(b, r)
+
+
 def test_distributed_reg_local():
     n1, n2 = 32, 24
     v = _field(n1, n2, 7)
@@ -91,6 +105,11 @@ def _worker(rank, world, port, q):
         comm = slab.DistComm()
         loc = v[:, rank * L:(rank + 1) * L].contiguous()
         ex = comm.exchange_rows([loc], 7, 9)[0]
+        buf = torch.zeros(2, 7 + L + 9, n2, dtype=torch.float64)
+        buf[:, 7:7 + L] = loc
+        comm.fill_halos([buf[0]], L, 7, 9)
+        comm.fill_halos([buf[1]], L, 7, 9)
+        assert torch.equal(buf, ex)
         reg = slab.distributed_reg(comm, [loc], n1, n2, 1, 1e-2)[0]
         m = comm.allreduce_max([torch.tensor([float(rank), -float(rank)])])[0]
         # numpy copies: tensors would travel as shared-memory handles the exiting worker frees

@@ -17,7 +17,7 @@ for n, nt, G, sc in [(256, 4, 1, 0.5), (256, 4, 1, 1.0), (1024, 8, 1, 1.0), (102
     outs = [[ctx.empty(L, n) for _ in range(G)] for _ in range(nt)]
     for j in range(1, nt + 1):
         if j > 1:
-            S._windows_from_rows(S.rows)
+            S._windows_from_rows()
         for i in range(G):
             S._step(i, slab.KIND_STATE, S.win[i], S.parts[i]["Xf"], [outs[j-1][i]], 1.0/nt, 0.0, S.rows[i], S.partials[i][j], None)
         got = np.concatenate([o.cpu().numpy() for o in outs[j-1]], axis=0)
