@@ -33,7 +33,12 @@ int guarded(vrg_ctx_s* c, F&& f) {
     int code = VRG_OK;
     try {
         if (c) VRG_CUDA(cudaSetDevice(c->ctx.device));
-        f();
+        if (c) {
+            vrg::AllocStreamScope as_(c->ctx.stream);
+            f();
+        } else {
+            f();
+        }
         return VRG_OK;
     } catch (const vrg::BlowupError& e) {
         code = VRG_BLOWUP;
@@ -239,7 +244,11 @@ int vrg_solver_create(vrg_ctx_t c, int n1, int n2, const double* v1, const doubl
     return guarded(c, [&] { *out = new vrg_solver_s{c, vrg::Solver(c->ctx, dims(n1, n2), v1, v2, nt)}; });
 }
 
-void vrg_solver_destroy(vrg_solver_t s) { delete s; }
+void vrg_solver_destroy(vrg_solver_t s) {
+    if (!s) return;
+    vrg::AllocStreamScope as_(s->owner->ctx.stream);  // stream-ordered release into the pool
+    delete s;
+}
 
 int vrg_solver_state(vrg_solver_t s, const double* m0, double* traj) {
     return guarded(s->owner, [&] { s->solver.state(m0, traj, true); });
@@ -369,7 +378,11 @@ int vrg_hess_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double*
     });
 }
 
-void vrg_hess_destroy(vrg_hess_t h) { delete h; }
+void vrg_hess_destroy(vrg_hess_t h) {
+    if (!h) return;
+    vrg::AllocStreamScope as_(h->owner->ctx.stream);  // stream-ordered release into the pool
+    delete h;
+}
 
 int vrg_hess_apply(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2) {
     return guarded(h->owner, [&] { h->hess.apply(vt1, vt2, o1, o2); });
@@ -517,7 +530,11 @@ int vrg_coarse_create(vrg_ctx_t c, int n1, int n2, const double* v1, const doubl
     });
 }
 
-void vrg_coarse_destroy(vrg_coarse_t c) { delete c; }
+void vrg_coarse_destroy(vrg_coarse_t c) {
+    if (!c) return;
+    vrg::AllocStreamScope as_(c->owner->ctx.stream);  // stream-ordered release into the pool
+    delete c;
+}
 
 int vrg_coarse_info(vrg_coarse_t c, int* n1c, int* n2c, int* nt) {
     *n1c = c->op->gc.n1;

@@ -52,6 +52,14 @@ void throwCufft(cufftResult r, const char* what, const char* file, int line);
     } while (0)
 #define VRG_LAUNCH_CHECK() VRG_CUDA(cudaGetLastError())
 
+// Stream of the library call in progress on this host thread (set by the C ABI entry points):
+// device buffers are allocated and freed stream-ordered on it (cudaMallocAsync/cudaFreeAsync
+// from the device's memory pool, which keeps freed blocks cached), so constructing operators
+// and solvers inside a Newton iteration costs no cudaMalloc/cudaFree device synchronisation.
+// Outside a library call (no stream set) buffers use cudaMalloc/cudaFree.
+extern thread_local cudaStream_t g_allocStream;
+extern thread_local bool g_allocStreamSet;
+
 // Owning device allocation (RAII).
 class DBuf {
 public:
@@ -67,11 +75,25 @@ public:
     }
     void alloc(std::size_t bytes) {
         release();
-        if (bytes) VRG_CUDA(cudaMalloc(&p_, bytes));
+        if (bytes) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (g_allocStreamSet) VRG_CUDA(cudaStreamIsCapturing(g_allocStream, &cs));
+            if (cs != cudaStreamCaptureStatusNone)
+                throw std::runtime_error("device allocation inside a CUDA graph capture");
+            if (g_allocStreamSet)
+                VRG_CUDA(cudaMallocAsync(&p_, bytes, g_allocStream));
+            else
+                VRG_CUDA(cudaMalloc(&p_, bytes));
+        }
         bytes_ = bytes;
     }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) {
+            if (g_allocStreamSet)
+                cudaFreeAsync(p_, g_allocStream);
+            else
+                cudaFree(p_);
+        }
         p_ = nullptr;
         bytes_ = 0;
     }
@@ -84,6 +106,20 @@ public:
 private:
     void* p_ = nullptr;
     std::size_t bytes_ = 0;
+};
+
+// Sets the allocation stream for the duration of a library call (restores the previous one).
+struct AllocStreamScope {
+    cudaStream_t prev;
+    bool prevSet;
+    explicit AllocStreamScope(cudaStream_t s) : prev(g_allocStream), prevSet(g_allocStreamSet) {
+        g_allocStream = s;
+        g_allocStreamSet = true;
+    }
+    ~AllocStreamScope() {
+        g_allocStream = prev;
+        g_allocStreamSet = prevSet;
+    }
 };
 
 struct GridDims {

@@ -797,6 +797,14 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
     const GraphKey key{kind, a, b, c, d};
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {
+        // first use of this (kind, pointers): launch directly; capture on the second use, so an
+        // operator applied once or twice (Newton iterations with few Krylov steps) pays no
+        // graph instantiation
+        launchSeq();
+        graphs_.emplace(key, GraphEntry{});
+        return;
+    }
+    if (!it->second.exec) {
         const long long l0 = ctx.launches;
         const std::size_t ev0 = ctx.evNext;
         cudaGraph_t graph = nullptr;
@@ -810,7 +818,7 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
             throw;
         }
         VRG_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
-        GraphEntry e;
+        GraphEntry& e = it->second;
         VRG_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
         cudaGraphDestroy(graph);
         e.launches = ctx.launches - l0;
@@ -821,7 +829,6 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
             ctx.evPool.erase(ctx.evPool.begin() + ev0, ctx.evPool.begin() + ctx.evNext);
             ctx.evNext = ev0;
         }
-        it = graphs_.emplace(key, std::move(e)).first;
     }
     VRG_CUDA(cudaGraphLaunch(it->second.exec, ctx.stream));
     ctx.launches += it->second.launches;
@@ -833,7 +840,7 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
 
 Hessian::~Hessian() {
     for (auto& kv : graphs_) {
-        cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         for (cudaEvent_t e : kv.second.events) cudaEventDestroy(e);
     }
 }

@@ -37,9 +37,18 @@ void checkGrid(int n1, int n2) {
         throw InvalidArgument("Grid: axis sizes must be even and >= 4");
 }
 
+thread_local cudaStream_t g_allocStream = nullptr;
+thread_local bool g_allocStreamSet = false;
+
 Ctx::Ctx(int dev, cudaStream_t s) : device(dev) {
     VRG_CUDA(cudaSetDevice(dev));
     VRG_CUDA(cudaFree(nullptr));
+    {  // keep freed blocks of the stream-ordered allocator cached (DBuf)
+        cudaMemPool_t pool;
+        VRG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        std::uint64_t keep = ~std::uint64_t(0);
+        VRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     if (s) {
         stream = s;
     } else {
