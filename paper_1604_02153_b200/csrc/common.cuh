@@ -52,13 +52,18 @@ void throwCufft(cufftResult r, const char* what, const char* file, int line);
     } while (0)
 #define VRG_LAUNCH_CHECK() VRG_CUDA(cudaGetLastError())
 
-// Stream of the library call in progress on this host thread (set by the C ABI entry points):
-// device buffers are allocated and freed stream-ordered on it (cudaMallocAsync/cudaFreeAsync
-// from the device's memory pool, which keeps freed blocks cached), so constructing operators
-// and solvers inside a Newton iteration costs no cudaMalloc/cudaFree device synchronisation.
-// Outside a library call (no stream set) buffers use cudaMalloc/cudaFree.
+// Stream of the library call in progress on this host thread (set by the C ABI entry points).
+// Device buffers released during a call go to a per-stream cache of cudaMalloc blocks instead
+// of cudaFree, and allocations on that stream reuse them (exact size): constructing operators
+// and solvers inside a Newton iteration then costs no cudaMalloc/cudaFree device
+// synchronisation.  Reuse is stream-ordered (a block only serves the stream that released it).
+// Outside a library call (no stream set) buffers use cudaMalloc/cudaFree directly.
 extern thread_local cudaStream_t g_allocStream;
 extern thread_local bool g_allocStreamSet;
+bool poolAllocations();  // VRG_POOL=0 disables the block cache
+void* cachedAlloc(std::size_t bytes, cudaStream_t s);
+void cachedFree(void* p, std::size_t bytes, cudaStream_t s);
+void releaseCachedBlocks(cudaStream_t s);
 
 // Owning device allocation (RAII).
 class DBuf {
@@ -76,12 +81,8 @@ public:
     void alloc(std::size_t bytes) {
         release();
         if (bytes) {
-            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-            if (g_allocStreamSet) VRG_CUDA(cudaStreamIsCapturing(g_allocStream, &cs));
-            if (cs != cudaStreamCaptureStatusNone)
-                throw std::runtime_error("device allocation inside a CUDA graph capture");
             if (g_allocStreamSet)
-                VRG_CUDA(cudaMallocAsync(&p_, bytes, g_allocStream));
+                p_ = cachedAlloc(bytes, g_allocStream);
             else
                 VRG_CUDA(cudaMalloc(&p_, bytes));
         }
@@ -90,7 +91,7 @@ public:
     void release() {
         if (p_) {
             if (g_allocStreamSet)
-                cudaFreeAsync(p_, g_allocStream);
+                cachedFree(p_, bytes_, g_allocStream);
             else
                 cudaFree(p_);
         }
@@ -114,7 +115,7 @@ struct AllocStreamScope {
     bool prevSet;
     explicit AllocStreamScope(cudaStream_t s) : prev(g_allocStream), prevSet(g_allocStreamSet) {
         g_allocStream = s;
-        g_allocStreamSet = true;
+        g_allocStreamSet = poolAllocations();
     }
     ~AllocStreamScope() {
         g_allocStream = prev;

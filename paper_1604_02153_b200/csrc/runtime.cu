@@ -2,6 +2,9 @@
 // BLAS-1 restates src/field.cpp:19-119: dot = h1*h2*sum(u*w) per component, normLinf = max|x|
 // with NaN ignored (std::max semantics), axpy/scale.  Reductions are two-stage with a fixed
 // block count and a fixed-order final pass, so results are run-to-run deterministic.
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 
@@ -40,15 +43,85 @@ void checkGrid(int n1, int n2) {
 thread_local cudaStream_t g_allocStream = nullptr;
 thread_local bool g_allocStreamSet = false;
 
+namespace {
+struct BlockCache {
+    std::mutex mu;
+    std::multimap<std::pair<cudaStream_t, std::size_t>, void*> blocks;
+    std::size_t held = 0;
+};
+BlockCache& blockCache() {
+    static BlockCache* c = new BlockCache;  // leaked on purpose: outlives every context
+    return *c;
+}
+constexpr std::size_t kCacheCap = std::size_t(48) << 30;  // beyond this, release for real
+}  // namespace
+
+void* cachedAlloc(std::size_t bytes, cudaStream_t s) {
+    BlockCache& c = blockCache();
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        auto it = c.blocks.find({s, bytes});
+        if (it != c.blocks.end()) {
+            void* p = it->second;
+            c.blocks.erase(it);
+            c.held -= bytes;
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {  // drop the cache and retry once
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lock(c.mu);
+        cudaStreamSynchronize(s);
+        for (auto& kv : c.blocks) cudaFree(kv.second);
+        c.blocks.clear();
+        c.held = 0;
+        e = cudaMalloc(&p, bytes);
+    }
+    VRG_CUDA(e);
+    return p;
+}
+
+void cachedFree(void* p, std::size_t bytes, cudaStream_t s) {
+    BlockCache& c = blockCache();
+    {
+        std::lock_guard<std::mutex> lock(c.mu);
+        if (c.held + bytes <= kCacheCap) {
+            c.blocks.emplace(std::make_pair(s, bytes), p);
+            c.held += bytes;
+            return;
+        }
+    }
+    cudaFree(p);
+}
+
+// Frees the cached blocks of a stream (its context is going away).
+void releaseCachedBlocks(cudaStream_t s) {
+    BlockCache& c = blockCache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    for (auto it = c.blocks.begin(); it != c.blocks.end();) {
+        if (it->first.first == s) {
+            cudaFree(it->second);
+            c.held -= it->first.second;
+            it = c.blocks.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+bool poolAllocations() {
+    static const bool on = [] {
+        const char* e = std::getenv("VRG_POOL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 Ctx::Ctx(int dev, cudaStream_t s) : device(dev) {
     VRG_CUDA(cudaSetDevice(dev));
     VRG_CUDA(cudaFree(nullptr));
-    {  // keep freed blocks of the stream-ordered allocator cached (DBuf)
-        cudaMemPool_t pool;
-        VRG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        std::uint64_t keep = ~std::uint64_t(0);
-        VRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    }
     if (s) {
         stream = s;
     } else {
@@ -74,6 +147,7 @@ Ctx::~Ctx() {
     scratch.clear();
     reduce.release();
     if (hostScalars) cudaFreeHost(hostScalars);
+    if (stream) releaseCachedBlocks(stream);
     if (ownStream && stream) cudaStreamDestroy(stream);
 }
 
