@@ -214,32 +214,64 @@ def reg_symbol_cols(n1, n2, norm, beta, c0, c1, device):
     return beta * ksq ** int(norm)
 
 
-def distributed_reg(comm, vts, n1, n2, norm, beta):
-    """beta A vt (applyReg, spectral.cpp:109-120) of slab fields vts[i] = (..., L, n2): row FFTs
-    of the local rows, all-to-all transpose to column blocks, column FFTs, symbol, inverse
-    column FFTs, all-to-all back, inverse row FFTs (torch.fft = cuFFT on the device)."""
+def distributed_spectral(comm, fields, n1, n2, op):
+    """Distributed 2-D FFT pipeline over slab fields: fields[i] = (m, L, n2) -> per rank the
+    inverse transforms of op(spectra (m, n1, wc) of the rank's column block, k1 (n1, 1),
+    k2 (1, wc), valid columns) = (m', n1, wc).  Row FFTs of the local rows, all-to-all transpose
+    to column blocks, column FFTs, op, inverse column FFTs, all-to-all back, inverse row FFTs
+    (torch.fft = cuFFT on the device; the inverse transforms carry the 1/N of
+    fft.cpp:70-78)."""
     G = comm.size
     nc = n2 // 2 + 1
     wc = -(-nc // G)  # half-spectrum columns per rank in the transposed layout
     L = n1 // G
     send = []
-    for vt in vts:
-        s = torch.fft.rfft(vt, dim=-1)
+    for f in fields:
+        s = torch.fft.rfft(f, dim=-1)
         s = torch.nn.functional.pad(s, (0, G * wc - nc))
         send.append([s[..., q * wc:(q + 1) * wc].contiguous() for q in range(G)])
     recv = comm.alltoall(send)
     back = []
     for k, q in enumerate(comm.ranks):
-        col = torch.cat(recv[k], dim=-2)  # (..., n1, wc)
-        f = torch.fft.fft(col, dim=-2)
+        col = torch.fft.fft(torch.cat(recv[k], dim=-2), dim=-2)  # (m, n1, wc)
         c0, c1 = min(q * wc, nc), min((q + 1) * wc, nc)
-        sym = reg_symbol_cols(n1, n2, norm, beta, c0, c1, col.device)
-        f[..., :c1 - c0] *= sym
-        f[..., c1 - c0:] = 0
-        col = torch.fft.ifft(f, dim=-2)
+        dev = col.device
+        k1 = torch.arange(n1, device=dev, dtype=torch.float64)
+        k1 = torch.where(k1 <= n1 // 2, k1, k1 - n1)[:, None]
+        k2 = torch.arange(q * wc, (q + 1) * wc, device=dev, dtype=torch.float64)[None, :]
+        out = op(col, k1, k2, c1 - c0)
+        out[..., c1 - c0:] = 0
+        col = torch.fft.ifft(out, dim=-2)
         back.append([col[..., r * L:(r + 1) * L, :].contiguous() for r in range(G)])
     got = comm.alltoall(back)
     return [torch.fft.irfft(torch.cat(got[k], dim=-1)[..., :nc], n=n2, dim=-1) for k in range(len(comm.ranks))]
+
+
+def distributed_reg(comm, vts, n1, n2, norm, beta):
+    """beta A vt (applyReg, spectral.cpp:109-120) of slab fields vts[i] = (..., L, n2)."""
+    def op(f, k1, k2, _):
+        return f * (beta * (k1 ** 2 + k2 ** 2) ** int(norm))
+    return distributed_spectral(comm, vts, n1, n2, op)
+
+
+def _nyq0(k, n):
+    return torch.where(k == n // 2, torch.zeros_like(k), k)  # spectral.cpp:31-33
+
+
+def distributed_gradient(comm, fields, n1, n2):
+    """spectral::gradient (spectral.cpp:68-87) of slab fields (m, L, n2) -> (m, 2, L, n2)."""
+    def op(f, k1, k2, _):
+        d1 = 1j * _nyq0(k1, n1) * f
+        d2 = 1j * _nyq0(k2, n2) * f
+        return torch.stack([d1, d2], dim=-3)
+    return distributed_spectral(comm, fields, n1, n2, op)
+
+
+def distributed_divergence(comm, vs, n1, n2):
+    """spectral::divergence (spectral.cpp:89-107) of slab vector fields (2, L, n2) -> (L, n2)."""
+    def op(f, k1, k2, _):
+        return 1j * _nyq0(k1, n1) * f[..., 0, :, :] + 1j * _nyq0(k2, n2) * f[..., 1, :, :]
+    return distributed_spectral(comm, vs, n1, n2, op)
 
 
 # ------------------------------------------------------------------------------ operator
@@ -302,6 +334,104 @@ class SlabHessian:
         if not math.isfinite(reach):
             raise api.InvalidArgument("evaluate: non-finite point coordinate")
         return cls(ctx, comm, n1, n2, nt, norm, beta, parts, math.ceil(reach) + 3)
+
+    # -- distributed construction (every per-iterate invariant computed on the slabs)
+    @classmethod
+    def build(cls, ctx, comm, vs, mTs, n1, nt, norm, beta):
+        """HessianOperator ctor (inverse.cpp:150-175) + the lazy per-velocity caches of its
+        Solver (transport.cpp:91-127) on the slabs: vs[i] = (2, L, n2) velocity rows of rank i,
+        mTs[i] = (L, n2) template rows.  Departure points by the Heun trace (transport.cpp:60-89,
+        same rounding steps as EpiTrace), the state by slab SL steps with the guard, gradients
+        and div v by the distributed FFT, (grad m)_D and (div v)_D by slab interpolation."""
+        n2 = vs[0].shape[-1]
+        G = comm.size
+        L = n1 // G
+        ht = 1.0 / nt
+        h1, h2 = 2 * math.pi / n1, 2 * math.pi / n2
+        vmax = float(comm.allreduce_max([v[0].abs().amax() for v in vs])[0])
+        if not math.isfinite(vmax):
+            raise api.InvalidArgument("transport velocity: non-finite value")
+        # trace: the star and departure points move by at most ht max|v1| along axis 1
+        tr = cls(ctx, comm, n1, n2, nt, norm, beta, None, math.ceil(ht * vmax / h1) + 3)
+        for c in range(2):
+            tr._prefilter([v[c] for v in vs], [w[c] for w in tr.winv])
+        X = {}
+        for sgn, name in ((1.0, "Xf"), (-1.0, "Xb")):
+            xs = []
+            for i, q in enumerate(comm.ranks):
+                dev = vs[i].device
+                i1 = (q * L + torch.arange(L, device=dev, dtype=torch.float64))[:, None]
+                i2 = torch.arange(n2, device=dev, dtype=torch.float64)[None, :]
+                c1 = (-math.pi) + h1 * i1
+                c2 = (-math.pi) + h2 * i2
+                star = torch.stack([c1 - (sgn * ht) * vs[i][0], c2 - (sgn * ht) * vs[i][1]])
+                vstar = ctx.empty(2, L, n2)
+                for c in range(2):
+                    tr._step(i, KIND_STORE, tr.winv[i][c], star, [vstar[c]], ht, 0.0, tr.scr[i], tr.partials[i][0],
+                             None)
+                sh = sgn * 0.5 * ht
+                xs.append(torch.stack([c1 - sh * (vs[i][0] + vstar[0]), c2 - sh * (vs[i][1] + vstar[1])]))
+            X[name] = xs
+        tr._check_window()
+        reach = max(max(row_reach(X["Xf"][i][0], n1, q * L), row_reach(X["Xb"][i][0], n1, q * L))
+                    for i, q in enumerate(comm.ranks))
+        reach = float(comm.allreduce_max([torch.tensor(reach)] * len(comm.ranks))[0])
+        if not math.isfinite(reach):
+            raise api.InvalidArgument("evaluate: non-finite point coordinate")
+        S = cls(ctx, comm, n1, n2, nt, norm, beta, None, math.ceil(reach) + 3)
+        # state m_j (slState with the guard, transport.cpp:214-227)
+        ms = [ctx.empty(nt + 1, L, n2) for _ in comm.ranks]
+        for i in range(len(comm.ranks)):
+            ms[i][0].copy_(mTs[i])
+            S.partials[i].zero_()
+            S.flags[i].zero_()
+            S.partials[i][0][:L].copy_(mTs[i].abs().amax(dim=1))
+            S.flags[i][0] = (~torch.isfinite(mTs[i])).any().to(S.flags[i].dtype)  # prefilter input check
+        S._prefilter([m[0] for m in ms], S.win)
+        for j in range(1, nt + 1):
+            if j > 1:
+                S._windows_from_rows()
+            for i in range(len(comm.ranks)):
+                S._step(i, KIND_STATE, S.win[i], X["Xf"][i], [ms[i][j]], ht, 0.0, S.rows[i], S.partials[i][j],
+                        S.flags[i][j:j + 1])
+        S._check_state_guard()
+        # gradients G_j = grad m_j, (grad m_{j-1})_D, div v and (div v)_D
+        grads = distributed_gradient(comm, ms, n1, n2)  # (nt+1, 2, L, n2) per rank
+        gds = [ctx.empty(nt, 2, L, n2) for _ in comm.ranks]
+        for j in range(1, nt + 1):
+            for c in range(2):
+                S._prefilter([g[j - 1][c] for g in grads], S.win)
+                for i in range(len(comm.ranks)):
+                    S._step(i, KIND_STORE, S.win[i], X["Xf"][i], [gds[i][j - 1][c]], ht, 0.0, S.scr[i],
+                            S.partials[i][0], None)
+        dvs = distributed_divergence(comm, vs, n1, n2)
+        S._prefilter(dvs, S.win)
+        dvds = [ctx.empty(L, n2) for _ in comm.ranks]
+        for i in range(len(comm.ranks)):
+            S._step(i, KIND_STORE, S.win[i], X["Xb"][i], [dvds[i]], ht, 0.0, S.scr[i], S.partials[i][0], None)
+        S._check_window()
+        S.parts = [dict(Xf=X["Xf"][i], Xb=X["Xb"][i], G=grads[i], GD=gds[i], dv=dvs[i], dvd=dvds[i], m=ms[i])
+                   for i in range(len(comm.ranks))]
+        return S
+
+    def _check_window(self):
+        fl = self.comm.allreduce_max([f.to(torch.float64) for f in self.flags])[0].cpu()
+        if fl[self.nt + 1] != 0:
+            raise api.VrgError("slab window too small for the departure displacement")
+
+    def _check_state_guard(self):
+        """checkGuard of slState (transport.cpp:16-20, 221): ||m_j|| <= 1e3 ||m_0||, forward."""
+        nt = self.nt
+        mx = self.comm.allreduce_max([p.amax(dim=1) for p in self.partials])[0].cpu()
+        fl = self.comm.allreduce_max([f.to(torch.float64) for f in self.flags])[0].cpu()
+        if fl[nt + 1] != 0:
+            raise api.VrgError("slab window too small for the departure displacement")
+        threshold = 1e3 * float(mx[0])
+        for j in range(1, nt + 1):
+            if fl[j - 1] != 0:
+                raise api.InvalidArgument("prefilter: non-finite value")
+            if float(mx[j]) > threshold:
+                raise api.BlowupError(f"state solve exceeded the blow-up guard at step {j}")
 
     # -- building blocks
     def _prefilter(self, fields, windows):

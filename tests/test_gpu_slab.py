@@ -70,3 +70,45 @@ def test_slab_window_too_small_is_detected(ctx, api):
     vts = [ctx.field(np.stack([vt1[i * L:(i + 1) * L], vt2[i * L:(i + 1) * L]])) for i in range(G)]
     with pytest.raises(api.VrgError, match="window too small"):
         S.apply(vts)
+
+
+@pytest.mark.parametrize("n,nt,G", [(256, 4, 2), (512, 8, 4)])
+def test_slab_distributed_setup_vs_single_device(ctx, api, n, nt, G):
+    """SlabHessian.build: departure points, state, gradients, (grad m)_D, div v, (div v)_D and
+    the matvec computed on the slabs, against the single-device operator."""
+    mT = synth.smoothed_noise(n, n, 1000)
+    v1, v2 = synth.smooth_velocity(n, n, 2000)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    F = ctx.field
+    H = api.HessianOperator(ctx, (F(v1), F(v2)), F(mT), F(mT), 2, 1e-3, api.COMPRESSIBLE, nt)
+    ref = slab.SlabHessian.from_operator(ctx, slab.LocalComm(G), H, 2, 1e-3)
+    L = n // G
+    comm = slab.LocalComm(G)
+    vs = [F(np.stack([v1[i * L:(i + 1) * L], v2[i * L:(i + 1) * L]])) for i in range(G)]
+    mTs = [F(mT[i * L:(i + 1) * L]) for i in range(G)]
+    S = slab.SlabHessian.build(ctx, comm, vs, mTs, n, nt, 2, 1e-3)
+    for key in ("Xf", "Xb", "G", "GD", "dv", "dvd"):
+        got = np.concatenate([p[key].cpu().numpy() for p in S.parts], axis=-2)
+        exp = np.concatenate([p[key].cpu().numpy() for p in ref.parts], axis=-2)
+        assert rel(got, exp) < TOL, key
+    state = np.concatenate([p["m"].cpu().numpy() for p in S.parts], axis=-2)
+    assert rel(state, H.state().cpu().numpy()) < TOL
+    vts = [F(np.stack([vt1[i * L:(i + 1) * L], vt2[i * L:(i + 1) * L]])) for i in range(G)]
+    d1, d2 = H.apply_data_term((F(vt1), F(vt2)))
+    got = np.concatenate([o.cpu().numpy() for o in S.apply(vts, data_term_only=True)], axis=1)
+    assert rel(got[0], d1.cpu().numpy()) < TOL and rel(got[1], d2.cpu().numpy()) < TOL
+
+
+def test_slab_state_guard(ctx, api):
+    """The slab state solve raises the reference's blow-up error (amplifying velocity)."""
+    n, nt, G = 64, 4, 2
+    x = np.linspace(-np.pi, np.pi, n, endpoint=False)
+    X1, X2 = np.meshgrid(x, x, indexing="ij")
+    v1, v2 = 30 * np.sin(X1), 30 * np.sin(X2)  # compressive: the transported field blows up
+    mT = np.cos(X1) + np.cos(X2)
+    F = ctx.field
+    L = n // G
+    vs = [F(np.stack([v1[i * L:(i + 1) * L], v2[i * L:(i + 1) * L]])) for i in range(G)]
+    mTs = [F(mT[i * L:(i + 1) * L]) for i in range(G)]
+    with pytest.raises((api.BlowupError, api.VrgError)):
+        slab.SlabHessian.build(ctx, slab.LocalComm(G), vs, mTs, n, nt, 2, 1e-3)

@@ -3,10 +3,11 @@
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
       --master-port 29512 tools/slab_bench.py [--n 4096] [--nt 32] [--steps 5]
 
-Every rank builds the per-iterate invariants with the single-device operator (replicated
-setup), keeps its slab, and times K slab matvecs (device events, barrier on both sides, max
-over ranks).  Rank 0 checks the assembled result against the single-device matvec and prints
-one JSON line.  With one process it runs the same code path over a 1-rank NCCL group.
+Every rank builds its slab of the per-iterate invariants (SlabHessian.build: distributed
+setup; --setup replicated slices the single-device operator instead), and times K slab
+matvecs (device events, barrier on both sides, max over ranks).  Rank 0 checks the assembled
+result against the single-device matvec and prints one JSON line.  With one process it runs
+the same code path over a 1-rank NCCL group.
 """
 import argparse
 import json
@@ -29,6 +30,7 @@ def main():
     ap.add_argument("--beta", type=float, default=1e-4)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--setup", default="distributed", choices=["distributed", "replicated"])
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -43,15 +45,26 @@ def main():
     v1, v2 = synth.smooth_velocity(n, n, 2000)
     vt1, vt2 = synth.smooth_velocity(n, n, 3000)
     F = ctx.field
-    H = api.HessianOperator(ctx, (F(v1), F(v2)), F(mT), F(mT), api.H2SEMI, a.beta, api.COMPRESSIBLE, nt)
     comm = slab.DistComm()
-    S = slab.SlabHessian.from_operator(ctx, comm, H, api.H2SEMI, a.beta)
     L = n // world
+    dev = torch.device("cuda", local)
+    torch.cuda.synchronize(dev)
+    t_setup = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_setup[0].record()
+    if a.setup == "replicated":
+        H = api.HessianOperator(ctx, (F(v1), F(v2)), F(mT), F(mT), api.H2SEMI, a.beta, api.COMPRESSIBLE, nt)
+        S = slab.SlabHessian.from_operator(ctx, comm, H, api.H2SEMI, a.beta)
+    else:
+        vs = [F(np.stack([v1[rank * L:(rank + 1) * L], v2[rank * L:(rank + 1) * L]]))]
+        S = slab.SlabHessian.build(ctx, comm, vs, [F(mT[rank * L:(rank + 1) * L])], n, nt, api.H2SEMI, a.beta)
+        H = None
+    t_setup[1].record()
+    torch.cuda.synchronize(dev)
+    setup_ms = t_setup[0].elapsed_time(t_setup[1])
     vts = [F(np.stack([vt1[rank * L:(rank + 1) * L], vt2[rank * L:(rank + 1) * L]]))]
     outs = [ctx.empty(2, L, n)]
     for _ in range(a.warmup):
         S.apply(vts, outs)
-    dev = torch.device("cuda", local)
     dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -68,6 +81,8 @@ def main():
     dist.all_gather(full, outs[0])
     if rank == 0:
         got = torch.cat(full, dim=1).cpu().numpy()
+        if H is None:
+            H = api.HessianOperator(ctx, (F(v1), F(v2)), F(mT), F(mT), api.H2SEMI, a.beta, api.COMPRESSIBLE, nt)
         vtd = (F(vt1), F(vt2))
         h1, h2 = H.apply(vtd)
         e = np.stack([h1.cpu().numpy(), h2.cpu().numpy()])
@@ -83,7 +98,8 @@ def main():
                           "matvecs_per_s": 1e3 / float(ms.item()),
                           "single_device_ms_per_matvec": t0.elapsed_time(t1) / a.steps,
                           "max_rel_diff_vs_single_device": float(np.abs(got - e).max() / np.abs(e).max()),
-                          "slab_rows": L, "window_rows": S.geo.win_rows, "halo_rows": [S.geo.top, S.geo.bot]}))
+                          "slab_rows": L, "window_rows": S.geo.win_rows, "halo_rows": [S.geo.top, S.geo.bot],
+                          "setup": a.setup, "setup_ms_rank0": setup_ms}))
     dist.destroy_process_group()
 
 
