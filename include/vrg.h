@@ -204,7 +204,8 @@ int vrg_solve_kkt(vrg_hess_t h, const double* rhs1, const double* rhs2, double t
                   double coarse_cfl, double* sol1, double* sol2, double* result);
 
 /* ---- newton (newton.hpp:10-12): inverse::newtonSolve on HOST images mR/mT, v returned on the host.
- * cfg_int = [maxOuterIter, maxInnerIter, ntOverride(0 = CFL), lsMaxSteps]
+ * cfg_int = [maxOuterIter, maxInnerIter, ntOverride(0 = CFL), lsMaxSteps, hessianMode (VRG_GAUSS_NEWTON |
+ *            VRG_FULL_NEWTON)]
  * cfg_dbl = [tolRelGrad, tolAbsGrad, forcingCap, lsC1, lsShrink, gradCfl]
  * pc_int / pc_dbl as for vrg_solve_kkt (has_eig = 0: estimated at v = 0 like newton.cpp:36-40)
  * records: per outer iteration 12 doubles [iter, gradNormInf, gradNormRel, objective, mismatch,

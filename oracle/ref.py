@@ -36,7 +36,7 @@ def lib():
             raise FileNotFoundError(f"{LIB_PATH} missing: run `make -C oracle`")
         _lib = C.CDLL(LIB_PATH)
         _lib.ref_last_error.restype = C.c_char_p
-        for name in ("ref_hess_create", "ref_coarse_create"):
+        for name in ("ref_hess_create", "ref_hess_create_mode", "ref_coarse_create"):
             getattr(_lib, name).restype = C.c_void_p
         _lib.ref_hess_apply.argtypes = [C.c_void_p, _D, _D, C.c_int, _D, _D]
         _lib.ref_hess_destroy.argtypes = [C.c_void_p]
@@ -122,6 +122,16 @@ def solve_incstate(v1, v2, nt, m0, vt1, vt2):
 
 def solve_incadjoint_gn(v1, v2, nt, lt1):
     return _traj_call(lib().ref_solve_incadjoint_gn, v1, v2, nt, lt1)
+
+
+def solve_incadjoint_fn(v1, v2, nt, vt1, vt2, lt1, adj):
+    """full-Newton SL incremental adjoint from the adjoint trajectory adj ((nt+1, n1, n2))."""
+    v1, v2 = _c(v1), _c(v2)
+    n1, n2 = v1.shape
+    out = np.empty((nt + 1, n1, n2))
+    vt1, vt2, lt1, adj = map(_c, (vt1, vt2, lt1, adj))
+    _check(lib().ref_solve_incadjoint_fn(n1, n2, _p(v1), _p(v2), nt, _p(vt1), _p(vt2), _p(lt1), _p(adj), _p(out)))
+    return out
 
 
 def solve_state_final(v1, v2, nt, m0):
@@ -216,12 +226,12 @@ def random_bandlimited_velocity(n1, n2, seed):
 class Hessian:
     """inverse::HessianOperator (GN, SL, fixed nt) held open for steady-state applies."""
 
-    def __init__(self, v1, v2, mR, mT, norm, beta, deform, nt):
+    def __init__(self, v1, v2, mR, mT, norm, beta, deform, nt, mode=0):
         v1, v2, mR, mT = map(_c, (v1, v2, mR, mT))
         self.shape = v1.shape
         st = C.c_int()
-        self.h = lib().ref_hess_create(v1.shape[0], v1.shape[1], _p(v1), _p(v2), _p(mR), _p(mT), norm,
-                                       C.c_double(beta), deform, nt, C.byref(st))
+        self.h = lib().ref_hess_create_mode(v1.shape[0], v1.shape[1], _p(v1), _p(v2), _p(mR), _p(mT), norm,
+                                            C.c_double(beta), deform, nt, int(mode), C.byref(st))
         _check(st.value)
 
     def apply(self, vt1, vt2, data_only=False):
@@ -293,10 +303,10 @@ def estimate_eigs(mR, mT, norm, beta, deform):
 
 
 def newton_solve(mR, mT, norm, beta, deform, *, max_outer=50, max_inner=500, nt=0, grad_cfl=1.0,
-                 two_level=True, cheb=True, cheb_iters=10, tol_rel=1e-2, tol_abs=1e-5, eps_scale=0.1):
+                 two_level=True, cheb=True, cheb_iters=10, tol_rel=1e-2, tol_abs=1e-5, eps_scale=0.1, mode=0):
     mR, mT = _c(mR), _c(mT)
     n1, n2 = mR.shape
-    cfg_i = np.array([max_outer, max_inner, nt, int(two_level), int(cheb), cheb_iters], dtype=np.int32)
+    cfg_i = np.array([max_outer, max_inner, nt, int(two_level), int(cheb), cheb_iters, int(mode)], dtype=np.int32)
     cfg_d = np.array([tol_rel, tol_abs, grad_cfl, eps_scale])
     v1, v2 = np.empty_like(mR), np.empty_like(mR)
     rep = np.zeros((max_outer + 1, 10))

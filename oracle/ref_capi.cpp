@@ -192,6 +192,20 @@ int ref_solve_incadjoint_gn(int n1, int n2, const double* v1, const double* v2, 
     });
 }
 
+// full-Newton SL incremental adjoint (transport.cpp:403-420) from an adjoint trajectory
+int ref_solve_incadjoint_fn(int n1, int n2, const double* v1, const double* v2, int nt, const double* vt1,
+                            const double* vt2, const double* lt1, const double* adjTraj, double* traj) {
+    return guarded([&] {
+        transport::Solver s(vf(n1, n2, v1, v2), transport::TimeGrid(nt), slCfg(nt, 1.0));
+        transport::TransportSolution adj;
+        adj.nodes.frames.resize(static_cast<std::size_t>(nt) + 1);
+        const std::size_t N = static_cast<std::size_t>(n1) * n2;
+        for (int j = 0; j <= nt; ++j) adj.nodes.frames[j] = sf(n1, n2, adjTraj + j * N);
+        putTraj(s.solveIncAdjoint(vf(n1, n2, vt1, vt2), sf(n1, n2, lt1), &adj, transport::HessianMode::FullNewton),
+                traj);
+    });
+}
+
 int ref_jacobian_det(int n1, int n2, const double* v1, const double* v2, int nt, double cfl, double* out) {
     return guarded([&] {
         VectorField v = vf(n1, n2, v1, v2);
@@ -265,18 +279,23 @@ struct RefHess {
     std::unique_ptr<inverse::HessianOperator> op;
 };
 
-void* ref_hess_create(int n1, int n2, const double* v1, const double* v2, const double* mR, const double* mT,
-                      int norm, double beta, int deform, int nt, int* status) {
+void* ref_hess_create_mode(int n1, int n2, const double* v1, const double* v2, const double* mR, const double* mT,
+                           int norm, double beta, int deform, int nt, int mode, int* status) {
     RefHess* h = nullptr;
     *status = guarded([&] {
         auto* hh = new RefHess;
         hh->problem = problemOf(n1, n2, mR, mT);
-        hh->op = std::make_unique<inverse::HessianOperator>(vf(n1, n2, v1, v2), hh->problem, modelOf(norm, beta, deform),
-                                                            transport::TimeGrid(nt), slCfg(nt, 1.0),
-                                                            transport::HessianMode::GaussNewton);
+        hh->op = std::make_unique<inverse::HessianOperator>(
+            vf(n1, n2, v1, v2), hh->problem, modelOf(norm, beta, deform), transport::TimeGrid(nt), slCfg(nt, 1.0),
+            mode == 1 ? transport::HessianMode::FullNewton : transport::HessianMode::GaussNewton);
         h = hh;
     });
     return h;
+}
+
+void* ref_hess_create(int n1, int n2, const double* v1, const double* v2, const double* mR, const double* mT,
+                      int norm, double beta, int deform, int nt, int* status) {
+    return ref_hess_create_mode(n1, n2, v1, v2, mR, mT, norm, beta, deform, nt, 0, status);
 }
 
 int ref_hess_apply(void* handle, const double* vt1, const double* vt2, int dataOnly, double* o1, double* o2) {
@@ -397,6 +416,7 @@ int ref_newton_solve(int n1, int n2, const double* mR, const double* mT, int nor
         pc.coarseSolver = cfgI[4] ? precond::CoarseSolverKind::Cheb : precond::CoarseSolverKind::Pcg;
         pc.chebIters = cfgI[5];
         pc.epsScale = cfgD[3];
+        cfg.hessianMode = cfgI[6] == 1 ? transport::HessianMode::FullNewton : transport::HessianMode::GaussNewton;
         auto [v, r] = inverse::newtonSolve(p, modelOf(norm, beta, deform), cfg, pc);
         put(v[0], v1);
         put(v[1], v2);

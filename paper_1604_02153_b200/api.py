@@ -444,14 +444,15 @@ RECORD_FIELDS = ("iter", "gradNormInf", "gradNormRel", "objective", "mismatch", 
 
 def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=0, ls_max_steps=20,
                  tol_rel=1e-2, tol_abs=1e-5, forcing_cap=0.5, ls_c1=1e-4, ls_shrink=0.5, grad_cfl=1.0,
-                 kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10, eps_scale=0.1, eig=None):
+                 kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10, eps_scale=0.1, eig=None,
+                 hessian_mode=GAUSS_NEWTON):
     """inverse::newtonSolve on host images (numpy); returns (v1, v2, records, summary)."""
     import numpy as np
 
     mR = np.ascontiguousarray(mR, dtype=np.float64)
     mT = np.ascontiguousarray(mT, dtype=np.float64)
     n1, n2 = mR.shape
-    ci = (C.c_int * 4)(max_outer, max_inner, nt, ls_max_steps)
+    ci = (C.c_int * 5)(max_outer, max_inner, nt, ls_max_steps, hessian_mode)
     cd = (C.c_double * 6)(tol_rel, tol_abs, forcing_cap, ls_c1, ls_shrink, grad_cfl)
     pi, pd = _pc_arrays(kind, coarse_solver, cheb_iters, eps_scale, eig)
     v1, v2 = np.empty_like(mR), np.empty_like(mR)

@@ -273,12 +273,19 @@ int vrg_solver_incstate(vrg_solver_t s, const double* vt1, const double* vt2, co
 int vrg_solver_incadjoint(vrg_solver_t s, const double* vt1, const double* vt2, const double* lt1,
                           const double* adjoint, int mode, double* traj) {
     return guarded(s->owner, [&] {
-        (void)vt1;
-        (void)vt2;
         if (mode == VRG_FULL_NEWTON) {
             if (!adjoint)
                 throw vrg::InvalidArgument("solveIncAdjoint: full Newton mode requires the adjoint trajectory");
-            throw vrg::NotSupported("solveIncAdjoint: full-Newton SL incremental adjoint is not implemented yet");
+            vrg::Solver& S = s->solver;
+            const std::size_t N = S.g.points();
+            vrg::DBuf work(sizeof(double) * 5 * N), flag(64);
+            VRG_CUDA(cudaMemsetAsync(flag.d(), 0, sizeof(unsigned), S.ctx.stream));
+            S.incAdjointFullNewton(vt1, vt2, lt1, adjoint, traj, work.d(), flag.as<unsigned>());
+            unsigned h = 0;
+            VRG_CUDA(cudaMemcpyAsync(&h, flag.d(), sizeof h, cudaMemcpyDeviceToHost, S.ctx.stream));
+            S.ctx.sync();
+            if (h) throw vrg::InvalidArgument("prefilter: non-finite value");
+            return;
         }
         // Gauss-Newton drops every term in lambda: same operator as the adjoint
         // (transport.cpp:392-397), unguarded.
@@ -370,10 +377,10 @@ int vrg_hess_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double*
                     vrg_hess_t* out) {
     *out = nullptr;
     return guarded(c, [&] {
-        if (mode != VRG_GAUSS_NEWTON)
-            throw vrg::NotSupported("HessianOperator: full-Newton mode is not implemented on the device yet");
+        if (mode != VRG_GAUSS_NEWTON && mode != VRG_FULL_NEWTON)
+            throw vrg::InvalidArgument("HessianOperator: unknown Hessian mode");
         *out = new vrg_hess_s{c, vrg::Hessian(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation),
-                                              nt, state),
+                                              nt, state, mode == VRG_FULL_NEWTON ? 1 : 0),
                               vrg::DBuf()};
     });
 }
@@ -619,6 +626,9 @@ int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const d
         cfg.maxInnerIter = cfg_int[1];
         cfg.ntOverride = cfg_int[2];
         cfg.lsMaxSteps = cfg_int[3];
+        cfg.hessianMode = cfg_int[4];
+        if (cfg.hessianMode != VRG_GAUSS_NEWTON && cfg.hessianMode != VRG_FULL_NEWTON)
+            throw vrg::InvalidArgument("newtonSolve: unknown Hessian mode");
         cfg.tolRelGrad = cfg_dbl[0];
         cfg.tolAbsGrad = cfg_dbl[1];
         cfg.forcingCap = cfg_dbl[2];

@@ -64,6 +64,33 @@ struct EpiContinuity {
     }
 };
 
+// Full-Newton SL incremental adjoint step (solveIncAdjoint, src/transport.cpp:409-418): the
+// continuity step with the source q = div(lambda vt) at the departure points (qD) and at the
+// arrival points of the next time node (qPrev).
+struct EpiContinuityFN {
+    static constexpr const char* kName = "evaluate/continuity_fn";
+    static constexpr bool kGuard = false;
+    double* guardPartials = nullptr;
+    const double* dvDep;
+    const double* dv;
+    const double* qD;
+    const double* qPrev;
+    double ht;
+    double* out;
+    struct Pre {
+        double dvDep, dv, qD, qPrev;
+    };
+    __device__ Pre prefetch(std::size_t p) const { return {dvDep[p], dv[p], qD[p], qPrev[p]}; }
+    __device__ double operator()(std::size_t p, const double* v, const Pre& q) const {
+        const double lamTD = v[0];
+        const double f0 = lamTD * q.dvDep + q.qD;
+        const double pred = lamTD + ht * f0;
+        const double o = lamTD + 0.5 * ht * (f0 + pred * q.dv + q.qPrev);
+        out[p] = o;
+        return o;
+    }
+};
+
 // K6 epilogue (solveIncState SL, src/transport.cpp:333-338).
 struct EpiIncState {
     static constexpr const char* kName = "evaluate/incstate";

@@ -303,9 +303,8 @@ __global__ void k_row_disp(const double* __restrict__ x1, int n1, int n2, double
 }  // namespace
 
 Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2, const double* mR, const double* mT,
-                 const Model& mdl, int steps, const double* stateTraj)
-    : ctx(c), g(gd), model(mdl), nt(steps), solver(c, gd, v1, v2, steps), weights(gd, mdl.norm) {
-    (void)mR;
+                 const Model& mdl, int steps, const double* stateTraj, int hmode, const double* adjTraj)
+    : ctx(c), g(gd), model(mdl), nt(steps), solver(c, gd, v1, v2, steps), weights(gd, mdl.norm), mode_(hmode) {
     if (mdl.deformation == kNearIncompressible)
         throw NotSupported("HessianOperator: near-incompressible model is not implemented on the device");
     if (!(mdl.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
@@ -341,6 +340,28 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     // lazily-built per-velocity work the reference does on the first apply
     // (charBwd 2 + dvDepBwd 1 interps, divv 3 FFTs; + charFwd 2 if the state was reused)
     lazyInterps_ = 3 + (hadFwd ? 0 : 2);
+    if (mode_ == 1) {
+        adj_.alloc(sizeof(double) * (nt + 1) * N);
+        fn_.alloc(sizeof(double) * (2 * (nt + 1) + 7) * N);
+        fnFlag_.alloc(64);
+    }
+    if (mode_ == 1 && adjTraj) {  // adjoint trajectory reused (inverse.cpp:166-168), copied
+        VRG_CUDA(cudaMemcpyAsync(adj_.d(), adjTraj, sizeof(double) * (nt + 1) * N, cudaMemcpyDeviceToDevice,
+                                 ctx.stream));
+    } else if (mode_ == 1) {
+        // full Newton: adjoint seeded with lambda(1) = -(m(1) - mR), guarded (inverse.cpp:169-171);
+        // the reference builds the backward characteristics and (div v)_D here, not in the apply
+        if (!mR) throw InvalidArgument("HessianOperator: full Newton mode needs the reference image");
+        double* lam1 = fn_.d();
+        lincomb(ctx, N, 1.0, state_.d() + static_cast<std::size_t>(nt) * N, -1.0, mR, lam1);
+        lincomb(ctx, N, -1.0, lam1, 0.0, lam1, lam1);
+        solver.adjoint(lam1, adj_.d(), true);  // counted below
+        ctx.ffts = f0;
+        ctx.interps = i0;
+        ctx.interps += nt + 3;  // adjoint + charBwd + dvDep
+        ctx.ffts += 3;          // div v
+        lazyInterps_ = hadFwd ? 0 : 2;
+    }
     // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
     // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
     // 1024^2 on B200 (0.815 vs 0.867 ms).  VRG_FUSED_BANDS=0 selects the plain step.
@@ -349,7 +370,7 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     fused_ = useFusedBands && want && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
     if (const char* ge = std::getenv("VRG_GRAPHS")) useGraphs = ge[0] != '0';  // debugging switch
     setupWave();
-    lazyFfts_ = 3;
+    lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     adjLog_.ensure(nt + 1, evalBlocks(g));
     weights.regSymbol(model.betaV);
@@ -478,6 +499,15 @@ void Hessian::setupWave() {
 }
 
 void Hessian::countDataTerm() {
+    if (mode_ == 1) {
+        // incState 2 + 3nt interps, 3 + 3nt FFTs; FN incAdjoint 2nt interps, 3(nt+1) FFTs
+        // (div of products); body force 3(nt+1) + 3(nt+1) FFTs (grad m_j, grad m~_j)
+        ctx.interps += 5LL * nt + 2 + lazyInterps_;
+        ctx.ffts += (3 + 3LL * nt) + 9LL * (nt + 1) + lazyFfts_ + (model.deformation == kIncompressible ? 4 : 0);
+        lazyInterps_ = 0;
+        lazyFfts_ = 0;
+        return;
+    }
     ctx.interps += 4LL * nt + 2 + lazyInterps_;
     ctx.ffts += (3 + 3LL * nt) + 3LL * (nt + 1) + lazyFfts_ + (model.deformation == kIncompressible ? 4 : 0);
     lazyInterps_ = 0;
@@ -486,6 +516,10 @@ void Hessian::countDataTerm() {
 
 void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                        const double* reg2, double* out1, double* out2) {
+    if (mode_ == 1) {
+        dataTermFN(vt1, vt2, b1, b2, reg1, reg2, out1, out2);
+        return;
+    }
     const std::size_t N = g.points();
     const double ht = solver.ht;
     double* vtD = work_.d();
@@ -640,6 +674,91 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     adjLog_.finalize(ctx);
 }
 
+// Full-Newton data term (HessianOperator::Impl::dataTerm FN branch, inverse.cpp:187-211, SL):
+// incremental state trajectory, full-Newton incremental adjoint, and the body force
+// b = sum_j w_j (lt_j grad m_j + lambda_j grad m~_j), trapezoid weights, in the reference's
+// order (j = 0..nt).
+namespace {
+__global__ void k_bf_fn(std::size_t N, double w, const double* __restrict__ lt, const double* __restrict__ g1,
+                        const double* __restrict__ g2, const double* __restrict__ lam, const double* __restrict__ t1,
+                        const double* __restrict__ t2, double* __restrict__ b1, double* __restrict__ b2) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const double term1 = lt[p] * g1[p] + 1.0 * (lam[p] * t1[p]);
+    const double term2 = lt[p] * g2[p] + 1.0 * (lam[p] * t2[p]);
+    b1[p] = b1[p] + w * term1;
+    b2[p] = b2[p] + w * term2;
+}
+__global__ void k_add2(std::size_t N, const double* __restrict__ a1, const double* __restrict__ a2,
+                       const double* __restrict__ c1, const double* __restrict__ c2, double* __restrict__ o1,
+                       double* __restrict__ o2) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    o1[p] = a1[p] + 1.0 * c1[p];
+    o2[p] = a2[p] + 1.0 * c2[p];
+}
+}  // namespace
+
+void Hessian::dataTermFN(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
+                         const double* reg2, double* out1, double* out2) {
+    const std::size_t N = g.points();
+    const long long f0 = ctx.ffts, i0 = ctx.interps;  // logical counts come from countDataTerm
+    const double ht = solver.ht;
+    double* vtD = work_.d();
+    double* c2 = vtD + 11 * N;
+    double* mt = fn_.d();
+    double* lt = mt + static_cast<std::size_t>(nt + 1) * N;
+    double* work = lt + static_cast<std::size_t>(nt + 1) * N;  // 5N
+    double* gmt = work + 5 * N;                                 // 2N
+    unsigned* flag = fnFlag_.as<unsigned>();
+    VRG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), ctx.stream));
+    const double* Xf = solver.departure(kForward);
+    double* coef = solver.coef();
+    double* tmp = solver.tmp();
+    auto G = [&](int j) { return G_.d() + static_cast<std::size_t>(j) * 2 * N; };
+    auto GD = [&](int j) { return GD_.d() + static_cast<std::size_t>(j - 1) * 2 * N; };
+    // incremental state trajectory (solveIncState SL)
+    launchPrefilter(ctx, g, vt1, coef, tmp, flag);
+    launchPrefilter(ctx, g, vt2, c2, tmp, flag);
+    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
+    fill(ctx, N, 0.0, mt);
+    for (int j = 1; j <= nt; ++j) {
+        EpiIncState epi{nullptr, vtD, vtD + N, GD(j), GD(j) + N, vt1, vt2, G(j), G(j) + N, 0.5 * ht,
+                        mt + static_cast<std::size_t>(j) * N};
+        if (j == 1) {
+            launchPointwise(ctx, g, epi);
+        } else {
+            launchPrefilter(ctx, g, mt + static_cast<std::size_t>(j - 1) * N, coef, tmp, flag);
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, true);
+        }
+    }
+    // lt(1) = -m~(1), full-Newton incremental adjoint
+    double* lt1 = lt + static_cast<std::size_t>(nt) * N;
+    lincomb(ctx, N, -1.0, mt + static_cast<std::size_t>(nt) * N, 0.0, mt + static_cast<std::size_t>(nt) * N, lt1);
+    solver.incAdjointFullNewton(vt1, vt2, lt1, adj_.d(), lt, work, flag);
+    // body force, trapezoid over the nodes
+    fill(ctx, 2 * N, 0.0, b1);
+    if (b2 != b1 + N) fill(ctx, N, 0.0, b2);
+    for (int j = 0; j <= nt; ++j) {
+        const double w = ht * ((j == 0 || j == nt) ? 0.5 : 1.0);
+        gradient(ctx, g, mt + static_cast<std::size_t>(j) * N, gmt, gmt + N);
+        {
+            LaunchScope ls_(ctx, "k_bf_fn");
+            k_bf_fn<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, w, lt + static_cast<std::size_t>(j) * N, G(j),
+                                                             G(j) + N, adj_.d() + static_cast<std::size_t>(j) * N,
+                                                             gmt, gmt + N, b1, b2);
+        }
+        VRG_LAUNCH_CHECK();
+    }
+    if (out1) {
+        LaunchScope ls_(ctx, "k_add2");
+        k_add2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, reg1, reg2, b1, b2, out1, out2);
+        VRG_LAUNCH_CHECK();
+    }
+    ctx.ffts = f0;
+    ctx.interps = i0;
+}
+
 // ------------------------------------------------------------------------------ slabs
 // One SL step of a slab-decomposed grid (slab.py): the band kernel over the slab's L rows with
 // the coefficients in a window (BandWindow), epilogue by kind (see include/vrg.h).
@@ -689,7 +808,16 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
     }
 }
 
-void Hessian::checkLastGuard() { adjLog_.check(ctx, "adjoint", nt, false, true, nt); }
+void Hessian::checkLastGuard() {
+    if (mode_ == 1) {  // full Newton: no guard in the incremental solves, prefilter input checks only
+        unsigned h = 0;
+        VRG_CUDA(cudaMemcpyAsync(&h, fnFlag_.d(), sizeof h, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        if (h) throw InvalidArgument("prefilter: non-finite value");
+        return;
+    }
+    adjLog_.check(ctx, "adjoint", nt, false, true, nt);
+}
 
 // Average device time of one launch of a matvec kernel class, `iters` back-to-back launches
 // between two events on the context stream, with the operands of a mid-trajectory step

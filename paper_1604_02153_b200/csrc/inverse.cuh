@@ -27,8 +27,10 @@ struct Model {
 class Hessian {
 public:
     // `stateTraj` (nullable): reuse a state trajectory (HessianOperator ctor, inverse.cpp:162-172).
+    // hmode: 0 Gauss-Newton, 1 full Newton (HessianMode, transport.hpp; the full-Newton
+    // operator solves the adjoint in the ctor, inverse.cpp:164-172)
     Hessian(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR, const double* mT,
-            const Model& model, int nt, const double* stateTraj);
+            const Model& model, int nt, const double* stateTraj, int hmode = 0, const double* adjTraj = nullptr);
 
     Ctx& ctx;
     GridDims g;
@@ -89,6 +91,12 @@ private:
     GuardLog adjLog_;
     long long lazyInterps_ = 0, lazyFfts_ = 0;
     bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh
+    int mode_ = 0;        // 1: full Newton
+    DBuf adj_;            // full Newton: adjoint trajectory lambda_j, (nt+1) N
+    DBuf fn_;             // full Newton: m~ and lt trajectories (2 (nt+1) N), work (7N)
+    DBuf fnFlag_;         // full Newton: non-finite prefilter input
+    void dataTermFN(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
+                    const double* reg2, double* out1, double* out2);
     // persistent wavefront kernel for the whole data term (wave.cuh, k_wave)
     bool wave_ = false;
     int waveDRows_ = 0;      // rows a gather may reach from its own row (displacement + stencil)

@@ -510,7 +510,8 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
 
         const double eta = std::min(cfg.forcingCap, std::sqrt(grel));
         std::unique_ptr<PhaseTimer> ptH(new PhaseTimer(ctx, "Hessian ctor"));
-        Hessian hess(ctx, g, v, v + N, mR, mT, model, nt, state.d());
+        Hessian hess(ctx, g, v, v + N, mR, mT, model, nt, state.d(), cfg.hessianMode,
+                     cfg.hessianMode == 1 ? adjoint.d() : nullptr);
         ptH.reset();
         // rhs = -g
         lincomb(ctx, 2 * N, -1.0, gBuf.d(), 0.0, gBuf.d(), tmpBuf.d());

@@ -101,6 +101,7 @@ struct NewtonConfig {
     int lsMaxSteps = 20;
     double gradCfl = 1.0;
     int ntOverride = 0;  // 0 = CFL-derived
+    int hessianMode = 0;  // 0 Gauss-Newton, 1 full Newton (NewtonConfig::hessianMode)
 };
 
 struct IterationRecord {

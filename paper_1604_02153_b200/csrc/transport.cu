@@ -374,6 +374,50 @@ void Solver::incState(const double* vt1, const double* vt2, const double* stateT
     ctx.sync();
 }
 
+namespace {
+// m * v_i per component (hadamard(m, v[i]), divOfProduct of transport.cpp:31-36)
+__global__ void k_mul2(std::size_t N, const double* __restrict__ m, const double* __restrict__ v1,
+                       const double* __restrict__ v2, double* __restrict__ o1, double* __restrict__ o2) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    o1[p] = m[p] * v1[p];
+    o2[p] = m[p] * v2[p];
+}
+}  // namespace
+
+void Solver::incAdjointFullNewton(const double* vt1, const double* vt2, const double* lt1, const double* adj,
+                                  double* traj, double* work, unsigned* flag) {
+    const std::size_t N = g.points();
+    const double* X = departure(kBackward);
+    const double* dv = divVelocity();
+    const double* dvd = divVelocityAtDeparture(kBackward);
+    double* qCur = work;
+    double* qPrev = work + N;
+    double* qD = work + 2 * N;
+    double* prod = work + 3 * N;  // 2N
+    auto divProd = [&](const double* m, double* q) {
+        {
+            LaunchScope ls_(ctx, "k_mul2");
+            k_mul2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, m, vt1, vt2, prod, prod + N);
+        }
+        VRG_LAUNCH_CHECK();
+        divergence(ctx, g, prod, prod + N, q);
+    };
+    if (traj + static_cast<std::size_t>(nt) * N != lt1) copy(ctx, N, lt1, traj + static_cast<std::size_t>(nt) * N);
+    divProd(adj + static_cast<std::size_t>(nt) * N, qCur);
+    for (int j = nt; j >= 1; --j) {
+        launchPrefilter(ctx, g, qCur, coef_.d(), tmp_.d(), flag);
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, EpiStore1{nullptr, qD}, true);
+        divProd(adj + static_cast<std::size_t>(j - 1) * N, qPrev);
+        launchPrefilter(ctx, g, traj + static_cast<std::size_t>(j) * N, coef_.d(), tmp_.d(), flag);
+        launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N,
+                          EpiContinuityFN{nullptr, dvd, dv, qD, qPrev, ht, traj + static_cast<std::size_t>(j - 1) * N},
+                          true);
+        ctx.interps += 2;
+        std::swap(qCur, qPrev);
+    }
+}
+
 void Solver::jacobian(double* out) {
     const std::size_t N = g.points();
     double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);

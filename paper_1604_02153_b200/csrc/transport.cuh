@@ -72,6 +72,12 @@ public:
     void adjointFinal(const double* lam1, double* out);
     // solveIncState SL (src/transport.cpp:322-342): out trajectory (nt+1) fields.
     void incState(const double* vt1, const double* vt2, const double* stateTraj, double* out);
+    // solveIncAdjoint, full-Newton SL (src/transport.cpp:403-420): traj (nt+1 frames, traj[nt] =
+    // lt1) from the adjoint trajectory `adj`; work holds 5N; a non-finite prefilter input sets
+    // *flag.  No guard (as in the reference).
+    void incAdjointFullNewton(const double* vt1, const double* vt2, const double* lt1, const double* adj,
+                              double* traj, double* work, unsigned* flag);
+
     // jacobianDeterminant SL (src/transport.cpp:456-464).
     void jacobian(double* out);
 

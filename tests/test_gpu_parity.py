@@ -318,3 +318,46 @@ def test_band_and_wave_paths_vs_plain(ctx, api, monkeypatch, n1, n2, nt):
             for i, (x, y) in enumerate(zip(res["plain"][k], res[mode][k])):
                 err = np.abs(x - y).max() / np.abs(x).max()
                 assert err <= 1e-13, (mode, k, i, err)
+
+
+@pytest.mark.parametrize("n,nt,deform", [(48, 4, 0), (64, 4, 1), (128, 8, 0)])
+def test_full_newton_hessian_vs_reference(ctx, api, ref, n, nt, deform):
+    """HessianMode::FullNewton (inverse.cpp:164-211): the adjoint in the ctor, the full-Newton SL
+    incremental adjoint and the two-term body force, against the compiled reference: matvec,
+    data term and the per-call counters (ctor, first and steady-state apply)."""
+    mT, (v1, v2) = synth.config12_fields(n)
+    mR = ref.solve_state_final(v1, v2, nt, mT)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    w1, w2 = 0.6 * v1, 0.6 * v2
+    ref.counters_reset()
+    R = ref.Hessian(w1, w2, mR, mT, 2, 1e-2, deform, nt, mode=1)
+    rc_ctor = ref.counters()
+    ctx.reset_counters()
+    H = api.HessianOperator(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT), api.H2SEMI, 1e-2,
+                            deform, nt, mode=api.FULL_NEWTON)
+    assert ctx.counters() == rc_ctor
+    vt = (ctx.field(vt1), ctx.field(vt2))
+    for _ in range(2):
+        ref.counters_reset()
+        e1, e2 = R.apply(vt1, vt2)
+        rc = ref.counters()
+        ctx.reset_counters()
+        h1, h2 = H.apply(vt)
+        assert ctx.counters() == rc
+        assert rel(h1, e1) < TOL and rel(h2, e2) < TOL
+    d1, d2 = R.apply(vt1, vt2, data_only=True)
+    g1, g2 = H.apply_data_term(vt)
+    assert rel(g1, d1) < TOL and rel(g2, d2) < TOL
+
+
+def test_full_newton_incadjoint_vs_reference(ctx, api, ref):
+    n, nt = 64, 4
+    mT, (v1, v2) = synth.config12_fields(n)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    lt1 = synth.smoothed_noise(n, n, 1000)
+    adj = ref.solve_adjoint(v1, v2, nt, mT)
+    e = ref.solve_incadjoint_fn(v1, v2, nt, vt1, vt2, lt1, adj)
+    S = api.Solver(ctx, (ctx.field(v1), ctx.field(v2)), nt)
+    got = S.solve_inc_adjoint((ctx.field(vt1), ctx.field(vt2)), ctx.field(lt1), adjoint=ctx.field(adj),
+                              mode=api.FULL_NEWTON)
+    assert rel(got, e) < TOL
