@@ -55,6 +55,9 @@ int vrg_ctx_create(int device, void* cuda_stream /* nullable: own stream */, vrg
 /* the CUDA stream the context launches on (its own non-blocking stream when created with a
  * NULL stream), for callers that order their own work with the library's */
 void* vrg_ctx_stream(vrg_ctx_t ctx);
+/* Model::betaW (inverse.hpp:21), the H1 penalty weight on div v of the near-incompressible
+ * model (deformation 2), used by the calls on this context; default 0.1 as in the reference */
+int vrg_set_penalty_weight(vrg_ctx_t ctx, double beta_w);
 void vrg_ctx_destroy(vrg_ctx_t ctx);
 const char* vrg_last_error(vrg_ctx_t ctx); /* ctx may be NULL: last error of this thread */
 int vrg_sync(vrg_ctx_t ctx);

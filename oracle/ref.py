@@ -61,6 +61,10 @@ def _check(code: int):
         raise RefError(code, lib().ref_last_error().decode())
 
 
+def set_penalty_weight(beta_w):
+    lib().ref_set_penalty_weight(C.c_double(beta_w))
+
+
 def counters_reset():
     lib().ref_counters_reset()
 

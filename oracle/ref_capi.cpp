@@ -89,11 +89,14 @@ problems::RegistrationProblem problemOf(int n1, int n2, const double* mR, const 
     return p;
 }
 
+double g_betaW = 1e-1;  // Model::betaW default (inverse.hpp:21)
+
 inverse::Model modelOf(int norm, double beta, int deform) {
     inverse::Model m;
     m.norm = normOf(norm);
     m.betaV = beta;
     m.deformation = defOf(deform);
+    m.betaW = g_betaW;
     return m;
 }
 
@@ -104,6 +107,7 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 void ref_counters_reset() { counters::reset(); }
+void ref_set_penalty_weight(double betaW) { g_betaW = betaW; }
 void ref_counters(long long* ffts, long long* interps) {
     const auto s = counters::snapshot();
     *ffts = s.ffts;

@@ -77,6 +77,10 @@ class Context:
             if torch.cuda.current_stream(self.device) != stream:
                 torch.cuda.set_stream(stream)
 
+    def set_penalty_weight(self, beta_w: float):
+        """Model::betaW of the near-incompressible model for calls on this context."""
+        self.check(self.lib.vrg_set_penalty_weight(self.h, float(beta_w)))
+
     def check(self, code: int):
         if code:
             raise _ERRORS.get(code, VrgError)(self.lib.vrg_last_error(self.h).decode())

@@ -11,6 +11,7 @@
 
 struct vrg_ctx_s {
     vrg::Ctx ctx;
+    double betaW = 1e-1;  // Model::betaW of the near-incompressible model (inverse.hpp:21)
     vrg_ctx_s(int dev, cudaStream_t s) : ctx(dev, s) {}
 };
 struct vrg_solver_s {
@@ -26,6 +27,7 @@ struct vrg_hess_s {
 namespace {
 
 thread_local std::string g_threadErr;
+thread_local double g_betaW = 1e-1;  // betaW of the context of the call in progress (modelOf)
 
 template <class F>
 int guarded(vrg_ctx_s* c, F&& f) {
@@ -35,6 +37,7 @@ int guarded(vrg_ctx_s* c, F&& f) {
         if (c) VRG_CUDA(cudaSetDevice(c->ctx.device));
         if (c) {
             vrg::AllocStreamScope as_(c->ctx.stream);
+            g_betaW = c->betaW;
             f();
         } else {
             f();
@@ -70,6 +73,7 @@ vrg::Model modelOf(int norm, double beta, int deformation) {
     m.norm = norm;
     m.betaV = beta;
     m.deformation = deformation;
+    m.betaW = g_betaW;
     return m;
 }
 
@@ -87,6 +91,13 @@ int vrg_ctx_create(int device, void* stream, vrg_ctx_t* out) {
 void vrg_ctx_destroy(vrg_ctx_t c) { delete c; }
 
 void* vrg_ctx_stream(vrg_ctx_t c) { return c ? static_cast<void*>(c->ctx.stream) : nullptr; }
+
+int vrg_set_penalty_weight(vrg_ctx_t c, double betaW) {
+    return guarded(c, [&] {
+        if (!(betaW >= 0.0)) throw vrg::InvalidArgument("near-incompressible penalty weight must be >= 0");
+        c->betaW = betaW;
+    });
+}
 
 const char* vrg_last_error(vrg_ctx_t c) { return c ? c->ctx.err.c_str() : g_threadErr.c_str(); }
 

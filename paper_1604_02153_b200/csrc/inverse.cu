@@ -305,8 +305,6 @@ __global__ void k_row_disp(const double* __restrict__ x1, int n1, int n2, double
 Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2, const double* mR, const double* mT,
                  const Model& mdl, int steps, const double* stateTraj, int hmode, const double* adjTraj)
     : ctx(c), g(gd), model(mdl), nt(steps), solver(c, gd, v1, v2, steps), weights(gd, mdl.norm), mode_(hmode) {
-    if (mdl.deformation == kNearIncompressible)
-        throw NotSupported("HessianOperator: near-incompressible model is not implemented on the device");
     if (!(mdl.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
     const std::size_t N = g.points();
     state_.alloc(sizeof(double) * (nt + 1) * N);
@@ -499,6 +497,7 @@ void Hessian::setupWave() {
 }
 
 void Hessian::countDataTerm() {
+    if (model.deformation == kNearIncompressible) ctx.ffts += 8;  // penalty gradient of vt
     if (mode_ == 1) {
         // incState 2 + 3nt interps, 3 + 3nt FFTs; FN incAdjoint 2nt interps, 3(nt+1) FFTs
         // (div of products); body force 3(nt+1) + 3(nt+1) FFTs (grad m_j, grad m~_j)
@@ -759,6 +758,18 @@ void Hessian::dataTermFN(const double* vt1, const double* vt2, double* b1, doubl
     ctx.interps = i0;
 }
 
+// b += -betaW grad((1 - Lap) div vt) (inverse.cpp:214-215), without touching the op counters
+// (the matvec's logical counts come from countDataTerm; graph replays run no host code)
+void Hessian::addPenalty(const double* vt1, const double* vt2, double* b1, double* b2) {
+    const std::size_t N = g.points();
+    const long long f0 = ctx.ffts;
+    double* pen = ctx.scratchBuf(42, sizeof(double) * 2 * N);
+    divergencePenaltyGradient(ctx, g, vt1, vt2, model.betaW, pen, pen + N);
+    axpby(ctx, N, 1.0, pen, 1.0, b1);
+    axpby(ctx, N, 1.0, pen + N, 1.0, b2);
+    ctx.ffts = f0;
+}
+
 // ------------------------------------------------------------------------------ slabs
 // One SL step of a slab-decomposed grid (slab.py): the band kernel over the slab's L rows with
 // the coefficients in a window (BandWindow), epilogue by kind (see include/vrg.h).
@@ -1015,7 +1026,16 @@ void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, doub
         }
         specScale(ctx, g, S, 2, regSym, 1.0 / N);
         fftInverse(ctx, g, S, reg, 2);
-        dataTerm(vt1, vt2, b, b + N, reg, reg + N, o1, o2);
+        if (model.deformation == kNearIncompressible) {
+            // out = beta A vt + (b + penalty gradient) (inverse.cpp:212-233)
+            dataTerm(vt1, vt2, b, b + N, nullptr, nullptr, nullptr, nullptr);
+            addPenalty(vt1, vt2, b, b + N);
+            LaunchScope ls_(ctx, "k_add2");
+            k_add2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, reg, reg + N, b, b + N, o1, o2);
+            VRG_LAUNCH_CHECK();
+        } else {
+            dataTerm(vt1, vt2, b, b + N, reg, reg + N, o1, o2);
+        }
     }
 }
 
@@ -1035,6 +1055,7 @@ void Hessian::applyDataTerm(const double* vt1, const double* vt2, double* o1, do
                 fftInverse(ctx, g, T + g.specPoints(), o2, 1);
             }
         } else {
+            if (model.deformation == kNearIncompressible) addPenalty(vt1, vt2, b, b + N);
             copy(ctx, N, b, o1);
             copy(ctx, N, b + N, o2);
         }
@@ -1067,6 +1088,7 @@ void Hessian::launchSplit(const double* s1, const double* s2, double* o1, double
     specCombine(ctx, g, S, S + NS, nullptr, nullptr, inv, false, 1.0 / N, T, T + NS);
     fftInverse(ctx, g, T, t, 2);
     dataTerm(t, t + N, b, b + N, nullptr, nullptr, nullptr, nullptr);
+    if (model.deformation == kNearIncompressible) addPenalty(t, t + N, b, b + N);
     fftForward(ctx, g, b, T, 2);
     specCombine(ctx, g, T, T + NS, S, S + NS, inv, model.deformation == kIncompressible, 1.0 / N, T, T + NS);
     if (o2 == o1 + N) {
@@ -1113,7 +1135,6 @@ void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, con
 // incompressible models.  stateOut / adjOut (nullable) receive the trajectories.
 void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                        const double* mT, const Model& model, int nt, double* scalars, double* stateOut) {
-    if (model.deformation == kNearIncompressible) throw NotSupported("near-incompressible model not implemented");
     const std::size_t N = g.points();
     Solver solver(ctx, g, v1, v2, nt);
     DBuf stateBuf;
@@ -1131,7 +1152,9 @@ void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const doub
     if (!(model.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
     applyRealSymbol(ctx, g, v1, v2, reg, reg + N, w.regSymbol(model.betaV));
     const double regTerm = 0.5 * dot(ctx, g, reg, reg + N, v1, v2);
-    scalars[0] = mismatch + regTerm;
+    const double penalty =
+        model.deformation == kNearIncompressible ? divergencePenaltyValue(ctx, g, v1, v2, model.betaW) : 0.0;
+    scalars[0] = mismatch + regTerm + penalty;
     scalars[1] = mismatch;
     scalars[2] = regTerm;
 }
@@ -1139,7 +1162,6 @@ void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const doub
 void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
                       double* stateOut, double* adjOut, const double* reuseState) {
-    if (model.deformation == kNearIncompressible) throw NotSupported("near-incompressible model not implemented");
     const std::size_t N = g.points();
     Solver solver(ctx, g, v1, v2, nt);
     DBuf stBuf, adBuf;
@@ -1169,10 +1191,18 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
     if (!(model.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
     applyRealSymbol(ctx, g, v1, v2, g1, g2, w.regSymbol(model.betaV));
     const double regTerm = 0.5 * dot(ctx, g, g1, g2, v1, v2);
+    double penalty = 0.0;
+    if (model.deformation == kNearIncompressible) {
+        penalty = divergencePenaltyValue(ctx, g, v1, v2, model.betaW);
+        double* pen = ctx.scratchBuf(42, sizeof(double) * 2 * N);
+        divergencePenaltyGradient(ctx, g, v1, v2, model.betaW, pen, pen + N);
+        axpby(ctx, N, 1.0, pen, 1.0, g1);
+        axpby(ctx, N, 1.0, pen + N, 1.0, g2);
+    }
     if (model.deformation == kIncompressible) projectDivFree(ctx, g, b, b + N, b, b + N);
     axpby(ctx, N, 1.0, b, 1.0, g1);
     axpby(ctx, N, 1.0, b + N, 1.0, g2);
-    scalars[0] = mismatch + regTerm;
+    scalars[0] = mismatch + regTerm + penalty;
     scalars[1] = mismatch;
     scalars[2] = regTerm;
 }

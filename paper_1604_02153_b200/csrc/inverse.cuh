@@ -97,6 +97,7 @@ private:
     DBuf fnFlag_;         // full Newton: non-finite prefilter input
     void dataTermFN(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                     const double* reg2, double* out1, double* out2);
+    void addPenalty(const double* vt1, const double* vt2, double* b1, double* b2);
     // persistent wavefront kernel for the whole data term (wave.cuh, k_wave)
     bool wave_ = false;
     int waveDRows_ = 0;      // rows a gather may reach from its own row (displacement + stencil)

@@ -1,6 +1,7 @@
 // K7 implementation: cuFFT plans from the context cache + symbol kernels.
 #include <cmath>
 
+#include "blas.cuh"
 #include "spectral.cuh"
 
 namespace vrg {
@@ -39,6 +40,17 @@ __global__ void k_div(const cplx* __restrict__ s1, const cplx* __restrict__ s2, 
     const cplx a = cmulI(waveNyq0(r, n1), s1[i]);
     const cplx b = cmulI(waveNyq0(c, n2), s2[i]);
     o[i] = cscale(make_double2(a.x + b.x, a.y + b.y), scale);
+}
+
+// applyHelmholtz symbol 1 + k1^2 + k2^2 with Nyquist-zeroed waves (spectral.cpp:214-223)
+__global__ void k_helm(cplx* s, int n1, int n2, double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const double k1 = waveNyq0(r, n1), k2 = waveNyq0(c, n2);
+    s[i] = cscale(s[i], (1.0 + k1 * k1 + k2 * k2) * scale);
 }
 
 __global__ void k_scale(cplx* s, std::size_t n, int nf, const double* __restrict__ sym, double scale) {
@@ -254,6 +266,37 @@ void applyRealSymbol(Ctx& ctx, const GridDims& g, const double* v1, const double
     specScale(ctx, g, s, 2, sym, 1.0 / g.points());
     fftInverse2(ctx, g, s, o1, o2);
     ctx.ffts += 4;
+}
+
+void applyHelmholtz(Ctx& ctx, const GridDims& g, const double* u, double* out) {
+    cplx* s = specScratch(ctx, g, 0, 1);
+    fftForward(ctx, g, u, s, 1);
+    {
+        LaunchScope ls_(ctx, "k_helm");
+        k_helm<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.n1, g.n2, 1.0 / g.points());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, g, s, out, 1);
+    ctx.ffts += 2;
+}
+
+void divergencePenaltyGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double betaW,
+                               double* o1, double* o2) {
+    double* w = ctx.scratchBuf(40, sizeof(double) * g.points());
+    divergence(ctx, g, v1, v2, w);
+    applyHelmholtz(ctx, g, w, w);
+    gradient(ctx, g, w, o1, o2);
+    lincomb(ctx, g.points(), -betaW, o1, 0.0, o1, o1);
+    lincomb(ctx, g.points(), -betaW, o2, 0.0, o2, o2);
+}
+
+double divergencePenaltyValue(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double betaW) {
+    const std::size_t N = g.points();
+    double* w = ctx.scratchBuf(40, sizeof(double) * N);
+    double* gw = ctx.scratchBuf(41, sizeof(double) * 2 * N);
+    divergence(ctx, g, v1, v2, w);
+    gradient(ctx, g, w, gw, gw + N);
+    return 0.5 * betaW * (dot(ctx, g, w, nullptr, w, nullptr) + dot(ctx, g, gw, gw + N, gw, gw + N));
 }
 
 void projectDivFree(Ctx& ctx, const GridDims& g, const double* b1, const double* b2, double* o1, double* o2) {

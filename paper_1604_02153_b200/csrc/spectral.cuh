@@ -40,6 +40,13 @@ void fftInverse(Ctx& ctx, const GridDims& g, cplx* s, double* u, int batch);    
 
 // Field-level operators (device pointers, stream-ordered on ctx.stream).
 void gradient(Ctx& ctx, const GridDims& g, const double* u, double* g1, double* g2);
+// applyHelmholtz (spectral.cpp:214-223): (1 - Lap) u with Nyquist-zeroed waves; 2 FFTs
+void applyHelmholtz(Ctx& ctx, const GridDims& g, const double* u, double* out);
+// near-incompressible penalty (inverse.cpp:17-28): -betaW grad((1 - Lap) div v) (8 FFTs) and
+// 1/2 betaW (<w, w> + <grad w, grad w>), w = div v (6 FFTs)
+void divergencePenaltyGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double betaW,
+                               double* o1, double* o2);
+double divergencePenaltyValue(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double betaW);
 void divergence(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double* out);
 // out_i = IFFT(sym * FFT(v_i)); v and out are 2 contiguous fields when `pair`.
 void applyRealSymbol(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double* o1, double* o2,

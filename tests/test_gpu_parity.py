@@ -361,3 +361,50 @@ def test_full_newton_incadjoint_vs_reference(ctx, api, ref):
     got = S.solve_inc_adjoint((ctx.field(vt1), ctx.field(vt2)), ctx.field(lt1), adjoint=ctx.field(adj),
                               mode=api.FULL_NEWTON)
     assert rel(got, e) < TOL
+
+
+@pytest.mark.parametrize("beta_w", [1e-1, 3e-2])
+def test_near_incompressible_vs_reference(ctx, api, ref, beta_w):
+    """Deformation::NearIncompressible (inverse.cpp:17-28, 110-112, 141-146, 214-215): the
+    divergence penalty in the matvec, the gradient and the objective, with Model::betaW set on
+    both sides; counters included.  The penalty -betaW grad((1 - Lap) div v) carries FFT
+    rounding amplified by betaW |k|^4, the same conditioning floor as beta A (apply_floor)."""
+    n, nt = 64, 4
+    mT, (v1, v2) = synth.config12_fields(n)
+    mR = ref.solve_state_final(v1, v2, nt, mT)
+    vt1, vt2 = synth.smooth_velocity(n, n, 3000)
+    w1, w2 = 0.6 * v1, 0.6 * v2
+    ref.set_penalty_weight(beta_w)
+    ctx.set_penalty_weight(beta_w)
+    try:
+        R = ref.Hessian(w1, w2, mR, mT, 2, 1e-2, 2, nt)
+        H = api.HessianOperator(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT), api.H2SEMI, 1e-2,
+                                api.NEAR_INCOMPRESSIBLE, nt)
+        vt = (ctx.field(vt1), ctx.field(vt2))
+        vmax = max(np.abs(vt1).max(), np.abs(vt2).max())
+        for _ in range(2):
+            ref.counters_reset()
+            e1, e2 = R.apply(vt1, vt2)
+            rc = ref.counters()
+            ctx.reset_counters()
+            h1, h2 = H.apply(vt)
+            assert ctx.counters() == rc
+            tol = max(TOL, apply_floor(n, 2, 1e-2 + beta_w, vmax, np.abs(e1).max()))
+            assert rel(h1, e1) < tol and rel(h2, e2) < tol
+        d1, d2 = R.apply(vt1, vt2, data_only=True)
+        g1, g2 = H.apply_data_term(vt)
+        tol = max(TOL, apply_floor(n, 2, beta_w, vmax, np.abs(d1).max()))
+        assert rel(g1, d1) < tol and rel(g2, d2) < tol
+        (q1, q2), sc = api.evaluate_gradient(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT),
+                                             api.H2SEMI, 1e-2, api.NEAR_INCOMPRESSIBLE, nt)
+        r1, r2, rsc = ref.evaluate_gradient(w1, w2, mR, mT, 2, 1e-2, 2, nt)
+        tol = max(TOL, apply_floor(n, 2, 1e-2 + beta_w, max(np.abs(w1).max(), np.abs(w2).max()), np.abs(r1).max()))
+        assert rel(q1, r1) < tol and rel(q2, r2) < tol
+        assert abs(sc[0] - rsc[0]) <= 1e-12 * abs(rsc[0])
+        osc = api.evaluate_objective(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT), api.H2SEMI,
+                                     1e-2, api.NEAR_INCOMPRESSIBLE, nt)
+        rosc = ref.evaluate_objective(w1, w2, mR, mT, 2, 1e-2, 2, nt)
+        assert abs(osc[0] - rosc[0]) <= 1e-12 * abs(rosc[0])
+    finally:
+        ref.set_penalty_weight(1e-1)
+        ctx.set_penalty_weight(1e-1)
