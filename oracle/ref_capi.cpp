@@ -11,6 +11,7 @@
 #include <string>
 
 #include "veloreg/counters.hpp"
+#include "veloreg/io.hpp"
 #include "veloreg/field.hpp"
 #include "veloreg/interp.hpp"
 #include "veloreg/inverse.hpp"
@@ -449,3 +450,41 @@ int ref_newton_solve(int n1, int n2, const double* mR, const double* mT, int nor
 }
 
 }  // extern "C"
+
+
+// ---- io (io.cpp) ----------------------------------------------------------------------------
+extern "C" {
+int ref_write_field(const char* path, int n1, int n2, int comps, const double* data) {
+    return guarded([&] {
+        const std::size_t N = static_cast<std::size_t>(n1) * n2;
+        if (comps == 1) {
+            io::writeField(path, sf(n1, n2, data));
+        } else {
+            io::writeField(path, vf(n1, n2, data, data + N));
+        }
+    });
+}
+
+int ref_read_field(const char* path, int* n1, int* n2, int* comps, double* data, long long cap) {
+    return guarded([&] {
+        const int nc = io::fieldComponents(path);
+        *comps = nc;
+        if (nc == 1) {
+            ScalarField u = io::readScalarField(path);
+            *n1 = u.grid.n[0];
+            *n2 = u.grid.n[1];
+            if (data && static_cast<long long>(u.v.size()) <= cap) put(u, data);
+        } else {
+            VectorField u = io::readVectorField(path);
+            *n1 = u.grid().n[0];
+            *n2 = u.grid().n[1];
+            const std::size_t N = u[0].v.size();
+            if (data && static_cast<long long>(2 * N) <= cap) {
+                put(u[0], data);
+                put(u[1], data + N);
+            }
+        }
+    });
+}
+
+}
