@@ -41,6 +41,11 @@ extern "C" {
 #define VRG_BACKWARD 1
 #define VRG_GAUSS_NEWTON 0 /* transport::HessianMode (transport.hpp:16) */
 #define VRG_FULL_NEWTON 1
+
+/* transport schemes (transport::Scheme, transport.hpp) */
+#define VRG_SCHEME_SL 0
+#define VRG_SCHEME_RK2 1
+#define VRG_SCHEME_RK2A 2
 #define VRG_BAND_LOW 0 /* spectral::Band (spectral.hpp:44) */
 #define VRG_BAND_HIGH 1
 
@@ -58,6 +63,11 @@ void* vrg_ctx_stream(vrg_ctx_t ctx);
 /* Model::betaW (inverse.hpp:21), the H1 penalty weight on div v of the near-incompressible
  * model (deformation 2), used by the calls on this context; default 0.1 as in the reference */
 int vrg_set_penalty_weight(vrg_ctx_t ctx, double beta_w);
+/* SchemeConfig::scheme (VRG_SCHEME_SL default, VRG_SCHEME_RK2, VRG_SCHEME_RK2A: Heun steps with
+ * spectral advection, transport.cpp:129-195) of the solvers, operators, gradients and Newton
+ * solves created on this context; the two-level preconditioner's coarse problem stays SL(5)
+ * as in the reference (precond.cpp kCoarseScheme) */
+int vrg_set_scheme(vrg_ctx_t ctx, int scheme);
 void vrg_ctx_destroy(vrg_ctx_t ctx);
 const char* vrg_last_error(vrg_ctx_t ctx); /* ctx may be NULL: last error of this thread */
 int vrg_sync(vrg_ctx_t ctx);

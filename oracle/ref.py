@@ -61,6 +61,11 @@ def _check(code: int):
         raise RefError(code, lib().ref_last_error().decode())
 
 
+def set_scheme(scheme):
+    """0 SL, 1 RK2, 2 RK2A for the solvers/operators/gradients/Newton built afterwards."""
+    lib().ref_set_scheme(int(scheme))
+
+
 def set_penalty_weight(beta_w):
     lib().ref_set_penalty_weight(C.c_double(beta_w))
 
@@ -128,13 +133,14 @@ def solve_incadjoint_gn(v1, v2, nt, lt1):
     return _traj_call(lib().ref_solve_incadjoint_gn, v1, v2, nt, lt1)
 
 
-def solve_incadjoint_fn(v1, v2, nt, vt1, vt2, lt1, adj):
-    """full-Newton SL incremental adjoint from the adjoint trajectory adj ((nt+1, n1, n2))."""
+def solve_incadjoint_fn(v1, v2, nt, vt1, vt2, lt1, adj_seed):
+    """full-Newton incremental adjoint, the adjoint solved from adj_seed (lambda(1)) inside."""
     v1, v2 = _c(v1), _c(v2)
     n1, n2 = v1.shape
     out = np.empty((nt + 1, n1, n2))
-    vt1, vt2, lt1, adj = map(_c, (vt1, vt2, lt1, adj))
-    _check(lib().ref_solve_incadjoint_fn(n1, n2, _p(v1), _p(v2), nt, _p(vt1), _p(vt2), _p(lt1), _p(adj), _p(out)))
+    vt1, vt2, lt1, seed = map(_c, (vt1, vt2, lt1, adj_seed))
+    _check(lib().ref_solve_incadjoint_fn(n1, n2, _p(v1), _p(v2), nt, _p(vt1), _p(vt2), _p(lt1), _p(seed),
+                                         _p(out)))
     return out
 
 

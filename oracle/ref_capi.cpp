@@ -76,8 +76,12 @@ inverse::Deformation defOf(int k) {
                   : k == 2 ? inverse::Deformation::NearIncompressible : inverse::Deformation::Compressible;
 }
 
+int g_scheme = 0;  // 0 SL, 1 RK2, 2 RK2A for the operators built through this wrapper
+
 transport::SchemeConfig slCfg(int nt, double cfl) {
-    transport::SchemeConfig c{transport::Scheme::SL, cfl, std::nullopt};
+    transport::SchemeConfig c{g_scheme == 1 ? transport::Scheme::RK2 : g_scheme == 2 ? transport::Scheme::RK2A
+                                                                                    : transport::Scheme::SL,
+                              cfl, std::nullopt};
     if (nt > 0) c.ntOverride = nt;
     return c;
 }
@@ -109,6 +113,7 @@ const char* ref_last_error() { return g_err.c_str(); }
 
 void ref_counters_reset() { counters::reset(); }
 void ref_set_penalty_weight(double betaW) { g_betaW = betaW; }
+void ref_set_scheme(int scheme) { g_scheme = scheme; }
 void ref_counters(long long* ffts, long long* interps) {
     const auto s = counters::snapshot();
     *ffts = s.ffts;
@@ -197,15 +202,13 @@ int ref_solve_incadjoint_gn(int n1, int n2, const double* v1, const double* v2, 
     });
 }
 
-// full-Newton SL incremental adjoint (transport.cpp:403-420) from an adjoint trajectory
+// full-Newton incremental adjoint (transport.cpp:403-453) with the adjoint solved from adjSeed
+// here (so the RK2 schemes have its stage fields)
 int ref_solve_incadjoint_fn(int n1, int n2, const double* v1, const double* v2, int nt, const double* vt1,
-                            const double* vt2, const double* lt1, const double* adjTraj, double* traj) {
+                            const double* vt2, const double* lt1, const double* adjSeed, double* traj) {
     return guarded([&] {
         transport::Solver s(vf(n1, n2, v1, v2), transport::TimeGrid(nt), slCfg(nt, 1.0));
-        transport::TransportSolution adj;
-        adj.nodes.frames.resize(static_cast<std::size_t>(nt) + 1);
-        const std::size_t N = static_cast<std::size_t>(n1) * n2;
-        for (int j = 0; j <= nt; ++j) adj.nodes.frames[j] = sf(n1, n2, adjTraj + j * N);
+        transport::TransportSolution adj = s.solveAdjoint(sf(n1, n2, adjSeed));
         putTraj(s.solveIncAdjoint(vf(n1, n2, vt1, vt2), sf(n1, n2, lt1), &adj, transport::HessianMode::FullNewton),
                 traj);
     });

@@ -24,6 +24,7 @@ _SIG = {
     "vrg_ctx_destroy": ("p", None),
     "vrg_ctx_stream": ("p", C.c_void_p),
     "vrg_set_penalty_weight": ("pd", C.c_int),
+    "vrg_set_scheme": ("pi", C.c_int),
     "vrg_last_error": ("p", C.c_char_p),
     "vrg_sync": ("p", C.c_int),
     "vrg_malloc": ("pup", C.c_int),

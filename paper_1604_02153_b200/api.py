@@ -20,6 +20,7 @@ COMPRESSIBLE, INCOMPRESSIBLE, NEAR_INCOMPRESSIBLE = 0, 1, 2
 FORWARD, BACKWARD = 0, 1
 GAUSS_NEWTON, FULL_NEWTON = 0, 1
 BAND_LOW, BAND_HIGH = 0, 1
+SL, RK2, RK2A = 0, 1, 2
 
 
 class VrgError(RuntimeError):
@@ -76,6 +77,10 @@ class Context:
         with torch.cuda.device(self.device):
             if torch.cuda.current_stream(self.device) != stream:
                 torch.cuda.set_stream(stream)
+
+    def set_scheme(self, scheme: int):
+        """Transport scheme (SL, RK2, RK2A) of solvers/operators/gradients created on this context."""
+        self.check(self.lib.vrg_set_scheme(self.h, int(scheme)))
 
     def set_penalty_weight(self, beta_w: float):
         """Model::betaW of the near-incompressible model for calls on this context."""

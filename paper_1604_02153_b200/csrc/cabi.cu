@@ -7,16 +7,20 @@
 #include <memory>
 
 #include "../../include/vrg.h"
+#include "heun.cuh"
 #include "precond.cuh"
 
 struct vrg_ctx_s {
     vrg::Ctx ctx;
     double betaW = 1e-1;  // Model::betaW of the near-incompressible model (inverse.hpp:21)
+    int scheme = 0;       // SchemeConfig::scheme for the calls on this context (SL, RK2, RK2A)
     vrg_ctx_s(int dev, cudaStream_t s) : ctx(dev, s) {}
 };
 struct vrg_solver_s {
     vrg_ctx_s* owner;
     vrg::Solver solver;
+    std::unique_ptr<vrg::HeunTransport> heun;  // RK2 / RK2A solver (scheme != SL)
+    vrg::DBuf stages;                           // nt predictor fields of the last trajectory
 };
 struct vrg_hess_s {
     vrg_ctx_s* owner;
@@ -28,6 +32,7 @@ namespace {
 
 thread_local std::string g_threadErr;
 thread_local double g_betaW = 1e-1;  // betaW of the context of the call in progress (modelOf)
+thread_local int g_scheme = 0;       // transport scheme of the context of the call in progress
 
 template <class F>
 int guarded(vrg_ctx_s* c, F&& f) {
@@ -38,6 +43,7 @@ int guarded(vrg_ctx_s* c, F&& f) {
         if (c) {
             vrg::AllocStreamScope as_(c->ctx.stream);
             g_betaW = c->betaW;
+            g_scheme = c->scheme;
             f();
         } else {
             f();
@@ -74,6 +80,7 @@ vrg::Model modelOf(int norm, double beta, int deformation) {
     m.betaV = beta;
     m.deformation = deformation;
     m.betaW = g_betaW;
+    m.scheme = g_scheme;
     return m;
 }
 
@@ -91,6 +98,13 @@ int vrg_ctx_create(int device, void* stream, vrg_ctx_t* out) {
 void vrg_ctx_destroy(vrg_ctx_t c) { delete c; }
 
 void* vrg_ctx_stream(vrg_ctx_t c) { return c ? static_cast<void*>(c->ctx.stream) : nullptr; }
+
+int vrg_set_scheme(vrg_ctx_t c, int scheme) {
+    return guarded(c, [&] {
+        if (scheme < VRG_SCHEME_SL || scheme > VRG_SCHEME_RK2A) throw vrg::InvalidArgument("unknown transport scheme");
+        c->scheme = scheme;
+    });
+}
 
 int vrg_set_penalty_weight(vrg_ctx_t c, double betaW) {
     return guarded(c, [&] {
@@ -252,7 +266,15 @@ int vrg_trace(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, d
 
 int vrg_solver_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, int nt, vrg_solver_t* out) {
     *out = nullptr;
-    return guarded(c, [&] { *out = new vrg_solver_s{c, vrg::Solver(c->ctx, dims(n1, n2), v1, v2, nt)}; });
+    return guarded(c, [&] {
+        auto* h = new vrg_solver_s{c, vrg::Solver(c->ctx, dims(n1, n2), v1, v2, nt), nullptr, vrg::DBuf()};
+        if (c->scheme != VRG_SCHEME_SL) {
+            h->heun = std::make_unique<vrg::HeunTransport>(c->ctx, dims(n1, n2), v1, v2, nt,
+                                                           c->scheme == VRG_SCHEME_RK2A);
+            h->stages.alloc(sizeof(double) * nt * dims(n1, n2).points());
+        }
+        *out = h;
+    });
 }
 
 void vrg_solver_destroy(vrg_solver_t s) {
@@ -262,23 +284,54 @@ void vrg_solver_destroy(vrg_solver_t s) {
 }
 
 int vrg_solver_state(vrg_solver_t s, const double* m0, double* traj) {
-    return guarded(s->owner, [&] { s->solver.state(m0, traj, true); });
+    return guarded(s->owner, [&] {
+        if (s->heun)
+            s->heun->forward(m0, traj, s->stages.d(), true);
+        else
+            s->solver.state(m0, traj, true);
+    });
 }
 
 int vrg_solver_adjoint(vrg_solver_t s, const double* lam1, double* traj) {
-    return guarded(s->owner, [&] { s->solver.adjoint(lam1, traj, true); });
+    return guarded(s->owner, [&] {
+        if (s->heun)
+            s->heun->backward(lam1, traj, s->stages.d(), true);
+        else
+            s->solver.adjoint(lam1, traj, true);
+    });
 }
 
 int vrg_solver_state_final(vrg_solver_t s, const double* m0, double* out) {
-    return guarded(s->owner, [&] { s->solver.stateFinal(m0, out); });
+    return guarded(s->owner, [&] {
+        if (s->heun)
+            s->heun->stateFinal(m0, out);
+        else
+            s->solver.stateFinal(m0, out);
+    });
 }
 
 int vrg_solver_adjoint_final(vrg_solver_t s, const double* lam1, double* out) {
-    return guarded(s->owner, [&] { s->solver.adjointFinal(lam1, out); });
+    return guarded(s->owner, [&] {
+        if (s->heun)
+            s->heun->adjointFinal(lam1, out);
+        else
+            s->solver.adjointFinal(lam1, out);
+    });
 }
 
 int vrg_solver_incstate(vrg_solver_t s, const double* vt1, const double* vt2, const double* state, double* traj) {
-    return guarded(s->owner, [&] { s->solver.incState(vt1, vt2, state, traj); });
+    return guarded(s->owner, [&] {
+        if (s->heun) {  // the state's Heun predictors, recomputed from its nodes
+            vrg::HeunTransport& H = *s->heun;
+            const long long f0 = H.ctx.ffts;
+            H.forwardStages(state, s->stages.d());
+            H.ctx.ffts = f0;  // the reference holds them from the state solve
+            H.incState(vt1, vt2, state, s->stages.d(), traj);
+            H.ctx.sync();
+        } else {
+            s->solver.incState(vt1, vt2, state, traj);
+        }
+    });
 }
 
 int vrg_solver_incadjoint(vrg_solver_t s, const double* vt1, const double* vt2, const double* lt1,
@@ -287,6 +340,15 @@ int vrg_solver_incadjoint(vrg_solver_t s, const double* vt1, const double* vt2, 
         if (mode == VRG_FULL_NEWTON) {
             if (!adjoint)
                 throw vrg::InvalidArgument("solveIncAdjoint: full Newton mode requires the adjoint trajectory");
+            if (s->heun) {
+                vrg::HeunTransport& H = *s->heun;
+                const long long f0 = H.ctx.ffts;
+                H.backwardStages(adjoint, s->stages.d());
+                H.ctx.ffts = f0;
+                H.incAdjointFullNewton(vt1, vt2, lt1, adjoint, s->stages.d(), traj);
+                H.ctx.sync();
+                return;
+            }
             vrg::Solver& S = s->solver;
             const std::size_t N = S.g.points();
             vrg::DBuf work(sizeof(double) * 5 * N), flag(64);
@@ -300,16 +362,25 @@ int vrg_solver_incadjoint(vrg_solver_t s, const double* vt1, const double* vt2, 
         }
         // Gauss-Newton drops every term in lambda: same operator as the adjoint
         // (transport.cpp:392-397), unguarded.
-        s->solver.adjoint(lt1, traj, false);
+        if (s->heun)
+            s->heun->backward(lt1, traj, s->stages.d(), false);
+        else
+            s->solver.adjoint(lt1, traj, false);
     });
 }
 
 int vrg_solver_jacobian(vrg_solver_t s, double* out) {
-    return guarded(s->owner, [&] { s->solver.jacobian(out); });
+    return guarded(s->owner, [&] {
+        if (s->heun)
+            s->heun->jacobian(out);
+        else
+            s->solver.jacobian(out);
+    });
 }
 
 int vrg_solver_departure(vrg_solver_t s, int direction, double* x1, double* x2) {
     return guarded(s->owner, [&] {
+        if (s->heun) throw vrg::NotSupported("departure points exist for the SL scheme only");
         const double* X = s->solver.departure(direction);
         const std::size_t N = s->solver.g.points();
         vrg::copy(s->solver.ctx, N, X, x1);

@@ -9,6 +9,7 @@
 #include "blas.cuh"
 #include "epilogues.cuh"
 #include "evalband.cuh"
+#include "heun.cuh"
 #include "inverse.cuh"
 #include "wave.cuh"
 
@@ -302,12 +303,37 @@ __global__ void k_row_disp(const double* __restrict__ x1, int n1, int n2, double
 
 }  // namespace
 
+namespace {
+__global__ void k_bf_fn(std::size_t N, double w, const double* __restrict__ lt, const double* __restrict__ g1,
+                        const double* __restrict__ g2, const double* __restrict__ lam, const double* __restrict__ t1,
+                        const double* __restrict__ t2, double* __restrict__ b1, double* __restrict__ b2) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const double term1 = lt[p] * g1[p] + 1.0 * (lam[p] * t1[p]);
+    const double term2 = lt[p] * g2[p] + 1.0 * (lam[p] * t2[p]);
+    b1[p] = b1[p] + w * term1;
+    b2[p] = b2[p] + w * term2;
+}
+__global__ void k_add2(std::size_t N, const double* __restrict__ a1, const double* __restrict__ a2,
+                       const double* __restrict__ c1, const double* __restrict__ c2, double* __restrict__ o1,
+                       double* __restrict__ o2) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    o1[p] = a1[p] + 1.0 * c1[p];
+    o2[p] = a2[p] + 1.0 * c2[p];
+}
+}  // namespace
+
 Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2, const double* mR, const double* mT,
                  const Model& mdl, int steps, const double* stateTraj, int hmode, const double* adjTraj)
     : ctx(c), g(gd), model(mdl), nt(steps), solver(c, gd, v1, v2, steps), weights(gd, mdl.norm), mode_(hmode) {
     if (!(mdl.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
     const std::size_t N = g.points();
     state_.alloc(sizeof(double) * (nt + 1) * N);
+    if (model.scheme != kSchemeSL) {
+        initHeun(mR, mT, stateTraj, adjTraj);
+        return;
+    }
     if (stateTraj) {
         VRG_CUDA(cudaMemcpyAsync(state_.d(), stateTraj, sizeof(double) * (nt + 1) * N, cudaMemcpyDeviceToDevice,
                                  ctx.stream));
@@ -496,8 +522,114 @@ void Hessian::setupWave() {
     wave_ = true;
 }
 
+// RK2 / RK2A operator (heun.cuh): state (and, full Newton, adjoint) trajectories with their Heun
+// predictors; no graph capture (the Heun solves check their guards on the host).
+void Hessian::initHeun(const double* mR, const double* mT, const double* stateTraj, const double* adjTraj) {
+    const std::size_t N = g.points();
+    const bool anti = model.scheme == kSchemeRK2A;
+    heun_ = std::make_unique<HeunTransport>(ctx, g, solver.v1(), solver.v2(), nt, anti);
+    stStages_.alloc(sizeof(double) * nt * N);
+    if (stateTraj) {
+        VRG_CUDA(cudaMemcpyAsync(state_.d(), stateTraj, sizeof(double) * (nt + 1) * N, cudaMemcpyDeviceToDevice,
+                                 ctx.stream));
+        const long long f0 = ctx.ffts;
+        heun_->forwardStages(state_.d(), stStages_.d());  // the reference holds them with the state
+        ctx.ffts = f0;
+        lazyFfts_ = anti ? 3 : 0;  // div v, built lazily by the first apply in the reference
+    } else {
+        heun_->forward(mT, state_.d(), stStages_.d(), true);
+    }
+    if (mode_ == 1) {
+        adj_.alloc(sizeof(double) * (nt + 1) * N);
+        adjStages_.alloc(sizeof(double) * nt * N);
+        if (adjTraj) {
+            VRG_CUDA(cudaMemcpyAsync(adj_.d(), adjTraj, sizeof(double) * (nt + 1) * N, cudaMemcpyDeviceToDevice,
+                                     ctx.stream));
+            const long long f0 = ctx.ffts;
+            heun_->backwardStages(adj_.d(), adjStages_.d());
+            ctx.ffts = f0;
+        } else {
+            if (!mR) throw InvalidArgument("HessianOperator: full Newton mode needs the reference image");
+            double* lam1 = ctx.scratchBuf(43, sizeof(double) * N);
+            lincomb(ctx, N, 1.0, state_.d() + static_cast<std::size_t>(nt) * N, -1.0, mR, lam1);
+            lincomb(ctx, N, -1.0, lam1, 0.0, lam1, lam1);
+            heun_->backward(lam1, adj_.d(), adjStages_.d(), true);
+        }
+    }
+    work_.alloc(sizeof(double) * (11 * N + paddedPoints(g.n1, g.n2)));
+    fn_.alloc(sizeof(double) * (3 * (nt + 1)) * N);  // m~ and lt trajectories, lt predictors
+    useGraphs = false;
+    lazyInterps_ = 0;
+    spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
+    adjLog_.ensure(nt + 1, evalBlocks(g));
+    weights.regSymbol(model.betaV);
+    weights.invRegSymbol(model.betaV, -0.5);
+    ctx.sync();
+}
+
+namespace {
+__global__ void k_bf_terms(std::size_t N, double w, const double* __restrict__ a1, const double* __restrict__ a2,
+                           const double* __restrict__ c1, const double* __restrict__ c2, double* __restrict__ b1,
+                           double* __restrict__ b2) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    b1[p] = __dadd_rn(b1[p], __dmul_rn(w, __dadd_rn(a1[p], c1[p])));
+    b2[p] = __dadd_rn(b2[p], __dmul_rn(w, __dadd_rn(a2[p], c2[p])));
+}
+}  // namespace
+
+// Data term of the RK2 / RK2A operator (inverse.cpp:176-211 with the Heun solves).
+void Hessian::dataTermHeun(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
+                           const double* reg2, double* out1, double* out2) {
+    const std::size_t N = g.points();
+    const double ht = 1.0 / nt;
+    const bool anti = model.scheme == kSchemeRK2A;
+    double* mt = fn_.d();
+    double* lt = mt + static_cast<std::size_t>(nt + 1) * N;
+    double* ltS = lt + static_cast<std::size_t>(nt + 1) * N;
+    heun_->incState(vt1, vt2, state_.d(), stStages_.d(), mt);
+    double* lt1 = lt + static_cast<std::size_t>(nt) * N;
+    lincomb(ctx, N, -1.0, mt + static_cast<std::size_t>(nt) * N, 0.0, mt + static_cast<std::size_t>(nt) * N, lt1);
+    if (mode_ == 0) {
+        heun_->backward(lt1, lt, ltS, true);  // solveAdjoint(-m~(1)), guarded (inverse.cpp:185)
+        bodyForceHeun(ctx, g, nt, anti, state_.d(), stStages_.d(), lt, ltS, b1, b2);
+    } else {
+        heun_->incAdjointFullNewton(vt1, vt2, lt1, adj_.d(), adjStages_.d(), lt);
+        double* t = ctx.scratchBuf(44, sizeof(double) * 4 * N);
+        fill(ctx, N, 0.0, b1);
+        fill(ctx, N, 0.0, b2);
+        for (int j = 0; j <= nt; ++j) {
+            const double w = ht * ((j == 0 || j == nt) ? 0.5 : 1.0);
+            const std::size_t o = static_cast<std::size_t>(j) * N;
+            if (anti) {
+                antisymmetricForceTerm(ctx, g, state_.d() + o, lt + o, t, t + N);
+                antisymmetricForceTerm(ctx, g, mt + o, adj_.d() + o, t + 2 * N, t + 3 * N);
+                LaunchScope ls_(ctx, "k_bf_terms");
+                k_bf_terms<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, w, t, t + N, t + 2 * N, t + 3 * N, b1, b2);
+            } else {
+                gradient(ctx, g, state_.d() + o, t, t + N);
+                gradient(ctx, g, mt + o, t + 2 * N, t + 3 * N);
+                LaunchScope ls_(ctx, "k_bf_fn");
+                k_bf_fn<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, w, lt + o, t, t + N, adj_.d() + o, t + 2 * N,
+                                                                 t + 3 * N, b1, b2);
+            }
+            VRG_LAUNCH_CHECK();
+        }
+    }
+    if (out1) {
+        LaunchScope ls_(ctx, "k_add2");
+        k_add2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, reg1, reg2, b1, b2, out1, out2);
+        VRG_LAUNCH_CHECK();
+    }
+}
+
 void Hessian::countDataTerm() {
     if (model.deformation == kNearIncompressible) ctx.ffts += 8;  // penalty gradient of vt
+    if (heun_) {  // the Heun solves count as they run (no graph replay); projection and lazy div v
+        ctx.ffts += (model.deformation == kIncompressible ? 4 : 0) + lazyFfts_;
+        lazyFfts_ = 0;
+        return;
+    }
     if (mode_ == 1) {
         // incState 2 + 3nt interps, 3 + 3nt FFTs; FN incAdjoint 2nt interps, 3(nt+1) FFTs
         // (div of products); body force 3(nt+1) + 3(nt+1) FFTs (grad m_j, grad m~_j)
@@ -515,6 +647,10 @@ void Hessian::countDataTerm() {
 
 void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                        const double* reg2, double* out1, double* out2) {
+    if (heun_) {
+        dataTermHeun(vt1, vt2, b1, b2, reg1, reg2, out1, out2);
+        return;
+    }
     if (mode_ == 1) {
         dataTermFN(vt1, vt2, b1, b2, reg1, reg2, out1, out2);
         return;
@@ -677,26 +813,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
 // incremental state trajectory, full-Newton incremental adjoint, and the body force
 // b = sum_j w_j (lt_j grad m_j + lambda_j grad m~_j), trapezoid weights, in the reference's
 // order (j = 0..nt).
-namespace {
-__global__ void k_bf_fn(std::size_t N, double w, const double* __restrict__ lt, const double* __restrict__ g1,
-                        const double* __restrict__ g2, const double* __restrict__ lam, const double* __restrict__ t1,
-                        const double* __restrict__ t2, double* __restrict__ b1, double* __restrict__ b2) {
-    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    const double term1 = lt[p] * g1[p] + 1.0 * (lam[p] * t1[p]);
-    const double term2 = lt[p] * g2[p] + 1.0 * (lam[p] * t2[p]);
-    b1[p] = b1[p] + w * term1;
-    b2[p] = b2[p] + w * term2;
-}
-__global__ void k_add2(std::size_t N, const double* __restrict__ a1, const double* __restrict__ a2,
-                       const double* __restrict__ c1, const double* __restrict__ c2, double* __restrict__ o1,
-                       double* __restrict__ o2) {
-    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    o1[p] = a1[p] + 1.0 * c1[p];
-    o2[p] = a2[p] + 1.0 * c2[p];
-}
-}  // namespace
+
 
 void Hessian::dataTermFN(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                          const double* reg2, double* out1, double* out2) {
@@ -820,6 +937,7 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
 }
 
 void Hessian::checkLastGuard() {
+    if (heun_) return;  // the Heun solves checked their guards as they ran
     if (mode_ == 1) {  // full Newton: no guard in the incremental solves, prefilter input checks only
         unsigned h = 0;
         VRG_CUDA(cudaMemcpyAsync(&h, fnFlag_.d(), sizeof h, cudaMemcpyDeviceToHost, ctx.stream));
@@ -1136,14 +1254,20 @@ void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, con
 void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                        const double* mT, const Model& model, int nt, double* scalars, double* stateOut) {
     const std::size_t N = g.points();
-    Solver solver(ctx, g, v1, v2, nt);
     DBuf stateBuf;
     double* st = stateOut;
     if (!st) {
         stateBuf.alloc(sizeof(double) * (nt + 1) * N);
         st = stateBuf.d();
     }
-    solver.state(mT, st, true);
+    if (model.scheme != kSchemeSL) {
+        HeunTransport heun(ctx, g, v1, v2, nt, model.scheme == kSchemeRK2A);
+        DBuf stages(sizeof(double) * nt * N);
+        heun.forward(mT, st, stages.d(), true);
+    } else {
+        Solver solver(ctx, g, v1, v2, nt);
+        solver.state(mT, st, true);
+    }
     double* resid = ctx.scratchBuf(21, sizeof(double) * N);
     lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
     const double mismatch = 0.5 * dot(ctx, g, resid, nullptr, resid, nullptr);
@@ -1163,7 +1287,6 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
                       double* stateOut, double* adjOut, const double* reuseState) {
     const std::size_t N = g.points();
-    Solver solver(ctx, g, v1, v2, nt);
     DBuf stBuf, adBuf;
     double* st = stateOut;
     double* ad = adjOut;
@@ -1175,18 +1298,39 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
         adBuf.alloc(sizeof(double) * (nt + 1) * N);
         ad = adBuf.d();
     }
-    if (reuseState) {
-        if (reuseState != st) copy(ctx, (nt + 1) * N, reuseState, st);
-    } else {
-        solver.state(mT, st, true);
-    }
-    double* resid = ctx.scratchBuf(21, sizeof(double) * N);
-    lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
-    const double mismatch = 0.5 * dot(ctx, g, resid, nullptr, resid, nullptr);
-    lincomb(ctx, N, -1.0, resid, 0.0, resid, resid);  // lambda1 = -1.0 * resid
-    solver.adjoint(resid, ad, true);
     double* b = ctx.scratchBuf(23, sizeof(double) * 2 * N);
-    bodyForce(ctx, g, nt, st, ad, b, b + N);
+    double* resid = ctx.scratchBuf(21, sizeof(double) * N);
+    double mismatch = 0.0;
+    if (model.scheme != kSchemeSL) {  // RK2 / RK2A: Heun solves, stage-paired body force
+        const bool anti = model.scheme == kSchemeRK2A;
+        HeunTransport heun(ctx, g, v1, v2, nt, anti);
+        DBuf stS(sizeof(double) * nt * N), adS(sizeof(double) * nt * N);
+        if (reuseState) {
+            if (reuseState != st) copy(ctx, (nt + 1) * N, reuseState, st);
+            const long long f0 = ctx.ffts;
+            heun.forwardStages(st, stS.d());
+            ctx.ffts = f0;
+        } else {
+            heun.forward(mT, st, stS.d(), true);
+        }
+        lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
+        mismatch = 0.5 * dot(ctx, g, resid, nullptr, resid, nullptr);
+        lincomb(ctx, N, -1.0, resid, 0.0, resid, resid);
+        heun.backward(resid, ad, adS.d(), true);
+        bodyForceHeun(ctx, g, nt, anti, st, stS.d(), ad, adS.d(), b, b + N);
+    } else {
+        Solver solver(ctx, g, v1, v2, nt);
+        if (reuseState) {
+            if (reuseState != st) copy(ctx, (nt + 1) * N, reuseState, st);
+        } else {
+            solver.state(mT, st, true);
+        }
+        lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
+        mismatch = 0.5 * dot(ctx, g, resid, nullptr, resid, nullptr);
+        lincomb(ctx, N, -1.0, resid, 0.0, resid, resid);  // lambda1 = -1.0 * resid
+        solver.adjoint(resid, ad, true);
+        bodyForce(ctx, g, nt, st, ad, b, b + N);
+    }
     Weights w(g, model.norm);
     if (!(model.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
     applyRealSymbol(ctx, g, v1, v2, g1, g2, w.regSymbol(model.betaV));

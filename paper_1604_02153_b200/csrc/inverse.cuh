@@ -15,6 +15,7 @@ struct Model {
     double betaV = 1e-2;
     int deformation = kCompressible;
     double betaW = 1e-1;
+    int scheme = 0;  // transport scheme (heun.cuh TransportScheme); SchemeConfig in the reference
 };
 
 // GN Hessian at one velocity iterate, everything device-resident.
@@ -98,6 +99,12 @@ private:
     void dataTermFN(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                     const double* reg2, double* out1, double* out2);
     void addPenalty(const double* vt1, const double* vt2, double* b1, double* b2);
+    // RK2 / RK2A scheme (heun.cuh)
+    std::unique_ptr<class HeunTransport> heun_;
+    DBuf stStages_, adjStages_;
+    void initHeun(const double* mR, const double* mT, const double* stateTraj, const double* adjTraj);
+    void dataTermHeun(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
+                      const double* reg2, double* out1, double* out2);
     // persistent wavefront kernel for the whole data term (wave.cuh, k_wave)
     bool wave_ = false;
     int waveDRows_ = 0;      // rows a gather may reach from its own row (displacement + stencil)

@@ -10,6 +10,7 @@
 #include <memory>
 #include <random>
 
+#include "heun.cuh"
 #include "precond.cuh"
 
 namespace vrg {
@@ -142,7 +143,9 @@ CoarseOperator::CoarseOperator(Ctx& c, const GridDims& fg, const double* v, cons
         ctx.ffts += 4;  // the reference resamples the zero velocity too
     }
     nt = deriveSteps(ctx, gc, vc.d(), vc.d() + Nc, coarseCfl);
-    hess = std::make_unique<Hessian>(ctx, gc, vc.d(), vc.d() + Nc, mRc.d(), mTc.d(), model, nt, nullptr);
+    Model coarseModel = model;
+    coarseModel.scheme = kSchemeSL;  // the coarse problem is SL(5) whatever the fine scheme (kCoarseScheme)
+    hess = std::make_unique<Hessian>(ctx, gc, vc.d(), vc.d() + Nc, mRc.d(), mTc.d(), coarseModel, nt, nullptr);
 }
 
 // ------------------------------------------------------------------------------ Chebyshev / PCG

@@ -356,7 +356,7 @@ def test_full_newton_incadjoint_vs_reference(ctx, api, ref):
     vt1, vt2 = synth.smooth_velocity(n, n, 3000)
     lt1 = synth.smoothed_noise(n, n, 1000)
     adj = ref.solve_adjoint(v1, v2, nt, mT)
-    e = ref.solve_incadjoint_fn(v1, v2, nt, vt1, vt2, lt1, adj)
+    e = ref.solve_incadjoint_fn(v1, v2, nt, vt1, vt2, lt1, mT)
     S = api.Solver(ctx, (ctx.field(v1), ctx.field(v2)), nt)
     got = S.solve_inc_adjoint((ctx.field(vt1), ctx.field(vt2)), ctx.field(lt1), adjoint=ctx.field(adj),
                               mode=api.FULL_NEWTON)
