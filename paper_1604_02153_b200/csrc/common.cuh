@@ -156,8 +156,9 @@ struct Ctx {
 
     struct PlanKey {
         int n1, n2, type, batch;
+        cudaStream_t stream;  // plans are bound to the stream current at creation
         bool operator<(const PlanKey& o) const {
-            return std::tie(n1, n2, type, batch) < std::tie(o.n1, o.n2, o.type, o.batch);
+            return std::tie(n1, n2, type, batch, stream) < std::tie(o.n1, o.n2, o.type, o.batch, o.stream);
         }
     };
     std::map<PlanKey, cufftHandle> plans;
@@ -193,6 +194,15 @@ struct Ctx {
     cufftHandle plan(const GridDims& g, cufftType type, int batch);
     double* scratchBuf(int slot, std::size_t bytes);
     void sync();
+};
+
+// Runs the library's launches of a scope on another stream (ctx.stream swapped), e.g. an
+// independent branch forked with events.
+struct StreamSwap {
+    Ctx& c;
+    cudaStream_t old;
+    StreamSwap(Ctx& ctx, cudaStream_t s) : c(ctx), old(ctx.stream) { c.stream = s; }
+    ~StreamSwap() { c.stream = old; }
 };
 
 // Marks one kernel launch of this library; records a CUDA event pair around it when the

@@ -617,6 +617,7 @@ void Hessian::dataTermHeun(const double* vt1, const double* vt2, double* b1, dou
         }
     }
     if (out1) {
+        waitReg();
         LaunchScope ls_(ctx, "k_add2");
         k_add2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, reg1, reg2, b1, b2, out1, out2);
         VRG_LAUNCH_CHECK();
@@ -777,11 +778,13 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
             const bool last = j == 1;
             EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, nullptr, G(j - 1), G(j - 1) + N, wOf(j - 1),
                              b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
-            if (last)
+            if (last) {
+                waitReg();
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
-            else
+            } else {
                 launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, R[(j - 1) & 1],
                                                    adjLog_.flag(j - 1));
+            }
         }
         adjLog_.finalize(ctx);
         return;
@@ -804,6 +807,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         const bool last = (j == 1) && out1;
         EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, lam[(j - 1) & 1], G(j - 1), G(j - 1) + N, wOf(j - 1),
                          b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
+        if (j == 1) waitReg();
         launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
     }
     adjLog_.finalize(ctx);
@@ -867,12 +871,19 @@ void Hessian::dataTermFN(const double* vt1, const double* vt2, double* b1, doubl
         VRG_LAUNCH_CHECK();
     }
     if (out1) {
+        waitReg();
         LaunchScope ls_(ctx, "k_add2");
         k_add2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, reg1, reg2, b1, b2, out1, out2);
         VRG_LAUNCH_CHECK();
     }
     ctx.ffts = f0;
     ctx.interps = i0;
+}
+
+void Hessian::waitReg() {
+    if (!regPending_) return;
+    VRG_CUDA(cudaStreamWaitEvent(ctx.stream, evJoin_, 0));
+    regPending_ = false;
 }
 
 // b += -betaW grad((1 - Lap) div vt) (inverse.cpp:214-215), without touching the op counters
@@ -1007,6 +1018,12 @@ double Hessian::benchKernel(int id, int iters) {
                                                    adjLog_.flag(0));
                 break;
             }
+            case 11: {  // band incremental-state step without the gather (m~_0 = 0 form): operand traffic only
+                if (!fused_) throw NotSupported("bench kernel 11: band path not active on this grid");
+                EpiIncState epi{nullptr, vtD, vtD + N, GD, GD + N, vtD, vtD + N, G, G + N, 0.5 * ht, nullptr};
+                launchEvalBand<EpiIncState, false>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, tmp, nullptr);
+                break;
+            }
             case 9:  // SL state step (config 4 unit ii), band form: gather + m_j + next row pass, column pass
                 if (!solver.bandPath()) throw NotSupported("bench kernel 9: band path not active on this grid");
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N,
@@ -1096,6 +1113,12 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
 }
 
 Hessian::~Hessian() {
+    if (aux_) {
+        cudaStreamSynchronize(aux_);
+        cudaEventDestroy(evFork_);
+        cudaEventDestroy(evJoin_);
+        cudaStreamDestroy(aux_);
+    }
     for (auto& kv : graphs_) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         for (cudaEvent_t e : kv.second.events) cudaEventDestroy(e);
@@ -1135,19 +1158,41 @@ void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, doub
             fftInverse(ctx, g, S + 3 * NS, o2, 1);
         }
     } else {
-        // reg = beta A vt, then the last adjoint step writes out = reg + b
-        if (vt2 == vt1 + N) {
-            fftForward(ctx, g, vt1, S, 2);
-        } else {
-            fftForward(ctx, g, vt1, S, 1);
-            fftForward(ctx, g, vt2, S + NS, 1);
+        // reg = beta A vt on the second stream (independent of the data term until its last
+        // step), then the last adjoint step writes out = reg + b
+        static const bool regStream = [] {
+            const char* e = std::getenv("VRG_REG_STREAM");
+            return !(e && e[0] == '0');
+        }();
+        if (!aux_ && regStream) {
+            VRG_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+            VRG_CUDA(cudaEventCreateWithFlags(&evFork_, cudaEventDisableTiming));
+            VRG_CUDA(cudaEventCreateWithFlags(&evJoin_, cudaEventDisableTiming));
         }
-        specScale(ctx, g, S, 2, regSym, 1.0 / N);
-        fftInverse(ctx, g, S, reg, 2);
+        if (aux_) {
+            VRG_CUDA(cudaEventRecord(evFork_, ctx.stream));
+            VRG_CUDA(cudaStreamWaitEvent(aux_, evFork_, 0));
+        }
+        {
+            StreamSwap sw(ctx, aux_ ? aux_ : ctx.stream);
+            if (vt2 == vt1 + N) {
+                fftForward(ctx, g, vt1, S, 2);
+            } else {
+                fftForward(ctx, g, vt1, S, 1);
+                fftForward(ctx, g, vt2, S + NS, 1);
+            }
+            specScale(ctx, g, S, 2, regSym, 1.0 / N);
+            fftInverse(ctx, g, S, reg, 2);
+        }
+        if (aux_) {
+            VRG_CUDA(cudaEventRecord(evJoin_, aux_));
+            regPending_ = true;
+        }
         if (model.deformation == kNearIncompressible) {
             // out = beta A vt + (b + penalty gradient) (inverse.cpp:212-233)
             dataTerm(vt1, vt2, b, b + N, nullptr, nullptr, nullptr, nullptr);
             addPenalty(vt1, vt2, b, b + N);
+            waitReg();
             LaunchScope ls_(ctx, "k_add2");
             k_add2<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, reg, reg + N, b, b + N, o1, o2);
             VRG_LAUNCH_CHECK();

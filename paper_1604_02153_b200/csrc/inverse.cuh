@@ -99,6 +99,11 @@ private:
     void dataTermFN(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                     const double* reg2, double* out1, double* out2);
     void addPenalty(const double* vt1, const double* vt2, double* b1, double* b2);
+    // beta A vt on a second stream, joined before the data term's last step consumes it
+    cudaStream_t aux_ = nullptr;
+    cudaEvent_t evFork_ = nullptr, evJoin_ = nullptr;
+    bool regPending_ = false;
+    void waitReg();
     // RK2 / RK2A scheme (heun.cuh)
     std::unique_ptr<class HeunTransport> heun_;
     DBuf stStages_, adjStages_;

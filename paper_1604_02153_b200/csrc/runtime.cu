@@ -152,7 +152,7 @@ Ctx::~Ctx() {
 }
 
 cufftHandle Ctx::plan(const GridDims& g, cufftType type, int batch) {
-    PlanKey key{g.n1, g.n2, static_cast<int>(type), batch};
+    PlanKey key{g.n1, g.n2, static_cast<int>(type), batch, stream};
     auto it = plans.find(key);
     if (it != plans.end()) return it->second;
     cufftHandle h;
