@@ -119,9 +119,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
                 const int b1 = tapRow(cellBase(xa, inv1, n1, w1));
                 const int b2 = cellBase(xb, inv2, n2, w2);
                 base = b1 * PW + b2;
-#ifdef VRG_BAND_EXPERIMENT_NOGATHER
-                base = r * PW + col;  // experiment only: coalesced taps at the arrival node
-#endif
+
             }
             cur = pre;
             if (k + 1 < per) {
@@ -136,9 +134,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
                 const int b1 = tapRow(cellBase(__ldg(x1 + p), inv1, n1, w1));
                 const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
                 base = b1 * PW + b2;
-#ifdef VRG_BAND_EXPERIMENT_NOGATHER
-                base = r * PW + col;  // experiment only: coalesced taps at the arrival node
-#endif
+
             }
             cur = epi.prefetch(p);
             if (kGather && k == 0) {
