@@ -142,7 +142,7 @@ KERNEL_CLASSES_BAND = {
     6: ("reference: field axpy kernel (not in matvec)", 0, 3),
 }
 # ncu kernel-name fragments of the band-path classes (for the traffic lookup)
-NCU_NAMES = {7: "k_eval_band<EpiIncState, 1>", 8: "EpiAdjointBF, 1>", 4: "k_pf_cols_reg"}
+NCU_NAMES = {7: "k_eval_band<EpiIncState, 1, 0>", 8: "EpiAdjointBF, 1, 0>", 4: "k_pf_cols_reg"}
 KERNEL_CLASSES_PLAIN = {
     0: ("evaluate/incstate (K6)", NT - 1, 12),
     1: ("evaluate/adjoint_bodyforce (K5+K8)", NT, 12),
