@@ -141,6 +141,12 @@ int vrg_hess_apply_split(vrg_hess_t h, const double* s1, const double* s2, doubl
 /* apply() from HOST buffers: H2D of vtilde, matvec, D2H of the result (the drop-in call a
  * host-side caller of HessianOperator::apply makes; value semantics of inverse.hpp:83). */
 int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);
+/* k independent apply_host calls (inputs vt1[i], vt2[i] -> outputs o1[i], o2[i], host buffers,
+ * pinned for overlap) with the host<->device copies of neighbouring matvecs overlapped with the
+ * compute of the current one (two copy streams, two device slots).  Same results and error
+ * behaviour as k apply_host calls in order; the first failing matvec's error is returned. */
+int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, const double* const* vt2,
+                              double* const* o1, double* const* o2);
 int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajectory */
 /* instrumentation: average ms of one launch of a matvec kernel class (0 incremental-state
  * step, 1 incremental-adjoint + body-force step, 2 prefilter (both passes), 3 two-field

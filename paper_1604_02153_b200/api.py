@@ -339,6 +339,26 @@ class HessianOperator:
             return C.c_void_p(a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr())
         self.ctx.check(self.ctx.lib.vrg_hess_apply_host(self.h, hp(vt1), hp(vt2), hp(o1), hp(o2)))
 
+    def apply_host_batch(self, vts, outs):
+        """apply_host over k independent inputs vts[i] = (vt1, vt2) -> outs[i] = (o1, o2), host
+        buffers (pinned for overlap); neighbouring matvecs' copies overlap the compute."""
+        k = len(vts)
+        if len(outs) != k:
+            raise ValueError("apply_host_batch: as many outputs as inputs")
+
+        def hp(a):
+            return a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr()
+        arr = [(C.c_void_p * max(k, 1))(*[hp(x[j]) for x in seq]) for seq, j in
+               ((vts, 0), (vts, 1), (outs, 0), (outs, 1))]
+        self.ctx.check(self.ctx.lib.vrg_hess_apply_host_batch(self.h, k, *[C.cast(a, C.c_void_p) for a in arr]))
+
+    @property
+    def band_path(self):
+        """True when the matvec runs the fused band kernels (evalband.cuh), False on the 3-kernel step."""
+        b = C.c_int()
+        self.ctx.check(self.ctx.lib.vrg_hess_band_path(self.h, C.byref(b)))
+        return bool(b.value)
+
     def state(self):
         t = self.ctx.empty(self.nt + 1, *self.shape)
         self.ctx.check(self.ctx.lib.vrg_hess_state(self.h, _p(t)))

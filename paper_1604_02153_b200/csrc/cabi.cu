@@ -22,10 +22,32 @@ struct vrg_solver_s {
     std::unique_ptr<vrg::HeunTransport> heun;  // RK2 / RK2A solver (scheme != SL)
     vrg::DBuf stages;                           // nt predictor fields of the last trajectory
 };
+// Copy streams and events of the pipelined host-buffer batch (vrg_hess_apply_host_batch).
+struct HostPipe {
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t start = nullptr, evIn[2] = {}, evComp[2] = {}, evOut[2] = {};
+    void init() {
+        if (in) return;
+        VRG_CUDA(cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking));
+        VRG_CUDA(cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&start, &evIn[0], &evIn[1], &evComp[0], &evComp[1], &evOut[0], &evOut[1]})
+            VRG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    ~HostPipe() {
+        if (!in) return;
+        cudaStreamSynchronize(in);
+        cudaStreamSynchronize(out);
+        for (cudaEvent_t e : {start, evIn[0], evIn[1], evComp[0], evComp[1], evOut[0], evOut[1]}) cudaEventDestroy(e);
+        cudaStreamDestroy(in);
+        cudaStreamDestroy(out);
+    }
+};
+
 struct vrg_hess_s {
     vrg_ctx_s* owner;
     vrg::Hessian hess;
-    vrg::DBuf io;  // device staging for the host-buffer entry point
+    vrg::DBuf io;     // device staging for the host-buffer entry points
+    HostPipe pipe;    // copy streams of the batch entry point
 };
 
 namespace {
@@ -496,6 +518,59 @@ int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, doub
         h->hess.apply(d, d + N, d + 2 * N, d + 3 * N);
         VRG_CUDA(cudaMemcpyAsync(o1, d + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
         VRG_CUDA(cudaMemcpyAsync(o2, d + 3 * N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+    });
+}
+
+// k independent matvecs from host buffers, copies overlapped with compute: two device slots;
+// the H2D of matvec i+1 (copy stream `in`) and the D2H of matvec i-1 (copy stream `out`) run
+// while matvec i computes on the context stream.  Each apply() still checks its guard before the
+// next is issued, so errors surface at the matvec that raised them, as with apply_host.
+int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, const double* const* vt2,
+                              double* const* o1, double* const* o2) {
+    return guarded(h->owner, [&] {
+        if (k < 0) throw vrg::InvalidArgument("apply_host_batch: negative count");
+        if (k == 0) return;
+        vrg::Ctx& ctx = h->hess.ctx;
+        const std::size_t N = h->hess.g.points(), B = sizeof(double) * N;
+        if (h->io.bytes() < 8 * B) h->io.alloc(8 * B);
+        HostPipe& P = h->pipe;
+        P.init();
+        double* base = h->io.d();
+        auto in = [&](int s) { return base + static_cast<std::size_t>(s) * 4 * N; };
+        auto outp = [&](int s) { return in(s) + 2 * N; };
+        VRG_CUDA(cudaEventRecord(P.start, ctx.stream));  // slots free of earlier work on the stream
+        VRG_CUDA(cudaStreamWaitEvent(P.in, P.start, 0));
+        VRG_CUDA(cudaStreamWaitEvent(P.out, P.start, 0));
+        auto upload = [&](int i) {
+            const int s = i & 1;
+            if (i >= 2) VRG_CUDA(cudaStreamWaitEvent(P.in, P.evComp[s], 0));  // matvec i-2 read slot s
+            VRG_CUDA(cudaMemcpyAsync(in(s), vt1[i], B, cudaMemcpyHostToDevice, P.in));
+            VRG_CUDA(cudaMemcpyAsync(in(s) + N, vt2[i], B, cudaMemcpyHostToDevice, P.in));
+            VRG_CUDA(cudaEventRecord(P.evIn[s], P.in));
+        };
+        try {
+            upload(0);
+            for (int i = 0; i < k; ++i) {
+                const int s = i & 1;
+                if (i + 1 < k) upload(i + 1);
+                VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evIn[s], 0));
+                if (i >= 2) VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evOut[s], 0));  // D2H i-2 read slot s
+                h->hess.apply(in(s), in(s) + N, outp(s), outp(s) + N);
+                VRG_CUDA(cudaEventRecord(P.evComp[s], ctx.stream));
+                VRG_CUDA(cudaStreamWaitEvent(P.out, P.evComp[s], 0));
+                VRG_CUDA(cudaMemcpyAsync(o1[i], outp(s), B, cudaMemcpyDeviceToHost, P.out));
+                VRG_CUDA(cudaMemcpyAsync(o2[i], outp(s) + N, B, cudaMemcpyDeviceToHost, P.out));
+                VRG_CUDA(cudaEventRecord(P.evOut[s], P.out));
+            }
+        } catch (...) {
+            cudaStreamSynchronize(P.in);  // no copy outlives the call
+            cudaStreamSynchronize(P.out);
+            throw;
+        }
+        VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evIn[(k - 1) & 1], 0));
+        VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evOut[(k - 1) & 1], 0));
+        if (k > 1) VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evOut[k & 1], 0));
         ctx.sync();
     });
 }

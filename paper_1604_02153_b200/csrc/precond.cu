@@ -55,8 +55,8 @@ __global__ void k_restrict_low(const double2* __restrict__ f, int n1f, int n2f, 
 
 // out^ = (prolong(sc^) * amp + highpass(r^)) * scale on the fine half spectrum
 // (resample(sc, fine) + cutoffFilter(r, High), precond.cpp:267, 286-287).
-__global__ void k_prolong_add_high(const double2* __restrict__ sc, int n1c, int n2c, const double2* __restrict__ rf,
-                                   double2* __restrict__ out, int n1f, int n2f, double amp, double scale) {
+// rf and out may alias (in-place update, one element per thread)
+__global__ void k_prolong_add_high(const double2* __restrict__ sc, int n1c, int n2c, const double2* rf, double2* out, int n1f, int n2f, double amp, double scale) {
     const int ncc = n2c / 2 + 1, ncf = n2f / 2 + 1;
     const std::size_t n = static_cast<std::size_t>(n1f) * ncf;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -287,7 +287,8 @@ def apply_floor(n, p, beta, vmax, outmax):
     return 4 * 2.2e-16 * beta * kmax2 ** p * vmax / outmax
 
 
-@pytest.mark.parametrize("n1,n2,nt", [(256, 256, 1), (256, 512, 3), (512, 256, 8), (1024, 1024, 4)])
+@pytest.mark.parametrize("n1,n2,nt", [(256, 256, 1), (256, 512, 3), (512, 256, 8), (1024, 1024, 4), (768, 768, 2),
+                                      (96, 1280, 3), (160, 256, 2)])
 def test_band_and_wave_paths_vs_plain(ctx, api, monkeypatch, n1, n2, nt):
     """The fused band step (gather + epilogue + next row pass, evalband.cuh) and the persistent
     wavefront kernel (wave.cuh) are the same algorithm as the plain 3-kernel step: data term
@@ -306,6 +307,7 @@ def test_band_and_wave_paths_vs_plain(ctx, api, monkeypatch, n1, n2, nt):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         H = api.HessianOperator(ctx, (F(0.5 * v1), F(0.5 * v2)), F(mT), F(mT), 2, 1e-3, 0, nt)
+        assert H.band_path == (mode != "plain"), mode
         out = []
         for _ in range(2):  # first call captures the graph, second replays it
             d = H.apply_data_term((F(vt1), F(vt2)))
