@@ -59,3 +59,70 @@ def test_two_rank_gloo(n_items):
     assert [r["item"] for r in res] == list(range(n_items))
     assert all(r["value"] == r["item"] ** 2 and r["owner"] == r["item"] % 2 for r in res)
     assert tmax == 2.0
+
+
+def test_lanes_order_runner_reuse_and_errors():
+    import threading
+    import time
+
+    from paper_1604_02153_b200.batch import run_lanes
+
+    built, active, peak = [], [0], [0]
+    lock = threading.Lock()
+
+    def make_runner(k):
+        built.append(k)
+
+        def run(i):
+            with lock:
+                active[0] += 1
+                peak[0] = max(peak[0], active[0])
+            time.sleep(0.01)
+            with lock:
+                active[0] -= 1
+            return {"sq": i * i}
+        return run
+
+    items = [3, 1, 4, 15, 9, 2, 6]
+    res = run_lanes(items, make_runner, 3)
+    assert [r["item"] for r in res] == items and all(r["sq"] == r["item"] ** 2 for r in res)
+    assert sorted(built) == [0, 1, 2] and peak[0] > 1  # one runner per lane, lanes overlap
+    assert run_lanes([], make_runner, 4) == []
+
+    def failing(k):
+        def run(i):
+            if i == 5:
+                raise RuntimeError("pair 5 failed")
+            return {}
+        return run
+    with pytest.raises(RuntimeError, match="pair 5"):
+        run_lanes(list(range(10)), failing, 2)
+    with pytest.raises(ValueError):
+        run_lanes([1], failing, 0)
+
+
+def _lanes_worker(rank, world, port, n_items, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = run_sharded(n_items, None, rank, world, make_runner=lambda k: (lambda i: {"owner": rank}), lanes=3)
+        if rank == 0:
+            out.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_with_lanes():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lanes_worker, args=(r, 2, port, 11, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r["item"] for r in res] == list(range(11))
+    assert all(r["owner"] == r["item"] % 2 and 0 <= r["lane"] < 3 for r in res)
