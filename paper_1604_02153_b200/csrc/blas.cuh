@@ -12,8 +12,14 @@ constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 // reduction area) and stays stream-ordered.
 double* launchDot(Ctx& ctx, std::size_t n, const double* a0, const double* b0, const double* a1, const double* b1,
                   double scale, int slot);
+// the same reduction with the result written to `out` (any device double)
+void launchDotInto(Ctx& ctx, std::size_t n, const double* a0, const double* b0, const double* a1, const double* b1,
+                   double scale, double* out);
 double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1, double scale, int slot);
 void launchMaxFinal(Ctx& ctx, const double* partials, int nb, double scale, double* out);
+
+// grid size of the element-wise kernels (grid-stride loops, at most 8 blocks of 256 per SM)
+unsigned elemBlocks(const Ctx& ctx, std::size_t n);
 
 // Synchronous host-visible reductions.
 double readScalar(Ctx& ctx, const double* dev);
@@ -25,6 +31,9 @@ bool anyNonFinite(Ctx& ctx, std::size_t n, const double* a0, const double* a1 = 
 
 // y = a*x + b*y ; out = a*x + b*y ; fill ; copy
 void axpby(Ctx& ctx, std::size_t n, double a, const double* x, double b, double* y);
+// y = y + (-c[0]) * x with c a device scalar: the same arithmetic as axpby(ctx, n, -c, x, 1, y)
+// without reading c on the host (stream-ordered Gram-Schmidt)
+void axpyNegDevCoef(Ctx& ctx, std::size_t n, const double* c, const double* x, double* y);
 void lincomb(Ctx& ctx, std::size_t n, double a, const double* x, double b, const double* y, double* out);
 void fill(Ctx& ctx, std::size_t n, double v, double* y);
 void copy(Ctx& ctx, std::size_t n, const double* src, double* dst);

@@ -20,17 +20,16 @@ __global__ void k_advect(std::size_t N, const double* __restrict__ v1, const dou
 
 // o_i = m v_i   (the products of divOfProduct)
 __global__ void k_prod(std::size_t N, const double* __restrict__ m, const double* __restrict__ v1,
-                       const double* __restrict__ v2, double* __restrict__ o1, double* __restrict__ o2) {
+                       const double* __restrict__ v2, double* o1, double* o2) {  // o1 == o2 allowed
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= N) return;
     o1[p] = __dmul_rn(m[p], v1[p]);
     o2[p] = __dmul_rn(m[p], v2[p]);
 }
 
-// out = ((a + c1 b) + c2 (m d)) * s, with b / m d optional (null)
-__global__ void k_comb(std::size_t N, const double* __restrict__ a, double c1, const double* __restrict__ b,
-                       double c2, const double* __restrict__ m, const double* __restrict__ d, double s,
-                       double* __restrict__ out) {
+// out = ((a + c1 b) + c2 (m d)) * s, with b / m d optional (null); out may alias an input
+__global__ void k_comb(std::size_t N, const double* a, double c1, const double* b, double c2, const double* m,
+                       const double* d, double s, double* out) {
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= N) return;
     double r = a[p];

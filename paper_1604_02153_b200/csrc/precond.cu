@@ -10,6 +10,8 @@
 #include <memory>
 #include <random>
 
+#include <cooperative_groups.h>
+
 #include "heun.cuh"
 #include "precond.cuh"
 
@@ -83,6 +85,133 @@ double secondsSince(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+
+// Unpreconditioned PCG step with the scalars on the device: alpha = rz / pAp, x += alpha p,
+// r -= alpha ap (the arithmetic of axpby(alpha, p, 1, x) and axpby(-alpha, ap, 1, r)); no
+// update when !(pAp > 0), where pcg() returns with negative curvature and x as it was.
+__global__ void k_pcg_update(std::size_t n, const double* __restrict__ rz, const double* __restrict__ pAp,
+                             const double* __restrict__ p, const double* __restrict__ ap, double* x, double* r) {
+    const double d = *pAp;
+    if (!(d > 0.0)) return;
+    const double alpha = *rz / d, na = -alpha;
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        x[i] = x[i] + alpha * p[i];
+        r[i] = r[i] + na * ap[i];
+    }
+}
+
+// ------------------------------------------------------------------------------ Lanczos step
+// One Lanczos step's orthogonalisation in one launch: w -= beta_{j-1} q_{j-1}; alpha_j = <w,q_j>;
+// w -= alpha_j q_j; modified Gram-Schmidt against q_0..q_{nb-1}; |w|^2.  One thread-block
+// cluster of kLzCtas CTAs holds w in registers (kPer elements per thread); each inner product is
+// a warp / block / cluster (DSMEM) reduction in a fixed order, identical in every CTA, so the
+// coefficients never leave the device.  Replaces 3(nb+2) launches and nb+2 host reads per step
+// on small coarse grids (2 N <= kLzCtas * 1024 * 8), where launch latency dominates.
+constexpr int kLzCtas = 8;
+constexpr int kLzThreads = 1024;
+
+struct LzRed {
+    double warp[32];
+    double part[2];  // this CTA's partial, double-buffered by call parity
+    double total[2];
+};
+
+__device__ __forceinline__ double lzClusterSum(double v, LzRed& red, int& parity) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red.warp[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double x = red.warp[lane];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) red.part[parity] = x;
+    }
+    cluster.sync();  // every CTA's partial of this call is visible cluster-wide
+    if (wid == 0) {
+        double x = 0.0;
+        if (lane < kLzCtas) x = *cluster.map_shared_rank(&red.part[parity], lane);
+        for (int o = 4; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) red.total[parity] = x;
+    }
+    __syncthreads();
+    const double t = red.total[parity];
+    parity ^= 1;
+    return t;
+}
+
+template <int kPer>
+__global__ void __cluster_dims__(kLzCtas, 1, 1) __launch_bounds__(kLzThreads, 1)
+    k_lanczos_orth(double* __restrict__ w, const double* __restrict__ Q, std::size_t n, int j, int nb, double betaPrev,
+                   double hh, double* __restrict__ alphaOut, double* __restrict__ bsqOut) {
+    __shared__ LzRed red;
+    int parity = 0;
+    const std::size_t base = static_cast<std::size_t>(blockIdx.x) * kLzThreads + threadIdx.x;
+    constexpr std::size_t kStride = static_cast<std::size_t>(kLzCtas) * kLzThreads;
+    double x[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const std::size_t e = base + k * kStride;
+        x[k] = e < n ? w[e] : 0.0;
+    }
+    auto qv = [&](int i, double (&q)[kPer]) {
+        const double* qi = Q + static_cast<std::size_t>(i) * n;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const std::size_t e = base + k * kStride;
+            q[k] = e < n ? qi[e] : 0.0;
+        }
+    };
+    auto project = [&](int i, bool storeAlpha) {
+        double q[kPer];
+        qv(i, q);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) s += x[k] * q[k];
+        const double c = hh * lzClusterSum(s, red, parity);
+        if (storeAlpha && blockIdx.x == 0 && threadIdx.x == 0) *alphaOut = c;
+        const double a = -c;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) x[k] = x[k] + a * q[k];
+    };
+    if (j > 0) {
+        double q[kPer];
+        qv(j - 1, q);
+        const double a = -betaPrev;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) x[k] = x[k] + a * q[k];
+    }
+    project(j, true);
+    for (int i = 0; i < nb; ++i) project(i, false);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) s += x[k] * x[k];
+    const double bsq = hh * lzClusterSum(s, red, parity);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bsqOut = bsq;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const std::size_t e = base + k * kStride;
+        if (e < n) w[e] = x[k];
+    }
+}
+
+bool launchLanczosOrth(Ctx& ctx, double* w, const double* Q, std::size_t n, int j, int nb, double betaPrev, double hh,
+                       double* alphaOut, double* bsqOut) {
+    const std::size_t per = (n + kLzCtas * kLzThreads - 1) / (kLzCtas * kLzThreads);
+    LaunchScope ls_(ctx, "k_lanczos_orth");
+    const dim3 grid(kLzCtas), block(kLzThreads);
+#define VRG_LZ(P) k_lanczos_orth<P><<<grid, block, 0, ctx.stream>>>(w, Q, n, j, nb, betaPrev, hh, alphaOut, bsqOut)
+    if (per <= 1) VRG_LZ(1);
+    else if (per <= 2) VRG_LZ(2);
+    else if (per <= 4) VRG_LZ(4);
+    else if (per <= 8) VRG_LZ(8);
+    else return false;
+#undef VRG_LZ
+    VRG_LAUNCH_CHECK();
+    return true;
+}
 }  // namespace
 
 // ------------------------------------------------------------------------------ vector BLAS
@@ -176,6 +305,52 @@ void chebyshevSolve(Ctx& ctx, const GridDims& g, const LinOpDev& op, const doubl
     }
 }
 
+// The M = null branch of pcg() (the coarse solve of the two-level preconditioner) with one host
+// read per iteration: pAp and rzNew land in adjacent device scalars (k_pcg_update applies the
+// step only when pAp > 0) and come back together.  Same decisions and arithmetic as the loop
+// in pcg().
+static PcgOut pcgUnpreconditioned(Ctx& ctx, const GridDims& g, const LinOpDev& A, double rz, double norm0, int maxIter,
+                           double tol, double* x, double* r, double* p, double* ap) {
+    PcgOut out;
+    const std::size_t N = g.points(), n = 2 * N;
+    const double hh = g.h1() * g.h2();
+    double* sc = ctx.reduce.d() + 2 * kReduceBlocks + 40;  // [rz, pAp, rzNew]
+    fill(ctx, 1, rz, sc);
+    for (int it = 0; it < maxIter; ++it) {
+        A(p, ap);
+        launchDotInto(ctx, N, p, ap, p + N, ap + N, hh, sc + 1);
+        {
+            LaunchScope ls_(ctx, "k_pcg_update");
+            k_pcg_update<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, sc, sc + 1, p, ap, x, r);
+        }
+        VRG_LAUNCH_CHECK();
+        launchDotInto(ctx, N, r, r, r + N, r + N, hh, sc + 2);
+        VRG_CUDA(cudaMemcpyAsync(ctx.hostScalars, sc + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        const double pAp = ctx.hostScalars[0], rzNew = ctx.hostScalars[1];
+        if (!(pAp > 0.0)) {
+            out.negativeCurvature = true;
+            out.relResidual = std::sqrt(std::max(rz, 0.0)) / norm0;
+            return out;
+        }
+        out.iterations = it + 1;
+        if (rzNew < 0.0 || !std::isfinite(rzNew)) {
+            out.indefinitePreconditioner = true;
+            return out;
+        }
+        out.relResidual = std::sqrt(rzNew) / norm0;
+        if (out.relResidual <= tol) {
+            out.converged = true;
+            return out;
+        }
+        const double beta = rzNew / rz;
+        rz = rzNew;
+        VRG_CUDA(cudaMemcpyAsync(sc, sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+        lincomb(ctx, n, beta, p, 1.0, r, p);
+    }
+    return out;
+}
+
 PcgOut pcg(Ctx& ctx, const GridDims& g, const LinOpDev& A, const double* b, const LinOpDev* M, double tol,
            int maxIter, double* x) {
     PcgOut out;
@@ -199,6 +374,7 @@ PcgOut pcg(Ctx& ctx, const GridDims& g, const LinOpDev& A, const double* b, cons
         return out;
     }
     copy(ctx, n, z, p);
+    if (!M) return pcgUnpreconditioned(ctx, g, A, rz, norm0, maxIter, tol, x, r, p, ap);
     for (int it = 0; it < maxIter; ++it) {
         A(p, ap);
         const double pAp = vdot(ctx, g, p, ap);
@@ -280,40 +456,89 @@ static double powerIterationEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op
     return lambda;
 }
 
+// VRG_TRACE=1: per-phase host wall times of newtonSolve on stderr (diagnostics only).
+static bool traceOn() {
+    static const bool on = [] {
+        const char* e = std::getenv("VRG_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+struct PhaseTimer {
+    Ctx& ctx;
+    const char* what;
+    std::chrono::steady_clock::time_point t0;
+    PhaseTimer(Ctx& c, const char* w) : ctx(c), what(w), t0(std::chrono::steady_clock::now()) {}
+    ~PhaseTimer() {
+        if (!traceOn()) return;
+        ctx.sync();
+        std::fprintf(stderr, "trace %-22s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 double lanczosEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, std::uint64_t seed) {
-    const std::size_t n = 2 * g.points();
+    // The alpha and Gram-Schmidt coefficients stay on the device, so a step costs two host
+    // syncs (the operator's guard and beta) instead of 3 + j: on small grids one cluster
+    // launch per step (k_lanczos_orth), else launchDotInto + axpyNegDevCoef per basis vector
+    // (the same arithmetic as vdot + axpby).
+    const std::size_t N = g.points(), n = 2 * N;
+    const double hh = g.h1() * g.h2();
     DBuf basisBuf(sizeof(double) * n * (steps + 1));
-    DBuf wBuf(sizeof(double) * n);
+    DBuf wBuf(sizeof(double) * 2 * n);
+    DBuf coefBuf(sizeof(double) * (steps + 1));
     auto Q = [&](int j) { return basisBuf.d() + static_cast<std::size_t>(j) * n; };
     double* w = wBuf.d();
-    std::vector<double> alpha, beta;
+    double* qIn = w + n;  // fixed operator input: the operator's CUDA graph replays from step 2
+    double* alphaDev = coefBuf.d();   // alpha_j
+    double* cDev = alphaDev + steps;  // reorthogonalisation coefficient
+    auto dotInto = [&](const double* a, const double* b, double* out) {
+        launchDotInto(ctx, N, a, b, a + N, b + N, hh, out);
+    };
+    std::vector<double> beta;
+    int nAlpha = 0;
     randomBandLimitedVelocity(ctx, g, seed, Q(0));
     const double nq = vnormL2(ctx, g, Q(0));
     if (!(nq > 0.0)) return 1.0;
     axpby(ctx, n, 0.0, Q(0), 1.0 / nq, Q(0));
     int nb = 1;
     for (int j = 0; j < steps; ++j) {
-        op(Q(j), w);
-        if (j > 0) axpby(ctx, n, -beta[j - 1], Q(j - 1), 1.0, w);
-        const double a = vdot(ctx, g, w, Q(j));
-        alpha.push_back(a);
-        axpby(ctx, n, -a, Q(j), 1.0, w);
-        for (int i = 0; i < nb; ++i) axpby(ctx, n, -vdot(ctx, g, w, Q(i)), Q(i), 1.0, w);  // full reorth.
-        const double b = vnormL2(ctx, g, w);
+        copy(ctx, n, Q(j), qIn);
+        op(qIn, w);
+        double b;
+        if (launchLanczosOrth(ctx, w, Q(0), n, j, nb, j > 0 ? beta[j - 1] : 0.0, hh, alphaDev + j, cDev)) {
+            ++nAlpha;
+            b = std::sqrt(readScalar(ctx, cDev));  // cDev = |w|^2
+        } else {
+            if (j > 0) axpby(ctx, n, -beta[j - 1], Q(j - 1), 1.0, w);
+            dotInto(w, Q(j), alphaDev + j);
+            ++nAlpha;
+            axpyNegDevCoef(ctx, n, alphaDev + j, Q(j), w);
+            for (int i = 0; i < nb; ++i) {  // full reorthogonalisation (modified Gram-Schmidt)
+                dotInto(w, Q(i), cDev);
+                axpyNegDevCoef(ctx, n, cDev, Q(i), w);
+            }
+            b = vnormL2(ctx, g, w);
+        }
         if (!std::isfinite(b)) return powerIterationEmax(ctx, g, op, seed ^ 0x1234567);
         if (b < 1e-12) break;
         beta.push_back(b);
         lincomb(ctx, n, 1.0 / b, w, 0.0, w, Q(nb));
         ++nb;
     }
-    if (alpha.empty()) return powerIterationEmax(ctx, g, op, seed ^ 0x1234567);
+    if (nAlpha == 0) return powerIterationEmax(ctx, g, op, seed ^ 0x1234567);
+    std::vector<double> alpha(nAlpha);
+    VRG_CUDA(cudaMemcpyAsync(alpha.data(), alphaDev, sizeof(double) * nAlpha, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
     beta.resize(alpha.size() - 1);
     return tridiagMaxEig(alpha, beta);
 }
 
 std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const double* v, const double* mR,
                                          const double* mT, const Model& model, double coarseCfl, std::uint64_t seed) {
+    std::unique_ptr<PhaseTimer> pt(new PhaseTimer(ctx, "eigs: coarse setup"));
     CoarseOperator coarse(ctx, g, v, mR, mT, model, coarseCfl);
+    pt.reset(new PhaseTimer(ctx, "eigs: lanczos(30)"));
     LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
     return {1.0, lanczosEmax(ctx, coarse.gc, op, 30, seed)};
 }
@@ -425,27 +650,6 @@ KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int m
 }
 
 // ------------------------------------------------------------------------------ Newton
-// VRG_TRACE=1: per-phase host wall times of newtonSolve on stderr (diagnostics only).
-static bool traceOn() {
-    static const bool on = [] {
-        const char* e = std::getenv("VRG_TRACE");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-struct PhaseTimer {
-    Ctx& ctx;
-    const char* what;
-    std::chrono::steady_clock::time_point t0;
-    PhaseTimer(Ctx& c, const char* w) : ctx(c), what(w), t0(std::chrono::steady_clock::now()) {}
-    ~PhaseTimer() {
-        if (!traceOn()) return;
-        ctx.sync();
-        std::fprintf(stderr, "trace %-22s %9.3f ms\n", what,
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    }
-};
-
 SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const double* mT, const Model& model,
                          const NewtonConfig& cfg, const PrecondChoice& pc, double* vOut) {
     const std::size_t N = g.points();

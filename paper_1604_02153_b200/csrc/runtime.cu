@@ -337,6 +337,13 @@ __global__ void k_axpby(std::size_t n, double a, const double* __restrict__ x, d
         y[i] = b == 1.0 ? y[i] + a * x[i] : (b == 0.0 ? a * x[i] : b * y[i] + a * x[i]);
 }
 
+__global__ void k_axpy_negcoef(std::size_t n, const double* __restrict__ c, const double* __restrict__ x, double* y) {
+    const double a = -c[0];
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        y[i] = y[i] + a * x[i];
+}
+
 __global__ void k_lincomb(std::size_t n, double a, const double* __restrict__ x, double b,
                           const double* __restrict__ y, double* out) {
     const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
@@ -350,18 +357,25 @@ __global__ void k_fill(std::size_t n, double v, double* y) {
         y[i] = v;
 }
 
+}  // namespace
+
 unsigned elemBlocks(const Ctx& ctx, std::size_t n) {
     const std::size_t want = (n + 255) / 256;
     const std::size_t cap = static_cast<std::size_t>(ctx.numSMs) * 8;
     return static_cast<unsigned>(std::max<std::size_t>(1, std::min(want, cap)));
 }
 
-}  // namespace
 
 double* launchDot(Ctx& ctx, std::size_t n, const double* a0, const double* b0, const double* a1, const double* b1,
                   double scale, int slot) {
+    double* out = ctx.reduce.d() + 2 * kReduceBlocks + slot;
+    launchDotInto(ctx, n, a0, b0, a1, b1, scale, out);
+    return out;
+}
+
+void launchDotInto(Ctx& ctx, std::size_t n, const double* a0, const double* b0, const double* a1, const double* b1,
+                   double scale, double* out) {
     double* partial = ctx.reduce.d();
-    double* out = partial + 2 * kReduceBlocks + slot;
     const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
     {
         LaunchScope ls_(ctx, "k_dot_partial");
@@ -373,8 +387,7 @@ double* launchDot(Ctx& ctx, std::size_t n, const double* a0, const double* b0, c
         k_dot_final<<<1, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
     }
     VRG_LAUNCH_CHECK();
-    return out;
-}
+    }
 
 double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1, double scale, int slot) {
     double* partial = ctx.reduce.d();
@@ -441,6 +454,14 @@ void axpby(Ctx& ctx, std::size_t n, double a, const double* x, double b, double*
     {
         LaunchScope ls_(ctx, "k_axpby");
         k_axpby<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, a, x, b, y);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
+void axpyNegDevCoef(Ctx& ctx, std::size_t n, const double* c, const double* x, double* y) {
+    {
+        LaunchScope ls_(ctx, "k_axpy_negcoef");
+        k_axpy_negcoef<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, c, x, y);
     }
     VRG_LAUNCH_CHECK();
 }
