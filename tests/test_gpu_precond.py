@@ -126,3 +126,20 @@ def test_newton_full_newton_mode_vs_reference(ctx, api, n, nt, cheb):
         assert abs(r["objective"] - q[3]) <= 1e-8 * abs(q[3])
         assert abs(r["gradNormInf"] - q[1]) <= 1e-7 * g0
     assert abs(summ["finalGradNormRel"] - rs[2]) <= 1e-7
+
+
+@pytest.mark.parametrize("n", [128, 256, 512])
+def test_estimate_eigs_vs_reference_sizes(ctx, api, ref, n):
+    """estimateEigs (precond.cpp:242-262): 30-step Lanczos with full reorthogonalisation on the
+    coarse grid.  n = 128 and 256 run the one-launch cluster Gram-Schmidt sweep
+    (k_lanczos_orth, 1 and 4 elements per thread), n = 512 the per-vector launches; all three
+    against the compiled reference."""
+    from paper_1604_02153_b200 import synth
+
+    mT = synth.smoothed_noise(n, n, 1000)
+    v1, v2 = synth.smooth_velocity(n, n, 2000)
+    mR = ref.solve_state_final(v1, v2, 4, mT)
+    want = ref.estimate_eigs(mR, mT, 2, 1e-3, 0)
+    emin, emax = api.estimate_eigs(ctx, ctx.field(mR), ctx.field(mT), api.H2SEMI, 1e-3, api.COMPRESSIBLE)
+    assert emin == want[0] == 1.0
+    assert abs(emax - want[1]) <= 1e-9 * want[1], (emax, want)
