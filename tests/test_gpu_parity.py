@@ -410,3 +410,35 @@ def test_near_incompressible_vs_reference(ctx, api, ref, beta_w):
     finally:
         ref.set_penalty_weight(1e-1)
         ctx.set_penalty_weight(1e-1)
+
+
+@pytest.mark.parametrize("n1,n2,nt,deform", [(36, 52, 3, 0), (100, 64, 4, 1), (64, 200, 2, 0), (96, 1280, 2, 0),
+                                             (128, 8192, 2, 0), (8192, 128, 2, 0)])
+def test_hessian_irregular_grids_vs_reference(ctx, api, ref, n1, n2, nt, deform):
+    """GN matvec on rectangular grids off the fast paths, against the compiled reference:
+    axes that are not multiples of 16 (generic prefilter), n2 beyond the band kernels' 4096
+    (plain 3-kernel step), a band-path grid with 5 nodes per thread, and the 8192 limits of
+    the row and column prefilters; compressible and incompressible."""
+    mT = synth.smoothed_noise(n1, n2, 1000)
+    v1, v2 = synth.smooth_velocity(n1, n2, 2000)
+    vt1, vt2 = synth.smooth_velocity(n1, n2, 3000)
+    mR = ref.solve_state_final(v1, v2, nt, mT)
+    w1, w2 = 0.5 * v1, 0.5 * v2
+    e1, e2 = ref.Hessian(w1, w2, mR, mT, 2, 1e-3, deform, nt).apply(vt1, vt2)
+    H = api.HessianOperator(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT), api.H2SEMI, 1e-3,
+                            deform, nt)
+    assert H.band_path == (n2 % 256 == 0 and 256 <= n2 <= 4096 and n1 % 32 == 0)
+    # The data term (transport solves + body force, the hot path) to the north-star bar.  The
+    # full matvec adds beta A vt, which amplifies FFT rounding (~eps |vt|) by beta |k|^4 at the
+    # highest modes: 2.8e11 at n2 = 8192.  Two correct implementations with different FFTs
+    # (cuFFT, the reference's FFTW-API shim) then differ at that floor; the full matvec is held
+    # to max(bar, 10 x floor) in the relative l2 norm of SURVEY 8(d).
+    d1, d2 = ref.Hessian(w1, w2, mR, mT, 2, 1e-3, deform, nt).apply(vt1, vt2, data_only=True)
+    e = np.stack([e1, e2])
+    floor = 2.2e-16 * 1e-3 * ((n1 // 2) ** 2 + (n2 // 2) ** 2) ** 2 * np.linalg.norm([vt1, vt2]) / np.linalg.norm(e)
+    tol = max(TOL, 10 * floor)
+    for _ in range(2):
+        g1, g2 = H.apply_data_term((ctx.field(vt1), ctx.field(vt2)))
+        assert rel(g1, d1) < TOL and rel(g2, d2) < TOL
+        h = np.stack([x.cpu().numpy() for x in H.apply((ctx.field(vt1), ctx.field(vt2)))])
+        assert np.linalg.norm(h - e) / np.linalg.norm(e) < tol, (np.linalg.norm(h - e) / np.linalg.norm(e), tol)
