@@ -52,8 +52,13 @@ struct BandWindow {
     unsigned* err = nullptr;
 };
 
+#ifdef VRG_BAND_MINB  // experiment: more resident blocks per SM at fewer registers
+#define VRG_BAND_BOUNDS __launch_bounds__(kBandThreads, VRG_BAND_MINB)
+#else
+#define VRG_BAND_BOUNDS __launch_bounds__(kBandThreads)
+#endif
 template <class Epi, bool kGather, bool kWindow = false>
-__global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
+__global__ void VRG_BAND_BOUNDS k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
                                                             const double* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
                                                             BandWindow win = BandWindow{}) {
