@@ -236,6 +236,18 @@ int vrg_newton_solve(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, const
                      const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
                      double* summary);
 
+/* ---- external fine operator (the precond::LinOp plug-in point, precond.hpp:25, as used by
+ * solveKkt's split Hessian, precond.cpp:20-26,313).  While set, vrg_newton_solve does not build
+ * its own fine HessianOperator (newton.cpp:90-96): it calls build(user, v, nt) once per outer
+ * iteration (v = 2 contiguous device fields) and data_term(user, vt, b) per fine matvec
+ * (b = K[b(vt)], inverse.cpp:235-237, 2 contiguous device fields), on the context's stream;
+ * the spectral parts of the split operator, the preconditioner, gradient, objective and line
+ * search stay in the library.  A nonzero callback return fails the solve (VRG_RUNTIME_ERROR).
+ * Gauss-Newton, compressible, SL only.  Pass NULL callbacks to clear. */
+typedef int (*vrg_fine_build_fn)(void* user, const double* v, int nt);
+typedef int (*vrg_fine_data_term_fn)(void* user, const double* vt, double* b);
+int vrg_set_fine_operator(vrg_ctx_t ctx, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term, void* user);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,7 @@ _SIG = {
     "vrg_estimate_eigs": ("piippppididupp", C.c_int),
     "vrg_solve_kkt": ("pppdippppppdppp", C.c_int),
     "vrg_newton_solve": ("piippidipppppppip", C.c_int),
+    "vrg_set_fine_operator": ("pppp", C.c_int),
 }
 
 _KIND = {"p": C.c_void_p, "i": C.c_int, "d": C.c_double, "u": C.c_ulonglong}

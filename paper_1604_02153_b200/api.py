@@ -471,11 +471,19 @@ RECORD_FIELDS = ("iter", "gradNormInf", "gradNormRel", "objective", "mismatch", 
                  "lineSearchSteps", "stepLength", "searchDirDivRatio", "wallTimeSec", "ffts", "interps")
 
 
+FINE_BUILD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int)
+FINE_DATA_TERM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
 def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=0, ls_max_steps=20,
                  tol_rel=1e-2, tol_abs=1e-5, forcing_cap=0.5, ls_c1=1e-4, ls_shrink=0.5, grad_cfl=1.0,
                  kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10, eps_scale=0.1, eig=None,
-                 hessian_mode=GAUSS_NEWTON):
-    """inverse::newtonSolve on host images (numpy); returns (v1, v2, records, summary)."""
+                 hessian_mode=GAUSS_NEWTON, fine_operator=None):
+    """inverse::newtonSolve on host images (numpy); returns (v1, v2, records, summary).
+
+    fine_operator: an object with `callbacks()` -> (build, data_term) ctypes callbacks and an
+    `error` attribute (e.g. slab.SlabFineOperator); the solve then takes its fine GN data term
+    from it (C ABI vrg_set_fine_operator) and re-raises the callback's exception."""
     import numpy as np
 
     mR = np.ascontiguousarray(mR, dtype=np.float64)
@@ -488,9 +496,20 @@ def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inne
     rec = np.zeros((max_outer + 1, 12))
     summ = np.zeros(7)
     hp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
-    ctx.check(ctx.lib.vrg_newton_solve(ctx.h, n1, n2, hp(mR), hp(mT), norm, beta, deformation,
-                                       C.cast(ci, C.c_void_p), C.cast(cd, C.c_void_p), C.cast(pi, C.c_void_p),
-                                       C.cast(pd, C.c_void_p), hp(v1), hp(v2), hp(rec), max_outer + 1, hp(summ)))
+    if fine_operator is not None:
+        fb, fd = fine_operator.callbacks()
+        fine_operator.error = None
+        ctx.check(ctx.lib.vrg_set_fine_operator(ctx.h, C.cast(fb, C.c_void_p), C.cast(fd, C.c_void_p), None))
+    try:
+        code = ctx.lib.vrg_newton_solve(ctx.h, n1, n2, hp(mR), hp(mT), norm, beta, deformation,
+                                        C.cast(ci, C.c_void_p), C.cast(cd, C.c_void_p), C.cast(pi, C.c_void_p),
+                                        C.cast(pd, C.c_void_p), hp(v1), hp(v2), hp(rec), max_outer + 1, hp(summ))
+    finally:
+        if fine_operator is not None:
+            ctx.lib.vrg_set_fine_operator(ctx.h, None, None, None)
+    if fine_operator is not None and code and fine_operator.error is not None:
+        raise fine_operator.error
+    ctx.check(code)
     k = int(summ[1])
     records = [dict(zip(RECORD_FIELDS, row)) for row in rec[:k]]
     summary = dict(status=int(summ[0]), iterations=k, finalGradNormRel=summ[2], finalResidualRel=summ[3],

@@ -767,6 +767,17 @@ int vrg_solve_kkt(vrg_hess_t h, const double* rhs1, const double* rhs2, double t
     });
 }
 
+int vrg_set_fine_operator(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term, void* user) {
+    return guarded(c, [&] {
+        if (!c) throw vrg::InvalidArgument("null context");
+        if ((build == nullptr) != (data_term == nullptr))
+            throw vrg::InvalidArgument("external fine operator: give both callbacks or neither");
+        c->ctx.fine.build = build;
+        c->ctx.fine.dataTerm = data_term;
+        c->ctx.fine.user = build ? user : nullptr;
+    });
+}
+
 int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const double* mT_host, int norm, double beta,
                      int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
                      const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,

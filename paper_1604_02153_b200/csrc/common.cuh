@@ -168,6 +168,15 @@ struct Ctx {
     DBuf gridSync;  // grid-barrier state (count, generation) of cooperative kernels, zeroed at creation
     int coopPrefilterBlocks = -1;  // co-resident blocks of the cooperative prefilter (lazy)
     double* hostScalars = nullptr;  // pinned staging for scalar reads
+    // External fine-level GN data term for newtonSolve (C ABI vrg_set_fine_operator): the
+    // plug-in point of precond::LinOp (precond.hpp:25) that a slab-decomposed operator fills.
+    // build(v, nt) is called once per Newton iterate, dataTerm(vt, b) per matvec (2N fields,
+    // device pointers on this context's stream); nonzero return = failure.
+    struct FineHook {
+        int (*build)(void* user, const double* v, int nt) = nullptr;
+        int (*dataTerm)(void* user, const double* vt, double* b) = nullptr;
+        void* user = nullptr;
+    } fine;
 
     // Kernel launches issued by this library (cuFFT's own kernels are not counted), and an
     // optional per-tag CUDA-event profile of every launch site (bench.py roofline).

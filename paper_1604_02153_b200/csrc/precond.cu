@@ -602,27 +602,34 @@ KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int m
         if (choice.hasEig && !(choice.eMax > choice.eMin && choice.eMin > 0.0))
             throw InvalidArgument("solveKkt: need eMax > eMin > 0");
     }
-    const GridDims& g = hess.g;
+    const std::size_t N = hess.g.points();
+    LinOpDev A = [&](const double* s, double* o) { hess.applySplit(s, s + N, o, o + N); };
+    return solveKktOp(ctx, hess.g, hess.model, hess.weights, A, rhs, tol, maxIter, choice, mR, mT, v, coarseCfl,
+                      solution);
+}
+
+KktResult solveKktOp(Ctx& ctx, const GridDims& g, const Model& model, Weights& weights, const LinOpDev& A,
+                     const double* rhs, double tol, int maxIter, const PrecondChoice& choice, const double* mR,
+                     const double* mT, const double* v, double coarseCfl, double* solution) {
     const std::size_t N = g.points();
     const auto t0 = std::chrono::steady_clock::now();
     double precondTime = 0.0;
-    const double* invHalf = hess.weights.invRegSymbol(hess.model.betaV, -0.5);
+    const double* invHalf = weights.invRegSymbol(model.betaV, -0.5);
     double* rhsSplit = ctx.scratchBuf(140, sizeof(double) * 2 * N);
     double* x = ctx.scratchBuf(141, sizeof(double) * 2 * N);
     applyRealSymbol(ctx, g, rhs, rhs + N, rhsSplit, rhsSplit + N, invHalf);
-    LinOpDev A = [&](const double* s, double* o) { hess.applySplit(s, s + N, o, o + N); };
 
     std::unique_ptr<CoarseOperator> coarse;
     double eMin = 1.0, eMax = 10.0;
     LinOpDev M;
     if (choice.kind == kPcTwoLevel) {
-        coarse = std::make_unique<CoarseOperator>(ctx, g, v, mR, mT, hess.model, coarseCfl);
+        coarse = std::make_unique<CoarseOperator>(ctx, g, v, mR, mT, model, coarseCfl);
         if (choice.coarseSolver == kCoarseCheb) {
             if (choice.hasEig) {
                 eMin = choice.eMin;
                 eMax = choice.eMax;
             } else {
-                std::tie(eMin, eMax) = estimateEigsAt(ctx, g, nullptr, mR, mT, hess.model, coarseCfl);
+                std::tie(eMin, eMax) = estimateEigsAt(ctx, g, nullptr, mR, mT, model, coarseCfl);
             }
         }
         M = [&](const double* r, double* z) {
@@ -647,6 +654,42 @@ KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int m
     res.totalTimeSec = secondsSince(t0);
     res.precondTimeSec = precondTime;
     return res;
+}
+
+// ------------------------------------------------------------------------------ external fine operator
+ExternalFineOperator::ExternalFineOperator(Ctx& ctx, const GridDims& g, const double* v, const Model& model, int nt,
+                                           Weights& weights)
+    : ctx_(ctx), g_(g), model_(model), nt_(nt), weights_(weights) {
+    if (model.scheme != kSchemeSL || model.deformation != kCompressible)
+        throw NotSupported("external fine operator: compressible Gauss-Newton SL model only");
+    if (ctx.fine.build(ctx.fine.user, v, nt) != 0) throw std::runtime_error("external fine operator: build callback failed");
+    for (int batch = 1; batch <= 2; ++batch) {
+        ctx.plan(g, CUFFT_D2Z, batch);
+        ctx.plan(g, CUFFT_Z2D, batch);
+    }
+}
+
+// Hessian::launchSplit with the data term of the hook: t = M^{-1/2} s, b = Q t, o = M^{-1/2} b + s.
+void ExternalFineOperator::applySplit(const double* s, double* o) {
+    const std::size_t N = g_.points(), NS = g_.specPoints();
+    cplx* S = reinterpret_cast<cplx*>(ctx_.scratchBuf(150, sizeof(cplx) * 4 * NS));
+    cplx* T = S + 2 * NS;
+    double* t = ctx_.scratchBuf(151, sizeof(double) * 2 * N);
+    double* b = ctx_.scratchBuf(152, sizeof(double) * 2 * N);
+    const double* inv = weights_.invRegSymbol(model_.betaV, -0.5);
+    fftForward(ctx_, g_, s, S, 2);
+    specCombine(ctx_, g_, S, S + NS, nullptr, nullptr, inv, false, 1.0 / N, T, T + NS);
+    fftInverse(ctx_, g_, T, t, 2);
+    if (ctx_.fine.dataTerm(ctx_.fine.user, t, b) != 0)
+        throw std::runtime_error("external fine operator: data-term callback failed");
+    fftForward(ctx_, g_, b, T, 2);
+    specCombine(ctx_, g_, T, T + NS, S, S + NS, inv, false, 1.0 / N, T, T + NS);
+    fftInverse(ctx_, g_, T, o, 2);
+    // counters of one split matvec (Hessian::applySplit + countDataTerm, GN SL compressible)
+    ctx_.ffts += 8 + (3 + 3LL * nt_) + 3LL * (nt_ + 1) + lazyFfts_;
+    ctx_.interps += 4LL * nt_ + 2 + lazyInterps_;
+    lazyInterps_ = 0;
+    lazyFfts_ = 0;
 }
 
 // ------------------------------------------------------------------------------ Newton
@@ -717,14 +760,28 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
 
         const double eta = std::min(cfg.forcingCap, std::sqrt(grel));
         std::unique_ptr<PhaseTimer> ptH(new PhaseTimer(ctx, "Hessian ctor"));
-        Hessian hess(ctx, g, v, v + N, mR, mT, model, nt, state.d(), cfg.hessianMode,
-                     cfg.hessianMode == 1 ? adjoint.d() : nullptr);
+        // the fine operator: this library's Hessian, or the external (e.g. slab-decomposed) one
+        std::unique_ptr<Hessian> hess;
+        std::unique_ptr<ExternalFineOperator> ext;
+        if (ctx.fine.build) {
+            if (cfg.hessianMode != 0) throw NotSupported("external fine operator: Gauss-Newton mode only");
+            ext = std::make_unique<ExternalFineOperator>(ctx, g, v, model, nt, weights);
+        } else {
+            hess = std::make_unique<Hessian>(ctx, g, v, v + N, mR, mT, model, nt, state.d(), cfg.hessianMode,
+                                             cfg.hessianMode == 1 ? adjoint.d() : nullptr);
+        }
         ptH.reset();
         // rhs = -g
         lincomb(ctx, 2 * N, -1.0, gBuf.d(), 0.0, gBuf.d(), tmpBuf.d());
         std::unique_ptr<PhaseTimer> ptK(new PhaseTimer(ctx, "solveKkt"));
-        KktResult kkt = solveKkt(ctx, hess, tmpBuf.d(), eta, cfg.maxInnerIter, choice, mR, mT, v, kCoarseCfl,
-                                 dvBuf.d());
+        KktResult kkt;
+        if (ext) {
+            LinOpDev A = [&](const double* s, double* o) { ext->applySplit(s, o); };
+            kkt = solveKktOp(ctx, g, model, weights, A, tmpBuf.d(), eta, cfg.maxInnerIter, choice, mR, mT, v,
+                             kCoarseCfl, dvBuf.d());
+        } else {
+            kkt = solveKkt(ctx, *hess, tmpBuf.d(), eta, cfg.maxInnerIter, choice, mR, mT, v, kCoarseCfl, dvBuf.d());
+        }
         ptK.reset();
         rec.innerIterations = kkt.iterations;
         double* dv = dvBuf.d();

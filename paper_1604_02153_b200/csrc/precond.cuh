@@ -88,6 +88,28 @@ struct KktResult {
 // solveKkt (precond.cpp:291-358).  `solution` receives delta-v (2 contiguous fields).
 KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int maxIter, const PrecondChoice& choice,
                    const double* mR, const double* mT, const double* v, double coarseCfl, double* solution);
+// The same with the fine split operator A(s) = M^{-1/2} Q M^{-1/2} s + s given as a LinOp
+// (precond::LinOp, precond.hpp:25), M = beta A from `weights`.
+KktResult solveKktOp(Ctx& ctx, const GridDims& g, const Model& model, Weights& weights, const LinOpDev& A,
+                     const double* rhs, double tol, int maxIter, const PrecondChoice& choice, const double* mR,
+                     const double* mT, const double* v, double coarseCfl, double* solution);
+
+// Fine GN operator whose data term Q comes from Ctx::fine (an external, e.g. slab-decomposed,
+// implementation): applySplit mirrors Hessian::launchSplit's spectral steps around the hook and
+// bumps the reference's counters per matvec (Hessian::countDataTerm).
+class ExternalFineOperator {
+public:
+    ExternalFineOperator(Ctx& ctx, const GridDims& g, const double* v, const Model& model, int nt, Weights& weights);
+    void applySplit(const double* s, double* o);
+
+private:
+    Ctx& ctx_;
+    GridDims g_;
+    Model model_;
+    int nt_;
+    Weights& weights_;
+    long long lazyInterps_ = 5, lazyFfts_ = 3;  // charFwd + charBwd + dvDep, div v (state reused)
+};
 
 // inverse::newtonSolve (newton.cpp:24-159) ---------------------------------------------------
 struct NewtonConfig {

@@ -83,6 +83,14 @@ def test_distributed_reg_local():
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
+def test_local_allgather_rows():
+    v = _field(32, 24, 5)
+    comm = slab.LocalComm(4)
+    out = torch.empty_like(v)
+    comm.allgather_rows(list(v.split(8, dim=-2)), out)
+    assert torch.equal(out, v)
+
+
 def test_row_reach():
     n1, n2 = 16, 4
     h = 2 * np.pi / n1
@@ -112,6 +120,9 @@ def _worker(rank, world, port, q):
         assert torch.equal(buf, ex)
         reg = slab.distributed_reg(comm, [loc], n1, n2, 1, 1e-2)[0]
         m = comm.allreduce_max([torch.tensor([float(rank), -float(rank)])])[0]
+        gathered = torch.full_like(v, float("nan"))
+        comm.allgather_rows([loc], gathered)  # SlabFineOperator's b gather
+        assert torch.equal(gathered, v)
         # numpy copies: tensors would travel as shared-memory handles the exiting worker frees
         q.put((rank, ex.numpy().copy(), reg.numpy().copy(), m.tolist()))
     finally:
