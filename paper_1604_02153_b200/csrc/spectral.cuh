@@ -19,8 +19,6 @@ enum RegNorm : int { kH1 = 1, kH2 = 2, kH3 = 3 };
 struct Weights {
     GridDims g;
     int norm = kH2;
-    std::vector<double> gammaHost, gammaRegHost;  // half spectrum n1 x (n2/2+1)
-    DBuf gamma;
     std::map<double, DBuf> regSymbols;                  // beta -> beta*gamma
     std::map<std::pair<double, double>, DBuf> symbols;  // (beta, power) -> (beta*gammaReg)^power
     Weights(const GridDims& g, int norm);
@@ -28,6 +26,9 @@ struct Weights {
     const double* regSymbol(double beta);
     // (beta*gammaReg)^power (applyInvReg)
     const double* invRegSymbol(double beta, double power);
+
+private:
+    const double* makeSymbol(int kind, double beta, double power, DBuf& b);
 };
 
 using cplx = double2;
