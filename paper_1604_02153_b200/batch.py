@@ -125,6 +125,33 @@ def registration_runner(ctx, n: int, nt: int, beta: float, norm: int, cheb_iters
     return run
 
 
+def _reference_batch(a, images, rank, world):
+    """The same pairs through the reference's own newtonSolve on host threads (CPU baseline of
+    configs 3/5b): one single-threaded solve per thread, threads in parallel (the reference's
+    solves are reentrant, proj/README.md:157-158; ctypes releases the GIL).  Images as for
+    the GPU arm (m_R transported on the device, bit-compatible with the reference's)."""
+    from oracle import ref
+
+    threads = a.threads or os.cpu_count() or 1
+
+    def make_runner(_lane):
+        def run(p):
+            mR, mT = images[p]
+            t0 = time.perf_counter()
+            _, _, rep, rs = ref.newton_solve(mR, mT, a.norm, a.beta, 0, nt=a.nt, two_level=True, cheb=True,
+                                             cheb_iters=a.cheb, tol_rel=a.tol_rel)
+            return {"seconds": time.perf_counter() - t0, "newton_iterations": int(rs[1]),
+                    "inner_iterations": int(sum(int(q[5]) for q in rep[:int(rs[1])]))}
+        return run
+
+    t0 = time.perf_counter()
+    res = run_lanes(sorted(images), make_runner, threads)
+    wall = time.perf_counter() - t0
+    if rank == 0:
+        print(json.dumps({"impl": "reference", "pairs": len(images), "n": a.n, "nt": a.nt, "world": world,
+                          "threads": threads, "wall_s": wall, "pairs_per_s": len(images) / wall, "results": res}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=512)
@@ -136,6 +163,9 @@ def main():
     ap.add_argument("--tol-rel", type=float, default=1e-2)
     ap.add_argument("--lanes", type=int, default=1, help="concurrent solves per GPU (own context + stream each)")
     ap.add_argument("--passes", type=int, default=1, help="passes over the pairs; the last one is reported")
+    ap.add_argument("--impl", default="vrg", choices=["vrg", "reference"],
+                    help="reference: the unmodified reference's newtonSolve (oracle/_ref) on --threads host threads")
+    ap.add_argument("--threads", type=int, default=0, help="host threads of --impl reference (0: all)")
     a = ap.parse_args()
     import torch
 
@@ -152,6 +182,8 @@ def main():
     # pass over the same pairs (plans, graphs and the block cache warm)
     main_ctx = api.Context(local)
     images = {p: make_images(main_ctx, a.n, p, a.nt) for p in shard(a.pairs, rank, world)}
+    if a.impl == "reference":
+        return _reference_batch(a, images, rank, world)
     ctxs = [main_ctx] + [api.Context(local, stream=torch.cuda.Stream(local)) for _ in range(1, a.lanes)]
 
     def make_runner(lane: int):
