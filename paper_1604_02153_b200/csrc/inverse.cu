@@ -1030,6 +1030,11 @@ double Hessian::benchKernel(int id, int iters) {
                                                    EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
                 launchPrefilterCols(ctx, g, tmp, coef);
                 break;
+            case 12:  // the band kernel of the SL state step alone (no column pass)
+                if (!solver.bandPath()) throw NotSupported("bench kernel 12: band path not active on this grid");
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N,
+                                                   EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
+                break;
             case 10:  // SL state step, plain form: prefilter (rows + cols) + gather
                 launchPrefilter(ctx, g, mt, coef, tmp, nullptr);
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, EpiStateStep{adjLog_.partial(0), mt + N}, true);
