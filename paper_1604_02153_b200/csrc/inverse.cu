@@ -947,6 +947,52 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
     }
 }
 
+void Hessian::beginDeferredGuards(int maxCalls) {
+    if (heun_ || mode_ == 1 || maxCalls <= 0) return;  // those paths check as they run / differently
+    const std::size_t per = static_cast<std::size_t>(nt + 1);
+    if (maxCalls > deferCap_) {
+        deferMax_.alloc(sizeof(double) * per * maxCalls);
+        deferFlags_.alloc(sizeof(unsigned) * per * maxCalls);
+        deferCap_ = maxCalls;
+    }
+    deferring_ = true;
+    deferCount_ = 0;
+}
+
+void Hessian::endDeferredGuards() {
+    if (!deferring_) return;
+    deferring_ = false;
+    const int k = deferCount_;
+    if (k == 0) return;
+    const std::size_t per = static_cast<std::size_t>(nt + 1);
+    std::vector<double> mx(per * k);
+    std::vector<unsigned> fl(per * k);
+    VRG_CUDA(cudaMemcpyAsync(mx.data(), deferMax_.d(), sizeof(double) * per * k, cudaMemcpyDeviceToHost, ctx.stream));
+    VRG_CUDA(cudaMemcpyAsync(fl.data(), deferFlags_.d(), sizeof(unsigned) * per * k, cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    ctx.sync();
+    for (int c = 0; c < k; ++c)
+        GuardLog::checkHost(mx.data() + c * per, fl.data() + c * per, "adjoint", nt, false, true, nt);
+}
+
+void Hessian::guardAfterMatvec() {
+    if (!deferring_) {
+        checkLastGuard();
+        return;
+    }
+    if (deferCount_ >= deferCap_) {  // log full: check what is there, then continue immediately
+        endDeferredGuards();
+        checkLastGuard();
+        return;
+    }
+    const std::size_t per = static_cast<std::size_t>(nt + 1);
+    VRG_CUDA(cudaMemcpyAsync(deferMax_.d() + per * deferCount_, adjLog_.stepMax.d(), sizeof(double) * per,
+                             cudaMemcpyDeviceToDevice, ctx.stream));
+    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + per * deferCount_, adjLog_.flags.d(),
+                             sizeof(unsigned) * per, cudaMemcpyDeviceToDevice, ctx.stream));
+    ++deferCount_;
+}
+
 void Hessian::checkLastGuard() {
     if (heun_) return;  // the Heun solves checked their guards as they ran
     if (mode_ == 1) {  // full Newton: no guard in the incremental solves, prefilter input checks only
@@ -1236,7 +1282,7 @@ void Hessian::applySplit(const double* s1, const double* s2, double* o1, double*
     replay(2, s1, s2, o1, o2, [&] { launchSplit(s1, s2, o1, o2); });
     ctx.ffts += 8;
     countDataTerm();
-    checkLastGuard();
+    guardAfterMatvec();
 }
 
 void Hessian::launchSplit(const double* s1, const double* s2, double* o1, double* o2) {

@@ -58,6 +58,13 @@ public:
     double benchKernel(int id, int iters);
     // device-visible guard check result of the last data term (throws like solveAdjoint).
     void checkLastGuard();
+    // Deferred guard checks for a device-resident loop of matvecs (the coarse Chebyshev
+    // solve): between begin and end, each matvec appends its per-step guard maxima and flags
+    // to a device log instead of synchronising; endDeferredGuards() reads the log once and
+    // throws the first error in call order (the one the reference would have thrown).  GN SL
+    // operators only; otherwise the checks stay immediate.
+    void beginDeferredGuards(int maxCalls);
+    void endDeferredGuards();
     // counter increments of one data term in the reference (steady state)
     void countDataTerm();
 
@@ -90,6 +97,10 @@ private:
     DBuf work_;   // vtD (2N), mt ping-pong (2N), lam ping-pong (2N), b (2N), coef2 (N), reg (2N)
     DBuf spec_;   // 4 half spectra
     GuardLog adjLog_;
+    bool deferring_ = false;
+    int deferCap_ = 0, deferCount_ = 0;
+    DBuf deferMax_, deferFlags_;
+    void guardAfterMatvec();
     long long lazyInterps_ = 0, lazyFfts_ = 0;
     bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh
     int mode_ = 0;        // 1: full Newton

@@ -534,13 +534,28 @@ double lanczosEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, s
     return tridiagMaxEig(alpha, beta);
 }
 
+// Lanczos on the coarse split operator with its guard checks deferred: a step then needs one
+// host read (beta) instead of two; the first guard violation is thrown at the end, in order.
+double coarseLanczosEmax(Ctx& ctx, CoarseOperator& coarse, int steps, std::uint64_t seed) {
+    LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
+    coarse.hess->beginDeferredGuards(steps + 1);
+    double e;
+    try {
+        e = lanczosEmax(ctx, coarse.gc, op, steps, seed);
+    } catch (...) {
+        coarse.hess->endDeferredGuards();
+        throw;
+    }
+    coarse.hess->endDeferredGuards();
+    return e;
+}
+
 std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const double* v, const double* mR,
                                          const double* mT, const Model& model, double coarseCfl, std::uint64_t seed) {
     std::unique_ptr<PhaseTimer> pt(new PhaseTimer(ctx, "eigs: coarse setup"));
     CoarseOperator coarse(ctx, g, v, mR, mT, model, coarseCfl);
     pt.reset(new PhaseTimer(ctx, "eigs: lanczos(30)"));
-    LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
-    return {1.0, lanczosEmax(ctx, coarse.gc, op, 30, seed)};
+    return {1.0, coarseLanczosEmax(ctx, coarse, 30, seed)};
 }
 
 // ------------------------------------------------------------------------------ two-level
@@ -565,7 +580,16 @@ bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator&
     }
     LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
     if (choice.coarseSolver == kCoarseCheb) {
-        chebyshevSolve(ctx, gc, op, rc, choice.chebIters, eMin, kEmaxInflation * eMax, sc);
+        // the Chebyshev loop has no host decisions: its coarse matvecs run back to back on the
+        // stream and their guards are checked once at the end, in order
+        coarse.hess->beginDeferredGuards(choice.chebIters);
+        try {
+            chebyshevSolve(ctx, gc, op, rc, choice.chebIters, eMin, kEmaxInflation * eMax, sc);
+        } catch (...) {
+            coarse.hess->endDeferredGuards();
+            throw;
+        }
+        coarse.hess->endDeferredGuards();
     } else {
         pcg(ctx, gc, op, rc, nullptr, choice.epsScale * outerTol, 500, sc);
     }
@@ -640,8 +664,7 @@ KktResult solveKktOp(Ctx& ctx, const GridDims& g, const Model& model, Weights& w
     }
     PcgOut out = pcg(ctx, g, A, rhsSplit, M ? &M : nullptr, tol, maxIter, x);
     if (out.indefinitePreconditioner && choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb) {
-        LinOpDev op = [&](const double* s, double* o) { coarse->applySplit(s, o); };
-        eMax = lanczosEmax(ctx, coarse->gc, op, 30, 0x5eed);
+        eMax = coarseLanczosEmax(ctx, *coarse, 30, 0x5eed);
         std::fprintf(stderr, "precond: re-estimated Chebyshev bound eMax=%.6g after breakdown\n", eMax);
         out = pcg(ctx, g, A, rhsSplit, &M, tol, maxIter, x);
     }

@@ -104,6 +104,11 @@ void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard,
     VRG_CUDA(cudaMemcpyAsync(mx.data(), stepMax.d(), sizeof(double) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
     VRG_CUDA(cudaMemcpyAsync(fl.data(), flags.d(), sizeof(unsigned) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
+    checkHost(mx.data(), fl.data(), eq, nt, forward, guard, thresholdStep);
+}
+
+void GuardLog::checkHost(const double* mx, const unsigned* fl, const char* eq, int nt, bool forward, bool guard,
+                         int thresholdStep) {
     const double threshold = kBlowupFactor * mx[thresholdStep];
     for (int s = 1; s <= nt; ++s) {
         const int j = forward ? s : nt + 1 - s;    // step label (transport.cpp:221, 235)

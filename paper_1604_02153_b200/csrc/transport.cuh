@@ -38,6 +38,9 @@ struct GuardLog {
     // Host readback; throws the reference's first error in solve order.
     //   order: steps visited, each (prefilter-input step index, output step index).
     void check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep);
+    // The same decisions on host copies of stepMax / flags (deferred checks).
+    static void checkHost(const double* mx, const unsigned* fl, const char* eq, int nt, bool forward, bool guard,
+                          int thresholdStep);
 };
 
 class Solver {
