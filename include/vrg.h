@@ -126,6 +126,12 @@ int vrg_project_div_free(vrg_ctx_t ctx, int n1, int n2, const double* b1, const 
 int vrg_resample(vrg_ctx_t ctx, int n1, int n2, const double* u, int t1, int t2, double* out);
 int vrg_cutoff(vrg_ctx_t ctx, int n1, int n2, const double* u, int band, double* out);
 int vrg_gaussian_smooth(vrg_ctx_t ctx, int n1, int n2, const double* u, double sigma, double* out);
+/* applyHelmholtz (spectral.hpp:56, spectral.cpp:214-223): (1 - Lap) u, Nyquist-zeroed waves */
+int vrg_apply_helmholtz(vrg_ctx_t ctx, int n1, int n2, const double* u, double* out);
+/* assembleBodyForce, SL scheme (inverse.cpp:50-65): b = sum_j w_j lambda_j grad m_j, trapezoid
+ * weights ht/2 at the ends, ht inside; state_traj / adj_traj = (nt+1) contiguous fields each */
+int vrg_body_force(vrg_ctx_t ctx, int n1, int n2, int nt, const double* state_traj, const double* adj_traj,
+                   double* b1, double* b2);
 
 /* ---- inverse (inverse.hpp:60-105) ---- */
 /* inverse::HessianOperator(v, problem, model, tg, cfg{SL}, mode, state) (inverse.hpp:74-80).

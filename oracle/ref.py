@@ -215,6 +215,13 @@ def cutoff(u, high):
     return out
 
 
+def apply_helmholtz(u):
+    u = _c(u)
+    out = np.empty_like(u)
+    _check(lib().ref_apply_helmholtz(u.shape[0], u.shape[1], _p(u), _p(out)))
+    return out
+
+
 def gaussian_smooth(u, sigma):
     u = _c(u)
     out = np.empty_like(u)

@@ -272,6 +272,10 @@ int ref_cutoff(int n1, int n2, const double* u, int high, double* out) {
     });
 }
 
+int ref_apply_helmholtz(int n1, int n2, const double* u, double* out) {
+    return guarded([&] { put(spectral::applyHelmholtz(sf(n1, n2, u)), out); });
+}
+
 int ref_gaussian_smooth(int n1, int n2, const double* u, double sigma, double* out) {
     return guarded([&] { put(spectral::gaussianSmooth(sf(n1, n2, u), sigma), out); });
 }

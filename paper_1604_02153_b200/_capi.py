@@ -56,6 +56,8 @@ _SIG = {
     "vrg_solver_jacobian": ("pp", C.c_int),
     "vrg_solver_departure": ("pipp", C.c_int),
     "vrg_gradient": ("piippp", C.c_int),
+    "vrg_apply_helmholtz": ("piipp", C.c_int),
+    "vrg_body_force": ("piiipppp", C.c_int),
     "vrg_divergence": ("piippp", C.c_int),
     "vrg_apply_reg": ("piiidpppp", C.c_int),
     "vrg_apply_inv_reg": ("piiiddpppp", C.c_int),

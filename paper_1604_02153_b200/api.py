@@ -177,6 +177,26 @@ def gradient(ctx, u):
     return g[0], g[1]
 
 
+def apply_helmholtz(ctx, u):
+    """spectral::applyHelmholtz (spectral.cpp:214-223): (1 - Laplacian) u."""
+    n1, n2 = _shape(u)
+    out = ctx.empty(n1, n2)
+    ctx.check(ctx.lib.vrg_apply_helmholtz(ctx.h, n1, n2, _p(u), _p(out)))
+    return out
+
+
+def body_force(ctx, state, adjoint):
+    """assembleBodyForce, SL (inverse.cpp:50-65): trajectories (nt+1, n1, n2) -> (b1, b2)."""
+    if tuple(state.shape) != tuple(adjoint.shape):
+        raise InvalidArgument("assembleBodyForce: trajectory length mismatch")
+    nt = int(state.shape[0]) - 1
+    n1, n2 = _shape(state)
+    b = ctx.empty(2, n1, n2)
+    ctx.check(ctx.lib.vrg_body_force(ctx.h, n1, n2, nt, _p(state.contiguous()), _p(adjoint.contiguous()), _p(b[0]),
+                                     _p(b[1])))
+    return b[0], b[1]
+
+
 def divergence(ctx, v):
     n1, n2 = _shape(v[0])
     out = ctx.empty(n1, n2)

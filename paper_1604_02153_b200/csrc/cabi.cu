@@ -419,6 +419,22 @@ int vrg_gradient(vrg_ctx_t c, int n1, int n2, const double* u, double* g1, doubl
     });
 }
 
+int vrg_apply_helmholtz(vrg_ctx_t c, int n1, int n2, const double* u, double* out) {
+    return guarded(c, [&] {
+        vrg::applyHelmholtz(c->ctx, dims(n1, n2), u, out);
+        c->ctx.sync();
+    });
+}
+
+int vrg_body_force(vrg_ctx_t c, int n1, int n2, int nt, const double* state_traj, const double* adj_traj, double* b1,
+                   double* b2) {
+    return guarded(c, [&] {
+        if (nt < 1) throw vrg::InvalidArgument("assembleBodyForce: trajectory length mismatch");
+        vrg::bodyForce(c->ctx, dims(n1, n2), nt, state_traj, adj_traj, b1, b2);
+        c->ctx.sync();
+    });
+}
+
 int vrg_divergence(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, double* out) {
     return guarded(c, [&] {
         vrg::divergence(c->ctx, dims(n1, n2), v1, v2, out);

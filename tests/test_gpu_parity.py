@@ -126,6 +126,27 @@ def test_gradient_closed_form(ctx, api):
     assert np.abs(g2.cpu().numpy() + 2 * np.sin(X1) * np.sin(2 * X2)).max() < 1e-12
 
 
+def test_helmholtz_and_body_force(ctx, api, ref):
+    # applyHelmholtz (spectral.cpp:214-223) against the compiled reference and in closed form;
+    # assembleBodyForce SL (inverse.cpp:50-65) against the restatement, with its FFT count
+    for shape in ((48, 32), (64, 64)):
+        u = synth.smooth_scalar(*shape, 7)
+        assert rel(api.apply_helmholtz(ctx, ctx.field(u)), ref.apply_helmholtz(u)) < 1e-13
+    X1, X2 = O.coords((64, 64))
+    u = np.sin(X1) * np.cos(2 * X2)
+    assert np.abs(api.apply_helmholtz(ctx, ctx.field(u)).cpu().numpy() - 6 * u).max() < 1e-12
+    nt, shape = 4, (48, 32)
+    st = np.stack([synth.smooth_scalar(*shape, 100 + j) for j in range(nt + 1)])
+    ad = np.stack([synth.smooth_scalar(*shape, 200 + j) for j in range(nt + 1)])
+    ctx.reset_counters()
+    b1, b2 = api.body_force(ctx, ctx.field(st), ctx.field(ad))
+    assert ctx.counters() == (3 * (nt + 1), 0)
+    e1, e2 = O.body_force(st, ad, 1.0 / nt)
+    assert rel(b1, e1) < 1e-13 and rel(b2, e2) < 1e-13
+    with pytest.raises(api.InvalidArgument):
+        api.body_force(ctx, ctx.field(st), ctx.field(ad[:nt]))
+
+
 # ------------------------------------------------------------------ transport (K3-K6)
 def _cfg1(ctx):
     d = gold("cfg1_64")
