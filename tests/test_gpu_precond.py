@@ -143,3 +143,38 @@ def test_estimate_eigs_vs_reference_sizes(ctx, api, ref, n):
     emin, emax = api.estimate_eigs(ctx, ctx.field(mR), ctx.field(mT), api.H2SEMI, 1e-3, api.COMPRESSIBLE)
     assert emin == want[0] == 1.0
     assert abs(emax - want[1]) <= 1e-9 * want[1], (emax, want)
+
+
+@pytest.mark.parametrize("amp", [4.0, 8.0, 14.0])
+def test_two_level_cheb_guard_matches_reference(ctx, api, ref, amp):
+    """A strongly compressive velocity makes the coarse GN adjoint exceed the blow-up guard
+    inside the Chebyshev coarse solve.  The device path defers the guard checks of the
+    Chebyshev loop to its end (Hessian::beginDeferredGuards); it must raise the reference's
+    error (type, message, step index) at the same matvec, or succeed where it succeeds."""
+    from paper_1604_02153_b200 import synth
+
+    n = 64
+    X1, X2 = np.meshgrid(np.linspace(-np.pi, np.pi, n, endpoint=False),
+                         np.linspace(-np.pi, np.pi, n, endpoint=False), indexing="ij")
+    v1, v2 = amp * np.sin(X1), 0.5 * amp * np.sin(X2)
+    mT = synth.smoothed_noise(n, n, 5)
+    mR = synth.smoothed_noise(n, n, 6)
+    r1, r2 = synth.smooth_velocity(n, n, 3000)
+    emin, emax = 1.0, 50.0
+    rc = ref.Coarse(v1, v2, mR, mT, 2, 1e-2, 0)
+    try:
+        e1, e2 = rc.two_level(r1, r2, True, 10, 0.1, 0.5, emin, emax)
+        ref_err = None
+    except ref.RefError as e:
+        ref_err = e
+    assert (ref_err is None) == (amp < 5), ref_err  # 8, 14: guard exceeded at steps 2 and 8
+    F = ctx.field
+    c = api.CoarseOperator(ctx, (F(v1), F(v2)), F(mR), F(mT), api.H2SEMI, 1e-2, api.COMPRESSIBLE)
+    if ref_err is None:
+        (o1, o2), _ = c.two_level((F(r1), F(r2)), api.COARSE_CHEB, 10, 0.1, 0.5, emin, emax)
+        assert rel(o1, e1) < 1e-8 and rel(o2, e2) < 1e-8
+    else:
+        assert ref_err.code == 2, ref_err
+        with pytest.raises(api.BlowupError) as ei:
+            c.two_level((F(r1), F(r2)), api.COARSE_CHEB, 10, 0.1, 0.5, emin, emax)
+        assert str(ei.value) == str(ref_err), (str(ei.value), str(ref_err))
