@@ -11,7 +11,7 @@ library's per-call state is per context (plans, graphs, scratch) or thread-local
 newton_solve is a single C call that releases the GIL.
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-        -m paper_1604_02153_b200.batch --n 512 --pairs 8 --nt 16
+        -m paper_1604_02153_b200.batch --size 512 --pairs 8 --nt 16   (--size, not --n: torchrun rejects --n as an ambiguous abbreviation of its own options)
 """
 from __future__ import annotations
 
@@ -154,7 +154,7 @@ def _reference_batch(a, images, rank, world):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=512)
     ap.add_argument("--pairs", type=int, default=8)
     ap.add_argument("--nt", type=int, default=16)
     ap.add_argument("--beta", type=float, default=1e-3)

@@ -1,7 +1,7 @@
 """Slab-decomposed GN Hessian matvec (config 5a: 4096^2, nt=32, H2 beta=1e-4) over NCCL.
 
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
-      --master-port 29512 tools/slab_bench.py [--n 4096] [--nt 32] [--steps 5]
+      --master-port 29512 tools/slab_bench.py [--size 4096] [--nt 32] [--steps 5]
 
 Every rank builds its slab of the per-iterate invariants (SlabHessian.build: distributed
 setup; --setup replicated slices the single-device operator instead), and times K slab
@@ -25,7 +25,7 @@ from paper_1604_02153_b200 import api, slab, synth
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=4096)
     ap.add_argument("--nt", type=int, default=32)
     ap.add_argument("--beta", type=float, default=1e-4)
     ap.add_argument("--steps", type=int, default=5)

@@ -30,7 +30,7 @@ from paper_1604_02153_b200 import api, slab, synth
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=4096)
     ap.add_argument("--nt", type=int, default=32)
     ap.add_argument("--beta", type=float, default=1e-4)
     ap.add_argument("--mode", default="single", choices=["single", "slab"])
