@@ -591,7 +591,16 @@ bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator&
         }
         coarse.hess->endDeferredGuards();
     } else {
-        pcg(ctx, gc, op, rc, nullptr, choice.epsScale * outerTol, 500, sc);
+        // the coarse PCG reads its scalars once per iteration; the matvecs' guard checks ride
+        // on those reads instead of adding a sync each (checked in order at the end)
+        coarse.hess->beginDeferredGuards(500);
+        try {
+            pcg(ctx, gc, op, rc, nullptr, choice.epsScale * outerTol, 500, sc);
+        } catch (...) {
+            coarse.hess->endDeferredGuards();
+            throw;
+        }
+        coarse.hess->endDeferredGuards();
     }
     // reference counting: cutoff Low/High (8 FFTs) + restrict (4); prolong (4) below
     ctx.ffts += 12;

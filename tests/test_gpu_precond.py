@@ -145,11 +145,12 @@ def test_estimate_eigs_vs_reference_sizes(ctx, api, ref, n):
     assert abs(emax - want[1]) <= 1e-9 * want[1], (emax, want)
 
 
+@pytest.mark.parametrize("cheb", [True, False])
 @pytest.mark.parametrize("amp", [4.0, 8.0, 14.0])
-def test_two_level_cheb_guard_matches_reference(ctx, api, ref, amp):
+def test_two_level_cheb_guard_matches_reference(ctx, api, ref, amp, cheb):
     """A strongly compressive velocity makes the coarse GN adjoint exceed the blow-up guard
     inside the Chebyshev coarse solve.  The device path defers the guard checks of the
-    Chebyshev loop to its end (Hessian::beginDeferredGuards); it must raise the reference's
+    Chebyshev loop (and of the coarse PCG) to its end (Hessian::beginDeferredGuards); it must raise the reference's
     error (type, message, step index) at the same matvec, or succeed where it succeeds."""
     from paper_1604_02153_b200 import synth
 
@@ -163,7 +164,7 @@ def test_two_level_cheb_guard_matches_reference(ctx, api, ref, amp):
     emin, emax = 1.0, 50.0
     rc = ref.Coarse(v1, v2, mR, mT, 2, 1e-2, 0)
     try:
-        e1, e2 = rc.two_level(r1, r2, True, 10, 0.1, 0.5, emin, emax)
+        e1, e2 = rc.two_level(r1, r2, cheb, 10, 0.1, 0.5, emin, emax)
         ref_err = None
     except ref.RefError as e:
         ref_err = e
@@ -171,10 +172,11 @@ def test_two_level_cheb_guard_matches_reference(ctx, api, ref, amp):
     F = ctx.field
     c = api.CoarseOperator(ctx, (F(v1), F(v2)), F(mR), F(mT), api.H2SEMI, 1e-2, api.COMPRESSIBLE)
     if ref_err is None:
-        (o1, o2), _ = c.two_level((F(r1), F(r2)), api.COARSE_CHEB, 10, 0.1, 0.5, emin, emax)
+        (o1, o2), _ = c.two_level((F(r1), F(r2)), api.COARSE_CHEB if cheb else api.COARSE_PCG, 10, 0.1, 0.5, emin,
+                                  emax)
         assert rel(o1, e1) < 1e-8 and rel(o2, e2) < 1e-8
     else:
         assert ref_err.code == 2, ref_err
         with pytest.raises(api.BlowupError) as ei:
-            c.two_level((F(r1), F(r2)), api.COARSE_CHEB, 10, 0.1, 0.5, emin, emax)
+            c.two_level((F(r1), F(r2)), api.COARSE_CHEB if cheb else api.COARSE_PCG, 10, 0.1, 0.5, emin, emax)
         assert str(ei.value) == str(ref_err), (str(ei.value), str(ref_err))
