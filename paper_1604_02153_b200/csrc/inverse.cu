@@ -325,7 +325,8 @@ __global__ void k_add2(std::size_t N, const double* __restrict__ a1, const doubl
 }  // namespace
 
 Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2, const double* mR, const double* mT,
-                 const Model& mdl, int steps, const double* stateTraj, int hmode, const double* adjTraj)
+                 const Model& mdl, int steps, const double* stateTraj, int hmode, const double* adjTraj,
+                 const double* gradTraj)
     : ctx(c), g(gd), model(mdl), nt(steps), solver(c, gd, v1, v2, steps), weights(gd, mdl.norm), mode_(hmode) {
     if (!(mdl.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
     const std::size_t N = g.points();
@@ -346,7 +347,13 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     const bool hadFwd = !stateTraj;
     G_.alloc(sizeof(double) * (nt + 1) * 2 * N);
     GD_.alloc(sizeof(double) * nt * 2 * N);
-    for (int j = 0; j <= nt; ++j) gradient(ctx, g, state_.d() + j * N, G_.d() + j * 2 * N, G_.d() + j * 2 * N + N);
+    if (gradTraj && stateTraj) {  // grad m_j of this state, computed by the gradient evaluation (same kernels)
+        VRG_CUDA(cudaMemcpyAsync(G_.d(), gradTraj, sizeof(double) * (nt + 1) * 2 * N, cudaMemcpyDeviceToDevice,
+                                 ctx.stream));
+    } else {
+        for (int j = 0; j <= nt; ++j)
+            gradient(ctx, g, state_.d() + j * N, G_.d() + j * 2 * N, G_.d() + j * 2 * N + N);
+    }
     const double* Xf = solver.departure(kForward);
     work_.alloc(sizeof(double) * (11 * N + paddedPoints(g.n1, g.n2)));
     double* c2 = work_.d() + 11 * N;
@@ -1328,14 +1335,15 @@ __global__ void k_bf_accum(std::size_t N, double w, const double* __restrict__ l
 
 // assembleBodyForce SL (src/inverse.cpp:58-64): b = sum_j w_j lam_j grad m_j.
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
-               double* b2) {
+               double* b2, double* gradTrajOut) {
     const std::size_t N = g.points();
     const double ht = 1.0 / nt;
-    double* gm = ctx.scratchBuf(20, sizeof(double) * 2 * N);
+    double* scratch = gradTrajOut ? nullptr : ctx.scratchBuf(20, sizeof(double) * 2 * N);
     fill(ctx, N, 0.0, b1);
     fill(ctx, N, 0.0, b2);
     for (int j = 0; j <= nt; ++j) {
         const double w = ht * ((j == 0 || j == nt) ? 0.5 : 1.0);
+        double* gm = gradTrajOut ? gradTrajOut + static_cast<std::size_t>(j) * 2 * N : scratch;
         gradient(ctx, g, stateTraj + j * N, gm, gm + N);
         {
             LaunchScope ls_(ctx, "k_bf_accum");
@@ -1381,7 +1389,7 @@ void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const doub
 
 void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
-                      double* stateOut, double* adjOut, const double* reuseState) {
+                      double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut) {
     const std::size_t N = g.points();
     DBuf stBuf, adBuf;
     double* st = stateOut;
@@ -1425,7 +1433,7 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
         mismatch = 0.5 * dot(ctx, g, resid, nullptr, resid, nullptr);
         lincomb(ctx, N, -1.0, resid, 0.0, resid, resid);  // lambda1 = -1.0 * resid
         solver.adjoint(resid, ad, true);
-        bodyForce(ctx, g, nt, st, ad, b, b + N);
+        bodyForce(ctx, g, nt, st, ad, b, b + N, gradTrajOut);
     }
     Weights w(g, model.norm);
     if (!(model.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");

@@ -31,7 +31,8 @@ public:
     // hmode: 0 Gauss-Newton, 1 full Newton (HessianMode, transport.hpp; the full-Newton
     // operator solves the adjoint in the ctor, inverse.cpp:164-172)
     Hessian(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR, const double* mT,
-            const Model& model, int nt, const double* stateTraj, int hmode = 0, const double* adjTraj = nullptr);
+            const Model& model, int nt, const double* stateTraj, int hmode = 0, const double* adjTraj = nullptr,
+            const double* gradTraj = nullptr);  // gradTraj: grad m_j of stateTraj ((nt+1) x 2N), reused
 
     Ctx& ctx;
     GridDims g;
@@ -149,11 +150,11 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
               double* rowOut, double* guardPartials, unsigned* flag, unsigned* winErr);
 
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
-               double* b2);
+               double* b2, double* gradTrajOut = nullptr);  // gradTrajOut: keeps grad m_j ((nt+1) x 2N)
 void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                        const double* mT, const Model& model, int nt, double* scalars, double* stateOut);
 void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
-                      double* stateOut, double* adjOut, const double* reuseState);
+                      double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut = nullptr);
 
 }  // namespace vrg

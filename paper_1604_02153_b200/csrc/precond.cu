@@ -748,7 +748,7 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
     double g0inf = 0.0;
     int ntRatchet = 0;
     int carriedNt = -1;
-    DBuf carried, state, adjoint;
+    DBuf carried, state, adjoint, grads;
     DBuf finalDeformed(sizeof(double) * N);
     copy(ctx, N, mT, finalDeformed.d());
     double scal[3];
@@ -760,11 +760,14 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
         const int nt = ntRatchet;
         state.alloc(sizeof(double) * (nt + 1) * N);
         adjoint.alloc(sizeof(double) * (nt + 1) * N);
+        // grad m_j of the gradient's state, reused by the GN SL Hessian of this iterate
+        const bool keepGrads = model.scheme == kSchemeSL && cfg.hessianMode == 0 && !ctx.fine.build;
+        if (keepGrads) grads.alloc(sizeof(double) * (nt + 1) * 2 * N);
         const bool reuse = carriedNt == nt;
         {
             PhaseTimer pt(ctx, "evaluateGradient");
             evaluateGradient(ctx, g, v, v + N, mR, mT, model, nt, gBuf.d(), gBuf.d() + N, scal, state.d(),
-                             adjoint.d(), reuse ? carried.d() : nullptr);
+                             adjoint.d(), reuse ? carried.d() : nullptr, keepGrads ? grads.d() : nullptr);
         }
         const double objective = scal[0], mismatch = scal[1];
         copy(ctx, N, state.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
@@ -800,7 +803,8 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
             ext = std::make_unique<ExternalFineOperator>(ctx, g, v, model, nt, weights);
         } else {
             hess = std::make_unique<Hessian>(ctx, g, v, v + N, mR, mT, model, nt, state.d(), cfg.hessianMode,
-                                             cfg.hessianMode == 1 ? adjoint.d() : nullptr);
+                                             cfg.hessianMode == 1 ? adjoint.d() : nullptr,
+                                             keepGrads ? grads.d() : nullptr);
         }
         ptH.reset();
         // rhs = -g
