@@ -89,3 +89,32 @@ def test_fine_operator_errors(ctx, api):
     assert summ["iterations"] >= 1
     with pytest.raises(api.InvalidArgument):
         slab.SlabFineOperator(ctx, slab.LocalComm(3), mT, 2, 1e-3)
+
+
+def test_slab_newton_over_nccl_world1(ctx, api):
+    """The same registration through DistComm on a one-rank NCCL group (the torchrun path of
+    tools/slab_newton.py): identical iteration counts to the single-device solve."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    n, nt = 256, 8
+    mR, mT = _pair(ctx, api, n, nt)
+    kw = dict(KW, kind=api.PC_TWO_LEVEL, coarse_solver=api.COARSE_CHEB, nt=nt)
+    _, _, recs, summ = api.newton_solve(ctx, mR, mT, 2, 1e-3, api.COMPRESSIBLE, **kw)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        fo = slab.SlabFineOperator(ctx, slab.DistComm(), mT, 2, 1e-3)
+        _, _, srecs, ssumm = api.newton_solve(ctx, mR, mT, 2, 1e-3, api.COMPRESSIBLE, fine_operator=fo, **kw)
+    finally:
+        dist.destroy_process_group()
+    assert ssumm["iterations"] == summ["iterations"]
+    assert [r["innerIterations"] for r in srecs] == [r["innerIterations"] for r in recs]
+    assert abs(ssumm["finalGradNormRel"] - summ["finalGradNormRel"]) < 1e-8
