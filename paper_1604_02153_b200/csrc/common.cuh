@@ -165,8 +165,6 @@ struct Ctx {
     // Scratch spectra / fields reused across calls (grown on demand, freed with the context).
     std::map<std::pair<int, std::size_t>, DBuf> scratch;
     DBuf reduce;  // reduction scratch (partials + results)
-    DBuf gridSync;  // grid-barrier state (count, generation) of cooperative kernels, zeroed at creation
-    int coopPrefilterBlocks = -1;  // co-resident blocks of the cooperative prefilter (lazy)
     double* hostScalars = nullptr;  // pinned staging for scalar reads
     // External fine-level GN data term for newtonSolve (C ABI vrg_set_fine_operator): the
     // plug-in point of precond::LinOp (precond.hpp:25) that a slab-decomposed operator fills.
@@ -248,8 +246,10 @@ __device__ __forceinline__ void pdlWait() { asm volatile("griddepcontrol.wait;\n
 __device__ __forceinline__ void pdlTrigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // Which kernel families get the PDL attribute (bit 0: evaluate/pointwise, bit 1: prefilter);
-// the kernels' wait/trigger instructions are no-ops under a plain launch.
-int pdlMask();
+// the kernels' wait/trigger instructions are no-ops under a plain launch.  Evaluate/pointwise
+// only: measured on B200 at 1024^2 (matvecs/s) none 1093, evaluate 1112, prefilter 1034, both
+// 1049 -- early-launched prefilter blocks take SM slots from the gather they wait on.
+constexpr int kPdlMask = 1;
 
 template <class... KArgs, class... Args>
 void launchPdl(int family, void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,
@@ -263,7 +263,7 @@ void launchPdl(int family, void (*kernel)(KArgs...), dim3 grid, dim3 block, std:
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (pdlMask() & family) ? 1 : 0;
+    cfg.numAttrs = (kPdlMask & family) ? 1 : 0;
     VRG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

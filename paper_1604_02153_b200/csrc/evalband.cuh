@@ -14,9 +14,6 @@
 namespace vrg {
 
 constexpr int kBandThreads = 256;
-#ifndef VRG_BAND_PIPE
-#define VRG_BAND_PIPE 1
-#endif
 
 // one block per row; n2 a multiple of 256 up to 4096 (chunks per row <= threads)
 inline bool bandFusable(const GridDims& g) { return g.n2 >= 256 && g.n2 <= 4096 && g.n2 % 256 == 0; }
@@ -52,13 +49,8 @@ struct BandWindow {
     unsigned* err = nullptr;
 };
 
-#ifdef VRG_BAND_MINB  // experiment: more resident blocks per SM at fewer registers
-#define VRG_BAND_BOUNDS __launch_bounds__(kBandThreads, VRG_BAND_MINB)
-#else
-#define VRG_BAND_BOUNDS __launch_bounds__(kBandThreads)
-#endif
 template <class Epi, bool kGather, bool kWindow = false>
-__global__ void VRG_BAND_BOUNDS k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
+__global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
                                                             const double* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
                                                             BandWindow win = BandWindow{}) {
@@ -99,7 +91,7 @@ __global__ void VRG_BAND_BOUNDS k_eval_band(CoeffSet<1> cs, const double* __rest
     // taps are in flight, one memory round trip per node instead of two (the gather is latency
     // bound).  The adjoint step's four prefetched operands would cost a resident block per SM
     // (78 registers), which measured slower, so it keeps the plain order.
-    constexpr bool kPipe = VRG_BAND_PIPE && sizeof(typename Epi::Pre) <= sizeof(double);
+    constexpr bool kPipe = sizeof(typename Epi::Pre) <= sizeof(double);
     double xa = 0.0, xb = 0.0;
     typename Epi::Pre pre{};
     if constexpr (kPipe) {

@@ -170,10 +170,7 @@ __global__ void __launch_bounds__(kColBX* kColBY) k_prefilter_cols(const double*
 // parallelism); shared layout pads one slot per 16-chunk so the per-thread chunk walks are
 // bank-conflict free.
 constexpr int kHalo = 2 * kL;
-#ifndef VRG_PF_LINES
-#define VRG_PF_LINES 8
-#endif
-constexpr int kLines = VRG_PF_LINES;  // lines per segment block (power of two)
+constexpr int kLines = 8;  // lines per segment block (power of two)
 constexpr int kLinesLog2 = kLines == 16 ? 4 : kLines == 8 ? 3 : kLines == 4 ? 2 : 1;
 
 
@@ -375,16 +372,6 @@ __global__ void k_unpad(const double* __restrict__ pc, double* __restrict__ out,
     out[static_cast<std::size_t>(i) * n2 + j] = pc[static_cast<std::size_t>(i + 1) * (n2 + 3) + j + 1];
 }
 
-bool coopPrefilter() {
-    static const bool on = [] {
-        // opt-in: one cooperative launch (rows, grid barrier, columns) measured no faster than
-        // the two launches on B200 at 1024^2 (12.35 us either way; matvec 0.93 vs 0.87 ms)
-        const char* e = std::getenv("VRG_COOP_PREFILTER");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 struct SegPlan {
     int R = 0, LS = 0, threads = 0;
     std::size_t smem = 0;
@@ -430,10 +417,7 @@ void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in,
 // the block), so no shared staging of samples is needed; only the chunk summaries go through
 // shared memory.  kCR = kR/16 + 4 chunk rows (2-chunk periodic halo above and below); output
 // in the padded coefficient layout.
-#ifndef VRG_COLW
-#define VRG_COLW 16
-#endif
-constexpr int kColW = VRG_COLW;
+constexpr int kColW = 16;
 
 template <int kR>
 struct ColsShared {
@@ -516,57 +500,6 @@ __global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const doubl
     pfColsReg<kR>(in, out, n1, n2, blockIdx.x, blockIdx.y, threadIdx.x, sh);
 }
 
-// Grid-wide barrier for a cooperatively launched grid (all blocks co-resident): arrive on a
-// counter, the last block bumps the generation that the others spin on.
-__device__ __forceinline__ void gridBarrier(unsigned* count, unsigned* generation, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = generation;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == nblocks - 1) {
-            *count = 0;
-            __threadfence();
-            atomicAdd(generation, 1u);
-        } else {
-            while (*gen == g0) __nanosleep(20);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// Both prefilter passes in one cooperative launch: row segments (two 160-thread halves per
-// block, kLines lines each) -> grid barrier -> column segments (320 threads).  Saves a kernel
-// boundary per prefilter.  kR = 256 only (R/16 + 4 = 20 chunks: 8*20 = 160, 16*20 = 320).
-constexpr int kCoopThreads = 320;
-
-__global__ void __launch_bounds__(kCoopThreads) k_pf_coop(const double* __restrict__ u, double* __restrict__ tmp,
-                                                          double* __restrict__ c, int n1, int n2, int LS,
-                                                          unsigned* nonfinite, unsigned* barrier) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ ColsShared<256> sh;
-    pdlWait();
-    const int half = threadIdx.x >= 160 ? 1 : 0;
-    const int th = threadIdx.x - 160 * half;
-    const int halfSmem = kLines * LS + 3 * kLines * 20;
-    const int segX = n2 / 256, rowItems = segX * ((n1 + kLines - 1) / kLines);
-    for (int base = 2 * blockIdx.x; base < rowItems; base += 2 * gridDim.x) {
-        const int item = base + half;
-        const bool active = item < rowItems;
-        pfSeg<true, false, 256>(u, tmp, n1, n2, LS, nonfinite, active ? item % segX : 0, active ? item / segX : 0, th,
-                                sm + half * halfSmem, active);
-        __syncthreads();
-    }
-    gridBarrier(barrier, barrier + 1, gridDim.x);
-    pdlTrigger();
-    const int segY = n1 / 256, colItems = segY * ((n2 + kColW - 1) / kColW);
-    for (int item = blockIdx.x; item < colItems; item += gridDim.x) {
-        pfColsReg<256>(tmp, c, n1, n2, item % segY, item / segY, threadIdx.x, sh);
-        __syncthreads();
-    }
-}
-
 template <int kR>
 void launchColsReg(Ctx& ctx, const GridDims& g, const double* in, double* out) {
     launchPdl(2, k_pf_cols_reg<kR>, dim3(g.n1 / kR, (g.n2 + kColW - 1) / kColW), dim3(kColW * (kR / kL + 4)), 0,
@@ -577,9 +510,6 @@ void launchColsReg(Ctx& ctx, const GridDims& g, const double* in, double* out) {
 bool launchColumnPass(Ctx& ctx, const GridDims& g, const double* in, double* out) {
     SegPlan pc = segPlan(g.n1);
     if (!pc.ok) return false;
-#ifdef VRG_COLS_RMAX
-    while (pc.R > VRG_COLS_RMAX) pc.R /= 2;
-#endif
     {
         LaunchScope ls_(ctx, "k_prefilter_cols");
         switch (pc.R) {
@@ -674,38 +604,6 @@ void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered,
 
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite) {
     const SegPlan pr = segPlan(g.n2), pc = segPlan(g.n1);
-    if (pr.ok && pc.ok && pr.R == 256 && pc.R == 256 && coopPrefilter()) {
-        const int halfSmem = kLines * pr.LS + 3 * kLines * 20;
-        const std::size_t smem = sizeof(double) * 2 * halfSmem;
-        if (ctx.coopPrefilterBlocks < 0) {
-            VRG_CUDA(cudaFuncSetAttribute(k_pf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
-            int perSM = 0;
-            VRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_pf_coop, kCoopThreads, smem));
-            ctx.coopPrefilterBlocks = perSM * ctx.numSMs;
-        }
-        const int rowItems = (g.n2 / 256) * ((g.n1 + kLines - 1) / kLines);
-        const int colItems = (g.n1 / 256) * ((g.n2 + kColW - 1) / kColW);
-        const int blocks = std::min(ctx.coopPrefilterBlocks, std::max((rowItems + 1) / 2, colItems));
-        if (blocks > 0) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(blocks);
-            cfg.blockDim = dim3(kCoopThreads);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = ctx.stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeCooperative;
-            attr[0].val.cooperative = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            unsigned* bar = ctx.gridSync.as<unsigned>();
-            {
-                LaunchScope ls_(ctx, "k_prefilter_coop");
-                VRG_CUDA(cudaLaunchKernelEx(&cfg, k_pf_coop, u, tmp, c, g.n1, g.n2, pr.LS, nonfinite, bar));
-            }
-            return;
-        }
-    }
     if (pr.ok && pc.ok) {
         {
             LaunchScope ls_(ctx, "k_prefilter_rows");

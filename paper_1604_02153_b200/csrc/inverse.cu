@@ -11,7 +11,6 @@
 #include "evalband.cuh"
 #include "heun.cuh"
 #include "inverse.cuh"
-#include "wave.cuh"
 
 namespace vrg {
 
@@ -115,191 +114,6 @@ struct EpiIncSeed {
     }
 };
 
-// Persistent wavefront kernel of the data term (wave.cuh).  Phases q = 0 .. 2nt-1: q < nt is
-// incremental-state step j = q+1, q >= nt is incremental-adjoint step j = 2nt-q.  Phase q >= 1
-// has column tasks B(q, s, cg) (column pass of the row-filtered field of phase q-1, ring slot
-// (q-1)%NB of R, into slot q%NB of C) and every phase has row tasks A(q, r) (gather from C slot
-// q%NB + epilogue + row pass into R slot q%NB).
-// Schedule (Hessian::setupWave): the tasks are dispatched in the order of a host-built list
-// sorted by a key that interleaves consecutive phases along the rows -- phase q starts its
-// rows Delta rows after phase q-1 did and K key units later -- so a row's per-velocity data
-// (departure points, vt, vt_D, div v, ...) is re-read by the next step while it is still in
-// L2 (temporal blocking), and each task's dependencies have smaller keys (deadlock free).
-// R and C are rings of NB fields so that several phases can be in flight.
-struct WaveArgs {
-    int n1, n2, nt, SR, CW, nseg, ncg, ngrp, dRows, ySmemOffset, NB;
-    unsigned total;
-    const unsigned* tasks;  // key-sorted task list: q << 20 | kind << 19 | index
-    double* Cring;          // NB padded coefficient fields
-    double* Rring;          // NB row-filtered fields
-    std::size_t cStride;    // padded points
-    const double* Xf;
-    const double* Xb;
-    const double* vtD;
-    const double* vt1;
-    const double* vt2;
-    const double* G;   // (nt+1) x [g1 | g2]
-    const double* GD;  // nt x [gd1 | gd2]
-    const double* dvd;
-    const double* dv;
-    double ht;
-    double* b1;
-    double* b2;
-    const double* reg1;
-    const double* reg2;
-    double* o1;
-    double* o2;
-    double* partials;
-    unsigned blocksPerStep;
-    unsigned* flags;
-    unsigned* next;     // task counter
-    unsigned* grpA;     // [2nt][ngrp] rows done per row group
-    unsigned* segB;     // [2nt][nseg] column tasks done per segment
-    unsigned* stepA;    // [2nt]
-    unsigned* stepB;    // [2nt]
-};
-constexpr unsigned kWaveKindB = 1u << 19;
-
-#ifndef VRG_WAVE_MINB
-#define VRG_WAVE_MINB 3  // resident blocks per SM (register cap 80: no spills)
-#endif
-#ifdef VRG_WAVE_STATS
-// instrumentation build: per kind (A, B) summed wait cycles, work cycles, task count; dispatch
-__device__ unsigned long long gWaveStats[8];
-#define WAVE_T(x) const long long x = clock64()
-#define WAVE_ADD(i, v) \
-    if (t == 0) atomicAdd(&gWaveStats[i], static_cast<unsigned long long>(v))
-#else
-#define WAVE_T(x)
-#define WAVE_ADD(i, v)
-#endif
-
-__global__ void __launch_bounds__(kWaveThreads, VRG_WAVE_MINB) k_wave(WaveArgs args) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ double red[kWaveThreads / 32];
-    __shared__ unsigned sTask;
-    // The arguments are read from shared memory inside the task loop: read from the parameter
-    // space they would be hoisted out of the loop and held in registers across all tasks.
-    __shared__ WaveArgs sa;
-    const int t = threadIdx.x;
-    if (t == 0) sa = args;
-    __syncthreads();
-    const WaveArgs& a = sa;
-    double* Y = sm + a.ySmemOffset;
-    for (;;) {
-        WAVE_T(tD0);
-        if (t == 0) sTask = atomicAdd(a.next, 1u);
-        __syncthreads();
-        const long long id = sTask;
-        __syncthreads();
-        if (id >= a.total) return;
-        WAVE_T(tD1);
-        WAVE_ADD(6, tD1 - tD0);
-        const std::size_t N = static_cast<std::size_t>(a.n1) * a.n2;
-        const int Q = 2 * a.nt;
-        const int nB = a.nseg * a.ncg;
-        const unsigned code = a.tasks[id];
-        const int q = static_cast<int>(code >> 20);
-        const int idx = static_cast<int>(code & (kWaveKindB - 1));
-        const bool isB = (code & kWaveKindB) != 0;
-        if (isB) {
-            // ---- column task B(q, s, cg)
-            const int s = idx / a.ncg, cg = idx - s * a.ncg;
-            const int gPerSeg = a.SR / kWaveRG, hg = kWaveHalo / kWaveRG;
-            const int ng = gPerSeg + 2 * hg;
-            if (t < ng) {
-                int gi = s * gPerSeg - hg + t;
-                gi += gi < 0 ? a.ngrp : 0;
-                gi -= gi >= a.ngrp ? a.ngrp : 0;
-                waitAtLeast(a.grpA + static_cast<std::size_t>(q - 1) * a.ngrp + gi, kWaveRG);
-            }
-            if (t == 0 && q >= a.NB) waitAtLeast(a.stepA + q - a.NB, a.n1);  // C slot free (read by A(q-NB))
-            __syncthreads();
-            WAVE_T(tB1);
-            waveColsTask(a.Rring + static_cast<std::size_t>((q - 1) % a.NB) * N,
-                         a.Cring + static_cast<std::size_t>(q % a.NB) * a.cStride, a.n1, a.n2, a.SR, a.CW, s, cg, sm,
-                         Y);
-            signalDone(a.segB + static_cast<std::size_t>(q) * a.nseg + s, a.stepB + q);
-            WAVE_T(tB2);
-            WAVE_ADD(3, tB1 - tD1);
-            WAVE_ADD(4, tB2 - tB1);
-            WAVE_ADD(5, 1);
-            continue;
-        }
-        // ---- row task A(q, r)
-        const int r = idx;
-        if (t == 0 && q >= a.NB) waitAtLeast(a.stepB + q + 1 - a.NB, nB);  // R slot free (read by B(q+1-NB))
-        if (q >= 1 && t == 0) {
-            const int lo = r - a.dRows, hi = r + a.dRows;
-            if (hi - lo + 1 >= a.n1) {
-                for (int s = 0; s < a.nseg; ++s) waitAtLeast(a.segB + static_cast<std::size_t>(q) * a.nseg + s, a.ncg);
-            } else {
-                const int s0 = (lo < 0 ? lo - a.SR + 1 : lo) / a.SR, s1 = hi / a.SR;  // floor division
-                for (int s = s0; s <= s1; ++s) {
-                    const int sw = ((s % a.nseg) + a.nseg) % a.nseg;
-                    waitAtLeast(a.segB + static_cast<std::size_t>(q) * a.nseg + sw, a.ncg);
-                }
-            }
-        }
-        __syncthreads();
-        WAVE_T(tA1);
-        WAVE_ADD(0, tA1 - tD1);
-        double* rowOut = a.Rring + static_cast<std::size_t>(q % a.NB) * N;
-        const double* coef = a.Cring + static_cast<std::size_t>(q % a.NB) * a.cStride;
-        if (q < a.nt) {
-            const int j = q + 1;
-            const double* Gj = a.G + static_cast<std::size_t>(j) * 2 * N;
-            const double* GDj = a.GD + static_cast<std::size_t>(j - 1) * 2 * N;
-            const EpiIncState inc{nullptr, a.vtD, a.vtD + N, GDj, GDj + N, a.vt1, a.vt2, Gj, Gj + N, 0.5 * a.ht, nullptr};
-            if (j == a.nt) {
-                const EpiIncSeed seed{a.partials + static_cast<std::size_t>(a.nt) * a.blocksPerStep, inc,
-                                      a.ht * 0.5, a.b1, a.b2};
-                if (q == 0)
-                    waveRowTask<EpiIncSeed, false, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, seed, rowOut,
-                                                         a.flags + a.nt, sm, red, Y);
-                else
-                    waveRowTask<EpiIncSeed, true, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, seed, rowOut,
-                                                        a.flags + a.nt, sm, red, Y);
-            } else if (q == 0) {
-                waveRowTask<EpiIncState, false, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, inc, rowOut, nullptr, sm,
-                                                      red, Y);
-            } else {
-                waveRowTask<EpiIncState, true, true>(coef, a.Xf, a.Xf + N, a.n1, a.n2, r, inc, rowOut, nullptr, sm,
-                                                     red, Y);
-            }
-        } else {
-            const int j = Q - q;  // adjoint step j -> lt_{j-1}
-            const double w = a.ht * ((j - 1 == 0 || j - 1 == a.nt) ? 0.5 : 1.0);
-            const double* Gm = a.G + static_cast<std::size_t>(j - 1) * 2 * N;
-            const bool last = j == 1;
-            const EpiAdjointBF epi{a.partials + static_cast<std::size_t>(j - 1) * a.blocksPerStep, a.dvd, a.dv, a.ht,
-                                   nullptr, Gm, Gm + N, w, a.b1, a.b2, a.reg1, a.reg2, last ? a.o1 : nullptr,
-                                   last ? a.o2 : nullptr};
-            if (last)
-                waveRowTask<EpiAdjointBF, true, false>(coef, a.Xb, a.Xb + N, a.n1, a.n2, r, epi, rowOut, nullptr, sm,
-                                                       red, Y);
-            else
-                waveRowTask<EpiAdjointBF, true, true>(coef, a.Xb, a.Xb + N, a.n1, a.n2, r, epi, rowOut,
-                                                      a.flags + (j - 1), sm, red, Y);
-        }
-        signalDone(a.grpA + static_cast<std::size_t>(q) * a.ngrp + r / kWaveRG, a.stepA + q);
-        WAVE_T(tA2);
-        WAVE_ADD(1, tA2 - tA1);
-        WAVE_ADD(2, 1);
-    }
-}
-
-// |departure - arrival| along axis 1 in grid cells (minimum image), per node.
-__global__ void k_row_disp(const double* __restrict__ x1, int n1, int n2, double* __restrict__ out) {
-    const std::size_t N = static_cast<std::size_t>(n1) * n2;
-    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    const double h = kTwoPi / n1;
-    const double xa = -kPi + static_cast<double>(p / n2) * h;
-    double d = x1[p] - xa;
-    d -= kTwoPi * floor((d + kPi) / kTwoPi);
-    out[p] = fabs(d) / h;
-}
 
 }  // namespace
 
@@ -395,12 +209,8 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     }
     // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
     // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
-    // 1024^2 on B200 (0.815 vs 0.867 ms).  VRG_FUSED_BANDS=0 selects the plain step.
-    const char* env = std::getenv("VRG_FUSED_BANDS");
-    const bool want = !(env && env[0] == '0');
-    fused_ = useFusedBands && want && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
-    if (const char* ge = std::getenv("VRG_GRAPHS")) useGraphs = ge[0] != '0';  // debugging switch
-    setupWave();
+    // 1024^2 on B200 (0.815 vs 0.867 ms).  The plain step is the generic-grid path.
+    fused_ = bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
     lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     adjLog_.ensure(nt + 1, evalBlocks(g));
@@ -414,120 +224,6 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     ctx.sync();
 }
 
-// Wavefront path (k_wave, opt-in with VRG_WAVE=1 on the band-path grids): correct and equal to
-// the band path to rounding, but slower on B200 at 1024^2 nt=16 (band 1226 matvec/s; wave with
-// phase-ordered queue 871, with the temporally blocked key order 380-640 depending on K).  The
-// machine keeps ~580 rows in flight (9 us row-task latency x 65 rows/us), more than half the
-// grid, so consecutive steps cannot be overlapped along the rows without stalling on their
-// dependencies (tools/wave_stats.py: 6-16 us of dependency wait per row task), and a single
-// step is already memory bound.  Kept for larger grids and as the base of a cross-step schedule.
-// The dependency reach of a row task is the largest departure displacement along axis 1 over
-// both characteristics (fixed per Hessian), rounded up, plus the 4-tap stencil and one row of
-// margin; a non-finite departure point makes every row depend on every segment.
-void Hessian::setupWave() {
-    const char* env = std::getenv("VRG_WAVE");
-    wave_ = false;
-    if (!fused_ || !(env && env[0] == '1') || g.n1 % kWaveRG != 0) return;
-    const std::size_t N = g.points();
-    double* d = solver.tmp();
-    double reach = 0.0;
-    bool finite = true;
-    for (int dir : {kForward, kBackward}) {
-        const double* X = solver.departure(dir);
-        k_row_disp<<<grid1d(N, 256), 256, 0, ctx.stream>>>(X, g.n1, g.n2, d);
-        VRG_LAUNCH_CHECK();
-        finite = finite && !anyNonFinite(ctx, N, d);
-        reach = std::max(reach, normLinf(ctx, N, d));
-    }
-    waveDRows_ = finite ? static_cast<int>(std::ceil(reach)) + 3 : g.n1;
-    const char* sr = std::getenv("VRG_WAVE_SR");
-    waveSR_ = sr ? std::atoi(sr) : 64;
-    while (waveSR_ > 32 && (g.n1 % waveSR_ != 0 || g.n2 % waveColsWidth(waveSR_) != 0)) waveSR_ /= 2;
-    if (waveSR_ < 64 || waveSR_ > 256) return;  // halo summaries need 4 CW <= 256 threads
-    const int SR = waveSR_, D = waveDRows_, n1 = g.n1;
-    if (2 * D + SR >= n1) return;  // no locality to exploit
-    // Schedule keys (see WaveArgs): rows of phase q start at row start_q + M, its column
-    // segments at start_q, start_q = q * Delta; key(A) = q K + M + pos, key(B) = q K + spos - D - 1.
-    // Conditions for every dependency to have a smaller key: M >= D + SR, Delta >= M + 32,
-    // K > Delta + SR + D + 32.
-    const int M = D + SR;
-    const int Delta = (M + 32 + SR - 1) / SR * SR;
-    const char* kenv = std::getenv("VRG_WAVE_K");
-    const int K = std::max(kenv ? std::atoi(kenv) : 0, Delta + SR + D + 33);
-    const int Q = 2 * nt, nseg = n1 / SR, ncg = g.n2 / waveColsWidth(SR), nB = nseg * ncg;
-    waveNB_ = std::max(2, (n1 + D + K - 1) / K + 2);
-    struct T {
-        long long key;
-        unsigned code;
-    };
-    std::vector<T> list;
-    list.reserve(static_cast<std::size_t>(Q) * (n1 + nB));
-    for (int q = 0; q < Q; ++q) {
-        const long long start = (static_cast<long long>(q) * Delta) % n1;
-        for (int r = 0; r < n1; ++r) {
-            const long long pos = ((r - start - M) % n1 + n1) % n1;
-            list.push_back({static_cast<long long>(q) * K + M + pos, (static_cast<unsigned>(q) << 20) | r});
-        }
-        if (q == 0) continue;
-        for (int sgi = 0; sgi < nseg; ++sgi) {
-            const long long spos = ((static_cast<long long>(sgi) * SR - start) % n1 + n1) % n1;
-            for (int cg = 0; cg < ncg; ++cg)
-                list.push_back({static_cast<long long>(q) * K + spos - D - 1,
-                                (static_cast<unsigned>(q) << 20) | kWaveKindB | (sgi * ncg + cg)});
-        }
-    }
-    std::stable_sort(list.begin(), list.end(), [](const T& x, const T& y) { return x.key < y.key; });
-    // Host check of the schedule: every dependency (and every ring-slot reuse wait) of a task
-    // sits earlier in the list; otherwise the band path is kept.
-    std::vector<int> posA(static_cast<std::size_t>(Q) * n1), lastA(Q, -1), lastB(Q, -1), posSeg(static_cast<std::size_t>(Q) * nseg, -1);
-    for (int i = 0; i < static_cast<int>(list.size()); ++i) {
-        const unsigned c = list[i].code;
-        const int q = static_cast<int>(c >> 20), idx = static_cast<int>(c & (kWaveKindB - 1));
-        if (c & kWaveKindB) {
-            lastB[q] = i;
-            int& ps = posSeg[static_cast<std::size_t>(q) * nseg + idx / ncg];
-            ps = std::max(ps, i);
-        } else {
-            posA[static_cast<std::size_t>(q) * n1 + idx] = i;
-            lastA[q] = i;
-        }
-    }
-    bool ok = true;
-    for (int i = 0; i < static_cast<int>(list.size()) && ok; ++i) {
-        const unsigned c = list[i].code;
-        const int q = static_cast<int>(c >> 20), idx = static_cast<int>(c & (kWaveKindB - 1));
-        if (c & kWaveKindB) {
-            const int sgi = idx / ncg;
-            for (int rr = sgi * SR - kWaveHalo; rr < sgi * SR + SR + kWaveHalo && ok; ++rr)
-                ok = posA[static_cast<std::size_t>(q - 1) * n1 + ((rr % n1) + n1) % n1] < i;
-            if (q >= waveNB_) ok = ok && lastA[q - waveNB_] < i;
-        } else {
-            if (q >= waveNB_) ok = ok && lastB[q + 1 - waveNB_] < i;
-            if (q >= 1)
-                for (int rr = idx - D; rr <= idx + D && ok; ++rr)
-                    ok = posSeg[static_cast<std::size_t>(q) * nseg + (((rr % n1) + n1) % n1) / SR] < i;
-        }
-    }
-    if (!ok) return;
-    std::vector<unsigned> codes(list.size());
-    for (std::size_t i = 0; i < list.size(); ++i) codes[i] = list[i].code;
-    waveTasks_.alloc(sizeof(unsigned) * codes.size());
-    VRG_CUDA(cudaMemcpyAsync(waveTasks_.d(), codes.data(), sizeof(unsigned) * codes.size(), cudaMemcpyHostToDevice,
-                             ctx.stream));
-    waveTaskCount_ = static_cast<unsigned>(codes.size());
-    waveRing_.alloc(sizeof(double) * waveNB_ * (N + paddedPoints(g.n1, g.n2)));
-    waveSmem_ = waveSmemFor(g, waveSR_);
-    if (waveSmem_ > 48 * 1024)
-        VRG_CUDA(cudaFuncSetAttribute(k_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(waveSmem_)));
-    int perSM = 0;
-    VRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_wave, kWaveThreads, waveSmem_));
-    if (perSM < 1) return;
-    waveBlocks_ = perSM * ctx.numSMs;
-    const int ngrp = g.n1 / kWaveRG;
-    waveCnt_.alloc(sizeof(unsigned) * (1 + 2 * Q + static_cast<std::size_t>(Q) * (ngrp + nseg)));
-    ctx.sync();
-    wave_ = true;
-}
 
 // RK2 / RK2A operator (heun.cuh): state (and, full Newton, adjoint) trajectories with their Heun
 // predictors; no graph capture (the Heun solves check their guards on the host).
@@ -683,79 +379,6 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     launchPrefilter(ctx, g, vt2, c2, tmp, nullptr);
     launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
     auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
-    if (wave_) {
-        adjLog_.reset(ctx);
-        VRG_CUDA(cudaMemsetAsync(waveCnt_.d(), 0, waveCnt_.bytes(), ctx.stream));
-        const int Q = 2 * nt, ngrp = g.n1 / kWaveRG, nseg = g.n1 / waveSR_, CW = waveColsWidth(waveSR_);
-        const int ncg = g.n2 / CW;
-        unsigned* cnt = waveCnt_.as<unsigned>();
-        WaveArgs a{};
-        a.n1 = g.n1;
-        a.n2 = g.n2;
-        a.nt = nt;
-        a.SR = waveSR_;
-        a.CW = CW;
-        a.ySmemOffset = static_cast<int>(waveSmemBase(g, waveSR_) / sizeof(double));
-        a.nseg = nseg;
-        a.ncg = ncg;
-        a.ngrp = ngrp;
-        a.dRows = waveDRows_;
-        a.total = waveTaskCount_;
-        a.tasks = waveTasks_.as<unsigned>();
-        a.NB = waveNB_;
-        a.Rring = waveRing_.d();
-        a.Cring = waveRing_.d() + static_cast<std::size_t>(waveNB_) * N;
-        a.cStride = paddedPoints(g.n1, g.n2);
-        a.Xf = Xf;
-        a.Xb = Xb;
-        a.vtD = vtD;
-        a.vt1 = vt1;
-        a.vt2 = vt2;
-        a.G = G_.d();
-        a.GD = GD_.d();
-        a.dvd = dvd;
-        a.dv = dv;
-        a.ht = ht;
-        a.b1 = b1;
-        a.b2 = b2;
-        a.reg1 = reg1;
-        a.reg2 = reg2;
-        a.o1 = out1;
-        a.o2 = out2;
-        a.partials = adjLog_.partial(0);
-        a.blocksPerStep = adjLog_.blocks;
-        a.flags = adjLog_.flag(0);
-        a.next = cnt;
-        a.stepA = cnt + 1;
-        a.stepB = cnt + 1 + Q;
-        a.grpA = cnt + 1 + 2 * Q;
-        a.segB = cnt + 1 + 2 * Q + static_cast<std::size_t>(Q) * ngrp;
-#ifdef VRG_WAVE_STATS
-        {
-            unsigned long long z[8] = {};
-            VRG_CUDA(cudaMemcpyToSymbolAsync(gWaveStats, z, sizeof(z), 0, cudaMemcpyHostToDevice, ctx.stream));
-        }
-#endif
-        {
-            LaunchScope ls_(ctx, "wave/matvec");
-            k_wave<<<std::min<unsigned>(waveBlocks_, a.total), kWaveThreads, waveSmem_, ctx.stream>>>(a);
-            VRG_LAUNCH_CHECK();
-        }
-#ifdef VRG_WAVE_STATS
-        if (!useGraphs || ctx.profOn) {
-            unsigned long long z[8];
-            VRG_CUDA(cudaMemcpyFromSymbolAsync(z, gWaveStats, sizeof(z), 0, cudaMemcpyDeviceToHost, ctx.stream));
-            VRG_CUDA(cudaStreamSynchronize(ctx.stream));
-            std::fprintf(stderr,
-                         "wave stats: blocks %d | A n=%llu wait %.2f us work %.2f us | B n=%llu wait %.2f us work "
-                         "%.2f us | dispatch %.2f us (per task, at 1.965 GHz)\n",
-                         waveBlocks_, z[2], z[0] / 1965.0 / z[2], z[1] / 1965.0 / z[2], z[5], z[3] / 1965.0 / z[5],
-                         z[4] / 1965.0 / z[5], z[6] / 1965.0 / (z[2] + z[5]));
-        }
-#endif
-        adjLog_.finalize(ctx);
-        return;
-    }
     if (fused_) {
         // Band path: every step's gather kernel also row-filters its output (evalband.cuh), so
         // each step is [column pass] + [gather + epilogue + row pass].  R[.] ping-pong holds
@@ -1218,11 +841,7 @@ void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, doub
     } else {
         // reg = beta A vt on the second stream (independent of the data term until its last
         // step), then the last adjoint step writes out = reg + b
-        static const bool regStream = [] {
-            const char* e = std::getenv("VRG_REG_STREAM");
-            return !(e && e[0] == '0');
-        }();
-        if (!aux_ && regStream) {
+        if (!aux_) {
             VRG_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
             VRG_CUDA(cudaEventCreateWithFlags(&evFork_, cudaEventDisableTiming));
             VRG_CUDA(cudaEventCreateWithFlags(&evJoin_, cudaEventDisableTiming));

@@ -53,7 +53,7 @@ public:
     Hessian& operator=(const Hessian&) = delete;
 
     const double* state() const { return state_.d(); }
-    bool useGraphs = true;
+    bool useGraphs = true;  // false for the RK2/RK2A operator (host-checked Heun guards)
     // ms per launch of a matvec kernel class (0 incstate step, 1 adjoint+body-force step,
     // 2 prefilter (both passes), 3 two-field evaluate), timed back to back.
     double benchKernel(int id, int iters);
@@ -122,26 +122,12 @@ private:
     void initHeun(const double* mR, const double* mT, const double* stateTraj, const double* adjTraj);
     void dataTermHeun(const double* vt1, const double* vt2, double* b1, double* b2, const double* reg1,
                       const double* reg2, double* out1, double* out2);
-    // persistent wavefront kernel for the whole data term (wave.cuh, k_wave)
-    bool wave_ = false;
-    int waveDRows_ = 0;      // rows a gather may reach from its own row (displacement + stencil)
-    int waveSR_ = 0;         // column-pass segment height
-    int waveBlocks_ = 0;     // resident blocks of k_wave
-    std::size_t waveSmem_ = 0;
-    DBuf waveCnt_;           // task counter + dependency counters, zeroed per matvec
-    DBuf waveTasks_;         // key-sorted task list
-    DBuf waveRing_;          // NB row-filtered fields, then NB padded coefficient fields
-    unsigned waveTaskCount_ = 0;
-    int waveNB_ = 2;
-    void setupWave();
 
 public:
-    static inline bool useFusedBands = true;  // process-wide switch (tests compare both paths)
     bool bandPath() const { return fused_; }
     // device buffers of the per-iterate invariants: state (nt+1)N, G (nt+1)2N, GD nt 2N
     const double* gradTraj() const { return G_.d(); }
     const double* gradDepTraj() const { return GD_.d(); }
-    bool wavePath() const { return wave_; }
 };
 
 // One SL step of a slab-decomposed grid (C ABI vrg_slab_step).

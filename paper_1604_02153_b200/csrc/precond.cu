@@ -164,17 +164,32 @@ __global__ void __cluster_dims__(kLzCtas, 1, 1) __launch_bounds__(kLzThreads, 1)
             q[k] = e < n ? qi[e] : 0.0;
         }
     };
+    // kPer = 8 re-reads q_i (L1/L2 hits) after the cluster sum instead of holding it across
+    // the sum: 64 registers at 1024 threads cannot hold x, q and the addresses without spills
+    constexpr bool kReload = kPer >= 8;
     auto project = [&](int i, bool storeAlpha) {
-        double q[kPer];
-        qv(i, q);
+        double q[kReload ? 1 : kPer];
+        const double* qi = Q + static_cast<std::size_t>(i) * n;
         double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) s += x[k] * q[k];
+        for (int k = 0; k < kPer; ++k) {
+            const std::size_t e = base + k * kStride;
+            const double qk = e < n ? qi[e] : 0.0;
+            if constexpr (!kReload) q[k] = qk;
+            s += x[k] * qk;
+        }
         const double c = hh * lzClusterSum(s, red, parity);
         if (storeAlpha && blockIdx.x == 0 && threadIdx.x == 0) *alphaOut = c;
         const double a = -c;
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) x[k] = x[k] + a * q[k];
+        for (int k = 0; k < kPer; ++k) {
+            if constexpr (kReload) {
+                const std::size_t e = base + k * kStride;
+                x[k] = x[k] + a * (e < n ? qi[e] : 0.0);
+            } else {
+                x[k] = x[k] + a * q[k];
+            }
+        }
     };
     if (j > 0) {
         double q[kPer];

@@ -25,16 +25,6 @@ void throwCufft(cufftResult r, const char* what, const char* file, int line) {
     throw std::runtime_error(buf);
 }
 
-int pdlMask() {
-    static const int mask = [] {
-        // default: evaluate/pointwise only.  Measured on B200 at 1024^2 (matvecs/s): none 1093,
-        // evaluate 1112, prefilter 1034, both 1049 — early-launched prefilter blocks hurt.
-        const char* e = std::getenv("VRG_PDL");
-        return e ? std::atoi(e) : 1;
-    }();
-    return mask;
-}
-
 void checkGrid(int n1, int n2) {
     if (n1 < 4 || n1 % 2 != 0 || n2 < 4 || n2 % 2 != 0)
         throw InvalidArgument("Grid: axis sizes must be even and >= 4");
@@ -133,8 +123,6 @@ Ctx::Ctx(int dev, cudaStream_t s) : device(dev) {
     VRG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
     l2Bytes = static_cast<std::size_t>(l2);
     reduce.alloc(sizeof(double) * (kReduceBlocks * 4 + 64));
-    gridSync.alloc(64);
-    VRG_CUDA(cudaMemset(gridSync.d(), 0, 64));
     VRG_CUDA(cudaMallocHost(&hostScalars, sizeof(double) * 64));
 }
 

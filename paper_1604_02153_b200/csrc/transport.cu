@@ -162,16 +162,10 @@ Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2,
     log.ensure(nt + 1, evalBlocks(g));
 }
 
-// Band path for the SL time loops (evalband.cuh): each step is the gather + epilogue + the next
-// prefilter's row pass in one kernel, then the column pass; same arithmetic as
-// prefilter + evaluate (VRG_FUSED_BANDS=0 selects the plain 3-kernel step).
-bool Solver::bandPath() const {
-    static const bool on = [] {
-        const char* e = std::getenv("VRG_FUSED_BANDS");
-        return !(e && e[0] == '0');
-    }();
-    return on && bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
-}
+// Band path for the SL time loops (evalband.cuh) wherever the grid allows it: each step is the
+// gather + epilogue + the next prefilter's row pass in one kernel, then the column pass; same
+// arithmetic as prefilter + evaluate (the plain 3-kernel step, the generic-grid path).
+bool Solver::bandPath() const { return bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g); }
 
 double* Solver::coef() { return coef_.d(); }
 double* Solver::tmp() { return tmp_.d(); }
@@ -248,120 +242,13 @@ void Solver::continuityBand(const double* lam1, DstFn dst) {
     ctx.interps += nt;
 }
 
-// ------------------------------------------------------------------------------ ADI steps
-namespace {
-// |departure - node| along each axis in cells (minimum image), one node per thread
-__global__ void k_adi_disp(const double* __restrict__ X, int n1, int n2, double h1, double h2, double* d1,
-                           double* d2) {
-    const std::size_t N = static_cast<std::size_t>(n1) * n2;
-    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    const int i1 = static_cast<int>(p / n2), i2 = static_cast<int>(p - static_cast<std::size_t>(i1) * n2);
-    double a = X[p] - (-kPi + i1 * h1);
-    double b = X[N + p] - (-kPi + i2 * h2);
-    a -= kTwoPi * floor((a + kPi) / kTwoPi);
-    b -= kTwoPi * floor((b + kPi) / kTwoPi);
-    d1[p] = fabs(a) / h1;
-    d2[p] = fabs(b) / h2;
-}
-}  // namespace
-
-void adiReach(Ctx& ctx, const GridDims& g, const double* X, double& rows, double& cols) {
-    const std::size_t N = g.points();
-    double* d = ctx.scratchBuf(13, sizeof(double) * 2 * N);
-    k_adi_disp<<<grid1d(N, 256), 256, 0, ctx.stream>>>(X, g.n1, g.n2, g.h1(), g.h2(), d, d + N);
-    VRG_LAUNCH_CHECK();
-    if (anyNonFinite(ctx, 2 * N, d)) {
-        rows = cols = INFINITY;
-        return;
-    }
-    rows = normLinf(ctx, N, d);
-    cols = normLinf(ctx, N, d + N);
-}
-
-AdiPlan adiPlan(const Ctx& ctx, const GridDims& g, double reachRows, double reachCols) {
-    AdiPlan pl;
-    const double reach[2] = {reachRows, reachCols};
-    for (int dir = 0; dir < 2; ++dir) {
-        const int n = dir == 0 ? g.n2 : g.n1, nLines = dir == 0 ? g.n1 : g.n2;
-        if (n % kL != 0 || n < 64 || !std::isfinite(reach[dir])) return AdiPlan{};
-        const int H = static_cast<int>(std::ceil(reach[dir])) + 2;
-        if (2 * H + 1 > nLines) return AdiPlan{};
-        int R = (nLines + ctx.numSMs - 1) / ctx.numSMs;
-        R = std::min(R, kAdiMaxPer * kAdiThreads / n);
-        while (R >= 1 && adiSmem(n, R + 2 * H) > static_cast<std::size_t>(kAdiMaxSmem)) --R;
-        if (R < 1) return AdiPlan{};
-        pl.R[dir] = R;
-        pl.H[dir] = H;
-        pl.blocks[dir] = (nLines + R - 1) / R;
-        pl.smem[dir] = adiSmem(n, R + 2 * H);
-    }
-    pl.ok = true;
-    return pl;
-}
-
-bool Solver::adiEnabled() {
-    const char* e = std::getenv("VRG_ADI");  // read per call: tests switch it
-    return e && e[0] == '1';
-}
-
-const AdiPlan& Solver::adiPlanFor(int dir) {
-    if (!haveAdi_[dir]) {
-        double r = 0.0, c = 0.0;
-        adiReach(ctx, g, departure(dir), r, c);
-        adi_[dir] = adiPlan(ctx, g, r, c);
-        haveAdi_[dir] = true;
-    }
-    return adi_[dir];
-}
-
-unsigned* Solver::adiErr() {
-    if (!adiErr_) {
-        adiErr_.alloc(64);
-        VRG_CUDA(cudaMemsetAsync(adiErr_.d(), 0, 64, ctx.stream));
-    }
-    return adiErr_.as<unsigned>();
-}
-
-// slState with alternating-direction fused steps: p_0 = P_row m_0, then kinds B, A, B, ...
-// Returns false (nothing committed) if the plan does not allow it.
-bool Solver::stateAdi(const double* m0, double* traj) {
-    const AdiPlan& pl = adiPlanFor(kForward);
-    if (!pl.ok) return false;
-    const double* X = departure(kForward);
-    const std::size_t N = g.points();
-    double* buf = tmp_.d();  // 2N: ping-pong of the filtered fields
-    launchPrefilterRows(ctx, g, traj, buf, log.flag(0));
-    for (int j = 1; j <= nt; ++j) {
-        const int dir = (j % 2 == 1) ? 1 : 0;  // B first: its input is row-filtered
-        const double* in = buf + ((j - 1) % 2) * N;
-        double* out = (j == nt) ? nullptr : buf + (j % 2) * N;
-        launchAdiStep<EpiStateStep, true>(ctx, g, pl, dir, in, X, X + N, EpiStateStep{log.partial(j), traj + j * N},
-                                          out, log.flag(j), adiErr());
-    }
-    return true;
-}
-
 void Solver::state(const double* m0, double* traj, bool guard) {
     const double* X = departure(kForward);
     const std::size_t N = g.points();
     log.reset(ctx);
     copy(ctx, N, m0, traj);
     launchFieldMax(ctx, g, traj, log.partial(0));
-    bool done = false;
-    if (adiEnabled() && stateAdi(m0, traj)) {
-        unsigned e = 0;
-        VRG_CUDA(cudaMemcpyAsync(&e, adiErr(), sizeof e, cudaMemcpyDeviceToHost, ctx.stream));
-        ctx.sync();
-        done = e == 0;
-        if (!done) {  // a departure point beyond the planned strip (never expected): redo
-            VRG_CUDA(cudaMemsetAsync(adiErr(), 0, sizeof e, ctx.stream));
-            log.reset(ctx);
-            launchFieldMax(ctx, g, traj, log.partial(0));
-        }
-    }
-    if (done) {
-    } else if (bandPath()) {
+    if (bandPath()) {
         launchPrefilter(ctx, g, traj, coef_.d(), tmp_.d(), log.flag(0));
         for (int j = 1; j <= nt; ++j) {
             const EpiStateStep epi{log.partial(j), traj + j * N};

@@ -3,7 +3,6 @@
 // of scope and raise NotSupported at the C ABI.
 #pragma once
 
-#include "adi.cuh"
 #include "blas.cuh"
 #include "eval.cuh"
 #include "spectral.cuh"
@@ -90,11 +89,6 @@ public:
 
     GuardLog log;
 
-    // Alternating-direction fused steps (adi.cuh) for this velocity: plan for the
-    // characteristics of `dir` (both kinds), or !ok where the grid or reach does not allow it.
-    const AdiPlan& adiPlanFor(int dir);
-    unsigned* adiErr();  // device flag: a tap fell outside a strip (set by the kernels)
-    static bool adiEnabled();
 
 private:
     template <class DstFn>
@@ -104,10 +98,6 @@ private:
     DBuf divv_, dvDep_[2];
     DBuf coef_, tmp_;
     bool haveCv_ = false, haveX_[2] = {false, false}, haveDivv_ = false, haveDvDep_[2] = {false, false};
-    AdiPlan adi_[2];
-    bool haveAdi_[2] = {false, false};
-    DBuf adiErr_;
-    bool stateAdi(const double* m0, double* traj);
 };
 
 }  // namespace vrg
