@@ -40,6 +40,10 @@ CARRY = 32  # rows of chunk-carry reach of the column pass (2 chunks of 16)
 
 
 # ------------------------------------------------------------------------------ communicators
+def _nan_to_inf(t):
+    return torch.nan_to_num(t, nan=float("inf")) if t.is_floating_point() else t
+
+
 class LocalComm:
     """G virtual slabs in one process: exchanges are tensor copies."""
 
@@ -76,12 +80,15 @@ class LocalComm:
         return [[send[i][q] for i in self.ranks] for q in self.ranks]
 
     def allreduce_max(self, vals):
-        m = torch.stack([torch.as_tensor(v) for v in vals]).amax(0)
+        m = torch.stack([_nan_to_inf(torch.as_tensor(v)) for v in vals]).amax(0)
         return [m for _ in self.ranks]
 
     def allgather_rows(self, locs, out):
         """locs[i] = (m, L, n2) slab of rank i -> out (m, n1, n2), the slabs in rank order."""
         out.copy_(torch.cat(locs, dim=-2))
+
+    def any_failed(self, failed: bool) -> bool:
+        return bool(failed)
 
 
 class DistComm:
@@ -166,11 +173,23 @@ class DistComm:
         return [recv]
 
     def allreduce_max(self, vals):
+        """Max over ranks.  NaN becomes +inf first, so a rank's non-finite value reaches every
+        rank whatever the backend does with NaN under MAX.  NCCL reduces device tensors only:
+        a host input (e.g. a departure reach computed on the host) travels to the rank's
+        device and the result comes back to the input's device."""
         (v,) = vals
-        t = torch.as_tensor(v).clone()
+        t = _nan_to_inf(torch.as_tensor(v)).clone()
         if self.size > 1:
+            home = t.device
+            if self.dist.get_backend(self.group) == "nccl" and t.device.type != "cuda":
+                t = t.to(torch.device("cuda", torch.cuda.current_device()))
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+            t = t.to(home)
         return [t]
+
+    def any_failed(self, failed: bool) -> bool:
+        """True on every rank when any rank reports a failure (the callbacks' common verdict)."""
+        return bool(self.allreduce_max([torch.tensor(1.0 if failed else 0.0)])[0].item() > 0.0)
 
     def allgather_rows(self, locs, out):
         (loc,) = locs
@@ -586,9 +605,22 @@ class SlabFineOperator:
         L = self.L
         return [f[:, q * L:(q + 1) * L].contiguous() for q in self.comm.ranks]
 
+    def _verdict(self, failed: bool) -> int:
+        """Every rank returns the same status: the driver aborts on all ranks together instead
+        of one rank leaving while the others wait in its next collective."""
+        try:
+            anyf = self.comm.any_failed(failed)
+        except BaseException as e:  # the verdict itself failed: fail locally
+            self.error = self.error or e
+            return 1
+        if anyf and self.error is None:
+            self.error = RuntimeError("slab fine operator failed on another rank")
+        return 1 if anyf else 0
+
     def _build(self, _user, vptr, nt):
         import time
 
+        failed = False
         try:
             t0 = time.perf_counter()
             self.S = None
@@ -596,24 +628,25 @@ class SlabFineOperator:
                                        self.norm, self.beta)
             self.builds += 1
             self.build_s += time.perf_counter() - t0
-            return 0
         except BaseException as e:  # re-raised by api.newton_solve
             self.error = e
-            return 1
+            failed = True
+        return self._verdict(failed)
 
     def _data_term(self, _user, vtptr, bptr):
         import time
 
+        failed = False
         try:
             t0 = time.perf_counter()
             outs = self.S.apply(self._slabs(self._full(vtptr)), data_term_only=True)
             self.comm.allgather_rows(outs, self._full(bptr))
             self.matvecs += 1
             self.apply_s += time.perf_counter() - t0
-            return 0
         except BaseException as e:
             self.error = e
-            return 1
+            failed = True
+        return self._verdict(failed)
 
 
 class _DeviceView:
