@@ -189,3 +189,19 @@ def test_oracle_vs_compiled_reference_random(ref):
     r1 = c.two_level(x[0], x[1], 1, 10, 0.1, 0.5, 1.0, 4.0)
     r2 = O.two_level(x[0], x[1], co, 1, 10, 0.1, 0.5, 1.0, 4.0)
     assert rel(r2[0], r1[0]) < 1e-12
+
+
+def test_reference_default_path_golden_reproducible():
+    """The round-2 default-path goldens (tests/golden/make_golden_r2.py: newtonSolve without
+    ntOverride, PrecondKind::Reg, config 1) are what the compiled reference produces now."""
+    from oracle import ref
+    from paper_1604_02153_b200 import synth
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    d = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "newton_default.npz")))
+    mT, (v1, v2) = synth.config12_fields(64)
+    mR = ref.solve_state_final(v1, v2, 4, mT)
+    _, _, rep, s = ref.newton_solve(mR, mT, 2, 1e-2, 0, nt=0, two_level=False, cheb=False, tol_rel=1e-2)
+    assert np.array_equal(s, d["cfg1_reg_summary"])
+    assert np.array_equal(rep, d["cfg1_reg_records"])
