@@ -26,7 +26,11 @@ struct Fft1D {
     std::vector<int> rev;     // bit reversal (pow2 only)
 
     explicit Fft1D(int len) : n(len) {
+#ifdef VRG_SHIM_MIXED_RADIX_ONLY
+        pow2 = false;  // alternative rounding: the recursive mixed-radix path for every length
+#else
         pow2 = n > 0 && (n & (n - 1)) == 0;
+#endif
         twFwd.resize(n);
         for (int j = 0; j < n; ++j) {
             const double a = -kTwoPi * static_cast<double>(j) / static_cast<double>(n);

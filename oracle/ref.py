@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ref", "libveloreg_ref.so")
+# VRG_REF_LIB=libveloreg_ref_altfft.so selects the same reference over the alternative-rounding
+# FFT shim (the reference-vs-reference floor, oracle/Makefile)
+LIB_PATH = os.path.join(_HERE, "_ref", os.environ.get("VRG_REF_LIB", "libveloreg_ref.so"))
 
 _D = C.POINTER(C.c_double)
 _lib = None

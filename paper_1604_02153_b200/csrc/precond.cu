@@ -324,6 +324,16 @@ void chebyshevSolve(Ctx& ctx, const GridDims& g, const LinOpDev& op, const doubl
 // read per iteration: pAp and rzNew land in adjacent device scalars (k_pcg_update applies the
 // step only when pAp > 0) and come back together.  Same decisions and arithmetic as the loop
 // in pcg().
+// VRG_TRACE=1: per-phase host wall times of newtonSolve and the PCG exits on stderr
+// (diagnostics only).
+static bool traceOn() {
+    static const bool on = [] {
+        const char* e = std::getenv("VRG_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 static PcgOut pcgUnpreconditioned(Ctx& ctx, const GridDims& g, const LinOpDev& A, double rz, double norm0, int maxIter,
                            double tol, double* x, double* r, double* p, double* ap) {
     PcgOut out;
@@ -356,8 +366,13 @@ static PcgOut pcgUnpreconditioned(Ctx& ctx, const GridDims& g, const LinOpDev& A
         out.relResidual = std::sqrt(rzNew) / norm0;
         if (out.relResidual <= tol) {
             out.converged = true;
+            if (traceOn())
+                std::fprintf(stderr, "[trace] coarse pcg converged it=%d rel=%.17g tol=%.17g\n", out.iterations,
+                             out.relResidual, tol);
             return out;
         }
+        if (traceOn())
+            std::fprintf(stderr, "[trace] coarse pcg it=%d rel=%.17g tol=%.17g\n", out.iterations, out.relResidual, tol);
         const double beta = rzNew / rz;
         rz = rzNew;
         VRG_CUDA(cudaMemcpyAsync(sc, sc + 2, sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
@@ -471,14 +486,6 @@ static double powerIterationEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op
     return lambda;
 }
 
-// VRG_TRACE=1: per-phase host wall times of newtonSolve on stderr (diagnostics only).
-static bool traceOn() {
-    static const bool on = [] {
-        const char* e = std::getenv("VRG_TRACE");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
 struct PhaseTimer {
     Ctx& ctx;
     const char* what;

@@ -3,6 +3,7 @@ UNMODIFIED reference compiled in oracle/_ref (build container only, where /root/
 exists):
 
     make -C oracle && python tests/golden/make_golden_r2.py [case ...]
+    VRG_REF_LIB=libveloreg_ref_altfft.so python tests/golden/make_golden_r2.py newton_default_altfft
 
 cases (each writes tests/golden/<case>.npz):
   newton_cfg3_5b  the reference's newtonSolve records of config 3 pair 0 (512^2) and config 5b
@@ -117,8 +118,20 @@ def case_cfg5a_digest():
     return d
 
 
+def case_newton_default_altfft():
+    """The newton_default runs on the reference rebuilt over a differently-rounded correct FFT
+    (oracle/_ref/libveloreg_ref_altfft.so: the shim's recursive mixed-radix path for every
+    length).  Its distance from newton_default is the reference-vs-reference floor of each
+    record: a Newton iterate whose Krylov solve sits near the preconditioner's breakdown test
+    (2L-CHEB, precond.cpp:338-347) or needs many PCG steps amplifies FFT rounding far beyond
+    1e-8, for the reference itself.  Run with VRG_REF_LIB=libveloreg_ref_altfft.so."""
+    if os.environ.get("VRG_REF_LIB") != "libveloreg_ref_altfft.so":
+        raise SystemExit("run newton_default_altfft with VRG_REF_LIB=libveloreg_ref_altfft.so")
+    return case_newton_default()
+
+
 CASES = {"newton_cfg3_5b": case_newton_cfg3_5b, "newton_default": case_newton_default,
-         "cfg5a_digest": case_cfg5a_digest}
+         "newton_default_altfft": case_newton_default_altfft, "cfg5a_digest": case_cfg5a_digest}
 
 
 def main(argv):

@@ -104,18 +104,25 @@ def test_config4_bench_inputs_vs_reference(ctx, api, ref, bench_mod):
 
 
 # ------------------------------------------------------------------ configs 3 and 5b (batched pairs)
-def _check_records(recs, summ, rrec, rsum, tol=1e-8):
+def _check_records(recs, summ, rrec, rsum, tol=1e-8, alt=None):
+    """Identical Newton / Krylov / line-search counts and step lengths; per-iteration objective
+    and ||g||_inf (on the ||g_0|| scale the solver stops on, newton.cpp:62) within `tol`, or
+    within 10x the reference-vs-reference floor where that is larger: `alt` = the same solve's
+    records from the reference over another correct FFT (tests/golden/make_golden_r2.py)."""
     assert summ["status"] == int(rsum[0])
     assert summ["iterations"] == int(rsum[1])
     g0 = rrec[0][1]
-    for r, q in zip(recs, rrec):
+    arec, asum = alt if alt is not None else (rrec, rsum)
+    for r, q, a in zip(recs, rrec, arec):
         assert r["innerIterations"] == int(q[5]), (r, q)
         assert r["lineSearchSteps"] == int(q[6]), (r, q)
         assert r["stepLength"] == q[7]
-        assert abs(r["objective"] - q[3]) <= tol * abs(q[3])
-        assert abs(r["gradNormInf"] - q[1]) <= tol * g0
-    assert abs(summ["finalGradNormRel"] - rsum[2]) <= tol
-    assert abs(summ["finalResidualRel"] - rsum[3]) <= tol * rsum[3]
+        tj = max(tol, 10.0 * abs(a[3] - q[3]) / abs(q[3]))
+        tg = max(tol, 10.0 * abs(a[1] - q[1]) / g0)
+        assert abs(r["objective"] - q[3]) <= tj * abs(q[3]), (int(q[0]), r["objective"], q[3], tj)
+        assert abs(r["gradNormInf"] - q[1]) <= tg * g0, (int(q[0]), r["gradNormInf"], q[1], tg)
+    assert abs(summ["finalGradNormRel"] - rsum[2]) <= max(tol, 10.0 * abs(asum[2] - rsum[2]))
+    assert abs(summ["finalResidualRel"] - rsum[3]) <= max(tol, 10.0 * abs(asum[3] - rsum[3]) / rsum[3]) * rsum[3]
 
 
 PAIRS = [("cfg3_p0", 512, 0), ("cfg5b_p0", 256, 0), ("cfg5b_p1", 256, 1), ("cfg5b_p2", 256, 2), ("cfg5b_p3", 256, 3)]
@@ -143,7 +150,11 @@ def test_default_path_registration_vs_reference(ctx, api, ref, name):
     """No ntOverride: nt = max(ratchet, deriveSteps(v, cfl=1)) per outer iteration
     (newton.cpp:49-52, the ceil of transport.cpp:48), so the step count grows with v and the
     carried line-search state is reused only when it matches (newton.cpp:54-55).  PrecondKind::Reg
-    is the library default (precond.hpp:17): M^{-1/2} splitting, no coarse grid."""
+    is the library default (precond.hpp:17): M^{-1/2} splitting, no coarse grid.  The last
+    iterate of the config 2 solves is FFT-sensitive for the reference itself: rebuilt over a
+    differently-rounded correct FFT it moves by 9.7e-5 (2L-CHEB: its Krylov solve sits at the
+    preconditioner's breakdown test and re-estimates e_max) and 5.8e-9 in J (REG, 8 PCG steps),
+    so those records are held to 10x that measured floor; all other records to 1e-8."""
     d = gold("newton_default")
     n, norm, beta, two_level, cheb = d[name + "_meta"]
     n, norm = int(n), int(norm)
@@ -153,7 +164,9 @@ def test_default_path_registration_vs_reference(ctx, api, ref, name):
     _, _, recs, summ = api.newton_solve(ctx, mR, mT, norm, float(beta), api.COMPRESSIBLE, nt=0, kind=kind,
                                         coarse_solver=api.COARSE_CHEB if cheb else api.COARSE_PCG, cheb_iters=10,
                                         tol_rel=1e-2)
-    _check_records(recs, summ, d[name + "_records"], d[name + "_summary"])
+    alt = gold("newton_default_altfft")
+    _check_records(recs, summ, d[name + "_records"], d[name + "_summary"],
+                   alt=(alt[name + "_records"], alt[name + "_summary"]))
 
 
 # ------------------------------------------------------------------ config 5a (4096^2 digest)
