@@ -49,6 +49,48 @@ extern "C" {
 #define VRG_BAND_LOW 0 /* spectral::Band (spectral.hpp:44) */
 #define VRG_BAND_HIGH 1
 
+/* inverse::Model (inverse.hpp:18-23), passed per call to the _ex entry points: the legacy entry
+ * points take norm / beta / deformation as arguments and betaW / the scheme from the context
+ * (vrg_set_penalty_weight, vrg_set_scheme); the _ex ones take everything per call, so operators
+ * with different models can share one context. */
+typedef struct vrg_model_s {
+    int norm;          /* VRG_H1SEMI .. VRG_H3SEMI (spectral::RegNorm) */
+    double beta_v;     /* Model::betaV */
+    int deformation;   /* VRG_COMPRESSIBLE, VRG_INCOMPRESSIBLE, VRG_NEAR_INCOMPRESSIBLE */
+    double beta_w;     /* Model::betaW (near-incompressible penalty weight), default 0.1 */
+} vrg_model;
+/* transport::SchemeConfig (transport.hpp:23-27) */
+typedef struct vrg_scheme_cfg_s {
+    int scheme;        /* VRG_SCHEME_SL / _RK2 / _RK2A */
+    double cfl;
+    int nt_override;   /* 0 = none (CFL-derived step count) */
+} vrg_scheme_cfg;
+/* inverse::NewtonConfig (inverse.hpp:25-41) */
+typedef struct vrg_newton_cfg_s {
+    int max_outer_iter;        /* 50 */
+    double tol_rel_grad;       /* 1e-2 */
+    double tol_abs_grad;       /* 1e-5 */
+    int max_inner_iter;        /* 500 */
+    double forcing_cap;        /* 0.5 */
+    double ls_c1;              /* 1e-4 */
+    double ls_shrink;          /* 0.5 */
+    int ls_max_steps;          /* 20 */
+    int hessian_mode;          /* VRG_GAUSS_NEWTON / VRG_FULL_NEWTON */
+    vrg_scheme_cfg grad_scheme;  /* {SL, 1.0, none} */
+    int has_hess_scheme;       /* NewtonConfig::hessScheme engaged (0: the gradient's) */
+    vrg_scheme_cfg hess_scheme;
+} vrg_newton_cfg;
+/* precond::PrecondChoice (precond.hpp:19-27) */
+typedef struct vrg_precond_choice_s {
+    int kind;                  /* 0 Reg (default), 1 TwoLevel */
+    int coarse_solver;         /* 0 Pcg, 1 Cheb (default) */
+    double eps_scale;          /* 0.1 */
+    int cheb_iters;            /* 10 */
+    int has_eig;               /* eigEstimate engaged */
+    double emin, emax;
+    int reestimate_each_iteration;
+} vrg_precond_choice;
+
 typedef struct vrg_ctx_s* vrg_ctx_t;
 typedef struct vrg_solver_s* vrg_solver_t;
 typedef struct vrg_hess_s* vrg_hess_t;
@@ -103,6 +145,12 @@ int vrg_trace(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2,
               double* x1, double* x2); /* traceCharacteristics, transport.hpp:49 */
 /* transport::Solver (transport.hpp:71-100), scheme SL. */
 int vrg_solver_create(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, int nt, vrg_solver_t* out);
+/* transport::Solver(v, TimeGrid(nt), SchemeConfig{scheme}) with the scheme given per call */
+int vrg_solver_create_ex(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, int nt, int scheme,
+                         vrg_solver_t* out);
+/* TransportSolution::stages (transport.hpp:61-66): the nt Heun predictor fields of the solver's
+ * last state / adjoint solve (RK2 / RK2A; VRG_NOT_SUPPORTED for SL, whose stages are empty) */
+int vrg_solver_stages(vrg_solver_t s, double* out);
 void vrg_solver_destroy(vrg_solver_t s);
 int vrg_solver_state(vrg_solver_t s, const double* m0, double* traj);        /* solveState */
 int vrg_solver_adjoint(vrg_solver_t s, const double* lam1, double* traj);    /* solveAdjoint */
@@ -139,6 +187,13 @@ int vrg_body_force(vrg_ctx_t ctx, int n1, int n2, int nt, const double* state_tr
 int vrg_hess_create(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
                     const double* mT, int norm, double beta, int deformation, int nt, int mode,
                     const double* state_traj, vrg_hess_t* out);
+/* inverse::HessianOperator(v, problem, model, TimeGrid(nt), SchemeConfig{scheme}, mode, state,
+ * adjoint) (inverse.hpp:74-80): model and scheme per call; state_traj / adjoint_traj (nullable)
+ * are the reused trajectories (inverse.cpp:162-172), copied; the adjoint is used in full-Newton
+ * mode only.  RK2 / RK2A predictor fields are recomputed from the nodes (same arithmetic). */
+int vrg_hess_create_ex(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                       const double* mT, const vrg_model* model, int scheme, int nt, int mode,
+                       const double* state_traj, const double* adjoint_traj, vrg_hess_t* out);
 void vrg_hess_destroy(vrg_hess_t h);
 int vrg_hess_apply(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);      /* apply */
 int vrg_hess_apply_data(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2); /* applyDataTerm */
@@ -201,6 +256,20 @@ int vrg_evaluate_gradient(vrg_ctx_t ctx, int n1, int n2, const double* v1, const
 int vrg_evaluate_objective(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
                            const double* mT, int norm, double beta, int deformation, int nt, double* scalars);
 
+/* evaluateGradient(v, problem, model, TimeGrid(nt), {scheme}, reuseState) (inverse.hpp:65-68,
+ * inverse.cpp:119-148) with every GradientResult member: g, bodyForce (before the Leray
+ * projection), state and adjoint trajectories ((nt+1) fields each) and their Heun predictor
+ * fields (nt fields each, RK2 / RK2A only); scalars = [objective, mismatch, regTerm, penaltyTerm].
+ * reuse_state and every output except g1/g2/scalars are nullable. */
+int vrg_evaluate_gradient_ex(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                             const double* mT, const vrg_model* model, int scheme, int nt, const double* reuse_state,
+                             double* g1, double* g2, double* body /* [b1 | b2] */, double* state_traj,
+                             double* state_stages, double* adjoint_traj, double* adjoint_stages, double* scalars);
+/* evaluateObjective (inverse.hpp:60-63, inverse.cpp:96-117): ObjectiveResult with the state */
+int vrg_evaluate_objective_ex(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                              const double* mT, const vrg_model* model, int scheme, int nt, double* state_traj,
+                              double* state_stages, double* scalars);
+
 /* ---- precond (precond.hpp:25-95) ---- */
 /* problems::randomBandLimitedField (problems.hpp:45): libstdc++ mt19937_64 + normal draws */
 int vrg_random_bandlimited_field(vrg_ctx_t ctx, int n1, int n2, unsigned long long seed, double* out);
@@ -241,6 +310,12 @@ int vrg_newton_solve(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, const
                      double beta, int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
                      const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
                      double* summary);
+
+/* newtonSolve with the whole NewtonConfig (hessScheme included) and PrecondChoice per call;
+ * records / summary as for vrg_newton_solve */
+int vrg_newton_solve_ex(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, const double* mT_host,
+                        const vrg_model* model, const vrg_newton_cfg* cfg, const vrg_precond_choice* pc,
+                        double* v1_host, double* v2_host, double* records, int records_cap, double* summary);
 
 /* ---- external fine operator (the precond::LinOp plug-in point, precond.hpp:25, as used by
  * solveKkt's split Hessian, precond.cpp:20-26,313).  While set, vrg_newton_solve does not build

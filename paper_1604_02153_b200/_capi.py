@@ -46,6 +46,8 @@ _SIG = {
     "vrg_derive_steps": ("piippdp", C.c_int),
     "vrg_trace": ("piippdipp", C.c_int),
     "vrg_solver_create": ("piippip", C.c_int),
+    "vrg_solver_create_ex": ("piippiip", C.c_int),
+    "vrg_solver_stages": ("pp", C.c_int),
     "vrg_solver_destroy": ("p", None),
     "vrg_solver_state": ("ppp", C.c_int),
     "vrg_solver_adjoint": ("ppp", C.c_int),
@@ -66,6 +68,7 @@ _SIG = {
     "vrg_cutoff": ("piipip", C.c_int),
     "vrg_gaussian_smooth": ("piipdp", C.c_int),
     "vrg_hess_create": ("piippppidiiipp", C.c_int),
+    "vrg_hess_create_ex": ("piipppppiiippp", C.c_int),
     "vrg_hess_destroy": ("p", None),
     "vrg_hess_apply": ("ppppp", C.c_int),
     "vrg_hess_apply_data": ("ppppp", C.c_int),
@@ -80,6 +83,8 @@ _SIG = {
     "vrg_slab_cols": ("piipp", C.c_int),
     "vrg_slab_step": ("piiiiiippppiddpppp", C.c_int),
     "vrg_evaluate_gradient": ("piippppidiippp", C.c_int),
+    "vrg_evaluate_gradient_ex": ("piipppppiippppppppp", C.c_int),
+    "vrg_evaluate_objective_ex": ("piipppppiippp", C.c_int),
     "vrg_evaluate_objective": ("piippppidiip", C.c_int),
     "vrg_random_bandlimited_field": ("piiup", C.c_int),
     "vrg_coarse_create": ("piippppididp", C.c_int),
@@ -90,6 +95,7 @@ _SIG = {
     "vrg_estimate_eigs": ("piippppididupp", C.c_int),
     "vrg_solve_kkt": ("pppdippppppdppp", C.c_int),
     "vrg_newton_solve": ("piippidipppppppip", C.c_int),
+    "vrg_newton_solve_ex": ("piippppppppip", C.c_int),
     "vrg_set_fine_operator": ("pppp", C.c_int),
 }
 

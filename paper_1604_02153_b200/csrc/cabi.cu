@@ -106,6 +106,17 @@ vrg::Model modelOf(int norm, double beta, int deformation) {
     return m;
 }
 
+// Model and scheme given per call (the _ex entry points): no context state involved.
+vrg::Model modelEx(const vrg_model* m, int scheme) {
+    if (!m) throw vrg::InvalidArgument("null model");
+    if (scheme < VRG_SCHEME_SL || scheme > VRG_SCHEME_RK2A) throw vrg::InvalidArgument("unknown transport scheme");
+    if (!(m->beta_w >= 0.0)) throw vrg::InvalidArgument("near-incompressible penalty weight must be >= 0");
+    vrg::Model r = modelOf(m->norm, m->beta_v, m->deformation);
+    r.betaW = m->beta_w;
+    r.scheme = scheme;
+    return r;
+}
+
 }  // namespace
 
 extern "C" {
@@ -296,6 +307,29 @@ int vrg_solver_create(vrg_ctx_t c, int n1, int n2, const double* v1, const doubl
             h->stages.alloc(sizeof(double) * nt * dims(n1, n2).points());
         }
         *out = h;
+    });
+}
+
+int vrg_solver_create_ex(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, int nt, int scheme,
+                         vrg_solver_t* out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        if (scheme < VRG_SCHEME_SL || scheme > VRG_SCHEME_RK2A) throw vrg::InvalidArgument("unknown transport scheme");
+        auto* h = new vrg_solver_s{c, vrg::Solver(c->ctx, dims(n1, n2), v1, v2, nt), nullptr, vrg::DBuf()};
+        if (scheme != VRG_SCHEME_SL) {
+            h->heun = std::make_unique<vrg::HeunTransport>(c->ctx, dims(n1, n2), v1, v2, nt,
+                                                           scheme == VRG_SCHEME_RK2A);
+            h->stages.alloc(sizeof(double) * nt * dims(n1, n2).points());
+        }
+        *out = h;
+    });
+}
+
+int vrg_solver_stages(vrg_solver_t s, double* out) {
+    return guarded(s->owner, [&] {
+        if (!s->heun) throw vrg::NotSupported("Heun predictor fields exist for the RK2 / RK2A schemes only");
+        vrg::copy(s->solver.ctx, static_cast<std::size_t>(s->solver.nt) * s->solver.g.points(), s->stages.d(), out);
+        s->solver.ctx.sync();
     });
 }
 
@@ -505,6 +539,21 @@ int vrg_hess_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double*
     });
 }
 
+int vrg_hess_create_ex(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                       const double* mT, const vrg_model* model, int scheme, int nt, int mode, const double* state,
+                       const double* adjoint, vrg_hess_t* out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        if (mode != VRG_GAUSS_NEWTON && mode != VRG_FULL_NEWTON)
+            throw vrg::InvalidArgument("HessianOperator: unknown Hessian mode");
+        const vrg::Model m = modelEx(model, scheme);
+        *out = new vrg_hess_s{c, vrg::Hessian(c->ctx, dims(n1, n2), v1, v2, mR, mT, m, nt, state,
+                                              mode == VRG_FULL_NEWTON ? 1 : 0,
+                                              mode == VRG_FULL_NEWTON ? adjoint : nullptr),
+                              vrg::DBuf()};
+    });
+}
+
 void vrg_hess_destroy(vrg_hess_t h) {
     if (!h) return;
     vrg::AllocStreamScope as_(h->owner->ctx.stream);  // stream-ordered release into the pool
@@ -641,17 +690,44 @@ int vrg_evaluate_gradient(vrg_ctx_t c, int n1, int n2, const double* v1, const d
                           const double* mT, int norm, double beta, int deformation, int nt, double* g1, double* g2,
                           double* scalars) {
     return guarded(c, [&] {
+        double sc[4];
         vrg::evaluateGradient(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation), nt, g1, g2,
-                              scalars, nullptr, nullptr, nullptr);
+                              sc, nullptr, nullptr, nullptr);
         c->ctx.sync();
+        std::copy(sc, sc + 3, scalars);
     });
 }
 
 int vrg_evaluate_objective(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
                            const double* mT, int norm, double beta, int deformation, int nt, double* scalars) {
     return guarded(c, [&] {
-        vrg::evaluateObjective(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation), nt, scalars,
+        double sc[4];
+        vrg::evaluateObjective(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelOf(norm, beta, deformation), nt, sc,
                                nullptr);
+        c->ctx.sync();
+        std::copy(sc, sc + 3, scalars);
+    });
+}
+
+int vrg_evaluate_gradient_ex(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                             const double* mT, const vrg_model* model, int scheme, int nt, const double* reuse_state,
+                             double* g1, double* g2, double* body, double* state, double* state_stages,
+                             double* adjoint, double* adjoint_stages, double* scalars) {
+    return guarded(c, [&] {
+        if (nt < 1) throw vrg::InvalidArgument("TimeGrid: nt must be >= 1");
+        vrg::evaluateGradient(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelEx(model, scheme), nt, g1, g2, scalars,
+                              state, adjoint, reuse_state, nullptr, body, state_stages, adjoint_stages);
+        c->ctx.sync();
+    });
+}
+
+int vrg_evaluate_objective_ex(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
+                              const double* mT, const vrg_model* model, int scheme, int nt, double* state,
+                              double* state_stages, double* scalars) {
+    return guarded(c, [&] {
+        if (nt < 1) throw vrg::InvalidArgument("TimeGrid: nt must be >= 1");
+        vrg::evaluateObjective(c->ctx, dims(n1, n2), v1, v2, mR, mT, modelEx(model, scheme), nt, scalars, state,
+                               state_stages);
         c->ctx.sync();
     });
 }
@@ -794,33 +870,20 @@ int vrg_set_fine_operator(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_te
     });
 }
 
-int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const double* mT_host, int norm, double beta,
-                     int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
-                     const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
-                     double* summary) {
-    return guarded(c, [&] {
+namespace {
+void newtonToHost(vrg_ctx_s* c, int n1, int n2, const double* mR_host, const double* mT_host, const vrg::Model& model,
+                  const vrg::NewtonConfig& cfg, const vrg::PrecondChoice& pc, double* v1_host, double* v2_host,
+                  double* records, int records_cap, double* summary) {
+    {
         vrg::Ctx& ctx = c->ctx;
         const auto g = dims(n1, n2);
         const std::size_t N = g.points();
+        if (cfg.hessianMode != VRG_GAUSS_NEWTON && cfg.hessianMode != VRG_FULL_NEWTON)
+            throw vrg::InvalidArgument("newtonSolve: unknown Hessian mode");
         vrg::DBuf img(sizeof(double) * 2 * N), v(sizeof(double) * 2 * N);
         VRG_CUDA(cudaMemcpyAsync(img.d(), mR_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
         VRG_CUDA(cudaMemcpyAsync(img.d() + N, mT_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
-        vrg::NewtonConfig cfg;
-        cfg.maxOuterIter = cfg_int[0];
-        cfg.maxInnerIter = cfg_int[1];
-        cfg.ntOverride = cfg_int[2];
-        cfg.lsMaxSteps = cfg_int[3];
-        cfg.hessianMode = cfg_int[4];
-        if (cfg.hessianMode != VRG_GAUSS_NEWTON && cfg.hessianMode != VRG_FULL_NEWTON)
-            throw vrg::InvalidArgument("newtonSolve: unknown Hessian mode");
-        cfg.tolRelGrad = cfg_dbl[0];
-        cfg.tolAbsGrad = cfg_dbl[1];
-        cfg.forcingCap = cfg_dbl[2];
-        cfg.lsC1 = cfg_dbl[3];
-        cfg.lsShrink = cfg_dbl[4];
-        cfg.gradCfl = cfg_dbl[5];
-        const auto rep = vrg::newtonSolve(ctx, g, img.d(), img.d() + N, modelOf(norm, beta, deformation), cfg,
-                                          choiceOf(pc_int, pc_dbl), v.d());
+        const auto rep = vrg::newtonSolve(ctx, g, img.d(), img.d() + N, model, cfg, pc, v.d());
         VRG_CUDA(cudaMemcpyAsync(v1_host, v.d(), sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
         VRG_CUDA(cudaMemcpyAsync(v2_host, v.d() + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
         ctx.sync();
@@ -848,6 +911,72 @@ int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const d
         summary[4] = rep.jacMin;
         summary[5] = rep.jacMax;
         summary[6] = rep.totalTimeSec;
+    }
+}
+}  // namespace
+
+int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const double* mT_host, int norm, double beta,
+                     int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
+                     const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
+                     double* summary) {
+    return guarded(c, [&] {
+        vrg::NewtonConfig cfg;
+        cfg.maxOuterIter = cfg_int[0];
+        cfg.maxInnerIter = cfg_int[1];
+        cfg.ntOverride = cfg_int[2];
+        cfg.lsMaxSteps = cfg_int[3];
+        cfg.hessianMode = cfg_int[4];
+        cfg.tolRelGrad = cfg_dbl[0];
+        cfg.tolAbsGrad = cfg_dbl[1];
+        cfg.forcingCap = cfg_dbl[2];
+        cfg.lsC1 = cfg_dbl[3];
+        cfg.lsShrink = cfg_dbl[4];
+        cfg.gradCfl = cfg_dbl[5];
+        newtonToHost(c, n1, n2, mR_host, mT_host, modelOf(norm, beta, deformation), cfg, choiceOf(pc_int, pc_dbl),
+                     v1_host, v2_host, records, records_cap, summary);
+    });
+}
+
+int vrg_newton_solve_ex(vrg_ctx_t c, int n1, int n2, const double* mR_host, const double* mT_host,
+                        const vrg_model* model, const vrg_newton_cfg* cfg, const vrg_precond_choice* pc,
+                        double* v1_host, double* v2_host, double* records, int records_cap, double* summary) {
+    return guarded(c, [&] {
+        if (!cfg || !pc) throw vrg::InvalidArgument("null Newton or preconditioner configuration");
+        const vrg_scheme_cfg& gs = cfg->grad_scheme;
+        if (gs.nt_override < 0 || (cfg->has_hess_scheme && cfg->hess_scheme.nt_override < 0))
+            throw vrg::InvalidArgument("TimeGrid: nt must be >= 1");
+        vrg::NewtonConfig nc;
+        nc.maxOuterIter = cfg->max_outer_iter;
+        nc.tolRelGrad = cfg->tol_rel_grad;
+        nc.tolAbsGrad = cfg->tol_abs_grad;
+        nc.maxInnerIter = cfg->max_inner_iter;
+        nc.forcingCap = cfg->forcing_cap;
+        nc.lsC1 = cfg->ls_c1;
+        nc.lsShrink = cfg->ls_shrink;
+        nc.lsMaxSteps = cfg->ls_max_steps;
+        nc.hessianMode = cfg->hessian_mode;
+        nc.gradCfl = gs.cfl;
+        nc.ntOverride = gs.nt_override;
+        nc.hasHessScheme = cfg->has_hess_scheme != 0;
+        if (nc.hasHessScheme) {
+            const vrg_scheme_cfg& hs = cfg->hess_scheme;
+            if (hs.scheme < VRG_SCHEME_SL || hs.scheme > VRG_SCHEME_RK2A)
+                throw vrg::InvalidArgument("unknown transport scheme");
+            nc.hessScheme = hs.scheme;
+            nc.hessCfl = hs.cfl;
+            nc.hessNtOverride = hs.nt_override;
+        }
+        vrg::PrecondChoice ch;
+        ch.kind = pc->kind ? vrg::kPcTwoLevel : vrg::kPcReg;
+        ch.coarseSolver = pc->coarse_solver ? vrg::kCoarseCheb : vrg::kCoarsePcg;
+        ch.epsScale = pc->eps_scale;
+        ch.chebIters = pc->cheb_iters;
+        ch.hasEig = pc->has_eig != 0;
+        ch.eMin = pc->emin;
+        ch.eMax = pc->emax;
+        ch.reestimateEachIteration = pc->reestimate_each_iteration != 0;
+        newtonToHost(c, n1, n2, mR_host, mT_host, modelEx(model, gs.scheme), nc, ch, v1_host, v2_host, records,
+                     records_cap, summary);
     });
 }
 

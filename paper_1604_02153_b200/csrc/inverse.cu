@@ -975,7 +975,8 @@ void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, con
 // evaluateObjective / evaluateGradient (src/inverse.cpp:96-148) for the compressible and
 // incompressible models.  stateOut / adjOut (nullable) receive the trajectories.
 void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
-                       const double* mT, const Model& model, int nt, double* scalars, double* stateOut) {
+                       const double* mT, const Model& model, int nt, double* scalars, double* stateOut,
+                       double* stateStagesOut) {
     const std::size_t N = g.points();
     DBuf stateBuf;
     double* st = stateOut;
@@ -985,8 +986,9 @@ void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const doub
     }
     if (model.scheme != kSchemeSL) {
         HeunTransport heun(ctx, g, v1, v2, nt, model.scheme == kSchemeRK2A);
-        DBuf stages(sizeof(double) * nt * N);
-        heun.forward(mT, st, stages.d(), true);
+        DBuf stages;
+        if (!stateStagesOut) stages.alloc(sizeof(double) * nt * N);
+        heun.forward(mT, st, stateStagesOut ? stateStagesOut : stages.d(), true);
     } else {
         Solver solver(ctx, g, v1, v2, nt);
         solver.state(mT, st, true);
@@ -1004,11 +1006,13 @@ void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const doub
     scalars[0] = mismatch + regTerm + penalty;
     scalars[1] = mismatch;
     scalars[2] = regTerm;
+    scalars[3] = penalty;
 }
 
 void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
-                      double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut) {
+                      double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut,
+                      double* bodyOut, double* stateStagesOut, double* adjStagesOut) {
     const std::size_t N = g.points();
     DBuf stBuf, adBuf;
     double* st = stateOut;
@@ -1027,20 +1031,24 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
     if (model.scheme != kSchemeSL) {  // RK2 / RK2A: Heun solves, stage-paired body force
         const bool anti = model.scheme == kSchemeRK2A;
         HeunTransport heun(ctx, g, v1, v2, nt, anti);
-        DBuf stS(sizeof(double) * nt * N), adS(sizeof(double) * nt * N);
+        DBuf stB, adB;
+        if (!stateStagesOut) stB.alloc(sizeof(double) * nt * N);
+        if (!adjStagesOut) adB.alloc(sizeof(double) * nt * N);
+        double* stS = stateStagesOut ? stateStagesOut : stB.d();
+        double* adS = adjStagesOut ? adjStagesOut : adB.d();
         if (reuseState) {
             if (reuseState != st) copy(ctx, (nt + 1) * N, reuseState, st);
             const long long f0 = ctx.ffts;
-            heun.forwardStages(st, stS.d());
+            heun.forwardStages(st, stS);
             ctx.ffts = f0;
         } else {
-            heun.forward(mT, st, stS.d(), true);
+            heun.forward(mT, st, stS, true);
         }
         lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
         mismatch = 0.5 * dot(ctx, g, resid, nullptr, resid, nullptr);
         lincomb(ctx, N, -1.0, resid, 0.0, resid, resid);
-        heun.backward(resid, ad, adS.d(), true);
-        bodyForceHeun(ctx, g, nt, anti, st, stS.d(), ad, adS.d(), b, b + N);
+        heun.backward(resid, ad, adS, true);
+        bodyForceHeun(ctx, g, nt, anti, st, stS, ad, adS, b, b + N);
     } else {
         Solver solver(ctx, g, v1, v2, nt);
         if (reuseState) {
@@ -1066,12 +1074,14 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
         axpby(ctx, N, 1.0, pen, 1.0, g1);
         axpby(ctx, N, 1.0, pen + N, 1.0, g2);
     }
+    if (bodyOut) copy(ctx, 2 * N, b, bodyOut);
     if (model.deformation == kIncompressible) projectDivFree(ctx, g, b, b + N, b, b + N);
     axpby(ctx, N, 1.0, b, 1.0, g1);
     axpby(ctx, N, 1.0, b + N, 1.0, g2);
     scalars[0] = mismatch + regTerm + penalty;
     scalars[1] = mismatch;
     scalars[2] = regTerm;
+    scalars[3] = penalty;
 }
 
 }  // namespace vrg

@@ -137,10 +137,16 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
 
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
                double* b2, double* gradTrajOut = nullptr);  // gradTrajOut: keeps grad m_j ((nt+1) x 2N)
+// scalars[4] = [objective, mismatch, regTerm, penaltyTerm] (ObjectiveResult / GradientResult,
+// inverse.hpp:47-58).  Nullable outputs: the state (and adjoint) trajectories, their RK2 / RK2A
+// Heun predictor fields (nt fields each; ignored for SL), the body force before the Leray
+// projection (GradientResult::bodyForce, 2 fields), grad m_j of the SL state ((nt+1) x 2N).
 void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
-                       const double* mT, const Model& model, int nt, double* scalars, double* stateOut);
+                       const double* mT, const Model& model, int nt, double* scalars, double* stateOut,
+                       double* stateStagesOut = nullptr);
 void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
-                      double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut = nullptr);
+                      double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut = nullptr,
+                      double* bodyOut = nullptr, double* stateStagesOut = nullptr, double* adjStagesOut = nullptr);
 
 }  // namespace vrg

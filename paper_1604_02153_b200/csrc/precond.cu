@@ -773,7 +773,7 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
     DBuf carried, state, adjoint, grads;
     DBuf finalDeformed(sizeof(double) * N);
     copy(ctx, N, mT, finalDeformed.d());
-    double scal[3];
+    double scal[4];
 
     for (int iter = 0; iter < cfg.maxOuterIter; ++iter) {
         const auto tIter = std::chrono::steady_clock::now();
@@ -824,9 +824,19 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
             if (cfg.hessianMode != 0) throw NotSupported("external fine operator: Gauss-Newton mode only");
             ext = std::make_unique<ExternalFineOperator>(ctx, g, v, model, nt, weights);
         } else {
-            hess = std::make_unique<Hessian>(ctx, g, v, v + N, mR, mT, model, nt, state.d(), cfg.hessianMode,
-                                             cfg.hessianMode == 1 ? adjoint.d() : nullptr,
-                                             keepGrads ? grads.d() : nullptr);
+            // NewtonConfig::hessianScheme (newton.cpp:83-92): the gradient's discretization
+            // unless hessScheme is set; the state (and adjoint) are reused only when both
+            // the step count and the scheme agree
+            Model hmodel = model;
+            int hnt = nt;
+            if (cfg.hasHessScheme) {
+                hmodel.scheme = cfg.hessScheme;
+                hnt = cfg.hessNtOverride > 0 ? cfg.hessNtOverride : deriveSteps(ctx, g, v, v + N, cfg.hessCfl);
+            }
+            const bool same = hnt == nt && hmodel.scheme == model.scheme;
+            hess = std::make_unique<Hessian>(ctx, g, v, v + N, mR, mT, hmodel, hnt, same ? state.d() : nullptr,
+                                             cfg.hessianMode, (same && cfg.hessianMode == 1) ? adjoint.d() : nullptr,
+                                             (same && keepGrads) ? grads.d() : nullptr);
         }
         ptH.reset();
         // rhs = -g
@@ -863,7 +873,7 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
         for (; lsSteps < cfg.lsMaxSteps; ++lsSteps) {
             lincomb(ctx, 2 * N, 1.0, v, alpha, dv, trialBuf.d());
             bool blewUp = false;
-            double ob[3] = {0, 0, 0};
+            double ob[4] = {0, 0, 0, 0};
             try {
                 evaluateObjective(ctx, g, trialBuf.d(), trialBuf.d() + N, mR, mT, model, nt, ob, carried.d());
             } catch (const BlowupError&) {

@@ -124,6 +124,12 @@ struct NewtonConfig {
     double gradCfl = 1.0;
     int ntOverride = 0;  // 0 = CFL-derived
     int hessianMode = 0;  // 0 Gauss-Newton, 1 full Newton (NewtonConfig::hessianMode)
+    // NewtonConfig::hessScheme (inverse.hpp:35-40): the Hessian's own transport scheme and step
+    // count (CFL-derived from its own cfl unless hessNtOverride > 0); absent = gradient's
+    bool hasHessScheme = false;
+    int hessScheme = 0;
+    double hessCfl = 0.2;
+    int hessNtOverride = 0;
 };
 
 struct IterationRecord {

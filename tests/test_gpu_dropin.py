@@ -1,0 +1,94 @@
+"""The drop-in, built for real (paper_1604_02153_b200/dropin): the reference's own code over the
+device implementations of its hot-path modules.
+
+dropin/Makefile compiles the UNMODIFIED reference field / counters / fft / problems / precond /
+newton / io / diag sources with this repo's transport / inverse / spectral / interp pImpls and
+free functions over libvrg's C ABI (include/vrg.h) into dropin/_build/libveloreg_vrg.so, and
+links against it, unmodified:
+  * the reference's unit tests (proj/tests/test_*.cpp) -> every case passes on the GPU path;
+  * the reference's acceptance suite (proj/tests/acceptance/acceptance_main.cpp) -> C1-C11 pass;
+  * the reference's newtonSolve (dropin_newton.cpp) -> configs 1, 2 and 2-incompressible give the
+    pure reference's Newton / Krylov / line-search counts, FFT / interpolation counters and
+    objectives within 1e-8 (tests/golden/newton.npz).
+The binaries are built in the build container (where /root/reference exists) by
+__graft_entry__.build() and travel to the GPU box with the snapshot.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1604_02153_b200 import synth, vrf
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "paper_1604_02153_b200", "dropin", "_build")
+GOLD = os.path.join(ROOT, "tests", "golden")
+UNITS = ["test_interp", "test_spectral", "test_transport", "test_problems", "test_inverse", "test_precond",
+         "test_diag_io"]
+
+
+def _bin(name):
+    p = os.path.join(BUILD, name)
+    if not os.path.exists(p):
+        pytest.fail(f"{p} missing: build the drop-in (python -c 'import __graft_entry__ as g; g.build()')")
+    return p
+
+
+def _run(args, timeout):
+    return subprocess.run(args, capture_output=True, text=True, timeout=timeout, cwd=BUILD)
+
+
+@pytest.mark.parametrize("unit", UNITS)
+def test_reference_unit_tests_over_libvrg(ctx, unit):
+    """The reference's doctest suites, unmodified, with transport / inverse / spectral / interp
+    on the device: its analytic pins (half-cell shift, 4th-order convergence, overshoot,
+    rotation, SL full period, mass, stability, split-spectrum floor, KKT REG vs 2L, exact
+    interpolation counts, ...) hold for the GPU implementation."""
+    r = _run([_bin(unit)], 900)
+    assert r.returncode == 0 and "Status: SUCCESS" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+def test_reference_acceptance_over_libvrg(ctx):
+    """acceptance_main.cpp C1-C11 (adjoint consistency, gradient oracle, Hessian symmetry,
+    self-convergence, preconditioner effectiveness and correctness, eigenvalue scaling,
+    end-to-end inversion, interpolation counts) on the GPU path."""
+    r = _run([_bin("acceptance")], 1500)
+    out = r.stdout
+    assert r.returncode == 0 and "ACCEPTANCE PASS" in out, out[-4000:] + r.stderr[-2000:]
+    assert out.count("[PASS]") >= 11 and "[FAIL]" not in out
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg2_incomp"])
+def test_reference_newton_over_libvrg(ctx, ref, tmp_path, name):
+    """inverse::newtonSolve (newton.cpp:24-159) and precond::solveKkt (precond.cpp:291-358), the
+    reference's own objects, driving the device HessianOperator / evaluateGradient /
+    evaluateObjective / transport::Solver / CoarseOperator's operator: the pure reference's
+    iteration counts and operation counters, objectives within 1e-8."""
+    d = dict(np.load(os.path.join(GOLD, "newton.npz")))
+    n, nt, norm, beta, deform, cheb = d[name + "_meta"]
+    n, nt, norm, deform = int(n), int(nt), int(norm), int(deform)
+    mT, (v1, v2) = synth.config12_fields(n)
+    mR = ref.solve_state_final(v1, v2, nt, mT)
+    vrf.write_field(str(tmp_path / "mR.vrf"), mR)
+    vrf.write_field(str(tmp_path / "mT.vrf"), mT)
+    r = _run([_bin("dropin_newton"), str(tmp_path / "mR.vrf"), str(tmp_path / "mT.vrf"), str(norm), repr(float(beta)),
+              str(deform), str(nt), "2l", "cheb" if cheb else "pcg", "10", "1e-2"], 900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    recs, summ = [x for x in lines if "iter" in x], lines[-1]
+    rrec, rsum = d[name + "_records"], d[name + "_summary"]
+    assert summ["status"] == int(rsum[0]) and summ["iterations"] == int(rsum[1])
+    g0 = rrec[0][1]
+    for r_, q in zip(recs, rrec):
+        assert (r_["innerIterations"], r_["lineSearchSteps"]) == (int(q[5]), int(q[6])), (r_, q)
+        assert r_["stepLength"] == q[7]
+        assert (r_["ffts"], r_["interps"]) == (int(q[8]), int(q[9])), (r_, q)
+        assert abs(r_["objective"] - q[3]) <= 1e-8 * abs(q[3])
+        assert abs(r_["gradNormInf"] - q[1]) <= 1e-8 * g0
+    assert abs(summ["finalGradNormRel"] - rsum[2]) <= 1e-8
+    assert abs(summ["finalResidualRel"] - rsum[3]) <= 1e-8 * rsum[3]
