@@ -92,3 +92,35 @@ def test_reference_newton_over_libvrg(ctx, ref, tmp_path, name):
         assert abs(r_["gradNormInf"] - q[1]) <= 1e-8 * g0
     assert abs(summ["finalGradNormRel"] - rsum[2]) <= 1e-8
     assert abs(summ["finalResidualRel"] - rsum[3]) <= 1e-8 * rsum[3]
+
+
+@pytest.mark.parametrize("name", ["cfg1_reg", "cfg1_2lpcg", "cfg2_2lcheb", "cfg2_reg"])
+def test_reference_default_path_newton_over_libvrg(ctx, ref, tmp_path, name):
+    """The reference's default path (no ntOverride: the CFL ratchet; PrecondKind::Reg) through its
+    own newtonSolve over the drop-in: the pure reference's counts and counters, objectives within
+    1e-8 or 10x the measured reference-vs-reference floor (tests/golden/newton_default_altfft.npz)
+    where the reference itself is FFT-sensitive."""
+    d = dict(np.load(os.path.join(GOLD, "newton_default.npz")))
+    alt = dict(np.load(os.path.join(GOLD, "newton_default_altfft.npz")))
+    n, norm, beta, two_level, cheb = d[name + "_meta"]
+    n, norm = int(n), int(norm)
+    mT, (v1, v2) = synth.config12_fields(n)
+    mR = ref.solve_state_final(v1, v2, {64: 4, 256: 8}[n], mT)
+    vrf.write_field(str(tmp_path / "mR.vrf"), mR)
+    vrf.write_field(str(tmp_path / "mT.vrf"), mT)
+    r = _run([_bin("dropin_newton"), str(tmp_path / "mR.vrf"), str(tmp_path / "mT.vrf"), str(norm), repr(float(beta)),
+              "0", "0", "2l" if two_level else "reg", "cheb" if cheb else "pcg", "10", "1e-2"], 900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    recs, summ = [x for x in lines if "iter" in x], lines[-1]
+    rrec, rsum, arec = d[name + "_records"], d[name + "_summary"], alt[name + "_records"]
+    assert summ["status"] == int(rsum[0]) and summ["iterations"] == int(rsum[1])
+    g0 = rrec[0][1]
+    for r_, q, a in zip(recs, rrec, arec):
+        assert (r_["innerIterations"], r_["lineSearchSteps"]) == (int(q[5]), int(q[6])), (r_, q)
+        assert r_["stepLength"] == q[7]
+        assert (r_["ffts"], r_["interps"]) == (int(q[8]), int(q[9])), (r_, q)
+        tj = max(1e-8, 10.0 * abs(a[3] - q[3]) / abs(q[3]))
+        tg = max(1e-8, 10.0 * abs(a[1] - q[1]) / g0)
+        assert abs(r_["objective"] - q[3]) <= tj * abs(q[3]), (int(q[0]), r_["objective"], q[3])
+        assert abs(r_["gradNormInf"] - q[1]) <= tg * g0, (int(q[0]), r_["gradNormInf"], q[1])
