@@ -246,10 +246,12 @@ __device__ __forceinline__ void pdlWait() { asm volatile("griddepcontrol.wait;\n
 __device__ __forceinline__ void pdlTrigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // Which kernel families get the PDL attribute (bit 0: evaluate/pointwise, bit 1: prefilter);
-// the kernels' wait/trigger instructions are no-ops under a plain launch.  Evaluate/pointwise
-// only: measured on B200 at 1024^2 (matvecs/s) none 1093, evaluate 1112, prefilter 1034, both
-// 1049 -- early-launched prefilter blocks take SM slots from the gather they wait on.
-constexpr int kPdlMask = 1;
+// the kernels' wait/trigger instructions are no-ops under a plain launch.  Both families: the
+// band kernels and the column pass trigger their dependents only at their end, so an early
+// launched successor never takes SM slots from the tail of the kernel it waits on (measured on
+// B200 at 1024^2: SL state step 18.5 -> 16.4 us, column pass 6.2 -> 4.4 us back to back;
+// triggering at the start instead, with both families, made the matvec 4% slower).
+constexpr int kPdlMask = 3;
 
 template <class... KArgs, class... Args>
 void launchPdl(int family, void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t stream,

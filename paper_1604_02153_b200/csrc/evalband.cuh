@@ -54,10 +54,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
                                                             const double* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
                                                             BandWindow win = BandWindow{}) {
-    if (!kGather) {
-        pdlWait();
-        pdlTrigger();
-    }
+    if (!kGather) pdlWait();
     extern __shared__ __align__(16) double sm[];
     const int nc = n2 / kL;
     double* E = sm + nc * kCS;
@@ -100,10 +97,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
             xb = __ldg(x2 + r * n2 + t);
         }
         pre = epi.prefetch(r * n2 + t);
-        if (kGather) {
-            pdlWait();
-            pdlTrigger();
-        }
+        if (kGather) pdlWait();
     }
     for (int k = 0; k < per; ++k) {
         const int col = t + kBandThreads * k;
@@ -134,10 +128,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
 
             }
             cur = epi.prefetch(p);
-            if (kGather && k == 0) {
-                pdlWait();
-                pdlTrigger();
-            }
+            if (kGather && k == 0) pdlWait();
         }
         double val = 0.0;
         if (kGather) {
@@ -223,6 +214,7 @@ __global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, cons
         const int col = t + kBandThreads * k;
         dst[col] = sm[slot(col)];
     }
+    pdlTrigger();  // at the end: the dependent column pass must not take this kernel's slots
 }
 
 template <class Epi, bool kGather>

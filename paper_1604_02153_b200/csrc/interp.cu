@@ -496,8 +496,8 @@ __global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const doubl
                                                                      double* __restrict__ out, int n1, int n2) {
     __shared__ ColsShared<kR> sh;
     pdlWait();  // the input is the predecessor's output
-    pdlTrigger();
     pfColsReg<kR>(in, out, n1, n2, blockIdx.x, blockIdx.y, threadIdx.x, sh);
+    pdlTrigger();  // at the end (common.cuh kPdlMask)
 }
 
 template <int kR>
