@@ -49,8 +49,15 @@ struct BandWindow {
     unsigned* err = nullptr;
 };
 
+// Resident blocks per SM the band kernel is compiled for (register cap 65536 / (256 x value)):
+// 4 (64 registers) by default; an epilogue with more live state specialises it.
+template <class Epi>
+struct BandMinBlocks {
+    static constexpr int value = 4;
+};
+
 template <class Epi, bool kGather, bool kWindow = false>
-__global__ void __launch_bounds__(kBandThreads) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
+__global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
                                                             const double* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
                                                             BandWindow win = BandWindow{}) {

@@ -114,6 +114,15 @@ struct EpiIncSeed {
     }
 };
 
+}  // namespace
+// the last incremental-state step carries the seed's body-force operands too: 64 registers
+// spill 8 bytes, so it runs at 3 resident blocks (once per matvec)
+template <>
+struct BandMinBlocks<EpiIncSeed> {
+    static constexpr int value = 3;
+};
+namespace {
+
 
 }  // namespace
 
