@@ -299,8 +299,15 @@ def run_vrg(args, rank, world, local_rank):
 
     # SL transport unit: one SL state step m_j = I[m_{j-1}](X_D) at 1024^2 (config 4 unit ii)
     sl = sl_step_rate(ctx, H)
+    # logical operation counts of one steady-state apply (the reference's counters::, which it
+    # would execute) next to what the device executes (per-iterate invariants cached, the
+    # reference recomputes them in every apply): separates caching from hardware speed-up
+    ctx.reset_counters()
+    H.apply((vts[0][0], vts[0][1]), out=(out[0], out[1]))
+    ctx.sync()
+    logical = ctx.counters()
     return dict(value=value, ms=ms, launches=launches, clocks=clk, e2e=e2e_value, ms_e2e=ms_e2e, e2e_serial=e2e_serial,
-                wall_e2e=wall_e2e, prof=prof, sl=sl, kernels=kernels, ctx=ctx, api=api)
+                wall_e2e=wall_e2e, prof=prof, sl=sl, kernels=kernels, ctx=ctx, api=api, logical=logical)
 
 
 def ctypes_launches(ctx):
@@ -415,13 +422,44 @@ def run_reference(args, rank):
     value = threads * args.steps / dt
     sample = (f"each step = {threads} concurrent steady-state HessianOperator::apply calls (one per host thread) "
               f"of the unmodified reference, 1024^2 nt=16 H2, FFT backend = repo FFTW3-API shim")
+    fft = fft_backend_probe()
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(CONFIG, parallelism=f"pairs{args.gpus}"),  # the GPU arm's config at N=gpus
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                             "fft_backend": fft},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def fft_backend_probe():
+    """The reference's FFT on this host: libfftw3 is looked up with `ldconfig -p` (use it
+    if present); the reference as built here uses the repo's FFTW3-API shim (oracle/fftw_shim,
+    FFTW3 is not in the image), timed per 1024^2 transform (spectral::gradient = 1 r2c + 2 c2r)."""
+    from oracle import ref
+
+    try:
+        out = subprocess.run(["ldconfig", "-p"], capture_output=True, text=True, timeout=30).stdout
+        fftw = sorted({ln.split()[0] for ln in out.splitlines() if "fftw3" in ln})
+    except (OSError, subprocess.SubprocessError):
+        fftw = None
+    u = np.random.default_rng(0).standard_normal((N_GRID, N_GRID))
+    ref.gradient(u)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        ref.gradient(u)
+    per_fft = (time.perf_counter() - t0) / 9
+    t0 = time.perf_counter()
+    for _ in range(3):
+        np.fft.irfft2(np.fft.rfft2(u), s=u.shape)
+    per_np = (time.perf_counter() - t0) / 6
+    return {"libfftw3_on_host": fftw if fftw else "absent (ldconfig -p)",
+            "backend_used": "repo FFTW3-API shim (oracle/fftw_shim: radix-2 complex FFT, real transforms by "
+                            "half-length packing)",
+            "ms_per_fft_1024": per_fft * 1e3,
+            "numpy_pocketfft_ms_per_fft_1024": per_np * 1e3,
+            "logical_ffts_per_reference_matvec": 6 * NT + 10}
 
 
 def cpu_baseline_leg():
@@ -433,7 +471,8 @@ def cpu_baseline_leg():
     dt, nmv, _ = reference_sample(threads)
     return {"value": nmv / dt, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{nmv} steady-state reference HessianOperator::apply calls at 1024^2 nt=16, one per host "
-                      f"thread in parallel ({dt:.1f} s); FFT via the repo's FFTW3-API shim"}
+                      f"thread in parallel ({dt:.1f} s); FFT via the repo's FFTW3-API shim",
+            "fft_backend": fft_backend_probe()}
 
 
 # ------------------------------------------------------------------------------ time to solution
@@ -584,6 +623,16 @@ def main():
                                 "achieved_gbps": mv_bytes * r["value"] / world / 1e9,
                                 "frac": mv_bytes * r["value"] / world / 1e9 / peak},
             "sl_interp": r["sl"],
+            "op_counts_per_matvec": {
+                "logical": {"ffts": r["logical"][0], "interps": r["logical"][1],
+                            "note": "the reference's counters:: per apply (what the reference executes)"},
+                "executed": {"ffts": 2 * (prof.get("cufft_d2z", (0, 0))[0] + prof.get("cufft_z2d", (0, 0))[0]) // args.steps,
+                             "interps": (sum(prof.get(k, (0, 0))[0] for k in ("evaluate/adjoint_bodyforce", "evaluate/incstate",
+                                                                               "evaluate/incstate_seed"))
+                                         + 2 * prof.get("evaluate/store2", (0, 0))[0]) // args.steps,
+                             "note": "field transforms / scalar-field gathers the device runs per apply (cuFFT calls "
+                                     "are batched over the 2 components); grad m_j, (grad m_{j-1})_D, X_D, div v, "
+                                     "(div v)_D are per-iterate invariants cached at HessianOperator construction"}},
             "kernels": kernels,
             "kernel_model_ms_per_matvec": sum(k["avg_us"] * k["launches_per_matvec"] for k in kernels.values()) / 1e3,
             "event_profile": {"note": "per-launch event pairs (each pair adds its own overhead); shares only",

@@ -4,12 +4,20 @@
 //   ref_io_tool write-graymap <in.vrf> <out.pgm>
 //   ref_io_tool read-graymap <in.pgm> <n1> <n2> <out.vrf>
 //   ref_io_tool csv <rows.f64> <count>          (rows of 11 doubles, prints the CSV)
+//   ref_io_tool summary <in.txt>                 (prints the CLI's summary.json for the values in
+//                                                 in.txt, built as proj/tools/main.cpp:254-272 does:
+//                                                 lines "config <key> <s|i|d> <value>" and "<field> <value>")
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <string>
 #include <vector>
+
+#include <cmath>
+#include <sstream>
+
+#include <nlohmann/json.hpp>
 
 #include "veloreg/inverse.hpp"
 #include "veloreg/io.hpp"
@@ -47,6 +55,43 @@ int main(int argc, char** argv) {
                 r.iterations.push_back(it);
             }
             std::fputs(io::solverReportCsv(r).c_str(), stdout);
+        } else if (cmd == "summary" && argc == 3) {
+            using nlohmann::json;
+            std::ifstream is(argv[2]);
+            json config = json::object(), summary;
+            std::string line;
+            int status = 0;
+            double jmin = 1.0, jmax = 1.0;
+            while (std::getline(is, line)) {
+                std::istringstream ls(line);
+                std::string key;
+                ls >> key;
+                if (key == "config") {
+                    std::string name, type, value;
+                    ls >> name >> type;
+                    std::getline(ls >> std::ws, value);
+                    if (type == "s") config[name] = value;
+                    else if (type == "i") config[name] = std::stoll(value);
+                    else config[name] = std::stod(value);
+                } else if (key == "status") {
+                    ls >> status;
+                } else if (key == "outer_iterations" || key == "ffts" || key == "interps") {
+                    long long v = 0;
+                    ls >> v;
+                    summary[key] = v;
+                } else if (!key.empty()) {
+                    std::string v;
+                    ls >> v;
+                    const double d = std::stod(v);
+                    summary[key] = d;
+                    if (key == "jacobian_min") jmin = d;
+                    if (key == "jacobian_max") jmax = d;
+                }
+            }
+            summary["config"] = config;
+            summary["status"] = status == 0 ? "converged" : status == 1 ? "iteration-limit" : "line-search-failure";
+            summary["max_abs_jacobian_deviation"] = std::max(std::abs(jmin - 1.0), std::abs(jmax - 1.0));
+            std::fputs((summary.dump(2) + "\n").c_str(), stdout);
         } else {
             return 2;
         }

@@ -4,7 +4,8 @@ VRF1: "VRF1", then n1, n2, components as little-endian uint32, then the componen
 as little-endian binary64, row-major (io.cpp:16-94, 112-154).  Binary PGM (P5) images are
 read as one period of a periodic field in [0, 1] and, if their size differs from the target
 grid, resampled spectrally on the device (io.cpp:156-216).  `solver_report_csv` writes the
-per-iteration records with the reference's columns and number format (io.cpp:227-239).
+per-iteration records with the reference's columns and number format (io.cpp:227-239), and
+`summary_json` the run summary of the reference's CLI (proj/tools/main.cpp:254-272).
 """
 from __future__ import annotations
 
@@ -147,3 +148,22 @@ def solver_report_csv(records):
             f"{r['mismatch']:.12e}", str(int(r["innerIterations"])), str(int(r["lineSearchSteps"])),
             f"{r['stepLength']:.12e}", f"{r['wallTimeSec']:.12e}", str(int(r["ffts"])), str(int(r["interps"]))]))
     return "\n".join(lines) + "\n"
+
+
+STATUS_NAMES = {0: "converged", 1: "iteration-limit", 2: "line-search-failure"}
+
+
+def summary_json(config, summary, ffts, interps):
+    """summary.json of a registration run, as the reference's CLI writes it (proj/tools/main.cpp:
+    254-272, nlohmann::json dump(2): keys sorted, two-space indent): `config` is the run's
+    configuration echo (main.cpp:97-117), `summary` api.newton_solve's summary dict, ffts /
+    interps the process operation counters after the run."""
+    import json
+
+    jmin, jmax = float(summary["jacMin"]), float(summary["jacMax"])
+    doc = {"config": config, "status": STATUS_NAMES[int(summary["status"])],
+           "outer_iterations": int(summary["iterations"]), "grad_rel": float(summary["finalGradNormRel"]),
+           "residual_rel": float(summary["finalResidualRel"]), "jacobian_min": jmin, "jacobian_max": jmax,
+           "max_abs_jacobian_deviation": max(abs(jmin - 1.0), abs(jmax - 1.0)), "ffts": int(ffts),
+           "interps": int(interps), "time_sec": float(summary["totalTimeSec"])}
+    return json.dumps(doc, indent=2, sort_keys=True, ensure_ascii=False) + "\n"

@@ -101,3 +101,32 @@ def test_graymap_resampled_on_device(tmp_path):
     _tool("read-graymap", tmp_path / "g.pgm", 48, 40, tmp_path / "g.vrf")
     ref = vrf.read_scalar_field(str(tmp_path / "g.vrf"))
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_summary_json_matches_reference_cli_format(tmp_path):
+    """summary.json (proj/tools/main.cpp:254-272) byte-identical to the nlohmann::json document the
+    reference's CLI builds from the same values (ref_io_tool summary, oracle/ref_io_tool.cpp)."""
+    if not os.path.exists(TOOL):
+        pytest.skip("oracle/_ref/ref_io_tool not built")
+    config = {"mr": "data/ref.vrf", "mt": "data/tmpl.vrf", "grid": 256, "norm": "h1", "betav": 0.001,
+              "model": "compressible", "betaw": 0.1, "scheme": "sl", "cfl": 1.0, "pc": "2l-cheb", "cheb_iters": 10,
+              "tol_rel": 0.01, "tol_abs": 1e-05, "maxit": 50, "sigma": 0.0, "out": "out dir", "seed": 1234,
+              "protocol": "none", "problem": "file"}
+    for status, summ in [(0, dict(iterations=5, finalGradNormRel=0.0028532699925499488, finalResidualRel=0.0321754197,
+                                  jacMin=0.788873058129, jacMax=1.35304261003, totalTimeSec=0.0391)),
+                         (2, dict(iterations=50, finalGradNormRel=0.35, finalResidualRel=0.96, jacMin=0.5,
+                                  jacMax=2.25, totalTimeSec=10.4))]:
+        summ["status"] = status
+        got = vrf.summary_json(config, summ, 4445, 1915)
+        spec = tmp_path / "in.txt"
+        lines = []
+        for k, v in config.items():
+            t = "s" if isinstance(v, str) else ("i" if isinstance(v, int) else "d")
+            lines.append(f"config {k} {t} {v!r}" if t == "d" else f"config {k} {t} {v}")
+        lines += [f"status {status}", f"outer_iterations {summ['iterations']}",
+                  f"grad_rel {summ['finalGradNormRel']!r}", f"residual_rel {summ['finalResidualRel']!r}",
+                  f"jacobian_min {summ['jacMin']!r}", f"jacobian_max {summ['jacMax']!r}", "ffts 4445", "interps 1915",
+                  f"time_sec {summ['totalTimeSec']!r}"]
+        spec.write_text("\n".join(lines) + "\n")
+        want = subprocess.run([TOOL, "summary", str(spec)], capture_output=True, text=True, check=True).stdout
+        assert got == want
