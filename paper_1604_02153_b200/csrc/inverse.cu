@@ -816,6 +816,7 @@ Hessian::~Hessian() {
 }
 
 void Hessian::apply(const double* vt1, const double* vt2, double* o1, double* o2) {
+    NvtxRange nv_("HessianOperator::apply");
     replay(0, vt1, vt2, o1, o2, [&] { launchApply(vt1, vt2, o1, o2); });
     ctx.ffts += 4;
     countDataTerm();
@@ -889,6 +890,7 @@ void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, doub
 }
 
 void Hessian::applyDataTerm(const double* vt1, const double* vt2, double* o1, double* o2) {
+    NvtxRange nv_("HessianOperator::applyDataTerm");
     replay(1, vt1, vt2, o1, o2, [&] {
         const std::size_t N = g.points();
         double* b = work_.d() + 6 * N;
@@ -914,6 +916,7 @@ void Hessian::applyDataTerm(const double* vt1, const double* vt2, double* o1, do
 }
 
 void Hessian::applySplit(const double* s1, const double* s2, double* o1, double* o2) {
+    NvtxRange nv_("applySplitHessianOf");
     replay(2, s1, s2, o1, o2, [&] { launchSplit(s1, s2, o1, o2); });
     ctx.ffts += 8;
     countDataTerm();
@@ -986,6 +989,7 @@ void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, con
 void evaluateObjective(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, const double* mR,
                        const double* mT, const Model& model, int nt, double* scalars, double* stateOut,
                        double* stateStagesOut) {
+    NvtxRange nv_("evaluateObjective");
     const std::size_t N = g.points();
     DBuf stateBuf;
     double* st = stateOut;
@@ -1022,6 +1026,7 @@ void evaluateGradient(Ctx& ctx, const GridDims& g, const double* v1, const doubl
                       const double* mT, const Model& model, int nt, double* g1, double* g2, double* scalars,
                       double* stateOut, double* adjOut, const double* reuseState, double* gradTrajOut,
                       double* bodyOut, double* stateStagesOut, double* adjStagesOut) {
+    NvtxRange nv_("evaluateGradient");
     const std::size_t N = g.points();
     DBuf stBuf, adBuf;
     double* st = stateOut;

@@ -490,7 +490,8 @@ struct PhaseTimer {
     Ctx& ctx;
     const char* what;
     std::chrono::steady_clock::time_point t0;
-    PhaseTimer(Ctx& c, const char* w) : ctx(c), what(w), t0(std::chrono::steady_clock::now()) {}
+    NvtxRange nv_;
+    PhaseTimer(Ctx& c, const char* w) : ctx(c), what(w), t0(std::chrono::steady_clock::now()), nv_(w) {}
     ~PhaseTimer() {
         if (!traceOn()) return;
         ctx.sync();
@@ -583,6 +584,7 @@ std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const doub
 // ------------------------------------------------------------------------------ two-level
 bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator& coarse, const PrecondChoice& choice,
                    double outerTol, double eMin, double eMax, double* out) {
+    NvtxRange nv_("applyTwoLevel");
     const GridDims& gc = coarse.gc;
     const std::size_t N = g.points(), Nc = gc.points(), NS = g.specPoints(), NSc = gc.specPoints();
     cplx* R = specScratch(ctx, g, 5, 2);    // fine spectra of r (both components)
@@ -666,6 +668,7 @@ KktResult solveKkt(Ctx& ctx, Hessian& hess, const double* rhs, double tol, int m
 KktResult solveKktOp(Ctx& ctx, const GridDims& g, const Model& model, Weights& weights, const LinOpDev& A,
                      const double* rhs, double tol, int maxIter, const PrecondChoice& choice, const double* mR,
                      const double* mT, const double* v, double coarseCfl, double* solution) {
+    NvtxRange nv_("solveKkt");
     const std::size_t N = g.points();
     const auto t0 = std::chrono::steady_clock::now();
     double precondTime = 0.0;
@@ -749,6 +752,7 @@ void ExternalFineOperator::applySplit(const double* s, double* o) {
 // ------------------------------------------------------------------------------ Newton
 SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const double* mT, const Model& model,
                          const NewtonConfig& cfg, const PrecondChoice& pc, double* vOut) {
+    NvtxRange nv_("newtonSolve");
     const std::size_t N = g.points();
     const auto tStart = std::chrono::steady_clock::now();
     const long long f0 = ctx.ffts, i0 = ctx.interps;

@@ -243,6 +243,7 @@ void Solver::continuityBand(const double* lam1, DstFn dst) {
 }
 
 void Solver::state(const double* m0, double* traj, bool guard) {
+    NvtxRange nv_("Solver::solveState");
     const double* X = departure(kForward);
     const std::size_t N = g.points();
     log.reset(ctx);
@@ -273,6 +274,7 @@ void Solver::state(const double* m0, double* traj, bool guard) {
 }
 
 void Solver::stateFinal(const double* m0, double* out) {
+    NvtxRange nv_("Solver::solveStateFinal");
     const double* X = departure(kForward);
     const std::size_t N = g.points();
     double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
@@ -306,6 +308,7 @@ void Solver::stateFinal(const double* m0, double* out) {
 }
 
 void Solver::adjoint(const double* lam1, double* traj, bool guard) {
+    NvtxRange nv_("Solver::solveAdjoint");
     const std::size_t N = g.points();
     log.reset(ctx);
     copy(ctx, N, lam1, traj + nt * N);
@@ -321,6 +324,7 @@ void Solver::adjoint(const double* lam1, double* traj, bool guard) {
 }
 
 void Solver::adjointFinal(const double* lam1, double* out) {
+    NvtxRange nv_("Solver::solveAdjointFinal");
     const std::size_t N = g.points();
     double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
     log.reset(ctx);
