@@ -328,6 +328,19 @@ int vrg_newton_solve_ex(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, co
 typedef int (*vrg_fine_build_fn)(void* user, const double* v, int nt);
 typedef int (*vrg_fine_data_term_fn)(void* user, const double* vt, double* b);
 int vrg_set_fine_operator(vrg_ctx_t ctx, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term, void* user);
+/* The fine operator hook plus evaluateGradient / evaluateObjective (inverse.hpp:60-71) of the same
+ * external (slab-decomposed) implementation, so the Newton driver (newton.cpp:24-159) does no
+ * whole-grid transport itself: gradient(user, v, nt, reuse, g, m1, scalars) once per outer
+ * iteration (reuse = 1: the state of the last objective call, the accepted line-search trial,
+ * is this iterate's state, newton.cpp:54-56), objective(user, v, nt, m1, scalars) per line-search
+ * trial (return 2 for transport::BlowupError, newton.cpp:118-122).  v, g: 2 contiguous device
+ * fields; m1: m(1), one field; scalars = [objective, mismatch, regTerm, penaltyTerm].  The
+ * driver adds the reference's logical operation counts.  NULL gradient/objective: as
+ * vrg_set_fine_operator. */
+typedef int (*vrg_gradient_fn)(void* user, const double* v, int nt, int reuse, double* g, double* m1, double* scalars);
+typedef int (*vrg_objective_fn)(void* user, const double* v, int nt, double* m1, double* scalars);
+int vrg_set_external_ops(vrg_ctx_t ctx, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term,
+                         vrg_gradient_fn gradient, vrg_objective_fn objective, void* user);
 
 #ifdef __cplusplus
 }

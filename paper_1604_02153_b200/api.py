@@ -493,6 +493,9 @@ RECORD_FIELDS = ("iter", "gradNormInf", "gradNormRel", "objective", "mismatch", 
 
 FINE_BUILD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int)
 FINE_DATA_TERM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+# vrg_gradient_fn(user, v, nt, reuse, g, m1, scalars) / vrg_objective_fn(user, v, nt, m1, scalars)
+GRADIENT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
 
 
 def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=0, ls_max_steps=20,
@@ -501,9 +504,11 @@ def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inne
                  hessian_mode=GAUSS_NEWTON, fine_operator=None):
     """inverse::newtonSolve on host images (numpy); returns (v1, v2, records, summary).
 
-    fine_operator: an object with `callbacks()` -> (build, data_term) ctypes callbacks and an
-    `error` attribute (e.g. slab.SlabFineOperator); the solve then takes its fine GN data term
-    from it (C ABI vrg_set_fine_operator) and re-raises the callback's exception."""
+    fine_operator: an object with `callbacks()` -> (build, data_term) ctypes callbacks, or
+    (build, data_term, gradient, objective), and an `error` attribute (e.g.
+    slab.SlabFineOperator); the solve then takes its fine GN data term (and its gradient and
+    line-search objective) from it (C ABI vrg_set_fine_operator / vrg_set_external_ops) and
+    re-raises the callback's exception."""
     import numpy as np
 
     mR = np.ascontiguousarray(mR, dtype=np.float64)
@@ -517,16 +522,19 @@ def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inne
     summ = np.zeros(7)
     hp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
     if fine_operator is not None:
-        fb, fd = fine_operator.callbacks()
+        cbs = [C.cast(cb, C.c_void_p) for cb in fine_operator.callbacks()]
         fine_operator.error = None
-        ctx.check(ctx.lib.vrg_set_fine_operator(ctx.h, C.cast(fb, C.c_void_p), C.cast(fd, C.c_void_p), None))
+        if len(cbs) == 4:
+            ctx.check(ctx.lib.vrg_set_external_ops(ctx.h, *cbs, None))
+        else:
+            ctx.check(ctx.lib.vrg_set_fine_operator(ctx.h, *cbs, None))
     try:
         code = ctx.lib.vrg_newton_solve(ctx.h, n1, n2, hp(mR), hp(mT), norm, beta, deformation,
                                         C.cast(ci, C.c_void_p), C.cast(cd, C.c_void_p), C.cast(pi, C.c_void_p),
                                         C.cast(pd, C.c_void_p), hp(v1), hp(v2), hp(rec), max_outer + 1, hp(summ))
     finally:
         if fine_operator is not None:
-            ctx.lib.vrg_set_fine_operator(ctx.h, None, None, None)
+            ctx.lib.vrg_set_external_ops(ctx.h, None, None, None, None, None)
     if fine_operator is not None and code and fine_operator.error is not None:
         raise fine_operator.error
     ctx.check(code)

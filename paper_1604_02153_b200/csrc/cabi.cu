@@ -866,6 +866,23 @@ int vrg_set_fine_operator(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_te
             throw vrg::InvalidArgument("external fine operator: give both callbacks or neither");
         c->ctx.fine.build = build;
         c->ctx.fine.dataTerm = data_term;
+        c->ctx.fine.gradient = nullptr;
+        c->ctx.fine.objective = nullptr;
+        c->ctx.fine.user = build ? user : nullptr;
+    });
+}
+
+int vrg_set_external_ops(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term,
+                         vrg_gradient_fn gradient, vrg_objective_fn objective, void* user) {
+    return guarded(c, [&] {
+        if (!c) throw vrg::InvalidArgument("null context");
+        if ((build == nullptr) != (data_term == nullptr) || (gradient == nullptr) != (objective == nullptr) ||
+            (gradient && !build))
+            throw vrg::InvalidArgument("external operators: give build + data_term, optionally gradient + objective");
+        c->ctx.fine.build = build;
+        c->ctx.fine.dataTerm = data_term;
+        c->ctx.fine.gradient = gradient;
+        c->ctx.fine.objective = objective;
         c->ctx.fine.user = build ? user : nullptr;
     });
 }

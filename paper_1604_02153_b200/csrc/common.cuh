@@ -180,9 +180,16 @@ struct Ctx {
     // plug-in point of precond::LinOp (precond.hpp:25) that a slab-decomposed operator fills.
     // build(v, nt) is called once per Newton iterate, dataTerm(vt, b) per matvec (2N fields,
     // device pointers on this context's stream); nonzero return = failure.
+    // gradient / objective (optional, C ABI vrg_set_external_ops) replace evaluateGradient and
+    // the line search's evaluateObjective: gradient(v, nt, reuse, g, m1, scalars[4]) with reuse
+    // = 1 when the state of the last objective call (the accepted trial) is to be reused;
+    // objective(v, nt, m1, scalars[4]) returns 2 on a blow-up (BlowupError), other nonzero on
+    // failure.  m1 = the final state m(1) (N doubles).
     struct FineHook {
         int (*build)(void* user, const double* v, int nt) = nullptr;
         int (*dataTerm)(void* user, const double* vt, double* b) = nullptr;
+        int (*gradient)(void* user, const double* v, int nt, int reuse, double* g, double* m1, double* scalars) = nullptr;
+        int (*objective)(void* user, const double* v, int nt, double* m1, double* scalars) = nullptr;
         void* user = nullptr;
     } fine;
 

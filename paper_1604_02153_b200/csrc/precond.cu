@@ -763,6 +763,9 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
     double* v = vBuf.d();
     fill(ctx, 2 * N, 0.0, v);  // zero initial guess
 
+    if ((ctx.fine.gradient || ctx.fine.objective) &&
+        (model.scheme != kSchemeSL || model.deformation != kCompressible || cfg.hessianMode != 0 || !ctx.fine.build))
+        throw NotSupported("external gradient / objective: compressible Gauss-Newton SL with an external fine operator");
     PrecondChoice choice = pc;
     if (choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb && !choice.hasEig &&
         !choice.reestimateEachIteration) {
@@ -790,13 +793,22 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
         const bool keepGrads = model.scheme == kSchemeSL && cfg.hessianMode == 0 && !ctx.fine.build;
         if (keepGrads) grads.alloc(sizeof(double) * (nt + 1) * 2 * N);
         const bool reuse = carriedNt == nt;
-        {
+        if (ctx.fine.gradient) {
+            // external (e.g. slab-decomposed) evaluateGradient; logical counts as the reference's
+            // (inverse.cpp:119-148: state unless reused, adjoint with the lazy backward
+            // characteristics / div v / (div v)_D, body force, applyReg)
+            PhaseTimer pt(ctx, "evaluateGradient (external)");
+            if (ctx.fine.gradient(ctx.fine.user, v, nt, reuse ? 1 : 0, gBuf.d(), finalDeformed.d(), scal) != 0)
+                throw std::runtime_error("external fine operator: gradient callback failed");
+            ctx.interps += (reuse ? 0 : 2LL + nt) + 3 + nt;
+            ctx.ffts += 3 + 3LL * (nt + 1) + 4;
+        } else {
             PhaseTimer pt(ctx, "evaluateGradient");
             evaluateGradient(ctx, g, v, v + N, mR, mT, model, nt, gBuf.d(), gBuf.d() + N, scal, state.d(),
                              adjoint.d(), reuse ? carried.d() : nullptr, keepGrads ? grads.d() : nullptr);
+            copy(ctx, N, state.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
         }
         const double objective = scal[0], mismatch = scal[1];
-        copy(ctx, N, state.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
 
         const double ginf = vnormLinf(ctx, g, gBuf.d());
         if (iter == 0) g0inf = std::max(ginf, 1e-300);
@@ -878,15 +890,28 @@ SolverReport newtonSolve(Ctx& ctx, const GridDims& g, const double* mR, const do
             lincomb(ctx, 2 * N, 1.0, v, alpha, dv, trialBuf.d());
             bool blewUp = false;
             double ob[4] = {0, 0, 0, 0};
-            try {
-                evaluateObjective(ctx, g, trialBuf.d(), trialBuf.d() + N, mR, mT, model, nt, ob, carried.d());
-            } catch (const BlowupError&) {
-                blewUp = true;
+            double* trialM1 = tmpBuf.d();
+            if (ctx.fine.objective) {
+                const int rc = ctx.fine.objective(ctx.fine.user, trialBuf.d(), nt, trialM1, ob);
+                if (rc == 2) {
+                    blewUp = true;
+                } else if (rc != 0) {
+                    throw std::runtime_error("external fine operator: objective callback failed");
+                }
+                ctx.interps += 2LL + nt;  // evaluateObjective: solveState (inverse.cpp:101-103), applyReg
+                ctx.ffts += 4;
+            } else {
+                try {
+                    evaluateObjective(ctx, g, trialBuf.d(), trialBuf.d() + N, mR, mT, model, nt, ob, carried.d());
+                } catch (const BlowupError&) {
+                    blewUp = true;
+                }
+                copy(ctx, N, carried.d() + static_cast<std::size_t>(nt) * N, trialM1);
             }
             if (!blewUp && ob[0] <= objective + cfg.lsC1 * alpha * gdotd) {
                 copy(ctx, 2 * N, trialBuf.d(), v);
                 carriedNt = nt;
-                copy(ctx, N, carried.d() + static_cast<std::size_t>(nt) * N, finalDeformed.d());
+                copy(ctx, N, trialM1, finalDeformed.d());
                 accepted = true;
                 break;
             }

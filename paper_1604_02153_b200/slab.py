@@ -90,6 +90,13 @@ class LocalComm:
     def any_failed(self, failed: bool) -> bool:
         return bool(failed)
 
+    def allreduce_sum(self, vals):
+        """Sum over the virtual ranks in rank order."""
+        t = torch.as_tensor(vals[0]).clone()
+        for v in vals[1:]:
+            t = t + torch.as_tensor(v)
+        return [t for _ in self.ranks]
+
 
 class DistComm:
     """One slab per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
@@ -184,6 +191,18 @@ class DistComm:
             if self.dist.get_backend(self.group) == "nccl" and t.device.type != "cuda":
                 t = t.to(torch.device("cuda", torch.cuda.current_device()))
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+            t = t.to(home)
+        return [t]
+
+    def allreduce_sum(self, vals):
+        """Sum over ranks (device tensors under NCCL, as allreduce_max)."""
+        (v,) = vals
+        t = torch.as_tensor(v).clone()
+        if self.size > 1:
+            home = t.device
+            if self.dist.get_backend(self.group) == "nccl" and t.device.type != "cuda":
+                t = t.to(torch.device("cuda", torch.cuda.current_device()))
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
             t = t.to(home)
         return [t]
 
@@ -375,6 +394,17 @@ class SlabHessian:
         mTs[i] = (L, n2) template rows.  Departure points by the Heun trace (transport.cpp:60-89,
         same rounding steps as EpiTrace), the state by slab SL steps with the guard, gradients
         and div v by the distributed FFT, (grad m)_D and (div v)_D by slab interpolation."""
+        X = cls.trace(ctx, comm, vs, n1, nt, norm, beta, ("Xf", "Xb"))
+        S = cls.for_points(ctx, comm, X, n1, vs[0].shape[-1], nt, norm, beta)
+        ms = S.state(X["Xf"], mTs)
+        S.derive(vs, X, ms)
+        S.add_gd()
+        return S
+
+    @classmethod
+    def trace(cls, ctx, comm, vs, n1, nt, norm, beta, dirs):
+        """traceCharacteristics (transport.cpp:60-89) on the slabs for the directions in dirs
+        ("Xf" forward, "Xb" backward): {name: [per-rank (2, L, n2)]}."""
         n2 = vs[0].shape[-1]
         G = comm.size
         L = n1 // G
@@ -389,6 +419,8 @@ class SlabHessian:
             tr._prefilter([v[c] for v in vs], [w[c] for w in tr.winv])
         X = {}
         for sgn, name in ((1.0, "Xf"), (-1.0, "Xb")):
+            if name not in dirs:
+                continue
             xs = []
             for i, q in enumerate(comm.ranks):
                 dev = vs[i].device
@@ -405,46 +437,106 @@ class SlabHessian:
                 xs.append(torch.stack([c1 - sh * (vs[i][0] + vstar[0]), c2 - sh * (vs[i][1] + vstar[1])]))
             X[name] = xs
         tr._check_window()
-        reach = max(max(row_reach(X["Xf"][i][0], n1, q * L), row_reach(X["Xb"][i][0], n1, q * L))
-                    for i, q in enumerate(comm.ranks))
+        return X
+
+    @classmethod
+    def for_points(cls, ctx, comm, X, n1, n2, nt, norm, beta):
+        """An operator whose coefficient windows cover the departure displacement of the
+        point sets in X (max over ranks)."""
+        L = n1 // comm.size
+        reach = max(row_reach(xs[i][0], n1, q * L) for xs in X.values() for i, q in enumerate(comm.ranks))
         reach = float(comm.allreduce_max([torch.tensor(reach)] * len(comm.ranks))[0])
         if not math.isfinite(reach):
             raise api.InvalidArgument("evaluate: non-finite point coordinate")
-        S = cls(ctx, comm, n1, n2, nt, norm, beta, None, math.ceil(reach) + 3)
-        # state m_j (slState with the guard, transport.cpp:214-227)
+        return cls(ctx, comm, n1, n2, nt, norm, beta, None, math.ceil(reach) + 3)
+
+    def state(self, Xf, mTs):
+        """slState with the guard (transport.cpp:214-227): per-rank (nt+1, L, n2) trajectories."""
+        ctx, comm, nt = self.ctx, self.comm, self.nt
+        L, n2, ht = self.geo.L, self.n2, 1.0 / nt
         ms = [ctx.empty(nt + 1, L, n2) for _ in comm.ranks]
         for i in range(len(comm.ranks)):
             ms[i][0].copy_(mTs[i])
-            S.partials[i].zero_()
-            S.flags[i].zero_()
-            S.partials[i][0][:L].copy_(mTs[i].abs().amax(dim=1))
-            S.flags[i][0] = (~torch.isfinite(mTs[i])).any().to(S.flags[i].dtype)  # prefilter input check
-        S._prefilter([m[0] for m in ms], S.win)
+            self.partials[i].zero_()
+            self.flags[i].zero_()
+            self.partials[i][0][:L].copy_(mTs[i].abs().amax(dim=1))
+            self.flags[i][0] = (~torch.isfinite(mTs[i])).any().to(self.flags[i].dtype)  # prefilter input check
+        self._prefilter([m[0] for m in ms], self.win)
         for j in range(1, nt + 1):
             if j > 1:
-                S._windows_from_rows()
+                self._windows_from_rows()
             for i in range(len(comm.ranks)):
-                S._step(i, KIND_STATE, S.win[i], X["Xf"][i], [ms[i][j]], ht, 0.0, S.rows[i], S.partials[i][j],
-                        S.flags[i][j:j + 1])
-        S._check_state_guard()
-        # gradients G_j = grad m_j, (grad m_{j-1})_D, div v and (div v)_D
+                self._step(i, KIND_STATE, self.win[i], Xf[i], [ms[i][j]], ht, 0.0, self.rows[i], self.partials[i][j],
+                           self.flags[i][j:j + 1])
+        self._check_state_guard()
+        return ms
+
+    def derive(self, vs, X, ms):
+        """grad m_j, div v and (div v)_D of the state ms at velocity vs (the lazy caches of the
+        GN operator and of evaluateGradient's adjoint / body force)."""
+        ctx, comm, nt, n1, n2 = self.ctx, self.comm, self.nt, self.n1, self.n2
+        L, ht = self.geo.L, 1.0 / nt
         grads = distributed_gradient(comm, ms, n1, n2)  # (nt+1, 2, L, n2) per rank
+        dvs = distributed_divergence(comm, vs, n1, n2)
+        self._prefilter(dvs, self.win)
+        dvds = [ctx.empty(L, n2) for _ in comm.ranks]
+        for i in range(len(comm.ranks)):
+            self._step(i, KIND_STORE, self.win[i], X["Xb"][i], [dvds[i]], ht, 0.0, self.scr[i], self.partials[i][0],
+                       None)
+        self._check_window()
+        self.parts = [dict(Xf=X["Xf"][i], Xb=X["Xb"][i], G=grads[i], dv=dvs[i], dvd=dvds[i], m=ms[i])
+                      for i in range(len(comm.ranks))]
+
+    def add_gd(self):
+        """(grad m_{j-1})_D at the forward departure points: the last per-iterate invariant of
+        the GN operator (inverse.cpp:177-187)."""
+        ctx, comm, nt = self.ctx, self.comm, self.nt
+        L, n2, ht = self.geo.L, self.n2, 1.0 / nt
         gds = [ctx.empty(nt, 2, L, n2) for _ in comm.ranks]
         for j in range(1, nt + 1):
             for c in range(2):
-                S._prefilter([g[j - 1][c] for g in grads], S.win)
+                self._prefilter([p["G"][j - 1][c] for p in self.parts], self.win)
                 for i in range(len(comm.ranks)):
-                    S._step(i, KIND_STORE, S.win[i], X["Xf"][i], [gds[i][j - 1][c]], ht, 0.0, S.scr[i],
-                            S.partials[i][0], None)
-        dvs = distributed_divergence(comm, vs, n1, n2)
-        S._prefilter(dvs, S.win)
-        dvds = [ctx.empty(L, n2) for _ in comm.ranks]
-        for i in range(len(comm.ranks)):
-            S._step(i, KIND_STORE, S.win[i], X["Xb"][i], [dvds[i]], ht, 0.0, S.scr[i], S.partials[i][0], None)
-        S._check_window()
-        S.parts = [dict(Xf=X["Xf"][i], Xb=X["Xb"][i], G=grads[i], GD=gds[i], dv=dvs[i], dvd=dvds[i], m=ms[i])
-                   for i in range(len(comm.ranks))]
-        return S
+                    self._step(i, KIND_STORE, self.win[i], self.parts[i]["Xf"], [gds[i][j - 1][c]], ht, 0.0,
+                               self.scr[i], self.partials[i][0], None)
+        self._check_window()
+        for i, p in enumerate(self.parts):
+            p["GD"] = gds[i]
+
+    def gradient(self, mRs, regs, outs):
+        """evaluateGradient's adjoint and body force (inverse.cpp:130-146, SL): lambda(1) =
+        -(m(1) - m_R), the adjoint solved back with the guard, b = sum_j w_j lambda_j grad m_j
+        accumulated by the adjoint steps, outs[i] = beta A v + b (compressible)."""
+        nt, ht = self.nt, 1.0 / self.nt
+        ranks = range(len(self.comm.ranks))
+        wof = lambda j: ht * (0.5 if j in (0, nt) else 1.0)  # noqa: E731
+        lams = []
+        for i in ranks:
+            p = self.parts[i]
+            lam = -1.0 * (p["m"][nt] - mRs[i])
+            lams.append(lam)
+            self.flags[i].zero_()
+            self.partials[i].zero_()
+            self.partials[i][nt][:self.geo.L].copy_(lam.abs().amax(dim=1))
+            self.flags[i][nt] = (~torch.isfinite(lam)).any().to(self.flags[i].dtype)
+            self.b[i][0].copy_(wof(nt) * (lam * p["G"][nt][0]))
+            self.b[i][1].copy_(wof(nt) * (lam * p["G"][nt][1]))
+        self._prefilter(lams, self.win)
+        for j in range(nt, 0, -1):
+            if j < nt:
+                self._windows_from_rows()
+            for i in ranks:
+                p = self.parts[i]
+                ops = [p["dvd"], p["dv"], p["G"][j - 1][0], p["G"][j - 1][1], self.b[i][0], self.b[i][1]]
+                if j == 1:
+                    ops += [regs[i][0], regs[i][1], outs[i][0], outs[i][1]]
+                    self._step(i, KIND_ADJ_LAST, self.win[i], p["Xb"], ops, ht, wof(0), self.scr[i],
+                               self.partials[i][0], None)
+                else:
+                    self._step(i, KIND_ADJ, self.win[i], p["Xb"], ops, ht, wof(j - 1), self.rows[i],
+                               self.partials[i][j - 1], self.flags[i][j - 1:j])
+        self._check_guard()
+        return lams
 
     def _check_window(self):
         fl = self.comm.allreduce_max([f.to(torch.float64) for f in self.flags])[0].cpu()
@@ -566,17 +658,24 @@ class SlabHessian:
 
 
 class SlabFineOperator:
-    """Slab-decomposed fine GN data term for `api.newton_solve(..., fine_operator=...)` (config
-    5a): the library's Newton driver (newton.cpp:24-159) calls `build(v, nt)` once per outer
-    iteration and `data_term(vt) -> b` per fine matvec of its PCG through the C ABI hook
-    `vrg_set_fine_operator` (the precond::LinOp plug-in point, precond.hpp:25).  Every rank runs
-    the same driver on the whole grid (gradient, objective, line search and the two-level
-    preconditioner are replicated); the fine matvec, the hot path, is decomposed: each rank
-    builds and applies `SlabHessian` on its rows (halo exchanges and all-to-all FFT transposes
-    inside), and the slabs of b are all-gathered back into the driver's field.  All ranks call
-    the hooks in the same order because the driver is deterministic and sees identical data."""
+    """Slab-decomposed operators for `api.newton_solve(..., fine_operator=...)` (config 5a).
 
-    def __init__(self, ctx, comm, mT, norm, beta):
+    The library's Newton driver (newton.cpp:24-159, host C++) keeps the control flow and the
+    whole-grid vectors (v, g, the PCG vectors); the transport-heavy parts run decomposed, each
+    rank on its rows (halo exchanges and all-to-all FFT transposes inside), their slab outputs
+    all-gathered back into the driver's fields:
+      * build(v, nt) per outer iteration and data_term(vt) -> b per fine matvec (the
+        precond::LinOp plug-in point, precond.hpp:25, C ABI vrg_set_fine_operator);
+      * with mR given, also gradient(v, nt, reuse) -> g, m(1) and the objective terms
+        (evaluateGradient, inverse.cpp:119-148) and objective(v, nt) per line-search trial
+        (evaluateObjective, inverse.cpp:96-117), C ABI vrg_set_external_ops: the state, adjoint
+        and body force of the gradient and the state of every trial are slab SL solves, and
+        the Hessian's per-iterate invariants reuse the gradient's (trace, state, grad m_j, div v).
+    What stays replicated is the vector algebra of the driver and the two-level
+    preconditioner's coarse solve.  All ranks call the hooks in the same order because the
+    driver is deterministic and sees identical data; every callback reaches a common verdict."""
+
+    def __init__(self, ctx, comm, mT, norm, beta, mR=None):
         import numpy as np
 
         self.ctx, self.comm = ctx, comm
@@ -587,23 +686,34 @@ class SlabFineOperator:
         self.norm, self.beta = int(norm), float(beta)
         self.L = self.n1 // comm.size
         self.mTs = [mT[q * self.L:(q + 1) * self.L].contiguous() for q in comm.ranks]
+        self.full = mR is not None
+        if self.full:
+            mR = ctx.field(np.asarray(mR) if not torch.is_tensor(mR) else mR)
+            self.mRs = [mR[q * self.L:(q + 1) * self.L].contiguous() for q in comm.ranks]
         self.S = None
         self.error = None
-        self.builds = self.matvecs = 0
-        self.build_s = self.apply_s = 0.0
+        self._stage = None       # (v, SlabHessian with the gradient's invariants) of the iterate
+        self._candidate = None   # (nt, Xf, state) of the last objective call (the accepted trial)
+        self.builds = self.matvecs = self.gradients = self.objectives = 0
+        self.build_s = self.apply_s = self.gradient_s = self.objective_s = 0.0
         self._cb_build = api.FINE_BUILD_FN(self._build)
         self._cb_data_term = api.FINE_DATA_TERM_FN(self._data_term)
+        self._cb_gradient = api.GRADIENT_FN(self._gradient)
+        self._cb_objective = api.OBJECTIVE_FN(self._objective)
 
     def callbacks(self):
+        if self.full:
+            return self._cb_build, self._cb_data_term, self._cb_gradient, self._cb_objective
         return self._cb_build, self._cb_data_term
 
-    def _full(self, ptr):
+    def _full(self, ptr, comps=2):
         N = self.n1 * self.n2
-        return _DeviceView(ptr, 2 * N, self.ctx.device).tensor().view(2, self.n1, self.n2)
+        t = _DeviceView(ptr, comps * N, self.ctx.device).tensor()
+        return t.view(comps, self.n1, self.n2) if comps > 1 else t.view(self.n1, self.n2)
 
     def _slabs(self, f):
         L = self.L
-        return [f[:, q * L:(q + 1) * L].contiguous() for q in self.comm.ranks]
+        return [f[..., q * L:(q + 1) * L, :].contiguous() for q in self.comm.ranks]
 
     def _verdict(self, failed: bool) -> int:
         """Every rank returns the same status: the driver aborts on all ranks together instead
@@ -617,6 +727,87 @@ class SlabFineOperator:
             self.error = RuntimeError("slab fine operator failed on another rank")
         return 1 if anyf else 0
 
+    def _dot(self, a, b):
+        """dot (field.cpp:51-57) of slab fields, summed over ranks: h1 h2 sum(a b)."""
+        h = (2 * math.pi / self.n1) * (2 * math.pi / self.n2)
+        part = [torch.sum(x * y).reshape(1) for x, y in zip(a, b)]
+        return h * float(self.comm.allreduce_sum(part)[0].item())
+
+    def _objective_terms(self, vs, ms, nt):
+        """mismatch = 1/2 |m(1) - m_R|^2 and regTerm = 1/2 <beta A v, v> (inverse.cpp:104-108);
+        returns them with beta A v."""
+        resid = [m[nt] - r for m, r in zip(ms, self.mRs)]
+        mismatch = 0.5 * self._dot(resid, resid)
+        regs = distributed_reg(self.comm, vs, self.n1, self.n2, self.norm, self.beta)
+        reg_term = 0.5 * self._dot(regs, vs)
+        return mismatch, reg_term, regs
+
+    @staticmethod
+    def _scalars(ptr, mismatch, reg_term):
+        out = (C.c_double * 4).from_address(ptr)
+        out[0], out[1], out[2], out[3] = mismatch + reg_term, mismatch, reg_term, 0.0
+
+    def _objective(self, _user, vptr, nt, m1ptr, scptr):
+        import time
+
+        failed, blowup = False, False
+        try:
+            t0 = time.perf_counter()
+            vs = self._slabs(self._full(vptr))
+            X = SlabHessian.trace(self.ctx, self.comm, vs, self.n1, int(nt), self.norm, self.beta, ("Xf",))
+            S = SlabHessian.for_points(self.ctx, self.comm, X, self.n1, self.n2, int(nt), self.norm, self.beta)
+            try:
+                ms = S.state(X["Xf"], self.mTs)
+            except api.BlowupError:  # common to all ranks: the guard reduces over them
+                self._candidate = None
+                blowup = True
+            if not blowup:
+                mismatch, reg_term, _ = self._objective_terms(vs, ms, int(nt))
+                self._scalars(scptr, mismatch, reg_term)
+                self.comm.allgather_rows([m[int(nt)].unsqueeze(0) for m in ms], self._full(m1ptr, 1).unsqueeze(0))
+                self._candidate = (int(nt), X["Xf"], ms)
+            self.objectives += 1
+            self.objective_s += time.perf_counter() - t0
+        except BaseException as e:
+            self.error = e
+            failed = True
+        rc = self._verdict(failed)
+        return rc if rc else (2 if blowup else 0)
+
+    def _gradient(self, _user, vptr, nt, reuse, gptr, m1ptr, scptr):
+        import time
+
+        failed = False
+        try:
+            t0 = time.perf_counter()
+            nt = int(nt)
+            v = self._full(vptr)
+            vs = self._slabs(v)
+            if reuse and self._candidate is not None and self._candidate[0] == nt:
+                _, Xf, ms = self._candidate  # the accepted trial's state (newton.cpp:54-56)
+                X = dict(Xf=Xf, **SlabHessian.trace(self.ctx, self.comm, vs, self.n1, nt, self.norm, self.beta,
+                                                    ("Xb",)))
+                S = SlabHessian.for_points(self.ctx, self.comm, X, self.n1, self.n2, nt, self.norm, self.beta)
+            else:
+                X = SlabHessian.trace(self.ctx, self.comm, vs, self.n1, nt, self.norm, self.beta, ("Xf", "Xb"))
+                S = SlabHessian.for_points(self.ctx, self.comm, X, self.n1, self.n2, nt, self.norm, self.beta)
+                ms = S.state(X["Xf"], self.mTs)
+            S.derive(vs, X, ms)
+            mismatch, reg_term, regs = self._objective_terms(vs, ms, nt)
+            outs = [self.ctx.empty(2, self.L, self.n2) for _ in self.comm.ranks]
+            S.gradient(self.mRs, regs, outs)
+            self.comm.allgather_rows(outs, self._full(gptr))
+            self.comm.allgather_rows([m[nt].unsqueeze(0) for m in ms], self._full(m1ptr, 1).unsqueeze(0))
+            self._scalars(scptr, mismatch, reg_term)
+            self._stage = (v.clone(), nt, S)
+            self._candidate = None
+            self.gradients += 1
+            self.gradient_s += time.perf_counter() - t0
+        except BaseException as e:  # re-raised by api.newton_solve
+            self.error = e
+            failed = True
+        return self._verdict(failed)
+
     def _build(self, _user, vptr, nt):
         import time
 
@@ -624,8 +815,16 @@ class SlabFineOperator:
         try:
             t0 = time.perf_counter()
             self.S = None
-            self.S = SlabHessian.build(self.ctx, self.comm, self._slabs(self._full(vptr)), self.mTs, self.n1, int(nt),
-                                       self.norm, self.beta)
+            v = self._full(vptr)
+            st = self._stage
+            if st is not None and st[1] == int(nt) and torch.equal(st[0], v):
+                S = st[2]  # the gradient's trace, state, grad m_j and div v at this iterate
+                S.add_gd()
+                self.S = S
+            else:
+                self.S = SlabHessian.build(self.ctx, self.comm, self._slabs(v), self.mTs, self.n1, int(nt),
+                                           self.norm, self.beta)
+            self._stage = None
             self.builds += 1
             self.build_s += time.perf_counter() - t0
         except BaseException as e:  # re-raised by api.newton_solve

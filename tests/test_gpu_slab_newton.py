@@ -33,12 +33,16 @@ def rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
-@pytest.mark.parametrize("n,nt,G", [(256, 8, 1), (256, 8, 2), (256, 16, 4), (512, 8, 8)])
-def test_slab_newton_matches_single_device(ctx, api, n, nt, G):
+@pytest.mark.parametrize("n,nt,G,full", [(256, 8, 1, False), (256, 8, 2, False), (256, 16, 4, False),
+                                         (512, 8, 8, False), (256, 8, 1, True), (256, 8, 2, True),
+                                         (256, 16, 4, True), (512, 8, 8, True)])
+def test_slab_newton_matches_single_device(ctx, api, n, nt, G, full):
+    """full: the gradient and every line-search objective are slab solves too (vrg_set_external_ops),
+    so the driver runs no whole-grid transport; else only the fine matvec is decomposed."""
     mR, mT = _pair(ctx, api, n, nt)
     kw = dict(KW, kind=api.PC_TWO_LEVEL, coarse_solver=api.COARSE_CHEB, nt=nt)
     w1, w2, recs, summ = api.newton_solve(ctx, mR, mT, 2, 1e-3, api.COMPRESSIBLE, **kw)
-    fo = slab.SlabFineOperator(ctx, slab.LocalComm(G), mT, 2, 1e-3)
+    fo = slab.SlabFineOperator(ctx, slab.LocalComm(G), mT, 2, 1e-3, mR=mR if full else None)
     s1, s2, srecs, ssumm = api.newton_solve(ctx, mR, mT, 2, 1e-3, api.COMPRESSIBLE, fine_operator=fo, **kw)
     assert ssumm["status"] == summ["status"] and ssumm["iterations"] == summ["iterations"]
     assert summ["iterations"] >= 2
@@ -55,6 +59,9 @@ def test_slab_newton_matches_single_device(ctx, api, n, nt, G):
     # one slab build per Hessian (every iteration but a converged last one), one gather per matvec
     assert fo.builds == sum(1 for r in recs if r["innerIterations"] > 0)
     assert fo.matvecs >= sum(r["innerIterations"] for r in recs)
+    if full:  # one slab gradient per outer iteration, one slab objective per line-search trial
+        assert fo.gradients == len(recs)
+        assert fo.objectives == sum(r["lineSearchSteps"] for r in recs)
 
 
 class _Failing:

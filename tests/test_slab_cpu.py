@@ -126,7 +126,8 @@ def _worker(rank, world, port, q):
         # a NaN on one rank reaches every rank as +inf (guards and finiteness checks fail together)
         nanm = comm.allreduce_max([torch.tensor([float("nan") if rank == 1 else 0.5, 0.25])])[0]
         # the fine-operator callbacks' common verdict: one failing rank fails all
-        verdicts = (comm.any_failed(rank == 1), comm.any_failed(False))
+        verdicts = (comm.any_failed(rank == 1), comm.any_failed(False),
+                    float(comm.allreduce_sum([torch.tensor([rank + 1.0])])[0].item()))
         # numpy copies: tensors would travel as shared-memory handles the exiting worker frees
         q.put((rank, ex.numpy().copy(), reg.numpy().copy(), m.tolist(), nanm.tolist(), verdicts))
     finally:
@@ -151,7 +152,7 @@ def test_two_rank_gloo_slab_comm():
     ex_ref = local.exchange_rows(list(v.split(n1 // world, dim=-2)), 7, 9)
     reg_ref = _reg_reference(v, 1, 1e-2)
     for rank, ex, reg, m, nanm, verdicts in res:
-        assert nanm == [float("inf"), 0.25] and verdicts == (True, False)
+        assert nanm == [float("inf"), 0.25] and verdicts == (True, False, 3.0)
         assert np.array_equal(ex, ex_ref[rank].numpy())
         L = n1 // world
         assert np.abs(reg - reg_ref[:, rank * L:(rank + 1) * L]).max() <= 1e-12 * np.abs(reg_ref).max()
@@ -163,3 +164,4 @@ def test_local_allreduce_max_nan_and_verdict():
     m = comm.allreduce_max([torch.tensor([0.5, 1.0]), torch.tensor([float("nan"), 2.0]), torch.tensor([0.1, 3.0])])
     assert all(x.tolist() == [float("inf"), 3.0] for x in m)
     assert comm.any_failed(True) and not comm.any_failed(False)
+    assert [float(x) for x in comm.allreduce_sum([torch.tensor(1.0), torch.tensor(2.0), torch.tensor(4.0)])] == [7.0] * 3
