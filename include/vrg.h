@@ -328,19 +328,39 @@ int vrg_newton_solve_ex(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, co
 typedef int (*vrg_fine_build_fn)(void* user, const double* v, int nt);
 typedef int (*vrg_fine_data_term_fn)(void* user, const double* vt, double* b);
 int vrg_set_fine_operator(vrg_ctx_t ctx, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term, void* user);
-/* The fine operator hook plus evaluateGradient / evaluateObjective (inverse.hpp:60-71) of the same
- * external (slab-decomposed) implementation, so the Newton driver (newton.cpp:24-159) does no
- * whole-grid transport itself: gradient(user, v, nt, reuse, g, m1, scalars) once per outer
- * iteration (reuse = 1: the state of the last objective call, the accepted line-search trial,
- * is this iterate's state, newton.cpp:54-56), objective(user, v, nt, m1, scalars) per line-search
- * trial (return 2 for transport::BlowupError, newton.cpp:118-122).  v, g: 2 contiguous device
- * fields; m1: m(1), one field; scalars = [objective, mismatch, regTerm, penaltyTerm].  The
- * driver adds the reference's logical operation counts.  NULL gradient/objective: as
- * vrg_set_fine_operator. */
+/* External (e.g. slab-decomposed) implementations of everything transport-heavy in newtonSolve,
+ * so the driver (newton.cpp:24-159, precond.cpp:291-358: host control, whole-grid vectors) does
+ * no whole-grid transport itself.  build / data_term: as vrg_set_fine_operator.  Optional pairs:
+ *   gradient(user, v, nt, reuse, g, m1, scalars): evaluateGradient (inverse.cpp:119-148) once per
+ *     outer iteration; reuse = 1: the state of the last objective call (the accepted line-search
+ *     trial) is this iterate's (newton.cpp:54-56); m1 = m(1);
+ *   objective(user, v, nt, m1, scalars): evaluateObjective (inverse.cpp:96-117) per line-search
+ *     trial; return 2 for transport::BlowupError (newton.cpp:118-122);
+ *   coarse_build(user, v, &ntc) per solveKkt (precond::CoarseOperator, precond.cpp:207-240: the
+ *     restricted problem, coarse nt from CFL 5); two_level(user, r, z, k, emin, emax_inflated)
+ *     per application of the two-level CHEB(k) preconditioner (applyTwoLevel, precond.cpp:
+ *     264-289; return 3 when the coarse solve diverged and z = r); coarse_emax(user, &emax,
+ *     &applications) for the Chebyshev bound re-estimate after a breakdown (lanczosEmax from the
+ *     0x5eed probe, precond.cpp:338-347).
+ * v, g, r, z: 2 contiguous device fields; m1: one field; scalars = [objective, mismatch,
+ * regTerm, penaltyTerm].  The driver adds the reference's logical operation counts for the
+ * work the hooks do.  NULL ops clears. */
 typedef int (*vrg_gradient_fn)(void* user, const double* v, int nt, int reuse, double* g, double* m1, double* scalars);
 typedef int (*vrg_objective_fn)(void* user, const double* v, int nt, double* m1, double* scalars);
-int vrg_set_external_ops(vrg_ctx_t ctx, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term,
-                         vrg_gradient_fn gradient, vrg_objective_fn objective, void* user);
+typedef int (*vrg_coarse_build_fn)(void* user, const double* v, int* coarse_nt);
+typedef int (*vrg_two_level_fn)(void* user, const double* r, double* z, int cheb_iters, double emin, double emax);
+typedef int (*vrg_coarse_emax_fn)(void* user, double* emax, int* applications);
+typedef struct vrg_external_ops_s {
+    vrg_fine_build_fn build;
+    vrg_fine_data_term_fn data_term;
+    vrg_gradient_fn gradient;       /* nullable (with objective) */
+    vrg_objective_fn objective;
+    vrg_coarse_build_fn coarse_build;  /* nullable (with two_level and coarse_emax) */
+    vrg_two_level_fn two_level;
+    vrg_coarse_emax_fn coarse_emax;
+    void* user;
+} vrg_external_ops;
+int vrg_set_external_ops(vrg_ctx_t ctx, const vrg_external_ops* ops);
 
 #ifdef __cplusplus
 }

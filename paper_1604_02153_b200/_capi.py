@@ -97,7 +97,7 @@ _SIG = {
     "vrg_newton_solve": ("piippidipppppppip", C.c_int),
     "vrg_newton_solve_ex": ("piippppppppip", C.c_int),
     "vrg_set_fine_operator": ("pppp", C.c_int),
-    "vrg_set_external_ops": ("pppppp", C.c_int),
+    "vrg_set_external_ops": ("pp", C.c_int),
 }
 
 _KIND = {"p": C.c_void_p, "i": C.c_int, "d": C.c_double, "u": C.c_ulonglong}

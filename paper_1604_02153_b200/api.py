@@ -493,9 +493,17 @@ RECORD_FIELDS = ("iter", "gradNormInf", "gradNormRel", "objective", "mismatch", 
 
 FINE_BUILD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int)
 FINE_DATA_TERM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
-# vrg_gradient_fn(user, v, nt, reuse, g, m1, scalars) / vrg_objective_fn(user, v, nt, m1, scalars)
+# the external operators of include/vrg.h (vrg_external_ops)
 GRADIENT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
 OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
+COARSE_BUILD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int))
+TWO_LEVEL_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double)
+COARSE_EMAX_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int))
+EXTERNAL_OPS_FIELDS = ("build", "data_term", "gradient", "objective", "coarse_build", "two_level", "coarse_emax")
+
+
+class ExternalOps(C.Structure):
+    _fields_ = [(name, C.c_void_p) for name in EXTERNAL_OPS_FIELDS] + [("user", C.c_void_p)]
 
 
 def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=0, ls_max_steps=20,
@@ -522,19 +530,19 @@ def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inne
     summ = np.zeros(7)
     hp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
     if fine_operator is not None:
-        cbs = [C.cast(cb, C.c_void_p) for cb in fine_operator.callbacks()]
+        cbs = fine_operator.callbacks()
+        if not isinstance(cbs, dict):
+            cbs = dict(zip(EXTERNAL_OPS_FIELDS, cbs))
+        ops = ExternalOps(**{k: C.cast(cb, C.c_void_p) for k, cb in cbs.items() if cb is not None})
         fine_operator.error = None
-        if len(cbs) == 4:
-            ctx.check(ctx.lib.vrg_set_external_ops(ctx.h, *cbs, None))
-        else:
-            ctx.check(ctx.lib.vrg_set_fine_operator(ctx.h, *cbs, None))
+        ctx.check(ctx.lib.vrg_set_external_ops(ctx.h, C.c_void_p(C.addressof(ops))))
     try:
         code = ctx.lib.vrg_newton_solve(ctx.h, n1, n2, hp(mR), hp(mT), norm, beta, deformation,
                                         C.cast(ci, C.c_void_p), C.cast(cd, C.c_void_p), C.cast(pi, C.c_void_p),
                                         C.cast(pd, C.c_void_p), hp(v1), hp(v2), hp(rec), max_outer + 1, hp(summ))
     finally:
         if fine_operator is not None:
-            ctx.lib.vrg_set_external_ops(ctx.h, None, None, None, None, None)
+            ctx.lib.vrg_set_external_ops(ctx.h, None)
     if fine_operator is not None and code and fine_operator.error is not None:
         raise fine_operator.error
     ctx.check(code)

@@ -868,22 +868,35 @@ int vrg_set_fine_operator(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_te
         c->ctx.fine.dataTerm = data_term;
         c->ctx.fine.gradient = nullptr;
         c->ctx.fine.objective = nullptr;
+        c->ctx.fine.coarseBuild = nullptr;
+        c->ctx.fine.twoLevel = nullptr;
+        c->ctx.fine.coarseEmax = nullptr;
         c->ctx.fine.user = build ? user : nullptr;
     });
 }
 
-int vrg_set_external_ops(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_term_fn data_term,
-                         vrg_gradient_fn gradient, vrg_objective_fn objective, void* user) {
+int vrg_set_external_ops(vrg_ctx_t c, const vrg_external_ops* ops) {
     return guarded(c, [&] {
         if (!c) throw vrg::InvalidArgument("null context");
-        if ((build == nullptr) != (data_term == nullptr) || (gradient == nullptr) != (objective == nullptr) ||
-            (gradient && !build))
-            throw vrg::InvalidArgument("external operators: give build + data_term, optionally gradient + objective");
-        c->ctx.fine.build = build;
-        c->ctx.fine.dataTerm = data_term;
-        c->ctx.fine.gradient = gradient;
-        c->ctx.fine.objective = objective;
-        c->ctx.fine.user = build ? user : nullptr;
+        auto& f = c->ctx.fine;
+        if (!ops) {
+            f = {};
+            return;
+        }
+        if (!ops->build || !ops->data_term || (ops->gradient == nullptr) != (ops->objective == nullptr) ||
+            (ops->coarse_build == nullptr) != (ops->two_level == nullptr) ||
+            (ops->coarse_build == nullptr) != (ops->coarse_emax == nullptr))
+            throw vrg::InvalidArgument(
+                "external operators: build + data_term, optionally gradient + objective and coarse_build + two_level "
+                "+ coarse_emax");
+        f.build = ops->build;
+        f.dataTerm = ops->data_term;
+        f.gradient = ops->gradient;
+        f.objective = ops->objective;
+        f.coarseBuild = ops->coarse_build;
+        f.twoLevel = ops->two_level;
+        f.coarseEmax = ops->coarse_emax;
+        f.user = ops->user;
     });
 }
 

@@ -190,6 +190,13 @@ struct Ctx {
         int (*dataTerm)(void* user, const double* vt, double* b) = nullptr;
         int (*gradient)(void* user, const double* v, int nt, int reuse, double* g, double* m1, double* scalars) = nullptr;
         int (*objective)(void* user, const double* v, int nt, double* m1, double* scalars) = nullptr;
+        // two-level CHEB preconditioner of solveKkt (precond.cpp:264-289, 319-331):
+        // coarseBuild(v, &ntc) per solveKkt (the CoarseOperator), twoLevel(r, z, k, eMin,
+        // eMaxInflated) per application (3 = the coarse solve diverged, z = r), coarseEmax(&eMax,
+        // &applications) for the re-estimate after a breakdown (lanczosEmax, precond.cpp:338-347)
+        int (*coarseBuild)(void* user, const double* v, int* ntc) = nullptr;
+        int (*twoLevel)(void* user, const double* r, double* z, int chebIters, double eMin, double eMax) = nullptr;
+        int (*coarseEmax)(void* user, double* eMax, int* applications) = nullptr;
         void* user = nullptr;
     } fine;
 

@@ -680,8 +680,26 @@ KktResult solveKktOp(Ctx& ctx, const GridDims& g, const Model& model, Weights& w
     std::unique_ptr<CoarseOperator> coarse;
     double eMin = 1.0, eMax = 10.0;
     LinOpDev M;
+    // an external (slab-decomposed) coarse level: built per solve like the CoarseOperator, the
+    // two-level application and the re-estimate by the hooks; logical counts as the library's
+    const bool extCoarse = ctx.fine.coarseBuild && choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb;
+    int ntc = 0;
+    bool lazyCoarse = true;  // the coarse operator's lazy caches are counted by its first matvec
+    auto countCoarseMatvecs = [&](long long k) {
+        if (k <= 0) return;
+        ctx.ffts += k * (8 + (3 + 3LL * ntc) + 3LL * (ntc + 1)) + (lazyCoarse ? 3 : 0);
+        ctx.interps += k * (4LL * ntc + 2) + (lazyCoarse ? 3 : 0);
+        lazyCoarse = false;
+    };
     if (choice.kind == kPcTwoLevel) {
-        coarse = std::make_unique<CoarseOperator>(ctx, g, v, mR, mT, model, coarseCfl);
+        if (extCoarse) {
+            if (ctx.fine.coarseBuild(ctx.fine.user, v, &ntc) != 0)
+                throw std::runtime_error("external coarse operator: build callback failed");
+            ctx.ffts += 8;         // restrictProblem + the coarse velocity: 4 resamples (precond.cpp:166-167,221)
+            ctx.interps += 2 + ntc;  // the coarse GN Hessian's state solve
+        } else {
+            coarse = std::make_unique<CoarseOperator>(ctx, g, v, mR, mT, model, coarseCfl);
+        }
         if (choice.coarseSolver == kCoarseCheb) {
             if (choice.hasEig) {
                 eMin = choice.eMin;
@@ -692,13 +710,31 @@ KktResult solveKktOp(Ctx& ctx, const GridDims& g, const Model& model, Weights& w
         }
         M = [&](const double* r, double* z) {
             const auto tp = std::chrono::steady_clock::now();
-            applyTwoLevel(ctx, g, r, *coarse, choice, tol, eMin, eMax, z);
+            if (extCoarse) {
+                const int rc = ctx.fine.twoLevel(ctx.fine.user, r, z, choice.chebIters, eMin, kEmaxInflation * eMax);
+                if (rc == 3)
+                    std::fprintf(stderr, "precond: coarse solve diverged, falling back to identity\n");
+                else if (rc != 0)
+                    throw std::runtime_error("external coarse operator: two-level callback failed");
+                ctx.ffts += 16;  // cutoff low / high, restrict, prolong (precond.cpp:265-287)
+                countCoarseMatvecs(choice.chebIters);
+            } else {
+                applyTwoLevel(ctx, g, r, *coarse, choice, tol, eMin, eMax, z);
+            }
             precondTime += secondsSince(tp);
         };
     }
     PcgOut out = pcg(ctx, g, A, rhsSplit, M ? &M : nullptr, tol, maxIter, x);
     if (out.indefinitePreconditioner && choice.kind == kPcTwoLevel && choice.coarseSolver == kCoarseCheb) {
-        eMax = coarseLanczosEmax(ctx, *coarse, 30, 0x5eed);
+        if (extCoarse) {
+            int applied = 0;
+            if (ctx.fine.coarseEmax(ctx.fine.user, &eMax, &applied) != 0)
+                throw std::runtime_error("external coarse operator: re-estimate callback failed");
+            ctx.ffts += 4;  // the seeded random probe (randomBandLimitedVelocity: 2 fields x 2 FFTs)
+            countCoarseMatvecs(applied);
+        } else {
+            eMax = coarseLanczosEmax(ctx, *coarse, 30, 0x5eed);
+        }
         std::fprintf(stderr, "precond: re-estimated Chebyshev bound eMax=%.6g after breakdown\n", eMax);
         out = pcg(ctx, g, A, rhsSplit, &M, tol, maxIter, x);
     }

@@ -325,6 +325,97 @@ def distributed_divergence(comm, vs, n1, n2):
     return distributed_spectral(comm, vs, n1, n2, op)
 
 
+def _wave(n, device):
+    k = torch.arange(n, device=device, dtype=torch.int64)
+    return torch.where(k <= n // 2, k, k - n)  # fft.cpp:80
+
+
+def distributed_resample(comm, fields, n1, n2, t1, t2):
+    """spectral::resample (spectral.cpp:157-186) of slab fields (m, n1/G, n2) -> (m, t1/G, t2):
+    modes |k_i| < min(n_i, t_i)/2 kept (truncation or zero padding), amplitude x t1 t2 / (n1 n2);
+    the distributed 2-D FFT of distributed_spectral with the row count changing between the
+    forward and the inverse column transforms."""
+    G = comm.size
+    ncs, nct = n2 // 2 + 1, t2 // 2 + 1
+    wc = -(-nct // G)
+    band1, band2 = min(n1, t1) // 2, min(n2, t2) // 2
+    amp = (t1 * t2) / (n1 * n2)
+    Lt = t1 // G
+    take = min(ncs, nct)
+    send = []
+    for f in fields:
+        sp = torch.fft.rfft(f, dim=-1)[..., :take]
+        sp = torch.nn.functional.pad(sp, (0, G * wc - take))
+        send.append([sp[..., q * wc:(q + 1) * wc].contiguous() for q in range(G)])
+    recv = comm.alltoall(send)
+    back = []
+    for k, q in enumerate(comm.ranks):
+        col = torch.fft.fft(torch.cat(recv[k], dim=-2), dim=-2)  # (m, n1, wc)
+        dev = col.device
+        kt = _wave(t1, dev)
+        keep = kt.abs() < band1
+        rows = torch.remainder(kt[keep], n1)
+        out = torch.zeros(col.shape[:-2] + (t1, wc), dtype=col.dtype, device=dev)
+        out[..., keep, :] = amp * col[..., rows, :]
+        cidx = q * wc + torch.arange(wc, device=dev)
+        out[..., :, (cidx >= band2) | (cidx >= nct)] = 0
+        col = torch.fft.ifft(out, dim=-2)
+        back.append([col[..., r * Lt:(r + 1) * Lt, :].contiguous() for r in range(G)])
+    got = comm.alltoall(back)
+    return [torch.fft.irfft(torch.cat(got[k], dim=-1)[..., :nct], n=t2, dim=-1) for k in range(len(comm.ranks))]
+
+
+def distributed_cutoff_high(comm, fields, n1, n2):
+    """spectral::cutoffFilter(., High) (spectral.cpp:188-203) of slab fields: the modes outside
+    |k1| < n1/4 and |k2| < n2/4."""
+    def op(f, k1, k2, _):
+        low = (k1.abs() < n1 // 4) & (k2.abs() < n2 // 4)
+        return torch.where(low, torch.zeros_like(f), f)
+    return distributed_spectral(comm, fields, n1, n2, op)
+
+
+def inv_half_symbol(k1, k2, norm, beta):
+    """(beta gamma_reg)^(-1/2) (spectral.cpp:46-66, 121-131): gamma = |k|^(2p) by repeated
+    multiplication, gamma_reg(0) = 1, then a correctly rounded square root and division."""
+    ksq = k1 * k1 + k2 * k2
+    gam = ksq
+    for _ in range(int(norm) - 1):
+        gam = gam * ksq
+    gam = torch.where(gam == 0, torch.ones_like(gam), gam)
+    return 1.0 / torch.sqrt(beta * gam)
+
+
+def tridiag_max_eig(alpha, beta):
+    """tridiagMaxEig (precond.cpp:88-117): Sturm bisection, 100 halvings."""
+    m = len(alpha)
+    if m == 1:
+        return alpha[0]
+    lo = hi = alpha[0]
+    for i in range(m):
+        off = (abs(beta[i - 1]) if i > 0 else 0.0) + (abs(beta[i]) if i < m - 1 else 0.0)
+        lo = min(lo, alpha[i] - off)
+        hi = max(hi, alpha[i] + off)
+
+    def count_below(x):
+        count, d = 0, 1.0
+        for i in range(m):
+            offsq = beta[i - 1] * beta[i - 1] if i > 0 else 0.0
+            d = alpha[i] - x - offsq / d
+            if d == 0.0:
+                d = -1e-300
+            if d < 0.0:
+                count += 1
+        return count
+
+    for _ in range(100):
+        mid = 0.5 * (lo + hi)
+        if count_below(mid) >= m:
+            hi = mid
+        else:
+            lo = mid
+    return 0.5 * (lo + hi)
+
+
 # ------------------------------------------------------------------------------ operator
 class SlabHessian:
     """GN Hessian matvec of one grid decomposed over comm's ranks (see the module docstring)."""
@@ -657,6 +748,106 @@ class SlabHessian:
                 raise api.BlowupError(f"adjoint solve exceeded the blow-up guard at step {j}")
 
 
+class SlabCoarse:
+    """precond::CoarseOperator (precond.cpp:163-171, 207-240) on half-grid slabs: the problem and
+    the velocity restricted by distributed spectral truncation, the coarse nt from the CFL-5 rule
+    (transport.cpp:44-50, maxima over ranks), a slab GN operator at the coarse velocity, and the
+    pieces of the two-level CHEB preconditioner (precond.cpp:180-205, 264-289) and of the
+    Chebyshev bound re-estimate (lanczosEmax, precond.cpp:120-161) on those slabs."""
+
+    def __init__(self, ctx, comm, vs, mRs, mTs, n1, n2, norm, beta, cfl=5.0):
+        self.ctx, self.comm = ctx, comm
+        self.n1, self.n2, self.t1, self.t2 = n1, n2, n1 // 2, n2 // 2
+        if self.t1 % comm.size:
+            raise api.InvalidArgument("slab decomposition: the coarse grid's n1 must be a multiple of the ranks")
+        self.norm, self.beta = norm, beta
+        self.vc = distributed_resample(comm, vs, n1, n2, self.t1, self.t2)
+        ims = distributed_resample(comm, [torch.stack([r, t]) for r, t in zip(mRs, mTs)], n1, n2, self.t1, self.t2)
+        self.mTc = [im[1].contiguous() for im in ims]
+        h1, h2 = 2 * math.pi / self.t1, 2 * math.pi / self.t2
+        m1 = float(comm.allreduce_max([v[0].abs().amax() for v in self.vc])[0])
+        m2 = float(comm.allreduce_max([v[1].abs().amax() for v in self.vc])[0])
+        ratio = max(0.0, m1 / (cfl * h1), m2 / (cfl * h2))
+        self.nt = max(2, int(math.ceil(ratio)))
+        self.S = SlabHessian.build(ctx, comm, self.vc, self.mTc, self.t1, self.nt, norm, beta)
+
+    def _dot(self, a, b):
+        h = (2 * math.pi / self.t1) * (2 * math.pi / self.t2)
+        return h * float(self.comm.allreduce_sum([torch.sum(x * y).reshape(1) for x, y in zip(a, b)])[0].item())
+
+    def split(self, ss):
+        """applySplitHessianOf (precond.cpp:20-26): M^{-1/2} Q M^{-1/2} s + s on coarse slabs."""
+        op = lambda f, k1, k2, _: f * inv_half_symbol(k1, k2, self.norm, self.beta)  # noqa: E731
+        t = distributed_spectral(self.comm, ss, self.t1, self.t2, op)
+        b = self.S.apply(t, data_term_only=True)
+        o = distributed_spectral(self.comm, b, self.t1, self.t2, op)
+        return [x + s for x, s in zip(o, ss)]
+
+    def chebyshev(self, rhs, k, emin, emax):
+        """chebyshevSolve (precond.cpp:180-205): x_0 = 0, exactly k operator applications."""
+        theta, delta = 0.5 * (emax + emin), 0.5 * (emax - emin)
+        sigma = theta / delta
+        rho = 1.0 / sigma
+        x = [torch.zeros_like(r) for r in rhs]
+        r = [t.clone() for t in rhs]
+        d = [(1.0 / theta) * t for t in r]
+        for it in range(1, k + 1):
+            if it > 1:
+                rho_new = 1.0 / (2.0 * sigma - rho)
+                d = [(rho_new * rho) * di + (2.0 * rho_new / delta) * ri for di, ri in zip(d, r)]
+                rho = rho_new
+            x = [xi + di for xi, di in zip(x, d)]
+            ad = self.split(d)
+            r = [ri - ai for ri, ai in zip(r, ad)]
+        return x
+
+    def two_level(self, rs, k, emin, emax):
+        """applyTwoLevel (precond.cpp:264-289), CHEB(k): the low band restricted (the cutoff band
+        is the restriction band), solved, prolonged, plus the high band; (z slabs, diverged)."""
+        rc = distributed_resample(self.comm, rs, self.n1, self.n2, self.t1, self.t2)
+        high = distributed_cutoff_high(self.comm, rs, self.n1, self.n2)
+        sc = self.chebyshev(rc, k, emin, emax)
+        bad = torch.tensor(float(any(not bool(torch.isfinite(x).all()) for x in sc)))
+        if float(self.comm.allreduce_max([bad] * len(self.comm.ranks))[0]) > 0:
+            return [r.clone() for r in rs], True
+        up = distributed_resample(self.comm, sc, self.t1, self.t2, self.n1, self.n2)
+        return [u + h for u, h in zip(up, high)], False
+
+    def lanczos_emax(self, steps=30, seed=0x5EED):
+        """lanczosEmax (precond.cpp:120-161) of the coarse split operator from the seeded band-limited
+        probe (the library's randomBandLimitedVelocity on the whole coarse grid, sliced); returns
+        (eMax, operator applications)."""
+        Lc = self.t1 // self.comm.size
+        probe = api.random_bandlimited_velocity(self.ctx, (self.t1, self.t2), seed)
+        q = [torch.stack([probe[0][r * Lc:(r + 1) * Lc], probe[1][r * Lc:(r + 1) * Lc]]).contiguous()
+             for r in self.comm.ranks]
+        nq = math.sqrt(self._dot(q, q))
+        if not nq > 0.0:
+            return 1.0, 0
+        q = [(1.0 / nq) * x for x in q]
+        basis, alpha, beta, applied = [q], [], [], 0
+        for j in range(steps):
+            w = self.split(basis[j])
+            applied += 1
+            if j > 0:
+                w = [wi + (-beta[j - 1]) * bi for wi, bi in zip(w, basis[j - 1])]
+            a = self._dot(w, basis[j])
+            alpha.append(a)
+            w = [wi + (-a) * bi for wi, bi in zip(w, basis[j])]
+            for qi in basis:
+                c = self._dot(w, qi)
+                w = [wi + (-c) * qq for wi, qq in zip(w, qi)]
+            b = math.sqrt(self._dot(w, w))
+            if not math.isfinite(b):
+                raise api.NotSupported("slab coarse Lanczos broke down (non-finite); the power-iteration fallback "
+                                       "of precond.cpp:153 is not implemented on the slabs")
+            if b < 1e-12:
+                break
+            beta.append(b)
+            basis.append([(1.0 / b) * wi for wi in w])
+        return tridiag_max_eig(alpha, beta[:len(alpha) - 1]), applied
+
+
 class SlabFineOperator:
     """Slab-decomposed operators for `api.newton_solve(..., fine_operator=...)` (config 5a).
 
@@ -670,9 +861,12 @@ class SlabFineOperator:
         (evaluateGradient, inverse.cpp:119-148) and objective(v, nt) per line-search trial
         (evaluateObjective, inverse.cpp:96-117), C ABI vrg_set_external_ops: the state, adjoint
         and body force of the gradient and the state of every trial are slab SL solves, and
-        the Hessian's per-iterate invariants reuse the gradient's (trace, state, grad m_j, div v).
-    What stays replicated is the vector algebra of the driver and the two-level
-    preconditioner's coarse solve.  All ranks call the hooks in the same order because the
+        the Hessian's per-iterate invariants reuse the gradient's (trace, state, grad m_j, div v);
+      * and, where the half grid fits the slab step, the two-level CHEB preconditioner's coarse
+        level (SlabCoarse: restriction, coarse GN operator, Chebyshev, prolongation, the bound
+        re-estimate) on half-grid slabs.
+    What stays replicated is the vector algebra of the driver and the eigenvalue estimate at
+    v = 0 made once per solve.  All ranks call the hooks in the same order because the
     driver is deterministic and sees identical data; every callback reaches a common verdict."""
 
     def __init__(self, ctx, comm, mT, norm, beta, mR=None):
@@ -700,11 +894,26 @@ class SlabFineOperator:
         self._cb_data_term = api.FINE_DATA_TERM_FN(self._data_term)
         self._cb_gradient = api.GRADIENT_FN(self._gradient)
         self._cb_objective = api.OBJECTIVE_FN(self._objective)
+        self._cb_coarse_build = api.COARSE_BUILD_FN(self._coarse_build)
+        self._cb_two_level = api.TWO_LEVEL_FN(self._two_level)
+        self._cb_coarse_emax = api.COARSE_EMAX_FN(self._coarse_emax)
+        self.coarse = None
+        # the coarse level on slabs too where its rows fit the slab step (half-grid rows of a
+        # multiple of 256 up to 4096, half-grid n1 divisible by the ranks); else the driver's
+        # own coarse operator, replicated
+        c1, c2 = self.n1 // 2, self.n2 // 2
+        self.coarse_slabs = self.full and c2 % 256 == 0 and 256 <= c2 <= 4096 and c1 % comm.size == 0
+        self.coarse_builds = self.precond_applies = 0
+        self.coarse_s = self.precond_s = 0.0
 
     def callbacks(self):
+        cbs = {"build": self._cb_build, "data_term": self._cb_data_term}
         if self.full:
-            return self._cb_build, self._cb_data_term, self._cb_gradient, self._cb_objective
-        return self._cb_build, self._cb_data_term
+            cbs.update(gradient=self._cb_gradient, objective=self._cb_objective)
+        if self.coarse_slabs:
+            cbs.update(coarse_build=self._cb_coarse_build, two_level=self._cb_two_level,
+                       coarse_emax=self._cb_coarse_emax)
+        return cbs
 
     def _full(self, ptr, comps=2):
         N = self.n1 * self.n2
@@ -828,6 +1037,50 @@ class SlabFineOperator:
             self.builds += 1
             self.build_s += time.perf_counter() - t0
         except BaseException as e:  # re-raised by api.newton_solve
+            self.error = e
+            failed = True
+        return self._verdict(failed)
+
+    def _coarse_build(self, _user, vptr, ntc_ptr):
+        import time
+
+        failed = False
+        try:
+            t0 = time.perf_counter()
+            self.coarse = None
+            self.coarse = SlabCoarse(self.ctx, self.comm, self._slabs(self._full(vptr)), self.mRs, self.mTs, self.n1,
+                                     self.n2, self.norm, self.beta)
+            ntc_ptr[0] = self.coarse.nt
+            self.coarse_builds += 1
+            self.coarse_s += time.perf_counter() - t0
+        except BaseException as e:
+            self.error = e
+            failed = True
+        return self._verdict(failed)
+
+    def _two_level(self, _user, rptr, zptr, k, emin, emax):
+        import time
+
+        failed, diverged = False, False
+        try:
+            t0 = time.perf_counter()
+            zs, diverged = self.coarse.two_level(self._slabs(self._full(rptr)), int(k), emin, emax)
+            self.comm.allgather_rows(zs, self._full(zptr))
+            self.precond_applies += 1
+            self.precond_s += time.perf_counter() - t0
+        except BaseException as e:
+            self.error = e
+            failed = True
+        rc = self._verdict(failed)
+        return rc if rc else (3 if diverged else 0)
+
+    def _coarse_emax(self, _user, emax_ptr, applied_ptr):
+        failed = False
+        try:
+            e, applied = self.coarse.lanczos_emax()
+            emax_ptr[0] = e
+            applied_ptr[0] = applied
+        except BaseException as e:
             self.error = e
             failed = True
         return self._verdict(failed)

@@ -34,8 +34,8 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("n,nt,G,full", [(256, 8, 1, False), (256, 8, 2, False), (256, 16, 4, False),
-                                         (512, 8, 8, False), (256, 8, 1, True), (256, 8, 2, True),
-                                         (256, 16, 4, True), (512, 8, 8, True)])
+                                         (512, 8, 8, False), (256, 8, 2, True), (512, 8, 1, True),
+                                         (512, 16, 2, True), (512, 8, 4, True), (512, 8, 8, True)])
 def test_slab_newton_matches_single_device(ctx, api, n, nt, G, full):
     """full: the gradient and every line-search objective are slab solves too (vrg_set_external_ops),
     so the driver runs no whole-grid transport; else only the fine matvec is decomposed."""
@@ -59,9 +59,13 @@ def test_slab_newton_matches_single_device(ctx, api, n, nt, G, full):
     # one slab build per Hessian (every iteration but a converged last one), one gather per matvec
     assert fo.builds == sum(1 for r in recs if r["innerIterations"] > 0)
     assert fo.matvecs >= sum(r["innerIterations"] for r in recs)
-    if full:  # one slab gradient per outer iteration, one slab objective per line-search trial
+    if full:  # one slab gradient per outer iteration, one slab objective per line-search trial,
+        # one slab coarse operator per KKT solve and a two-level application per PCG step (+1)
         assert fo.gradients == len(recs)
         assert fo.objectives == sum(r["lineSearchSteps"] for r in recs)
+        if fo.coarse_slabs:  # n = 512: the half grid's 256-sample rows fit the slab step
+            assert fo.coarse_builds == fo.builds
+            assert fo.precond_applies >= sum(r["innerIterations"] + 1 for r in recs if r["innerIterations"] > 0)
 
 
 class _Failing:

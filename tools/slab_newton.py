@@ -3,16 +3,18 @@
 random smooth v* (seed 2000, max|v|=0.3) -> m_R.  Time to solution through newton_solve:
 
   --mode single : the library's single-device solve (its own fine Hessian);
-  --mode slab   : the fine GN data term slab-decomposed over the torchrun ranks
-                  (slab.SlabFineOperator over NCCL, one slab per GPU); everything else of the
-                  driver runs replicated on every rank.
+  --mode slab   : slab-decomposed over the torchrun ranks (slab.SlabFineOperator over NCCL,
+                  one slab per GPU): the fine GN data term, the gradient (state, adjoint, body
+                  force) and every line-search objective; the driver's vector algebra and the
+                  two-level preconditioner's coarse solve run replicated on every rank.
 
   python tools/slab_newton.py --mode single
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
       --master-port 29513 tools/slab_newton.py --mode slab
 
-Rank 0 prints one JSON line (iterations, Krylov iterations, wall time, time in the slab build
-and data term callbacks).  --max-outer bounds the run.
+Rank 0 prints one JSON line (iterations, Krylov iterations, wall time, the time in each slab
+callback and the share of the solve outside them: the non-decomposed work).  --max-outer bounds
+the run.
 """
 import argparse
 import json
@@ -56,7 +58,7 @@ def main():
     v1, v2 = synth.smooth_velocity(n, n, 2000)
     mR = api.Solver(ctx, (ctx.field(v1), ctx.field(v2)), nt).solve_state_final(ctx.field(mT)).cpu().numpy()
     t_inputs = time.perf_counter() - t0
-    fo = slab.SlabFineOperator(ctx, comm, mT, api.H2SEMI, a.beta) if comm is not None else None
+    fo = slab.SlabFineOperator(ctx, comm, mT, api.H2SEMI, a.beta, mR=mR) if comm is not None else None
     ctx.sync()
     if comm is not None:
         comm.dist.barrier()
@@ -84,8 +86,16 @@ def main():
             "v_max": float(max(np.abs(w1).max(), np.abs(w2).max())),
         }
         if fo is not None:
+            inside = fo.build_s + fo.apply_s + fo.gradient_s + fo.objective_s + fo.coarse_s + fo.precond_s
             line.update(slab_builds=fo.builds, slab_build_s=fo.build_s, slab_matvecs=fo.matvecs,
-                        slab_data_term_s=fo.apply_s)
+                        slab_data_term_s=fo.apply_s, slab_gradients=fo.gradients, slab_gradient_s=fo.gradient_s,
+                        slab_objectives=fo.objectives, slab_objective_s=fo.objective_s,
+                        slab_coarse_builds=fo.coarse_builds, slab_coarse_s=fo.coarse_s,
+                        slab_two_level_applies=fo.precond_applies, slab_two_level_s=fo.precond_s,
+                        decomposed_s=inside, non_decomposed_s=wall - inside,
+                        non_decomposed_share=(wall - inside) / wall,
+                        note="non-decomposed = the driver's whole-grid vector algebra, the eigenvalue estimate "
+                             "at v=0 (once per solve) and the final Jacobian (rank 0's clock)")
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.dist.destroy_process_group()
