@@ -350,6 +350,7 @@ typedef int (*vrg_objective_fn)(void* user, const double* v, int nt, double* m1,
 typedef int (*vrg_coarse_build_fn)(void* user, const double* v, int* coarse_nt);
 typedef int (*vrg_two_level_fn)(void* user, const double* r, double* z, int cheb_iters, double emin, double emax);
 typedef int (*vrg_coarse_emax_fn)(void* user, double* emax, int* applications);
+typedef int (*vrg_split_fn)(void* user, const double* s, double* o);
 typedef struct vrg_external_ops_s {
     vrg_fine_build_fn build;
     vrg_fine_data_term_fn data_term;
@@ -358,6 +359,8 @@ typedef struct vrg_external_ops_s {
     vrg_coarse_build_fn coarse_build;  /* nullable (with two_level and coarse_emax) */
     vrg_two_level_fn two_level;
     vrg_coarse_emax_fn coarse_emax;
+    vrg_split_fn split;             /* nullable: the whole split matvec M^{-1/2} Q M^{-1/2} s + s
+                                       (precond.cpp:20-26) instead of data_term + the driver's FFTs */
     void* user;
 } vrg_external_ops;
 int vrg_set_external_ops(vrg_ctx_t ctx, const vrg_external_ops* ops);

@@ -499,7 +499,9 @@ OBJECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
 COARSE_BUILD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int))
 TWO_LEVEL_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double)
 COARSE_EMAX_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int))
-EXTERNAL_OPS_FIELDS = ("build", "data_term", "gradient", "objective", "coarse_build", "two_level", "coarse_emax")
+SPLIT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+EXTERNAL_OPS_FIELDS = ("build", "data_term", "gradient", "objective", "coarse_build", "two_level", "coarse_emax",
+                       "split")
 
 
 class ExternalOps(C.Structure):

@@ -871,6 +871,7 @@ int vrg_set_fine_operator(vrg_ctx_t c, vrg_fine_build_fn build, vrg_fine_data_te
         c->ctx.fine.coarseBuild = nullptr;
         c->ctx.fine.twoLevel = nullptr;
         c->ctx.fine.coarseEmax = nullptr;
+        c->ctx.fine.split = nullptr;
         c->ctx.fine.user = build ? user : nullptr;
     });
 }
@@ -896,6 +897,7 @@ int vrg_set_external_ops(vrg_ctx_t c, const vrg_external_ops* ops) {
         f.coarseBuild = ops->coarse_build;
         f.twoLevel = ops->two_level;
         f.coarseEmax = ops->coarse_emax;
+        f.split = ops->split;
         f.user = ops->user;
     });
 }

@@ -197,6 +197,9 @@ struct Ctx {
         int (*coarseBuild)(void* user, const double* v, int* ntc) = nullptr;
         int (*twoLevel)(void* user, const double* r, double* z, int chebIters, double eMin, double eMax) = nullptr;
         int (*coarseEmax)(void* user, double* eMax, int* applications) = nullptr;
+        // the whole split matvec M^{-1/2} Q M^{-1/2} s + s (applySplitHessianOf, precond.cpp:20-26),
+        // so the regularisation symbols are applied on the slabs too (nullable: data_term is used)
+        int (*split)(void* user, const double* s, double* o) = nullptr;
         void* user = nullptr;
     } fine;
 

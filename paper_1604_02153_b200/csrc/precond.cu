@@ -764,6 +764,15 @@ ExternalFineOperator::ExternalFineOperator(Ctx& ctx, const GridDims& g, const do
 
 // Hessian::launchSplit with the data term of the hook: t = M^{-1/2} s, b = Q t, o = M^{-1/2} b + s.
 void ExternalFineOperator::applySplit(const double* s, double* o) {
+    if (ctx_.fine.split) {
+        if (ctx_.fine.split(ctx_.fine.user, s, o) != 0)
+            throw std::runtime_error("external fine operator: split callback failed");
+        ctx_.ffts += 8 + (3 + 3LL * nt_) + 3LL * (nt_ + 1) + lazyFfts_;
+        ctx_.interps += 4LL * nt_ + 2 + lazyInterps_;
+        lazyInterps_ = 0;
+        lazyFfts_ = 0;
+        return;
+    }
     const std::size_t N = g_.points(), NS = g_.specPoints();
     cplx* S = reinterpret_cast<cplx*>(ctx_.scratchBuf(150, sizeof(cplx) * 4 * NS));
     cplx* T = S + 2 * NS;

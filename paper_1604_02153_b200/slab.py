@@ -897,6 +897,7 @@ class SlabFineOperator:
         self._cb_coarse_build = api.COARSE_BUILD_FN(self._coarse_build)
         self._cb_two_level = api.TWO_LEVEL_FN(self._two_level)
         self._cb_coarse_emax = api.COARSE_EMAX_FN(self._coarse_emax)
+        self._cb_split = api.SPLIT_FN(self._split)
         self.coarse = None
         # the coarse level on slabs too where its rows fit the slab step (half-grid rows of a
         # multiple of 256 up to 4096, half-grid n1 divisible by the ranks); else the driver's
@@ -909,7 +910,7 @@ class SlabFineOperator:
     def callbacks(self):
         cbs = {"build": self._cb_build, "data_term": self._cb_data_term}
         if self.full:
-            cbs.update(gradient=self._cb_gradient, objective=self._cb_objective)
+            cbs.update(gradient=self._cb_gradient, objective=self._cb_objective, split=self._cb_split)
         if self.coarse_slabs:
             cbs.update(coarse_build=self._cb_coarse_build, two_level=self._cb_two_level,
                        coarse_emax=self._cb_coarse_emax)
@@ -1080,6 +1081,27 @@ class SlabFineOperator:
             e, applied = self.coarse.lanczos_emax()
             emax_ptr[0] = e
             applied_ptr[0] = applied
+        except BaseException as e:
+            self.error = e
+            failed = True
+        return self._verdict(failed)
+
+    def _split(self, _user, sptr, optr):
+        """applySplitHessianOf (precond.cpp:20-26) on the slabs: t = M^{-1/2} s, the slab data term,
+        o = M^{-1/2} b + s (the symbols by the distributed FFT)."""
+        import time
+
+        failed = False
+        try:
+            t0 = time.perf_counter()
+            op = lambda f, k1, k2, _: f * inv_half_symbol(k1, k2, self.norm, self.beta)  # noqa: E731
+            ss = self._slabs(self._full(sptr))
+            t = distributed_spectral(self.comm, ss, self.n1, self.n2, op)
+            b = self.S.apply(t, data_term_only=True)
+            o = distributed_spectral(self.comm, b, self.n1, self.n2, op)
+            self.comm.allgather_rows([x + y for x, y in zip(o, ss)], self._full(optr))
+            self.matvecs += 1
+            self.apply_s += time.perf_counter() - t0
         except BaseException as e:
             self.error = e
             failed = True
