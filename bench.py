@@ -593,8 +593,10 @@ def main():
         # DRAM traffic of the dominant kernel per launch, from the committed ncu --set full
         # capture (profiles/, cold-cache replay: an upper bound of the warm per-launch traffic)
         traffic = None
+        traffic_file = next((f for f in ("r2_ncu_traffic.json", "r1_ncu_traffic.json")
+                             if os.path.exists(os.path.join(ROOT, "profiles", f))), "r1_ncu_traffic.json")
         try:
-            with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", traffic_file)) as f:
                 tmap = json.load(f)
             pat = kd.get("ncu_kernel")
             hits = [v for k, v in tmap.items() if pat and pat in k]
@@ -616,7 +618,7 @@ def main():
             "clocks": r["clocks"],
             "roofline": {"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "traffic_source": "profiles/r1_ncu_traffic.json (ncu --set full, dram__bytes_read+write)",
+                         "traffic_source": f"profiles/{traffic_file} (ncu --set full, dram__bytes_read+write)",
                          "bytes_per_launch": bytes_launch, "avg_launch_us": avg_s * 1e6,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"},
             "matvec_roofline": {"algorithmic_bytes": mv_bytes, "model": "(24 nt + 12) F, SURVEY 8(d)",
