@@ -215,6 +215,11 @@ int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajec
  * incremental-adjoint step, 9 SL state step band form (gather + next row pass, then column
  * pass), 10 SL state step plain form (prefilter + gather)), `iters` back-to-back launches on the context stream (bench.py roofline) */
 int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch);
+/* instrumentation: row-to-SM mapping of the band steps for operators created afterwards (0 = by
+ * grid size, 1 = one block per grid row, 2 = strip blocks of consecutive rows where the row
+ * length allows it); process-wide, returns the previous mode.  Both forms compute identical
+ * bits; tests and the kernel benchmark use it to compare them. */
+int vrg_band_mapping(int mode);
 /* 1 when the time loops run the band kernels (gather + epilogue + next row pass fused; ids 7
  * and 8 of vrg_hess_bench_kernel), 0 for the plain 3-kernel step */
 int vrg_hess_band_path(vrg_hess_t h, int* band);

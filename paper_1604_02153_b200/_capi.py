@@ -78,6 +78,7 @@ _SIG = {
     "vrg_hess_state": ("pp", C.c_int),
     "vrg_hess_bench_kernel": ("piip", C.c_int),
     "vrg_hess_band_path": ("pp", C.c_int),
+    "vrg_band_mapping": ("i", C.c_int),
     "vrg_hess_buffers": ("pp", C.c_int),
     "vrg_prefilter_rows": ("piippp", C.c_int),
     "vrg_slab_cols": ("piipp", C.c_int),

@@ -7,6 +7,7 @@
 #include <memory>
 
 #include "../../include/vrg.h"
+#include "evalband.cuh"
 #include "heun.cuh"
 #include "precond.cuh"
 
@@ -642,6 +643,10 @@ int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, con
 
 int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch) {
     return guarded(h->owner, [&] { *ms_per_launch = h->hess.benchKernel(kernel, iters); });
+}
+
+int vrg_band_mapping(int mode) {
+    return vrg::g_bandMapping.exchange(mode < 0 || mode > 2 ? 0 : mode);
 }
 
 int vrg_hess_band_path(vrg_hess_t h, int* band) {

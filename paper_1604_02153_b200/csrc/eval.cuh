@@ -9,6 +9,8 @@
 // go to guardPartials[blockIdx.x] when Epi::kGuard.
 #pragma once
 
+#include <algorithm>
+
 #include "interp.cuh"
 
 namespace vrg {
@@ -30,12 +32,18 @@ struct CoeffSet {
 
 // xStable: the departure points are not written by any kernel still in flight (the matvec
 // time loops), so the cell computation runs before the programmatic-dependency wait.
+// blockIdx.y: member of a batch of coefficient sets at the same points (coefficient offset
+// csZ, epilogue index offset epiZ per member; guard-free epilogues only).
 template <int NF, class Epi>
 __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const double* __restrict__ x1,
                                                          const double* __restrict__ x2, int n1, int n2, int xStable,
-                                                         Epi epi) {
+                                                         Epi epi, std::size_t csZ, std::size_t epiZ) {
     const int N = n1 * n2;  // grids up to 2^31 points
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.y) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) cs.c[f] += blockIdx.y * csZ;
+    }
     double guard = 0.0;
     if (!xStable) pdlWait();
     double w1[4], w2[4];
@@ -48,7 +56,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const 
     // epilogue operands that no in-flight kernel writes (per-iterate fields) are loaded now,
     // so their latency overlaps the departure-point loads and the gather
     typename Epi::Pre pre{};
-    if (p < N) pre = epi.prefetch(p);
+    if (p < N) pre = epi.prefetch(p + blockIdx.y * epiZ);
     if (xStable) pdlWait();
     pdlTrigger();
     if (p < N) {
@@ -82,7 +90,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const 
             }
             val[f] = acc;
         }
-        const double gv = fabs(epi(p, val, pre));
+        const double gv = fabs(epi(p + blockIdx.y * epiZ, val, pre));
         if (gv == gv) guard = gv;  // NaN ignored, inf kept
     }
     if constexpr (Epi::kGuard) {
@@ -139,11 +147,28 @@ void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const double* 
     {
         LaunchScope ls_(ctx, Epi::kName);
         launchPdl(1, k_evaluate<NF, Epi>, grid1d(N, kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, cs, x1, x2, g.n1, g.n2,
-                  xStable ? 1 : 0, epi);
+                  xStable ? 1 : 0, epi, std::size_t(0), std::size_t(0));
+    }
+}
+
+// `count` coefficient sets cs + k*csZ evaluated at the same points in one launch, the
+// epilogue of member k at index p + k*epiZ (guard-free epilogues, e.g. EpiStore2).
+template <int NF, class Epi>
+void launchEvaluateBatch(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, std::size_t csZ, int count, const double* x1,
+                         const double* x2, const Epi& epi, std::size_t epiZ) {
+    static_assert(!Epi::kGuard, "batched evaluate: guard-free epilogues only");
+    const std::size_t N = g.points();
+    {
+        LaunchScope ls_(ctx, Epi::kName);
+        launchPdl(1, k_evaluate<NF, Epi>, dim3(grid1d(N, kEvalBlock).x, count), dim3(kEvalBlock), 0, ctx.stream, cs,
+                  x1, x2, g.n1, g.n2, 0, epi, csZ, epiZ);
     }
 }
 
 inline unsigned evalBlocks(const GridDims& g) { return grid1d(g.points(), kEvalBlock).x; }
+// Guard partials per step: one per evaluate block or per grid row (band kernels), whichever
+// is more (unused entries stay 0, GuardLog::reset).
+inline unsigned guardBlocks(const GridDims& g) { return std::max(evalBlocks(g), static_cast<unsigned>(g.n1)); }
 
 // Plain stores.
 struct EpiStore1 {

@@ -9,19 +9,33 @@
 // structure (256 threads, epilogue operands prefetched, programmatic dependent launch).
 #pragma once
 
+#include <atomic>
+
 #include "eval.cuh"
 
 namespace vrg {
 
 constexpr int kBandThreads = 256;
 
-// one block per row; n2 a multiple of 256 up to 4096 (chunks per row <= threads)
-inline bool bandFusable(const GridDims& g) { return g.n2 >= 256 && g.n2 <= 4096 && g.n2 % 256 == 0; }
-
-inline std::size_t bandSmem(const GridDims& g) {
-    const int nc = g.n2 / kL;
-    return sizeof(double) * (static_cast<std::size_t>(nc) * kCS + 3 * nc);
+// Threads per row (one thread per 16-sample chunk in the row filter, n2 / TW nodes per thread
+// in the gather): the largest of 256 / 128 / 64 / 32 dividing n2, so coarse and small grids
+// (n2 = 32 .. 192) take the band path too.
+inline int bandTW(int n2) {
+    for (int tw : {256, 128, 64, 32})
+        if (n2 % tw == 0) return tw;
+    return 0;
 }
+
+// one block per row; n2 a multiple of 32 with its chunks (n2 / 16) within the row's threads
+inline bool bandFusable(const GridDims& g) {
+    const int tw = bandTW(g.n2);
+    return tw && g.n2 >= 32 && g.n2 / kL <= tw;
+}
+
+// Doubles of shared memory one row needs (chunked row + chunk summaries + guard partials).
+__host__ __device__ inline int bandRowSmem(int n2, int tw) { return (n2 / kL) * (kCS + 3) + (tw + 31) / 32; }
+
+inline std::size_t bandSmem(const GridDims& g) { return sizeof(double) * bandRowSmem(g.n2, bandTW(g.n2)); }
 
 inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n1); }
 
@@ -56,20 +70,43 @@ struct BandMinBlocks {
     static constexpr int value = 4;
 };
 
-template <class Epi, bool kGather, bool kWindow = false>
-__global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
-                                                            const double* __restrict__ x2, int n1, int n2, Epi epi,
-                                                            double* __restrict__ rowOut, unsigned* nonfinite,
-                                                            BandWindow win = BandWindow{}) {
+// Barrier policies of one row's work: the whole block (k_eval_band) or one row worker of a
+// strip block (k_eval_strip: named barrier `id` over the worker's TW threads).
+struct BarBlock {
+    __device__ void sync() const { __syncthreads(); }
+    __device__ bool syncOr(bool p) const { return __syncthreads_or(p); }
+};
+template <int TW>
+struct BarNamed {
+    int id;
+    __device__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(TW) : "memory"); }
+    __device__ bool syncOr(bool p) const {
+        unsigned o;
+        asm volatile(
+            "{ .reg .pred pi, po;\n\t setp.ne.u32 pi, %1, 0;\n\t bar.red.or.pred po, %2, %3, pi;\n\t"
+            " selp.u32 %0, 1, 0, po; }"
+            : "=r"(o)
+            : "r"(static_cast<unsigned>(p)), "r"(id), "n"(TW)
+            : "memory");
+        return o != 0;
+    }
+};
+
+// One grid row r by TW threads (t = 0..TW-1): gather at the row's departure points, step
+// epilogue, guard partial of the row, then the exact periodic row filter in shared memory and
+// the row-filtered output.  `sm` holds bandRowSmem(n2, TW) doubles.
+template <class Epi, bool kGather, bool kWindow, int TW, class Bar>
+__device__ __forceinline__ void bandRow(const CoeffSet<1>& cs, const double* __restrict__ x1,
+                                        const double* __restrict__ x2, int n1, int n2, const Epi& epi,
+                                        double* __restrict__ rowOut, unsigned* nonfinite, const BandWindow& win,
+                                        int r, int t, double* sm, Bar bar) {
     if (!kGather) pdlWait();
-    extern __shared__ __align__(16) double sm[];
     const int nc = n2 / kL;
     double* E = sm + nc * kCS;
     double* F0 = E + nc;
     double* P0 = F0 + nc;
-    const int t = threadIdx.x;
-    const int r = blockIdx.x;
-    const int per = n2 / kBandThreads;  // nodes per thread (<= 16)
+    double* red = P0 + nc;
+    const int per = n2 / TW;  // nodes per thread
     const int PW = n2 + 3;
     const double inv1 = n1 * (1.0 / kTwoPi), inv2 = n2 * (1.0 / kTwoPi);
     // padded-layout row of the first tap (cellBase) -> row of the coefficient array
@@ -107,7 +144,7 @@ __global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eva
         if (kGather) pdlWait();
     }
     for (int k = 0; k < per; ++k) {
-        const int col = t + kBandThreads * k;
+        const int col = t + TW * k;
         const int p = r * n2 + col;
         double w1[4], w2[4];
         int base = 0;
@@ -117,22 +154,20 @@ __global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eva
                 const int b1 = tapRow(cellBase(xa, inv1, n1, w1));
                 const int b2 = cellBase(xb, inv2, n2, w2);
                 base = b1 * PW + b2;
-
             }
             cur = pre;
             if (k + 1 < per) {
                 if (kGather) {
-                    xa = __ldg(x1 + p + kBandThreads);
-                    xb = __ldg(x2 + p + kBandThreads);
+                    xa = __ldg(x1 + p + TW);
+                    xb = __ldg(x2 + p + TW);
                 }
-                pre = epi.prefetch(p + kBandThreads);
+                pre = epi.prefetch(p + TW);
             }
         } else {
             if (kGather) {
                 const int b1 = tapRow(cellBase(__ldg(x1 + p), inv1, n1, w1));
                 const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
                 base = b1 * PW + b2;
-
             }
             cur = epi.prefetch(p);
             if (kGather && k == 0) pdlWait();
@@ -160,20 +195,19 @@ __global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eva
         sm[slot(col)] = o;
     }
     if constexpr (Epi::kGuard) {
-        __shared__ double red[kBandThreads / 32];
         for (int o = 16; o > 0; o >>= 1) guard = fmax(guard, __shfl_xor_sync(0xffffffffu, guard, o));
         if ((t & 31) == 0) red[t >> 5] = guard;
-        __syncthreads();
+        bar.sync();
         if (t == 0) {
             double m = red[0];
-            for (int w = 1; w < kBandThreads / 32; ++w) m = fmax(m, red[w]);
-            epi.guardPartials[blockIdx.x] = m;
+            for (int w = 1; w < TW / 32; ++w) m = fmax(m, red[w]);
+            epi.guardPartials[r] = m;
         }
     }
     // the next prefilter's input check (checkFinite(u, "prefilter"), interp.cpp:76)
-    if (__syncthreads_or(bad) && t == 0 && nonfinite) atomicOr(nonfinite, 1u);
+    if (bar.syncOr(bad) && t == 0 && nonfinite) atomicOr(nonfinite, 1u);
 
-    // ---- row pass of the prefilter (exact: the whole periodic row is in the block)
+    // ---- row pass of the prefilter (exact: the whole periodic row is in shared memory)
     double f[kL];
     double2* s2 = reinterpret_cast<double2*>(sm + t * kCS);
     if (t < nc) {
@@ -193,7 +227,7 @@ __global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eva
         F0[t] = f[0];
         P0[t] = b;
     }
-    __syncthreads();
+    bar.sync();
     if (t < nc) {
         const ZPow zp;
         const int c = t;
@@ -215,21 +249,124 @@ __global__ void __launch_bounds__(kBandThreads, BandMinBlocks<Epi>::value) k_eva
             s2[k / 2] = make_double2(o0, o1);
         }
     }
-    __syncthreads();
+    bar.sync();
     double* dst = rowOut + static_cast<std::size_t>(r) * n2;
     for (int k = 0; k < per; ++k) {
-        const int col = t + kBandThreads * k;
+        const int col = t + TW * k;
         dst[col] = sm[slot(col)];
     }
+}
+
+// Resident blocks per SM of the row-per-block kernel: the 256-thread count scaled to TW (same
+// register cap).
+template <class Epi, int TW>
+constexpr int bandMinBlocks() {
+    return BandMinBlocks<Epi>::value * (kBandThreads / TW);
+}
+
+template <class Epi, bool kGather, bool kWindow = false, int TW = kBandThreads>
+__global__ void __launch_bounds__(TW, (bandMinBlocks<Epi, TW>())) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
+                                                            const double* __restrict__ x2, int n1, int n2, Epi epi,
+                                                            double* __restrict__ rowOut, unsigned* nonfinite,
+                                                            BandWindow win = BandWindow{}) {
+    extern __shared__ __align__(16) double sm[];
+    bandRow<Epi, kGather, kWindow, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, win, blockIdx.x, threadIdx.x, sm,
+                                       BarBlock{});
     pdlTrigger();  // at the end: the dependent column pass must not take this kernel's slots
+}
+
+// Strip form (large grids): one block (one per SM: its register file) owns W consecutive rows,
+// one row worker of TW threads each (named barriers, no block-wide synchronisation), so the
+// rows an SM gathers at the same time are neighbours and share their coefficient rows in L1 —
+// with one block per row, consecutive rows land on different SMs and every SM fetches the 4
+// tap rows of each of its rows from L2 (tap traffic 4.3x the coefficient field).
+// Row workers per strip block: 7 x 128 threads (72 registers; ~7 rows per SM at 1024 rows on
+// 148 SMs, one round), one worker less where the epilogue carries more live state
+// (BandMinBlocks < 4).
+template <class Epi, int TW>
+constexpr int stripWorkers() {
+    return 7 - (BandMinBlocks<Epi>::value < 4 ? 1 : 0);
+}
+
+template <class Epi, bool kGather, int TW>
+__global__ void __launch_bounds__(TW* stripWorkers<Epi, TW>(), 1)
+    k_eval_strip(CoeffSet<1> cs, const double* __restrict__ x1, const double* __restrict__ x2, int n1, int n2, Epi epi,
+                 double* __restrict__ rowOut, unsigned* nonfinite) {
+    extern __shared__ __align__(16) double sm[];
+    constexpr int W = stripWorkers<Epi, TW>();
+    const int w = threadIdx.x / TW;
+    const int t = threadIdx.x - w * TW;
+    const int r = blockIdx.x * W + w;
+    if (r < n1)
+        bandRow<Epi, kGather, false, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, BandWindow{}, r, t,
+                                         sm + w * bandRowSmem(n2, TW), BarNamed<TW>{1 + w});
+    pdlTrigger();
+}
+
+// Row-to-SM mapping of the band step: 0 = by grid size (strip blocks when every SM gets >= 4
+// rows), 1 = one block per row, 2 = strip blocks.  Only the kernel benchmark
+// (vrg_hess_bench_kernel) sets it, to time both forms on the same operator.
+inline std::atomic<int> g_bandMapping{0};
+
+// Strip blocks where every SM gets >= 4 rows and a row's chunks fit 128 threads (n2 <= 2048).
+// Measured on B200 (tools/sl_step_probe.py, ids +100/+200): at 1024^2 the state / incremental-
+// state / adjoint band steps take 11.0 / 13.8 / 14.7 us as strips against 11.6 / 14.7 / 16.3 us
+// with one block per row; at 2048^2 5% faster except the incremental-state step (1% slower); at
+// 4096^2 (3 x 256-thread workers) 15-20% slower, so the row-per-block form stays there.
+inline bool stripPath(const Ctx& ctx, const GridDims& g) {
+    const bool fits = g.n2 % 128 == 0 && g.n2 / kL <= 128;
+    if (g_bandMapping) return g_bandMapping == 2 && fits;
+    return g.n1 >= 4 * ctx.numSMs && fits;
+}
+
+template <class Epi, bool kGather, int TW>
+void launchEvalStrip(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x1, const double* x2, const Epi& epi,
+                     double* rowOut, unsigned* nonfinite) {
+    constexpr int W = stripWorkers<Epi, TW>();
+    constexpr int kThreads = W * TW;
+    const std::size_t smem = sizeof(double) * W * bandRowSmem(g.n2, TW);
+    static std::mutex mu;
+    static bool attr[64] = {};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!attr[ctx.device]) {
+            VRG_CUDA(cudaFuncSetAttribute(k_eval_strip<Epi, kGather, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024));
+            attr[ctx.device] = true;
+        }
+    }
+    launchPdl(1, k_eval_strip<Epi, kGather, TW>, dim3((g.n1 + W - 1) / W), dim3(kThreads), smem, ctx.stream,
+              cs, x1, x2, g.n1, g.n2, epi, rowOut, nonfinite);
 }
 
 template <class Epi, bool kGather>
 void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x1, const double* x2, const Epi& epi,
                     double* rowOut, unsigned* nonfinite) {
     LaunchScope ls_(ctx, Epi::kName);
-    launchPdl(1, k_eval_band<Epi, kGather>, dim3(bandBlocks(g)), dim3(kBandThreads), bandSmem(g), ctx.stream, cs, x1,
-              x2, g.n1, g.n2, epi, rowOut, nonfinite, BandWindow{});
+    if (stripPath(ctx, g)) {
+        launchEvalStrip<Epi, kGather, 128>(ctx, g, cs, x1, x2, epi, rowOut, nonfinite);
+        return;
+    }
+    const std::size_t smem = bandSmem(g);
+    const dim3 grid(bandBlocks(g));
+    switch (bandTW(g.n2)) {
+        case 256:
+            launchPdl(1, k_eval_band<Epi, kGather, false, 256>, grid, dim3(256), smem, ctx.stream, cs, x1, x2, g.n1,
+                      g.n2, epi, rowOut, nonfinite, BandWindow{});
+            break;
+        case 128:
+            launchPdl(1, k_eval_band<Epi, kGather, false, 128>, grid, dim3(128), smem, ctx.stream, cs, x1, x2, g.n1,
+                      g.n2, epi, rowOut, nonfinite, BandWindow{});
+            break;
+        case 64:
+            launchPdl(1, k_eval_band<Epi, kGather, false, 64>, grid, dim3(64), smem, ctx.stream, cs, x1, x2, g.n1, g.n2,
+                      epi, rowOut, nonfinite, BandWindow{});
+            break;
+        default:
+            launchPdl(1, k_eval_band<Epi, kGather, false, 32>, grid, dim3(32), smem, ctx.stream, cs, x1, x2, g.n1, g.n2,
+                      epi, rowOut, nonfinite, BandWindow{});
+            break;
+    }
 }
 
 // Slab launch: L local rows (blocks) of a grid with n1 global rows, coefficients in a window.
@@ -238,6 +375,7 @@ void launchEvalBandWindow(Ctx& ctx, int n1, int L, int n2, CoeffSet<1> cs, const
                           const Epi& epi, double* rowOut, unsigned* nonfinite, BandWindow win) {
     LaunchScope ls_(ctx, Epi::kName);
     const GridDims gl(L, n2);
+    if (bandTW(n2) != kBandThreads) throw NotSupported("slab step: the row length must be a multiple of 256");
     launchPdl(1, k_eval_band<Epi, kGather, true>, dim3(L), dim3(kBandThreads), bandSmem(gl), ctx.stream, cs, x1, x2,
               n1, n2, epi, rowOut, nonfinite, win);
 }

@@ -343,14 +343,16 @@ __device__ __forceinline__ void pfSeg(const double* __restrict__ in, double* __r
     }
 }
 
+// blockIdx.z: field of a batch (input / output strides inZ / outZ doubles).
 template <bool kRows, bool kPadOut, int kR>
 __global__ void __launch_bounds__(kLines*(kR / kL + 4)) k_pf_seg(const double* __restrict__ in,
                                                                  double* __restrict__ out, int n1, int n2, int LS,
-                                                                 unsigned* nonfinite) {
+                                                                 unsigned* nonfinite, std::size_t inZ, std::size_t outZ) {
     extern __shared__ __align__(16) double sm[];
     pdlWait();  // the input is the predecessor's output
     pdlTrigger();
-    pfSeg<kRows, kPadOut, kR>(in, out, n1, n2, LS, nonfinite, blockIdx.x, blockIdx.y, threadIdx.x, sm, true);
+    pfSeg<kRows, kPadOut, kR>(in + blockIdx.z * inZ, out + blockIdx.z * outZ, n1, n2, LS, nonfinite, blockIdx.x,
+                              blockIdx.y, threadIdx.x, sm, true);
 }
 
 // Periodic padding of an unpadded field (for coefficient sets that arrive unpadded).
@@ -396,19 +398,21 @@ SegPlan segPlan(int n) {
 }
 
 template <bool kRows, bool kPad, int kR>
-void launchSeg(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite) {
+void launchSeg(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite,
+               int count, std::size_t inZ, std::size_t outZ) {
     const int n = kRows ? g.n2 : g.n1, lines = kRows ? g.n1 : g.n2;
-    launchPdl(2, k_pf_seg<kRows, kPad, kR>, dim3(n / kR, (lines + kLines - 1) / kLines), dim3(p.threads), p.smem,
-              ctx.stream, in, out, g.n1, g.n2, p.LS, nonfinite);
+    launchPdl(2, k_pf_seg<kRows, kPad, kR>, dim3(n / kR, (lines + kLines - 1) / kLines, count), dim3(p.threads),
+              p.smem, ctx.stream, in, out, g.n1, g.n2, p.LS, nonfinite, inZ, outZ);
 }
 
 template <bool kRows, bool kPad>
-void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite) {
+void launchSegR(Ctx& ctx, const GridDims& g, const SegPlan& p, const double* in, double* out, unsigned* nonfinite,
+                int count = 1, std::size_t inZ = 0, std::size_t outZ = 0) {
     switch (p.R) {
-        case 256: launchSeg<kRows, kPad, 256>(ctx, g, p, in, out, nonfinite); break;
-        case 128: launchSeg<kRows, kPad, 128>(ctx, g, p, in, out, nonfinite); break;
-        case 64: launchSeg<kRows, kPad, 64>(ctx, g, p, in, out, nonfinite); break;
-        default: launchSeg<kRows, kPad, 32>(ctx, g, p, in, out, nonfinite); break;
+        case 256: launchSeg<kRows, kPad, 256>(ctx, g, p, in, out, nonfinite, count, inZ, outZ); break;
+        case 128: launchSeg<kRows, kPad, 128>(ctx, g, p, in, out, nonfinite, count, inZ, outZ); break;
+        case 64: launchSeg<kRows, kPad, 64>(ctx, g, p, in, out, nonfinite, count, inZ, outZ); break;
+        default: launchSeg<kRows, kPad, 32>(ctx, g, p, in, out, nonfinite, count, inZ, outZ); break;
     }
 }
 
@@ -493,30 +497,34 @@ __device__ __forceinline__ void pfColsReg(const double* __restrict__ in, double*
 
 template <int kR>
 __global__ void __launch_bounds__(kColW*(kR / kL + 4)) k_pf_cols_reg(const double* __restrict__ in,
-                                                                     double* __restrict__ out, int n1, int n2) {
+                                                                     double* __restrict__ out, int n1, int n2,
+                                                                     std::size_t inZ, std::size_t outZ) {
     __shared__ ColsShared<kR> sh;
     pdlWait();  // the input is the predecessor's output
-    pfColsReg<kR>(in, out, n1, n2, blockIdx.x, blockIdx.y, threadIdx.x, sh);
+    pfColsReg<kR>(in + blockIdx.z * inZ, out + blockIdx.z * outZ, n1, n2, blockIdx.x, blockIdx.y, threadIdx.x, sh);
     pdlTrigger();  // at the end (common.cuh kPdlMask)
 }
 
 template <int kR>
-void launchColsReg(Ctx& ctx, const GridDims& g, const double* in, double* out) {
-    launchPdl(2, k_pf_cols_reg<kR>, dim3(g.n1 / kR, (g.n2 + kColW - 1) / kColW), dim3(kColW * (kR / kL + 4)), 0,
-              ctx.stream, in, out, g.n1, g.n2);
+void launchColsReg(Ctx& ctx, const GridDims& g, const double* in, double* out, int count, std::size_t inZ,
+                   std::size_t outZ) {
+    launchPdl(2, k_pf_cols_reg<kR>, dim3(g.n1 / kR, (g.n2 + kColW - 1) / kColW, count), dim3(kColW * (kR / kL + 4)),
+              0, ctx.stream, in, out, g.n1, g.n2, inZ, outZ);
 }
 
-// Column pass into the padded layout; false if n1 is not a multiple of 32.
-bool launchColumnPass(Ctx& ctx, const GridDims& g, const double* in, double* out) {
+// Column pass into the padded layout; false if n1 is not a multiple of 32.  `count` fields at
+// strides inZ / outZ doubles (one launch).
+bool launchColumnPass(Ctx& ctx, const GridDims& g, const double* in, double* out, int count = 1, std::size_t inZ = 0,
+                      std::size_t outZ = 0) {
     SegPlan pc = segPlan(g.n1);
     if (!pc.ok) return false;
     {
         LaunchScope ls_(ctx, "k_prefilter_cols");
         switch (pc.R) {
-            case 256: launchColsReg<256>(ctx, g, in, out); break;
-            case 128: launchColsReg<128>(ctx, g, in, out); break;
-            case 64: launchColsReg<64>(ctx, g, in, out); break;
-            default: launchColsReg<32>(ctx, g, in, out); break;
+            case 256: launchColsReg<256>(ctx, g, in, out, count, inZ, outZ); break;
+            case 128: launchColsReg<128>(ctx, g, in, out, count, inZ, outZ); break;
+            case 64: launchColsReg<64>(ctx, g, in, out, count, inZ, outZ); break;
+            default: launchColsReg<32>(ctx, g, in, out, count, inZ, outZ); break;
         }
     }
     VRG_LAUNCH_CHECK();
@@ -588,6 +596,22 @@ void launchSlabCols(Ctx& ctx, int winRows, int n2, const double* inHalo, double*
     LaunchScope ls_(ctx, "k_slab_cols");
     launchPdl(2, k_slab_cols, dim3((winRows / kL + 15) / 16, (n2 + kColW - 1) / kColW), dim3(kColW * 20), 0,
               ctx.stream, inHalo, window, winRows, n2);
+}
+
+void launchPrefilterBatch(Ctx& ctx, const GridDims& g, const double* u, std::size_t uStride, int count, double* c,
+                          std::size_t cStride, double* tmp, unsigned* nonfinite) {
+    if (count <= 0) return;
+    const SegPlan pr = segPlan(g.n2), pc = segPlan(g.n1);
+    if (!(pr.ok && pc.ok) || uStride < g.points() || cStride < paddedPoints(g.n1, g.n2)) {
+        for (int k = 0; k < count; ++k) launchPrefilter(ctx, g, u + k * uStride, c + k * cStride, tmp, nonfinite);
+        return;
+    }
+    {
+        LaunchScope ls_(ctx, "k_prefilter_rows");
+        launchSegR<true, false>(ctx, g, pr, u, tmp, nonfinite, count, uStride, g.points());
+    }
+    VRG_LAUNCH_CHECK();
+    launchColumnPass(ctx, g, tmp, c, count, g.points(), cStride);
 }
 
 void launchPrefilterRows(Ctx& ctx, const GridDims& g, const double* u, double* rowFiltered, unsigned* nonfinite) {

@@ -39,6 +39,11 @@ __device__ __forceinline__ int slot(int p) { return p + 2 * (p >> 4); }
 // doubles (see cellBase).  `tmp` holds 2*n1*n2 doubles.  If `nonfinite` is non-null, a
 // non-finite input value sets *nonfinite = 1 (checkFinite(u, "prefilter"), interp.cpp:76).
 void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, double* tmp, unsigned* nonfinite);
+// `count` fields u + k*uStride -> padded coefficients c + k*cStride in two launches (rows, then
+// columns, blockIdx.z = field); tmp holds count*n1*n2 doubles.  Grids off the segment path
+// loop over launchPrefilter (tmp then needs 2*n1*n2).
+void launchPrefilterBatch(Ctx& ctx, const GridDims& g, const double* u, std::size_t uStride, int count, double* c,
+                          std::size_t cStride, double* tmp, unsigned* nonfinite);
 // Column pass only (input already row-filtered, e.g. by a fused band kernel, evalband.cuh).
 bool colPassFusable(const GridDims& g);
 void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c);

@@ -174,18 +174,28 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
         VRG_CUDA(cudaMemcpyAsync(G_.d(), gradTraj, sizeof(double) * (nt + 1) * 2 * N, cudaMemcpyDeviceToDevice,
                                  ctx.stream));
     } else {
-        for (int j = 0; j <= nt; ++j)
-            gradient(ctx, g, state_.d() + j * N, G_.d() + j * 2 * N, G_.d() + j * 2 * N + N);
+        gradientBatch(ctx, g, state_.d(), nt + 1, G_.d());  // one batched transform chain per chunk
     }
     const double* Xf = solver.departure(kForward);
-    work_.alloc(sizeof(double) * (11 * N + paddedPoints(g.n1, g.n2)));
-    double* c2 = work_.d() + 11 * N;
-    for (int j = 1; j <= nt; ++j) {
-        const double* gp = G_.d() + (j - 1) * 2 * N;
-        launchPrefilter(ctx, g, gp, solver.coef(), solver.tmp(), nullptr);
-        launchPrefilter(ctx, g, gp + N, c2, solver.tmp(), nullptr);
-        double* gd = GD_.d() + (j - 1) * 2 * N;
-        launchEvaluate<2>(ctx, g, CoeffSet<2>{{solver.coef(), c2}}, Xf, Xf + N, EpiStore2{nullptr, gd, gd + N});
+    work_.alloc(sizeof(double) * (11 * N + 2 * paddedPoints(g.n1, g.n2)));  // + vt coefficients (2 padded)
+    // GD_j = (grad m_{j-1})_D, j = 1..nt: the 2nt gradient components prefiltered in one batch
+    // (two launches) and evaluated at the forward departure points in one launch per chunk
+    {
+        const std::size_t P = paddedPoints(g.n1, g.n2);
+        const int total = nt;  // gradient fields G_0 .. G_{nt-1}, two components each
+        const std::size_t perField = sizeof(double) * (2 * P + 2 * N);
+        const int chunk = static_cast<int>(std::max<std::size_t>(
+            1, std::min<std::size_t>(total, (std::size_t(256) << 20) / perField)));
+        double* coefs = ctx.scratchBuf(45, sizeof(double) * 2 * chunk * P);
+        double* rows = ctx.scratchBuf(46, sizeof(double) * std::max<std::size_t>(2 * chunk * N, 2 * N));
+        for (int j0 = 0; j0 < total; j0 += chunk) {
+            const int c = std::min(chunk, total - j0);
+            launchPrefilterBatch(ctx, g, G_.d() + static_cast<std::size_t>(j0) * 2 * N, N, 2 * c, coefs, P, rows,
+                                 nullptr);
+            double* gd = GD_.d() + static_cast<std::size_t>(j0) * 2 * N;
+            launchEvaluateBatch<2>(ctx, g, CoeffSet<2>{{coefs, coefs + P}}, 2 * P, c, Xf, Xf + N,
+                                   EpiStore2{nullptr, gd, gd + N}, 2 * N);
+        }
     }
     solver.departure(kBackward);
     solver.divVelocityAtDeparture(kBackward);
@@ -219,10 +229,10 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
     // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
     // 1024^2 on B200 (0.815 vs 0.867 ms).  The plain step is the generic-grid path.
-    fused_ = bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g);
+    fused_ = bandFusable(g) && colPassFusable(g);
     lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
-    adjLog_.ensure(nt + 1, evalBlocks(g));
+    adjLog_.ensure(nt + 1, guardBlocks(g));
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
     // every plan a matvec uses exists before any graph capture (plan creation allocates)
@@ -273,7 +283,7 @@ void Hessian::initHeun(const double* mR, const double* mT, const double* stateTr
     useGraphs = false;
     lazyInterps_ = 0;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
-    adjLog_.ensure(nt + 1, evalBlocks(g));
+    adjLog_.ensure(nt + 1, guardBlocks(g));
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
     ctx.sync();
@@ -373,7 +383,6 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     double* vtD = work_.d();
     double* mt[2] = {vtD + 2 * N, vtD + 3 * N};
     double* lam[2] = {vtD + 4 * N, vtD + 5 * N};
-    double* c2 = vtD + 11 * N;  // padded coefficients of the second component
     const double* Xf = solver.departure(kForward);
     const double* Xb = solver.departure(kBackward);
     const double* dv = solver.divVelocity();
@@ -383,10 +392,19 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     auto G = [&](int j) { return G_.d() + static_cast<std::size_t>(j) * 2 * N; };
     auto GD = [&](int j) { return GD_.d() + static_cast<std::size_t>(j - 1) * 2 * N; };  // j = 1..nt
 
-    // incremental state (solveIncState SL, transport.cpp:322-342)
-    launchPrefilter(ctx, g, vt1, coef, tmp, nullptr);
-    launchPrefilter(ctx, g, vt2, c2, tmp, nullptr);
-    launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
+    // incremental state (solveIncState SL, transport.cpp:322-342); vt's two components are
+    // prefiltered in one batch (two launches) when contiguous
+    {
+        const std::size_t P = paddedPoints(g.n1, g.n2);
+        double* cv = vtD + 11 * N;
+        if (vt2 == vt1 + N) {
+            launchPrefilterBatch(ctx, g, vt1, N, 2, cv, P, tmp, nullptr);
+        } else {
+            launchPrefilter(ctx, g, vt1, cv, tmp, nullptr);
+            launchPrefilter(ctx, g, vt2, cv + P, tmp, nullptr);
+        }
+        launchEvaluate<2>(ctx, g, CoeffSet<2>{{cv, cv + P}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
+    }
     auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
     if (fused_) {
         // Band path: every step's gather kernel also row-filters its output (evalband.cuh), so
@@ -546,7 +564,8 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
     static const int kNeed[] = {1, 8, 8, 10, 10, 6, 10, 1};
     if (kind < 0 || kind > 7) throw InvalidArgument("slab step: unknown kind");
     if (nops < kNeed[kind]) throw InvalidArgument("slab step: too few operand fields");
-    if (!bandFusable(GridDims(L, n2)) || L < 1 || n1 < L) throw NotSupported("slab step: unsupported row length");
+    if (!bandFusable(GridDims(L, n2)) || n2 % kBandThreads != 0 || L < 1 || n1 < L)
+        throw NotSupported("slab step: unsupported row length");
     const BandWindow win{winBase, winRows, winErr};
     const CoeffSet<1> cs{{coef}};
     auto inc = [&] {
@@ -648,6 +667,18 @@ void Hessian::checkLastGuard() {
 // between two events on the context stream, with the operands of a mid-trajectory step
 // (steady state after a matvec has run, so the operands are the ones the matvec produced).
 double Hessian::benchKernel(int id, int iters) {
+    // id + 100: band steps with strip blocks, id + 200: one block per row (evalband.cuh)
+    struct MappingScope {
+        int old = g_bandMapping.load();
+        ~MappingScope() { g_bandMapping = old; }
+    } mappingScope_;
+    if (id >= 200) {
+        g_bandMapping = 1;
+        id -= 200;
+    } else if (id >= 100) {
+        g_bandMapping = 2;
+        id -= 100;
+    }
     const std::size_t N = g.points();
     const double ht = solver.ht;
     const int j = std::max(2, nt / 2);
@@ -954,31 +985,47 @@ void Hessian::launchSplit(const double* s1, const double* s2, double* o1, double
 // ------------------------------------------------------------------------------ gradient / objective
 namespace {
 
-__global__ void k_bf_accum(std::size_t N, double w, const double* __restrict__ lam, const double* __restrict__ g1,
-                           const double* __restrict__ g2, double* b1, double* b2) {
+// The trapezoid sum over a chunk of frames j0 .. j0+c-1 in one launch, accumulated in the
+// order of the per-frame loop (same expression per frame as k_bf_accum, bit-identical).
+__global__ void k_bf_accum_frames(std::size_t N, int j0, int c, int nt, double ht, const double* __restrict__ lam,
+                                  const double* __restrict__ G, double* b1, double* b2, int first) {
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= N) return;
-    b1[p] += w * (lam[p] * g1[p]);
-    b2[p] += w * (lam[p] * g2[p]);
+    double a1 = first ? 0.0 : b1[p], a2 = first ? 0.0 : b2[p];
+    for (int k = 0; k < c; ++k) {
+        const int j = j0 + k;
+        const double w = ht * ((j == 0 || j == nt) ? 0.5 : 1.0);
+        const double l = lam[static_cast<std::size_t>(j) * N + p];
+        const double* g = G + static_cast<std::size_t>(k) * 2 * N;
+        a1 += w * (l * g[p]);
+        a2 += w * (l * g[N + p]);
+    }
+    b1[p] = a1;
+    b2[p] = a2;
 }
 
 }  // namespace
 
-// assembleBodyForce SL (src/inverse.cpp:58-64): b = sum_j w_j lam_j grad m_j.
+// assembleBodyForce SL (src/inverse.cpp:58-64): b = sum_j w_j lam_j grad m_j, the gradients of
+// the state frames by batched transforms (gradientBatch) and the sum in one launch per chunk.
 void bodyForce(Ctx& ctx, const GridDims& g, int nt, const double* stateTraj, const double* adjTraj, double* b1,
                double* b2, double* gradTrajOut) {
     const std::size_t N = g.points();
     const double ht = 1.0 / nt;
-    double* scratch = gradTrajOut ? nullptr : ctx.scratchBuf(20, sizeof(double) * 2 * N);
-    fill(ctx, N, 0.0, b1);
-    fill(ctx, N, 0.0, b2);
-    for (int j = 0; j <= nt; ++j) {
-        const double w = ht * ((j == 0 || j == nt) ? 0.5 : 1.0);
-        double* gm = gradTrajOut ? gradTrajOut + static_cast<std::size_t>(j) * 2 * N : scratch;
-        gradient(ctx, g, stateTraj + j * N, gm, gm + N);
+    const int frames = nt + 1;
+    // without an output trajectory the gradients go through a scratch of one chunk
+    const int chunk = gradTrajOut ? frames
+                                  : static_cast<int>(std::max<std::size_t>(
+                                        1, std::min<std::size_t>(frames, (std::size_t(256) << 20) / (16 * N))));
+    double* scratch = gradTrajOut ? nullptr : ctx.scratchBuf(20, sizeof(double) * 2 * N * chunk);
+    for (int j0 = 0; j0 < frames; j0 += chunk) {
+        const int c = std::min(chunk, frames - j0);
+        double* gm = gradTrajOut ? gradTrajOut + static_cast<std::size_t>(j0) * 2 * N : scratch;
+        gradientBatch(ctx, g, stateTraj + static_cast<std::size_t>(j0) * N, c, gm);
         {
             LaunchScope ls_(ctx, "k_bf_accum");
-            k_bf_accum<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, w, adjTraj + j * N, gm, gm + N, b1, b2);
+            k_bf_accum_frames<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, j0, c, nt, ht, adjTraj, gm, b1, b2,
+                                                                      j0 == 0 ? 1 : 0);
         }
         VRG_LAUNCH_CHECK();
     }

@@ -293,12 +293,45 @@ CoarseOperator::CoarseOperator(Ctx& c, const GridDims& fg, const double* v, cons
 }
 
 // ------------------------------------------------------------------------------ Chebyshev / PCG
+namespace {
+// The vector updates of chebyshevSolve fused per iteration, with the rounding of the separate
+// BLAS kernels they replace (k_lincomb: fma(x, a, b*y); k_axpby with b = 1: fma(x, a, y)), so
+// the iterates are bit-identical:
+//   init:  r = rhs, d = (1/theta) r + 0 r, x = 0 + d
+//   step:  r -= A d, d = c1 d + c2 r, x += d   (the last iteration's r -= A d is dead)
+__global__ void k_cheb_init(std::size_t n, const double* __restrict__ rhs, double* __restrict__ r,
+                            double* __restrict__ d, double* __restrict__ x, double invTheta) {
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double ri = rhs[i];
+        r[i] = ri;
+        const double di = __fma_rn(ri, invTheta, __dmul_rn(ri, 0.0));
+        d[i] = di;
+        x[i] = __fma_rn(di, 1.0, 0.0);
+    }
+}
+
+__global__ void k_cheb_step(std::size_t n, const double* __restrict__ ad, double* __restrict__ r,
+                            double* __restrict__ d, double* __restrict__ x, double c1, double c2) {
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double ri = __fma_rn(ad[i], -1.0, r[i]);
+        r[i] = ri;
+        const double di = __fma_rn(d[i], c1, __dmul_rn(ri, c2));
+        d[i] = di;
+        x[i] = __fma_rn(di, 1.0, x[i]);
+    }
+}
+}  // namespace
+
 void chebyshevSolve(Ctx& ctx, const GridDims& g, const LinOpDev& op, const double* rhs, int k, double eMin,
                     double eMax, double* x) {
     if (!(eMax > eMin) || !(eMin > 0.0)) throw InvalidArgument("chebyshevSolve: need eMax > eMin > 0");
     const std::size_t n = 2 * g.points();
-    fill(ctx, n, 0.0, x);
-    if (k <= 0) return;
+    if (k <= 0) {
+        fill(ctx, n, 0.0, x);
+        return;
+    }
     const double theta = 0.5 * (eMax + eMin);
     const double delta = 0.5 * (eMax - eMin);
     const double sigma = theta / delta;
@@ -306,17 +339,22 @@ void chebyshevSolve(Ctx& ctx, const GridDims& g, const LinOpDev& op, const doubl
     double* r = ctx.scratchBuf(120, sizeof(double) * n);
     double* d = ctx.scratchBuf(121, sizeof(double) * n);
     double* ad = ctx.scratchBuf(122, sizeof(double) * n);
-    copy(ctx, n, rhs, r);
-    lincomb(ctx, n, 1.0 / theta, r, 0.0, r, d);
+    {
+        LaunchScope ls_(ctx, "k_cheb_init");
+        k_cheb_init<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, rhs, r, d, x, 1.0 / theta);
+    }
+    VRG_LAUNCH_CHECK();
     for (int it = 1; it <= k; ++it) {
-        if (it > 1) {
-            const double rhoNew = 1.0 / (2.0 * sigma - rho);
-            lincomb(ctx, n, rhoNew * rho, d, 2.0 * rhoNew / delta, r, d);
-            rho = rhoNew;
-        }
-        axpby(ctx, n, 1.0, d, 1.0, x);
         op(d, ad);
-        axpby(ctx, n, -1.0, ad, 1.0, r);
+        if (it == k) break;
+        const double rhoNew = 1.0 / (2.0 * sigma - rho);
+        const double c1 = rhoNew * rho, c2 = 2.0 * rhoNew / delta;
+        rho = rhoNew;
+        {
+            LaunchScope ls_(ctx, "k_cheb_step");
+            k_cheb_step<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, ad, r, d, x, c1, c2);
+        }
+        VRG_LAUNCH_CHECK();
     }
 }
 

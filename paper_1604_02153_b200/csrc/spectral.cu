@@ -1,4 +1,5 @@
 // K7 implementation: cuFFT plans from the context cache + symbol kernels.
+#include <algorithm>
 #include <cmath>
 
 #include "blas.cuh"
@@ -28,6 +29,20 @@ __global__ void k_grad(const cplx* __restrict__ s, cplx* __restrict__ o1, cplx* 
     const cplx v = s[i];
     o1[i] = cscale(cmulI(waveNyq0(r, n1), v), scale);
     o2[i] = cscale(cmulI(waveNyq0(c, n2), v), scale);
+}
+
+// k_grad over a batch of spectra (blockIdx.y = field): field f's gradient spectra at
+// o + 2f*NS (axis 0) and o + (2f+1)*NS (axis 1), the [g1 | g2] layout of a gradient trajectory.
+__global__ void k_grad_batch(const cplx* __restrict__ s, cplx* __restrict__ o, int n1, int n2, double scale) {
+    const int nc = n2 / 2 + 1;
+    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const std::size_t f = blockIdx.y;
+    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const cplx v = s[f * n + i];
+    o[2 * f * n + i] = cscale(cmulI(waveNyq0(r, n1), v), scale);
+    o[(2 * f + 1) * n + i] = cscale(cmulI(waveNyq0(c, n2), v), scale);
 }
 
 __global__ void k_div(const cplx* __restrict__ s1, const cplx* __restrict__ s2, cplx* __restrict__ o, int n1, int n2,
@@ -265,6 +280,33 @@ void gradient(Ctx& ctx, const GridDims& g, const double* u, double* g1, double* 
     VRG_LAUNCH_CHECK();
     fftInverse2(ctx, g, o, g1, g2);
     ctx.ffts += 3;
+}
+
+int gradientChunk(const GridDims& g, int count) {
+    // spectra of the chunk (3 per field) within 256 MiB of scratch
+    const std::size_t perField = 3 * sizeof(cplx) * g.specPoints();
+    const std::size_t cap = std::size_t(256) << 20;
+    return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(count, cap / perField)));
+}
+
+void gradientBatch(Ctx& ctx, const GridDims& g, const double* u, int count, double* G) {
+    const std::size_t N = g.points(), NS = g.specPoints();
+    const int chunk = gradientChunk(g, count);
+    cplx* s = specScratch(ctx, g, 7, chunk);
+    cplx* o = specScratch(ctx, g, 8, 2 * chunk);
+    for (int f0 = 0; f0 < count; f0 += chunk) {
+        const int c = std::min(chunk, count - f0);
+        fftForward(ctx, g, u + f0 * N, s, c);
+        {
+            LaunchScope ls_(ctx, "k_grad");
+            const dim3 grid(specGrid(g).x, c);
+            k_grad_batch<<<grid, kSpecBlock, 0, ctx.stream>>>(s, o, g.n1, g.n2, 1.0 / N);
+        }
+        VRG_LAUNCH_CHECK();
+        fftInverse(ctx, g, o, G + 2 * f0 * N, 2 * c);
+    }
+    ctx.ffts += 3LL * count;
+    (void)NS;
 }
 
 void divergence(Ctx& ctx, const GridDims& g, const double* v1, const double* v2, double* out) {

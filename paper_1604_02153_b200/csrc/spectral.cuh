@@ -41,6 +41,11 @@ void fftInverse(Ctx& ctx, const GridDims& g, cplx* s, double* u, int batch);    
 
 // Field-level operators (device pointers, stream-ordered on ctx.stream).
 void gradient(Ctx& ctx, const GridDims& g, const double* u, double* g1, double* g2);
+// Gradients of `count` contiguous fields u_f -> G + 2f*N = [d1 u_f | d2 u_f] with batched
+// transforms (one D2Z, one symbol launch, one Z2D per chunk of gradientChunk fields); same
+// arithmetic per field as gradient().
+void gradientBatch(Ctx& ctx, const GridDims& g, const double* u, int count, double* G);
+int gradientChunk(const GridDims& g, int count);
 // applyHelmholtz (spectral.cpp:214-223): (1 - Lap) u with Nyquist-zeroed waves; 2 FFTs
 void applyHelmholtz(Ctx& ctx, const GridDims& g, const double* u, double* out);
 // near-incompressible penalty (inverse.cpp:17-28): -betaW grad((1 - Lap) div v) (8 FFTs) and

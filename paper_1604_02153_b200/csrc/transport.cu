@@ -159,13 +159,13 @@ Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2,
     if (anyNonFinite(ctx, 2 * g.points(), v.d())) throw InvalidArgument("transport velocity: non-finite value");
     coef_.alloc(sizeof(double) * paddedPoints(g.n1, g.n2));
     tmp_.alloc(sizeof(double) * 2 * g.points());
-    log.ensure(nt + 1, evalBlocks(g));
+    log.ensure(nt + 1, guardBlocks(g));
 }
 
 // Band path for the SL time loops (evalband.cuh) wherever the grid allows it: each step is the
 // gather + epilogue + the next prefilter's row pass in one kernel, then the column pass; same
 // arithmetic as prefilter + evaluate (the plain 3-kernel step, the generic-grid path).
-bool Solver::bandPath() const { return bandFusable(g) && colPassFusable(g) && bandBlocks(g) <= evalBlocks(g); }
+bool Solver::bandPath() const { return bandFusable(g) && colPassFusable(g); }
 
 double* Solver::coef() { return coef_.d(); }
 double* Solver::tmp() { return tmp_.d(); }

@@ -308,8 +308,16 @@ def apply_floor(n, p, beta, vmax, outmax):
     return 4 * 2.2e-16 * beta * kmax2 ** p * vmax / outmax
 
 
+def expect_band(n1, n2):
+    """evalband.cuh bandFusable + colPassFusable: rows of 32..4096 samples in 256/128/64/32-thread
+    blocks (one thread per 16-sample chunk), columns a multiple of 32."""
+    tw = next((t for t in (256, 128, 64, 32) if n2 % t == 0), 0)
+    return bool(tw) and n2 >= 32 and n2 // 16 <= tw and n1 >= 32 and n1 % 32 == 0
+
+
 @pytest.mark.parametrize("n1,n2,nt", [(256, 256, 1), (256, 512, 3), (512, 256, 8), (1024, 1024, 4), (768, 768, 2),
-                                      (96, 1280, 3), (160, 256, 2), (48, 40, 3)])
+                                      (96, 1280, 3), (160, 256, 2), (48, 40, 3), (64, 64, 4), (128, 96, 3),
+                                      (32, 192, 2), (128, 128, 5)])
 def test_band_path_vs_reference_under_replay(ctx, api, ref, n1, n2, nt):
     """The time loops run the fused band step (gather + epilogue + next row pass,
     evalband.cuh) wherever the grid allows it and the plain 3-kernel step elsewhere (48 x 40
@@ -322,7 +330,7 @@ def test_band_path_vs_reference_under_replay(ctx, api, ref, n1, n2, nt):
     vt1, vt2 = synth.smooth_velocity(n1, n2, 3000)
     F = ctx.field
     H = api.HessianOperator(ctx, (F(0.5 * v1), F(0.5 * v2)), F(mT), F(mT), 2, 1e-3, 0, nt)
-    assert H.band_path == (n2 % 256 == 0), H.band_path
+    assert H.band_path == expect_band(n1, n2), H.band_path
     out = []
     for _ in range(2):  # first call captures the graph, second replays it
         d = H.apply_data_term((F(vt1), F(vt2)))
@@ -337,6 +345,37 @@ def test_band_path_vs_reference_under_replay(ctx, api, ref, n1, n2, nt):
     assert rel(out[0][0], d1) < TOL and rel(out[0][1], d2) < TOL
     tol = max(TOL, apply_floor(max(n1, n2), 2, 1e-3, max(np.abs(vt1).max(), np.abs(vt2).max()), np.abs(e1).max()))
     assert rel(out[0][2], e1) < tol and rel(out[0][3], e2) < tol
+
+
+@pytest.mark.parametrize("n1,n2,nt", [(1024, 1024, 4), (640, 512, 3), (2048, 256, 2)])
+def test_strip_blocks_bit_identical_to_row_blocks(ctx, api, n1, n2, nt):
+    """The band steps of large grids run as strip blocks (W consecutive rows per block, one row
+    worker each, evalband.cuh k_eval_strip) instead of one block per row; the per-row arithmetic
+    is the same code, so state/adjoint solves, the data term and the full matvec are bit-identical
+    between the two mappings (vrg_band_mapping forces one or the other)."""
+    mT = synth.smoothed_noise(n1, n2, 1000)
+    v1, v2 = synth.smooth_velocity(n1, n2, 2000)
+    vt1, vt2 = synth.smooth_velocity(n1, n2, 3000)
+    F = ctx.field
+    res = {}
+    try:
+        for mode in (1, 2):
+            ctx.lib.vrg_band_mapping(mode)
+            S = api.Solver(ctx, (F(v1), F(v2)), nt)
+            st = S.solve_state(F(mT)).cpu().numpy()
+            ad = S.solve_adjoint(F(mT)).cpu().numpy()
+            H = api.HessianOperator(ctx, (F(0.5 * v1), F(0.5 * v2)), F(mT), F(mT), 2, 1e-3, 0, nt)
+            out = []
+            for _ in range(2):  # direct launch, then graph capture / replay
+                d = H.apply_data_term((F(vt1), F(vt2)))
+                a = H.apply((F(vt1), F(vt2)))
+                out.append([t.cpu().numpy() for t in (*d, *a)])
+            del H, S
+            res[mode] = [st, ad, *out[0], *out[1]]
+    finally:
+        ctx.lib.vrg_band_mapping(0)
+    for x, y in zip(res[1], res[2]):
+        assert np.array_equal(x, y)
 
 
 @pytest.mark.parametrize("n,nt,deform", [(48, 4, 0), (64, 4, 1), (128, 8, 0)])
@@ -435,7 +474,8 @@ def test_hessian_irregular_grids_vs_reference(ctx, api, ref, n1, n2, nt, deform)
     """GN matvec on rectangular grids off the fast paths, against the compiled reference:
     axes that are not multiples of 16 (generic prefilter), n2 beyond the band kernels' 4096
     (plain 3-kernel step), a band-path grid with 5 nodes per thread, and the 8192 limits of
-    the row and column prefilters; compressible and incompressible."""
+    the row and column prefilters (8192 x 128: strip blocks of 128-thread rows); compressible
+    and incompressible."""
     mT = synth.smoothed_noise(n1, n2, 1000)
     v1, v2 = synth.smooth_velocity(n1, n2, 2000)
     vt1, vt2 = synth.smooth_velocity(n1, n2, 3000)
@@ -444,7 +484,7 @@ def test_hessian_irregular_grids_vs_reference(ctx, api, ref, n1, n2, nt, deform)
     e1, e2 = ref.Hessian(w1, w2, mR, mT, 2, 1e-3, deform, nt).apply(vt1, vt2)
     H = api.HessianOperator(ctx, (ctx.field(w1), ctx.field(w2)), ctx.field(mR), ctx.field(mT), api.H2SEMI, 1e-3,
                             deform, nt)
-    assert H.band_path == (n2 % 256 == 0 and 256 <= n2 <= 4096 and n1 % 32 == 0)
+    assert H.band_path == expect_band(n1, n2)
     # The data term (transport solves + body force, the hot path) to the north-star bar.  The
     # full matvec adds beta A vt, which amplifies FFT rounding (~eps |vt|) by beta |k|^4 at the
     # highest modes: 2.8e11 at n2 = 8192.  Two correct implementations with different FFTs
