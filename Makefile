@@ -7,7 +7,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall 
 PKG       := paper_1604_02153_b200
 SRC       := $(PKG)/csrc
 BUILD     := $(PKG)/build
-CU        := runtime interp spectral transport heun inverse precond cabi
+CU        := runtime interp spectral transport heun inverse precond batch cabi
 OBJS      := $(addprefix $(BUILD)/,$(addsuffix .o,$(CU)))
 HDRS      := $(wildcard $(SRC)/*.cuh) include/vrg.h
 

@@ -194,6 +194,12 @@ int vrg_hess_create(vrg_ctx_t ctx, int n1, int n2, const double* v1, const doubl
 int vrg_hess_create_ex(vrg_ctx_t ctx, int n1, int n2, const double* v1, const double* v2, const double* mR,
                        const double* mT, const vrg_model* model, int scheme, int nt, int mode,
                        const double* state_traj, const double* adjoint_traj, vrg_hess_t* out);
+/* A Gauss-Newton SL HessianOperator of `pairs` stacked image pairs (batch fields: pair after pair,
+ * v1 / v2 / mR / mT each pairs x n1 x n2 device doubles); apply / apply_data / apply_split then
+ * take and return batch fields, each pair's result equal to its own operator's. */
+int vrg_hess_create_batch(vrg_ctx_t ctx, int n1, int n2, int pairs, const double* v1, const double* v2,
+                          const double* mR, const double* mT, int norm, double beta, int deformation, int nt,
+                          vrg_hess_t* out);
 void vrg_hess_destroy(vrg_hess_t h);
 int vrg_hess_apply(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);      /* apply */
 int vrg_hess_apply_data(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2); /* applyDataTerm */
@@ -315,6 +321,19 @@ int vrg_newton_solve(vrg_ctx_t ctx, int n1, int n2, const double* mR_host, const
                      double beta, int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,
                      const double* pc_dbl, double* v1_host, double* v2_host, double* records, int records_cap,
                      double* summary);
+
+/* inverse::newtonSolve for `pairs` independent image pairs at once (configs 3 and 5b: batches of
+ * pairs on one GPU): the pairs' transport, spectral and Krylov steps run in the same kernel
+ * launches (stacked fields, one scalar state per pair), each pair taking the decisions of its own
+ * newtonSolve.  mR/mT/v1/v2: pairs x n1 x n2 doubles (pair after pair); cfg/pc as for
+ * vrg_newton_solve (Gauss-Newton SL with cfg_int[2] = ntOverride > 0; Reg or two-level Chebyshev);
+ * records: pairs x records_cap x 12, summary: pairs x 7, pair_status: per pair 0 or the status
+ * of the error that pair's solve raised (message on stderr).  n1 * n2 a multiple of 256,
+ * 1 <= pairs <= 64. */
+int vrg_newton_solve_batch(vrg_ctx_t ctx, int n1, int n2, int pairs, const double* mR_host, const double* mT_host,
+                           int norm, double beta, int deformation, const int* cfg_int, const double* cfg_dbl,
+                           const int* pc_int, const double* pc_dbl, double* v1_host, double* v2_host, double* records,
+                           int records_cap, double* summary, int* pair_status);
 
 /* newtonSolve with the whole NewtonConfig (hessScheme included) and PrecondChoice per call;
  * records / summary as for vrg_newton_solve */

@@ -70,6 +70,7 @@ _SIG = {
     "vrg_hess_create": ("piippppidiiipp", C.c_int),
     "vrg_hess_create_ex": ("piipppppiiippp", C.c_int),
     "vrg_hess_destroy": ("p", None),
+    "vrg_hess_create_batch": ("piiippppidiip", C.c_int),
     "vrg_hess_apply": ("ppppp", C.c_int),
     "vrg_hess_apply_data": ("ppppp", C.c_int),
     "vrg_hess_apply_split": ("ppppp", C.c_int),
@@ -79,6 +80,7 @@ _SIG = {
     "vrg_hess_bench_kernel": ("piip", C.c_int),
     "vrg_hess_band_path": ("pp", C.c_int),
     "vrg_band_mapping": ("i", C.c_int),
+    "vrg_newton_solve_batch": ("piiippidipppppppipp", C.c_int),
     "vrg_hess_buffers": ("pp", C.c_int),
     "vrg_prefilter_rows": ("piippp", C.c_int),
     "vrg_slab_cols": ("piipp", C.c_int),

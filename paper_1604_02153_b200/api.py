@@ -508,6 +508,42 @@ class ExternalOps(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in EXTERNAL_OPS_FIELDS] + [("user", C.c_void_p)]
 
 
+def newton_solve_batch(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=16,
+                       ls_max_steps=20, tol_rel=1e-2, tol_abs=1e-5, forcing_cap=0.5, ls_c1=1e-4, ls_shrink=0.5,
+                       grad_cfl=1.0, kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10, eps_scale=0.1,
+                       eig=None):
+    """newtonSolve of P independent image pairs in lockstep (C ABI vrg_newton_solve_batch): mR, mT
+    are (P, n1, n2) host arrays; returns one (v1, v2, records, summary) per pair, each identical to
+    that pair's own newton_solve.  A pair whose solve raised gets summary['error'] = the status
+    code (the message goes to stderr); the others are unaffected."""
+    import numpy as np
+
+    mR = np.ascontiguousarray(mR, dtype=np.float64)
+    mT = np.ascontiguousarray(mT, dtype=np.float64)
+    P, n1, n2 = mR.shape
+    ci = (C.c_int * 5)(max_outer, max_inner, nt, ls_max_steps, GAUSS_NEWTON)
+    cd = (C.c_double * 6)(tol_rel, tol_abs, forcing_cap, ls_c1, ls_shrink, grad_cfl)
+    pi, pd = _pc_arrays(kind, coarse_solver, cheb_iters, eps_scale, eig)
+    v1, v2 = np.empty_like(mR), np.empty_like(mR)
+    rec = np.zeros((P, max_outer + 1, 12))
+    summ = np.zeros((P, 7))
+    st = np.zeros(P, dtype=np.int32)
+    hp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    ctx.check(ctx.lib.vrg_newton_solve_batch(ctx.h, n1, n2, P, hp(mR), hp(mT), norm, beta, deformation,
+                                             C.cast(ci, C.c_void_p), C.cast(cd, C.c_void_p), C.cast(pi, C.c_void_p),
+                                             C.cast(pd, C.c_void_p), hp(v1), hp(v2), hp(rec), max_outer + 1,
+                                             hp(summ), hp(st)))
+    out = []
+    for k in range(P):
+        n = int(summ[k, 1])
+        records = [dict(zip(RECORD_FIELDS, row)) for row in rec[k, :n]]
+        summary = dict(status=int(summ[k, 0]), iterations=n, finalGradNormRel=summ[k, 2],
+                       finalResidualRel=summ[k, 3], jacMin=summ[k, 4], jacMax=summ[k, 5], totalTimeSec=summ[k, 6],
+                       error=int(st[k]))
+        out.append((v1[k], v2[k], records, summary))
+    return out
+
+
 def newton_solve(ctx, mR, mT, norm, beta, deformation, *, max_outer=50, max_inner=500, nt=0, ls_max_steps=20,
                  tol_rel=1e-2, tol_abs=1e-5, forcing_cap=0.5, ls_c1=1e-4, ls_shrink=0.5, grad_cfl=1.0,
                  kind=PC_TWO_LEVEL, coarse_solver=COARSE_CHEB, cheb_iters=10, eps_scale=0.1, eig=None,

@@ -21,6 +21,14 @@ void launchMaxFinal(Ctx& ctx, const double* partials, int nb, double scale, doub
 // grid size of the element-wise kernels (grid-stride loops, at most 8 blocks of 256 per SM)
 unsigned elemBlocks(const Ctx& ctx, std::size_t n);
 
+// Per-pair reductions of a batch (GridDims::pairs): results for every pair in a device array
+// (slot 0..7), each bit-identical to the single-field reduction of that pair; a0/b0 (a1/b1) are
+// fields of the batch.  readPairs copies P results to the host (synchronises).
+double* launchDotPairs(Ctx& ctx, const GridDims& g, const double* a0, const double* b0, const double* a1,
+                       const double* b1, double scale, int slot);
+double* launchMaxAbsPairs(Ctx& ctx, const GridDims& g, const double* a0, const double* a1, int slot);
+void readPairs(Ctx& ctx, const double* dev, int P, double* host);
+
 // Synchronous host-visible reductions.
 double readScalar(Ctx& ctx, const double* dev);
 // dot (field.cpp:47-54): h1*h2*sum(a0*b0) + h1*h2*sum(a1*b1) (a1/b1 may be null).

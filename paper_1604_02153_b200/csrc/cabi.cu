@@ -7,6 +7,7 @@
 #include <memory>
 
 #include "../../include/vrg.h"
+#include "batch.cuh"
 #include "evalband.cuh"
 #include "heun.cuh"
 #include "precond.cuh"
@@ -540,6 +541,18 @@ int vrg_hess_create(vrg_ctx_t c, int n1, int n2, const double* v1, const double*
     });
 }
 
+int vrg_hess_create_batch(vrg_ctx_t c, int n1, int n2, int pairs, const double* v1, const double* v2, const double* mR,
+                          const double* mT, int norm, double beta, int deformation, int nt, vrg_hess_t* out) {
+    *out = nullptr;
+    return guarded(c, [&] {
+        if (pairs < 1) throw vrg::InvalidArgument("batched HessianOperator: pairs must be >= 1");
+        dims(n1, n2);
+        *out = new vrg_hess_s{c, vrg::Hessian(c->ctx, vrg::GridDims(n1, n2, pairs), v1, v2, mR, mT,
+                                              modelOf(norm, beta, deformation), nt, nullptr, 0),
+                              vrg::DBuf()};
+    });
+}
+
 int vrg_hess_create_ex(vrg_ctx_t c, int n1, int n2, const double* v1, const double* v2, const double* mR,
                        const double* mT, const vrg_model* model, int scheme, int nt, int mode, const double* state,
                        const double* adjoint, vrg_hess_t* out) {
@@ -951,6 +964,72 @@ void newtonToHost(vrg_ctx_s* c, int n1, int n2, const double* mR_host, const dou
     }
 }
 }  // namespace
+
+int vrg_newton_solve_batch(vrg_ctx_t c, int n1, int n2, int pairs, const double* mR_host, const double* mT_host,
+                           int norm, double beta, int deformation, const int* cfg_int, const double* cfg_dbl,
+                           const int* pc_int, const double* pc_dbl, double* v1_host, double* v2_host, double* records,
+                           int records_cap, double* summary, int* pair_status) {
+    return guarded(c, [&] {
+        vrg::NewtonConfig cfg;
+        cfg.maxOuterIter = cfg_int[0];
+        cfg.maxInnerIter = cfg_int[1];
+        cfg.ntOverride = cfg_int[2];
+        cfg.lsMaxSteps = cfg_int[3];
+        cfg.hessianMode = cfg_int[4];
+        cfg.tolRelGrad = cfg_dbl[0];
+        cfg.tolAbsGrad = cfg_dbl[1];
+        cfg.forcingCap = cfg_dbl[2];
+        cfg.lsC1 = cfg_dbl[3];
+        cfg.lsShrink = cfg_dbl[4];
+        cfg.gradCfl = cfg_dbl[5];
+        if (pairs < 1) throw vrg::InvalidArgument("batched newtonSolve: pairs must be >= 1");
+        vrg::Ctx& ctx = c->ctx;
+        const auto g1 = dims(n1, n2);
+        const vrg::GridDims g(n1, n2, pairs);
+        const std::size_t Np = g1.points(), N = g.points();
+        vrg::DBuf img(sizeof(double) * 2 * N), v(sizeof(double) * 2 * N);
+        VRG_CUDA(cudaMemcpyAsync(img.d(), mR_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+        VRG_CUDA(cudaMemcpyAsync(img.d() + N, mT_host, sizeof(double) * N, cudaMemcpyHostToDevice, ctx.stream));
+        std::vector<int> status;
+        std::vector<std::string> errors;
+        const auto reps = vrg::newtonSolveBatch(ctx, g, img.d(), img.d() + N, modelOf(norm, beta, deformation), cfg,
+                                                choiceOf(pc_int, pc_dbl), v.d(), status, errors);
+        VRG_CUDA(cudaMemcpyAsync(v1_host, v.d(), sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        VRG_CUDA(cudaMemcpyAsync(v2_host, v.d() + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        for (int k = 0; k < pairs; ++k) {
+            const auto& rep = reps[k];
+            int j = 0;
+            for (const auto& it : rep.iterations) {
+                if (j >= records_cap) break;
+                double* r = records + (static_cast<std::size_t>(k) * records_cap + j++) * 12;
+                r[0] = it.iter;
+                r[1] = it.gradNormInf;
+                r[2] = it.gradNormRel;
+                r[3] = it.objective;
+                r[4] = it.mismatch;
+                r[5] = it.innerIterations;
+                r[6] = it.lineSearchSteps;
+                r[7] = it.stepLength;
+                r[8] = it.searchDirDivRatio;
+                r[9] = it.wallTimeSec;
+                r[10] = static_cast<double>(it.ffts);
+                r[11] = static_cast<double>(it.interps);
+            }
+            double* sm = summary + 7 * k;
+            sm[0] = rep.status;
+            sm[1] = static_cast<double>(rep.iterations.size());
+            sm[2] = rep.finalGradNormRel;
+            sm[3] = rep.finalResidualRel;
+            sm[4] = rep.jacMin;
+            sm[5] = rep.jacMax;
+            sm[6] = rep.totalTimeSec;
+            pair_status[k] = status[k];
+            if (status[k]) std::fprintf(stderr, "batched newtonSolve: pair %d: %s\n", k, errors[k].c_str());
+        }
+        (void)Np;
+    });
+}
 
 int vrg_newton_solve(vrg_ctx_t c, int n1, int n2, const double* mR_host, const double* mT_host, int norm, double beta,
                      int deformation, const int* cfg_int, const double* cfg_dbl, const int* pc_int,

@@ -133,18 +133,27 @@ struct AllocStreamScope {
     }
 };
 
+// An n1 x n2 periodic grid, or a batch of `pairs` independent image pairs on that grid stacked
+// pair after pair: a field of a batch holds the pairs' n1 x n2 fields one after the other
+// (pointsPer() apart), so element-wise work runs over points() = pairs * n1 * n2 values and
+// every spatial kernel maps a row / node / mode to (pair, local index).  A vector field of a
+// batch is [component 0 of all pairs | component 1 of all pairs].
 struct GridDims {
     int n1 = 0, n2 = 0;
+    int pairs = 1;
     GridDims() = default;
-    GridDims(int a, int b) : n1(a), n2(b) {}
-    std::size_t points() const { return static_cast<std::size_t>(n1) * n2; }
+    GridDims(int a, int b, int p = 1) : n1(a), n2(b), pairs(p) {}
+    std::size_t pointsPer() const { return static_cast<std::size_t>(n1) * n2; }
+    std::size_t points() const { return pointsPer() * pairs; }
     int specCols() const { return n2 / 2 + 1; }
-    std::size_t specPoints() const { return static_cast<std::size_t>(n1) * specCols(); }
+    std::size_t specPer() const { return static_cast<std::size_t>(n1) * specCols(); }
+    std::size_t specPoints() const { return specPer() * pairs; }
+    GridDims one() const { return GridDims(n1, n2); }
     double h1() const { return kTwoPi / n1; }
     double h2() const { return kTwoPi / n2; }
-    bool operator==(const GridDims& o) const { return n1 == o.n1 && n2 == o.n2; }
+    bool operator==(const GridDims& o) const { return n1 == o.n1 && n2 == o.n2 && pairs == o.pairs; }
     bool operator!=(const GridDims& o) const { return !(*this == o); }
-    bool operator<(const GridDims& o) const { return std::tie(n1, n2) < std::tie(o.n1, o.n2); }
+    bool operator<(const GridDims& o) const { return std::tie(n1, n2, pairs) < std::tie(o.n1, o.n2, o.pairs); }
 };
 
 // Grid::Grid validation (src/field.cpp:9-15).

@@ -15,11 +15,12 @@ struct EpiTrace {
     const double* v2;
     double* x1;
     double* x2;
-    int n2;
+    int n1, n2;  // one pair's grid (stacked pairs: node p is node p mod n1 n2 of its pair)
     double h1, h2, sgnHalfHt;
     VRG_NO_PREFETCH
     __device__ double operator()(std::size_t p, const double* vs, const Pre&) const {
-        const int i1 = static_cast<int>(p / n2), i2 = static_cast<int>(p - static_cast<std::size_t>(i1) * n2);
+        const std::size_t row = p / n2;
+        const int i1 = static_cast<int>(row % n1), i2 = static_cast<int>(p - row * n2);
         const double c1 = __dadd_rn(-kPi, __dmul_rn(h1, static_cast<double>(i1)));
         const double c2 = __dadd_rn(-kPi, __dmul_rn(h2, static_cast<double>(i2)));
         x1[p] = __dsub_rn(c1, __dmul_rn(sgnHalfHt, __dadd_rn(v1[p], vs[0])));

@@ -37,7 +37,7 @@ __host__ __device__ inline int bandRowSmem(int n2, int tw) { return (n2 / kL) * 
 
 inline std::size_t bandSmem(const GridDims& g) { return sizeof(double) * bandRowSmem(g.n2, bandTW(g.n2)); }
 
-inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n1); }
+inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n1) * g.pairs; }
 
 // Without a gather (kGather = false: m~_0 = 0, the first incremental-state step) the epilogue
 // operands come from the immediate predecessor (vt_D), so the kernel waits before any load;
@@ -95,12 +95,17 @@ struct BarNamed {
 // One grid row r by TW threads (t = 0..TW-1): gather at the row's departure points, step
 // epilogue, guard partial of the row, then the exact periodic row filter in shared memory and
 // the row-filtered output.  `sm` holds bandRowSmem(n2, TW) doubles.
+// Stacked pairs (GridDims::pairs): r runs over all pairs' rows; row r belongs to pair r / n1,
+// whose coefficients lie pair * paddedPoints(n1, n2) further on, and its guard partial goes to
+// entry pair * gE + local row (guardStride).
 template <class Epi, bool kGather, bool kWindow, int TW, class Bar>
-__device__ __forceinline__ void bandRow(const CoeffSet<1>& cs, const double* __restrict__ x1,
+__device__ __forceinline__ void bandRow(CoeffSet<1> cs, const double* __restrict__ x1,
                                         const double* __restrict__ x2, int n1, int n2, const Epi& epi,
                                         double* __restrict__ rowOut, unsigned* nonfinite, const BandWindow& win,
-                                        int r, int t, double* sm, Bar bar) {
+                                        int r, int t, double* sm, Bar bar, unsigned gE) {
     if (!kGather) pdlWait();
+    const int pair = kWindow ? 0 : r / n1;
+    if (!kWindow) cs.c[0] += static_cast<std::size_t>(pair) * paddedPoints(n1, n2);
     const int nc = n2 / kL;
     double* E = sm + nc * kCS;
     double* F0 = E + nc;
@@ -201,7 +206,7 @@ __device__ __forceinline__ void bandRow(const CoeffSet<1>& cs, const double* __r
         if (t == 0) {
             double m = red[0];
             for (int w = 1; w < TW / 32; ++w) m = fmax(m, red[w]);
-            epi.guardPartials[r] = m;
+            epi.guardPartials[pair * gE + (r - pair * n1)] = m;
         }
     }
     // the next prefilter's input check (checkFinite(u, "prefilter"), interp.cpp:76)
@@ -268,10 +273,10 @@ template <class Epi, bool kGather, bool kWindow = false, int TW = kBandThreads>
 __global__ void __launch_bounds__(TW, (bandMinBlocks<Epi, TW>())) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
                                                             const double* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
-                                                            BandWindow win = BandWindow{}) {
+                                                            BandWindow win, unsigned gE) {
     extern __shared__ __align__(16) double sm[];
     bandRow<Epi, kGather, kWindow, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, win, blockIdx.x, threadIdx.x, sm,
-                                       BarBlock{});
+                                       BarBlock{}, gE);
     pdlTrigger();  // at the end: the dependent column pass must not take this kernel's slots
 }
 
@@ -291,15 +296,15 @@ constexpr int stripWorkers() {
 template <class Epi, bool kGather, int TW>
 __global__ void __launch_bounds__(TW* stripWorkers<Epi, TW>(), 1)
     k_eval_strip(CoeffSet<1> cs, const double* __restrict__ x1, const double* __restrict__ x2, int n1, int n2, Epi epi,
-                 double* __restrict__ rowOut, unsigned* nonfinite) {
+                 double* __restrict__ rowOut, unsigned* nonfinite, int rows, unsigned gE) {
     extern __shared__ __align__(16) double sm[];
     constexpr int W = stripWorkers<Epi, TW>();
     const int w = threadIdx.x / TW;
     const int t = threadIdx.x - w * TW;
     const int r = blockIdx.x * W + w;
-    if (r < n1)
+    if (r < rows)
         bandRow<Epi, kGather, false, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, BandWindow{}, r, t,
-                                         sm + w * bandRowSmem(n2, TW), BarNamed<TW>{1 + w});
+                                         sm + w * bandRowSmem(n2, TW), BarNamed<TW>{1 + w}, gE);
     pdlTrigger();
 }
 
@@ -335,8 +340,9 @@ void launchEvalStrip(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* 
             attr[ctx.device] = true;
         }
     }
-    launchPdl(1, k_eval_strip<Epi, kGather, TW>, dim3((g.n1 + W - 1) / W), dim3(kThreads), smem, ctx.stream,
-              cs, x1, x2, g.n1, g.n2, epi, rowOut, nonfinite);
+    const int rows = g.n1 * g.pairs;
+    launchPdl(1, k_eval_strip<Epi, kGather, TW>, dim3((rows + W - 1) / W), dim3(kThreads), smem, ctx.stream, cs, x1,
+              x2, g.n1, g.n2, epi, rowOut, nonfinite, rows, guardStride(g));
 }
 
 template <class Epi, bool kGather>
@@ -352,19 +358,19 @@ void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x
     switch (bandTW(g.n2)) {
         case 256:
             launchPdl(1, k_eval_band<Epi, kGather, false, 256>, grid, dim3(256), smem, ctx.stream, cs, x1, x2, g.n1,
-                      g.n2, epi, rowOut, nonfinite, BandWindow{});
+                      g.n2, epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
             break;
         case 128:
             launchPdl(1, k_eval_band<Epi, kGather, false, 128>, grid, dim3(128), smem, ctx.stream, cs, x1, x2, g.n1,
-                      g.n2, epi, rowOut, nonfinite, BandWindow{});
+                      g.n2, epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
             break;
         case 64:
             launchPdl(1, k_eval_band<Epi, kGather, false, 64>, grid, dim3(64), smem, ctx.stream, cs, x1, x2, g.n1, g.n2,
-                      epi, rowOut, nonfinite, BandWindow{});
+                      epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
             break;
         default:
             launchPdl(1, k_eval_band<Epi, kGather, false, 32>, grid, dim3(32), smem, ctx.stream, cs, x1, x2, g.n1, g.n2,
-                      epi, rowOut, nonfinite, BandWindow{});
+                      epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
             break;
     }
 }
@@ -377,7 +383,7 @@ void launchEvalBandWindow(Ctx& ctx, int n1, int L, int n2, CoeffSet<1> cs, const
     const GridDims gl(L, n2);
     if (bandTW(n2) != kBandThreads) throw NotSupported("slab step: the row length must be a multiple of 256");
     launchPdl(1, k_eval_band<Epi, kGather, true>, dim3(L), dim3(kBandThreads), bandSmem(gl), ctx.stream, cs, x1, x2,
-              n1, n2, epi, rowOut, nonfinite, win);
+              n1, n2, epi, rowOut, nonfinite, win, 0u);
 }
 
 }  // namespace vrg

@@ -175,7 +175,7 @@ HeunTransport::HeunTransport(Ctx& c, const GridDims& gd, const double* v1, const
     copy(ctx, N, v2, v.d() + N);
     if (anyNonFinite(ctx, 2 * N, v.d())) throw InvalidArgument("transport velocity: non-finite value");
     work_.alloc(sizeof(double) * 8 * N);
-    log.ensure(nt + 1, guardBlocks(g));
+    log.ensure(nt + 1, g);
 }
 
 const double* HeunTransport::divVelocity() {

@@ -602,27 +602,31 @@ void launchPrefilterBatch(Ctx& ctx, const GridDims& g, const double* u, std::siz
                           std::size_t cStride, double* tmp, unsigned* nonfinite) {
     if (count <= 0) return;
     const SegPlan pr = segPlan(g.n2), pc = segPlan(g.n1);
-    if (!(pr.ok && pc.ok) || uStride < g.points() || cStride < paddedPoints(g.n1, g.n2)) {
+    const bool packed = g.pairs == 1 || (uStride == g.points() && cStride == paddedTotal(g));
+    if (!(pr.ok && pc.ok) || !packed || uStride < g.points() || cStride < paddedTotal(g)) {
         for (int k = 0; k < count; ++k) launchPrefilter(ctx, g, u + k * uStride, c + k * cStride, tmp, nonfinite);
         return;
     }
     {
+        // rows are independent: the pairs' rows form one (pairs * n1) x n2 row set
         LaunchScope ls_(ctx, "k_prefilter_rows");
-        launchSegR<true, false>(ctx, g, pr, u, tmp, nonfinite, count, uStride, g.points());
+        launchSegR<true, false>(ctx, GridDims(g.n1 * g.pairs, g.n2), pr, u, tmp, nonfinite, count, uStride,
+                                g.points());
     }
     VRG_LAUNCH_CHECK();
-    launchColumnPass(ctx, g, tmp, c, count, g.points(), cStride);
+    // columns are periodic per pair: count * pairs column sets, one pair's field apart
+    launchColumnPass(ctx, g.one(), tmp, c, count * g.pairs, g.pointsPer(), paddedPoints(g.n1, g.n2));
 }
 
 void launchPrefilterRows(Ctx& ctx, const GridDims& g, const double* u, double* rowFiltered, unsigned* nonfinite) {
     const SegPlan pr = segPlan(g.n2);
     if (!pr.ok) throw NotSupported("prefilter row pass: n2 must be a multiple of 32");
-    launchSegR<true, false>(ctx, g, pr, u, rowFiltered, nonfinite);
+    launchSegR<true, false>(ctx, GridDims(g.n1 * g.pairs, g.n2), pr, u, rowFiltered, nonfinite);
     VRG_LAUNCH_CHECK();
 }
 
 void launchPrefilterCols(Ctx& ctx, const GridDims& g, const double* rowFiltered, double* c) {
-    if (!launchColumnPass(ctx, g, rowFiltered, c))
+    if (!launchColumnPass(ctx, g.one(), rowFiltered, c, g.pairs, g.pointsPer(), paddedPoints(g.n1, g.n2)))
         throw NotSupported("prefilter column pass: n1 must be a multiple of 32");
 }
 
@@ -631,10 +635,15 @@ void launchPrefilter(Ctx& ctx, const GridDims& g, const double* u, double* c, do
     if (pr.ok && pc.ok) {
         {
             LaunchScope ls_(ctx, "k_prefilter_rows");
-            launchSegR<true, false>(ctx, g, pr, u, tmp, nonfinite);
+            launchSegR<true, false>(ctx, GridDims(g.n1 * g.pairs, g.n2), pr, u, tmp, nonfinite);
         }
         VRG_LAUNCH_CHECK();
-        launchColumnPass(ctx, g, tmp, c);
+        launchColumnPass(ctx, g.one(), tmp, c, g.pairs, g.pointsPer(), paddedPoints(g.n1, g.n2));
+        return;
+    }
+    if (g.pairs > 1) {  // generic path: pair by pair
+        for (int k = 0; k < g.pairs; ++k)
+            launchPrefilter(ctx, g.one(), u + k * g.pointsPer(), c + k * paddedPoints(g.n1, g.n2), tmp, nonfinite);
         return;
     }
     double* tmp2 = tmp + g.points();  // unpadded column-pass output of the generic path

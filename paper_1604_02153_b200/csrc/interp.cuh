@@ -98,6 +98,8 @@ __device__ __forceinline__ int cellBase(double x, double invh, int n, double w[4
 constexpr std::size_t paddedPoints(int n1, int n2) {
     return static_cast<std::size_t>(n1 + 3) * static_cast<std::size_t>(n2 + 3);
 }
+// padded coefficients of one field of a grid or batch (the pairs' padded fields one after another)
+inline std::size_t paddedTotal(const GridDims& g) { return paddedPoints(g.n1, g.n2) * g.pairs; }
 
 // Pads / unpads a coefficient field (used at the C ABI, whose coefficients are unpadded).
 void launchPad(Ctx& ctx, const GridDims& g, const double* c, double* padded);

@@ -152,6 +152,10 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
                  const double* gradTraj)
     : ctx(c), g(gd), model(mdl), nt(steps), solver(c, gd, v1, v2, steps), weights(gd, mdl.norm), mode_(hmode) {
     if (!(mdl.betaV > 0.0)) throw InvalidArgument("applyReg: beta must be positive");
+    if (g.pairs > 1 && (model.scheme != kSchemeSL || hmode != 0 || model.deformation == kNearIncompressible))
+        throw NotSupported("batched pairs: Gauss-Newton SL operators of the compressible / incompressible models only");
+    pairStatus.assign(g.pairs, 0);
+    pairError.assign(g.pairs, std::string());
     const std::size_t N = g.points();
     state_.alloc(sizeof(double) * (nt + 1) * N);
     if (model.scheme != kSchemeSL) {
@@ -163,6 +167,10 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
                                  ctx.stream));
     } else {
         solver.state(mT, state_.d(), true);  // counts 2 + nt interps like solveState in the ctor
+        if (g_collectGuards) {
+            pairStatus = solver.log.pairStatus;
+            pairError = solver.log.pairError;
+        }
     }
     // Per-iterate invariants, not counted here: the reference recomputes them inside every
     // matvec and the per-matvec counters below include them.
@@ -177,11 +185,11 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
         gradientBatch(ctx, g, state_.d(), nt + 1, G_.d());  // one batched transform chain per chunk
     }
     const double* Xf = solver.departure(kForward);
-    work_.alloc(sizeof(double) * (11 * N + 2 * paddedPoints(g.n1, g.n2)));  // + vt coefficients (2 padded)
+    work_.alloc(sizeof(double) * (11 * N + 2 * paddedTotal(g)));  // + vt coefficients (2 padded)
     // GD_j = (grad m_{j-1})_D, j = 1..nt: the 2nt gradient components prefiltered in one batch
     // (two launches) and evaluated at the forward departure points in one launch per chunk
     {
-        const std::size_t P = paddedPoints(g.n1, g.n2);
+        const std::size_t P = paddedTotal(g);
         const int total = nt;  // gradient fields G_0 .. G_{nt-1}, two components each
         const std::size_t perField = sizeof(double) * (2 * P + 2 * N);
         const int chunk = static_cast<int>(std::max<std::size_t>(
@@ -232,7 +240,7 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     fused_ = bandFusable(g) && colPassFusable(g);
     lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
-    adjLog_.ensure(nt + 1, guardBlocks(g));
+    adjLog_.ensure(nt + 1, g);
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
     // every plan a matvec uses exists before any graph capture (plan creation allocates)
@@ -283,7 +291,7 @@ void Hessian::initHeun(const double* mR, const double* mT, const double* stateTr
     useGraphs = false;
     lazyInterps_ = 0;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
-    adjLog_.ensure(nt + 1, guardBlocks(g));
+    adjLog_.ensure(nt + 1, g);
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
     ctx.sync();
@@ -395,7 +403,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     // incremental state (solveIncState SL, transport.cpp:322-342); vt's two components are
     // prefiltered in one batch (two launches) when contiguous
     {
-        const std::size_t P = paddedPoints(g.n1, g.n2);
+        const std::size_t P = paddedTotal(g);
         double* cv = vtD + 11 * N;
         if (vt2 == vt1 + N) {
             launchPrefilterBatch(ctx, g, vt1, N, 2, cv, P, tmp, nullptr);
@@ -607,7 +615,7 @@ void slabStep(Ctx& ctx, int kind, int n1, int n2, int L, int winBase, int winRow
 
 void Hessian::beginDeferredGuards(int maxCalls) {
     if (heun_ || mode_ == 1 || maxCalls <= 0) return;  // those paths check as they run / differently
-    const std::size_t per = static_cast<std::size_t>(nt + 1);
+    const std::size_t per = static_cast<std::size_t>(nt + 1) * g.pairs;
     if (maxCalls > deferCap_) {
         deferMax_.alloc(sizeof(double) * per * maxCalls);
         deferFlags_.alloc(sizeof(unsigned) * per * maxCalls);
@@ -622,15 +630,35 @@ void Hessian::endDeferredGuards() {
     deferring_ = false;
     const int k = deferCount_;
     if (k == 0) return;
-    const std::size_t per = static_cast<std::size_t>(nt + 1);
+    const int P = g.pairs;
+    const std::size_t steps = static_cast<std::size_t>(nt + 1), per = steps * P;
     std::vector<double> mx(per * k);
-    std::vector<unsigned> fl(per * k);
+    std::vector<unsigned> fl(steps * k);
     VRG_CUDA(cudaMemcpyAsync(mx.data(), deferMax_.d(), sizeof(double) * per * k, cudaMemcpyDeviceToHost, ctx.stream));
-    VRG_CUDA(cudaMemcpyAsync(fl.data(), deferFlags_.d(), sizeof(unsigned) * per * k, cudaMemcpyDeviceToHost,
+    VRG_CUDA(cudaMemcpyAsync(fl.data(), deferFlags_.d(), sizeof(unsigned) * steps * k, cudaMemcpyDeviceToHost,
                              ctx.stream));
     ctx.sync();
-    for (int c = 0; c < k; ++c)
-        GuardLog::checkHost(mx.data() + c * per, fl.data() + c * per, "adjoint", nt, false, true, nt);
+    if (!g_collectGuards) {
+        for (int c = 0; c < k; ++c)
+            GuardLog::checkHost(mx.data() + c * per, fl.data() + c * steps, "adjoint", nt, false, true, nt);
+        return;
+    }
+    // a batch: each pair's first error in call order, nothing thrown
+    std::vector<double> m1(steps);
+    for (int p = 0; p < P; ++p) {
+        for (int c = 0; c < k && !pairStatus[p]; ++c) {
+            for (std::size_t s = 0; s < steps; ++s) m1[s] = mx[c * per + s * P + p];
+            try {
+                GuardLog::checkHost(m1.data(), fl.data() + c * steps, "adjoint", nt, false, true, nt);
+            } catch (const BlowupError& e) {
+                pairStatus[p] = kBlowup;
+                pairError[p] = e.what();
+            } catch (const InvalidArgument& e) {
+                pairStatus[p] = kInvalidArgument;
+                pairError[p] = e.what();
+            }
+        }
+    }
 }
 
 void Hessian::guardAfterMatvec() {
@@ -643,11 +671,11 @@ void Hessian::guardAfterMatvec() {
         checkLastGuard();
         return;
     }
-    const std::size_t per = static_cast<std::size_t>(nt + 1);
+    const std::size_t steps = static_cast<std::size_t>(nt + 1), per = steps * g.pairs;
     VRG_CUDA(cudaMemcpyAsync(deferMax_.d() + per * deferCount_, adjLog_.stepMax.d(), sizeof(double) * per,
                              cudaMemcpyDeviceToDevice, ctx.stream));
-    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + per * deferCount_, adjLog_.flags.d(),
-                             sizeof(unsigned) * per, cudaMemcpyDeviceToDevice, ctx.stream));
+    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + steps * deferCount_, adjLog_.flags.d(),
+                             sizeof(unsigned) * steps, cudaMemcpyDeviceToDevice, ctx.stream));
     ++deferCount_;
 }
 
@@ -661,6 +689,12 @@ void Hessian::checkLastGuard() {
         return;
     }
     adjLog_.check(ctx, "adjoint", nt, false, true, nt);
+    if (g_collectGuards)
+        for (int p = 0; p < g.pairs; ++p)
+            if (!pairStatus[p] && adjLog_.pairStatus[p]) {
+                pairStatus[p] = adjLog_.pairStatus[p];
+                pairError[p] = adjLog_.pairError[p];
+            }
 }
 
 // Average device time of one launch of a matvec kernel class, `iters` back-to-back launches
@@ -872,7 +906,7 @@ void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, doub
         specScale(ctx, g, S, 2, regSym, 1.0);
         dataTerm(vt1, vt2, b, b + N, nullptr, nullptr, nullptr, nullptr);
         fftForward(ctx, g, b, S + 2 * NS, 2);
-        specCombine(ctx, g, S + 2 * NS, S + 3 * NS, S, S + NS, nullptr, true, 1.0 / N, S + 2 * NS, S + 3 * NS);
+        specCombine(ctx, g, S + 2 * NS, S + 3 * NS, S, S + NS, nullptr, true, 1.0 / g.pointsPer(), S + 2 * NS, S + 3 * NS);
         if (o2 == o1 + N) {
             fftInverse(ctx, g, S + 2 * NS, o1, 2);
         } else {
@@ -899,7 +933,7 @@ void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, doub
                 fftForward(ctx, g, vt1, S, 1);
                 fftForward(ctx, g, vt2, S + NS, 1);
             }
-            specScale(ctx, g, S, 2, regSym, 1.0 / N);
+            specScale(ctx, g, S, 2, regSym, 1.0 / g.pointsPer());
             fftInverse(ctx, g, S, reg, 2);
         }
         if (aux_) {
@@ -929,7 +963,7 @@ void Hessian::applyDataTerm(const double* vt1, const double* vt2, double* o1, do
         if (model.deformation == kIncompressible) {
             cplx* T = spec_.as<cplx>() + 2 * g.specPoints();
             fftForward(ctx, g, b, T, 2);
-            specCombine(ctx, g, T, T + g.specPoints(), nullptr, nullptr, nullptr, true, 1.0 / N, T, T + g.specPoints());
+            specCombine(ctx, g, T, T + g.specPoints(), nullptr, nullptr, nullptr, true, 1.0 / g.pointsPer(), T, T + g.specPoints());
             if (o2 == o1 + N) {
                 fftInverse(ctx, g, T, o1, 2);
             } else {
@@ -968,12 +1002,12 @@ void Hessian::launchSplit(const double* s1, const double* s2, double* o1, double
         fftForward(ctx, g, s1, S, 1);
         fftForward(ctx, g, s2, S + NS, 1);
     }
-    specCombine(ctx, g, S, S + NS, nullptr, nullptr, inv, false, 1.0 / N, T, T + NS);
+    specCombine(ctx, g, S, S + NS, nullptr, nullptr, inv, false, 1.0 / g.pointsPer(), T, T + NS);
     fftInverse(ctx, g, T, t, 2);
     dataTerm(t, t + N, b, b + N, nullptr, nullptr, nullptr, nullptr);
     if (model.deformation == kNearIncompressible) addPenalty(t, t + N, b, b + N);
     fftForward(ctx, g, b, T, 2);
-    specCombine(ctx, g, T, T + NS, S, S + NS, inv, model.deformation == kIncompressible, 1.0 / N, T, T + NS);
+    specCombine(ctx, g, T, T + NS, S, S + NS, inv, model.deformation == kIncompressible, 1.0 / g.pointsPer(), T, T + NS);
     if (o2 == o1 + N) {
         fftInverse(ctx, g, T, o1, 2);
     } else {

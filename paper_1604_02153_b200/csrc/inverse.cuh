@@ -68,6 +68,17 @@ public:
     void endDeferredGuards();
     // counter increments of one data term in the reference (steady state)
     void countDataTerm();
+    // forget the lazily-built per-velocity work still to be counted (an operator rebuilt for a
+    // problem whose operator already ran, batch.cu)
+    void clearLazyCounts() {
+        lazyInterps_ = 0;
+        lazyFfts_ = 0;
+    }
+    // a batch of stacked pairs (GridDims::pairs > 1): the guard verdicts of the matvecs so far
+    // (0 ok, else the C ABI status of the error the reference would throw; first error kept)
+    // instead of exceptions
+    std::vector<int> pairStatus;
+    std::vector<std::string> pairError;
 
 private:
     // b = sum_j w_j lt_j grad m_j of the GN incremental adjoint seeded with -m~(1).

@@ -37,13 +37,17 @@ __global__ void k_bandlimit(double2* s, int n1, int n2, double scale) {
 
 // Two-level restriction (cutoffFilter Low + resample to the half grid, precond.cpp:266-268):
 // coarse spectrum = amp * fine spectrum on |k_i| < n_i^c / 2, times 1/N_c.
+// `sets` spectra one after another (pairs x components of a batch).
 __global__ void k_restrict_low(const double2* __restrict__ f, int n1f, int n2f, double2* __restrict__ c, int n1c,
-                               int n2c, double amp, double scale) {
+                               int n2c, int sets, double amp, double scale) {
     const int ncc = n2c / 2 + 1, ncf = n2f / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1c) * ncc;
+    const std::size_t nPer = static_cast<std::size_t>(n1c) * ncc;
+    const std::size_t n = nPer * sets;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int rt = static_cast<int>(i / ncc), col = static_cast<int>(i - static_cast<std::size_t>(rt) * ncc);
+    const std::size_t set = i / nPer, li = i - set * nPer;
+    f += set * static_cast<std::size_t>(n1f) * ncf;
+    const int rt = static_cast<int>(li / ncc), col = static_cast<int>(li - static_cast<std::size_t>(rt) * ncc);
     const int k1 = waveOfP(rt, n1c), k2 = waveOfP(col, n2c);
     double2 v = make_double2(0.0, 0.0);
     // low band of the fine cut-off (|k_i| < n_i^f/4) intersected with the resample band
@@ -58,12 +62,16 @@ __global__ void k_restrict_low(const double2* __restrict__ f, int n1f, int n2f, 
 // out^ = (prolong(sc^) * amp + highpass(r^)) * scale on the fine half spectrum
 // (resample(sc, fine) + cutoffFilter(r, High), precond.cpp:267, 286-287).
 // rf and out may alias (in-place update, one element per thread)
-__global__ void k_prolong_add_high(const double2* __restrict__ sc, int n1c, int n2c, const double2* rf, double2* out, int n1f, int n2f, double amp, double scale) {
+__global__ void k_prolong_add_high(const double2* __restrict__ sc, int n1c, int n2c, const double2* rf, double2* out,
+                                   int n1f, int n2f, int sets, double amp, double scale) {
     const int ncc = n2c / 2 + 1, ncf = n2f / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1f) * ncf;
+    const std::size_t nPer = static_cast<std::size_t>(n1f) * ncf;
+    const std::size_t n = nPer * sets;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int rt = static_cast<int>(i / ncf), col = static_cast<int>(i - static_cast<std::size_t>(rt) * ncf);
+    const std::size_t set = i / nPer, li = i - set * nPer;
+    sc += set * static_cast<std::size_t>(n1c) * ncc;
+    const int rt = static_cast<int>(li / ncf), col = static_cast<int>(li - static_cast<std::size_t>(rt) * ncf);
     const int k1 = waveOfP(rt, n1f), k2 = waveOfP(col, n2f);
     double2 v = make_double2(0.0, 0.0);
     if (abs(k1) < n1c / 2 && abs(k2) < n2c / 2) {
@@ -620,6 +628,33 @@ std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const doub
 }
 
 // ------------------------------------------------------------------------------ two-level
+// restriction of a (batched) vector field r on g to rc on gc: R, C spectra scratch of the two
+// components; the components of all pairs are 2 * pairs spectra in a row
+void restrictLow(Ctx& ctx, const GridDims& g, const GridDims& gc, const double* r, cplx* R, cplx* C, double* rc,
+                 double ampDown) {
+    fftForward(ctx, g, r, R, 2);
+    {
+        LaunchScope ls_(ctx, "k_restrict_low");
+        k_restrict_low<<<static_cast<unsigned>((2 * gc.specPoints() + 255) / 256), 256, 0, ctx.stream>>>(
+            R, g.n1, g.n2, C, gc.n1, gc.n2, 2 * gc.pairs, ampDown, 1.0 / gc.pointsPer());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, gc, C, rc, 2);
+}
+
+// out = prolong(sc) + high band of r (R holds r's spectra from restrictLow)
+void prolongAddHigh(Ctx& ctx, const GridDims& g, const GridDims& gc, const double* sc, cplx* C, cplx* R, double* out,
+                    double ampUp) {
+    fftForward(ctx, gc, sc, C, 2);
+    {
+        LaunchScope ls_(ctx, "k_prolong_add_high");
+        k_prolong_add_high<<<static_cast<unsigned>((2 * g.specPoints() + 255) / 256), 256, 0, ctx.stream>>>(
+            C, gc.n1, gc.n2, R, R, g.n1, g.n2, 2 * g.pairs, ampUp, 1.0 / g.pointsPer());
+    }
+    VRG_LAUNCH_CHECK();
+    fftInverse(ctx, g, R, out, 2);
+}
+
 bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator& coarse, const PrecondChoice& choice,
                    double outerTol, double eMin, double eMax, double* out) {
     NvtxRange nv_("applyTwoLevel");
@@ -630,16 +665,8 @@ bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator&
     double* rc = ctx.scratchBuf(130, sizeof(double) * 2 * Nc);
     double* sc = ctx.scratchBuf(131, sizeof(double) * 2 * Nc);
     const double ampDown = static_cast<double>(Nc) / static_cast<double>(N);
-    for (int i = 0; i < 2; ++i) {
-        fftForward(ctx, g, r + i * N, R + i * NS, 1);
-        {
-            LaunchScope ls_(ctx, "k_restrict_low");
-            k_restrict_low<<<specBlocks(gc), 256, 0, ctx.stream>>>(R + i * NS, g.n1, g.n2, C + i * NSc, gc.n1, gc.n2,
-                                                                   ampDown, 1.0 / Nc);
-        }
-        VRG_LAUNCH_CHECK();
-        fftInverse(ctx, gc, C + i * NSc, rc + i * Nc, 1);
-    }
+    // both components (and every pair of a batch) in one transform chain
+    restrictLow(ctx, g, gc, r, R, C, rc, ampDown);
     LinOpDev op = [&](const double* s, double* o) { coarse.applySplit(s, o); };
     if (choice.coarseSolver == kCoarseCheb) {
         // the Chebyshev loop has no host decisions: its coarse matvecs run back to back on the
@@ -672,17 +699,10 @@ bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator&
         return false;
     }
     const double ampUp = static_cast<double>(N) / static_cast<double>(Nc);
-    for (int i = 0; i < 2; ++i) {
-        fftForward(ctx, gc, sc + i * Nc, C + i * NSc, 1);
-        {
-            LaunchScope ls_(ctx, "k_prolong_add_high");
-            k_prolong_add_high<<<specBlocks(g), 256, 0, ctx.stream>>>(C + i * NSc, gc.n1, gc.n2, R + i * NS, R + i * NS,
-                                                                      g.n1, g.n2, ampUp, 1.0 / N);
-        }
-        VRG_LAUNCH_CHECK();
-        fftInverse(ctx, g, R + i * NS, out + i * N, 1);
-    }
+    prolongAddHigh(ctx, g, gc, sc, C, R, out, ampUp);
     ctx.ffts += 4;
+    (void)NS;
+    (void)NSc;
     return true;
 }
 
@@ -818,12 +838,12 @@ void ExternalFineOperator::applySplit(const double* s, double* o) {
     double* b = ctx_.scratchBuf(152, sizeof(double) * 2 * N);
     const double* inv = weights_.invRegSymbol(model_.betaV, -0.5);
     fftForward(ctx_, g_, s, S, 2);
-    specCombine(ctx_, g_, S, S + NS, nullptr, nullptr, inv, false, 1.0 / N, T, T + NS);
+    specCombine(ctx_, g_, S, S + NS, nullptr, nullptr, inv, false, 1.0 / g_.pointsPer(), T, T + NS);
     fftInverse(ctx_, g_, T, t, 2);
     if (ctx_.fine.dataTerm(ctx_.fine.user, t, b) != 0)
         throw std::runtime_error("external fine operator: data-term callback failed");
     fftForward(ctx_, g_, b, T, 2);
-    specCombine(ctx_, g_, T, T + NS, S, S + NS, inv, false, 1.0 / N, T, T + NS);
+    specCombine(ctx_, g_, T, T + NS, S, S + NS, inv, false, 1.0 / g_.pointsPer(), T, T + NS);
     fftInverse(ctx_, g_, T, o, 2);
     // counters of one split matvec (Hessian::applySplit + countDataTerm, GN SL compressible)
     ctx_.ffts += 8 + (3 + 3LL * nt_) + 3LL * (nt_ + 1) + lazyFfts_;

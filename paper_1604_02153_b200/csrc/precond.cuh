@@ -69,10 +69,21 @@ double tridiagMaxEig(const std::vector<double>& alpha, const std::vector<double>
 // lanczosEmax (precond.cpp:134-161) with the power-iteration fallback (precond.cpp:119-132).
 double lanczosEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, std::uint64_t seed);
 
+// Two-level restriction / prolongation of a (batched) vector field between g and its half grid
+// gc (cutoffFilter Low + resample, resample + cutoffFilter High; precond.cpp:266-268, 286-287);
+// R and C hold the two components' spectra of every pair.
+void restrictLow(Ctx& ctx, const GridDims& g, const GridDims& gc, const double* r, cplx* R, cplx* C, double* rc,
+                 double ampDown);
+void prolongAddHigh(Ctx& ctx, const GridDims& g, const GridDims& gc, const double* sc, cplx* C, cplx* R, double* out,
+                    double ampUp);
+
 // applyTwoLevel (precond.cpp:264-289); returns false when the coarse solve diverged and the
 // identity fallback was taken.
 bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator& coarse, const PrecondChoice& choice,
                    double outerTol, double eMin, double eMax, double* out);
+
+// lanczosEmax of a coarse operator's split Hessian with its guard checks deferred (precond.cpp:134-161)
+double coarseLanczosEmax(Ctx& ctx, CoarseOperator& coarse, int steps, std::uint64_t seed);
 
 // estimateEigsAt / estimateEigs (precond.cpp:242-258): (1, Lanczos eMax of the coarse split
 // Hessian at v; v = nullptr means v = 0).

@@ -140,7 +140,9 @@ Ctx::~Ctx() {
 }
 
 cufftHandle Ctx::plan(const GridDims& g, cufftType type, int batch) {
-    PlanKey key{g.n1, g.n2, static_cast<int>(type), batch, stream};
+    // `batch` fields of the grid: batch * pairs 2-D transforms of one n1 x n2 field each
+    const int transforms = batch * g.pairs;
+    PlanKey key{g.n1, g.n2, static_cast<int>(type), transforms, stream};
     auto it = plans.find(key);
     if (it != plans.end()) return it->second;
     cufftHandle h;
@@ -148,11 +150,11 @@ cufftHandle Ctx::plan(const GridDims& g, cufftType type, int batch) {
     VRG_CUFFT(cufftCreate(&h));
     std::size_t work = 0;
     if (type == CUFFT_D2Z) {
-        VRG_CUFFT(cufftMakePlanMany(h, 2, n, nullptr, 1, static_cast<int>(g.points()), nullptr, 1,
-                                    static_cast<int>(g.specPoints()), CUFFT_D2Z, batch, &work));
+        VRG_CUFFT(cufftMakePlanMany(h, 2, n, nullptr, 1, static_cast<int>(g.pointsPer()), nullptr, 1,
+                                    static_cast<int>(g.specPer()), CUFFT_D2Z, transforms, &work));
     } else {
-        VRG_CUFFT(cufftMakePlanMany(h, 2, n, nullptr, 1, static_cast<int>(g.specPoints()), nullptr, 1,
-                                    static_cast<int>(g.points()), CUFFT_Z2D, batch, &work));
+        VRG_CUFFT(cufftMakePlanMany(h, 2, n, nullptr, 1, static_cast<int>(g.specPer()), nullptr, 1,
+                                    static_cast<int>(g.pointsPer()), CUFFT_Z2D, transforms, &work));
     }
     VRG_CUFFT(cufftSetStream(h, stream));
     plans[key] = h;
@@ -254,6 +256,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot_partial(const double* __
 // Stage 2: out = scale*(sum partial0) + scale*(sum partial1)  (dot per component, then added,
 // field.cpp:47-54).
 __global__ void k_dot_final(const double* partial, int nb, double scale, double* out) {
+    partial += static_cast<std::size_t>(blockIdx.x) * 2 * kReduceBlocks;  // block = pair of a batch
+    out += blockIdx.x;
     __shared__ double r0[32], r1[32];
     double s0 = 0.0, s1 = 0.0;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) {
@@ -298,6 +302,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial(const double*
 }
 
 __global__ void k_max_final(const double* partial, int nb, double scale, double* out) {
+    partial += static_cast<std::size_t>(blockIdx.x) * 2 * kReduceBlocks;  // block = pair of a batch
+    out += blockIdx.x;
     __shared__ double r[32];
     double m = 0.0;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) m = fmax(m, partial[i]);
@@ -308,6 +314,61 @@ __global__ void k_max_final(const double* partial, int nb, double scale, double*
         double t = 0.0;
         for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t = fmax(t, r[w]);
         *out = scale * t;
+    }
+}
+
+// Per-pair forms of the two-stage reductions (stacked pairs, GridDims::pairs): blockIdx.y = pair,
+// each pair reduced over its own nPer values with the block partition and summation order of the
+// single-field kernels above, so a pair's result is bit-identical to reducing it alone.
+__global__ void __launch_bounds__(kReduceThreads) k_dot_partial_pairs(const double* __restrict__ a0,
+                                                                      const double* __restrict__ b0,
+                                                                      const double* __restrict__ a1,
+                                                                      const double* __restrict__ b1, std::size_t nPer,
+                                                                      double* partial) {
+    const std::size_t off = blockIdx.y * nPer;
+    double s0 = 0.0, s1 = 0.0;
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nPer; i += stride) {
+        s0 += a0[off + i] * b0[off + i];
+        if (a1) s1 += a1[off + i] * b1[off + i];
+    }
+    __shared__ double r0[kReduceThreads / 32], r1[kReduceThreads / 32];
+    s0 = warpSum(s0);
+    s1 = warpSum(s1);
+    if ((threadIdx.x & 31) == 0) {
+        r0[threadIdx.x >> 5] = s0;
+        r1[threadIdx.x >> 5] = s1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int w = 0; w < kReduceThreads / 32; ++w) {
+            t0 += r0[w];
+            t1 += r1[w];
+        }
+        partial[blockIdx.y * 2 * kReduceBlocks + blockIdx.x] = t0;
+        partial[blockIdx.y * 2 * kReduceBlocks + kReduceBlocks + blockIdx.x] = t1;
+    }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial_pairs(const double* __restrict__ a0,
+                                                                         const double* __restrict__ a1,
+                                                                         std::size_t nPer, double* partial) {
+    const std::size_t off = blockIdx.y * nPer;
+    double m = 0.0;
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nPer; i += stride) {
+        m = fmax(m, fabs(a0[off + i]));
+        if (a1) m = fmax(m, fabs(a1[off + i]));
+    }
+    __shared__ double r[kReduceThreads / 32];
+    m = warpMax(m);
+    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kReduceThreads / 32; ++w) t = fmax(t, r[w]);
+        partial[blockIdx.y * 2 * kReduceBlocks + blockIdx.x] = t;
     }
 }
 
@@ -400,6 +461,50 @@ void launchMaxFinal(Ctx& ctx, const double* partials, int nb, double scale, doub
         k_max_final<<<1, 1024, 0, ctx.stream>>>(partials, nb, scale, out);
     }
     VRG_LAUNCH_CHECK();
+}
+
+double* launchDotPairs(Ctx& ctx, const GridDims& g, const double* a0, const double* b0, const double* a1,
+                       const double* b1, double scale, int slot) {
+    const std::size_t n = g.pointsPer();
+    const int P = g.pairs;
+    double* partial = ctx.scratchBuf(200, sizeof(double) * 2 * kReduceBlocks * P);
+    double* out = ctx.scratchBuf(201 + slot, sizeof(double) * P);
+    const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
+    {
+        LaunchScope ls_(ctx, "k_dot_partial");
+        k_dot_partial_pairs<<<dim3(nb, P), kReduceThreads, 0, ctx.stream>>>(a0, b0, a1, b1, n, partial);
+    }
+    VRG_LAUNCH_CHECK();
+    {
+        LaunchScope ls_(ctx, "k_dot_final");
+        k_dot_final<<<P, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
+    }
+    VRG_LAUNCH_CHECK();
+    return out;
+}
+
+double* launchMaxAbsPairs(Ctx& ctx, const GridDims& g, const double* a0, const double* a1, int slot) {
+    const std::size_t n = g.pointsPer();
+    const int P = g.pairs;
+    double* partial = ctx.scratchBuf(200, sizeof(double) * 2 * kReduceBlocks * P);
+    double* out = ctx.scratchBuf(201 + slot, sizeof(double) * P);
+    const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
+    {
+        LaunchScope ls_(ctx, "k_maxabs_partial");
+        k_maxabs_partial_pairs<<<dim3(nb, P), kReduceThreads, 0, ctx.stream>>>(a0, a1, n, partial);
+    }
+    VRG_LAUNCH_CHECK();
+    {
+        LaunchScope ls_(ctx, "k_max_final");
+        k_max_final<<<P, 1024, 0, ctx.stream>>>(partial, nb, 1.0, out);
+    }
+    VRG_LAUNCH_CHECK();
+    return out;
+}
+
+void readPairs(Ctx& ctx, const double* dev, int P, double* host) {
+    VRG_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
 }
 
 double readScalar(Ctx& ctx, const double* dev) {

@@ -20,12 +20,14 @@ __device__ __forceinline__ cplx cmulI(double k, cplx v) { return make_double2(-k
 __device__ __forceinline__ cplx cscale(cplx v, double a) { return make_double2(v.x * a, v.y * a); }
 
 __global__ void k_grad(const cplx* __restrict__ s, cplx* __restrict__ o1, cplx* __restrict__ o2, int n1, int n2,
-                       double scale) {
+                       int pairs, double scale) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const cplx v = s[i];
     o1[i] = cscale(cmulI(waveNyq0(r, n1), v), scale);
     o2[i] = cscale(cmulI(waveNyq0(c, n2), v), scale);
@@ -33,45 +35,53 @@ __global__ void k_grad(const cplx* __restrict__ s, cplx* __restrict__ o1, cplx* 
 
 // k_grad over a batch of spectra (blockIdx.y = field): field f's gradient spectra at
 // o + 2f*NS (axis 0) and o + (2f+1)*NS (axis 1), the [g1 | g2] layout of a gradient trajectory.
-__global__ void k_grad_batch(const cplx* __restrict__ s, cplx* __restrict__ o, int n1, int n2, double scale) {
+__global__ void k_grad_batch(const cplx* __restrict__ s, cplx* __restrict__ o, int n1, int n2, int pairs,
+                             double scale) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;  // one field of the batch (all pairs)
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const std::size_t f = blockIdx.y;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const cplx v = s[f * n + i];
     o[2 * f * n + i] = cscale(cmulI(waveNyq0(r, n1), v), scale);
     o[(2 * f + 1) * n + i] = cscale(cmulI(waveNyq0(c, n2), v), scale);
 }
 
 __global__ void k_div(const cplx* __restrict__ s1, const cplx* __restrict__ s2, cplx* __restrict__ o, int n1, int n2,
-                      double scale) {
+                      int pairs, double scale) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const cplx a = cmulI(waveNyq0(r, n1), s1[i]);
     const cplx b = cmulI(waveNyq0(c, n2), s2[i]);
     o[i] = cscale(make_double2(a.x + b.x, a.y + b.y), scale);
 }
 
 // applyHelmholtz symbol 1 + k1^2 + k2^2 with Nyquist-zeroed waves (spectral.cpp:214-223)
-__global__ void k_helm(cplx* s, int n1, int n2, double scale) {
+__global__ void k_helm(cplx* s, int n1, int n2, int pairs, double scale) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const double k1 = waveNyq0(r, n1), k2 = waveNyq0(c, n2);
     s[i] = cscale(s[i], (1.0 + k1 * k1 + k2 * k2) * scale);
 }
 
-__global__ void k_scale(cplx* s, std::size_t n, int nf, const double* __restrict__ sym, double scale) {
+__global__ void k_scale(cplx* s, std::size_t n, std::size_t nPer, int nf, const double* __restrict__ sym,
+                        double scale) {
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double m = sym ? sym[i] * scale : scale;
+    const double m = sym ? sym[i % nPer] * scale : scale;
     for (int f = 0; f < nf; ++f) s[f * n + i] = cscale(s[f * n + i], m);
 }
 
@@ -84,12 +94,14 @@ __device__ __forceinline__ void leray(int r, int c, int n1, int n2, cplx& s1, cp
     s2 = make_double2(s2.x - k2 * kdotb.x / ksq, s2.y - k2 * kdotb.y / ksq);
 }
 
-__global__ void k_leray(cplx* s1, cplx* s2, int n1, int n2) {
+__global__ void k_leray(cplx* s1, cplx* s2, int n1, int n2, int pairs) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     cplx a = s1[i], b = s2[i];
     leray(r, c, n1, n2, a, b);
     s1[i] = a;
@@ -98,18 +110,20 @@ __global__ void k_leray(cplx* s1, cplx* s2, int n1, int n2) {
 
 __global__ void k_combine(const cplx* __restrict__ b1, const cplx* __restrict__ b2, const cplx* __restrict__ a1,
                           const cplx* __restrict__ a2, const double* __restrict__ sym, bool doLeray, double scale,
-                          cplx* o1, cplx* o2, int n1, int n2) {
+                          cplx* o1, cplx* o2, int n1, int n2, int pairs) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const std::size_t li = i % nPer;
     cplx x = b1[i], y = b2[i];
     if (doLeray) {
-        const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+        const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
         leray(r, c, n1, n2, x, y);
     }
     if (sym) {
-        const double m = sym[i];
+        const double m = sym[li];
         x = cscale(x, m);
         y = cscale(y, m);
     }
@@ -123,12 +137,15 @@ __global__ void k_combine(const cplx* __restrict__ b1, const cplx* __restrict__ 
 
 // spectral::resample (src/spectral.cpp:157-179) from source spectrum to target spectrum.
 __global__ void k_resample(const cplx* __restrict__ s, int sn1, int sn2, cplx* __restrict__ t, int tn1, int tn2,
-                           double amp, double scale) {
+                           int pairs, double amp, double scale) {
     const int tc = tn2 / 2 + 1, sc = sn2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(tn1) * tc;
+    const std::size_t nPer = static_cast<std::size_t>(tn1) * tc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int rt = static_cast<int>(i / tc), c = static_cast<int>(i - static_cast<std::size_t>(rt) * tc);
+    const std::size_t pair = i / nPer, li = i - pair * nPer;
+    s += pair * static_cast<std::size_t>(sn1) * sc;
+    const int rt = static_cast<int>(li / tc), c = static_cast<int>(li - static_cast<std::size_t>(rt) * tc);
     const int band1 = min(sn1, tn1) / 2, band2 = min(sn2, tn2) / 2;
     const int k1 = waveOf(rt, tn1), k2 = waveOf(c, tn2);
     cplx v = make_double2(0.0, 0.0);
@@ -140,12 +157,14 @@ __global__ void k_resample(const cplx* __restrict__ s, int sn1, int sn2, cplx* _
 }
 
 // spectral::cutoffFilter (src/spectral.cpp:188-203): both bands from one spectrum.
-__global__ void k_cutoff(const cplx* __restrict__ s, cplx* lo, cplx* hi, int n1, int n2, double scale) {
+__global__ void k_cutoff(const cplx* __restrict__ s, cplx* lo, cplx* hi, int n1, int n2, int pairs, double scale) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const bool low = abs(waveOf(r, n1)) < n1 / 4 && abs(waveOf(c, n2)) < n2 / 4;
     const cplx v = cscale(s[i], scale);
     const cplx z = make_double2(0.0, 0.0);
@@ -153,12 +172,14 @@ __global__ void k_cutoff(const cplx* __restrict__ s, cplx* lo, cplx* hi, int n1,
     if (hi) hi[i] = low ? z : v;
 }
 
-__global__ void k_gauss(cplx* s, int n1, int n2, double s1, double s2, double scale) {
+__global__ void k_gauss(cplx* s, int n1, int n2, int pairs, double s1, double s2, double scale) {
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const double k1 = waveOf(r, n1), k2 = waveOf(c, n2);
     s[i] = cscale(s[i], exp(-0.5 * (k1 * k1 * s1 * s1 + k2 * k2 * s2 * s2)) * scale);
 }
@@ -177,11 +198,14 @@ namespace {
 // use the device pow (<= 2 ulp).  At 4096^2 the host loop with std::pow took ~0.2 s per symbol.
 __global__ void k_weight_symbol(double* __restrict__ out, int n1, int n2, int order, int kind, double beta,
                                 double power) {
+    constexpr int pairs = 1;  // one pair's symbol table
     const int nc = n2 / 2 + 1;
-    const std::size_t n = static_cast<std::size_t>(n1) * nc;
+    const std::size_t nPer = static_cast<std::size_t>(n1) * nc;
+    const std::size_t n = nPer * pairs;
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int r = static_cast<int>(i / nc), c = static_cast<int>(i - static_cast<std::size_t>(r) * nc);
+    const std::size_t li = i % nPer;  // mode of the pair's spectrum (stacked pairs)
+    const int r = static_cast<int>(li / nc), c = static_cast<int>(li - static_cast<std::size_t>(r) * nc);
     const double k1 = r <= n1 / 2 ? r : r - n1;
     const double k2 = c <= n2 / 2 ? c : c - n2;
     const double ksq = __dadd_rn(__dmul_rn(k1, k1), __dmul_rn(k2, k2));
@@ -205,7 +229,7 @@ __global__ void k_weight_symbol(double* __restrict__ out, int n1, int n2, int or
 }
 }  // namespace
 
-Weights::Weights(const GridDims& gd, int nrm) : g(gd), norm(nrm) {}
+Weights::Weights(const GridDims& gd, int nrm) : g(gd.one()), norm(nrm) {}  // one pair's symbols
 
 const double* Weights::makeSymbol(int kind, double beta, double power, DBuf& b) {
     const int order = norm == kH1 ? 1 : norm == kH3 ? 3 : 2;
@@ -275,7 +299,8 @@ void gradient(Ctx& ctx, const GridDims& g, const double* u, double* g1, double* 
     fftForward(ctx, g, u, s, 1);
     {
         LaunchScope ls_(ctx, "k_grad");
-        k_grad<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, o, o + g.specPoints(), g.n1, g.n2, 1.0 / g.points());
+        k_grad<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, o, o + g.specPoints(), g.n1, g.n2, g.pairs,
+                                                            1.0 / g.pointsPer());
     }
     VRG_LAUNCH_CHECK();
     fftInverse2(ctx, g, o, g1, g2);
@@ -300,7 +325,7 @@ void gradientBatch(Ctx& ctx, const GridDims& g, const double* u, int count, doub
         {
             LaunchScope ls_(ctx, "k_grad");
             const dim3 grid(specGrid(g).x, c);
-            k_grad_batch<<<grid, kSpecBlock, 0, ctx.stream>>>(s, o, g.n1, g.n2, 1.0 / N);
+            k_grad_batch<<<grid, kSpecBlock, 0, ctx.stream>>>(s, o, g.n1, g.n2, g.pairs, 1.0 / g.pointsPer());
         }
         VRG_LAUNCH_CHECK();
         fftInverse(ctx, g, o, G + 2 * f0 * N, 2 * c);
@@ -315,7 +340,8 @@ void divergence(Ctx& ctx, const GridDims& g, const double* v1, const double* v2,
     fftForward2(ctx, g, v1, v2, s);
     {
         LaunchScope ls_(ctx, "k_div");
-        k_div<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, s + g.specPoints(), o, g.n1, g.n2, 1.0 / g.points());
+        k_div<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, s + g.specPoints(), o, g.n1, g.n2, g.pairs,
+                                                           1.0 / g.pointsPer());
     }
     VRG_LAUNCH_CHECK();
     fftInverse(ctx, g, o, out, 1);
@@ -326,7 +352,7 @@ void applyRealSymbol(Ctx& ctx, const GridDims& g, const double* v1, const double
                      const double* sym) {
     cplx* s = specScratch(ctx, g, 1, 2);
     fftForward2(ctx, g, v1, v2, s);
-    specScale(ctx, g, s, 2, sym, 1.0 / g.points());
+    specScale(ctx, g, s, 2, sym, 1.0 / g.pointsPer());
     fftInverse2(ctx, g, s, o1, o2);
     ctx.ffts += 4;
 }
@@ -336,7 +362,7 @@ void applyHelmholtz(Ctx& ctx, const GridDims& g, const double* u, double* out) {
     fftForward(ctx, g, u, s, 1);
     {
         LaunchScope ls_(ctx, "k_helm");
-        k_helm<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.n1, g.n2, 1.0 / g.points());
+        k_helm<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.n1, g.n2, g.pairs, 1.0 / g.pointsPer());
     }
     VRG_LAUNCH_CHECK();
     fftInverse(ctx, g, s, out, 1);
@@ -367,15 +393,16 @@ void projectDivFree(Ctx& ctx, const GridDims& g, const double* b1, const double*
     fftForward2(ctx, g, b1, b2, s);
     {
         LaunchScope ls_(ctx, "k_leray");
-        k_leray<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, s + g.specPoints(), g.n1, g.n2);
+        k_leray<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, s + g.specPoints(), g.n1, g.n2, g.pairs);
     }
     VRG_LAUNCH_CHECK();
-    specScale(ctx, g, s, 2, nullptr, 1.0 / g.points());
+    specScale(ctx, g, s, 2, nullptr, 1.0 / g.pointsPer());
     fftInverse2(ctx, g, s, o1, o2);
     ctx.ffts += 4;
 }
 
 void resample(Ctx& ctx, const GridDims& src, const double* u, const GridDims& dst, double* out) {
+    if (src.pairs != dst.pairs) throw InvalidArgument("resample: source and target batches differ");
     if (src == dst) {
         if (out != u) VRG_CUDA(cudaMemcpyAsync(out, u, sizeof(double) * src.points(), cudaMemcpyDeviceToDevice, ctx.stream));
         return;
@@ -386,8 +413,8 @@ void resample(Ctx& ctx, const GridDims& src, const double* u, const GridDims& ds
     const double amp = static_cast<double>(dst.points()) / static_cast<double>(src.points());
     {
         LaunchScope ls_(ctx, "k_resample");
-        k_resample<<<specGrid(dst), kSpecBlock, 0, ctx.stream>>>(s, src.n1, src.n2, t, dst.n1, dst.n2, amp,
-                                                                 1.0 / dst.points());
+        k_resample<<<specGrid(dst), kSpecBlock, 0, ctx.stream>>>(s, src.n1, src.n2, t, dst.n1, dst.n2, dst.pairs, amp,
+                                                                 1.0 / dst.pointsPer());
     }
     VRG_LAUNCH_CHECK();
     fftInverse(ctx, dst, t, out, 1);
@@ -401,7 +428,7 @@ void cutoff(Ctx& ctx, const GridDims& g, const double* u, double* low, double* h
     {
         LaunchScope ls_(ctx, "k_cutoff");
         k_cutoff<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, low ? o : nullptr, high ? o + g.specPoints() : nullptr,
-                                                             g.n1, g.n2, 1.0 / g.points());
+                                                             g.n1, g.n2, g.pairs, 1.0 / g.pointsPer());
     }
     VRG_LAUNCH_CHECK();
     if (low) fftInverse(ctx, g, o, low, 1);
@@ -414,8 +441,8 @@ void gaussianSmooth(Ctx& ctx, const GridDims& g, const double* u, double sigma, 
     fftForward(ctx, g, u, s, 1);
     {
         LaunchScope ls_(ctx, "k_gauss");
-        k_gauss<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.n1, g.n2, sigma * g.h1(), sigma * g.h2(),
-                                                            1.0 / g.points());
+        k_gauss<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.n1, g.n2, g.pairs, sigma * g.h1(), sigma * g.h2(),
+                                                            1.0 / g.pointsPer());
     }
     VRG_LAUNCH_CHECK();
     fftInverse(ctx, g, s, out, 1);
@@ -425,7 +452,7 @@ void gaussianSmooth(Ctx& ctx, const GridDims& g, const double* u, double sigma, 
 void specScale(Ctx& ctx, const GridDims& g, cplx* s, int nf, const double* sym, double scale) {
     {
         LaunchScope ls_(ctx, "k_scale");
-        k_scale<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.specPoints(), nf, sym, scale);
+        k_scale<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s, g.specPoints(), g.specPer(), nf, sym, scale);
     }
     VRG_LAUNCH_CHECK();
 }
@@ -433,7 +460,7 @@ void specScale(Ctx& ctx, const GridDims& g, cplx* s, int nf, const double* sym, 
 void specLeray(Ctx& ctx, const GridDims& g, cplx* s1, cplx* s2) {
     {
         LaunchScope ls_(ctx, "k_leray");
-        k_leray<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s1, s2, g.n1, g.n2);
+        k_leray<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(s1, s2, g.n1, g.n2, g.pairs);
     }
     VRG_LAUNCH_CHECK();
 }
@@ -442,7 +469,8 @@ void specCombine(Ctx& ctx, const GridDims& g, const cplx* b1, const cplx* b2, co
                  const double* sym, bool doLeray, double scale, cplx* o1, cplx* o2) {
     {
         LaunchScope ls_(ctx, "k_combine");
-        k_combine<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(b1, b2, a1, a2, sym, doLeray, scale, o1, o2, g.n1, g.n2);
+        k_combine<<<specGrid(g), kSpecBlock, 0, ctx.stream>>>(b1, b2, a1, a2, sym, doLeray, scale, o1, o2, g.n1, g.n2,
+                                                               g.pairs);
     }
     VRG_LAUNCH_CHECK();
 }

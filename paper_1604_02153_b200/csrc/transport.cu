@@ -16,12 +16,13 @@ namespace vrg {
 namespace {
 
 // Star points x* = x - sgn*ht*v (src/transport.cpp:73-74), no FMA.
-__global__ void k_star(const double* __restrict__ v1, const double* __restrict__ v2, int n1, int n2, double h1,
-                       double h2, double sgnHt, double* x1, double* x2) {
-    const std::size_t N = static_cast<std::size_t>(n1) * n2;
+__global__ void k_star(const double* __restrict__ v1, const double* __restrict__ v2, int n1, int n2, int pairs,
+                       double h1, double h2, double sgnHt, double* x1, double* x2) {
+    const std::size_t N = static_cast<std::size_t>(n1) * n2 * pairs;
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p >= N) return;
-    const int i1 = static_cast<int>(p / n2), i2 = static_cast<int>(p - static_cast<std::size_t>(i1) * n2);
+    const std::size_t row = p / n2;
+    const int i1 = static_cast<int>(row % n1), i2 = static_cast<int>(p - row * n2);
     const double c1 = __dadd_rn(-kPi, __dmul_rn(h1, static_cast<double>(i1)));
     const double c2 = __dadd_rn(-kPi, __dmul_rn(h2, static_cast<double>(i2)));
     x1[p] = __dsub_rn(c1, __dmul_rn(sgnHt, v1[p]));
@@ -29,7 +30,8 @@ __global__ void k_star(const double* __restrict__ v1, const double* __restrict__
 }
 
 // Block maxima of |field| into guard partials (same block layout as k_evaluate).
-__global__ void __launch_bounds__(kEvalBlock) k_fieldmax(const double* __restrict__ f, std::size_t N, double* partial) {
+__global__ void __launch_bounds__(kEvalBlock) k_fieldmax(const double* __restrict__ f, std::size_t N, double* partial,
+                                                         unsigned blocksPer, unsigned gE) {
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     double g = 0.0;
     if (p < N) g = fmax(0.0, fabs(f[p]));
@@ -40,14 +42,16 @@ __global__ void __launch_bounds__(kEvalBlock) k_fieldmax(const double* __restric
     if (threadIdx.x == 0) {
         double m = red[0];
         for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
-        partial[blockIdx.x] = m;
+        partial[guardEntry(blockIdx.x, blocksPer, gE)] = m;
     }
 }
 
-__global__ void k_stepmax(const double* partials, unsigned blocks, double* out) {
-    const double* p = partials + static_cast<std::size_t>(blockIdx.x) * blocks;
+// Per (step, pair) maximum of the guard partials: block = step * pairs + pair reduces the
+// pair's `per` entries (blocks per step = pairs * per).
+__global__ void k_stepmax(const double* partials, unsigned per, double* out) {
+    const double* p = partials + static_cast<std::size_t>(blockIdx.x) * per;
     double m = 0.0;
-    for (unsigned i = threadIdx.x; i < blocks; i += blockDim.x) m = fmax(m, p[i]);
+    for (unsigned i = threadIdx.x; i < per; i += blockDim.x) m = fmax(m, p[i]);
     __shared__ double red[32];
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -69,18 +73,25 @@ __global__ void k_ones(std::size_t N, double* y) {
 void launchFieldMax(Ctx& ctx, const GridDims& g, const double* f, double* partial) {
     {
         LaunchScope ls_(ctx, "k_fieldmax");
-        k_fieldmax<<<evalBlocks(g), kEvalBlock, 0, ctx.stream>>>(f, g.points(), partial);
+        k_fieldmax<<<evalBlocks(g), kEvalBlock, 0, ctx.stream>>>(f, g.points(), partial, evalBlocksPer(g),
+                                                                 guardStride(g));
     }
     VRG_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------------------------ guard log
-void GuardLog::ensure(int nsteps, unsigned nblocks) {
-    if (nsteps <= steps && nblocks == blocks) return;
+thread_local bool g_collectGuards = false;
+
+void GuardLog::ensure(int nsteps, const GridDims& g) {
+    const unsigned nblocks = guardBlocks(g);
+    if (nsteps <= steps && nblocks == blocks && g.pairs == pairs) return;
+    if (g.pairs > 1 && g.pointsPer() % kEvalBlock != 0)
+        throw NotSupported("batched pairs: n1 * n2 must be a multiple of 256");
     steps = nsteps;
     blocks = nblocks;
+    pairs = g.pairs;
     partials.alloc(sizeof(double) * static_cast<std::size_t>(steps) * blocks);
-    stepMax.alloc(sizeof(double) * steps);
+    stepMax.alloc(sizeof(double) * steps * pairs);
     flags.alloc(sizeof(unsigned) * steps);
 }
 
@@ -93,18 +104,42 @@ void GuardLog::reset(Ctx& ctx) {
 void GuardLog::finalize(Ctx& ctx) {
     {
         LaunchScope ls_(ctx, "k_stepmax");
-        k_stepmax<<<steps, 256, 0, ctx.stream>>>(partials.d(), blocks, stepMax.d());
+        k_stepmax<<<steps * pairs, 256, 0, ctx.stream>>>(partials.d(), blocks / pairs, stepMax.d());
     }
     VRG_LAUNCH_CHECK();
 }
 
 void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep) {
-    std::vector<double> mx(nt + 1);
+    std::vector<double> mx(static_cast<std::size_t>(nt + 1) * pairs);
     std::vector<unsigned> fl(nt + 1);
-    VRG_CUDA(cudaMemcpyAsync(mx.data(), stepMax.d(), sizeof(double) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
+    VRG_CUDA(cudaMemcpyAsync(mx.data(), stepMax.d(), sizeof(double) * mx.size(), cudaMemcpyDeviceToHost, ctx.stream));
     VRG_CUDA(cudaMemcpyAsync(fl.data(), flags.d(), sizeof(unsigned) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
-    checkHost(mx.data(), fl.data(), eq, nt, forward, guard, thresholdStep);
+    if (pairs == 1 && !g_collectGuards) {
+        checkHost(mx.data(), fl.data(), eq, nt, forward, guard, thresholdStep);
+        return;
+    }
+    // a batch: every pair's verdict, nothing thrown (the non-finite flag is shared by the batch)
+    pairStatus.assign(pairs, 0);
+    pairError.assign(pairs, std::string());
+    std::vector<double> m1(nt + 1);
+    for (int k = 0; k < pairs; ++k) {
+        for (int s = 0; s <= nt; ++s) m1[s] = mx[static_cast<std::size_t>(s) * pairs + k];
+        try {
+            checkHost(m1.data(), fl.data(), eq, nt, forward, guard, thresholdStep);
+        } catch (const BlowupError& e) {
+            pairStatus[k] = kBlowup;
+            pairError[k] = e.what();
+        } catch (const InvalidArgument& e) {
+            pairStatus[k] = kInvalidArgument;
+            pairError[k] = e.what();
+        }
+    }
+    if (!g_collectGuards)  // a batched operator used on its own: the first pair's error throws
+        for (int k = 0; k < pairs; ++k) {
+            if (pairStatus[k] == kBlowup) throw BlowupError(pairError[k]);
+            if (pairStatus[k]) throw InvalidArgument(pairError[k]);
+        }
 }
 
 void GuardLog::checkHost(const double* mx, const unsigned* fl, const char* eq, int nt, bool forward, bool guard,
@@ -141,10 +176,11 @@ void launchTrace(Ctx& ctx, const GridDims& g, const double* v1, const double* v2
     double* s2 = ctx.scratchBuf(11, sizeof(double) * g.points());
     {
         LaunchScope ls_(ctx, "k_star");
-        k_star<<<grid1d(g.points(), 256), 256, 0, ctx.stream>>>(v1, v2, g.n1, g.n2, g.h1(), g.h2(), sgn * ht, s1, s2);
+        k_star<<<grid1d(g.points(), 256), 256, 0, ctx.stream>>>(v1, v2, g.n1, g.n2, g.pairs, g.h1(), g.h2(), sgn * ht,
+                                                                s1, s2);
     }
     VRG_LAUNCH_CHECK();
-    EpiTrace epi{nullptr, v1, v2, x1, x2, g.n2, g.h1(), g.h2(), sgn * 0.5 * ht};
+    EpiTrace epi{nullptr, v1, v2, x1, x2, g.n1, g.n2, g.h1(), g.h2(), sgn * 0.5 * ht};
     launchEvaluate<2>(ctx, g, CoeffSet<2>{{cv1, cv2}}, s1, s2, epi);
 }
 
@@ -157,9 +193,9 @@ Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2,
     copy(ctx, g.points(), vv1, v.d());
     copy(ctx, g.points(), vv2, v.d() + g.points());
     if (anyNonFinite(ctx, 2 * g.points(), v.d())) throw InvalidArgument("transport velocity: non-finite value");
-    coef_.alloc(sizeof(double) * paddedPoints(g.n1, g.n2));
+    coef_.alloc(sizeof(double) * paddedTotal(g));
     tmp_.alloc(sizeof(double) * 2 * g.points());
-    log.ensure(nt + 1, guardBlocks(g));
+    log.ensure(nt + 1, g);
 }
 
 // Band path for the SL time loops (evalband.cuh) wherever the grid allows it: each step is the
@@ -173,13 +209,13 @@ double* Solver::tmp() { return tmp_.d(); }
 const double* Solver::departure(int dir) {
     if (!haveX_[dir]) {
         if (!haveCv_) {
-            cv_.alloc(sizeof(double) * 2 * paddedPoints(g.n1, g.n2));
-            launchPrefilter(ctx, g, v1(), cv_.d(), tmp_.d(), nullptr);
-            launchPrefilter(ctx, g, v2(), cv_.d() + paddedPoints(g.n1, g.n2), tmp_.d(), nullptr);
+            // both components in one batch (v is contiguous [v1 | v2])
+            cv_.alloc(sizeof(double) * 2 * paddedTotal(g));
+            launchPrefilterBatch(ctx, g, v1(), g.points(), 2, cv_.d(), paddedTotal(g), tmp_.d(), nullptr);
             haveCv_ = true;
         }
         X_[dir].alloc(sizeof(double) * 2 * g.points());
-        launchTrace(ctx, g, v1(), v2(), cv_.d(), cv_.d() + paddedPoints(g.n1, g.n2), ht, dir, X_[dir].d(),
+        launchTrace(ctx, g, v1(), v2(), cv_.d(), cv_.d() + paddedTotal(g), ht, dir, X_[dir].d(),
                     X_[dir].d() + g.points());
         ctx.interps += 2;  // traceCharacteristics evaluates both components (transport.cpp:77-78)
         haveX_[dir] = true;
@@ -352,7 +388,7 @@ void Solver::incState(const double* vt1, const double* vt2, const double* stateT
     double* gPrev = vtD + 2 * N;     // grad m_{j-1}
     double* gCur = gPrev + 2 * N;    // grad m_j
     double* gD = gCur + 2 * N;       // (grad m_{j-1})_D
-    double* c2 = ctx.scratchBuf(13, sizeof(double) * paddedPoints(g.n1, g.n2));
+    double* c2 = ctx.scratchBuf(13, sizeof(double) * paddedTotal(g));
     launchPrefilter(ctx, g, vt1, coef_.d(), tmp_.d(), nullptr);
     launchPrefilter(ctx, g, vt2, c2, tmp_.d(), nullptr);
     launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef_.d(), c2}}, X, X + N, EpiStore2{nullptr, vtD, vtD + N}, true);

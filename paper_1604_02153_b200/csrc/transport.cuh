@@ -3,6 +3,9 @@
 // of scope and raise NotSupported at the C ABI.
 #pragma once
 
+#include <string>
+#include <vector>
+
 #include "blas.cuh"
 #include "eval.cuh"
 #include "spectral.cuh"
@@ -24,13 +27,28 @@ void launchFieldMax(Ctx& ctx, const GridDims& g, const double* f, double* partia
 
 // Per-step guard bookkeeping for one solve: block maxima per step, reduced per step, plus the
 // prefilter non-finite flags, read back once when the solve ends.
+// Batched solves (batch.cu) collect every pair's guard verdict instead of throwing, whatever
+// the number of pairs of an operator (a coarse group can hold a single pair); set for the
+// duration of a batched solve on the calling thread.
+extern thread_local bool g_collectGuards;
+struct CollectGuardsScope {
+    bool prev;
+    explicit CollectGuardsScope(bool on = true) : prev(g_collectGuards) { g_collectGuards = on; }
+    ~CollectGuardsScope() { g_collectGuards = prev; }
+};
+
 struct GuardLog {
     int steps = 0;        // number of step slots (nt+1)
-    unsigned blocks = 0;  // evaluate blocks per step
+    unsigned blocks = 0;  // guard partials per step (pairs * guardStride)
+    int pairs = 1;
     DBuf partials;        // steps*blocks
-    DBuf stepMax;         // steps doubles
+    DBuf stepMax;         // steps x pairs doubles
     DBuf flags;           // steps unsigned
-    void ensure(int nsteps, unsigned nblocks);
+    // batch (pairs > 1): check() records each pair's verdict instead of throwing (0 ok, else the
+    // C ABI status of the error the reference would throw) and its message
+    std::vector<int> pairStatus;
+    std::vector<std::string> pairError;
+    void ensure(int nsteps, const GridDims& g);
     double* partial(int step) const { return partials.d() + static_cast<std::size_t>(step) * blocks; }
     unsigned* flag(int step) const { return flags.as<unsigned>() + step; }
     void reset(Ctx& ctx);
