@@ -4,8 +4,10 @@ One process per GPU (torchrun).  The pairs are independent, so each rank takes a
 shard and there is no data-path collective: rank r solves pairs r, r+W, r+2W, ...  Only the
 small per-pair reports are gathered (all_gather_object) at the end.  `scaling` is weak.
 
-Within a GPU, `--lanes L` runs L solves at once: L host threads, each with its own library
-context and stream, take the rank's pairs from a shared queue.  A solve at 256^2 launches
+Within a GPU, `--batch B` solves B pairs together in lockstep (api.newton_solve_batch: every
+step of the B registrations in the same kernel launches, csrc/batch.cu), and `--lanes L` runs L
+solves (or batches) at once: L host threads, each with its own library context and stream,
+take the rank's pairs (or batches) from a shared queue.  A solve at 256^2 launches
 kernels too small to fill 148 SMs, so concurrent streams fill the device (config 5b).  The
 library's per-call state is per context (plans, graphs, scratch) or thread-local, and each
 newton_solve is a single C call that releases the GIL.
@@ -125,6 +127,33 @@ def registration_runner(ctx, n: int, nt: int, beta: float, norm: int, cheb_iters
     return run
 
 
+def batched_runner(ctx, n: int, nt: int, beta: float, norm: int, cheb_iters: int, tol_rel: float, images: dict,
+                   chunks: list[list[int]]):
+    """runner(c): the pairs chunks[c] solved together in lockstep (api.newton_solve_batch: one
+    launch per step for all of them, csrc/batch.cu); one result per pair under "pairs"."""
+    import numpy as np
+
+    from . import api
+
+    def run(c: int) -> dict:
+        ps = chunks[c]
+        mR = np.stack([images[p][0] for p in ps])
+        mT = np.stack([images[p][1] for p in ps])
+        t0 = time.perf_counter()
+        out = api.newton_solve_batch(ctx, mR, mT, norm, beta, api.COMPRESSIBLE, nt=nt, kind=api.PC_TWO_LEVEL,
+                                     coarse_solver=api.COARSE_CHEB, cheb_iters=cheb_iters, tol_rel=tol_rel)
+        dt = time.perf_counter() - t0
+        res = []
+        for p, (_, _, recs, summ) in zip(ps, out):
+            res.append({"item": p, "seconds": dt, "batch": len(ps), "newton_iterations": summ["iterations"],
+                        "inner_iterations": int(sum(r["innerIterations"] for r in recs)), "status": summ["status"],
+                        "error": summ["error"], "final_grad_rel": summ["finalGradNormRel"],
+                        "final_residual_rel": summ["finalResidualRel"]})
+        return {"pairs": res}
+
+    return run
+
+
 def _reference_batch(a, images, rank, world):
     """The same pairs through the reference's own newtonSolve on host threads (CPU baseline of
     configs 3/5b): one single-threaded solve per thread, threads in parallel (the reference's
@@ -162,6 +191,8 @@ def main():
     ap.add_argument("--cheb", type=int, default=10)
     ap.add_argument("--tol-rel", type=float, default=1e-2)
     ap.add_argument("--lanes", type=int, default=1, help="concurrent solves per GPU (own context + stream each)")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="pairs solved together in lockstep per solve (same kernel launches; 1 = one pair per solve)")
     ap.add_argument("--passes", type=int, default=1, help="passes over the pairs; the last one is reported")
     ap.add_argument("--impl", default="vrg", choices=["vrg", "reference"],
                     help="reference: the unmodified reference's newtonSolve (oracle/_ref) on --threads host threads")
@@ -189,19 +220,34 @@ def main():
     def make_runner(lane: int):
         return registration_runner(ctxs[lane], a.n, a.nt, a.beta, a.norm, a.cheb, a.tol_rel, images)
 
+    mine = shard(a.pairs, rank, world)
+    chunks = [mine[i:i + a.batch] for i in range(0, len(mine), max(1, a.batch))]
+
+    def make_batched(lane: int):
+        return batched_runner(ctxs[lane], a.n, a.nt, a.beta, a.norm, a.cheb, a.tol_rel, images, chunks)
+
     for _ in range(a.passes):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        res = run_sharded(a.pairs, None, rank, world, make_runner=make_runner, lanes=a.lanes)
+        if a.batch > 1:
+            part = [r for c in run_lanes(list(range(len(chunks))), make_batched, a.lanes) for r in c["pairs"]]
+            if world > 1:
+                gathered = [None] * world
+                torch.distributed.all_gather_object(gathered, part)
+                part = [r for g in gathered for r in g]
+            res = sorted(part, key=lambda r: r["item"]) if rank == 0 else None
+        else:
+            res = run_sharded(a.pairs, None, rank, world, make_runner=make_runner, lanes=a.lanes)
         wall = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([wall], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         wall = float(t.item())
     if rank == 0:
-        print(json.dumps({"pairs": a.pairs, "n": a.n, "nt": a.nt, "world": world, "lanes": a.lanes, "passes": a.passes, "wall_s": wall,
+        print(json.dumps({"pairs": a.pairs, "n": a.n, "nt": a.nt, "world": world, "lanes": a.lanes, "batch": a.batch,
+                          "passes": a.passes, "wall_s": wall,
                           "pairs_per_s": a.pairs / wall, "results": res}))
     if world > 1:
         torch.distributed.destroy_process_group()
