@@ -548,6 +548,48 @@ def time_to_solution(ctx, api, with_cpu):
     return out
 
 
+# Batched pairs (BASELINE configs 5b and 3) on this GPU: lanes of lockstep batches
+# (batch.py --lanes L --batch B; csrc/batch.cu), the second pass timed.
+BATCH_RUNS = {
+    "config5b_64pairs_256_nt16_H2_1e-3_2L-cheb10": dict(n=256, pairs=64, lanes=8, batch=8),
+    "config3_8pairs_512_nt16_H2_1e-3_2L-cheb10": dict(n=512, pairs=8, lanes=2, batch=4),
+}
+
+
+def batched_pairs(ctx, api):
+    import torch
+
+    from paper_1604_02153_b200 import batch
+
+    out = {}
+    for name, cfg in BATCH_RUNS.items():
+        n, nt = cfg["n"], 16
+        images = {p: batch.make_images(ctx, n, p, nt) for p in range(cfg["pairs"])}
+        ps = list(range(cfg["pairs"]))
+        chunks = [ps[i:i + cfg["batch"]] for i in range(0, len(ps), cfg["batch"])]
+        ctxs = [ctx] + [api.Context(0, stream=torch.cuda.Stream(0)) for _ in range(1, cfg["lanes"])]
+        walls = []
+        for _ in range(3):  # plans, graphs and the block cache of every lane warm after two passes
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = [r for c in batch.run_lanes(list(range(len(chunks))),
+                                              lambda lane: batch.batched_runner(ctxs[lane], n, nt, 1e-3, 2, 10, 1e-2,
+                                                                                images, chunks), cfg["lanes"])
+                   for r in c["pairs"]]
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        out[name] = {"pairs_per_s": cfg["pairs"] / walls[-1], "wall_s": walls[-1], "lanes": cfg["lanes"],
+                     "batch": cfg["batch"], "newton_iterations": sum(r["newton_iterations"] for r in res),
+                     "krylov_iterations": sum(r["inner_iterations"] for r in res),
+                     "status_counts": {str(s): sum(r["status"] == s for r in res) for s in sorted({r["status"] for r in res})},
+                     "errors": sum(r["error"] != 0 for r in res),
+                     "note": "pairs solved in lockstep batches (api.newton_solve_batch), batches on concurrent "
+                             "lanes; images made before the timed region; third pass timed; status 0 converged, "
+                             "1 the reference's 50-iteration cap"}
+        del ctxs[1:]
+    return out
+
+
 # ------------------------------------------------------------------------------ main
 def main():
     ap = argparse.ArgumentParser()
@@ -646,6 +688,8 @@ def main():
             line["cpu_baseline"] = cpu_baseline_leg()
         if not args.no_tts:
             line["time_to_solution"] = time_to_solution(r["ctx"], r["api"], world == 1 and not args.no_cpu_baseline)
+            if world == 1:
+                line["batched_pairs"] = batched_pairs(r["ctx"], r["api"])
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

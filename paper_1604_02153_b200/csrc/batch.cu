@@ -197,15 +197,42 @@ void copyPairs(Ctx& ctx, const double* src, int srcP, double* dst, int dstP, std
 
 // evaluateObjective / evaluateGradient (inverse.cpp:96-148) for a batch, compressible or
 // incompressible SL: per-pair scalars [objective, mismatch, regTerm, 0] and guard verdicts.
+// A pair whose velocity is not finite gets the status of the Solver's check (transport.cpp:
+// velocity validation) and is transported with v = 0 so that the other pairs go on.
+std::vector<int> saneVelocities(Ctx& ctx, const GridDims& g, const double*& v, DBuf& fixed) {
+    const auto bad = nonFinitePairs(ctx, g, 2, v);
+    std::vector<int> status(g.pairs, 0);
+    std::vector<std::pair<int, int>> keep;
+    bool any = false;
+    for (int k = 0; k < g.pairs; ++k) {
+        if (bad[k]) {
+            status[k] = kInvalidArgument;
+            any = true;
+        } else {
+            keep.push_back({k, k});
+        }
+    }
+    if (!any) return status;
+    fixed.alloc(sizeof(double) * 2 * g.points());
+    fill(ctx, 2 * g.points(), 0.0, fixed.d());
+    copyPairs(ctx, v, g.pairs, fixed.d(), g.pairs, g.pointsPer(), 2, keep);
+    v = fixed.d();
+    return status;
+}
+
 void evaluateObjectiveBatch(Ctx& ctx, const GridDims& g, const double* v, const double* mR, const double* mT,
                             const Model& model, int nt, std::vector<double>& scalars, double* st,
                             std::vector<int>& status) {
     const std::size_t N = g.points();
+    DBuf fixed;
+    const auto vst = saneVelocities(ctx, g, v, fixed);
     {
         Solver solver(ctx, g, v, v + N, nt);
         solver.state(mT, st, true);
         status = solver.log.pairStatus;
     }
+    for (int k = 0; k < g.pairs; ++k)
+        if (vst[k]) status[k] = vst[k];
     double* resid = ctx.scratchBuf(21, sizeof(double) * N);
     lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
     const auto mis = dotPairs(ctx, g, resid, resid, false);
@@ -228,13 +255,16 @@ void evaluateGradientBatch(Ctx& ctx, const GridDims& g, const double* v, const d
     const std::size_t N = g.points();
     double* b = ctx.scratchBuf(23, sizeof(double) * 2 * N);
     double* resid = ctx.scratchBuf(21, sizeof(double) * N);
-    status.assign(g.pairs, 0);
+    DBuf fixed;
+    status = saneVelocities(ctx, g, v, fixed);
+    const std::vector<int> vst = status;
     std::vector<double> mis;
     {
         Solver solver(ctx, g, v, v + N, nt);
         if (!reuseState) {
             solver.state(mT, st, true);
-            status = solver.log.pairStatus;
+            for (int k = 0; k < g.pairs; ++k)
+                if (!status[k]) status[k] = solver.log.pairStatus[k];
         }
         lincomb(ctx, N, 1.0, st + nt * N, -1.0, mR, resid);
         mis = dotPairs(ctx, g, resid, resid, false);
@@ -755,6 +785,7 @@ std::vector<SolverReport> newtonSolveBatch(Ctx& ctx, const GridDims& gAll, const
         // Armijo backtracking per pair (newton.cpp:109-131)
         std::vector<double> alpha(PA, 1.0);
         std::vector<char> searching = on, accepted(PA, 0);
+        copy(ctx, 2 * N, v, trialBuf.d());  // the pairs not searching evaluate their own iterate
         std::vector<int> lsSteps(PA, 0);
         std::vector<double> ones(PA, 1.0);
         for (int step = 0; step < cfg.lsMaxSteps; ++step) {

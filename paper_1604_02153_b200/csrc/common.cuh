@@ -71,7 +71,7 @@ void throwCufft(cufftResult r, const char* what, const char* file, int line);
 extern thread_local cudaStream_t g_allocStream;
 extern thread_local bool g_allocStreamSet;
 bool poolAllocations();  // VRG_POOL=0 disables the block cache
-void* cachedAlloc(std::size_t bytes, cudaStream_t s);
+void* cachedAlloc(std::size_t bytes, cudaStream_t s, std::size_t* got);  // got: the block's true size
 void cachedFree(void* p, std::size_t bytes, cudaStream_t s);
 void releaseCachedBlocks(cudaStream_t s);
 
@@ -83,16 +83,17 @@ public:
     ~DBuf() { release(); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr; o.bytes_ = 0; }
+    DBuf(DBuf&& o) noexcept : p_(o.p_), bytes_(o.bytes_), cap_(o.cap_) { o.p_ = nullptr; o.bytes_ = o.cap_ = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
-        if (this != &o) { release(); p_ = o.p_; bytes_ = o.bytes_; o.p_ = nullptr; o.bytes_ = 0; }
+        if (this != &o) { release(); p_ = o.p_; bytes_ = o.bytes_; cap_ = o.cap_; o.p_ = nullptr; o.bytes_ = o.cap_ = 0; }
         return *this;
     }
     void alloc(std::size_t bytes) {
         release();
+        cap_ = bytes;
         if (bytes) {
             if (g_allocStreamSet)
-                p_ = cachedAlloc(bytes, g_allocStream);
+                p_ = cachedAlloc(bytes, g_allocStream, &cap_);
             else
                 VRG_CUDA(cudaMalloc(&p_, bytes));
         }
@@ -101,12 +102,12 @@ public:
     void release() {
         if (p_) {
             if (g_allocStreamSet)
-                cachedFree(p_, bytes_, g_allocStream);
+                cachedFree(p_, cap_, g_allocStream);
             else
                 cudaFree(p_);
         }
         p_ = nullptr;
-        bytes_ = 0;
+        bytes_ = cap_ = 0;
     }
     template <typename T = double>
     T* as() const { return static_cast<T*>(p_); }
@@ -117,6 +118,7 @@ public:
 private:
     void* p_ = nullptr;
     std::size_t bytes_ = 0;
+    std::size_t cap_ = 0;  // size of the block behind p_ (>= bytes_ when it came from the cache)
 };
 
 // Sets the allocation stream for the duration of a library call (restores the previous one).

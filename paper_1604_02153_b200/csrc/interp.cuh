@@ -91,8 +91,10 @@ __device__ __forceinline__ int cellBase(double x, double invh, int n, double w[4
     const double s = __dadd_rn(xw, kPi) * invh;
     const double bf = floor(s);
     bsplineWeights(s - bf, w);
-    const int b = static_cast<int>(bf);  // in [0, n] for finite wrapped points
-    return b >= n ? b - n : (b < 0 ? 0 : b);
+    // in [0, n] for finite wrapped points; clamped so that no input (NaN, or a coordinate too
+    // large for the wrap to be exact) can address outside the padded field
+    const int b = static_cast<int>(fmin(fmax(bf, 0.0), static_cast<double>(n)));
+    return b >= n ? b - n : b;
 }
 
 constexpr std::size_t paddedPoints(int n1, int n2) {

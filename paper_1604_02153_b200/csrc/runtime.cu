@@ -46,18 +46,22 @@ BlockCache& blockCache() {
 constexpr std::size_t kCacheCap = std::size_t(48) << 30;  // beyond this, release for real
 }  // namespace
 
-void* cachedAlloc(std::size_t bytes, cudaStream_t s) {
+void* cachedAlloc(std::size_t bytes, cudaStream_t s, std::size_t* got) {
     BlockCache& c = blockCache();
     {
+        // best fit among the stream's blocks of bytes .. 2 x bytes (a batch that shrinks as its
+        // pairs finish reuses the larger blocks instead of allocating)
         std::lock_guard<std::mutex> lock(c.mu);
-        auto it = c.blocks.find({s, bytes});
-        if (it != c.blocks.end()) {
+        auto it = c.blocks.lower_bound({s, bytes});
+        if (it != c.blocks.end() && it->first.first == s && it->first.second <= 2 * bytes) {
             void* p = it->second;
+            *got = it->first.second;
+            c.held -= it->first.second;
             c.blocks.erase(it);
-            c.held -= bytes;
             return p;
         }
     }
+    *got = bytes;
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e == cudaErrorMemoryAllocation) {  // drop the cache and retry once
