@@ -32,6 +32,9 @@ inline bool bandFusable(const GridDims& g) {
     return tw && g.n2 >= 32 && g.n2 / kL <= tw;
 }
 
+// The SL time loops take the band path with packed departure cells (axes up to kCellMaxN).
+inline bool bandCellsFit(const GridDims& g) { return g.n1 <= kCellMaxN && g.n2 <= kCellMaxN; }
+
 // Doubles of shared memory one row needs (chunked row + chunk summaries + guard partials).
 __host__ __device__ inline int bandRowSmem(int n2, int tw) { return (n2 / kL) * (kCS + 3) + (tw + 31) / 32; }
 
@@ -48,11 +51,14 @@ inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n
 // body above it, which reads the coefficients before the predecessor column pass has written
 // them (seen in the SASS and as nondeterministic results under graph replay).  A coherent
 // load is ordered by the wait.
-__device__ __forceinline__ double ldAfterWait(const double* p) {
-    double v;
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    return v;
-}
+// (A plain coherent load: the compiler keeps it behind the wait's memory clobber and shares
+// the address arithmetic of the 16 taps, which an asm volatile load per tap did not.)
+__device__ __forceinline__ double ldAfterWait(const double* p) { return *p; }
+
+// First-tap row/column and weights of a departure point along one axis: from the coordinate
+// (slab windows, whose departure points are per call) or from its packed cell (interp.cuh).
+__device__ __forceinline__ int depCell(double x, double invh, int n, double w[4]) { return cellBase(x, invh, n, w); }
+__device__ __forceinline__ int depCell(Cell u, double, int, double w[4]) { return cellDecode(u, w); }
 
 // Coefficient window of a slab-decomposed grid (slab.py): the coefficients hold `rows` padded
 // rows, window row w = global grid row base + w (mod n1), instead of the whole periodically
@@ -98,9 +104,9 @@ struct BarNamed {
 // Stacked pairs (GridDims::pairs): r runs over all pairs' rows; row r belongs to pair r / n1,
 // whose coefficients lie pair * paddedPoints(n1, n2) further on, and its guard partial goes to
 // entry pair * gE + local row (guardStride).
-template <class Epi, bool kGather, bool kWindow, int TW, class Bar>
-__device__ __forceinline__ void bandRow(CoeffSet<1> cs, const double* __restrict__ x1,
-                                        const double* __restrict__ x2, int n1, int n2, const Epi& epi,
+template <class Epi, bool kGather, bool kWindow, int TW, class Bar, class Dep>
+__device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ x1,
+                                        const Dep* __restrict__ x2, int n1, int n2, const Epi& epi,
                                         double* __restrict__ rowOut, unsigned* nonfinite, const BandWindow& win,
                                         int r, int t, double* sm, Bar bar, unsigned gE) {
     if (!kGather) pdlWait();
@@ -138,7 +144,7 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const double* __restrict
     // bound).  The adjoint step's four prefetched operands would cost a resident block per SM
     // (78 registers), which measured slower, so it keeps the plain order.
     constexpr bool kPipe = sizeof(typename Epi::Pre) <= sizeof(double);
-    double xa = 0.0, xb = 0.0;
+    Dep xa{}, xb{};
     typename Epi::Pre pre{};
     if constexpr (kPipe) {
         if (kGather) {
@@ -156,8 +162,8 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const double* __restrict
         typename Epi::Pre cur;
         if constexpr (kPipe) {
             if (kGather) {
-                const int b1 = tapRow(cellBase(xa, inv1, n1, w1));
-                const int b2 = cellBase(xb, inv2, n2, w2);
+                const int b1 = tapRow(depCell(xa, inv1, n1, w1));
+                const int b2 = depCell(xb, inv2, n2, w2);
                 base = b1 * PW + b2;
             }
             cur = pre;
@@ -170,8 +176,8 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const double* __restrict
             }
         } else {
             if (kGather) {
-                const int b1 = tapRow(cellBase(__ldg(x1 + p), inv1, n1, w1));
-                const int b2 = cellBase(__ldg(x2 + p), inv2, n2, w2);
+                const int b1 = tapRow(depCell(__ldg(x1 + p), inv1, n1, w1));
+                const int b2 = depCell(__ldg(x2 + p), inv2, n2, w2);
                 base = b1 * PW + b2;
             }
             cur = epi.prefetch(p);
@@ -269,9 +275,11 @@ constexpr int bandMinBlocks() {
     return BandMinBlocks<Epi>::value * (kBandThreads / TW);
 }
 
-template <class Epi, bool kGather, bool kWindow = false, int TW = kBandThreads>
-__global__ void __launch_bounds__(TW, (bandMinBlocks<Epi, TW>())) k_eval_band(CoeffSet<1> cs, const double* __restrict__ x1,
-                                                            const double* __restrict__ x2, int n1, int n2, Epi epi,
+// Departure points as packed cells (Dep = Cell, the SL time loops) or coordinates (Dep = double,
+// slab windows).
+template <class Epi, bool kGather, bool kWindow = false, int TW = kBandThreads, class Dep = Cell>
+__global__ void __launch_bounds__(TW, (bandMinBlocks<Epi, TW>())) k_eval_band(CoeffSet<1> cs, const Dep* __restrict__ x1,
+                                                            const Dep* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
                                                             BandWindow win, unsigned gE) {
     extern __shared__ __align__(16) double sm[];
@@ -295,14 +303,16 @@ constexpr int stripWorkers() {
 
 template <class Epi, bool kGather, int TW>
 __global__ void __launch_bounds__(TW* stripWorkers<Epi, TW>(), 1)
-    k_eval_strip(CoeffSet<1> cs, const double* __restrict__ x1, const double* __restrict__ x2, int n1, int n2, Epi epi,
+    k_eval_strip(CoeffSet<1> cs, const Cell* __restrict__ x1, const Cell* __restrict__ x2, int n1, int n2, Epi epi,
                  double* __restrict__ rowOut, unsigned* nonfinite, int rows, unsigned gE) {
     extern __shared__ __align__(16) double sm[];
     constexpr int W = stripWorkers<Epi, TW>();
     const int w = threadIdx.x / TW;
     const int t = threadIdx.x - w * TW;
     const int r = blockIdx.x * W + w;
-    if (r < rows)
+    // r < rows is warp-uniform (TW is a multiple of 32); the vote tells the compiler so, which
+    // keeps the row's loads on uniform memory descriptors (no R2UR per tap)
+    if (__any_sync(0xffffffffu, r < rows))
         bandRow<Epi, kGather, false, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, BandWindow{}, r, t,
                                          sm + w * bandRowSmem(n2, TW), BarNamed<TW>{1 + w}, gE);
     pdlTrigger();
@@ -325,7 +335,7 @@ inline bool stripPath(const Ctx& ctx, const GridDims& g) {
 }
 
 template <class Epi, bool kGather, int TW>
-void launchEvalStrip(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x1, const double* x2, const Epi& epi,
+void launchEvalStrip(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const Cell* x1, const Cell* x2, const Epi& epi,
                      double* rowOut, unsigned* nonfinite) {
     constexpr int W = stripWorkers<Epi, TW>();
     constexpr int kThreads = W * TW;
@@ -346,7 +356,7 @@ void launchEvalStrip(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* 
 }
 
 template <class Epi, bool kGather>
-void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const double* x1, const double* x2, const Epi& epi,
+void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const Cell* x1, const Cell* x2, const Epi& epi,
                     double* rowOut, unsigned* nonfinite) {
     LaunchScope ls_(ctx, Epi::kName);
     if (stripPath(ctx, g)) {
@@ -382,7 +392,7 @@ void launchEvalBandWindow(Ctx& ctx, int n1, int L, int n2, CoeffSet<1> cs, const
     LaunchScope ls_(ctx, Epi::kName);
     const GridDims gl(L, n2);
     if (bandTW(n2) != kBandThreads) throw NotSupported("slab step: the row length must be a multiple of 256");
-    launchPdl(1, k_eval_band<Epi, kGather, true>, dim3(L), dim3(kBandThreads), bandSmem(gl), ctx.stream, cs, x1, x2,
+    launchPdl(1, k_eval_band<Epi, kGather, true, kBandThreads, double>, dim3(L), dim3(kBandThreads), bandSmem(gl), ctx.stream, cs, x1, x2,
               n1, n2, epi, rowOut, nonfinite, win, 0u);
 }
 

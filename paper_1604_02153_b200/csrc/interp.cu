@@ -694,4 +694,24 @@ void launchUnpad(Ctx& ctx, const GridDims& g, const double* padded, double* c) {
     VRG_LAUNCH_CHECK();
 }
 
+namespace {
+// Departure cells of N nodes (x1 = X[0..N), x2 = X[N..2N)): cells[p] / cells[N + p].
+__global__ void k_pack_cells(const double* __restrict__ X, std::size_t N, int n1, int n2, Cell* __restrict__ cells) {
+    const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    cells[p] = cellPack(X[p], n1 * (1.0 / kTwoPi), n1);
+    cells[N + p] = cellPack(X[N + p], n2 * (1.0 / kTwoPi), n2);
+}
+}  // namespace
+
+void launchPackCells(Ctx& ctx, const GridDims& g, const double* X, Cell* cells) {
+    if (g.n1 > kCellMaxN || g.n2 > kCellMaxN) throw NotSupported("departure cells: axis longer than 8192");
+    const std::size_t N = g.points();
+    {
+        LaunchScope ls_(ctx, "k_pack_cells");
+        k_pack_cells<<<static_cast<unsigned>((N + 255) / 256), 256, 0, ctx.stream>>>(X, N, g.n1, g.n2, cells);
+    }
+    VRG_LAUNCH_CHECK();
+}
+
 }  // namespace vrg

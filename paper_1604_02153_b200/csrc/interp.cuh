@@ -97,11 +97,50 @@ __device__ __forceinline__ int cellBase(double x, double invh, int n, double w[4
     return b >= n ? b - n : b;
 }
 
+// Departure cells: the per-iterate departure points of the SL time loops, reduced once to what
+// the gather needs.  One 64-bit word per node and axis: the padded-layout first-tap index b
+// (cellBase; 13 bits, axes up to kCellMaxN = 8192, the prefilter's own limit) above the
+// fractional offset s - floor(s) as a 51-bit fixed-point fraction.  s = (x_wrapped + pi)/h >= 2
+// has an ulp >= 2^-51, so there the fraction is stored exactly; below s = 2 (the first two
+// cells) it is rounded to 2^-51 (<= 2.2e-16 absolute on the weights).  Decoding costs four integer ops and one add instead of the wrap,
+// two floors, a float->int conversion and the clamps per axis (the band kernels are
+// issue-bound: profiles/r2s3_ncu_sl_step.md).
+using Cell = unsigned long long;
+constexpr int kCellMaxN = 8192;
+
+__device__ __forceinline__ Cell cellPack(double x, double invh, int n) {
+    constexpr double kInv2Pi = 1.0 / kTwoPi;
+    const double xw = __dsub_rn(x, __dmul_rn(kTwoPi, floor(__dadd_rn(x, kPi) * kInv2Pi)));
+    const double s = __dadd_rn(xw, kPi) * invh;
+    const double bf = floor(s);
+    const double f = s - bf;
+    int b = static_cast<int>(fmin(fmax(bf, 0.0), static_cast<double>(n)));
+    b = b >= n ? b - n : b;
+    constexpr Cell kMax = (Cell(1) << 51) - 1;
+    Cell q = (f == f) ? __double2ull_rn(f * 2251799813685248.0) : 0ull;  // f * 2^51
+    q = q > kMax ? kMax : q;
+    return (static_cast<Cell>(b) << 51) | q;
+}
+
+// Padded first-tap index and weights of a packed cell: the fraction's 51 bits become the top of
+// a [1, 2) mantissa.  The weights keep the reference's polynomials (an 11-operation regrouping
+// was 2-3% faster per band step but moved a FFT-sensitive default-path Newton record of config 2
+// past 10x the reference's own rounding floor).
+__device__ __forceinline__ int cellDecode(Cell u, double w[4]) {
+    const unsigned hi = static_cast<unsigned>(u >> 32), lo = static_cast<unsigned>(u);
+    const unsigned mhi = (__funnelshift_l(lo, hi, 1) & 0xFFFFFu) | 0x3FF00000u;
+    bsplineWeights(__hiloint2double(static_cast<int>(mhi), static_cast<int>(lo << 1)) - 1.0, w);
+    return static_cast<int>(hi >> 19);
+}
+
 constexpr std::size_t paddedPoints(int n1, int n2) {
     return static_cast<std::size_t>(n1 + 3) * static_cast<std::size_t>(n2 + 3);
 }
 // padded coefficients of one field of a grid or batch (the pairs' padded fields one after another)
 inline std::size_t paddedTotal(const GridDims& g) { return paddedPoints(g.n1, g.n2) * g.pairs; }
+
+// Departure cells of the departure points X = [x1 | x2] of a grid (or batch), cells = [c1 | c2].
+void launchPackCells(Ctx& ctx, const GridDims& g, const double* X, Cell* cells);
 
 // Pads / unpads a coefficient field (used at the C ABI, whose coefficients are unpadded).
 void launchPad(Ctx& ctx, const GridDims& g, const double* c, double* padded);

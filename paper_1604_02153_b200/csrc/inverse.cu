@@ -237,7 +237,11 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
     // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
     // 1024^2 on B200 (0.815 vs 0.867 ms).  The plain step is the generic-grid path.
-    fused_ = bandFusable(g) && colPassFusable(g);
+    fused_ = solver.bandPath();
+    if (fused_) {  // packed departure cells of both directions, before any graph capture
+        solver.cells(kForward);
+        solver.cells(kBackward);
+    }
     lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     adjLog_.ensure(nt + 1, g);
@@ -393,6 +397,8 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
     double* lam[2] = {vtD + 4 * N, vtD + 5 * N};
     const double* Xf = solver.departure(kForward);
     const double* Xb = solver.departure(kBackward);
+    const Cell* Cf = fused_ ? solver.cells(kForward) : nullptr;
+    const Cell* Cb = fused_ ? solver.cells(kBackward) : nullptr;
     const double* dv = solver.divVelocity();
     const double* dvd = solver.divVelocityAtDeparture(kBackward);
     double* coef = solver.coef();
@@ -429,13 +435,13 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
                 // step; its row pass then yields the row-filtered seed directly
                 const EpiIncSeed seed{adjLog_.partial(nt), epi, wOf(nt), b1, b2};
                 if (j == 1)
-                    launchEvalBand<EpiIncSeed, false>(ctx, g, cs, Xf, Xf + N, seed, R[j & 1], adjLog_.flag(nt));
+                    launchEvalBand<EpiIncSeed, false>(ctx, g, cs, Cf, Cf + N, seed, R[j & 1], adjLog_.flag(nt));
                 else
-                    launchEvalBand<EpiIncSeed, true>(ctx, g, cs, Xf, Xf + N, seed, R[j & 1], adjLog_.flag(nt));
+                    launchEvalBand<EpiIncSeed, true>(ctx, g, cs, Cf, Cf + N, seed, R[j & 1], adjLog_.flag(nt));
             } else if (j == 1) {
-                launchEvalBand<EpiIncState, false>(ctx, g, cs, Xf, Xf + N, epi, R[j & 1], nullptr);
+                launchEvalBand<EpiIncState, false>(ctx, g, cs, Cf, Cf + N, epi, R[j & 1], nullptr);
             } else {
-                launchEvalBand<EpiIncState, true>(ctx, g, cs, Xf, Xf + N, epi, R[j & 1], nullptr);
+                launchEvalBand<EpiIncState, true>(ctx, g, cs, Cf, Cf + N, epi, R[j & 1], nullptr);
             }
         }
         for (int j = nt; j >= 1; --j) {
@@ -447,7 +453,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
                 waitReg();
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
             } else {
-                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, R[(j - 1) & 1],
+                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, R[(j - 1) & 1],
                                                    adjLog_.flag(j - 1));
             }
         }
@@ -723,6 +729,8 @@ double Hessian::benchKernel(int id, int iters) {
     double* c2 = vtD + 11 * N;
     const double* Xf = solver.departure(kForward);
     const double* Xb = solver.departure(kBackward);
+    const Cell* Cf = fused_ ? solver.cells(kForward) : nullptr;
+    const Cell* Cb = fused_ ? solver.cells(kBackward) : nullptr;
     const double* dv = solver.divVelocity();
     const double* dvd = solver.divVelocityAtDeparture(kBackward);
     double* coef = solver.coef();
@@ -757,32 +765,32 @@ double Hessian::benchKernel(int id, int iters) {
             case 7: {  // band incremental-state step: gather + epilogue + next row pass
                 if (!fused_) throw NotSupported("bench kernel 7: band path not active on this grid");
                 EpiIncState epi{nullptr, vtD, vtD + N, GD, GD + N, vtD, vtD + N, G, G + N, 0.5 * ht, nullptr};
-                launchEvalBand<EpiIncState, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, tmp, nullptr);
+                launchEvalBand<EpiIncState, true>(ctx, g, CoeffSet<1>{{coef}}, Cf, Cf + N, epi, tmp, nullptr);
                 break;
             }
             case 8: {  // band incremental-adjoint + body-force step
                 if (!fused_) throw NotSupported("bench kernel 8: band path not active on this grid");
                 EpiAdjointBF epi{adjLog_.partial(0), dvd, dv, ht, nullptr, G, G + N, ht, b, b + N,
                                  nullptr, nullptr, nullptr, nullptr};
-                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, tmp + N,
+                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, tmp + N,
                                                    adjLog_.flag(0));
                 break;
             }
             case 11: {  // band incremental-state step without the gather (m~_0 = 0 form): operand traffic only
                 if (!fused_) throw NotSupported("bench kernel 11: band path not active on this grid");
                 EpiIncState epi{nullptr, vtD, vtD + N, GD, GD + N, vtD, vtD + N, G, G + N, 0.5 * ht, nullptr};
-                launchEvalBand<EpiIncState, false>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, tmp, nullptr);
+                launchEvalBand<EpiIncState, false>(ctx, g, CoeffSet<1>{{coef}}, Cf, Cf + N, epi, tmp, nullptr);
                 break;
             }
             case 9:  // SL state step (config 4 unit ii), band form: gather + m_j + next row pass, column pass
                 if (!solver.bandPath()) throw NotSupported("bench kernel 9: band path not active on this grid");
-                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N,
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Cf, Cf + N,
                                                    EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
                 launchPrefilterCols(ctx, g, tmp, coef);
                 break;
             case 12:  // the band kernel of the SL state step alone (no column pass)
                 if (!solver.bandPath()) throw NotSupported("bench kernel 12: band path not active on this grid");
-                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N,
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Cf, Cf + N,
                                                    EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
                 break;
             case 10:  // SL state step, plain form: prefilter (rows + cols) + gather

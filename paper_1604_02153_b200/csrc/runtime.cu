@@ -3,7 +3,9 @@
 // with NaN ignored (std::max semantics), axpy/scale.  Reductions are two-stage with a fixed
 // block count and a fixed-order final pass, so results are run-to-run deterministic.
 #include <cstdlib>
+#include <cstdint>
 #include <map>
+#include <set>
 #include <mutex>
 #include <cstdio>
 #include <cstring>
@@ -34,16 +36,59 @@ thread_local cudaStream_t g_allocStream = nullptr;
 thread_local bool g_allocStreamSet = false;
 
 namespace {
+// Per-stream block cache over the stream-ordered allocator.  A block is reused by the stream
+// that freed it (best fit); misses come from cudaMallocAsync and blocks beyond the cache cap go
+// back with cudaFreeAsync, so neither ever synchronises the device: a cudaFree there would
+// serialise every concurrent lane of a process (measured: config-5b lanes fell from 229 to
+// 83 pairs/s once an earlier 4096^2 registration had filled the cache up to its cap).
+// Blocks allocated while their stream is being captured come from cudaMalloc (an allocation
+// node inside a graph would change its lifetime) and are freed with cudaFree.
 struct BlockCache {
     std::mutex mu;
     std::multimap<std::pair<cudaStream_t, std::size_t>, void*> blocks;
+    std::set<void*> syncBlocks;  // from cudaMalloc (stream capture in progress)
     std::size_t held = 0;
 };
 BlockCache& blockCache() {
     static BlockCache* c = new BlockCache;  // leaked on purpose: outlives every context
     return *c;
 }
-constexpr std::size_t kCacheCap = std::size_t(48) << 30;  // beyond this, release for real
+constexpr std::size_t kCacheCap = std::size_t(48) << 30;  // beyond this, release (stream-ordered)
+constexpr std::uint64_t kPoolKeep = std::uint64_t(16) << 30;  // the pool keeps this much when trimming
+
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return st != cudaStreamCaptureStatusNone;
+}
+
+void poolSetup() {
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    VRG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(dev)) return;
+    cudaMemPool_t pool;
+    VRG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    std::uint64_t keep = kPoolKeep;
+    VRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    done.insert(dev);
+}
+
+// Returns a block to the driver in stream order (no device-wide synchronisation).
+void releaseBlock(BlockCache& c, void* p, cudaStream_t s) {
+    auto it = c.syncBlocks.find(p);
+    if (it != c.syncBlocks.end()) {
+        c.syncBlocks.erase(it);
+        cudaFree(p);
+    } else {
+        cudaFreeAsync(p, s);
+    }
+}
 }  // namespace
 
 void* cachedAlloc(std::size_t bytes, cudaStream_t s, std::size_t* got) {
@@ -63,31 +108,43 @@ void* cachedAlloc(std::size_t bytes, cudaStream_t s, std::size_t* got) {
     }
     *got = bytes;
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
+    const bool cap = capturing(s);
+    auto allocate = [&] {
+        if (cap) return cudaMalloc(&p, bytes);
+        poolSetup();
+        return cudaMallocAsync(&p, bytes, s);
+    };
+    cudaError_t e = allocate();
     if (e == cudaErrorMemoryAllocation) {  // drop the cache and retry once
         cudaGetLastError();
         std::lock_guard<std::mutex> lock(c.mu);
-        cudaStreamSynchronize(s);
-        for (auto& kv : c.blocks) cudaFree(kv.second);
+        for (auto& kv : c.blocks) releaseBlock(c, kv.second, kv.first.first);
         c.blocks.clear();
         c.held = 0;
-        e = cudaMalloc(&p, bytes);
+        cudaDeviceSynchronize();
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+            cudaMemPoolTrimTo(pool, 0);
+        e = allocate();
     }
     VRG_CUDA(e);
+    if (cap) {
+        std::lock_guard<std::mutex> lock(c.mu);
+        c.syncBlocks.insert(p);
+    }
     return p;
 }
 
 void cachedFree(void* p, std::size_t bytes, cudaStream_t s) {
     BlockCache& c = blockCache();
-    {
-        std::lock_guard<std::mutex> lock(c.mu);
-        if (c.held + bytes <= kCacheCap) {
-            c.blocks.emplace(std::make_pair(s, bytes), p);
-            c.held += bytes;
-            return;
-        }
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (c.held + bytes <= kCacheCap) {
+        c.blocks.emplace(std::make_pair(s, bytes), p);
+        c.held += bytes;
+        return;
     }
-    cudaFree(p);
+    releaseBlock(c, p, s);
 }
 
 // Frees the cached blocks of a stream (its context is going away).
@@ -96,7 +153,7 @@ void releaseCachedBlocks(cudaStream_t s) {
     std::lock_guard<std::mutex> lock(c.mu);
     for (auto it = c.blocks.begin(); it != c.blocks.end();) {
         if (it->first.first == s) {
-            cudaFree(it->second);
+            releaseBlock(c, it->second, s);
             c.held -= it->first.second;
             it = c.blocks.erase(it);
         } else {

@@ -201,7 +201,7 @@ Solver::Solver(Ctx& c, const GridDims& gd, const double* vv1, const double* vv2,
 // Band path for the SL time loops (evalband.cuh) wherever the grid allows it: each step is the
 // gather + epilogue + the next prefilter's row pass in one kernel, then the column pass; same
 // arithmetic as prefilter + evaluate (the plain 3-kernel step, the generic-grid path).
-bool Solver::bandPath() const { return bandFusable(g) && colPassFusable(g); }
+bool Solver::bandPath() const { return bandFusable(g) && colPassFusable(g) && bandCellsFit(g); }
 
 double* Solver::coef() { return coef_.d(); }
 double* Solver::tmp() { return tmp_.d(); }
@@ -221,6 +221,16 @@ const double* Solver::departure(int dir) {
         haveX_[dir] = true;
     }
     return X_[dir].d();
+}
+
+const Cell* Solver::cells(int dir) {
+    if (!haveCells_[dir]) {
+        const double* X = departure(dir);
+        cells_[dir].alloc(sizeof(Cell) * 2 * g.points());
+        launchPackCells(ctx, g, X, cells_[dir].as<Cell>());
+        haveCells_[dir] = true;
+    }
+    return cells_[dir].as<Cell>();
 }
 
 const double* Solver::divVelocity() {
@@ -261,6 +271,7 @@ void Solver::continuityStep(const double* u, double* out, int dir, double* guard
 template <class DstFn>
 void Solver::continuityBand(const double* lam1, DstFn dst) {
     const double* X = departure(kBackward);
+    const Cell* C = cells(kBackward);
     const double* dv = divVelocity();
     const double* dvd = divVelocityAtDeparture(kBackward);
     const std::size_t N = g.points();
@@ -270,7 +281,7 @@ void Solver::continuityBand(const double* lam1, DstFn dst) {
         if (j == 1) {
             launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
         } else {
-            launchEvalBand<EpiContinuity, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, tmp_.d(),
+            launchEvalBand<EpiContinuity, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                 log.flag(j - 1));
             launchPrefilterCols(ctx, g, tmp_.d(), coef_.d());
         }
@@ -281,6 +292,7 @@ void Solver::continuityBand(const double* lam1, DstFn dst) {
 void Solver::state(const double* m0, double* traj, bool guard) {
     NvtxRange nv_("Solver::solveState");
     const double* X = departure(kForward);
+    const Cell* C = bandPath() ? cells(kForward) : nullptr;
     const std::size_t N = g.points();
     log.reset(ctx);
     copy(ctx, N, m0, traj);
@@ -292,7 +304,7 @@ void Solver::state(const double* m0, double* traj, bool guard) {
             if (j == nt) {
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
             } else {
-                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, tmp_.d(),
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                    log.flag(j));
                 launchPrefilterCols(ctx, g, tmp_.d(), coef_.d());
             }
@@ -312,6 +324,7 @@ void Solver::state(const double* m0, double* traj, bool guard) {
 void Solver::stateFinal(const double* m0, double* out) {
     NvtxRange nv_("Solver::solveStateFinal");
     const double* X = departure(kForward);
+    const Cell* C = bandPath() ? cells(kForward) : nullptr;
     const std::size_t N = g.points();
     double* buf = ctx.scratchBuf(12, sizeof(double) * 2 * N);
     log.reset(ctx);
@@ -324,7 +337,7 @@ void Solver::stateFinal(const double* m0, double* out) {
             if (j == nt) {
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
             } else {
-                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, tmp_.d(),
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                    log.flag(j));
                 launchPrefilterCols(ctx, g, tmp_.d(), coef_.d());
             }

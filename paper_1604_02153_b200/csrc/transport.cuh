@@ -76,6 +76,9 @@ public:
     // Lazy per-velocity caches (src/transport.cpp:107-127), with the reference's counter
     // increments when first built.
     const double* departure(int dir);  // [x1 | x2]
+    // The departure points packed for the gathers of the band path (interp.cuh: Cell), [c1 | c2];
+    // built once per direction from departure(dir), no counter increments.
+    const Cell* cells(int dir);
     const double* divVelocity();
     const double* divVelocityAtDeparture(int dir);
 
@@ -112,10 +115,10 @@ private:
     template <class DstFn>
     void continuityBand(const double* lam1, DstFn dst);
     DBuf cv_;  // prefiltered velocity [c1 | c2]
-    DBuf X_[2];
+    DBuf X_[2], cells_[2];
     DBuf divv_, dvDep_[2];
     DBuf coef_, tmp_;
-    bool haveCv_ = false, haveX_[2] = {false, false}, haveDivv_ = false, haveDvDep_[2] = {false, false};
+    bool haveCv_ = false, haveX_[2] = {false, false}, haveCells_[2] = {false, false}, haveDivv_ = false, haveDvDep_[2] = {false, false};
 };
 
 }  // namespace vrg
