@@ -210,10 +210,19 @@ int vrg_hess_apply_split(vrg_hess_t h, const double* s1, const double* s2, doubl
 int vrg_hess_apply_host(vrg_hess_t h, const double* vt1, const double* vt2, double* o1, double* o2);
 /* k independent apply_host calls (inputs vt1[i], vt2[i] -> outputs o1[i], o2[i], host buffers,
  * pinned for overlap) with the host<->device copies of neighbouring matvecs overlapped with the
- * compute of the current one (two copy streams, two device slots).  Same results and error
- * behaviour as k apply_host calls in order; the first failing matvec's error is returned. */
+ * compute of the current one (two copy streams, two device slots), and each matvec's guard
+ * checked on the host while the next one runs.  Same results and error behaviour as k
+ * apply_host calls in order: the first failing matvec's error is returned, the outputs before
+ * it are delivered, the failing one's and later ones are not written. */
 int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, const double* const* vt2,
                               double* const* o1, double* const* o2);
+/* k apply calls on DEVICE buffers queued back to back (HessianOperator::apply, inverse.cpp:
+ * 229-233, repeated): each matvec's guard is checked on the host while the next one runs, so
+ * the device never waits for the host between matvecs.  Same results as k apply calls; on an
+ * error (the first failing matvec's, as apply would throw it) the outputs of the matvecs before
+ * it are final and the failing one's and the next one's may have been written. */
+int vrg_hess_apply_batch(vrg_hess_t h, int k, const double* const* vt1, const double* const* vt2, double* const* o1,
+                         double* const* o2);
 int vrg_hess_state(vrg_hess_t h, double* traj); /* copy of the held state trajectory */
 /* instrumentation: average ms of one launch of a matvec kernel class (0 incremental-state
  * step, 1 incremental-adjoint + body-force step, 2 prefilter (both passes), 3 two-field
@@ -228,6 +237,9 @@ int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_la
 int vrg_band_mapping(int mode);
 /* 1 when the time loops run the band kernels (gather + epilogue + next row pass fused; ids 7
  * and 8 of vrg_hess_bench_kernel), 0 for the plain 3-kernel step */
+/* instrumentation: nodes, edges and programmatic-dependent-launch edges of the operator's last
+ * captured matvec graph (info[3]) */
+int vrg_hess_graph_info(vrg_hess_t h, int* info);
 int vrg_hess_band_path(vrg_hess_t h, int* band);
 /* device pointers of the operator's per-iterate invariants (read only, owned by h):
  * [0] state m_j, (nt+1) fields; [1] grad m_j, (nt+1) x [d1 | d2]; [2] (grad m_{j-1})_D, nt x

@@ -76,6 +76,8 @@ _SIG = {
     "vrg_hess_apply_split": ("ppppp", C.c_int),
     "vrg_hess_apply_host": ("ppppp", C.c_int),
     "vrg_hess_apply_host_batch": ("pipppp", C.c_int),
+    "vrg_hess_apply_batch": ("pipppp", C.c_int),
+    "vrg_hess_graph_info": ("pp", C.c_int),
     "vrg_hess_state": ("pp", C.c_int),
     "vrg_hess_bench_kernel": ("piip", C.c_int),
     "vrg_hess_band_path": ("pp", C.c_int),

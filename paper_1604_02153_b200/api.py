@@ -372,6 +372,16 @@ class HessianOperator:
                ((vts, 0), (vts, 1), (outs, 0), (outs, 1))]
         self.ctx.check(self.ctx.lib.vrg_hess_apply_host_batch(self.h, k, *[C.cast(a, C.c_void_p) for a in arr]))
 
+    def apply_batch(self, vts, outs):
+        """apply() over k device inputs vts[i] = (vt1, vt2) -> outs[i] = (o1, o2), queued back to
+        back: matvec i's guard is checked on the host while matvec i+1 runs (vrg_hess_apply_batch)."""
+        k = len(vts)
+        if len(outs) != k:
+            raise ValueError("apply_batch: as many outputs as inputs")
+        arr = [(C.c_void_p * max(k, 1))(*[_p(x[j]).value for x in seq]) for seq, j in
+               ((vts, 0), (vts, 1), (outs, 0), (outs, 1))]
+        self.ctx.check(self.ctx.lib.vrg_hess_apply_batch(self.h, k, *[C.cast(a, C.c_void_p) for a in arr]))
+
     @property
     def band_path(self):
         """True when the matvec runs the fused band kernels (evalband.cuh), False on the 3-kernel step."""

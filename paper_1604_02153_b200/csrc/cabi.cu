@@ -628,6 +628,15 @@ int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, con
             VRG_CUDA(cudaMemcpyAsync(in(s) + N, vt2[i], B, cudaMemcpyHostToDevice, P.in));
             VRG_CUDA(cudaEventRecord(P.evIn[s], P.in));
         };
+        // matvec j's result leaves only after its guard check passed (an error delivers nothing
+        // from the failing matvec on)
+        auto download = [&](int j) {
+            const int s = j & 1;
+            VRG_CUDA(cudaStreamWaitEvent(P.out, P.evComp[s], 0));
+            VRG_CUDA(cudaMemcpyAsync(o1[j], outp(s), B, cudaMemcpyDeviceToHost, P.out));
+            VRG_CUDA(cudaMemcpyAsync(o2[j], outp(s) + N, B, cudaMemcpyDeviceToHost, P.out));
+            VRG_CUDA(cudaEventRecord(P.evOut[s], P.out));
+        };
         try {
             upload(0);
             for (int i = 0; i < k; ++i) {
@@ -635,15 +644,18 @@ int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, con
                 if (i + 1 < k) upload(i + 1);
                 VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evIn[s], 0));
                 if (i >= 2) VRG_CUDA(cudaStreamWaitEvent(ctx.stream, P.evOut[s], 0));  // D2H i-2 read slot s
-                h->hess.apply(in(s), in(s) + N, outp(s), outp(s) + N);
+                h->hess.applyQueued(in(s), in(s) + N, outp(s), outp(s) + N, s);
                 VRG_CUDA(cudaEventRecord(P.evComp[s], ctx.stream));
-                VRG_CUDA(cudaStreamWaitEvent(P.out, P.evComp[s], 0));
-                VRG_CUDA(cudaMemcpyAsync(o1[i], outp(s), B, cudaMemcpyDeviceToHost, P.out));
-                VRG_CUDA(cudaMemcpyAsync(o2[i], outp(s) + N, B, cudaMemcpyDeviceToHost, P.out));
-                VRG_CUDA(cudaEventRecord(P.evOut[s], P.out));
+                if (i >= 1) {  // matvec i-1's guard, checked while matvec i runs
+                    h->hess.checkQueued((i - 1) & 1);
+                    download(i - 1);
+                }
             }
+            h->hess.checkQueued((k - 1) & 1);
+            download(k - 1);
         } catch (...) {
-            cudaStreamSynchronize(P.in);  // no copy outlives the call
+            cudaStreamSynchronize(ctx.stream);  // nothing outlives the call
+            cudaStreamSynchronize(P.in);
             cudaStreamSynchronize(P.out);
             throw;
         }
@@ -654,12 +666,36 @@ int vrg_hess_apply_host_batch(vrg_hess_t h, int k, const double* const* vt1, con
     });
 }
 
+int vrg_hess_apply_batch(vrg_hess_t h, int k, const double* const* vt1, const double* const* vt2, double* const* o1,
+                         double* const* o2) {
+    return guarded(h->owner, [&] {
+        if (k < 0) throw vrg::InvalidArgument("apply_batch: negative count");
+        vrg::Hessian& H = h->hess;
+        try {
+            for (int i = 0; i < k; ++i) {
+                H.applyQueued(vt1[i], vt2[i], o1[i], o2[i], i & 1);
+                if (i >= 1) H.checkQueued((i - 1) & 1);  // matvec i-1's guard while matvec i runs
+            }
+            if (k > 0) H.checkQueued((k - 1) & 1);
+        } catch (...) {
+            cudaStreamSynchronize(H.ctx.stream);
+            throw;
+        }
+    });
+}
+
 int vrg_hess_bench_kernel(vrg_hess_t h, int kernel, int iters, double* ms_per_launch) {
     return guarded(h->owner, [&] { *ms_per_launch = h->hess.benchKernel(kernel, iters); });
 }
 
 int vrg_band_mapping(int mode) {
     return vrg::g_bandMapping.exchange(mode < 0 || mode > 2 ? 0 : mode);
+}
+
+int vrg_hess_graph_info(vrg_hess_t h, int* info) {
+    return guarded(h->owner, [&] {
+        for (int i = 0; i < 3; ++i) info[i] = h->hess.graphInfo_[i];
+    });
 }
 
 int vrg_hess_band_path(vrg_hess_t h, int* band) {

@@ -244,7 +244,7 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
     }
     lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
-    adjLog_.ensure(nt + 1, g);
+    for (auto& l : guardLogs_) l.ensure(nt + 1, g);
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
     // every plan a matvec uses exists before any graph capture (plan creation allocates)
@@ -295,7 +295,7 @@ void Hessian::initHeun(const double* mR, const double* mT, const double* stateTr
     useGraphs = false;
     lazyInterps_ = 0;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
-    adjLog_.ensure(nt + 1, g);
+    for (auto& l : guardLogs_) l.ensure(nt + 1, g);
     weights.regSymbol(model.betaV);
     weights.invRegSymbol(model.betaV, -0.5);
     ctx.sync();
@@ -425,7 +425,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         // each step is [column pass] + [gather + epilogue + row pass].  R[.] ping-pong holds
         // the row-filtered m~_j, then the row-filtered lt_j.
         double* R[2] = {tmp, tmp + N};
-        adjLog_.reset(ctx);
+        adjLog_->reset(ctx);
         for (int j = 1; j <= nt; ++j) {
             const EpiIncState epi{nullptr, vtD, vtD + N, GD(j), GD(j) + N, vt1, vt2, G(j), G(j) + N, 0.5 * ht, nullptr};
             if (j > 1) launchPrefilterCols(ctx, g, R[(j - 1) & 1], coef);
@@ -433,11 +433,11 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
             if (j == nt) {
                 // the adjoint seed lt(1) = -m~(1) and b = w lt(1) grad m_nt fused into the last
                 // step; its row pass then yields the row-filtered seed directly
-                const EpiIncSeed seed{adjLog_.partial(nt), epi, wOf(nt), b1, b2};
+                const EpiIncSeed seed{adjLog_->partial(nt), epi, wOf(nt), b1, b2};
                 if (j == 1)
-                    launchEvalBand<EpiIncSeed, false>(ctx, g, cs, Cf, Cf + N, seed, R[j & 1], adjLog_.flag(nt));
+                    launchEvalBand<EpiIncSeed, false>(ctx, g, cs, Cf, Cf + N, seed, R[j & 1], adjLog_->flag(nt));
                 else
-                    launchEvalBand<EpiIncSeed, true>(ctx, g, cs, Cf, Cf + N, seed, R[j & 1], adjLog_.flag(nt));
+                    launchEvalBand<EpiIncSeed, true>(ctx, g, cs, Cf, Cf + N, seed, R[j & 1], adjLog_->flag(nt));
             } else if (j == 1) {
                 launchEvalBand<EpiIncState, false>(ctx, g, cs, Cf, Cf + N, epi, R[j & 1], nullptr);
             } else {
@@ -447,17 +447,17 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         for (int j = nt; j >= 1; --j) {
             launchPrefilterCols(ctx, g, R[j & 1], coef);
             const bool last = j == 1;
-            EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, nullptr, G(j - 1), G(j - 1) + N, wOf(j - 1),
+            EpiAdjointBF epi{adjLog_->partial(j - 1), dvd, dv, ht, nullptr, G(j - 1), G(j - 1) + N, wOf(j - 1),
                              b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
             if (last) {
                 waitReg();
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
             } else {
                 launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, R[(j - 1) & 1],
-                                                   adjLog_.flag(j - 1));
+                                                   adjLog_->flag(j - 1));
             }
         }
-        adjLog_.finalize(ctx);
+        adjLog_->finalize(ctx);
         return;
     }
     for (int j = 1; j <= nt; ++j) {
@@ -470,18 +470,18 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         }
     }
     // incremental adjoint (GN: solveAdjoint(-m~(1)), guarded, inverse.cpp:185) + body force
-    adjLog_.reset(ctx);
+    adjLog_->reset(ctx);
     launchPointwise(ctx, g,
-                    EpiAdjointSeed{adjLog_.partial(nt), mt[nt & 1], lam[nt & 1], G(nt), G(nt) + N, wOf(nt), b1, b2});
+                    EpiAdjointSeed{adjLog_->partial(nt), mt[nt & 1], lam[nt & 1], G(nt), G(nt) + N, wOf(nt), b1, b2});
     for (int j = nt; j >= 1; --j) {
-        launchPrefilter(ctx, g, lam[j & 1], coef, tmp, adjLog_.flag(j));
+        launchPrefilter(ctx, g, lam[j & 1], coef, tmp, adjLog_->flag(j));
         const bool last = (j == 1) && out1;
-        EpiAdjointBF epi{adjLog_.partial(j - 1), dvd, dv, ht, lam[(j - 1) & 1], G(j - 1), G(j - 1) + N, wOf(j - 1),
+        EpiAdjointBF epi{adjLog_->partial(j - 1), dvd, dv, ht, lam[(j - 1) & 1], G(j - 1), G(j - 1) + N, wOf(j - 1),
                          b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
         if (j == 1) waitReg();
         launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
     }
-    adjLog_.finalize(ctx);
+    adjLog_->finalize(ctx);
 }
 
 // Full-Newton data term (HessianOperator::Impl::dataTerm FN branch, inverse.cpp:187-211, SL):
@@ -678,9 +678,9 @@ void Hessian::guardAfterMatvec() {
         return;
     }
     const std::size_t steps = static_cast<std::size_t>(nt + 1), per = steps * g.pairs;
-    VRG_CUDA(cudaMemcpyAsync(deferMax_.d() + per * deferCount_, adjLog_.stepMax.d(), sizeof(double) * per,
+    VRG_CUDA(cudaMemcpyAsync(deferMax_.d() + per * deferCount_, adjLog_->stepMax.d(), sizeof(double) * per,
                              cudaMemcpyDeviceToDevice, ctx.stream));
-    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + steps * deferCount_, adjLog_.flags.d(),
+    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + steps * deferCount_, adjLog_->flags.d(),
                              sizeof(unsigned) * steps, cudaMemcpyDeviceToDevice, ctx.stream));
     ++deferCount_;
 }
@@ -694,12 +694,12 @@ void Hessian::checkLastGuard() {
         if (h) throw InvalidArgument("prefilter: non-finite value");
         return;
     }
-    adjLog_.check(ctx, "adjoint", nt, false, true, nt);
+    adjLog_->check(ctx, "adjoint", nt, false, true, nt);
     if (g_collectGuards)
         for (int p = 0; p < g.pairs; ++p)
-            if (!pairStatus[p] && adjLog_.pairStatus[p]) {
-                pairStatus[p] = adjLog_.pairStatus[p];
-                pairError[p] = adjLog_.pairError[p];
+            if (!pairStatus[p] && adjLog_->pairStatus[p]) {
+                pairStatus[p] = adjLog_->pairStatus[p];
+                pairError[p] = adjLog_->pairError[p];
             }
 }
 
@@ -745,7 +745,7 @@ double Hessian::benchKernel(int id, int iters) {
                 break;
             }
             case 1: {  // incremental-adjoint step + body force (K5+K8)
-                EpiAdjointBF epi{adjLog_.partial(0), dvd, dv, ht, lam + N, G, G + N, ht, b, b + N,
+                EpiAdjointBF epi{adjLog_->partial(0), dvd, dv, ht, lam + N, G, G + N, ht, b, b + N,
                                  nullptr, nullptr, nullptr, nullptr};
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
                 break;
@@ -770,10 +770,10 @@ double Hessian::benchKernel(int id, int iters) {
             }
             case 8: {  // band incremental-adjoint + body-force step
                 if (!fused_) throw NotSupported("bench kernel 8: band path not active on this grid");
-                EpiAdjointBF epi{adjLog_.partial(0), dvd, dv, ht, nullptr, G, G + N, ht, b, b + N,
+                EpiAdjointBF epi{adjLog_->partial(0), dvd, dv, ht, nullptr, G, G + N, ht, b, b + N,
                                  nullptr, nullptr, nullptr, nullptr};
                 launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, tmp + N,
-                                                   adjLog_.flag(0));
+                                                   adjLog_->flag(0));
                 break;
             }
             case 11: {  // band incremental-state step without the gather (m~_0 = 0 form): operand traffic only
@@ -785,18 +785,30 @@ double Hessian::benchKernel(int id, int iters) {
             case 9:  // SL state step (config 4 unit ii), band form: gather + m_j + next row pass, column pass
                 if (!solver.bandPath()) throw NotSupported("bench kernel 9: band path not active on this grid");
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Cf, Cf + N,
-                                                   EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
+                                                   EpiStateStep{adjLog_->partial(0), mt + N}, tmp, nullptr);
                 launchPrefilterCols(ctx, g, tmp, coef);
                 break;
             case 12:  // the band kernel of the SL state step alone (no column pass)
                 if (!solver.bandPath()) throw NotSupported("bench kernel 12: band path not active on this grid");
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef}}, Cf, Cf + N,
-                                                   EpiStateStep{adjLog_.partial(0), mt + N}, tmp, nullptr);
+                                                   EpiStateStep{adjLog_->partial(0), mt + N}, tmp, nullptr);
                 break;
             case 10:  // SL state step, plain form: prefilter (rows + cols) + gather
                 launchPrefilter(ctx, g, mt, coef, tmp, nullptr);
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, EpiStateStep{adjLog_.partial(0), mt + N}, true);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, EpiStateStep{adjLog_->partial(0), mt + N}, true);
                 break;
+            case 13:  // one whole matvec launched directly on the stream (programmatic dependent launch, no graph)
+            case 14: {  // the same matvec through its CUDA graph (the apply path's replay)
+                double* in = ctx.scratchBuf(130, sizeof(double) * 2 * N);
+                double* out = ctx.scratchBuf(131, sizeof(double) * 2 * N);
+                VRG_CUDA(cudaMemcpyAsync(in, vtD, sizeof(double) * 2 * N, cudaMemcpyDeviceToDevice, ctx.stream));
+                if (id == 13) {
+                    launchApply(in, in + N, out, out + N);
+                } else {
+                    replay(0, in, in + N, out, out + N, [&] { launchApply(in, in + N, out, out + N); });
+                }
+                break;
+            }
             default:  // vtilde at departure (K2, two fields)
                 launchEvaluate<2>(ctx, g, CoeffSet<2>{{coef, c2}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
                 break;
@@ -856,6 +868,19 @@ void Hessian::replay(int kind, const double* a, const double* b, const double* c
         }
         VRG_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
         GraphEntry& e = it->second;
+        {  // shape of the captured graph (instrumentation: vrg_hess_graph_info)
+            std::size_t nodes = 0, edges = 0;
+            VRG_CUDA(cudaGraphGetNodes(graph, nullptr, &nodes));
+            VRG_CUDA(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &edges));
+            std::vector<cudaGraphNode_t> from(edges), to(edges);
+            std::vector<cudaGraphEdgeData> data(edges);
+            if (edges) VRG_CUDA(cudaGraphGetEdges_v2(graph, from.data(), to.data(), data.data(), &edges));
+            int prog = 0;
+            for (const auto& d : data) prog += d.type == cudaGraphDependencyTypeProgrammatic;
+            graphInfo_[0] = static_cast<int>(nodes);
+            graphInfo_[1] = static_cast<int>(edges);
+            graphInfo_[2] = prog;
+        }
         VRG_CUDA(cudaGraphInstantiate(&e.exec, graph, 0));
         cudaGraphDestroy(graph);
         e.launches = ctx.launches - l0;
@@ -882,6 +907,13 @@ Hessian::~Hessian() {
         cudaEventDestroy(evJoin_);
         cudaStreamDestroy(aux_);
     }
+    if (hostGuard_) {
+        cudaStreamSynchronize(guardStream_);
+        for (auto& e : evGuard_) cudaEventDestroy(e);
+        for (auto& e : evDone_) cudaEventDestroy(e);
+        cudaStreamDestroy(guardStream_);
+        cudaFreeHost(hostGuard_);
+    }
     for (auto& kv : graphs_) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
         for (cudaEvent_t e : kv.second.events) cudaEventDestroy(e);
@@ -894,6 +926,54 @@ void Hessian::apply(const double* vt1, const double* vt2, double* o1, double* o2
     ctx.ffts += 4;
     countDataTerm();
     checkLastGuard();
+}
+
+bool Hessian::queuedGuards() const { return !heun_ && mode_ == 0 && g.pairs == 1 && !g_collectGuards; }
+
+void Hessian::applyQueued(const double* vt1, const double* vt2, double* o1, double* o2, int slot) {
+    if (!queuedGuards()) {
+        apply(vt1, vt2, o1, o2);
+        return;
+    }
+    NvtxRange nv_("HessianOperator::apply (queued)");
+    const std::size_t steps = static_cast<std::size_t>(nt + 1);
+    if (!hostGuard_) {
+        VRG_CUDA(cudaMallocHost(&hostGuard_, 2 * steps * (sizeof(double) + sizeof(unsigned))));
+        VRG_CUDA(cudaStreamCreateWithFlags(&guardStream_, cudaStreamNonBlocking));
+        for (int s = 0; s < 2; ++s) {
+            VRG_CUDA(cudaEventCreateWithFlags(&evGuard_[s], cudaEventDisableTiming));
+            VRG_CUDA(cudaEventCreateWithFlags(&evDone_[s], cudaEventDisableTiming));
+        }
+    }
+    // guard log `slot` (the graph of this slot writes it) is free once its previous readback is
+    // done; the readback of this matvec runs on the guard stream, off the matvec stream
+    VRG_CUDA(cudaStreamWaitEvent(ctx.stream, evGuard_[slot], 0));
+    adjLog_ = &guardLogs_[slot];
+    try {
+        replay(8 * slot, vt1, vt2, o1, o2, [&] { launchApply(vt1, vt2, o1, o2); });
+    } catch (...) {
+        adjLog_ = &guardLogs_[0];
+        throw;
+    }
+    adjLog_ = &guardLogs_[0];
+    ctx.ffts += 4;
+    countDataTerm();
+    VRG_CUDA(cudaEventRecord(evDone_[slot], ctx.stream));
+    VRG_CUDA(cudaStreamWaitEvent(guardStream_, evDone_[slot], 0));
+    double* mx = hostGuard_ + slot * steps;
+    unsigned* fl = reinterpret_cast<unsigned*>(hostGuard_ + 2 * steps) + slot * steps;
+    const GuardLog& L = guardLogs_[slot];
+    VRG_CUDA(cudaMemcpyAsync(mx, L.stepMax.d(), sizeof(double) * steps, cudaMemcpyDeviceToHost, guardStream_));
+    VRG_CUDA(cudaMemcpyAsync(fl, L.flags.d(), sizeof(unsigned) * steps, cudaMemcpyDeviceToHost, guardStream_));
+    VRG_CUDA(cudaEventRecord(evGuard_[slot], guardStream_));
+}
+
+void Hessian::checkQueued(int slot) {
+    if (!queuedGuards()) return;  // applyQueued checked already
+    const std::size_t steps = static_cast<std::size_t>(nt + 1);
+    VRG_CUDA(cudaEventSynchronize(evGuard_[slot]));
+    GuardLog::checkHost(hostGuard_ + slot * steps, reinterpret_cast<unsigned*>(hostGuard_ + 2 * steps) + slot * steps,
+                        "adjoint", nt, false, true, nt);
 }
 
 void Hessian::launchApply(const double* vt1, const double* vt2, double* o1, double* o2) {

@@ -66,6 +66,14 @@ public:
     // operators only; otherwise the checks stay immediate.
     void beginDeferredGuards(int maxCalls);
     void endDeferredGuards();
+    // Queued matvecs (apply batches, C ABI vrg_hess_apply_batch / _host_batch): apply() without
+    // the per-matvec host round trip.  The matvec's guard maxima and prefilter flags go to
+    // pinned host slot `slot` (0 or 1) in stream order; checkQueued(slot) waits for that copy
+    // only and throws what apply() would have thrown, so the host checks matvec i while matvec
+    // i+1 runs.  queuedGuards(): GN SL/RK operators of one pair (elsewhere apply() is used).
+    bool queuedGuards() const;
+    void applyQueued(const double* vt1, const double* vt2, double* o1, double* o2, int slot);
+    void checkQueued(int slot);
     // counter increments of one data term in the reference (steady state)
     void countDataTerm();
     // forget the lazily-built per-velocity work still to be counted (an operator rebuilt for a
@@ -108,11 +116,17 @@ private:
     DBuf GD_;     // nt x [gd1 | gd2], GD_[j-1] = (grad m_{j-1})_D
     DBuf work_;   // vtD (2N), mt ping-pong (2N), lam ping-pong (2N), b (2N), coef2 (N), reg (2N)
     DBuf spec_;   // 4 half spectra
-    GuardLog adjLog_;
+    // Guard log of the data term's adjoint; queued matvecs alternate between the two (the graph
+    // of slot s writes guardLogs_[s]: its readback overlaps the next matvec)
+    GuardLog guardLogs_[2];
+    GuardLog* adjLog_ = &guardLogs_[0];
     bool deferring_ = false;
     int deferCap_ = 0, deferCount_ = 0;
     DBuf deferMax_, deferFlags_;
     void guardAfterMatvec();
+    double* hostGuard_ = nullptr;  // queued matvecs: 2 slots x [(nt+1) maxima | (nt+1) flags]
+    cudaStream_t guardStream_ = nullptr;
+    cudaEvent_t evGuard_[2] = {nullptr, nullptr}, evDone_[2] = {nullptr, nullptr};
     long long lazyInterps_ = 0, lazyFfts_ = 0;
     bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh
     int mode_ = 0;        // 1: full Newton
@@ -136,6 +150,8 @@ private:
 
 public:
     bool bandPath() const { return fused_; }
+    // nodes, edges and programmatic (PDL) edges of the last captured matvec graph
+    int graphInfo_[3] = {0, 0, 0};
     // device buffers of the per-iterate invariants: state (nt+1)N, G (nt+1)2N, GD nt 2N
     const double* gradTraj() const { return G_.d(); }
     const double* gradDepTraj() const { return GD_.d(); }

@@ -1,7 +1,8 @@
 """GPU: the host-buffer entry points of the Hessian (the drop-in call a host-side caller of
 HessianOperator::apply makes, inverse.hpp:83): vrg_hess_apply_host and the pipelined
 vrg_hess_apply_host_batch give bit-identical results to the device apply, and the batch
-reports the reference's error at the matvec that raised it."""
+reports the reference's error at the matvec that raised it; the queued device batch
+(vrg_hess_apply_batch) likewise."""
 from __future__ import annotations
 
 import numpy as np
@@ -75,3 +76,45 @@ def test_apply_host_batch_error_at_the_failing_matvec(ctx, api):
     # the operator is still usable after the error
     H.apply_host_batch(hin[:2], hout[:2])
     assert np.array_equal(hout[0][0], ref0[0].cpu().numpy())
+
+
+@pytest.mark.parametrize("n,nt,deformation", [(256, 4, 0), (128, 3, 1), (1024, 4, 0)])
+def test_apply_batch_matches_device_apply(ctx, api, n, nt, deformation):
+    """Queued device matvecs (each guard checked while the next matvec runs) give the same bits
+    as apply() one call at a time, through direct launches, the capture and graph replays."""
+    H = _operator(ctx, api, n, nt, deformation)
+    k = 5
+    vts = [tuple(ctx.field(x) for x in synth.smooth_velocity(n, n, 3000 + i)) for i in range(k)]
+    want = [[t.cpu().numpy() for t in H.apply(vt)] for vt in vts]
+    outs = [(ctx.empty(n, n), ctx.empty(n, n)) for _ in range(k)]
+    for rep in range(3):
+        for o in outs:
+            o[0].fill_(float("nan"))
+            o[1].fill_(float("nan"))
+        H.apply_batch(vts, outs)
+        for i in range(k):
+            assert np.array_equal(outs[i][0].cpu().numpy(), want[i][0]), (rep, i)
+            assert np.array_equal(outs[i][1].cpu().numpy(), want[i][1]), (rep, i)
+    # alternating inputs into one output (the bench's timed loop): the last input's result
+    H.apply_batch([vts[i & 1] for i in range(6)], [outs[0]] * 6)
+    assert np.array_equal(outs[0][0].cpu().numpy(), want[1][0])
+    H.apply_batch([], [])
+
+
+def test_apply_batch_error_at_the_failing_matvec(ctx, api):
+    n = 128
+    H = _operator(ctx, api, n, 4, 0)
+    good = [synth.smooth_velocity(n, n, 5000 + i) for i in range(4)]
+    bad = (good[2][0].copy(), good[2][1].copy())
+    bad[0][7, 9] = np.nan
+    vts = [tuple(ctx.field(x) for x in p) for p in (good[0], good[1], bad, good[3])]
+    outs = [(ctx.field(np.full((n, n), -1.0)), ctx.field(np.full((n, n), -1.0))) for _ in range(4)]
+    with pytest.raises(api.InvalidArgument, match="non-finite"):
+        H.apply_batch(vts, outs)
+    ref0 = H.apply(vts[0])
+    ref1 = H.apply(vts[1])
+    assert np.array_equal(outs[0][0].cpu().numpy(), ref0[0].cpu().numpy())  # before the failing one: final
+    assert np.array_equal(outs[1][1].cpu().numpy(), ref1[1].cpu().numpy())
+    # the operator is still usable after the error
+    H.apply_batch(vts[:2], outs[:2])
+    assert np.array_equal(outs[1][0].cpu().numpy(), ref1[0].cpu().numpy())
