@@ -36,6 +36,14 @@ struct CoeffSet {
 // csZ, epilogue index offset epiZ per member; guard-free epilogues only).
 // Guard partial of evaluate block b of a batch (GridDims::pairs): entry pair * gE + local block
 // (guardStride), the same entry as block b for a single grid.
+// Per-(step, pair) guard maximum: guard values are >= +0 (NaN skipped, inf kept), whose IEEE bit
+// patterns order like unsigned integers, so an integer atomicMax on the bits is the maximum of
+// the doubles (order-independent, hence run-to-run deterministic) and no reduction kernel
+// follows the step.
+__device__ __forceinline__ void guardMax(double* slot, double m) {
+    atomicMax(reinterpret_cast<unsigned long long*>(slot), static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
 __device__ __forceinline__ unsigned guardEntry(unsigned b, unsigned blocksPer, unsigned gE) {
     const unsigned pair = b / blocksPer;
     return pair * gE + (b - pair * blocksPer);
@@ -44,9 +52,14 @@ __device__ __forceinline__ unsigned guardEntry(unsigned b, unsigned blocksPer, u
 // Stacked pairs (GridDims::pairs): node p belongs to pair p / (n1 n2), whose coefficients are the
 // pair's padded field (pair * paddedPoints(n1, n2) further on); n1 * n2 is then a multiple of
 // the block size, so a block never straddles two pairs.
-template <int NF, class Epi>
-__global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const double* __restrict__ x1,
-                                                         const double* __restrict__ x2, int n1, int n2, int xStable,
+// First-tap row/column and weights of a departure point along one axis: from the coordinate
+// or from its packed cell (interp.cuh: the per-iterate departure points of the SL loops).
+__device__ __forceinline__ int depCell(double x, double invh, int n, double w[4]) { return cellBase(x, invh, n, w); }
+__device__ __forceinline__ int depCell(Cell u, double, int, double w[4]) { return cellDecode(u, w); }
+
+template <int NF, class Epi, class Dep = double>
+__global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const Dep* __restrict__ x1,
+                                                         const Dep* __restrict__ x2, int n1, int n2, int xStable,
                                                          Epi epi, std::size_t csZ, std::size_t epiZ, int pairs,
                                                          unsigned gE) {
     const int Nper = n1 * n2;
@@ -66,8 +79,8 @@ __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const 
     double w1[4], w2[4];
     int base = 0;
     if (p < N) {
-        const int b1 = cellBase(__ldg(x1 + p), n1 * (1.0 / kTwoPi), n1, w1);  // 1/h = n / 2pi
-        const int b2 = cellBase(__ldg(x2 + p), n2 * (1.0 / kTwoPi), n2, w2);
+        const int b1 = depCell(__ldg(x1 + p), n1 * (1.0 / kTwoPi), n1, w1);  // 1/h = n / 2pi
+        const int b2 = depCell(__ldg(x2 + p), n2 * (1.0 / kTwoPi), n2, w2);
         base = b1 * (n2 + 3) + b2;
     }
     // epilogue operands that no in-flight kernel writes (per-iterate fields) are loaded now,
@@ -118,7 +131,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const 
         if (threadIdx.x == 0) {
             double m = red[0];
             for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
-            epi.guardPartials[guardEntry(blockIdx.x, (Nper + kEvalBlock - 1) / kEvalBlock, gE)] = m;
+            guardMax(epi.guardPartials + blockIdx.x / ((Nper + kEvalBlock - 1) / kEvalBlock), m);
         }
     }
 }
@@ -144,7 +157,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi
         if (threadIdx.x == 0) {
             double m = red[0];
             for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
-            epi.guardPartials[guardEntry(blockIdx.x, blocksPer, gE)] = m;
+            guardMax(epi.guardPartials + blockIdx.x / blocksPer, m);
         }
     }
 }
@@ -166,13 +179,13 @@ void launchPointwise(Ctx& ctx, const GridDims& g, const Epi& epi) {
     }
 }
 
-template <int NF, class Epi>
-void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const double* x1, const double* x2, const Epi& epi,
+template <int NF, class Epi, class Dep>
+void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const Dep* x1, const Dep* x2, const Epi& epi,
                     bool xStable = false) {
     const std::size_t N = g.points();
     {
         LaunchScope ls_(ctx, Epi::kName);
-        launchPdl(1, k_evaluate<NF, Epi>, grid1d(N, kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, cs, x1, x2, g.n1, g.n2,
+        launchPdl(1, k_evaluate<NF, Epi, Dep>, grid1d(N, kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, cs, x1, x2, g.n1, g.n2,
                   xStable ? 1 : 0, epi, std::size_t(0), std::size_t(0), g.pairs, guardStride(g));
     }
 }

@@ -55,11 +55,6 @@ inline unsigned bandBlocks(const GridDims& g) { return static_cast<unsigned>(g.n
 // the address arithmetic of the 16 taps, which an asm volatile load per tap did not.)
 __device__ __forceinline__ double ldAfterWait(const double* p) { return *p; }
 
-// First-tap row/column and weights of a departure point along one axis: from the coordinate
-// (slab windows, whose departure points are per call) or from its packed cell (interp.cuh).
-__device__ __forceinline__ int depCell(double x, double invh, int n, double w[4]) { return cellBase(x, invh, n, w); }
-__device__ __forceinline__ int depCell(Cell u, double, int, double w[4]) { return cellDecode(u, w); }
-
 // Coefficient window of a slab-decomposed grid (slab.py): the coefficients hold `rows` padded
 // rows, window row w = global grid row base + w (mod n1), instead of the whole periodically
 // padded field.  A departure cell whose 4 tap rows fall outside the window sets *err.
@@ -212,7 +207,10 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ 
         if (t == 0) {
             double m = red[0];
             for (int w = 1; w < TW / 32; ++w) m = fmax(m, red[w]);
-            epi.guardPartials[pair * gE + (r - pair * n1)] = m;
+            if constexpr (kWindow)
+                epi.guardPartials[r] = m;  // slab rows: per-row partials (slab.py reduces them)
+            else
+                guardMax(epi.guardPartials + pair, m);
         }
     }
     // the next prefilter's input check (checkFinite(u, "prefilter"), interp.cpp:76)

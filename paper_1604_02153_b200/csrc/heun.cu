@@ -258,7 +258,6 @@ void HeunTransport::forward(const double* m0, double* nodes, double* stages, boo
         heunStep(nodes + (j - 1) * N, nodes + j * N, stages + (j - 1) * N, true, nullptr, nullptr);
         launchFieldMax(ctx, g, nodes + j * N, log.partial(j));
     }
-    log.finalize(ctx);
     log.check(ctx, "state", nt, true, guard, 0);
 }
 
@@ -271,7 +270,6 @@ void HeunTransport::backward(const double* lam1, double* nodes, double* stages, 
         heunStep(nodes + j * N, nodes + (j - 1) * N, stages + (j - 1) * N, false, nullptr, nullptr);
         launchFieldMax(ctx, g, nodes + (j - 1) * N, log.partial(j - 1));
     }
-    log.finalize(ctx);
     log.check(ctx, "adjoint", nt, false, guard, nt);
 }
 
@@ -289,7 +287,6 @@ void HeunTransport::stateFinal(const double* m0, double* out) {
         launchFieldMax(ctx, g, dst, log.partial(j));
         cur = dst;
     }
-    log.finalize(ctx);
     log.check(ctx, "state", nt, true, true, 0);
 }
 
@@ -307,7 +304,6 @@ void HeunTransport::adjointFinal(const double* lam1, double* out) {
         launchFieldMax(ctx, g, dst, log.partial(j - 1));
         cur = dst;
     }
-    log.finalize(ctx);
     log.check(ctx, "adjoint", nt, false, true, nt);
 }
 

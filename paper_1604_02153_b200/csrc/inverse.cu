@@ -417,7 +417,10 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
             launchPrefilter(ctx, g, vt1, cv, tmp, nullptr);
             launchPrefilter(ctx, g, vt2, cv + P, tmp, nullptr);
         }
-        launchEvaluate<2>(ctx, g, CoeffSet<2>{{cv, cv + P}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
+        if (fused_)
+            launchEvaluate<2>(ctx, g, CoeffSet<2>{{cv, cv + P}}, Cf, Cf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
+        else
+            launchEvaluate<2>(ctx, g, CoeffSet<2>{{cv, cv + P}}, Xf, Xf + N, EpiStore2{nullptr, vtD, vtD + N}, true);
     }
     auto wOf = [&](int j) { return ht * ((j == 0 || j == nt) ? 0.5 : 1.0); };
     if (fused_) {
@@ -451,13 +454,12 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
                              b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
             if (last) {
                 waitReg();
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, true);
             } else {
                 launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, R[(j - 1) & 1],
                                                    adjLog_->flag(j - 1));
             }
         }
-        adjLog_->finalize(ctx);
         return;
     }
     for (int j = 1; j <= nt; ++j) {
@@ -481,7 +483,6 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
         if (j == 1) waitReg();
         launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
     }
-    adjLog_->finalize(ctx);
 }
 
 // Full-Newton data term (HessianOperator::Impl::dataTerm FN branch, inverse.cpp:187-211, SL):

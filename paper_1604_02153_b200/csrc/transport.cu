@@ -42,24 +42,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_fieldmax(const double* __restric
     if (threadIdx.x == 0) {
         double m = red[0];
         for (int w = 1; w < kEvalBlock / 32; ++w) m = fmax(m, red[w]);
-        partial[guardEntry(blockIdx.x, blocksPer, gE)] = m;
-    }
-}
-
-// Per (step, pair) maximum of the guard partials: block = step * pairs + pair reduces the
-// pair's `per` entries (blocks per step = pairs * per).
-__global__ void k_stepmax(const double* partials, unsigned per, double* out) {
-    const double* p = partials + static_cast<std::size_t>(blockIdx.x) * per;
-    double m = 0.0;
-    for (unsigned i = threadIdx.x; i < per; i += blockDim.x) m = fmax(m, p[i]);
-    __shared__ double red[32];
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t = fmax(t, red[w]);
-        out[blockIdx.x] = t;
+        guardMax(partial + blockIdx.x / blocksPer, m);
     }
 }
 
@@ -83,30 +66,18 @@ void launchFieldMax(Ctx& ctx, const GridDims& g, const double* f, double* partia
 thread_local bool g_collectGuards = false;
 
 void GuardLog::ensure(int nsteps, const GridDims& g) {
-    const unsigned nblocks = guardBlocks(g);
-    if (nsteps <= steps && nblocks == blocks && g.pairs == pairs) return;
+    if (nsteps <= steps && g.pairs == pairs) return;
     if (g.pairs > 1 && g.pointsPer() % kEvalBlock != 0)
         throw NotSupported("batched pairs: n1 * n2 must be a multiple of 256");
     steps = nsteps;
-    blocks = nblocks;
     pairs = g.pairs;
-    partials.alloc(sizeof(double) * static_cast<std::size_t>(steps) * blocks);
     stepMax.alloc(sizeof(double) * steps * pairs);
     flags.alloc(sizeof(unsigned) * steps);
 }
 
 void GuardLog::reset(Ctx& ctx) {
     VRG_CUDA(cudaMemsetAsync(flags.d(), 0, sizeof(unsigned) * steps, ctx.stream));
-    // kernels with fewer blocks than `blocks` (band kernels) leave the tail entries untouched
-    VRG_CUDA(cudaMemsetAsync(partials.d(), 0, sizeof(double) * steps * blocks, ctx.stream));
-}
-
-void GuardLog::finalize(Ctx& ctx) {
-    {
-        LaunchScope ls_(ctx, "k_stepmax");
-        k_stepmax<<<steps * pairs, 256, 0, ctx.stream>>>(partials.d(), blocks / pairs, stepMax.d());
-    }
-    VRG_LAUNCH_CHECK();
+    VRG_CUDA(cudaMemsetAsync(stepMax.d(), 0, sizeof(double) * steps * pairs, ctx.stream));
 }
 
 void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep) {
@@ -279,7 +250,7 @@ void Solver::continuityBand(const double* lam1, DstFn dst) {
     for (int j = nt; j >= 1; --j) {
         const EpiContinuity epi{log.partial(j - 1), dvd, dv, ht, dst(j)};
         if (j == 1) {
-            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
+            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, true);
         } else {
             launchEvalBand<EpiContinuity, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                 log.flag(j - 1));
@@ -302,7 +273,7 @@ void Solver::state(const double* m0, double* traj, bool guard) {
         for (int j = 1; j <= nt; ++j) {
             const EpiStateStep epi{log.partial(j), traj + j * N};
             if (j == nt) {
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, true);
             } else {
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                    log.flag(j));
@@ -317,7 +288,6 @@ void Solver::state(const double* m0, double* traj, bool guard) {
         }
     }
     ctx.interps += nt;
-    log.finalize(ctx);
     log.check(ctx, "state", nt, true, guard, 0);
 }
 
@@ -335,7 +305,7 @@ void Solver::stateFinal(const double* m0, double* out) {
             double* dst = (j == nt) ? out : buf + (j % 2) * N;
             const EpiStateStep epi{log.partial(j), dst};
             if (j == nt) {
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, X, X + N, epi, true);
+                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, true);
             } else {
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                    log.flag(j));
@@ -352,7 +322,6 @@ void Solver::stateFinal(const double* m0, double* out) {
         }
     }
     ctx.interps += nt;
-    log.finalize(ctx);
     log.check(ctx, "state", nt, true, true, 0);
 }
 
@@ -368,7 +337,6 @@ void Solver::adjoint(const double* lam1, double* traj, bool guard) {
         for (int j = nt; j >= 1; --j)
             continuityStep(traj + j * N, traj + (j - 1) * N, kBackward, log.partial(j - 1), log.flag(j));
     }
-    log.finalize(ctx);
     log.check(ctx, "adjoint", nt, false, guard, nt);
 }
 
@@ -388,7 +356,6 @@ void Solver::adjointFinal(const double* lam1, double* out) {
             cur = dst;
         }
     }
-    log.finalize(ctx);
     log.check(ctx, "adjoint", nt, false, true, nt);
 }
 

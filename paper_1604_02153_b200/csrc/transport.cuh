@@ -39,20 +39,18 @@ struct CollectGuardsScope {
 
 struct GuardLog {
     int steps = 0;        // number of step slots (nt+1)
-    unsigned blocks = 0;  // guard partials per step (pairs * guardStride)
     int pairs = 1;
-    DBuf partials;        // steps*blocks
-    DBuf stepMax;         // steps x pairs doubles
+    DBuf stepMax;         // steps x pairs doubles: per-step guard maxima (atomic max, eval.cuh guardMax)
     DBuf flags;           // steps unsigned
     // batch (pairs > 1): check() records each pair's verdict instead of throwing (0 ok, else the
     // C ABI status of the error the reference would throw) and its message
     std::vector<int> pairStatus;
     std::vector<std::string> pairError;
     void ensure(int nsteps, const GridDims& g);
-    double* partial(int step) const { return partials.d() + static_cast<std::size_t>(step) * blocks; }
+    // the kernels' guard slot of a step (one per pair)
+    double* partial(int step) const { return stepMax.d() + static_cast<std::size_t>(step) * pairs; }
     unsigned* flag(int step) const { return flags.as<unsigned>() + step; }
     void reset(Ctx& ctx);
-    void finalize(Ctx& ctx);  // per-step maxima from the partials (stream-ordered)
     // Host readback; throws the reference's first error in solve order.
     //   order: steps visited, each (prefilter-input step index, output step index).
     void check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep);

@@ -10,7 +10,7 @@ obj=/tmp/vrg_variant_$name
 mkdir -p "$out" "$obj"
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 pids=()
-for f in runtime interp spectral transport heun inverse precond cabi; do
+for f in runtime interp spectral transport heun inverse precond batch cabi; do
   /usr/local/cuda/bin/nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $flags \
     -c "$root/paper_1604_02153_b200/csrc/$f.cu" -o "$obj/$f.o" &
   pids+=($!)
