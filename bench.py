@@ -184,7 +184,8 @@ KERNEL_CLASSES_BAND = {
     6: ("reference: field axpy kernel (not in matvec)", 0, 3),
 }
 # ncu kernel-name fragments of the band-path classes (for the traffic lookup)
-NCU_NAMES = {7: "k_eval_band<EpiIncState, 1, 0>", 8: "EpiAdjointBF, 1, 0>", 4: "k_pf_cols_reg"}
+# ncu names of the band kernels at 1024^2 (strip blocks, evalband.cuh k_eval_strip)
+NCU_NAMES = {7: "k_eval_strip<EpiIncState, 1, 128>", 8: "EpiAdjointBF, 1, 128>", 4: "k_pf_cols_reg"}
 KERNEL_CLASSES_PLAIN = {
     0: ("evaluate/incstate (K6)", NT - 1, 12),
     1: ("evaluate/adjoint_bodyforce (K5+K8)", NT, 12),
@@ -646,7 +647,7 @@ def main():
         # DRAM traffic of the dominant kernel per launch, from the committed ncu --set full
         # capture (profiles/, cold-cache replay: an upper bound of the warm per-launch traffic)
         traffic = None
-        traffic_file = next((f for f in ("r2_ncu_traffic.json", "r1_ncu_traffic.json")
+        traffic_file = next((f for f in ("r2s3_ncu_traffic.json", "r2_ncu_traffic.json", "r1_ncu_traffic.json")
                              if os.path.exists(os.path.join(ROOT, "profiles", f))), "r1_ncu_traffic.json")
         try:
             with open(os.path.join(ROOT, "profiles", traffic_file)) as f:

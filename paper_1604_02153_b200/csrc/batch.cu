@@ -602,11 +602,44 @@ std::vector<SolverReport> newtonSolveBatch(Ctx& ctx, const GridDims& gAll, const
     fill(ctx, 2 * gAll.points(), 0.0, vAll.d());
     copy(ctx, gAll.points(), mTAll, finalAll.d());
 
-    // eigenvalue bounds at v = 0, once per solve (newton.cpp:36-40), per pair
+    // eigenvalue bounds at v = 0, once per solve (newton.cpp:36-40), per pair: the pairs' coarse
+    // problems at v = 0 (all coarse nt = 2) as one batched coarse operator and their Lanczos
+    // runs in lockstep (lanczosEmaxPairs), each pair's estimate that of its own estimateEigsAt
     if (pc.kind == kPcTwoLevel && !pc.hasEig) {
+        std::vector<char> single(P, 1);  // pairs estimated on their own
+        if (P > 1) {
+            std::vector<int> idAll(P);
+            for (int k = 0; k < P; ++k) idAll[k] = k;
+            const std::vector<char> allOn(P, 1);
+            CollectGuardsScope collect(true);
+            CountScope cs(ctx);
+            CoarseOperator coarse(ctx, gAll, nullptr, mRAll, mTAll, model, kCoarseCfl);
+            cs.to(counts, idAll, allOn);
+            std::vector<double> em;
+            std::vector<char> fb;
+            LinOpDev op = [&](const double* x, double* o) { coarse.applySplit(x, o); };
+            coarse.hess->beginDeferredGuards(31);
+            const bool done = lanczosEmaxPairs(ctx, coarse.gc, op, 30, 0x5eed, em, fb,
+                                               [&](const std::vector<char>& on) { cs.to(counts, idAll, on); });
+            coarse.hess->endDeferredGuards();
+            if (done) {
+                for (int k = 0; k < P; ++k) {
+                    if (coarse.hess->pairStatus[k]) {  // estimateEigsAt would have thrown for this pair
+                        status[k] = coarse.hess->pairStatus[k];
+                        errors[k] = coarse.hess->pairError[k];
+                        active[k] = 0;
+                        single[k] = 0;
+                    } else if (!fb[k]) {
+                        eMax[k] = em[k];
+                        single[k] = 0;
+                    }
+                }
+            }
+        }
         for (int k = 0; k < P; ++k) {
+            if (!single[k]) continue;
             const long long f0 = ctx.ffts, i0 = ctx.interps;
-            CollectGuardsScope single(false);  // a single-pair operation: its errors throw
+            CollectGuardsScope one(false);  // a single-pair operation: its errors throw
             eMax[k] = estimateEigsAt(ctx, gAll.one(), nullptr, mRAll + k * Np, mTAll + k * Np, model, kCoarseCfl).second;
             counts[k].ffts += ctx.ffts - f0;
             counts[k].interps += ctx.interps - i0;

@@ -1,3 +1,4 @@
+#include <functional>
 // Device-resident two-level preconditioner, Chebyshev / PCG / Lanczos and the inexact
 // Gauss-Newton-Krylov driver.  Host control flow mirrors src/precond.cpp and src/newton.cpp
 // line for line (same decisions, same comparisons); all vectors and operator applications
@@ -150,26 +151,48 @@ __device__ __forceinline__ double lzClusterSum(double v, LzRed& red, int& parity
     return t;
 }
 
-template <int kPer>
+// beta_{j-1} of every pair of a batch (kernel parameter)
+constexpr int kLzMaxPairs = 64;
+struct LzBeta {
+    double v[kLzMaxPairs];
+};
+
+// Batches of stacked pairs (GridDims::pairs): one cluster per pair (blockIdx.x / kLzCtas), the
+// pair's vector being its slots of the two components (nPer values each, component stride
+// nTot); with one pair this is the contiguous vector of length n = 2 nPer.  betaPrev, alphaOut
+// and bsqOut are per pair (alphaOut at stride alphaStride).
+template <int kPer, bool kBatch>
 __global__ void __cluster_dims__(kLzCtas, 1, 1) __launch_bounds__(kLzThreads, 1)
-    k_lanczos_orth(double* __restrict__ w, const double* __restrict__ Q, std::size_t n, int j, int nb, double betaPrev,
-                   double hh, double* __restrict__ alphaOut, double* __restrict__ bsqOut) {
+    k_lanczos_orth(double* __restrict__ w, const double* __restrict__ Q, std::size_t nPer, std::size_t nTot, int j,
+                   int nb, LzBeta betaPrev, double hh, double* __restrict__ alphaOut,
+                   int alphaStride, double* __restrict__ bsqOut) {
     __shared__ LzRed red;
     int parity = 0;
-    const std::size_t base = static_cast<std::size_t>(blockIdx.x) * kLzThreads + threadIdx.x;
+    const int pair = blockIdx.x / kLzCtas;
+    const std::size_t n = 2 * nPer;  // elements of one pair's vector
+    const std::size_t base = static_cast<std::size_t>(blockIdx.x % kLzCtas) * kLzThreads + threadIdx.x;
+    const std::size_t qStride = 2 * nTot;  // one basis vector of the batch
     constexpr std::size_t kStride = static_cast<std::size_t>(kLzCtas) * kLzThreads;
+    // batch offset of element e of this pair's vector
+    auto at = [&](std::size_t e) {
+        if constexpr (kBatch)
+            return e < nPer ? pair * nPer + e : nTot + pair * nPer + (e - nPer);
+        else
+            return e;
+    };
+    const bool lead = blockIdx.x % kLzCtas == 0 && threadIdx.x == 0;
     double x[kPer];
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const std::size_t e = base + k * kStride;
-        x[k] = e < n ? w[e] : 0.0;
+        x[k] = e < n ? w[at(e)] : 0.0;
     }
     auto qv = [&](int i, double (&q)[kPer]) {
-        const double* qi = Q + static_cast<std::size_t>(i) * n;
+        const double* qi = Q + static_cast<std::size_t>(i) * qStride;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const std::size_t e = base + k * kStride;
-            q[k] = e < n ? qi[e] : 0.0;
+            q[k] = e < n ? qi[at(e)] : 0.0;
         }
     };
     // kPer = 8 re-reads q_i (L1/L2 hits) after the cluster sum instead of holding it across
@@ -177,23 +200,23 @@ __global__ void __cluster_dims__(kLzCtas, 1, 1) __launch_bounds__(kLzThreads, 1)
     constexpr bool kReload = kPer >= 8;
     auto project = [&](int i, bool storeAlpha) {
         double q[kReload ? 1 : kPer];
-        const double* qi = Q + static_cast<std::size_t>(i) * n;
+        const double* qi = Q + static_cast<std::size_t>(i) * qStride;
         double s = 0.0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const std::size_t e = base + k * kStride;
-            const double qk = e < n ? qi[e] : 0.0;
+            const double qk = e < n ? qi[at(e)] : 0.0;
             if constexpr (!kReload) q[k] = qk;
             s += x[k] * qk;
         }
         const double c = hh * lzClusterSum(s, red, parity);
-        if (storeAlpha && blockIdx.x == 0 && threadIdx.x == 0) *alphaOut = c;
+        if (storeAlpha && lead) alphaOut[static_cast<std::size_t>(pair) * alphaStride] = c;
         const double a = -c;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             if constexpr (kReload) {
                 const std::size_t e = base + k * kStride;
-                x[k] = x[k] + a * (e < n ? qi[e] : 0.0);
+                x[k] = x[k] + a * (e < n ? qi[at(e)] : 0.0);
             } else {
                 x[k] = x[k] + a * q[k];
             }
@@ -202,7 +225,7 @@ __global__ void __cluster_dims__(kLzCtas, 1, 1) __launch_bounds__(kLzThreads, 1)
     if (j > 0) {
         double q[kPer];
         qv(j - 1, q);
-        const double a = -betaPrev;
+        const double a = -betaPrev.v[pair];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) x[k] = x[k] + a * q[k];
     }
@@ -212,25 +235,36 @@ __global__ void __cluster_dims__(kLzCtas, 1, 1) __launch_bounds__(kLzThreads, 1)
 #pragma unroll
     for (int k = 0; k < kPer; ++k) s += x[k] * x[k];
     const double bsq = hh * lzClusterSum(s, red, parity);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *bsqOut = bsq;
+    if (lead) bsqOut[pair] = bsq;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const std::size_t e = base + k * kStride;
-        if (e < n) w[e] = x[k];
+        if (e < n) w[at(e)] = x[k];
     }
 }
 
-bool launchLanczosOrth(Ctx& ctx, double* w, const double* Q, std::size_t n, int j, int nb, double betaPrev, double hh,
-                       double* alphaOut, double* bsqOut) {
-    const std::size_t per = (n + kLzCtas * kLzThreads - 1) / (kLzCtas * kLzThreads);
+// One pair or a batch of `pairs` (alphaOut / bsqOut per pair on the device).
+bool launchLanczosOrth(Ctx& ctx, double* w, const double* Q, std::size_t nPer, int pairs, int j, int nb,
+                       const LzBeta& betaPrev, double hh, double* alphaOut, int alphaStride, double* bsqOut) {
+    if (pairs > kLzMaxPairs) return false;
+    const std::size_t per = (2 * nPer + kLzCtas * kLzThreads - 1) / (kLzCtas * kLzThreads);
     LaunchScope ls_(ctx, "k_lanczos_orth");
-    const dim3 grid(kLzCtas), block(kLzThreads);
-#define VRG_LZ(P) k_lanczos_orth<P><<<grid, block, 0, ctx.stream>>>(w, Q, n, j, nb, betaPrev, hh, alphaOut, bsqOut)
-    if (per <= 1) VRG_LZ(1);
-    else if (per <= 2) VRG_LZ(2);
-    else if (per <= 4) VRG_LZ(4);
-    else if (per <= 8) VRG_LZ(8);
-    else return false;
+    const dim3 grid(kLzCtas * pairs), block(kLzThreads);
+    const std::size_t nTot = nPer * pairs;
+#define VRG_LZ(P, B) \
+    k_lanczos_orth<P, B><<<grid, block, 0, ctx.stream>>>(w, Q, nPer, nTot, j, nb, betaPrev, hh, alphaOut, alphaStride, bsqOut)
+    if (pairs == 1) {
+        if (per <= 1) VRG_LZ(1, false);
+        else if (per <= 2) VRG_LZ(2, false);
+        else if (per <= 4) VRG_LZ(4, false);
+        else if (per <= 8) VRG_LZ(8, false);
+        else return false;
+    } else {  // a batch: one cluster per pair, up to 4 values per thread (coarse grids up to 128^2)
+        if (per <= 1) VRG_LZ(1, true);
+        else if (per <= 2) VRG_LZ(2, true);
+        else if (per <= 4) VRG_LZ(4, true);
+        else return false;
+    }
 #undef VRG_LZ
     VRG_LAUNCH_CHECK();
     return true;
@@ -279,8 +313,10 @@ void randomBandLimitedVelocity(Ctx& ctx, const GridDims& g, std::uint64_t seed, 
 // ------------------------------------------------------------------------------ coarse operator
 CoarseOperator::CoarseOperator(Ctx& c, const GridDims& fg, const double* v, const double* mR, const double* mT,
                                const Model& model, double coarseCfl)
-    : ctx(c), fine(fg), gc(fg.n1 / 2, fg.n2 / 2) {
+    : ctx(c), fine(fg), gc(fg.n1 / 2, fg.n2 / 2, fg.pairs) {
     checkGrid(gc.n1, gc.n2);
+    // a batch of stacked pairs shares one coarse step count: only at v = 0 (every pair nt = 2)
+    if (fg.pairs > 1 && v) throw NotSupported("CoarseOperator: a batch of pairs at v = 0 only");
     const std::size_t Nc = gc.points(), Nf = fine.points();
     mRc.alloc(sizeof(double) * Nc);
     mTc.alloc(sizeof(double) * Nc);
@@ -575,7 +611,9 @@ double lanczosEmax(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, s
         copy(ctx, n, Q(j), qIn);
         op(qIn, w);
         double b;
-        if (launchLanczosOrth(ctx, w, Q(0), n, j, nb, j > 0 ? beta[j - 1] : 0.0, hh, alphaDev + j, cDev)) {
+        LzBeta bp{};
+        bp.v[0] = j > 0 ? beta[j - 1] : 0.0;
+        if (launchLanczosOrth(ctx, w, Q(0), N, 1, j, nb, bp, hh, alphaDev + j, 1, cDev)) {
             ++nAlpha;
             b = std::sqrt(readScalar(ctx, cDev));  // cDev = |w|^2
         } else {
@@ -617,6 +655,103 @@ double coarseLanczosEmax(Ctx& ctx, CoarseOperator& coarse, int steps, std::uint6
     }
     coarse.hess->endDeferredGuards();
     return e;
+}
+
+namespace {
+__global__ void k_scale_pairs(std::size_t n, std::size_t nPer, int P, LzBeta a, const double* __restrict__ w,
+                              double* __restrict__ out) {
+    const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+    for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double c = a.v[(i / nPer) % static_cast<std::size_t>(P)];
+        out[i] = c == 0.0 ? 0.0 : w[i] * c;  // lincomb(1/b, w, 0, w) of the single-pair path; 0 retires a pair
+    }
+}
+}  // namespace
+
+bool lanczosEmaxPairs(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, std::uint64_t seed,
+                      std::vector<double>& emax, std::vector<char>& fallback,
+                      const std::function<void(const std::vector<char>&)>& counted) {
+    const int P = g.pairs;
+    const std::size_t nPer = g.pointsPer(), N = g.points(), n = 2 * N;
+    if (P > kLzMaxPairs || 2 * nPer > static_cast<std::size_t>(4) * kLzCtas * kLzThreads) return false;
+    const double hh = g.h1() * g.h2();
+    emax.assign(P, 1.0);
+    fallback.assign(P, 0);
+    DBuf basisBuf(sizeof(double) * n * (steps + 1));
+    DBuf wBuf(sizeof(double) * 2 * n);
+    DBuf coefBuf(sizeof(double) * (static_cast<std::size_t>(steps) * P + P));
+    auto Q = [&](int j) { return basisBuf.d() + static_cast<std::size_t>(j) * n; };
+    double* w = wBuf.d();
+    double* qIn = w + n;
+    double* alphaDev = coefBuf.d();  // pair k, step j at k * steps + j
+    double* bsqDev = alphaDev + static_cast<std::size_t>(steps) * P;
+    // the seeded start vector of lanczosEmax, the same in every pair's slots
+    const GridDims one = g.one();
+    const std::size_t n1v = 2 * nPer;
+    double* q0 = ctx.scratchBuf(140, sizeof(double) * n1v);
+    randomBandLimitedVelocity(ctx, one, seed, q0);
+    const double nq = vnormL2(ctx, one, q0);
+    if (!(nq > 0.0)) return true;  // every pair: eMax 1 (lanczosEmax's early return)
+    axpby(ctx, n1v, 0.0, q0, 1.0 / nq, q0);
+    for (int k = 0; k < P; ++k)
+        for (int c = 0; c < 2; ++c)
+            VRG_CUDA(cudaMemcpyAsync(Q(0) + c * N + k * nPer, q0 + c * nPer, sizeof(double) * nPer,
+                                     cudaMemcpyDeviceToDevice, ctx.stream));
+    std::vector<std::vector<double>> beta(P);
+    std::vector<int> nAlpha(P, 0);
+    std::vector<char> on(P, 1);
+    std::vector<double> bsq(P);
+    int nb = 1;
+    for (int j = 0; j < steps; ++j) {
+        copy(ctx, n, Q(j), qIn);
+        op(qIn, w);
+        counted(on);
+        LzBeta bp{};
+        for (int k = 0; k < P; ++k) bp.v[k] = (j > 0 && on[k]) ? beta[k][j - 1] : 0.0;
+        if (!launchLanczosOrth(ctx, w, Q(0), nPer, P, j, nb, bp, hh, alphaDev + j, steps, bsqDev)) return false;
+        VRG_CUDA(cudaMemcpyAsync(bsq.data(), bsqDev, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        LzBeta inv{};
+        bool any = false;
+        for (int k = 0; k < P; ++k) {
+            if (!on[k]) continue;
+            ++nAlpha[k];
+            const double b = std::sqrt(bsq[k]);
+            if (!std::isfinite(b)) {
+                fallback[k] = 1;  // lanczosEmax: power iteration
+                on[k] = 0;
+            } else if (b < 1e-12) {
+                on[k] = 0;
+            } else {
+                beta[k].push_back(b);
+                inv.v[k] = 1.0 / b;
+                any = true;
+            }
+        }
+        {
+            LaunchScope ls_(ctx, "k_scale_pairs");
+            k_scale_pairs<<<elemBlocks(ctx, n), 256, 0, ctx.stream>>>(n, nPer, P, inv, w, Q(nb));
+        }
+        VRG_LAUNCH_CHECK();
+        ++nb;
+        if (!any) break;
+    }
+    std::vector<double> alpha(static_cast<std::size_t>(steps) * P);
+    VRG_CUDA(cudaMemcpyAsync(alpha.data(), alphaDev, sizeof(double) * alpha.size(), cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    for (int k = 0; k < P; ++k) {
+        if (fallback[k]) continue;
+        if (nAlpha[k] == 0) {
+            fallback[k] = 1;
+            continue;
+        }
+        std::vector<double> a(alpha.begin() + static_cast<std::ptrdiff_t>(k) * steps,
+                              alpha.begin() + static_cast<std::ptrdiff_t>(k) * steps + nAlpha[k]);
+        std::vector<double> b = beta[k];
+        b.resize(a.size() - 1);
+        emax[k] = tridiagMaxEig(a, b);
+    }
+    return true;
 }
 
 std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const double* v, const double* mR,

@@ -85,6 +85,16 @@ bool applyTwoLevel(Ctx& ctx, const GridDims& g, const double* r, CoarseOperator&
 // lanczosEmax of a coarse operator's split Hessian with its guard checks deferred (precond.cpp:134-161)
 double coarseLanczosEmax(Ctx& ctx, CoarseOperator& coarse, int steps, std::uint64_t seed);
 
+// lanczosEmax on the stacked pairs of a batch in lockstep: one operator application and one
+// orthogonalisation launch (a thread-block cluster per pair) per step for all pairs, each pair's
+// arithmetic that of lanczosEmax on it alone.  emax[k]: pair k's estimate; fallback[k]: pair k
+// needs lanczosEmax's power-iteration fallback (non-finite beta / no step) from the caller.
+// counted(on) after each operator application, with the pairs that took part in it.  False
+// (nothing decided) when the batch does not fit the cluster kernel (coarse grids above 128^2).
+bool lanczosEmaxPairs(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps, std::uint64_t seed,
+                      std::vector<double>& emax, std::vector<char>& fallback,
+                      const std::function<void(const std::vector<char>&)>& counted);
+
 // estimateEigsAt / estimateEigs (precond.cpp:242-258): (1, Lanczos eMax of the coarse split
 // Hessian at v; v = nullptr means v = 0).
 std::pair<double, double> estimateEigsAt(Ctx& ctx, const GridDims& g, const double* v, const double* mR,
