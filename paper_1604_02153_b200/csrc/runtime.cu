@@ -54,7 +54,10 @@ BlockCache& blockCache() {
     return *c;
 }
 constexpr std::size_t kCacheCap = std::size_t(48) << 30;  // beyond this, release (stream-ordered)
-constexpr std::uint64_t kPoolKeep = std::uint64_t(16) << 30;  // the pool keeps this much when trimming
+// The pool keeps what it holds (no trimming at synchronisation points: a trim unmaps memory the
+// next allocation maps again, and the batched lanes synchronise constantly); an allocation that
+// fails trims it explicitly (cachedAlloc).
+constexpr std::uint64_t kPoolKeep = ~std::uint64_t(0);
 
 bool capturing(cudaStream_t s) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
