@@ -184,6 +184,7 @@ KERNEL_CLASSES_BAND = {
     6: ("reference: field axpy kernel (not in matvec)", 0, 3),
 }
 # ncu kernel-name fragments of the band-path classes (for the traffic lookup)
+L2_STREAM_GBS = 10200.0  # streaming read of an 80 MB L2-resident set on B200 (tools/probe/l2probe.cu)
 # ncu names of the band kernels at 1024^2 (strip blocks, evalband.cuh k_eval_strip)
 NCU_NAMES = {7: "k_eval_strip<EpiIncState, 1, 128>", 8: "EpiAdjointBF, 1, 128>", 4: "k_pf_cols_reg"}
 KERNEL_CLASSES_PLAIN = {
@@ -677,7 +678,12 @@ def main():
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_source": f"profiles/{traffic_file} (ncu --set full, dram__bytes_read+write)",
                          "bytes_per_launch": bytes_launch, "avg_launch_us": avg_s * 1e6,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650",
+                         "note": "algorithmic bytes count operands that stay L2-resident across steps (departure "
+                                 "cells, vt, vt_D, div v), so frac can exceed 1: the kernel is bound by the L2->SM "
+                                 "path; l2_frac = achieved / the 10.2 TB/s an 80 MB L2-resident stream reaches on "
+                                 "B200 (tools/probe/l2probe.cu, DESIGN.md section 4)",
+                         "l2_frac": (achieved / L2_STREAM_GBS) if achieved else None},
             "matvec_roofline": {"algorithmic_bytes": mv_bytes, "model": "(24 nt + 12) F, SURVEY 8(d)",
                                 "achieved_gbps": mv_bytes * r["value"] / world / 1e9,
                                 "frac": mv_bytes * r["value"] / world / 1e9 / peak},
