@@ -10,6 +10,7 @@
 #pragma once
 
 #include <atomic>
+#include <type_traits>
 
 #include "eval.cuh"
 
@@ -141,6 +142,9 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ 
     constexpr bool kPipe = sizeof(typename Epi::Pre) <= sizeof(double);
     Dep xa{}, xb{};
     typename Epi::Pre pre{};
+    // the unpipelined steps still run their departure cells one node ahead (two more registers:
+    // the gather waits for one memory round trip per node instead of two; no spills at 64)
+    constexpr bool kPipeDep = !kPipe && kGather;
     if constexpr (kPipe) {
         if (kGather) {
             xa = __ldg(x1 + r * n2 + t);
@@ -148,6 +152,9 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ 
         }
         pre = epi.prefetch(r * n2 + t);
         if (kGather) pdlWait();
+    } else if constexpr (kPipeDep) {
+        xa = __ldg(x1 + r * n2 + t);
+        xb = __ldg(x2 + r * n2 + t);
     }
     for (int k = 0; k < per; ++k) {
         const int col = t + TW * k;
@@ -170,7 +177,15 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ 
                 pre = epi.prefetch(p + TW);
             }
         } else {
-            if (kGather) {
+            if constexpr (kPipeDep) {
+                const int b1 = tapRow(depCell(xa, inv1, n1, w1));
+                const int b2 = depCell(xb, inv2, n2, w2);
+                base = b1 * PW + b2;
+                if (k + 1 < per) {
+                    xa = __ldg(x1 + p + TW);
+                    xb = __ldg(x2 + p + TW);
+                }
+            } else if (kGather) {
                 const int b1 = tapRow(depCell(__ldg(x1 + p), inv1, n1, w1));
                 const int b2 = depCell(__ldg(x2 + p), inv2, n2, w2);
                 base = b1 * PW + b2;
