@@ -7,6 +7,7 @@ namespace vrg {
 
 constexpr int kReduceThreads = 256;
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
+constexpr int kReduceTicketSlots = 64;  // per-pair tickets of the fused reductions (pairs per batch)
 
 // Launch-only reductions: the result lands in a device scalar (slot 0..31 of the context's
 // reduction area) and stays stream-ordered.

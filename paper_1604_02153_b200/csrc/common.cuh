@@ -186,6 +186,7 @@ struct Ctx {
     // Scratch spectra / fields reused across calls (grown on demand, freed with the context).
     std::map<std::pair<int, std::size_t>, DBuf> scratch;
     DBuf reduce;  // reduction scratch (partials + results)
+    DBuf reduceTickets;  // per-pair block counters of the fused two-stage reductions (self-resetting)
     double* hostScalars = nullptr;  // pinned staging for scalar reads
     // External fine-level GN data term for newtonSolve (C ABI vrg_set_fine_operator): the
     // plug-in point of precond::LinOp (precond.hpp:25) that a slab-decomposed operator fills.

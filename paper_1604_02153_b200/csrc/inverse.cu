@@ -679,9 +679,9 @@ void Hessian::guardAfterMatvec() {
         return;
     }
     const std::size_t steps = static_cast<std::size_t>(nt + 1), per = steps * g.pairs;
-    VRG_CUDA(cudaMemcpyAsync(deferMax_.d() + per * deferCount_, adjLog_->stepMax.d(), sizeof(double) * per,
+    VRG_CUDA(cudaMemcpyAsync(deferMax_.d() + per * deferCount_, adjLog_->stepMax(), sizeof(double) * per,
                              cudaMemcpyDeviceToDevice, ctx.stream));
-    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + steps * deferCount_, adjLog_->flags.d(),
+    VRG_CUDA(cudaMemcpyAsync(deferFlags_.as<unsigned>() + steps * deferCount_, adjLog_->flags(),
                              sizeof(unsigned) * steps, cudaMemcpyDeviceToDevice, ctx.stream));
     ++deferCount_;
 }
@@ -908,12 +908,11 @@ Hessian::~Hessian() {
         cudaEventDestroy(evJoin_);
         cudaStreamDestroy(aux_);
     }
-    if (hostGuard_) {
+    if (guardStream_) {
         cudaStreamSynchronize(guardStream_);
         for (auto& e : evGuard_) cudaEventDestroy(e);
         for (auto& e : evDone_) cudaEventDestroy(e);
         cudaStreamDestroy(guardStream_);
-        cudaFreeHost(hostGuard_);
     }
     for (auto& kv : graphs_) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -937,9 +936,7 @@ void Hessian::applyQueued(const double* vt1, const double* vt2, double* o1, doub
         return;
     }
     NvtxRange nv_("HessianOperator::apply (queued)");
-    const std::size_t steps = static_cast<std::size_t>(nt + 1);
-    if (!hostGuard_) {
-        VRG_CUDA(cudaMallocHost(&hostGuard_, 2 * steps * (sizeof(double) + sizeof(unsigned))));
+    if (!guardStream_) {
         VRG_CUDA(cudaStreamCreateWithFlags(&guardStream_, cudaStreamNonBlocking));
         for (int s = 0; s < 2; ++s) {
             VRG_CUDA(cudaEventCreateWithFlags(&evGuard_[s], cudaEventDisableTiming));
@@ -961,19 +958,16 @@ void Hessian::applyQueued(const double* vt1, const double* vt2, double* o1, doub
     countDataTerm();
     VRG_CUDA(cudaEventRecord(evDone_[slot], ctx.stream));
     VRG_CUDA(cudaStreamWaitEvent(guardStream_, evDone_[slot], 0));
-    double* mx = hostGuard_ + slot * steps;
-    unsigned* fl = reinterpret_cast<unsigned*>(hostGuard_ + 2 * steps) + slot * steps;
     const GuardLog& L = guardLogs_[slot];
-    VRG_CUDA(cudaMemcpyAsync(mx, L.stepMax.d(), sizeof(double) * steps, cudaMemcpyDeviceToHost, guardStream_));
-    VRG_CUDA(cudaMemcpyAsync(fl, L.flags.d(), sizeof(unsigned) * steps, cudaMemcpyDeviceToHost, guardStream_));
+    VRG_CUDA(cudaMemcpyAsync(L.host, L.buf.d(), L.bytes(), cudaMemcpyDeviceToHost, guardStream_));
     VRG_CUDA(cudaEventRecord(evGuard_[slot], guardStream_));
 }
 
 void Hessian::checkQueued(int slot) {
     if (!queuedGuards()) return;  // applyQueued checked already
-    const std::size_t steps = static_cast<std::size_t>(nt + 1);
+    const GuardLog& L = guardLogs_[slot];
     VRG_CUDA(cudaEventSynchronize(evGuard_[slot]));
-    GuardLog::checkHost(hostGuard_ + slot * steps, reinterpret_cast<unsigned*>(hostGuard_ + 2 * steps) + slot * steps,
+    GuardLog::checkHost(L.host, reinterpret_cast<const unsigned*>(L.host + static_cast<std::size_t>(L.steps) * L.pairs),
                         "adjoint", nt, false, true, nt);
 }
 

@@ -124,8 +124,7 @@ private:
     int deferCap_ = 0, deferCount_ = 0;
     DBuf deferMax_, deferFlags_;
     void guardAfterMatvec();
-    double* hostGuard_ = nullptr;  // queued matvecs: 2 slots x [(nt+1) maxima | (nt+1) flags]
-    cudaStream_t guardStream_ = nullptr;
+    cudaStream_t guardStream_ = nullptr;  // queued matvecs: guard readback into guardLogs_[s].host
     cudaEvent_t evGuard_[2] = {nullptr, nullptr}, evDone_[2] = {nullptr, nullptr};
     long long lazyInterps_ = 0, lazyFfts_ = 0;
     bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh

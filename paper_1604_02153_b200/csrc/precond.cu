@@ -709,8 +709,7 @@ bool lanczosEmaxPairs(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps
         LzBeta bp{};
         for (int k = 0; k < P; ++k) bp.v[k] = (j > 0 && on[k]) ? beta[k][j - 1] : 0.0;
         if (!launchLanczosOrth(ctx, w, Q(0), nPer, P, j, nb, bp, hh, alphaDev + j, steps, bsqDev)) return false;
-        VRG_CUDA(cudaMemcpyAsync(bsq.data(), bsqDev, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx.stream));
-        ctx.sync();
+        readPairs(ctx, bsqDev, P, bsq.data());
         LzBeta inv{};
         bool any = false;
         for (int k = 0; k < P; ++k) {

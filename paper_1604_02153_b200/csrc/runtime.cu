@@ -187,6 +187,8 @@ Ctx::Ctx(int dev, cudaStream_t s) : device(dev) {
     VRG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
     l2Bytes = static_cast<std::size_t>(l2);
     reduce.alloc(sizeof(double) * (kReduceBlocks * 4 + 64));
+    reduceTickets.alloc(sizeof(unsigned) * kReduceTicketSlots);
+    VRG_CUDA(cudaMemsetAsync(reduceTickets.d(), 0, sizeof(unsigned) * kReduceTicketSlots, stream));
     VRG_CUDA(cudaMallocHost(&hostScalars, sizeof(double) * 64));
 }
 
@@ -286,12 +288,45 @@ __device__ __forceinline__ double warpMax(double v) {
     return v;
 }
 
+// Fused final stage of the two-stage reductions: the last block of a reduction (per pair:
+// blockIdx.y) to finish its partial takes a ticket and reduces the partials itself, with the
+// arithmetic of the 1024-thread final kernels it replaces (one launch instead of two; the
+// tickets reset themselves, so graph replays see them at 0).  "Virtual thread" i < 1024 holds
+// partial i (nb <= kReduceBlocks < 1024) or the identity, virtual warp w reduces its 32 values
+// with the xor butterfly, thread 0 then combines the 32 warp results in order.
+__device__ __forceinline__ bool lastBlockOf(unsigned* ticket) {
+    __shared__ bool last;
+    __threadfence();  // this block's partial (written by thread 0) before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+template <bool kMax>
+__device__ __forceinline__ double finalOf(const double* partial, int nb, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = 0; k < 1024 / kReduceThreads; ++k) {
+        const int i = k * kReduceThreads + threadIdx.x;
+        double v = i < nb ? __ldcg(partial + i) : 0.0;
+        v = kMax ? warpMax(v) : warpSum(v);
+        if (lane == 0) red[k * (kReduceThreads / 32) + warp] = v;
+    }
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < 32; ++w) t = kMax ? fmax(t, red[w]) : t + red[w];
+    return t;
+}
+
 // Stage 1: per-block partial sums of sum_i a_i*b_i for up to two (a,b) pairs (kept separate).
 __global__ void __launch_bounds__(kReduceThreads) k_dot_partial(const double* __restrict__ a0,
                                                                 const double* __restrict__ b0,
                                                                 const double* __restrict__ a1,
                                                                 const double* __restrict__ b1, std::size_t n,
-                                                                double* partial) {
+                                                                double* partial, unsigned* ticket, double scale,
+                                                                double* out) {
     double s0 = 0.0, s1 = 0.0;
     const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
     for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -315,39 +350,20 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot_partial(const double* __
         partial[blockIdx.x] = t0;
         partial[kReduceBlocks + blockIdx.x] = t1;
     }
-}
-
-// Stage 2: out = scale*(sum partial0) + scale*(sum partial1)  (dot per component, then added,
-// field.cpp:47-54).
-__global__ void k_dot_final(const double* partial, int nb, double scale, double* out) {
-    partial += static_cast<std::size_t>(blockIdx.x) * 2 * kReduceBlocks;  // block = pair of a batch
-    out += blockIdx.x;
-    __shared__ double r0[32], r1[32];
-    double s0 = 0.0, s1 = 0.0;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-        s0 += partial[i];
-        s1 += partial[kReduceBlocks + i];
-    }
-    s0 = warpSum(s0);
-    s1 = warpSum(s1);
-    if ((threadIdx.x & 31) == 0) {
-        r0[threadIdx.x >> 5] = s0;
-        r1[threadIdx.x >> 5] = s1;
-    }
-    __syncthreads();
+    if (!lastBlockOf(ticket)) return;
+    __shared__ double f0[32], f1[32];
+    const double t0 = finalOf<false>(partial, gridDim.x, f0);
+    const double t1 = finalOf<false>(partial + kReduceBlocks, gridDim.x, f1);
     if (threadIdx.x == 0) {
-        double t0 = 0.0, t1 = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
-            t0 += r0[w];
-            t1 += r1[w];
-        }
-        *out = scale * t0 + scale * t1;
+        *out = scale * t0 + scale * t1;  // dot per component, then added (field.cpp:47-54)
+        *ticket = 0;
     }
 }
 
 __global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial(const double* __restrict__ a0,
                                                                    const double* __restrict__ a1, std::size_t n,
-                                                                   double* partial) {
+                                                                   double* partial, unsigned* ticket, double scale,
+                                                                   double* out) {
     double m = 0.0;
     const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
     for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -362,6 +378,13 @@ __global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial(const double*
         double t = 0.0;
         for (int w = 0; w < kReduceThreads / 32; ++w) t = fmax(t, r[w]);
         partial[blockIdx.x] = t;
+    }
+    if (!lastBlockOf(ticket)) return;
+    __shared__ double f[32];
+    const double t = finalOf<true>(partial, gridDim.x, f);
+    if (threadIdx.x == 0) {
+        *out = scale * t;
+        *ticket = 0;
     }
 }
 
@@ -388,7 +411,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot_partial_pairs(const doub
                                                                       const double* __restrict__ b0,
                                                                       const double* __restrict__ a1,
                                                                       const double* __restrict__ b1, std::size_t nPer,
-                                                                      double* partial) {
+                                                                      double* partial, unsigned* tickets, double scale,
+                                                                      double* out) {
     const std::size_t off = blockIdx.y * nPer;
     double s0 = 0.0, s1 = 0.0;
     const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
@@ -413,11 +437,22 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot_partial_pairs(const doub
         partial[blockIdx.y * 2 * kReduceBlocks + blockIdx.x] = t0;
         partial[blockIdx.y * 2 * kReduceBlocks + kReduceBlocks + blockIdx.x] = t1;
     }
+    unsigned* ticket = tickets + blockIdx.y;
+    if (!lastBlockOf(ticket)) return;
+    __shared__ double f0[32], f1[32];
+    const double* pp = partial + blockIdx.y * 2 * kReduceBlocks;
+    const double t0 = finalOf<false>(pp, gridDim.x, f0);
+    const double t1 = finalOf<false>(pp + kReduceBlocks, gridDim.x, f1);
+    if (threadIdx.x == 0) {
+        out[blockIdx.y] = scale * t0 + scale * t1;
+        *ticket = 0;
+    }
 }
 
 __global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial_pairs(const double* __restrict__ a0,
                                                                          const double* __restrict__ a1,
-                                                                         std::size_t nPer, double* partial) {
+                                                                         std::size_t nPer, double* partial,
+                                                                         unsigned* tickets, double* out) {
     const std::size_t off = blockIdx.y * nPer;
     double m = 0.0;
     const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
@@ -433,6 +468,14 @@ __global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial_pairs(const d
         double t = 0.0;
         for (int w = 0; w < kReduceThreads / 32; ++w) t = fmax(t, r[w]);
         partial[blockIdx.y * 2 * kReduceBlocks + blockIdx.x] = t;
+    }
+    unsigned* ticket = tickets + blockIdx.y;
+    if (!lastBlockOf(ticket)) return;
+    __shared__ double f[32];
+    const double t = finalOf<true>(partial + blockIdx.y * 2 * kReduceBlocks, gridDim.x, f);
+    if (threadIdx.x == 0) {
+        out[blockIdx.y] = t;
+        *ticket = 0;
     }
 }
 
@@ -492,15 +535,11 @@ void launchDotInto(Ctx& ctx, std::size_t n, const double* a0, const double* b0, 
     const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
     {
         LaunchScope ls_(ctx, "k_dot_partial");
-        k_dot_partial<<<nb, kReduceThreads, 0, ctx.stream>>>(a0, b0, a1, b1, n, partial);
+        k_dot_partial<<<nb, kReduceThreads, 0, ctx.stream>>>(a0, b0, a1, b1, n, partial,
+                                                             ctx.reduceTickets.as<unsigned>(), scale, out);
     }
     VRG_LAUNCH_CHECK();
-    {
-        LaunchScope ls_(ctx, "k_dot_final");
-        k_dot_final<<<1, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
-    }
-    VRG_LAUNCH_CHECK();
-    }
+}
 
 double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1, double scale, int slot) {
     double* partial = ctx.reduce.d();
@@ -508,12 +547,8 @@ double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1
     const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
     {
         LaunchScope ls_(ctx, "k_maxabs_partial");
-        k_maxabs_partial<<<nb, kReduceThreads, 0, ctx.stream>>>(a0, a1, n, partial);
-    }
-    VRG_LAUNCH_CHECK();
-    {
-        LaunchScope ls_(ctx, "k_max_final");
-        k_max_final<<<1, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
+        k_maxabs_partial<<<nb, kReduceThreads, 0, ctx.stream>>>(a0, a1, n, partial, ctx.reduceTickets.as<unsigned>(),
+                                                                scale, out);
     }
     VRG_LAUNCH_CHECK();
     return out;
@@ -531,17 +566,14 @@ double* launchDotPairs(Ctx& ctx, const GridDims& g, const double* a0, const doub
                        const double* b1, double scale, int slot) {
     const std::size_t n = g.pointsPer();
     const int P = g.pairs;
+    if (P > kReduceTicketSlots) throw NotSupported("reductions: more pairs than ticket slots");
     double* partial = ctx.scratchBuf(200, sizeof(double) * 2 * kReduceBlocks * P);
     double* out = ctx.scratchBuf(201 + slot, sizeof(double) * P);
     const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
     {
         LaunchScope ls_(ctx, "k_dot_partial");
-        k_dot_partial_pairs<<<dim3(nb, P), kReduceThreads, 0, ctx.stream>>>(a0, b0, a1, b1, n, partial);
-    }
-    VRG_LAUNCH_CHECK();
-    {
-        LaunchScope ls_(ctx, "k_dot_final");
-        k_dot_final<<<P, 1024, 0, ctx.stream>>>(partial, nb, scale, out);
+        k_dot_partial_pairs<<<dim3(nb, P), kReduceThreads, 0, ctx.stream>>>(
+            a0, b0, a1, b1, n, partial, ctx.reduceTickets.as<unsigned>(), scale, out);
     }
     VRG_LAUNCH_CHECK();
     return out;
@@ -550,23 +582,26 @@ double* launchDotPairs(Ctx& ctx, const GridDims& g, const double* a0, const doub
 double* launchMaxAbsPairs(Ctx& ctx, const GridDims& g, const double* a0, const double* a1, int slot) {
     const std::size_t n = g.pointsPer();
     const int P = g.pairs;
+    if (P > kReduceTicketSlots) throw NotSupported("reductions: more pairs than ticket slots");
     double* partial = ctx.scratchBuf(200, sizeof(double) * 2 * kReduceBlocks * P);
     double* out = ctx.scratchBuf(201 + slot, sizeof(double) * P);
     const int nb = static_cast<int>(std::min<std::size_t>(kReduceBlocks, (n + kReduceThreads - 1) / kReduceThreads));
     {
         LaunchScope ls_(ctx, "k_maxabs_partial");
-        k_maxabs_partial_pairs<<<dim3(nb, P), kReduceThreads, 0, ctx.stream>>>(a0, a1, n, partial);
-    }
-    VRG_LAUNCH_CHECK();
-    {
-        LaunchScope ls_(ctx, "k_max_final");
-        k_max_final<<<P, 1024, 0, ctx.stream>>>(partial, nb, 1.0, out);
+        k_maxabs_partial_pairs<<<dim3(nb, P), kReduceThreads, 0, ctx.stream>>>(
+            a0, a1, n, partial, ctx.reduceTickets.as<unsigned>(), out);
     }
     VRG_LAUNCH_CHECK();
     return out;
 }
 
 void readPairs(Ctx& ctx, const double* dev, int P, double* host) {
+    if (P <= 64) {  // through the context's pinned staging (a pageable copy stages synchronously)
+        VRG_CUDA(cudaMemcpyAsync(ctx.hostScalars, dev, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        std::memcpy(host, ctx.hostScalars, sizeof(double) * P);
+        return;
+    }
     VRG_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
 }

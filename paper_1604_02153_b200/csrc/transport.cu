@@ -71,23 +71,25 @@ void GuardLog::ensure(int nsteps, const GridDims& g) {
         throw NotSupported("batched pairs: n1 * n2 must be a multiple of 256");
     steps = nsteps;
     pairs = g.pairs;
-    stepMax.alloc(sizeof(double) * steps * pairs);
-    flags.alloc(sizeof(unsigned) * steps);
+    buf.alloc(bytes());
+    if (host) cudaFreeHost(host);
+    host = nullptr;
+    VRG_CUDA(cudaMallocHost(&host, bytes()));
 }
 
-void GuardLog::reset(Ctx& ctx) {
-    VRG_CUDA(cudaMemsetAsync(flags.d(), 0, sizeof(unsigned) * steps, ctx.stream));
-    VRG_CUDA(cudaMemsetAsync(stepMax.d(), 0, sizeof(double) * steps * pairs, ctx.stream));
+GuardLog::~GuardLog() {
+    if (host) cudaFreeHost(host);
 }
+
+void GuardLog::reset(Ctx& ctx) { VRG_CUDA(cudaMemsetAsync(buf.d(), 0, bytes(), ctx.stream)); }
 
 void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep) {
-    std::vector<double> mx(static_cast<std::size_t>(nt + 1) * pairs);
-    std::vector<unsigned> fl(nt + 1);
-    VRG_CUDA(cudaMemcpyAsync(mx.data(), stepMax.d(), sizeof(double) * mx.size(), cudaMemcpyDeviceToHost, ctx.stream));
-    VRG_CUDA(cudaMemcpyAsync(fl.data(), flags.d(), sizeof(unsigned) * (nt + 1), cudaMemcpyDeviceToHost, ctx.stream));
+    VRG_CUDA(cudaMemcpyAsync(host, buf.d(), bytes(), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
+    const double* mx = host;
+    const unsigned* fl = reinterpret_cast<const unsigned*>(host + static_cast<std::size_t>(steps) * pairs);
     if (pairs == 1 && !g_collectGuards) {
-        checkHost(mx.data(), fl.data(), eq, nt, forward, guard, thresholdStep);
+        checkHost(mx, fl, eq, nt, forward, guard, thresholdStep);
         return;
     }
     // a batch: every pair's verdict, nothing thrown (the non-finite flag is shared by the batch)
@@ -97,7 +99,7 @@ void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard,
     for (int k = 0; k < pairs; ++k) {
         for (int s = 0; s <= nt; ++s) m1[s] = mx[static_cast<std::size_t>(s) * pairs + k];
         try {
-            checkHost(m1.data(), fl.data(), eq, nt, forward, guard, thresholdStep);
+            checkHost(m1.data(), fl, eq, nt, forward, guard, thresholdStep);
         } catch (const BlowupError& e) {
             pairStatus[k] = kBlowup;
             pairError[k] = e.what();

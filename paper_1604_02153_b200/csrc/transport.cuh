@@ -40,16 +40,25 @@ struct CollectGuardsScope {
 struct GuardLog {
     int steps = 0;        // number of step slots (nt+1)
     int pairs = 1;
-    DBuf stepMax;         // steps x pairs doubles: per-step guard maxima (atomic max, eval.cuh guardMax)
-    DBuf flags;           // steps unsigned
+    // one device buffer: steps x pairs doubles of per-step guard maxima (atomic max, eval.cuh
+    // guardMax), then steps unsigned prefilter flags; read back in one copy into pinned memory
+    DBuf buf;
+    double* host = nullptr;  // pinned mirror of buf
+    GuardLog() = default;
+    GuardLog(const GuardLog&) = delete;
+    GuardLog& operator=(const GuardLog&) = delete;
+    ~GuardLog();
+    std::size_t bytes() const { return sizeof(double) * steps * pairs + sizeof(unsigned) * steps; }
+    double* stepMax() const { return buf.d(); }
+    unsigned* flags() const { return reinterpret_cast<unsigned*>(buf.d() + static_cast<std::size_t>(steps) * pairs); }
     // batch (pairs > 1): check() records each pair's verdict instead of throwing (0 ok, else the
     // C ABI status of the error the reference would throw) and its message
     std::vector<int> pairStatus;
     std::vector<std::string> pairError;
     void ensure(int nsteps, const GridDims& g);
     // the kernels' guard slot of a step (one per pair)
-    double* partial(int step) const { return stepMax.d() + static_cast<std::size_t>(step) * pairs; }
-    unsigned* flag(int step) const { return flags.as<unsigned>() + step; }
+    double* partial(int step) const { return stepMax() + static_cast<std::size_t>(step) * pairs; }
+    unsigned* flag(int step) const { return flags() + step; }
     void reset(Ctx& ctx);
     // Host readback; throws the reference's first error in solve order.
     //   order: steps visited, each (prefilter-input step index, output step index).
