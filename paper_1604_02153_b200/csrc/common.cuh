@@ -188,6 +188,11 @@ struct Ctx {
     DBuf reduce;  // reduction scratch (partials + results)
     DBuf reduceTickets;  // per-pair block counters of the fused two-stage reductions (self-resetting)
     double* hostScalars = nullptr;  // pinned staging for scalar reads
+    // pinned staging of at least `bytes` for a synchronous readback (grown, never shrunk: the
+    // buffer lives as long as the context, so no pinned allocation per operation)
+    void* hostStage(std::size_t bytes);
+    void* hostStage_ = nullptr;
+    std::size_t hostStageBytes_ = 0;
     // External fine-level GN data term for newtonSolve (C ABI vrg_set_fine_operator): the
     // plug-in point of precond::LinOp (precond.hpp:25) that a slab-decomposed operator fills.
     // build(v, nt) is called once per Newton iterate, dataTerm(vt, b) per matvec (2N fields,

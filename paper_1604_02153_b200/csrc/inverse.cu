@@ -913,6 +913,7 @@ Hessian::~Hessian() {
         for (auto& e : evGuard_) cudaEventDestroy(e);
         for (auto& e : evDone_) cudaEventDestroy(e);
         cudaStreamDestroy(guardStream_);
+        cudaFreeHost(hostGuard_);
     }
     for (auto& kv : graphs_) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -937,6 +938,7 @@ void Hessian::applyQueued(const double* vt1, const double* vt2, double* o1, doub
     }
     NvtxRange nv_("HessianOperator::apply (queued)");
     if (!guardStream_) {
+        VRG_CUDA(cudaMallocHost(&hostGuard_, 2 * guardSlotBytes()));
         VRG_CUDA(cudaStreamCreateWithFlags(&guardStream_, cudaStreamNonBlocking));
         for (int s = 0; s < 2; ++s) {
             VRG_CUDA(cudaEventCreateWithFlags(&evGuard_[s], cudaEventDisableTiming));
@@ -959,7 +961,7 @@ void Hessian::applyQueued(const double* vt1, const double* vt2, double* o1, doub
     VRG_CUDA(cudaEventRecord(evDone_[slot], ctx.stream));
     VRG_CUDA(cudaStreamWaitEvent(guardStream_, evDone_[slot], 0));
     const GuardLog& L = guardLogs_[slot];
-    VRG_CUDA(cudaMemcpyAsync(L.host, L.buf.d(), L.bytes(), cudaMemcpyDeviceToHost, guardStream_));
+    VRG_CUDA(cudaMemcpyAsync(hostGuardSlot(slot), L.buf.d(), L.bytes(), cudaMemcpyDeviceToHost, guardStream_));
     VRG_CUDA(cudaEventRecord(evGuard_[slot], guardStream_));
 }
 
@@ -967,7 +969,8 @@ void Hessian::checkQueued(int slot) {
     if (!queuedGuards()) return;  // applyQueued checked already
     const GuardLog& L = guardLogs_[slot];
     VRG_CUDA(cudaEventSynchronize(evGuard_[slot]));
-    GuardLog::checkHost(L.host, reinterpret_cast<const unsigned*>(L.host + static_cast<std::size_t>(L.steps) * L.pairs),
+    const double* host = hostGuardSlot(slot);
+    GuardLog::checkHost(host, reinterpret_cast<const unsigned*>(host + static_cast<std::size_t>(L.steps) * L.pairs),
                         "adjoint", nt, false, true, nt);
 }
 

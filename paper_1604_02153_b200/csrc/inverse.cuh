@@ -124,7 +124,12 @@ private:
     int deferCap_ = 0, deferCount_ = 0;
     DBuf deferMax_, deferFlags_;
     void guardAfterMatvec();
-    cudaStream_t guardStream_ = nullptr;  // queued matvecs: guard readback into guardLogs_[s].host
+    cudaStream_t guardStream_ = nullptr;  // queued matvecs: guard readback of slot s into hostGuard_
+    double* hostGuard_ = nullptr;         // pinned, 2 slots of guardSlotBytes()
+    std::size_t guardSlotBytes() const { return (guardLogs_[0].bytes() + 15) / 16 * 16; }
+    double* hostGuardSlot(int slot) const {
+        return reinterpret_cast<double*>(reinterpret_cast<char*>(hostGuard_) + slot * guardSlotBytes());
+    }
     cudaEvent_t evGuard_[2] = {nullptr, nullptr}, evDone_[2] = {nullptr, nullptr};
     long long lazyInterps_ = 0, lazyFfts_ = 0;
     bool fused_ = false;  // band kernels (gather + row pass) in the time loops, evalband.cuh

@@ -201,6 +201,7 @@ Ctx::~Ctx() {
     scratch.clear();
     reduce.release();
     if (hostScalars) cudaFreeHost(hostScalars);
+    if (hostStage_) cudaFreeHost(hostStage_);
     if (stream) releaseCachedBlocks(stream);
     if (ownStream && stream) cudaStreamDestroy(stream);
 }
@@ -604,6 +605,20 @@ void readPairs(Ctx& ctx, const double* dev, int P, double* host) {
     }
     VRG_CUDA(cudaMemcpyAsync(host, dev, sizeof(double) * P, cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
+}
+
+void* Ctx::hostStage(std::size_t bytes) {
+    if (bytes > hostStageBytes_) {
+        if (hostStage_) {
+            VRG_CUDA(cudaStreamSynchronize(stream));
+            cudaFreeHost(hostStage_);
+        }
+        hostStage_ = nullptr;
+        const std::size_t want = std::max<std::size_t>(bytes, 64 * 1024);
+        VRG_CUDA(cudaMallocHost(&hostStage_, want));
+        hostStageBytes_ = want;
+    }
+    return hostStage_;
 }
 
 double readScalar(Ctx& ctx, const double* dev) {

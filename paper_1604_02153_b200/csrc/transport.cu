@@ -72,18 +72,12 @@ void GuardLog::ensure(int nsteps, const GridDims& g) {
     steps = nsteps;
     pairs = g.pairs;
     buf.alloc(bytes());
-    if (host) cudaFreeHost(host);
-    host = nullptr;
-    VRG_CUDA(cudaMallocHost(&host, bytes()));
-}
-
-GuardLog::~GuardLog() {
-    if (host) cudaFreeHost(host);
 }
 
 void GuardLog::reset(Ctx& ctx) { VRG_CUDA(cudaMemsetAsync(buf.d(), 0, bytes(), ctx.stream)); }
 
 void GuardLog::check(Ctx& ctx, const char* eq, int nt, bool forward, bool guard, int thresholdStep) {
+    double* host = static_cast<double*>(ctx.hostStage(bytes()));
     VRG_CUDA(cudaMemcpyAsync(host, buf.d(), bytes(), cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
     const double* mx = host;

@@ -41,13 +41,9 @@ struct GuardLog {
     int steps = 0;        // number of step slots (nt+1)
     int pairs = 1;
     // one device buffer: steps x pairs doubles of per-step guard maxima (atomic max, eval.cuh
-    // guardMax), then steps unsigned prefilter flags; read back in one copy into pinned memory
+    // guardMax), then steps unsigned prefilter flags; read back in one copy into the context's
+    // pinned staging (Ctx::hostStage)
     DBuf buf;
-    double* host = nullptr;  // pinned mirror of buf
-    GuardLog() = default;
-    GuardLog(const GuardLog&) = delete;
-    GuardLog& operator=(const GuardLog&) = delete;
-    ~GuardLog();
     std::size_t bytes() const { return sizeof(double) * steps * pairs + sizeof(unsigned) * steps; }
     double* stepMax() const { return buf.d(); }
     unsigned* flags() const { return reinterpret_cast<unsigned*>(buf.d() + static_cast<std::size_t>(steps) * pairs); }
