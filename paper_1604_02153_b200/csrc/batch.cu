@@ -883,9 +883,11 @@ std::vector<SolverReport> newtonSolveBatch(Ctx& ctx, const GridDims& gAll, const
         copyPairs(ctx, v, PA, vAll.d(), P, Np, 2, scatter);
     }
 
-    // final diagnostics per pair (newton.cpp:147-157)
+    // final diagnostics per pair (newton.cpp:147-157): residuals, then the SL Jacobian of every
+    // pair, the pairs grouped by their Jacobian step count (deriveSteps at CFL 0.2) and each
+    // group solved as one batch (a pair's determinant is that of its own solve)
     const GridDims g1 = gAll.one();
-    DBuf tmp(sizeof(double) * 2 * Np), vk(sizeof(double) * 2 * Np);
+    DBuf tmp(sizeof(double) * 2 * Np);
     for (int k = 0; k < P; ++k) {
         if (status[k]) continue;
         const double* mR = mRAll + k * Np;
@@ -894,16 +896,36 @@ std::vector<SolverReport> newtonSolveBatch(Ctx& ctx, const GridDims& gAll, const
         lincomb(ctx, Np, 1.0, finalAll.d() + k * Np, -1.0, mR, tmp.d());
         const double residNum = std::sqrt(dot(ctx, g1, tmp.d(), nullptr, tmp.d(), nullptr));
         reports[k].finalResidualRel = residDenom > 0.0 ? residNum / residDenom : 0.0;
-        copy(ctx, Np, vAll.d() + k * Np, vk.d());
-        copy(ctx, Np, vAll.d() + gAll.points() + k * Np, vk.d() + Np);
-        const int ntJ = deriveSteps(ctx, g1, vk.d(), vk.d() + Np, 0.2);
-        Solver js(ctx, g1, vk.d(), vk.d() + Np, ntJ);
-        js.jacobian(tmp.d());
-        std::vector<double> jac(Np);
-        VRG_CUDA(cudaMemcpyAsync(jac.data(), tmp.d(), sizeof(double) * Np, cudaMemcpyDeviceToHost, ctx.stream));
-        ctx.sync();
-        reports[k].jacMin = *std::min_element(jac.begin(), jac.end());
-        reports[k].jacMax = *std::max_element(jac.begin(), jac.end());
+    }
+    {
+        const auto m1 = linfPairs(ctx, gAll, vAll.d(), false);
+        const auto m2 = linfPairs(ctx, gAll, vAll.d() + gAll.points(), false);
+        std::map<int, std::vector<int>> byNt;
+        for (int k = 0; k < P; ++k) {
+            if (status[k]) continue;
+            double ratio = 0.0;
+            ratio = std::max(ratio, m1[k] / (0.2 * gAll.h1()));
+            ratio = std::max(ratio, m2[k] / (0.2 * gAll.h2()));
+            byNt[std::max(2, static_cast<int>(std::ceil(ratio)))].push_back(k);
+        }
+        for (auto& kv : byNt) {
+            const int Pg = static_cast<int>(kv.second.size());
+            const GridDims gg(gAll.n1, gAll.n2, Pg);
+            std::vector<std::pair<int, int>> map;
+            for (int j = 0; j < Pg; ++j) map.push_back({kv.second[j], j});
+            DBuf vg(sizeof(double) * 2 * gg.points()), jac(sizeof(double) * gg.points());
+            copyPairs(ctx, vAll.d(), P, vg.d(), Pg, Np, 2, map);
+            Solver js(ctx, gg, vg.d(), vg.d() + gg.points(), kv.first);
+            js.jacobian(jac.d());
+            std::vector<double> h(gg.points());
+            VRG_CUDA(cudaMemcpyAsync(h.data(), jac.d(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, ctx.stream));
+            ctx.sync();
+            for (int j = 0; j < Pg; ++j) {
+                const auto b = h.begin() + static_cast<std::ptrdiff_t>(j) * Np;
+                reports[kv.second[j]].jacMin = *std::min_element(b, b + Np);
+                reports[kv.second[j]].jacMax = *std::max_element(b, b + Np);
+            }
+        }
     }
     copy(ctx, 2 * gAll.points(), vAll.d(), vOut);
     ctx.sync();

@@ -232,16 +232,18 @@ void Solver::continuityStep(const double* u, double* out, int dir, double* guard
     ctx.interps += 1;
 }
 
-// Band form of the backward continuity loop (slAdjoint, transport.cpp:229-241): step j writes
-// lambda_{j-1} to dst(j) and row-filters it for step j-1; the prefilter input check of step j-1
+// Band form of a continuity loop (slAdjoint, transport.cpp:229-241, along kBackward; the SL
+// Jacobian, transport.cpp:456-464, along kForward): step j writes its result to dst(j) (j = nt
+// down to 1) and row-filters it for the next step; the prefilter input check of the next step
 // (flag j-1) is done by step j's kernel, as in the plain path's prefilter.
 template <class DstFn>
-void Solver::continuityBand(const double* lam1, DstFn dst) {
-    const double* X = departure(kBackward);
-    const Cell* C = cells(kBackward);
+void Solver::continuityBand(const double* lam1, DstFn dst, int dir) {
+    const double* X = departure(dir);
+    const Cell* C = cells(dir);
     const double* dv = divVelocity();
-    const double* dvd = divVelocityAtDeparture(kBackward);
+    const double* dvd = divVelocityAtDeparture(dir);
     const std::size_t N = g.points();
+    (void)X;
     launchPrefilter(ctx, g, lam1, coef_.d(), tmp_.d(), log.flag(nt));
     for (int j = nt; j >= 1; --j) {
         const EpiContinuity epi{log.partial(j - 1), dvd, dv, ht, dst(j)};
@@ -328,7 +330,7 @@ void Solver::adjoint(const double* lam1, double* traj, bool guard) {
     copy(ctx, N, lam1, traj + nt * N);
     launchFieldMax(ctx, g, traj + nt * N, log.partial(nt));
     if (bandPath()) {
-        continuityBand(traj + nt * N, [&](int j) { return traj + (j - 1) * N; });
+        continuityBand(traj + nt * N, [&](int j) { return traj + (j - 1) * N; }, kBackward);
     } else {
         for (int j = nt; j >= 1; --j)
             continuityStep(traj + j * N, traj + (j - 1) * N, kBackward, log.partial(j - 1), log.flag(j));
@@ -343,7 +345,7 @@ void Solver::adjointFinal(const double* lam1, double* out) {
     log.reset(ctx);
     launchFieldMax(ctx, g, lam1, log.partial(nt));
     if (bandPath()) {
-        continuityBand(lam1, [&](int j) { return (j == 1) ? out : buf + (j % 2) * N; });
+        continuityBand(lam1, [&](int j) { return (j == 1) ? out : buf + (j % 2) * N; }, kBackward);
     } else {
         const double* cur = lam1;
         for (int j = nt; j >= 1; --j) {
@@ -441,11 +443,19 @@ void Solver::jacobian(double* out) {
         k_ones<<<grid1d(N, 256), 256, 0, ctx.stream>>>(N, buf);
     }
     VRG_LAUNCH_CHECK();
-    const double* cur = buf;
-    for (int j = 1; j <= nt; ++j) {
-        double* dst = (j == nt) ? out : buf + (j % 2) * N;
-        continuityStep(cur, dst, kForward, log.partial(0), nullptr);
-        cur = dst;
+    log.reset(ctx);  // the steps' guard slots (unchecked: the Jacobian has no guard)
+    if (bandPath()) {
+        // nt forward continuity steps from 1; the band loop labels them nt .. 1, the last one
+        // (label 1) writing out.  The steps read their input from the coefficients, so the
+        // intermediate fields (unused) all go to buf, whose ones were prefiltered first.
+        continuityBand(buf, [&](int j) { return (j == 1) ? out : buf; }, kForward);
+    } else {
+        const double* cur = buf;
+        for (int j = 1; j <= nt; ++j) {
+            double* dst = (j == nt) ? out : buf + (j % 2) * N;
+            continuityStep(cur, dst, kForward, log.partial(0), nullptr);
+            cur = dst;
+        }
     }
     ctx.sync();
 }

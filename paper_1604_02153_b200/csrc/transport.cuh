@@ -116,7 +116,7 @@ public:
 
 private:
     template <class DstFn>
-    void continuityBand(const double* lam1, DstFn dst);
+    void continuityBand(const double* lam1, DstFn dst, int dir);
     DBuf cv_;  // prefiltered velocity [c1 | c2]
     DBuf X_[2], cells_[2];
     DBuf divv_, dvDep_[2];
