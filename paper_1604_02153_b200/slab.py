@@ -678,11 +678,59 @@ class SlabHessian:
     def reg(self, vts):
         return distributed_reg(self.comm, vts, self.n1, self.n2, self.norm, self.beta)
 
+    # The per-step orchestration of a slab matvec (one library call and one halo exchange per SL
+    # step, from Python) is captured into one CUDA graph per (inputs, outputs) and replayed: the
+    # first apply of a pointer set runs eagerly (warming every buffer), the second captures on
+    # the context's stream, later ones replay; the guard check stays on the host after the
+    # replay.  `graphs = False` keeps every apply eager.  With NCCL exchanges between processes
+    # (DistComm, more than one rank) the capture is opt-in (`graphs_multirank`) until it has run
+    # on a multi-GPU node; in-process slabs (LocalComm) and a one-rank group capture by default.
+    graphs = True
+    graphs_multirank = False
+
+    def _capturable(self, vts):
+        if not self.graphs or not vts[0].is_cuda:
+            return False
+        return isinstance(self.comm, LocalComm) or self.comm.size == 1 or self.graphs_multirank
+
     def apply(self, vts, outs=None, data_term_only=False):
         """vts[i] = (2, L, n2) slab of vt on rank i -> H vt slabs (or the data term b)."""
-        nt, ht = self.nt, 1.0 / self.nt
         ranks = range(len(self.comm.ranks))
         outs = outs if outs is not None else [self.ctx.empty(2, self.geo.L, self.n2) for _ in ranks]
+        if not self._capturable(vts):
+            self._apply_body(vts, outs, data_term_only)
+        else:
+            key = (tuple(t.data_ptr() for vt in vts for t in vt), tuple(o.data_ptr() for o in outs), data_term_only)
+            cache = self.__dict__.setdefault("_graph_cache", {})
+            entry = cache.get(key)
+            if entry is None and len(cache) >= 16:  # a caller cycling through many buffers
+                cache.clear()
+            if entry is None:
+                self._apply_body(vts, outs, data_term_only)
+                cache[key] = "seen"
+            elif entry == "seen":
+                try:
+                    graph = torch.cuda.CUDAGraph()
+                    graph.capture_begin(capture_error_mode="thread_local")
+                    try:
+                        self._apply_body(vts, outs, data_term_only)
+                    finally:
+                        graph.capture_end()
+                except Exception:  # noqa: BLE001 - not capturable here (e.g. the backend): stay eager
+                    self.graphs = False
+                    self._apply_body(vts, outs, data_term_only)
+                else:
+                    cache[key] = graph
+                    graph.replay()
+            else:
+                entry.replay()
+        self._check_guard()
+        return outs
+
+    def _apply_body(self, vts, outs, data_term_only):
+        """The launch sequence of one slab matvec (no host synchronisation: capturable)."""
+        nt, ht = self.nt, 1.0 / self.nt
+        ranks = range(len(self.comm.ranks))
         regs = self.reg(vts) if not data_term_only else None
         for i in ranks:
             self.flags[i].zero_()
@@ -728,8 +776,6 @@ class SlabHessian:
                 else:
                     self._step(i, KIND_ADJ, self.win[i], p["Xb"], ops, ht, wof(j - 1), self.rows[i],
                                self.partials[i][j - 1], self.flags[i][j - 1:j])
-        self._check_guard()
-        return outs
 
     def _check_guard(self):
         """transport.cpp:16-20 guard of the GN adjoint (inverse.cpp:185) over all slabs, in the
