@@ -680,13 +680,26 @@ class SlabHessian:
 
     # The per-step orchestration of a slab matvec (one library call and one halo exchange per SL
     # step, from Python) is captured into one CUDA graph per (inputs, outputs) and replayed: the
-    # first apply of a pointer set runs eagerly (warming every buffer), the second captures on
-    # the context's stream, later ones replay; the guard check stays on the host after the
-    # replay.  `graphs = False` keeps every apply eager.  With NCCL exchanges between processes
+    # first `capture_after` applies of a pointer set run eagerly (warming every buffer), the next
+    # captures on the context's stream, later ones replay; the guard check stays on the host
+    # after the replay.  `graphs = False` keeps every apply eager.  With NCCL exchanges between processes
     # (DistComm, more than one rank) the capture is opt-in (`graphs_multirank`) until it has run
     # on a multi-GPU node; in-process slabs (LocalComm) and a one-rank group capture by default.
     graphs = True
     graphs_multirank = False
+    capture_after = 8  # an operator rebuilt every Newton iteration applies ~4 times: stays eager
+
+    def apply_staged(self, vts, data_term_only=False):
+        """apply() through persistent input / output slabs owned by the operator (copies of vts
+        in, the result out): callers whose temporaries change address every call keep one
+        pointer set, so the captured graph replays."""
+        if not hasattr(self, "_stage_in"):
+            g = self.geo
+            self._stage_in = [self.ctx.empty(2, g.L, self.n2) for _ in self.comm.ranks]
+            self._stage_out = [self.ctx.empty(2, g.L, self.n2) for _ in self.comm.ranks]
+        for dst, src in zip(self._stage_in, vts):
+            dst.copy_(src)
+        return self.apply(self._stage_in, self._stage_out, data_term_only=data_term_only)
 
     def _capturable(self, vts):
         if not self.graphs or not vts[0].is_cuda:
@@ -705,10 +718,13 @@ class SlabHessian:
             entry = cache.get(key)
             if entry is None and len(cache) >= 16:  # a caller cycling through many buffers
                 cache.clear()
-            if entry is None:
+            if entry is None or (isinstance(entry, int) and entry < self.capture_after):
+                # eager until the pointer set has proved reused: a capture (its eager-speed run
+                # plus the graph instantiation) pays off only over several replays (the coarse
+                # level's Chebyshev loops), not for an operator rebuilt every Newton iteration
                 self._apply_body(vts, outs, data_term_only)
-                cache[key] = "seen"
-            elif entry == "seen":
+                cache[key] = (entry or 0) + 1
+            elif isinstance(entry, int):
                 try:
                     graph = torch.cuda.CUDAGraph()
                     graph.capture_begin(capture_error_mode="thread_local")
@@ -825,7 +841,7 @@ class SlabCoarse:
         """applySplitHessianOf (precond.cpp:20-26): M^{-1/2} Q M^{-1/2} s + s on coarse slabs."""
         op = lambda f, k1, k2, _: f * inv_half_symbol(k1, k2, self.norm, self.beta)  # noqa: E731
         t = distributed_spectral(self.comm, ss, self.t1, self.t2, op)
-        b = self.S.apply(t, data_term_only=True)
+        b = self.S.apply_staged(t, data_term_only=True)
         o = distributed_spectral(self.comm, b, self.t1, self.t2, op)
         return [x + s for x, s in zip(o, ss)]
 
@@ -1143,7 +1159,7 @@ class SlabFineOperator:
             op = lambda f, k1, k2, _: f * inv_half_symbol(k1, k2, self.norm, self.beta)  # noqa: E731
             ss = self._slabs(self._full(sptr))
             t = distributed_spectral(self.comm, ss, self.n1, self.n2, op)
-            b = self.S.apply(t, data_term_only=True)
+            b = self.S.apply_staged(t, data_term_only=True)
             o = distributed_spectral(self.comm, b, self.n1, self.n2, op)
             self.comm.allgather_rows([x + y for x, y in zip(o, ss)], self._full(optr))
             self.matvecs += 1
@@ -1159,7 +1175,7 @@ class SlabFineOperator:
         failed = False
         try:
             t0 = time.perf_counter()
-            outs = self.S.apply(self._slabs(self._full(vtptr)), data_term_only=True)
+            outs = self.S.apply_staged(self._slabs(self._full(vtptr)), data_term_only=True)
             self.comm.allgather_rows(outs, self._full(bptr))
             self.matvecs += 1
             self.apply_s += time.perf_counter() - t0

@@ -28,7 +28,7 @@ for G in (1, 2, 4, 8):
     res = {}
     for mode in ("eager", "graph"):
         S.graphs = mode == "graph"
-        for _ in range(3):
+        for _ in range(S.capture_after + 2):  # eager uses, then the capture
             S.apply(vts, outs)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
