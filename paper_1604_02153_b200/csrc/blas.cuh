@@ -17,7 +17,6 @@ double* launchDot(Ctx& ctx, std::size_t n, const double* a0, const double* b0, c
 void launchDotInto(Ctx& ctx, std::size_t n, const double* a0, const double* b0, const double* a1, const double* b1,
                    double scale, double* out);
 double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1, double scale, int slot);
-void launchMaxFinal(Ctx& ctx, const double* partials, int nb, double scale, double* out);
 
 // grid size of the element-wise kernels (grid-stride loops, at most 8 blocks of 256 per SM)
 unsigned elemBlocks(const Ctx& ctx, std::size_t n);

@@ -800,8 +800,8 @@ double Hessian::benchKernel(int id, int iters) {
                 break;
             case 13:  // one whole matvec launched directly on the stream (programmatic dependent launch, no graph)
             case 14: {  // the same matvec through its CUDA graph (the apply path's replay)
-                double* in = ctx.scratchBuf(130, sizeof(double) * 2 * N);
-                double* out = ctx.scratchBuf(131, sizeof(double) * 2 * N);
+                double* in = ctx.scratchBuf(160, sizeof(double) * 2 * N);
+                double* out = ctx.scratchBuf(161, sizeof(double) * 2 * N);
                 VRG_CUDA(cudaMemcpyAsync(in, vtD, sizeof(double) * 2 * N, cudaMemcpyDeviceToDevice, ctx.stream));
                 if (id == 13) {
                     launchApply(in, in + N, out, out + N);

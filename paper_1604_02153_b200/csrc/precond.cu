@@ -688,7 +688,7 @@ bool lanczosEmaxPairs(Ctx& ctx, const GridDims& g, const LinOpDev& op, int steps
     // the seeded start vector of lanczosEmax, the same in every pair's slots
     const GridDims one = g.one();
     const std::size_t n1v = 2 * nPer;
-    double* q0 = ctx.scratchBuf(140, sizeof(double) * n1v);
+    double* q0 = ctx.scratchBuf(162, sizeof(double) * n1v);
     randomBandLimitedVelocity(ctx, one, seed, q0);
     const double nq = vnormL2(ctx, one, q0);
     if (!(nq > 0.0)) return true;  // every pair: eMax 1 (lanczosEmax's early return)

@@ -389,21 +389,6 @@ __global__ void __launch_bounds__(kReduceThreads) k_maxabs_partial(const double*
     }
 }
 
-__global__ void k_max_final(const double* partial, int nb, double scale, double* out) {
-    partial += static_cast<std::size_t>(blockIdx.x) * 2 * kReduceBlocks;  // block = pair of a batch
-    out += blockIdx.x;
-    __shared__ double r[32];
-    double m = 0.0;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) m = fmax(m, partial[i]);
-    m = warpMax(m);
-    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t = fmax(t, r[w]);
-        *out = scale * t;
-    }
-}
 
 // Per-pair forms of the two-stage reductions (stacked pairs, GridDims::pairs): blockIdx.y = pair,
 // each pair reduced over its own nPer values with the block partition and summation order of the
@@ -555,13 +540,6 @@ double* launchMaxAbs(Ctx& ctx, std::size_t n, const double* a0, const double* a1
     return out;
 }
 
-void launchMaxFinal(Ctx& ctx, const double* partials, int nb, double scale, double* out) {
-    {
-        LaunchScope ls_(ctx, "k_max_final");
-        k_max_final<<<1, 1024, 0, ctx.stream>>>(partials, nb, scale, out);
-    }
-    VRG_LAUNCH_CHECK();
-}
 
 double* launchDotPairs(Ctx& ctx, const GridDims& g, const double* a0, const double* b0, const double* a1,
                        const double* b1, double scale, int slot) {

@@ -118,3 +118,26 @@ def test_apply_batch_error_at_the_failing_matvec(ctx, api):
     # the operator is still usable after the error
     H.apply_batch(vts[:2], outs[:2])
     assert np.array_equal(outs[1][0].cpu().numpy(), ref1[0].cpu().numpy())
+
+
+@pytest.mark.parametrize("mode,scheme", [(1, 0), (0, 1)])
+def test_apply_batch_on_operators_checked_per_call(ctx, api, mode, scheme):
+    """Full-Newton (mode 1) and RK2 (scheme 1) operators check their guards their own way: the
+    queued batch falls back to one checked apply per matvec, with the same results."""
+    n, nt = 128, 4
+    mT = synth.smoothed_noise(n, n, 1000)
+    v1, v2 = synth.smooth_velocity(n, n, 2000)
+    F = ctx.field
+    ctx.set_scheme(scheme)
+    try:
+        H = api.HessianOperator(ctx, (F(0.5 * v1), F(0.5 * v2)), F(mT), F(mT), api.H2SEMI, 1e-3, 0, nt, mode=mode)
+        vts = [tuple(F(x) for x in synth.smooth_velocity(n, n, 3000 + i)) for i in range(3)]
+        want = [[t.cpu().numpy() for t in H.apply(vt)] for vt in vts]
+        outs = [(ctx.empty(n, n), ctx.empty(n, n)) for _ in range(3)]
+        for _ in range(2):
+            H.apply_batch(vts, outs)
+            for i in range(3):
+                assert np.array_equal(outs[i][0].cpu().numpy(), want[i][0])
+                assert np.array_equal(outs[i][1].cpu().numpy(), want[i][1])
+    finally:
+        ctx.set_scheme(0)
