@@ -34,8 +34,6 @@ struct CoeffSet {
 // time loops), so the cell computation runs before the programmatic-dependency wait.
 // blockIdx.y: member of a batch of coefficient sets at the same points (coefficient offset
 // csZ, epilogue index offset epiZ per member; guard-free epilogues only).
-// Guard partial of evaluate block b of a batch (GridDims::pairs): entry pair * gE + local block
-// (guardStride), the same entry as block b for a single grid.
 // Per-(step, pair) guard maximum: guard values are >= +0 (NaN skipped, inf kept), whose IEEE bit
 // patterns order like unsigned integers, so an integer atomicMax on the bits is the maximum of
 // the doubles (order-independent, hence run-to-run deterministic) and no reduction kernel
@@ -44,10 +42,6 @@ __device__ __forceinline__ void guardMax(double* slot, double m) {
     atomicMax(reinterpret_cast<unsigned long long*>(slot), static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
-__device__ __forceinline__ unsigned guardEntry(unsigned b, unsigned blocksPer, unsigned gE) {
-    const unsigned pair = b / blocksPer;
-    return pair * gE + (b - pair * blocksPer);
-}
 
 // Stacked pairs (GridDims::pairs): node p belongs to pair p / (n1 n2), whose coefficients are the
 // pair's padded field (pair * paddedPoints(n1, n2) further on); n1 * n2 is then a multiple of
@@ -60,8 +54,7 @@ __device__ __forceinline__ int depCell(Cell u, double, int, double w[4]) { retur
 template <int NF, class Epi, class Dep = double>
 __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const Dep* __restrict__ x1,
                                                          const Dep* __restrict__ x2, int n1, int n2, int xStable,
-                                                         Epi epi, std::size_t csZ, std::size_t epiZ, int pairs,
-                                                         unsigned gE) {
+                                                         Epi epi, std::size_t csZ, std::size_t epiZ, int pairs) {
     const int Nper = n1 * n2;
     const int N = Nper * pairs;  // up to 2^31 points
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -139,7 +132,7 @@ __global__ void __launch_bounds__(kEvalBlock) k_evaluate(CoeffSet<NF> cs, const 
 // Same block layout and guard reduction as k_evaluate, without the gather (values = 0):
 // used where the interpolated field is identically zero (m~_0 = 0) or for pure pointwise work.
 template <class Epi>
-__global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi, unsigned blocksPer, unsigned gE) {
+__global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi, unsigned blocksPer) {
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     double guard = 0.0;
     pdlWait();
@@ -164,18 +157,13 @@ __global__ void __launch_bounds__(kEvalBlock) k_pointwise(std::size_t N, Epi epi
 
 inline unsigned evalBlocks(const GridDims& g) { return grid1d(g.points(), kEvalBlock).x; }
 inline unsigned evalBlocksPer(const GridDims& g) { return grid1d(g.pointsPer(), kEvalBlock).x; }
-// Guard partials per step and pair: one per evaluate block or per grid row (band kernels),
-// whichever is more (unused entries stay 0, GuardLog::reset); a batch keeps each pair's entries
-// together (pair * guardStride + local block / row).
-inline unsigned guardStride(const GridDims& g) { return std::max(evalBlocksPer(g), static_cast<unsigned>(g.n1)); }
-inline unsigned guardBlocks(const GridDims& g) { return guardStride(g) * static_cast<unsigned>(g.pairs); }
 
 template <class Epi>
 void launchPointwise(Ctx& ctx, const GridDims& g, const Epi& epi) {
     {
         LaunchScope ls_(ctx, Epi::kName);
         launchPdl(1, k_pointwise<Epi>, grid1d(g.points(), kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, g.points(), epi,
-                  evalBlocksPer(g), guardStride(g));
+                  evalBlocksPer(g));
     }
 }
 
@@ -186,7 +174,7 @@ void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const Dep* x1,
     {
         LaunchScope ls_(ctx, Epi::kName);
         launchPdl(1, k_evaluate<NF, Epi, Dep>, grid1d(N, kEvalBlock), dim3(kEvalBlock), 0, ctx.stream, cs, x1, x2, g.n1, g.n2,
-                  xStable ? 1 : 0, epi, std::size_t(0), std::size_t(0), g.pairs, guardStride(g));
+                  xStable ? 1 : 0, epi, std::size_t(0), std::size_t(0), g.pairs);
     }
 }
 
@@ -200,7 +188,7 @@ void launchEvaluateBatch(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, std::size
     {
         LaunchScope ls_(ctx, Epi::kName);
         launchPdl(1, k_evaluate<NF, Epi>, dim3(grid1d(N, kEvalBlock).x, count), dim3(kEvalBlock), 0, ctx.stream, cs,
-                  x1, x2, g.n1, g.n2, 0, epi, csZ, epiZ, g.pairs, guardStride(g));
+                  x1, x2, g.n1, g.n2, 0, epi, csZ, epiZ, g.pairs);
     }
 }
 

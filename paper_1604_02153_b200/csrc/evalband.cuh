@@ -36,7 +36,7 @@ inline bool bandFusable(const GridDims& g) {
 // The SL time loops take the band path with packed departure cells (axes up to kCellMaxN).
 inline bool bandCellsFit(const GridDims& g) { return g.n1 <= kCellMaxN && g.n2 <= kCellMaxN; }
 
-// Doubles of shared memory one row needs (chunked row + chunk summaries + guard partials).
+// Doubles of shared memory one row needs (chunked row + chunk summaries + warp guard maxima).
 __host__ __device__ inline int bandRowSmem(int n2, int tw) { return (n2 / kL) * (kCS + 3) + (tw + 31) / 32; }
 
 inline std::size_t bandSmem(const GridDims& g) { return sizeof(double) * bandRowSmem(g.n2, bandTW(g.n2)); }
@@ -95,16 +95,16 @@ struct BarNamed {
 };
 
 // One grid row r by TW threads (t = 0..TW-1): gather at the row's departure points, step
-// epilogue, guard partial of the row, then the exact periodic row filter in shared memory and
+// epilogue, the row's guard maximum, then the exact periodic row filter in shared memory and
 // the row-filtered output.  `sm` holds bandRowSmem(n2, TW) doubles.
 // Stacked pairs (GridDims::pairs): r runs over all pairs' rows; row r belongs to pair r / n1,
-// whose coefficients lie pair * paddedPoints(n1, n2) further on, and its guard partial goes to
-// entry pair * gE + local row (guardStride).
+// whose coefficients lie pair * paddedPoints(n1, n2) further on, and its guard maximum goes to
+// the pair's slot (eval.cuh guardMax); slab windows keep one partial per local row.
 template <class Epi, bool kGather, bool kWindow, int TW, class Bar, class Dep>
 __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ x1,
                                         const Dep* __restrict__ x2, int n1, int n2, const Epi& epi,
                                         double* __restrict__ rowOut, unsigned* nonfinite, const BandWindow& win,
-                                        int r, int t, double* sm, Bar bar, unsigned gE) {
+                                        int r, int t, double* sm, Bar bar) {
     if (!kGather) pdlWait();
     const int pair = kWindow ? 0 : r / n1;
     if (!kWindow) cs.c[0] += static_cast<std::size_t>(pair) * paddedPoints(n1, n2);
@@ -294,10 +294,10 @@ template <class Epi, bool kGather, bool kWindow = false, int TW = kBandThreads, 
 __global__ void __launch_bounds__(TW, (bandMinBlocks<Epi, TW>())) k_eval_band(CoeffSet<1> cs, const Dep* __restrict__ x1,
                                                             const Dep* __restrict__ x2, int n1, int n2, Epi epi,
                                                             double* __restrict__ rowOut, unsigned* nonfinite,
-                                                            BandWindow win, unsigned gE) {
+                                                            BandWindow win) {
     extern __shared__ __align__(16) double sm[];
     bandRow<Epi, kGather, kWindow, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, win, blockIdx.x, threadIdx.x, sm,
-                                       BarBlock{}, gE);
+                                       BarBlock{});
     pdlTrigger();  // at the end: the dependent column pass must not take this kernel's slots
 }
 
@@ -317,7 +317,7 @@ constexpr int stripWorkers() {
 template <class Epi, bool kGather, int TW>
 __global__ void __launch_bounds__(TW* stripWorkers<Epi, TW>(), 1)
     k_eval_strip(CoeffSet<1> cs, const Cell* __restrict__ x1, const Cell* __restrict__ x2, int n1, int n2, Epi epi,
-                 double* __restrict__ rowOut, unsigned* nonfinite, int rows, unsigned gE) {
+                 double* __restrict__ rowOut, unsigned* nonfinite, int rows) {
     extern __shared__ __align__(16) double sm[];
     constexpr int W = stripWorkers<Epi, TW>();
     const int w = threadIdx.x / TW;
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(TW* stripWorkers<Epi, TW>(), 1)
     // keeps the row's loads on uniform memory descriptors (no R2UR per tap)
     if (__any_sync(0xffffffffu, r < rows))
         bandRow<Epi, kGather, false, TW>(cs, x1, x2, n1, n2, epi, rowOut, nonfinite, BandWindow{}, r, t,
-                                         sm + w * bandRowSmem(n2, TW), BarNamed<TW>{1 + w}, gE);
+                                         sm + w * bandRowSmem(n2, TW), BarNamed<TW>{1 + w});
     pdlTrigger();
 }
 
@@ -365,7 +365,7 @@ void launchEvalStrip(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const Cell* x1
     }
     const int rows = g.n1 * g.pairs;
     launchPdl(1, k_eval_strip<Epi, kGather, TW>, dim3((rows + W - 1) / W), dim3(kThreads), smem, ctx.stream, cs, x1,
-              x2, g.n1, g.n2, epi, rowOut, nonfinite, rows, guardStride(g));
+              x2, g.n1, g.n2, epi, rowOut, nonfinite, rows);
 }
 
 template <class Epi, bool kGather>
@@ -381,19 +381,19 @@ void launchEvalBand(Ctx& ctx, const GridDims& g, CoeffSet<1> cs, const Cell* x1,
     switch (bandTW(g.n2)) {
         case 256:
             launchPdl(1, k_eval_band<Epi, kGather, false, 256>, grid, dim3(256), smem, ctx.stream, cs, x1, x2, g.n1,
-                      g.n2, epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
+                      g.n2, epi, rowOut, nonfinite, BandWindow{});
             break;
         case 128:
             launchPdl(1, k_eval_band<Epi, kGather, false, 128>, grid, dim3(128), smem, ctx.stream, cs, x1, x2, g.n1,
-                      g.n2, epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
+                      g.n2, epi, rowOut, nonfinite, BandWindow{});
             break;
         case 64:
             launchPdl(1, k_eval_band<Epi, kGather, false, 64>, grid, dim3(64), smem, ctx.stream, cs, x1, x2, g.n1, g.n2,
-                      epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
+                      epi, rowOut, nonfinite, BandWindow{});
             break;
         default:
             launchPdl(1, k_eval_band<Epi, kGather, false, 32>, grid, dim3(32), smem, ctx.stream, cs, x1, x2, g.n1, g.n2,
-                      epi, rowOut, nonfinite, BandWindow{}, guardStride(g));
+                      epi, rowOut, nonfinite, BandWindow{});
             break;
     }
 }
@@ -406,7 +406,7 @@ void launchEvalBandWindow(Ctx& ctx, int n1, int L, int n2, CoeffSet<1> cs, const
     const GridDims gl(L, n2);
     if (bandTW(n2) != kBandThreads) throw NotSupported("slab step: the row length must be a multiple of 256");
     launchPdl(1, k_eval_band<Epi, kGather, true, kBandThreads, double>, dim3(L), dim3(kBandThreads), bandSmem(gl), ctx.stream, cs, x1, x2,
-              n1, n2, epi, rowOut, nonfinite, win, 0u);
+              n1, n2, epi, rowOut, nonfinite, win);
 }
 
 }  // namespace vrg

@@ -1,7 +1,8 @@
 // Context, errors, cuFFT plan cache and BLAS-1 / reduction kernels (K9).
 // BLAS-1 restates src/field.cpp:19-119: dot = h1*h2*sum(u*w) per component, normLinf = max|x|
 // with NaN ignored (std::max semantics), axpy/scale.  Reductions are two-stage with a fixed
-// block count and a fixed-order final pass, so results are run-to-run deterministic.
+// block count and a fixed-order final pass (run by the last block of the same launch), so
+// results are run-to-run deterministic.
 #include <cstdlib>
 #include <cstdint>
 #include <map>

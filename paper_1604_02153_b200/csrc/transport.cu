@@ -29,9 +29,9 @@ __global__ void k_star(const double* __restrict__ v1, const double* __restrict__
     x2[p] = __dsub_rn(c2, __dmul_rn(sgnHt, v2[p]));
 }
 
-// Block maxima of |field| into guard partials (same block layout as k_evaluate).
+// Maximum of |field| per pair into the step's guard slots (same block layout as k_evaluate).
 __global__ void __launch_bounds__(kEvalBlock) k_fieldmax(const double* __restrict__ f, std::size_t N, double* partial,
-                                                         unsigned blocksPer, unsigned gE) {
+                                                         unsigned blocksPer) {
     const std::size_t p = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     double g = 0.0;
     if (p < N) g = fmax(0.0, fabs(f[p]));
@@ -56,8 +56,7 @@ __global__ void k_ones(std::size_t N, double* y) {
 void launchFieldMax(Ctx& ctx, const GridDims& g, const double* f, double* partial) {
     {
         LaunchScope ls_(ctx, "k_fieldmax");
-        k_fieldmax<<<evalBlocks(g), kEvalBlock, 0, ctx.stream>>>(f, g.points(), partial, evalBlocksPer(g),
-                                                                 guardStride(g));
+        k_fieldmax<<<evalBlocks(g), kEvalBlock, 0, ctx.stream>>>(f, g.points(), partial, evalBlocksPer(g));
     }
     VRG_LAUNCH_CHECK();
 }
