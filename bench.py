@@ -564,8 +564,9 @@ def time_to_solution(ctx, api, with_cpu):
 # Batched pairs (BASELINE configs 5b and 3) on this GPU: lanes of lockstep batches
 # (batch.py --lanes L --batch B; csrc/batch.cu), the second pass timed.
 BATCH_RUNS = {
-    "config5b_64pairs_256_nt16_H2_1e-3_2L-cheb10": dict(n=256, pairs=64, lanes=8, batch=8),
-    "config3_8pairs_512_nt16_H2_1e-3_2L-cheb10": dict(n=512, pairs=8, lanes=2, batch=4),
+    # lanes x batch from the sweep of tools/gpu_s4g.sh (profiles/r2s3_batch_sweep.txt)
+    "config5b_64pairs_256_nt16_H2_1e-3_2L-cheb10": dict(n=256, pairs=64, lanes=4, batch=16),
+    "config3_8pairs_512_nt16_H2_1e-3_2L-cheb10": dict(n=512, pairs=8, lanes=4, batch=2),
 }
 
 
