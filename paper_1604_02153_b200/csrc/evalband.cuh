@@ -230,6 +230,7 @@ __device__ __forceinline__ void bandRow(CoeffSet<1> cs, const Dep* __restrict__ 
     }
     // the next prefilter's input check (checkFinite(u, "prefilter"), interp.cpp:76)
     if (bar.syncOr(bad) && t == 0 && nonfinite) atomicOr(nonfinite, 1u);
+    if (!rowOut) return;  // the last step of a loop: nothing left to interpolate, no row pass
 
     // ---- row pass of the prefilter (exact: the whole periodic row is in shared memory)
     double f[kL];

@@ -454,7 +454,7 @@ void Hessian::dataTerm(const double* vt1, const double* vt2, double* b1, double*
                              b1, b2, reg1, reg2, last ? out1 : nullptr, last ? out2 : nullptr};
             if (last) {
                 waitReg();
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, true);
+                launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, nullptr, nullptr);
             } else {
                 launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, R[(j - 1) & 1],
                                                    adjLog_->flag(j - 1));
@@ -745,10 +745,13 @@ double Hessian::benchKernel(int id, int iters) {
                 launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xf, Xf + N, epi, true);
                 break;
             }
-            case 1: {  // incremental-adjoint step + body force (K5+K8)
+            case 1: {  // incremental-adjoint step + body force (K5+K8); band path: the last step's form
                 EpiAdjointBF epi{adjLog_->partial(0), dvd, dv, ht, lam + N, G, G + N, ht, b, b + N,
                                  nullptr, nullptr, nullptr, nullptr};
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
+                if (fused_)
+                    launchEvalBand<EpiAdjointBF, true>(ctx, g, CoeffSet<1>{{coef}}, Cb, Cb + N, epi, nullptr, nullptr);
+                else
+                    launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef}}, Xb, Xb + N, epi, true);
                 break;
             }
             case 2:  // prefilter, both passes (K1)

@@ -246,8 +246,8 @@ void Solver::continuityBand(const double* lam1, DstFn dst, int dir) {
     launchPrefilter(ctx, g, lam1, coef_.d(), tmp_.d(), log.flag(nt));
     for (int j = nt; j >= 1; --j) {
         const EpiContinuity epi{log.partial(j - 1), dvd, dv, ht, dst(j)};
-        if (j == 1) {
-            launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, true);
+        if (j == 1) {  // the last step: no row pass
+            launchEvalBand<EpiContinuity, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, nullptr, nullptr);
         } else {
             launchEvalBand<EpiContinuity, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                 log.flag(j - 1));
@@ -269,8 +269,8 @@ void Solver::state(const double* m0, double* traj, bool guard) {
         launchPrefilter(ctx, g, traj, coef_.d(), tmp_.d(), log.flag(0));
         for (int j = 1; j <= nt; ++j) {
             const EpiStateStep epi{log.partial(j), traj + j * N};
-            if (j == nt) {
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, true);
+            if (j == nt) {  // the last step: no row pass
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, nullptr, nullptr);
             } else {
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                    log.flag(j));
@@ -301,8 +301,8 @@ void Solver::stateFinal(const double* m0, double* out) {
         for (int j = 1; j <= nt; ++j) {
             double* dst = (j == nt) ? out : buf + (j % 2) * N;
             const EpiStateStep epi{log.partial(j), dst};
-            if (j == nt) {
-                launchEvaluate<1>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, true);
+            if (j == nt) {  // the last step: no row pass
+                launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, nullptr, nullptr);
             } else {
                 launchEvalBand<EpiStateStep, true>(ctx, g, CoeffSet<1>{{coef_.d()}}, C, C + N, epi, tmp_.d(),
                                                    log.flag(j));
