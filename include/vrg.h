@@ -113,6 +113,8 @@ int vrg_set_scheme(vrg_ctx_t ctx, int scheme);
 void vrg_ctx_destroy(vrg_ctx_t ctx);
 const char* vrg_last_error(vrg_ctx_t ctx); /* ctx may be NULL: last error of this thread */
 int vrg_sync(vrg_ctx_t ctx);
+/* device memory for use in the context's stream order (stream-ordered block cache: no device
+ * synchronisation on free); vrg_free takes only vrg_malloc blocks of the same context */
 int vrg_malloc(vrg_ctx_t ctx, unsigned long long bytes, void** out);
 int vrg_free(vrg_ctx_t ctx, void* p);
 int vrg_host_alloc(vrg_ctx_t ctx, unsigned long long bytes, void** out); /* pinned */

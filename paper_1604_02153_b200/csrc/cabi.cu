@@ -1,6 +1,8 @@
 // extern "C" boundary of libvrg (include/vrg.h).  Exceptions never cross it: each entry point
 // maps them to the status codes the reference's exception types correspond to.
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <map>
 
@@ -16,7 +18,13 @@ struct vrg_ctx_s {
     vrg::Ctx ctx;
     double betaW = 1e-1;  // Model::betaW of the near-incompressible model (inverse.hpp:21)
     int scheme = 0;       // SchemeConfig::scheme for the calls on this context (SL, RK2, RK2A)
+    // vrg_malloc blocks (the stream-ordered block cache of the context's stream): pointer -> size
+    std::mutex allocMu;
+    std::unordered_map<void*, std::size_t> allocs;
     vrg_ctx_s(int dev, cudaStream_t s) : ctx(dev, s) {}
+    ~vrg_ctx_s() {
+        for (auto& kv : allocs) vrg::cachedFree(kv.first, kv.second, ctx.stream);
+    }
 };
 struct vrg_solver_s {
     vrg_ctx_s* owner;
@@ -154,12 +162,31 @@ int vrg_sync(vrg_ctx_t c) {
     return guarded(c, [&] { c->ctx.sync(); });
 }
 
+// Device memory in the context's stream order, from the stream-ordered block cache: a drop-in
+// allocates the fields of every call (DevBuf), and cudaMalloc / cudaFree per call (the latter
+// synchronising the device) dominated the reference driver's time over the device pImpls.
 int vrg_malloc(vrg_ctx_t c, unsigned long long bytes, void** out) {
-    return guarded(c, [&] { VRG_CUDA(cudaMalloc(out, bytes)); });
+    return guarded(c, [&] {
+        std::size_t got = 0;
+        *out = vrg::cachedAlloc(bytes ? bytes : 1, c->ctx.stream, &got);
+        std::lock_guard<std::mutex> lock(c->allocMu);
+        c->allocs[*out] = got;
+    });
 }
 
 int vrg_free(vrg_ctx_t c, void* p) {
-    return guarded(c, [&] { VRG_CUDA(cudaFree(p)); });
+    return guarded(c, [&] {
+        if (!p) return;
+        std::size_t got = 0;
+        {
+            std::lock_guard<std::mutex> lock(c->allocMu);
+            auto it = c->allocs.find(p);
+            if (it == c->allocs.end()) throw vrg::InvalidArgument("vrg_free: not a vrg_malloc block of this context");
+            got = it->second;
+            c->allocs.erase(it);
+        }
+        vrg::cachedFree(p, got, c->ctx.stream);
+    });
 }
 
 int vrg_host_alloc(vrg_ctx_t c, unsigned long long bytes, void** out) {
