@@ -308,11 +308,12 @@ __global__ void __launch_bounds__(TW, (bandMinBlocks<Epi, TW>())) k_eval_band(Co
 // with one block per row, consecutive rows land on different SMs and every SM fetches the 4
 // tap rows of each of its rows from L2 (tap traffic 4.3x the coefficient field).
 // Row workers per strip block: 7 x 128 threads (72 registers; ~7 rows per SM at 1024 rows on
-// 148 SMs, one round), one worker less where the epilogue carries more live state
-// (BandMinBlocks < 4).
+// 148 SMs, one round) for every epilogue: with 6 workers the seed step needed 171 blocks, two
+// rounds on 148 SMs (twice the time of a regular step), while 72 registers hold its state
+// without spills (the 64-register row-per-block kernel is what needs BandMinBlocks = 3).
 template <class Epi, int TW>
 constexpr int stripWorkers() {
-    return 7 - (BandMinBlocks<Epi>::value < 4 ? 1 : 0);
+    return 7;
 }
 
 template <class Epi, bool kGather, int TW>
