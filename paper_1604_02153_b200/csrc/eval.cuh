@@ -180,14 +180,14 @@ void launchEvaluate(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, const Dep* x1,
 
 // `count` coefficient sets cs + k*csZ evaluated at the same points in one launch, the
 // epilogue of member k at index p + k*epiZ (guard-free epilogues, e.g. EpiStore2).
-template <int NF, class Epi>
-void launchEvaluateBatch(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, std::size_t csZ, int count, const double* x1,
-                         const double* x2, const Epi& epi, std::size_t epiZ) {
+template <int NF, class Epi, class Dep>
+void launchEvaluateBatch(Ctx& ctx, const GridDims& g, CoeffSet<NF> cs, std::size_t csZ, int count, const Dep* x1,
+                         const Dep* x2, const Epi& epi, std::size_t epiZ) {
     static_assert(!Epi::kGuard, "batched evaluate: guard-free epilogues only");
     const std::size_t N = g.points();
     {
         LaunchScope ls_(ctx, Epi::kName);
-        launchPdl(1, k_evaluate<NF, Epi>, dim3(grid1d(N, kEvalBlock).x, count), dim3(kEvalBlock), 0, ctx.stream, cs,
+        launchPdl(1, k_evaluate<NF, Epi, Dep>, dim3(grid1d(N, kEvalBlock).x, count), dim3(kEvalBlock), 0, ctx.stream, cs,
                   x1, x2, g.n1, g.n2, 0, epi, csZ, epiZ, g.pairs);
     }
 }

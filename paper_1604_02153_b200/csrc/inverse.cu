@@ -185,6 +185,12 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
         gradientBatch(ctx, g, state_.d(), nt + 1, G_.d());  // one batched transform chain per chunk
     }
     const double* Xf = solver.departure(kForward);
+    // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
+    // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
+    // 1024^2 on B200 (0.815 vs 0.867 ms).  The plain step is the generic-grid path.  Its packed
+    // departure cells (both directions) exist before any graph capture.
+    fused_ = solver.bandPath();
+    const Cell* Cf = fused_ ? solver.cells(kForward) : nullptr;
     work_.alloc(sizeof(double) * (11 * N + 2 * paddedTotal(g)));  // + vt coefficients (2 padded)
     // GD_j = (grad m_{j-1})_D, j = 1..nt: the 2nt gradient components prefiltered in one batch
     // (two launches) and evaluated at the forward departure points in one launch per chunk
@@ -201,8 +207,12 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
             launchPrefilterBatch(ctx, g, G_.d() + static_cast<std::size_t>(j0) * 2 * N, N, 2 * c, coefs, P, rows,
                                  nullptr);
             double* gd = GD_.d() + static_cast<std::size_t>(j0) * 2 * N;
-            launchEvaluateBatch<2>(ctx, g, CoeffSet<2>{{coefs, coefs + P}}, 2 * P, c, Xf, Xf + N,
-                                   EpiStore2{nullptr, gd, gd + N}, 2 * N);
+            if (fused_)
+                launchEvaluateBatch<2>(ctx, g, CoeffSet<2>{{coefs, coefs + P}}, 2 * P, c, Cf, Cf + N,
+                                       EpiStore2{nullptr, gd, gd + N}, 2 * N);
+            else
+                launchEvaluateBatch<2>(ctx, g, CoeffSet<2>{{coefs, coefs + P}}, 2 * P, c, Xf, Xf + N,
+                                       EpiStore2{nullptr, gd, gd + N}, 2 * N);
         }
     }
     solver.departure(kBackward);
@@ -234,14 +244,7 @@ Hessian::Hessian(Ctx& c, const GridDims& gd, const double* v1, const double* v2,
         ctx.ffts += 3;          // div v
         lazyInterps_ = hadFwd ? 0 : 2;
     }
-    // Band path (evalband.cuh) wherever the grid allows it: gather + epilogue + next row pass in
-    // one kernel per step, bit-identical to the plain 3-kernel step and 6% faster per matvec at
-    // 1024^2 on B200 (0.815 vs 0.867 ms).  The plain step is the generic-grid path.
-    fused_ = solver.bandPath();
-    if (fused_) {  // packed departure cells of both directions, before any graph capture
-        solver.cells(kForward);
-        solver.cells(kBackward);
-    }
+    if (fused_) solver.cells(kBackward);
     lazyFfts_ = (mode_ == 1 && !adjTraj) ? 0 : 3;
     spec_.alloc(sizeof(cplx) * 4 * g.specPoints());
     for (auto& l : guardLogs_) l.ensure(nt + 1, g);
